@@ -1,0 +1,174 @@
+/*
+ * sdqz_cuda.h -- C-ABI of libsdqz_cuda.so, the B200 (sm_100a) implementation of
+ * the sdqz compression path (cuSZ dual-quantization + canonical Huffman).
+ *
+ * The reference (`sdqz`, /root/reference/pkg/src/sdqz) is pure Python; its
+ * "plugin interface" for this path is the set of stage functions composed in
+ * pipeline.py.  Each entry point below replaces one of them (cited as
+ * reference file:line); the Python package paper_2007_09625_b200 binds them
+ * with ctypes and keeps the reference's names, argument meaning and error
+ * classes.  No torch types cross this boundary: plain pointers and sizes.
+ *
+ * Conventions
+ *   - Every function returns an sdqz_status; on failure the message is
+ *     available from sdqz_last_error(ctx).  Codes map to the reference's
+ *     exception classes: SDQZ_EINVAL -> SdqzError, SDQZ_ECORRUPT ->
+ *     CorruptionError, SDQZ_EFORMAT -> ArchiveFormatError (archive.py:44).
+ *   - Pointers named d_* are device pointers owned by the caller; h_* are host
+ *     pointers.  Scratch memory is owned by the context and reused.
+ *   - Calls are stream-ordered on the context's stream.  Functions returning
+ *     sizes or errors synchronize that stream before returning.
+ *   - dtype codes: 0 = float32, 1 = float64 (archive.py:38).
+ *   - dims/block arrays always have 3 entries; unused trailing entries are 1
+ *     (archive.py:15).
+ */
+#ifndef SDQZ_CUDA_H
+#define SDQZ_CUDA_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#if defined(__GNUC__)
+#define SDQZ_API __attribute__((visibility("default")))
+#else
+#define SDQZ_API
+#endif
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+    SDQZ_OK = 0,
+    SDQZ_EINVAL = 1,   /* SdqzError            (core.py:26)    */
+    SDQZ_ECORRUPT = 2, /* CorruptionError      (core.py:30)    */
+    SDQZ_EFORMAT = 3,  /* ArchiveFormatError   (archive.py:44) */
+    SDQZ_ECUDA = 4,    /* CUDA runtime failure                 */
+} sdqz_status;
+
+typedef struct sdqz_ctx sdqz_ctx;
+
+/* Header fields of one archive (archive.py:3-13, struct "<4s4B3Q2d5IB3Q"). */
+typedef struct {
+    uint8_t dtype_code;      /* 0 f32, 1 f64                     */
+    uint8_t ndims;           /* 1..3                             */
+    uint8_t eb_mode;         /* 0 abs, 1 valrel                  */
+    uint8_t unit_width;      /* 32 | 64                          */
+    uint64_t dims[3];
+    double eb_resolved;
+    double eb_specified;
+    uint32_t cap;
+    uint32_t block[3];
+    uint32_t chunk_size;
+    uint64_t n_outliers;
+    uint64_t n_chunks;
+    uint64_t payload_bytes;
+} sdqz_header;
+
+#define SDQZ_HEADER_SIZE 93
+
+/* ---- context ------------------------------------------------------------ */
+/* stream: a cudaStream_t (NULL = create a private non-blocking stream). */
+SDQZ_API int sdqz_ctx_create(int device, void* stream, sdqz_ctx** out);
+SDQZ_API int sdqz_ctx_destroy(sdqz_ctx* ctx);
+SDQZ_API int sdqz_ctx_set_stream(sdqz_ctx* ctx, void* stream);
+SDQZ_API const char* sdqz_last_error(const sdqz_ctx* ctx);
+/* Kernels launched by the most recent call (evidence for the bench). */
+SDQZ_API uint64_t sdqz_kernel_launches(const sdqz_ctx* ctx);
+
+/* ---- L1: field description (core.py:136-175) ---------------------------- */
+/* min/max in the input dtype (returned widened to double) + nonfinite flag. */
+SDQZ_API int sdqz_describe(sdqz_ctx* ctx, const void* d_in, int dtype, uint64_t n,
+                  double* vmin, double* vmax, int* nonfinite);
+
+/* ---- L2 lossy stage (dualquant.py) --------------------------------------- */
+/* prequantize (dualquant.py:62-78): d_out[i] = copysign(floor(|x/(2eb)|+.5), x/(2eb)). */
+SDQZ_API int sdqz_prequantize(sdqz_ctx* ctx, const void* d_in, int dtype, uint64_t n, double eb,
+                     double* d_out);
+
+/* compress_field codes (dualquant.py:172-194, :242-273): writes one uint16 code per
+ * point (0 = outlier) and, if d_hist != NULL, the exact histogram (uint64[cap],
+ * overwritten).  in_kind: 0 f32 data, 1 f64 data, 2 f64 already-prequantized
+ * units (postquantize_block, dualquant.py:132-147).  *nonfinite is set when an
+ * input value is NaN/Inf. */
+SDQZ_API int sdqz_dualquant(sdqz_ctx* ctx, const void* d_in, int in_kind, int ndims,
+                   const uint64_t dims[3], const uint32_t block[3], double eb, uint32_t cap,
+                   uint16_t* d_codes, uint64_t* d_hist, int* nonfinite);
+
+/* Outlier list of a code array (dualquant.py:190-194): records {uint64 flat index,
+ * fp64 prequantized value} for every code 0, ascending row-major, the value
+ * recomputed from the input.  Capacity max_k records; *k_out = number found. */
+SDQZ_API int sdqz_outliers(sdqz_ctx* ctx, const void* d_in, int in_kind, const uint16_t* d_codes,
+                  uint64_t n, double eb, void* d_records, uint64_t max_k, uint64_t* k_out);
+
+/* reconstruct_field (dualquant.py:276-332): validates like _validate_output and
+ * writes flat values: out_kind 0 -> float32(x*2eb), 1 -> float64 x*2eb.
+ * code_bytes: 2 (uint16 codes) or 4 (uint32 codes, range-checked against cap). */
+SDQZ_API int sdqz_reconstruct(sdqz_ctx* ctx, const void* d_codes, int code_bytes, uint64_t n,
+                     const uint64_t* d_idx, const double* d_val, uint64_t k, int ndims,
+                     const uint64_t dims[3], const uint32_t block[3], double eb, uint32_t cap,
+                     void* d_out, int out_kind);
+
+/* ---- L2 lossless stage (huffman.py) ------------------------------------- */
+/* histogram (huffman.py:77-95) over uint32 codes; counts uint64[cap]. */
+SDQZ_API int sdqz_histogram_u32(sdqz_ctx* ctx, const uint32_t* d_codes, uint64_t n, uint32_t cap,
+                       uint64_t* d_hist);
+
+/* build_tree (huffman.py:98-131) -> bitwidth per symbol (uint8[cap]). */
+SDQZ_API int sdqz_build_tree(sdqz_ctx* ctx, const uint64_t* d_hist, uint32_t cap, uint8_t* d_bw);
+
+/* canonize (huffman.py:146-190).  d_entries: uint64[cap] packed units (a 32-bit
+ * unit is stored zero-extended).  Reverse tables: d_first uint64[58],
+ * d_offsets int64[59], d_symbols uint32[cap]; *n_present symbols valid. */
+SDQZ_API int sdqz_canonize(sdqz_ctx* ctx, const uint8_t* d_bw, uint32_t cap, uint64_t* d_entries,
+                  uint64_t* d_first, int64_t* d_offsets, uint32_t* d_symbols,
+                  int* unit_width, int* max_bw, uint32_t* n_present);
+
+/* encode (huffman.py:193-203): d_units (uint32 or uint64 per unit_width). */
+SDQZ_API int sdqz_encode_u32(sdqz_ctx* ctx, const uint32_t* d_codes, uint64_t n, const uint64_t* d_entries,
+                    uint32_t cap, int unit_width, void* d_units);
+
+/* deflate (huffman.py:219-269) of packed units.  d_payload capacity
+ * payload_cap bytes; *payload_bytes = used.  chunk bit lengths uint32[C]. */
+SDQZ_API int sdqz_deflate_units(sdqz_ctx* ctx, const void* d_units, int unit_width, uint64_t n,
+                       uint32_t chunk, uint32_t* d_chunk_bits, uint8_t* d_payload,
+                       uint64_t payload_cap, uint64_t* payload_bytes);
+
+/* inflate (huffman.py:311-356) with the canonical reverse tables. */
+SDQZ_API int sdqz_inflate(sdqz_ctx* ctx, const uint8_t* d_payload, uint64_t payload_bytes,
+                 const uint32_t* d_chunk_bits, uint64_t n_chunks, uint32_t chunk,
+                 const uint64_t* d_first, const int64_t* d_offsets, const uint32_t* d_symbols,
+                 int max_bw, uint64_t n, uint32_t* d_codes_u32);
+
+/* ---- L4 fused pipeline (pipeline.py:15-58) ------------------------------- */
+/* compress (pipeline.py:15-39) of a device-resident field.  eb_mode 0 abs,
+ * 1 valrel; chunk 0 = default_chunk_size(n).  On success *hdr describes the
+ * archive, whose sections stay in context memory until the next compress. */
+SDQZ_API int sdqz_compress(sdqz_ctx* ctx, const void* d_in, int dtype, int ndims, const uint64_t dims[3],
+                  const uint32_t block[3], int eb_mode, double eb, uint32_t cap, uint32_t chunk,
+                  sdqz_header* hdr);
+/* Total archive bytes of the last compress. */
+SDQZ_API uint64_t sdqz_archive_size(const sdqz_ctx* ctx);
+/* Write the last compress's archive (header + sections) to host memory. */
+SDQZ_API int sdqz_archive_write(sdqz_ctx* ctx, uint8_t* h_dst, uint64_t capacity);
+/* Device pointers to the last compress's sections (bitwidths, outlier records,
+ * chunk bits, payload) -- for device-resident decompress and sharding. */
+SDQZ_API int sdqz_archive_sections(sdqz_ctx* ctx, const uint8_t** d_bw, const void** d_outliers,
+                          const uint32_t** d_chunk_bits, const uint8_t** d_payload);
+
+/* parse_header (archive.py:143-181): validate and decode the 93-byte header. */
+SDQZ_API int sdqz_parse_header(sdqz_ctx* ctx, const uint8_t* h_buf, uint64_t len, sdqz_header* hdr);
+
+/* decompress (pipeline.py:42-58 + archive.deserialize :184-246) of a host
+ * archive into device memory (d_out: float32/float64 per header dtype). */
+SDQZ_API int sdqz_decompress(sdqz_ctx* ctx, const uint8_t* h_archive, uint64_t len, void* d_out);
+
+/* decompress from device-resident sections (same checks as deserialize). */
+SDQZ_API int sdqz_decompress_sections(sdqz_ctx* ctx, const sdqz_header* hdr, const uint8_t* d_bw,
+                             const void* d_outliers, const uint32_t* d_chunk_bits,
+                             const uint8_t* d_payload, void* d_out);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SDQZ_CUDA_H */

@@ -1,0 +1,95 @@
+"""Device staging helpers: host/torch inputs -> contiguous CUDA buffers."""
+
+from __future__ import annotations
+
+import numpy as np
+
+from . import _lib
+
+
+def _torch():
+    import torch
+    return torch
+
+
+def is_tensor(x) -> bool:
+    try:
+        import torch
+    except ImportError:  # pragma: no cover
+        return False
+    return isinstance(x, torch.Tensor)
+
+
+def as_field(data):
+    return data if is_tensor(data) else np.asarray(data)
+
+
+def numel(arr) -> int:
+    return int(arr.numel()) if is_tensor(arr) else int(arr.size)
+
+
+_TORCH_OF = {np.dtype(np.float32): "float32", np.dtype(np.float64): "float64"}
+
+
+def field_dtype(arr) -> np.dtype:
+    if is_tensor(arr):
+        name = str(arr.dtype).replace("torch.", "")
+        dt = np.dtype(name) if name in ("float32", "float64") else np.dtype(np.float64)
+        return dt
+    return arr.dtype if arr.dtype in (np.float32, np.float64) else np.dtype(np.float64)
+
+
+def device_index() -> int:
+    torch = _torch()
+    _lib.require_cuda()
+    return torch.cuda.current_device()
+
+
+def to_device(arr, dtype=None):
+    """Flat contiguous CUDA tensor of `arr` in its field dtype (f32 / f64)."""
+    torch = _torch()
+    _lib.require_cuda()
+    dt = np.dtype(dtype) if dtype is not None else field_dtype(arr)
+    tdt = getattr(torch, _TORCH_OF[dt])
+    dev = torch.device("cuda", torch.cuda.current_device())
+    if is_tensor(arr):
+        t = arr.to(device=dev, dtype=tdt).contiguous().reshape(-1)
+    else:
+        a = np.ascontiguousarray(arr, dtype=dt).reshape(-1)
+        if not a.flags.writeable:
+            a = a.copy()
+        t = torch.from_numpy(a).to(dev, non_blocking=False)
+    return t, dt
+
+
+def upload(a: np.ndarray):
+    """Host numpy array -> CUDA tensor (same dtype, flat)."""
+    torch = _torch()
+    a = np.ascontiguousarray(a).reshape(-1)
+    if not a.flags.writeable:
+        a = a.copy()
+    return torch.from_numpy(a).to(torch.device("cuda", torch.cuda.current_device()))
+
+
+def empty(n: int, dtype):
+    torch = _torch()
+    return torch.empty(max(int(n), 1), dtype=dtype, device=torch.device("cuda", torch.cuda.current_device()))
+
+
+def zeros(n: int, dtype):
+    torch = _torch()
+    return torch.zeros(max(int(n), 1), dtype=dtype, device=torch.device("cuda", torch.cuda.current_device()))
+
+
+def download(t, n: int | None = None) -> np.ndarray:
+    out = t.cpu().numpy()
+    return out[:n] if n is not None else out
+
+
+def describe(t, dt):
+    ctx = _lib.context()
+    vmin, vmax, nf = _lib.c_double(), _lib.c_double(), _lib.c_int()
+    code = 0 if dt == np.float32 else 1
+    ctx.call("sdqz_describe", _lib.ptr(t), code, t.numel(), _lib.byref(vmin), _lib.byref(vmax),
+             _lib.byref(nf))
+    return float(vmin.value), float(vmax.value), bool(nf.value)

@@ -1,0 +1,203 @@
+"""ctypes binding of libsdqz_cuda.so (include/sdqz_cuda.h).
+
+There is no CPU fallback: if the shared library is missing the import of the
+package's compute entry points fails loudly, and every compute call needs a
+CUDA device.  Device buffers are torch tensors (torch is only the allocator /
+stream plumbing); the library sees plain pointers.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+import threading
+from ctypes import (POINTER, Structure, byref, c_char_p, c_double, c_int, c_int64, c_uint8,
+                    c_uint32, c_uint64, c_void_p)
+from pathlib import Path
+
+from .core import CorruptionError, SdqzError
+
+LIB_PATH = Path(__file__).resolve().parent / "libsdqz_cuda.so"
+
+SDQZ_OK, SDQZ_EINVAL, SDQZ_ECORRUPT, SDQZ_EFORMAT, SDQZ_ECUDA = range(5)
+HEADER_SIZE = 93
+
+
+class Header(Structure):
+    """sdqz_header (include/sdqz_cuda.h)."""
+
+    _fields_ = [
+        ("dtype_code", c_uint8), ("ndims", c_uint8), ("eb_mode", c_uint8), ("unit_width", c_uint8),
+        ("dims", c_uint64 * 3), ("eb_resolved", c_double), ("eb_specified", c_double),
+        ("cap", c_uint32), ("block", c_uint32 * 3), ("chunk_size", c_uint32),
+        ("n_outliers", c_uint64), ("n_chunks", c_uint64), ("payload_bytes", c_uint64),
+    ]
+
+    @property
+    def total_bytes(self) -> int:
+        return (HEADER_SIZE + self.cap + 16 * self.n_outliers + 4 * self.n_chunks
+                + self.payload_bytes)
+
+
+_SIGS = {
+    "sdqz_ctx_create": (c_int, [c_int, c_void_p, POINTER(c_void_p)]),
+    "sdqz_ctx_destroy": (c_int, [c_void_p]),
+    "sdqz_ctx_set_stream": (c_int, [c_void_p, c_void_p]),
+    "sdqz_last_error": (c_char_p, [c_void_p]),
+    "sdqz_kernel_launches": (c_uint64, [c_void_p]),
+    "sdqz_describe": (c_int, [c_void_p, c_void_p, c_int, c_uint64, POINTER(c_double),
+                              POINTER(c_double), POINTER(c_int)]),
+    "sdqz_prequantize": (c_int, [c_void_p, c_void_p, c_int, c_uint64, c_double, c_void_p]),
+    "sdqz_dualquant": (c_int, [c_void_p, c_void_p, c_int, c_int, POINTER(c_uint64),
+                               POINTER(c_uint32), c_double, c_uint32, c_void_p, c_void_p,
+                               POINTER(c_int)]),
+    "sdqz_outliers": (c_int, [c_void_p, c_void_p, c_int, c_void_p, c_uint64, c_double, c_void_p,
+                              c_uint64, POINTER(c_uint64)]),
+    "sdqz_reconstruct": (c_int, [c_void_p, c_void_p, c_int, c_uint64, c_void_p, c_void_p,
+                                 c_uint64, c_int, POINTER(c_uint64), POINTER(c_uint32), c_double,
+                                 c_uint32, c_void_p, c_int]),
+    "sdqz_histogram_u32": (c_int, [c_void_p, c_void_p, c_uint64, c_uint32, c_void_p]),
+    "sdqz_build_tree": (c_int, [c_void_p, c_void_p, c_uint32, c_void_p]),
+    "sdqz_canonize": (c_int, [c_void_p, c_void_p, c_uint32, c_void_p, c_void_p, c_void_p,
+                              c_void_p, POINTER(c_int), POINTER(c_int), POINTER(c_uint32)]),
+    "sdqz_encode_u32": (c_int, [c_void_p, c_void_p, c_uint64, c_void_p, c_uint32, c_int,
+                                c_void_p]),
+    "sdqz_deflate_units": (c_int, [c_void_p, c_void_p, c_int, c_uint64, c_uint32, c_void_p,
+                                   c_void_p, c_uint64, POINTER(c_uint64)]),
+    "sdqz_inflate": (c_int, [c_void_p, c_void_p, c_uint64, c_void_p, c_uint64, c_uint32,
+                             c_void_p, c_void_p, c_void_p, c_int, c_uint64, c_void_p]),
+    "sdqz_compress": (c_int, [c_void_p, c_void_p, c_int, c_int, POINTER(c_uint64),
+                              POINTER(c_uint32), c_int, c_double, c_uint32, c_uint32,
+                              POINTER(Header)]),
+    "sdqz_archive_size": (c_uint64, [c_void_p]),
+    "sdqz_archive_write": (c_int, [c_void_p, c_void_p, c_uint64]),
+    "sdqz_archive_sections": (c_int, [c_void_p, POINTER(c_void_p), POINTER(c_void_p),
+                                      POINTER(c_void_p), POINTER(c_void_p)]),
+    "sdqz_parse_header": (c_int, [c_void_p, c_void_p, c_uint64, POINTER(Header)]),
+    "sdqz_decompress": (c_int, [c_void_p, c_void_p, c_uint64, c_void_p]),
+    "sdqz_decompress_sections": (c_int, [c_void_p, POINTER(Header), c_void_p, c_void_p,
+                                         c_void_p, c_void_p, c_void_p]),
+}
+
+EXPORTS = tuple(_SIGS)
+
+_lib = None
+_lib_lock = threading.Lock()
+
+
+def load_library():
+    """Load libsdqz_cuda.so (no GPU needed for loading).  Raises if absent."""
+    global _lib
+    with _lib_lock:
+        if _lib is None:
+            if not LIB_PATH.exists():
+                raise ImportError(
+                    f"{LIB_PATH} is not built; run `python -c 'import __graft_entry__ as g; "
+                    f"g.build()'` (or make -C paper_2007_09625_b200/csrc). There is no CPU "
+                    f"fallback for the sdqz compute path.")
+            lib = ctypes.CDLL(str(LIB_PATH))
+            for name, (res, args) in _SIGS.items():
+                fn = getattr(lib, name)
+                fn.restype = res
+                fn.argtypes = args
+            _lib = lib
+    return _lib
+
+
+def _exc_for(rc: int, msg: str):
+    from .archive import ArchiveFormatError
+    if rc == SDQZ_ECORRUPT:
+        return CorruptionError(msg)
+    if rc == SDQZ_EFORMAT:
+        return ArchiveFormatError(msg)
+    if rc == SDQZ_EINVAL:
+        return SdqzError(msg)
+    return RuntimeError(f"sdqz CUDA failure: {msg}")
+
+
+class Context:
+    """One library context per (device, host thread): stream + scratch arena."""
+
+    def __init__(self, device: int):
+        import torch
+        self.lib = load_library()
+        self.device = device
+        self.torch = torch
+        h = c_void_p()
+        rc = self.lib.sdqz_ctx_create(device, c_void_p(torch.cuda.current_stream(device).cuda_stream),
+                                      byref(h))
+        if rc:
+            raise RuntimeError(f"sdqz_ctx_create failed ({rc}) on cuda:{device}")
+        self.h = h
+
+    def sync_stream(self):
+        s = self.torch.cuda.current_stream(self.device).cuda_stream
+        self.lib.sdqz_ctx_set_stream(self.h, c_void_p(s))
+
+    def call(self, name: str, *args):
+        rc = getattr(self.lib, name)(self.h, *args)
+        if rc != SDQZ_OK:
+            msg = self.lib.sdqz_last_error(self.h).decode(errors="replace")
+            raise _exc_for(rc, msg)
+        return rc
+
+    @property
+    def launches(self) -> int:
+        return int(self.lib.sdqz_kernel_launches(self.h))
+
+    def __del__(self):  # pragma: no cover - interpreter shutdown order varies
+        try:
+            if getattr(self, "h", None):
+                self.lib.sdqz_ctx_destroy(self.h)
+        except Exception:
+            pass
+
+
+_tls = threading.local()
+
+
+def require_cuda():
+    import torch
+    if not torch.cuda.is_available():
+        raise RuntimeError("sdqz (B200 build) needs a CUDA device; no CPU fallback exists")
+    load_library()
+
+
+def context(device: int | None = None) -> Context:
+    """The calling thread's context for `device` (default: torch's current device)."""
+    import torch
+    require_cuda()
+    if device is None:
+        device = torch.cuda.current_device()
+    ctxs = getattr(_tls, "ctxs", None)
+    if ctxs is None:
+        ctxs = _tls.ctxs = {}
+    ctx = ctxs.get(device)
+    if ctx is None:
+        with torch.cuda.device(device):
+            ctx = ctxs[device] = Context(device)
+    ctx.sync_stream()
+    return ctx
+
+
+def dims3(dims):
+    d = list(int(x) for x in dims) + [1] * (3 - len(dims))
+    return (c_uint64 * 3)(*d)
+
+
+def block3(block):
+    b = list(int(x) for x in block) + [1] * (3 - len(block))
+    return (c_uint32 * 3)(*b)
+
+
+def ptr(t) -> c_void_p:
+    return c_void_p(t.data_ptr()) if t is not None else c_void_p(0)
+
+
+def env_flag(name: str) -> bool:
+    return os.environ.get(name, "") not in ("", "0")
+
+
+__all__ = ["Context", "Header", "EXPORTS", "LIB_PATH", "load_library", "context", "dims3",
+           "block3", "ptr", "require_cuda", "c_int", "c_uint32", "c_uint64", "c_double",
+           "c_int64", "byref", "c_void_p"]

@@ -1,0 +1,752 @@
+// capi.cu -- the C-ABI (include/sdqz_cuda.h): context, scratch arena, status
+// readback with the reference's error classes/messages, header (de)coding, and
+// the fused compress / decompress pipelines (pipeline.py:15-58).
+#include <algorithm>
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <sstream>
+
+#include "kernels.cuh"
+
+namespace sdqz {
+
+int launch_count_zero(sdqz_ctx* ctx, const uint16_t* codes, uint64_t n);
+int launch_narrow_codes(sdqz_ctx* ctx, const uint32_t* in, uint64_t n, uint32_t cap, uint16_t* out);
+
+int set_error(sdqz_ctx* ctx, int code, const std::string& msg) {
+    if (ctx) ctx->err = msg;
+    return code;
+}
+
+int cuda_check(sdqz_ctx* ctx, cudaError_t e, const char* what) {
+    std::ostringstream os;
+    os << "CUDA error in " << what << ": " << cudaGetErrorString(e);
+    return set_error(ctx, SDQZ_ECUDA, os.str());
+}
+
+void* scratch(sdqz_ctx* ctx, int slot, size_t bytes, cudaError_t* e) {
+    if ((int)ctx->bufs.size() < S_NSLOTS) ctx->bufs.resize(S_NSLOTS);
+    auto& b = ctx->bufs[slot];
+    if (bytes == 0) bytes = 16;
+    if (b.bytes >= bytes) return b.p;
+    if (b.p) {
+        cudaStreamSynchronize(ctx->stream);
+        cudaFree(b.p);
+        b.p = nullptr;
+        b.bytes = 0;
+    }
+    size_t want = bytes + bytes / 8 + 256;   // headroom against regrowth
+    cudaError_t r = cudaMalloc(&b.p, want);
+    if (r != cudaSuccess) {
+        cudaGetLastError();
+        r = cudaMalloc(&b.p, bytes);
+        want = bytes;
+    }
+    if (r != cudaSuccess) {
+        *e = r;
+        b.p = nullptr;
+        return nullptr;
+    }
+    b.bytes = want;
+    return b.p;
+}
+
+namespace {
+
+__global__ void init_status_kernel(DevStatus* st) {
+    memset(st, 0, sizeof(DevStatus));
+    st->decode_key = ~0ull;
+    st->vmin_bits = ~0ull;
+    st->vmax_bits = 0;
+}
+
+__global__ void set_eb_kernel(DevStatus* st, double eb) {
+    st->eb = eb;
+    st->two_eb = __dmul_rn(2.0, eb);
+}
+
+}  // namespace
+
+int reset_status(sdqz_ctx* ctx) {
+    init_status_kernel<<<1, 1, 0, ctx->stream>>>(ctx->d_status);
+    SDQZ_LAUNCHED(ctx);
+    return SDQZ_OK;
+}
+
+int set_eb(sdqz_ctx* ctx, double eb) {
+    set_eb_kernel<<<1, 1, 0, ctx->stream>>>(ctx->d_status, eb);
+    SDQZ_LAUNCHED(ctx);
+    return SDQZ_OK;
+}
+
+int fetch_status(sdqz_ctx* ctx) {
+    SDQZ_CUDA(ctx, cudaMemcpyAsync(ctx->h_status, ctx->d_status, sizeof(DevStatus),
+                                   cudaMemcpyDeviceToHost, ctx->stream));
+    SDQZ_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
+    return SDQZ_OK;
+}
+
+}  // namespace sdqz
+
+using namespace sdqz;
+
+namespace {
+
+std::string fmt(const char* f, ...) {
+    char buf[512];
+    va_list ap;
+    va_start(ap, f);
+    vsnprintf(buf, sizeof buf, f, ap);
+    va_end(ap);
+    return buf;
+}
+
+bool valid_cap(uint32_t cap) { return cap >= 4 && cap <= 65536 && !(cap & (cap - 1)); }
+
+uint64_t prod3(const uint64_t d[3]) { return d[0] * d[1] * d[2]; }
+
+int unit_for(uint32_t mx) { return mx <= 24 ? 32 : 64; }
+
+// Book tables in the context arena.
+int book_tables(sdqz_ctx* ctx, uint32_t cap, BookDev* b) {
+    int rc = SDQZ_OK;
+    b->entries = scratch_as<uint64_t>(ctx, S_ENTRIES, cap, &rc);
+    b->bw = scratch_as<uint8_t>(ctx, S_BW, cap + 16, &rc);
+    b->first = scratch_as<uint64_t>(ctx, S_FIRST, 64 + 64 + 64, &rc);
+    b->offsets = (int64_t*)(b->first + 64);
+    b->lut = (uint32_t*)(b->first + 128);   // overwritten below (needs 4096 u32)
+    b->symbols = scratch_as<uint32_t>(ctx, S_SYMBOLS, cap, &rc);
+    b->lut = scratch_as<uint32_t>(ctx, S_LUT, 1u << kLutBits, &rc);
+    return (b->entries && b->bw && b->first && b->symbols && b->lut) ? SDQZ_OK : rc;
+}
+
+// Map table-stage flags (canonize / deserialize) to the reference messages.
+int table_error(sdqz_ctx* ctx, uint64_t flags, bool format) {
+    const DevStatus& s = *ctx->h_status;
+    if (flags & F_NO_PRESENT)
+        return format ? set_error(ctx, SDQZ_EFORMAT, "bitwidth table has no present symbols")
+                      : set_error(ctx, SDQZ_EINVAL, "cannot canonize an empty codebook");
+    if (flags & F_BW_TOO_BIG)
+        return format ? set_error(ctx, SDQZ_EFORMAT,
+                                  fmt("bitwidth %llu exceeds the supported maximum", s.max_bw))
+                      : set_error(ctx, SDQZ_EINVAL,
+                                  fmt("codeword bitwidth %llu exceeds the supported maximum of 56",
+                                      s.max_bw));
+    if (flags & F_KRAFT)
+        return set_error(ctx, format ? SDQZ_EFORMAT : SDQZ_EINVAL,
+                         "bitwidth table violates Kraft equality");
+    return SDQZ_OK;
+}
+
+int decode_error(sdqz_ctx* ctx) {
+    unsigned long long key = ctx->h_status->decode_key;
+    if (key == ~0ull) return SDQZ_OK;
+    switch (key & 3) {
+        case DK_NO_CODEWORD:
+            return set_error(ctx, SDQZ_ECORRUPT, "bit pattern matches no codeword bitwidth");
+        case DK_EXHAUSTED:
+            return set_error(ctx, SDQZ_ECORRUPT, "chunk bit budget exhausted mid-codeword");
+        default:
+            return set_error(ctx, SDQZ_ECORRUPT, "decoded bits disagree with recorded chunk length");
+    }
+}
+
+void put_header(uint8_t* p, const sdqz_header& h) {
+    memcpy(p, "SDQZ", 4);
+    p[4] = 1;
+    p[5] = h.dtype_code;
+    p[6] = h.ndims;
+    p[7] = h.eb_mode;
+    memcpy(p + 8, h.dims, 24);
+    memcpy(p + 32, &h.eb_resolved, 8);
+    memcpy(p + 40, &h.eb_specified, 8);
+    memcpy(p + 48, &h.cap, 4);
+    memcpy(p + 52, h.block, 12);
+    memcpy(p + 64, &h.chunk_size, 4);
+    p[68] = h.unit_width;
+    memcpy(p + 69, &h.n_outliers, 8);
+    memcpy(p + 77, &h.n_chunks, 8);
+    memcpy(p + 85, &h.payload_bytes, 8);
+}
+
+uint64_t archive_total(const sdqz_header& h) {
+    return SDQZ_HEADER_SIZE + (uint64_t)h.cap + 16 * h.n_outliers + 4 * h.n_chunks + h.payload_bytes;
+}
+
+// Shared decompress core over device-resident sections.
+int decompress_core(sdqz_ctx* ctx, const sdqz_header* hdr, const uint8_t* d_bw, const void* d_rec,
+                    const uint32_t* d_cbits, const uint8_t* d_payload, uint64_t payload_alloc,
+                    void* d_out) {
+    int rc = SDQZ_OK;
+    const uint64_t n = prod3(hdr->dims);
+    const uint32_t cap = hdr->cap;
+    const uint64_t C = hdr->n_chunks, k = hdr->n_outliers;
+    bool geom_ok = true;    // QuantConfig checks (core.py:87-94) come after deserialize
+    for (int a = 0; a < hdr->ndims; a++) geom_ok &= hdr->block[a] >= 1;
+    const bool eb_ok = hdr->eb_resolved > 0 && std::isfinite(hdr->eb_resolved);
+    const bool chunks_ok = C == ceil_div(n, hdr->chunk_size) && geom_ok && eb_ok;
+    BookDev book;
+    if ((rc = book_tables(ctx, cap, &book))) return rc;
+    uint16_t* codes = scratch_as<uint16_t>(ctx, S_CODES, n + 8, &rc);
+    uint64_t* dense = scratch_as<uint64_t>(ctx, S_DENSE, n, &rc);
+    uint64_t nblocks = 1;
+    for (int a = 0; a < hdr->ndims; a++) nblocks *= ceil_div(hdr->dims[a], hdr->block[a] ? hdr->block[a] : 1);
+    uint8_t* bflag = scratch_as<uint8_t>(ctx, S_BLOCKFLAG, nblocks, &rc);
+    if (!codes || !dense || !bflag) return rc;
+    uint32_t safe_block[3];
+    for (int a = 0; a < 3; a++) safe_block[a] = hdr->block[a] ? hdr->block[a] : 1;
+    if ((rc = reset_status(ctx))) return rc;
+    if ((rc = set_eb(ctx, hdr->eb_resolved))) return rc;
+    SDQZ_CUDA(ctx, cudaMemsetAsync(bflag, 0, nblocks, ctx->stream));
+    // canonical tables from the stored bitwidths (deserialize checks + canonize)
+    if ((rc = launch_codebook(ctx, nullptr, const_cast<uint8_t*>(d_bw), cap, book, false, true, true)))
+        return rc;
+    if ((rc = launch_build_lut(ctx, book.first, book.offsets, book.symbols, -1, book.lut))) return rc;
+    if (chunks_ok) {
+        if ((rc = launch_inflate(ctx, d_payload, payload_alloc, d_cbits, C, hdr->chunk_size,
+                                 book.first, book.offsets, book.symbols, book.lut, -1, n, codes,
+                                 false)))
+            return rc;
+    }
+    if ((rc = launch_outlier_scatter(ctx, d_rec, nullptr, nullptr, k, n, codes, hdr->ndims,
+                                     hdr->dims, safe_block, dense, bflag, true)))
+        return rc;
+    if (chunks_ok) {
+        double two_eb = 2.0 * hdr->eb_resolved;
+        if ((rc = launch_reconstruct(ctx, codes, dense, bflag, true, hdr->ndims, hdr->dims,
+                                     hdr->block, cap, two_eb, d_out, hdr->dtype_code)))
+            return rc;
+    }
+    if ((rc = fetch_status(ctx))) return rc;
+    const DevStatus& s = *ctx->h_status;
+    // deserialize order (archive.py:204-237)
+    if ((rc = table_error(ctx, s.flags, true))) return rc;
+    if (unit_for((uint32_t)s.max_bw) != hdr->unit_width)
+        return set_error(ctx, SDQZ_EFORMAT, fmt("unit width %u disagrees with maximum bitwidth %llu",
+                                                 hdr->unit_width, s.max_bw));
+    if (s.flags & F_OUT_RANGE) return set_error(ctx, SDQZ_EFORMAT, "outlier index out of range");
+    if (s.flags & F_OUT_ORDER)
+        return set_error(ctx, SDQZ_EFORMAT, "outlier indices not strictly ascending");
+    if (chunks_ok && s.payload_bytes != hdr->payload_bytes)
+        return set_error(ctx, SDQZ_EFORMAT,
+                         fmt("payload of %llu bytes disagrees with chunk bit lengths (%llu bytes)",
+                             (unsigned long long)hdr->payload_bytes, s.payload_bytes));
+    if (C != ceil_div(n, hdr->chunk_size))
+        return set_error(ctx, SDQZ_EFORMAT,
+                         fmt("%llu chunks inconsistent with %llu points at chunk size %u",
+                             (unsigned long long)C, (unsigned long long)n, hdr->chunk_size));
+    if (!eb_ok) return set_error(ctx, SDQZ_EINVAL, "error bound must be positive and finite");
+    if (!geom_ok) return set_error(ctx, SDQZ_EINVAL, "all extents must be >= 1");
+    // inflate (huffman.py:292-308) then _validate_output (dualquant.py:276-296)
+    if ((rc = decode_error(ctx))) return rc;
+    if (s.flags & F_OUT_NONZERO)
+        return set_error(ctx, SDQZ_ECORRUPT, "outlier entry at a position whose code is not 0");
+    if (s.n_zero != k)
+        return set_error(ctx, SDQZ_ECORRUPT, fmt("%llu zero codes but %llu outlier entries", s.n_zero,
+                                                 (unsigned long long)k));
+    return SDQZ_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int sdqz_ctx_create(int device, void* stream, sdqz_ctx** out) {
+    if (!out) return SDQZ_EINVAL;
+    *out = nullptr;
+    cudaError_t e = cudaSetDevice(device);
+    if (e != cudaSuccess) return SDQZ_ECUDA;
+    sdqz_ctx* ctx = new sdqz_ctx();
+    ctx->device = device;
+    cudaDeviceGetAttribute(&ctx->num_sms, cudaDevAttrMultiProcessorCount, device);
+    if (stream) {
+        ctx->stream = (cudaStream_t)stream;
+    } else {
+        cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking);
+        ctx->own_stream = true;
+    }
+    if (cudaMalloc(&ctx->d_status, sizeof(DevStatus)) != cudaSuccess ||
+        cudaMallocHost(&ctx->h_status, sizeof(DevStatus)) != cudaSuccess) {
+        delete ctx;
+        return SDQZ_ECUDA;
+    }
+    ctx->bufs.resize(S_NSLOTS);
+    *out = ctx;
+    return SDQZ_OK;
+}
+
+int sdqz_ctx_destroy(sdqz_ctx* ctx) {
+    if (!ctx) return SDQZ_OK;
+    cudaSetDevice(ctx->device);
+    cudaStreamSynchronize(ctx->stream);
+    for (auto& b : ctx->bufs)
+        if (b.p) cudaFree(b.p);
+    if (ctx->d_status) cudaFree(ctx->d_status);
+    if (ctx->h_status) cudaFreeHost(ctx->h_status);
+    if (ctx->own_stream) cudaStreamDestroy(ctx->stream);
+    delete ctx;
+    return SDQZ_OK;
+}
+
+int sdqz_ctx_set_stream(sdqz_ctx* ctx, void* stream) {
+    if (ctx->own_stream) {
+        cudaStreamSynchronize(ctx->stream);
+        cudaStreamDestroy(ctx->stream);
+        ctx->own_stream = false;
+    }
+    ctx->stream = (cudaStream_t)stream;
+    return SDQZ_OK;
+}
+
+const char* sdqz_last_error(const sdqz_ctx* ctx) { return ctx ? ctx->err.c_str() : "no context"; }
+
+uint64_t sdqz_kernel_launches(const sdqz_ctx* ctx) { return ctx ? ctx->launches : 0; }
+
+// ---------------------------------------------------------------------------
+int sdqz_describe(sdqz_ctx* ctx, const void* d_in, int dtype, uint64_t n, double* vmin,
+                  double* vmax, int* nonfinite) {
+    int rc;
+    if ((rc = reset_status(ctx))) return rc;
+    if ((rc = launch_describe(ctx, d_in, dtype, n))) return rc;
+    if ((rc = fetch_status(ctx))) return rc;
+    const DevStatus& s = *ctx->h_status;
+    if (dtype == 0) {
+        *vmin = (double)ord2f((uint32_t)s.vmin_bits);
+        *vmax = (double)ord2f((uint32_t)s.vmax_bits);
+    } else {
+        *vmin = ord2d(s.vmin_bits);
+        *vmax = ord2d(s.vmax_bits);
+    }
+    *nonfinite = (s.flags & F_NONFINITE) ? 1 : 0;
+    return SDQZ_OK;
+}
+
+int sdqz_prequantize(sdqz_ctx* ctx, const void* d_in, int dtype, uint64_t n, double eb,
+                     double* d_out) {
+    int rc;
+    if ((rc = reset_status(ctx)) || (rc = set_eb(ctx, eb))) return rc;
+    if ((rc = launch_prequantize(ctx, d_in, dtype, n, d_out))) return rc;
+    return fetch_status(ctx);
+}
+
+int sdqz_dualquant(sdqz_ctx* ctx, const void* d_in, int in_kind, int ndims, const uint64_t dims[3],
+                   const uint32_t block[3], double eb, uint32_t cap, uint16_t* d_codes,
+                   uint64_t* d_hist, int* nonfinite) {
+    int rc;
+    if (ndims < 1 || ndims > 3 || !valid_cap(cap)) return set_error(ctx, SDQZ_EINVAL, "bad geometry");
+    if ((rc = reset_status(ctx)) || (rc = set_eb(ctx, eb))) return rc;
+    if (d_hist) SDQZ_CUDA(ctx, cudaMemsetAsync(d_hist, 0, cap * 8ull, ctx->stream));
+    if ((rc = launch_dualquant(ctx, d_in, in_kind, ndims, dims, block, cap, d_codes,
+                               (unsigned long long*)d_hist)))
+        return rc;
+    if ((rc = fetch_status(ctx))) return rc;
+    if (nonfinite) *nonfinite = (ctx->h_status->flags & F_NONFINITE) ? 1 : 0;
+    return SDQZ_OK;
+}
+
+int sdqz_outliers(sdqz_ctx* ctx, const void* d_in, int in_kind, const uint16_t* d_codes, uint64_t n,
+                  double eb, void* d_records, uint64_t max_k, uint64_t* k_out) {
+    int rc;
+    *k_out = 0;
+    if (n == 0) return SDQZ_OK;
+    if ((rc = reset_status(ctx)) || (rc = set_eb(ctx, eb))) return rc;
+    uint32_t* cbits = scratch_as<uint32_t>(ctx, S_CHUNK_BITS, ceil_div(n, 4096), &rc);
+    if (!cbits) return rc;
+    DeflateJob job;
+    job.codes = d_codes;
+    job.n = n;
+    job.chunk = 4096;
+    job.entries = nullptr;
+    job.cap = 65536;
+    job.chunk_bits = cbits;
+    job.payload = nullptr;
+    job.payload_cap = ~0ull;
+    job.in = d_in;
+    job.in_kind = in_kind;
+    job.out_records = d_records;
+    job.out_cap = max_k;
+    job.want_payload = false;
+    if ((rc = launch_deflate(ctx, job))) return rc;
+    if ((rc = fetch_status(ctx))) return rc;
+    *k_out = ctx->h_status->n_outliers;
+    if (ctx->h_status->flags & F_OVERFLOW)
+        return set_error(ctx, SDQZ_EINVAL, "outlier capacity exceeded");
+    return SDQZ_OK;
+}
+
+int sdqz_reconstruct(sdqz_ctx* ctx, const void* d_codes, int code_bytes, uint64_t n,
+                     const uint64_t* d_idx, const double* d_val, uint64_t k, int ndims,
+                     const uint64_t dims[3], const uint32_t block[3], double eb, uint32_t cap,
+                     void* d_out, int out_kind) {
+    int rc = SDQZ_OK;
+    const uint16_t* codes = (const uint16_t*)d_codes;
+    if ((rc = reset_status(ctx)) || (rc = set_eb(ctx, eb))) return rc;
+    if (code_bytes == 4) {
+        uint16_t* c16 = scratch_as<uint16_t>(ctx, S_CODES, n + 8, &rc);
+        if (!c16) return rc;
+        if ((rc = launch_narrow_codes(ctx, (const uint32_t*)d_codes, n, cap, c16))) return rc;
+        codes = c16;
+    }
+    uint64_t* dense = scratch_as<uint64_t>(ctx, S_DENSE, n, &rc);
+    uint64_t nblocks = 1;
+    for (int a = 0; a < ndims; a++) nblocks *= ceil_div(dims[a], block[a]);
+    uint8_t* bflag = scratch_as<uint8_t>(ctx, S_BLOCKFLAG, nblocks, &rc);
+    if (!dense || !bflag) return rc;
+    SDQZ_CUDA(ctx, cudaMemsetAsync(bflag, 0, nblocks, ctx->stream));
+    if ((rc = launch_outlier_scatter(ctx, nullptr, d_idx, d_val, k, n, codes, ndims, dims, block,
+                                     dense, bflag, false)))
+        return rc;
+    if ((rc = launch_count_zero(ctx, codes, n))) return rc;
+    if ((rc = launch_reconstruct(ctx, codes, dense, bflag, true, ndims, dims, block, cap, 2.0 * eb,
+                                 d_out, out_kind)))
+        return rc;
+    if ((rc = fetch_status(ctx))) return rc;
+    const DevStatus& s = *ctx->h_status;
+    if (s.flags & F_CODE_RANGE)
+        return set_error(ctx, SDQZ_ECORRUPT, "quantization code out of range for cap");
+    if (s.flags & F_OUT_RANGE) return set_error(ctx, SDQZ_ECORRUPT, "outlier index out of range");
+    if (s.flags & F_OUT_ORDER)
+        return set_error(ctx, SDQZ_ECORRUPT, "outlier indices must be strictly ascending");
+    if (s.flags & F_OUT_NONZERO)
+        return set_error(ctx, SDQZ_ECORRUPT, "outlier entry at a position whose code is not 0");
+    if (s.n_zero != k)
+        return set_error(ctx, SDQZ_ECORRUPT, fmt("%llu zero codes but %llu outlier entries", s.n_zero,
+                                                 (unsigned long long)k));
+    return SDQZ_OK;
+}
+
+int sdqz_histogram_u32(sdqz_ctx* ctx, const uint32_t* d_codes, uint64_t n, uint32_t cap,
+                       uint64_t* d_hist) {
+    int rc;
+    if ((rc = reset_status(ctx))) return rc;
+    SDQZ_CUDA(ctx, cudaMemsetAsync(d_hist, 0, cap * 8ull, ctx->stream));
+    if (n && (rc = launch_histogram_u32(ctx, d_codes, n, cap, (unsigned long long*)d_hist))) return rc;
+    if ((rc = fetch_status(ctx))) return rc;
+    if (ctx->h_status->flags & F_CODE_RANGE)
+        return set_error(ctx, SDQZ_ECORRUPT, fmt("quantization code outside [0, %u)", cap));
+    return SDQZ_OK;
+}
+
+int sdqz_build_tree(sdqz_ctx* ctx, const uint64_t* d_hist, uint32_t cap, uint8_t* d_bw) {
+    int rc;
+    BookDev book{};
+    if ((rc = reset_status(ctx))) return rc;
+    if ((rc = launch_codebook(ctx, (const unsigned long long*)d_hist, d_bw, cap, book, true, false,
+                              false)))
+        return rc;
+    if ((rc = fetch_status(ctx))) return rc;
+    if (ctx->h_status->flags & F_ALL_ZERO_HIST)
+        return set_error(ctx, SDQZ_EINVAL, "cannot build a code from an all-zero histogram");
+    return SDQZ_OK;
+}
+
+int sdqz_canonize(sdqz_ctx* ctx, const uint8_t* d_bw, uint32_t cap, uint64_t* d_entries,
+                  uint64_t* d_first, int64_t* d_offsets, uint32_t* d_symbols, int* unit_width,
+                  int* max_bw, uint32_t* n_present) {
+    int rc;
+    BookDev book{};
+    book.entries = d_entries;
+    book.first = d_first;
+    book.offsets = d_offsets;
+    book.symbols = d_symbols;
+    if ((rc = reset_status(ctx))) return rc;
+    if ((rc = launch_codebook(ctx, nullptr, const_cast<uint8_t*>(d_bw), cap, book, false, true,
+                              false)))
+        return rc;
+    if ((rc = fetch_status(ctx))) return rc;
+    const DevStatus& s = *ctx->h_status;
+    *max_bw = (int)s.max_bw;
+    *n_present = (uint32_t)s.n_present;
+    *unit_width = unit_for((uint32_t)s.max_bw);
+    return table_error(ctx, s.flags, false);
+}
+
+int sdqz_encode_u32(sdqz_ctx* ctx, const uint32_t* d_codes, uint64_t n, const uint64_t* d_entries,
+                    uint32_t cap, int unit_width, void* d_units) {
+    int rc;
+    if ((rc = reset_status(ctx))) return rc;
+    if (n && (rc = launch_encode_u32(ctx, d_codes, n, d_entries, cap, unit_width, d_units))) return rc;
+    if ((rc = fetch_status(ctx))) return rc;
+    uint64_t f = ctx->h_status->flags;
+    if (f & F_CODE_RANGE) return set_error(ctx, SDQZ_ECORRUPT, fmt("quantization code outside [0, %u)", cap));
+    if (f & F_ABSENT_SYM)
+        return set_error(ctx, SDQZ_ECORRUPT, "code has no codebook entry (zero frequency at build time)");
+    return SDQZ_OK;
+}
+
+int sdqz_deflate_units(sdqz_ctx* ctx, const void* d_units, int unit_width, uint64_t n, uint32_t chunk,
+                       uint32_t* d_chunk_bits, uint8_t* d_payload, uint64_t payload_cap,
+                       uint64_t* payload_bytes) {
+    int rc;
+    *payload_bytes = 0;
+    if (chunk < 1) return set_error(ctx, SDQZ_EINVAL, "chunk_size must be >= 1");
+    if (n == 0) return SDQZ_OK;
+    if ((rc = reset_status(ctx))) return rc;
+    DeflateJob job;
+    job.units = d_units;
+    job.units_width = unit_width;
+    job.n = n;
+    job.chunk = chunk;
+    job.chunk_bits = d_chunk_bits;
+    job.payload = d_payload;
+    job.payload_cap = payload_cap;
+    if ((rc = launch_deflate(ctx, job))) return rc;
+    if ((rc = fetch_status(ctx))) return rc;
+    const DevStatus& s = *ctx->h_status;
+    if (s.flags & F_ZERO_WIDTH) return set_error(ctx, SDQZ_ECORRUPT, "packed unit with zero bitwidth");
+    if (s.flags & F_OVERFLOW) return set_error(ctx, SDQZ_EINVAL, "payload capacity exceeded");
+    *payload_bytes = s.payload_bytes;
+    return SDQZ_OK;
+}
+
+int sdqz_inflate(sdqz_ctx* ctx, const uint8_t* d_payload, uint64_t payload_bytes,
+                 const uint32_t* d_chunk_bits, uint64_t n_chunks, uint32_t chunk,
+                 const uint64_t* d_first, const int64_t* d_offsets, const uint32_t* d_symbols,
+                 int max_bw, uint64_t n, uint32_t* d_codes_u32) {
+    int rc = SDQZ_OK;
+    if (max_bw < 1 || max_bw > kMaxBw) return set_error(ctx, SDQZ_EINVAL, "bad max bitwidth");
+    uint32_t* lut = scratch_as<uint32_t>(ctx, S_LUT, 1u << kLutBits, &rc);
+    if (!lut) return rc;
+    if ((rc = reset_status(ctx))) return rc;
+    if ((rc = launch_build_lut(ctx, d_first, d_offsets, d_symbols, max_bw, lut))) return rc;
+    if ((rc = launch_inflate(ctx, d_payload, payload_bytes, d_chunk_bits, n_chunks, chunk, d_first,
+                             d_offsets, d_symbols, lut, max_bw, n, d_codes_u32, true)))
+        return rc;
+    if ((rc = fetch_status(ctx))) return rc;
+    return decode_error(ctx);
+}
+
+// ---------------------------------------------------------------------------
+// fused pipeline
+// ---------------------------------------------------------------------------
+int sdqz_compress(sdqz_ctx* ctx, const void* d_in, int dtype, int ndims, const uint64_t dims[3],
+                  const uint32_t block[3], int eb_mode, double eb, uint32_t cap, uint32_t chunk,
+                  sdqz_header* hdr) {
+    int rc = SDQZ_OK;
+    ctx->have_archive = false;
+    if (ndims < 1 || ndims > 3) return set_error(ctx, SDQZ_EINVAL, "rank must be 1-3");
+    if (!valid_cap(cap)) return set_error(ctx, SDQZ_EINVAL, "bad cap");
+    const uint64_t n = prod3(dims);
+    if (n == 0) return set_error(ctx, SDQZ_EINVAL, "empty field");
+    const uint32_t cs = chunk ? chunk : default_chunk_size(n);
+    const uint64_t C = ceil_div(n, cs);
+    const int in_kind = dtype;
+
+    uint16_t* codes = scratch_as<uint16_t>(ctx, S_CODES, n + 8, &rc);
+    unsigned long long* hist = scratch_as<unsigned long long>(ctx, S_HIST, cap, &rc);
+    uint32_t* cbits = scratch_as<uint32_t>(ctx, S_CHUNK_BITS, C, &rc);
+    BookDev book;
+    if (!codes || !hist || !cbits) return rc;
+    if ((rc = book_tables(ctx, cap, &book))) return rc;
+    // first-guess capacities; exact sizes are known after the chunk scan
+    uint64_t pay_cap = ctx->bufs[S_PAYLOAD].bytes ? ctx->bufs[S_PAYLOAD].bytes : (n / 2 + C + 4096);
+    uint64_t rec_cap = ctx->bufs[S_OUTREC].bytes ? ctx->bufs[S_OUTREC].bytes / 16 : (n / 32 + 1024);
+    uint8_t* payload = scratch_as<uint8_t>(ctx, S_PAYLOAD, pay_cap, &rc);
+    unsigned long long* rec = scratch_as<unsigned long long>(ctx, S_OUTREC, 2 * rec_cap, &rc);
+    if (!payload || !rec) return rc;
+
+    if ((rc = reset_status(ctx))) return rc;
+    if (eb_mode == 1 || !(eb > 0 && std::isfinite(eb))) {
+        if ((rc = launch_describe(ctx, d_in, dtype, n))) return rc;
+    }
+    if ((rc = launch_resolve(ctx, dtype, eb_mode, eb))) return rc;
+    SDQZ_CUDA(ctx, cudaMemsetAsync(hist, 0, cap * 8ull, ctx->stream));
+    if ((rc = launch_dualquant(ctx, d_in, in_kind, ndims, dims, block, cap, codes, hist))) return rc;
+    if ((rc = launch_codebook(ctx, hist, book.bw, cap, book, true, true, false))) return rc;
+    DeflateJob job;
+    job.codes = codes;
+    job.n = n;
+    job.chunk = cs;
+    job.entries = book.entries;
+    job.cap = cap;
+    job.chunk_bits = cbits;
+    job.payload = payload;
+    job.payload_cap = pay_cap;
+    job.in = d_in;
+    job.in_kind = in_kind;
+    job.out_records = rec;
+    job.out_cap = rec_cap;
+    if ((rc = launch_deflate(ctx, job))) return rc;
+    if ((rc = fetch_status(ctx))) return rc;
+    uint64_t f = ctx->h_status->flags;
+    // resolve_error_bound / QuantConfig order (core.py:161-175, :87-89)
+    if (f & F_NONFINITE)
+        return set_error(ctx, SDQZ_EINVAL, "field contains NaN/Inf values and cannot be compressed");
+    if (!(eb > 0 && std::isfinite(eb))) return set_error(ctx, SDQZ_EINVAL, "error bound must be positive");
+    if (f & F_RANGE_ZERO)
+        return set_error(ctx, SDQZ_EINVAL,
+                         "value-range-relative bound is undefined on a constant field; use an "
+                         "absolute error bound instead");
+    double ebr = ctx->h_status->eb;
+    if (!(ebr > 0 && std::isfinite(ebr)))
+        return set_error(ctx, SDQZ_EINVAL, "error bound must be positive and finite");
+    if ((rc = table_error(ctx, f, false))) return rc;
+    if (f & F_OVERFLOW) {
+        // grow to the exact sizes and redo the deflate stage only
+        uint64_t P = ctx->h_status->payload_bytes, K = ctx->h_status->n_outliers;
+        payload = scratch_as<uint8_t>(ctx, S_PAYLOAD, P + 64, &rc);
+        rec = scratch_as<unsigned long long>(ctx, S_OUTREC, 2 * (K + 1), &rc);
+        if (!payload || !rec) return rc;
+        job.payload = payload;
+        job.payload_cap = ctx->bufs[S_PAYLOAD].bytes;
+        job.out_records = rec;
+        job.out_cap = ctx->bufs[S_OUTREC].bytes / 16;
+        // clear the overflow flag, keep eb / max_bw
+        SDQZ_CUDA(ctx, cudaMemsetAsync(&ctx->d_status->flags, 0, 8, ctx->stream));
+        if ((rc = launch_deflate(ctx, job))) return rc;
+        if ((rc = fetch_status(ctx))) return rc;
+        if (ctx->h_status->flags & F_OVERFLOW)
+            return set_error(ctx, SDQZ_EINVAL, "internal: capacity still exceeded");
+    }
+    const DevStatus& s = *ctx->h_status;
+    // zero padding after the payload: decoders peek past the last chunk (huffman.py:338)
+    {
+        auto& pb = ctx->bufs[S_PAYLOAD];
+        uint64_t pad = std::min<uint64_t>(64, pb.bytes - s.payload_bytes);
+        SDQZ_CUDA(ctx, cudaMemsetAsync((uint8_t*)pb.p + s.payload_bytes, 0, pad, ctx->stream));
+    }
+    sdqz_header h{};
+    h.dtype_code = (uint8_t)dtype;
+    h.ndims = (uint8_t)ndims;
+    h.eb_mode = (uint8_t)eb_mode;
+    h.unit_width = (uint8_t)unit_for((uint32_t)s.max_bw);
+    for (int a = 0; a < 3; a++) {
+        h.dims[a] = a < ndims ? dims[a] : 1;
+        h.block[a] = a < ndims ? block[a] : 1;
+    }
+    h.eb_resolved = s.eb;
+    h.eb_specified = eb;
+    h.cap = cap;
+    h.chunk_size = cs;
+    h.n_outliers = s.n_outliers;
+    h.n_chunks = C;
+    h.payload_bytes = s.payload_bytes;
+    ctx->last_hdr = h;
+    ctx->have_archive = true;
+    if (hdr) *hdr = h;
+    return SDQZ_OK;
+}
+
+uint64_t sdqz_archive_size(const sdqz_ctx* ctx) {
+    return ctx->have_archive ? archive_total(ctx->last_hdr) : 0;
+}
+
+int sdqz_archive_sections(sdqz_ctx* ctx, const uint8_t** d_bw, const void** d_outliers,
+                          const uint32_t** d_chunk_bits, const uint8_t** d_payload) {
+    if (!ctx->have_archive) return set_error(ctx, SDQZ_EINVAL, "no archive");
+    *d_bw = (const uint8_t*)ctx->bufs[S_BW].p;
+    *d_outliers = ctx->bufs[S_OUTREC].p;
+    *d_chunk_bits = (const uint32_t*)ctx->bufs[S_CHUNK_BITS].p;
+    *d_payload = (const uint8_t*)ctx->bufs[S_PAYLOAD].p;
+    return SDQZ_OK;
+}
+
+int sdqz_archive_write(sdqz_ctx* ctx, uint8_t* h_dst, uint64_t capacity) {
+    if (!ctx->have_archive) return set_error(ctx, SDQZ_EINVAL, "no archive");
+    const sdqz_header& h = ctx->last_hdr;
+    uint64_t total = archive_total(h);
+    if (capacity < total) return set_error(ctx, SDQZ_EINVAL, "destination too small");
+    put_header(h_dst, h);
+    uint8_t* p = h_dst + SDQZ_HEADER_SIZE;
+    SDQZ_CUDA(ctx, cudaMemcpyAsync(p, ctx->bufs[S_BW].p, h.cap, cudaMemcpyDeviceToHost, ctx->stream));
+    p += h.cap;
+    if (h.n_outliers)
+        SDQZ_CUDA(ctx, cudaMemcpyAsync(p, ctx->bufs[S_OUTREC].p, 16 * h.n_outliers,
+                                       cudaMemcpyDeviceToHost, ctx->stream));
+    p += 16 * h.n_outliers;
+    SDQZ_CUDA(ctx, cudaMemcpyAsync(p, ctx->bufs[S_CHUNK_BITS].p, 4 * h.n_chunks,
+                                   cudaMemcpyDeviceToHost, ctx->stream));
+    p += 4 * h.n_chunks;
+    if (h.payload_bytes)
+        SDQZ_CUDA(ctx, cudaMemcpyAsync(p, ctx->bufs[S_PAYLOAD].p, h.payload_bytes,
+                                       cudaMemcpyDeviceToHost, ctx->stream));
+    SDQZ_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
+    return SDQZ_OK;
+}
+
+int sdqz_parse_header(sdqz_ctx* ctx, const uint8_t* b, uint64_t len, sdqz_header* h) {
+    if (len < SDQZ_HEADER_SIZE)
+        return set_error(ctx, SDQZ_EFORMAT, fmt("short read: %llu bytes, header needs %d",
+                                                 (unsigned long long)len, SDQZ_HEADER_SIZE));
+    if (memcmp(b, "SDQZ", 4) != 0) {
+        // Python formats the bytes literal; report a marker the binding rewrites
+        return set_error(ctx, SDQZ_EFORMAT, "bad magic");
+    }
+    if (b[4] != 1) return set_error(ctx, SDQZ_EFORMAT, fmt("unsupported version %u", b[4]));
+    if (b[5] > 1) return set_error(ctx, SDQZ_EFORMAT, fmt("unsupported dtype code %u", b[5]));
+    if (b[6] < 1 || b[6] > 3) return set_error(ctx, SDQZ_EFORMAT, fmt("unsupported rank %u", b[6]));
+    if (b[7] > 1) return set_error(ctx, SDQZ_EFORMAT, fmt("unknown error-bound mode %u", b[7]));
+    if (b[68] != 32 && b[68] != 64)
+        return set_error(ctx, SDQZ_EFORMAT, fmt("unsupported unit width %u", b[68]));
+    h->dtype_code = b[5];
+    h->ndims = b[6];
+    h->eb_mode = b[7];
+    h->unit_width = b[68];
+    memcpy(h->dims, b + 8, 24);
+    memcpy(&h->eb_resolved, b + 32, 8);
+    memcpy(&h->eb_specified, b + 40, 8);
+    memcpy(&h->cap, b + 48, 4);
+    memcpy(h->block, b + 52, 12);
+    memcpy(&h->chunk_size, b + 64, 4);
+    memcpy(&h->n_outliers, b + 69, 8);
+    memcpy(&h->n_chunks, b + 77, 8);
+    memcpy(&h->payload_bytes, b + 85, 8);
+    // n_points over the field dims (archive.py:68-73), Python ints never overflow:
+    // treat a product overflow as positive-but-huge (rejected by size checks).
+    uint64_t n = 1;
+    bool zero = false;
+    for (int a = 0; a < h->ndims; a++) {
+        if (h->dims[a] == 0) zero = true;
+        n *= h->dims[a];
+    }
+    if (zero) return set_error(ctx, SDQZ_EFORMAT, "dims product must be positive");
+    if (!valid_cap(h->cap))
+        return set_error(ctx, SDQZ_EFORMAT, fmt("cap %u is not a power of two in [4, 65536]", h->cap));
+    if (!(h->eb_resolved > 0)) return set_error(ctx, SDQZ_EFORMAT, "resolved error bound must be positive");
+    if (h->chunk_size < 1) return set_error(ctx, SDQZ_EFORMAT, "chunk size must be >= 1");
+    (void)n;
+    return SDQZ_OK;
+}
+
+int sdqz_decompress_sections(sdqz_ctx* ctx, const sdqz_header* hdr, const uint8_t* d_bw,
+                             const void* d_outliers, const uint32_t* d_chunk_bits,
+                             const uint8_t* d_payload, void* d_out) {
+    return decompress_core(ctx, hdr, d_bw, d_outliers, d_chunk_bits, d_payload, hdr->payload_bytes,
+                           d_out);
+}
+
+int sdqz_decompress(sdqz_ctx* ctx, const uint8_t* h, uint64_t len, void* d_out) {
+    int rc = SDQZ_OK;
+    sdqz_header hdr;
+    if ((rc = sdqz_parse_header(ctx, h, len, &hdr))) return rc;
+    uint64_t total = archive_total(hdr);
+    if (len < total)
+        return set_error(ctx, SDQZ_EFORMAT, fmt("short read: %llu bytes, header promises %llu",
+                                                 (unsigned long long)len, (unsigned long long)total));
+    if (len > total)
+        return set_error(ctx, SDQZ_EFORMAT,
+                         fmt("%llu trailing bytes after the archive", (unsigned long long)(len - total)));
+    // stage the sections into aligned device buffers (payload padded with zeros)
+    const uint8_t* p = h + SDQZ_HEADER_SIZE;
+    uint8_t* bw = scratch_as<uint8_t>(ctx, S_STAGE, hdr.cap + 16, &rc);
+    void* rec = scratch_as<uint8_t>(ctx, S_MISC, 16 * hdr.n_outliers + 16, &rc);
+    uint32_t* cb = scratch_as<uint32_t>(ctx, S_CHUNK_AUX, hdr.n_chunks + 4, &rc);
+    uint8_t* pay = scratch_as<uint8_t>(ctx, S_SORT, hdr.payload_bytes + 64, &rc);
+    if (!bw || !rec || !cb || !pay) return rc;
+    SDQZ_CUDA(ctx, cudaMemcpyAsync(bw, p, hdr.cap, cudaMemcpyHostToDevice, ctx->stream));
+    p += hdr.cap;
+    if (hdr.n_outliers)
+        SDQZ_CUDA(ctx, cudaMemcpyAsync(rec, p, 16 * hdr.n_outliers, cudaMemcpyHostToDevice, ctx->stream));
+    p += 16 * hdr.n_outliers;
+    if (hdr.n_chunks)
+        SDQZ_CUDA(ctx, cudaMemcpyAsync(cb, p, 4 * hdr.n_chunks, cudaMemcpyHostToDevice, ctx->stream));
+    p += 4 * hdr.n_chunks;
+    SDQZ_CUDA(ctx, cudaMemsetAsync(pay + hdr.payload_bytes, 0, 64, ctx->stream));
+    if (hdr.payload_bytes)
+        SDQZ_CUDA(ctx, cudaMemcpyAsync(pay, p, hdr.payload_bytes, cudaMemcpyHostToDevice, ctx->stream));
+    return sdqz_decompress_sections(ctx, &hdr, bw, rec, cb, pay, d_out);
+}
+
+}  // extern "C"

@@ -1,0 +1,559 @@
+// dualquant.cu -- K2: fused prequantization + blockwise Lorenzo postquantization
+// + quant-code histogram (dualquant.py:62-194, huffman.py:77-95).
+//
+// Layout: the field is row-major (axis 0 slowest).  A warp owns a "task" of
+// 512 points -- 3D: 4 blocks of 8x8x8 side by side along x (lane = x), the
+// warp walks the 8 planes x 8 rows; 2D: 2 blocks of 16x16 (lane = x, walks 16
+// rows); 1D: 16 consecutive blocks of 32 (lane = position in block).  Every
+// warp load/store is one contiguous 128 B (fp32 in) / 64 B (u16 codes) row
+// segment, so the kernel streams 4N + 2N bytes at HBM rate.
+//
+// Arithmetic.  Prequantization is IEEE fp64 division + floor(|x|+.5) +
+// copysign exactly as dualquant.py:76-77.  The Lorenzo residual is computed
+// in int32 as D_z D_y D_x d (finite differences, one shuffle per point) when
+// every prequantized value of the warp's task is below 2^27 in magnitude
+// (then all partial sums are exact integers and equal the reference's fp64
+// result); otherwise the warp recomputes its task in fp64 with the reference's
+// 7-term order (dualquant.py:125-129), which is bit-exact for any magnitude.
+// Non-default block shapes take a generic one-thread-per-point fp64 kernel.
+//
+// Histogram: 16 bins around the radius are counted in packed 8-bit register
+// counters (two u64 per thread, flushed per task with __reduce_add_sync);
+// codes outside that window use shared-memory atomics; each CTA merges its
+// shared histogram into the global uint64 histogram once.
+#include "kernels.cuh"
+
+namespace sdqz {
+
+namespace {
+
+constexpr int kThreads = 256;
+constexpr int kWarpsPerCta = kThreads / 32;
+constexpr uint32_t kSmemHistMax = 16384;   // caps above this count in global memory
+constexpr double kIntSafe = 134217728.0;   // 2^27
+
+struct HistCtx {
+    uint32_t* shist;                 // shared (or null => global)
+    unsigned long long* ghist;       // global uint64[cap] (may be null: no histogram)
+    uint32_t cap, wbase;             // window = [wbase, wbase + 16)
+    unsigned long long lo, hi;       // packed 8-bit counters
+};
+
+__device__ __forceinline__ void hist_add(HistCtx& h, uint32_t code) {
+    uint32_t dw = code - h.wbase;
+    if (dw < 16u) {
+        unsigned long long inc = 1ull << (8 * (dw & 7));
+        if (dw < 8) h.lo += inc; else h.hi += inc;
+    } else if (h.shist) {
+        atomicAdd(&h.shist[code], 1u);
+    } else if (h.ghist) {
+        atomicAdd(&h.ghist[code], 1ull);
+    }
+}
+
+__device__ __forceinline__ void hist_flush(HistCtx& h) {
+#pragma unroll
+    for (int k = 0; k < 16; k++) {
+        uint32_t c = (uint32_t)(((k < 8) ? (h.lo >> (8 * k)) : (h.hi >> (8 * (k - 8)))) & 0xFF);
+        uint32_t s = __reduce_add_sync(kFull, c);
+        if (s && lane_id() == 0) {
+            uint32_t bin = h.wbase + k;
+            if (h.shist) atomicAdd(&h.shist[bin], s);
+            else if (h.ghist) atomicAdd(&h.ghist[bin], (unsigned long long)s);
+        }
+    }
+    h.lo = h.hi = 0;
+}
+
+template <int KIND>
+__device__ __forceinline__ double load_q(const void* in, uint64_t i, double two_eb, bool& bad) {
+    double v;
+    if (KIND == 0) v = (double)__ldg((const float*)in + i);
+    else v = __ldg((const double*)in + i);
+    bad |= !isfinite(v);
+    return KIND == 2 ? v : prequant(v, two_eb);
+}
+
+__device__ __forceinline__ uint32_t code_of_int(int delta, int r) {
+    return (delta > -r && delta < r) ? (uint32_t)(delta + r) : 0u;
+}
+__device__ __forceinline__ uint32_t code_of_f64(double delta, int r) {
+    return (delta > (double)-r && delta < (double)r) ? (uint32_t)__dadd_rn(delta, (double)r) : 0u;
+}
+
+__device__ __forceinline__ void hist_init(HistCtx& h, uint32_t* smem, unsigned long long* ghist,
+                                          uint32_t cap) {
+    h.ghist = ghist;
+    h.cap = cap;
+    h.shist = (ghist && cap <= kSmemHistMax) ? smem : nullptr;
+    h.wbase = cap >= 16 ? cap / 2 - 8 : 0;
+    h.lo = h.hi = 0;
+    if (h.shist) {
+        for (uint32_t i = threadIdx.x; i < cap; i += blockDim.x) h.shist[i] = 0;
+    }
+    __syncthreads();
+}
+
+__device__ __forceinline__ void hist_finish(HistCtx& h) {
+    __syncthreads();
+    if (h.shist) {
+        for (uint32_t i = threadIdx.x; i < h.cap; i += blockDim.x) {
+            uint32_t c = h.shist[i];
+            if (c) atomicAdd(&h.ghist[i], (unsigned long long)c);
+        }
+    }
+}
+
+// ----------------------------------------------------------------------------
+// Task loading.  fp32 input: all of a task's values are loaded up front (one
+// coalesced 128 B row per load, 16-64 loads in flight per warp) and kept as
+// floats; a conservative bound max|x| / 2eb < 2^27 - 4 decides, per warp,
+// whether the exact int32 path applies (then every |d| < 2^27).  fp64 input
+// is loaded row by row (register budget) and always takes the fp64 path
+// check per value.
+// ----------------------------------------------------------------------------
+template <int KIND>
+struct Raw { using T = double; };
+template <>
+struct Raw<0> { using T = float; };
+
+template <int KIND>
+__device__ __forceinline__ typename Raw<KIND>::T load_raw(const void* in, uint64_t i) {
+    if (KIND == 0) return __ldg((const float*)in + i);
+    return __ldg((const double*)in + i);
+}
+
+template <int KIND>
+__device__ __forceinline__ double to_q(typename Raw<KIND>::T v, double two_eb) {
+    return KIND == 2 ? (double)v : prequant((double)v, two_eb);
+}
+
+constexpr double kIntBound = 134217724.0;   // 2^27 - 4
+
+// ----------------------------------------------------------------------------
+// 3D, block 8x8x8
+// ----------------------------------------------------------------------------
+template <int KIND>
+__global__ void __launch_bounds__(kThreads, 2) dq3d_kernel(const void* __restrict__ in, uint64_t Z,
+                                                           uint64_t Y, uint64_t X, uint32_t cap,
+                                                           DevStatus* st, uint16_t* __restrict__ codes,
+                                                           unsigned long long* ghist) {
+    using T = typename Raw<KIND>::T;
+    extern __shared__ uint32_t smem_hist[];
+    HistCtx h;
+    hist_init(h, smem_hist, ghist, cap);
+    const double two_eb = st->two_eb;
+    const int r = (int)(cap >> 1);
+    const uint32_t lane = lane_id(), xl = lane & 7;
+    const uint64_t nbx4 = ceil_div(ceil_div(X, 8), 4), nby = ceil_div(Y, 8), nbz = ceil_div(Z, 8);
+    const uint64_t ntask = nbx4 * nby * nbz;
+    const uint64_t YX = Y * X;
+    bool bad = false;
+    for (uint64_t task = blockIdx.x * (uint64_t)kWarpsPerCta + (threadIdx.x >> 5); task < ntask;
+         task += (uint64_t)gridDim.x * kWarpsPerCta) {
+        const uint64_t bx4 = task % nbx4, t2 = task / nbx4;
+        const uint64_t by = t2 % nby, bz = t2 / nby;
+        const uint64_t x = bx4 * 32 + lane, y0 = by * 8, z0 = bz * 8;
+        const bool xin = x < X;
+        const int ny = (int)umin(8, Y - y0), nz = (int)umin(8, Z - z0);
+        const uint64_t base = z0 * YX + y0 * X + x;
+        bool use_int = false;
+        if (KIND == 0) {
+            float raw[8][8];
+            float mx = 0.f;
+#pragma unroll
+            for (int z = 0; z < 8; z++)
+#pragma unroll
+                for (int y = 0; y < 8; y++) {
+                    float v = 0.f;
+                    if (xin && z < nz && y < ny) v = load_raw<0>(in, base + z * YX + y * X);
+                    raw[z][y] = v;
+                    mx = fmaxf(mx, fabsf(v));   // NaN -> ignored by fmaxf; flagged below
+                    bad |= !isfinite(v);
+                }
+            use_int = __all_sync(kFull, !bad && (double)mx / two_eb < kIntBound);
+            if (use_int) {
+                int hprev[8];
+#pragma unroll
+                for (int z = 0; z < 8; z++) {
+                    int gprev = 0;
+#pragma unroll
+                    for (int y = 0; y < 8; y++) {
+                        int v = (int)prequant((double)raw[z][y], two_eb);
+                        int left = __shfl_up_sync(kFull, v, 1);
+                        int g = v - (xl ? left : 0);
+                        int hh = g - gprev;
+                        gprev = g;
+                        int delta = hh - (z ? hprev[y] : 0);
+                        hprev[y] = hh;
+                        if (xin && z < nz && y < ny) {
+                            uint32_t c = code_of_int(delta, r);
+                            codes[base + z * YX + y * X] = (uint16_t)c;
+                            hist_add(h, c);
+                        }
+                    }
+                }
+            }
+        }
+        if (!use_int) {
+            // fp64, reference term order (dualquant.py:125-129):
+            // +(z-1,y,x) +(z,y-1,x) +(z,y,x-1) -(z-1,y-1,x) -(z-1,y,x-1) -(z,y-1,x-1) +(z-1,y-1,x-1)
+            double P[8];
+#pragma unroll
+            for (int y = 0; y < 8; y++) P[y] = 0.0;
+            for (int z = 0; z < 8; z++) {
+                double cprev = 0.0, pold = 0.0;
+#pragma unroll
+                for (int y = 0; y < 8; y++) {
+                    double q = 0.0;
+                    if (xin && z < nz && y < ny) {
+                        T v = load_raw<KIND>(in, base + z * YX + y * X);
+                        bad |= !isfinite((double)v);
+                        q = to_q<KIND>(v, two_eb);
+                    }
+                    const double pz = P[y];
+                    const double pzm = pold;           // P_old[y-1] (0 for y == 0)
+                    const double cm = cprev;           // (z, y-1, x)  (0 for y == 0)
+                    double n_c = __shfl_up_sync(kFull, q, 1);
+                    double n_pz = __shfl_up_sync(kFull, pz, 1);
+                    double n_cm = __shfl_up_sync(kFull, cm, 1);
+                    double n_pzm = __shfl_up_sync(kFull, pzm, 1);
+                    if (!xl) n_c = n_pz = n_cm = n_pzm = 0.0;
+                    double pred = __dadd_rn(pz, cm);
+                    pred = __dadd_rn(pred, n_c);
+                    pred = __dsub_rn(pred, pzm);
+                    pred = __dsub_rn(pred, n_pz);
+                    pred = __dsub_rn(pred, n_cm);
+                    pred = __dadd_rn(pred, n_pzm);
+                    const double delta = __dsub_rn(q, pred);
+                    pold = pz;
+                    P[y] = q;
+                    cprev = q;
+                    if (xin && z < nz && y < ny) {
+                        uint32_t c = code_of_f64(delta, r);
+                        codes[base + z * YX + y * X] = (uint16_t)c;
+                        hist_add(h, c);
+                    }
+                }
+            }
+        }
+        hist_flush(h);
+    }
+    if (__any_sync(kFull, bad) && lane == 0) atomicOr(&st->flags, (unsigned long long)F_NONFINITE);
+    hist_finish(h);
+}
+
+// ----------------------------------------------------------------------------
+// 2D, block 16x16
+// ----------------------------------------------------------------------------
+template <int KIND>
+__global__ void __launch_bounds__(kThreads, 2) dq2d_kernel(const void* __restrict__ in, uint64_t Y,
+                                                           uint64_t X, uint32_t cap, DevStatus* st,
+                                                           uint16_t* __restrict__ codes,
+                                                           unsigned long long* ghist) {
+    using T = typename Raw<KIND>::T;
+    extern __shared__ uint32_t smem_hist[];
+    HistCtx h;
+    hist_init(h, smem_hist, ghist, cap);
+    const double two_eb = st->two_eb;
+    const int r = (int)(cap >> 1);
+    const uint32_t lane = lane_id(), xl = lane & 15;
+    const uint64_t nbx2 = ceil_div(ceil_div(X, 16), 2), nby = ceil_div(Y, 16);
+    const uint64_t ntask = nbx2 * nby;
+    bool bad = false;
+    for (uint64_t task = blockIdx.x * (uint64_t)kWarpsPerCta + (threadIdx.x >> 5); task < ntask;
+         task += (uint64_t)gridDim.x * kWarpsPerCta) {
+        const uint64_t bx2 = task % nbx2, by = task / nbx2;
+        const uint64_t x = bx2 * 32 + lane, y0 = by * 16;
+        const bool xin = x < X;
+        const int ny = (int)umin(16, Y - y0);
+        const uint64_t base = y0 * X + x;
+        bool use_int = false;
+        if (KIND == 0) {
+            float raw[16];
+            float mx = 0.f;
+#pragma unroll
+            for (int y = 0; y < 16; y++) {
+                float v = 0.f;
+                if (xin && y < ny) v = load_raw<0>(in, base + y * X);
+                raw[y] = v;
+                mx = fmaxf(mx, fabsf(v));
+                bad |= !isfinite(v);
+            }
+            use_int = __all_sync(kFull, !bad && (double)mx / two_eb < kIntBound);
+            if (use_int) {
+                int gprev = 0;
+#pragma unroll
+                for (int y = 0; y < 16; y++) {
+                    int v = (int)prequant((double)raw[y], two_eb);
+                    int left = __shfl_up_sync(kFull, v, 1);
+                    int g = v - (xl ? left : 0);
+                    int delta = g - gprev;
+                    gprev = g;
+                    if (xin && y < ny) {
+                        uint32_t c = code_of_int(delta, r);
+                        codes[base + y * X] = (uint16_t)c;
+                        hist_add(h, c);
+                    }
+                }
+            }
+        }
+        if (!use_int) {
+            // (y-1,x) + (y,x-1) - (y-1,x-1)   (dualquant.py:123-124)
+            double cprev = 0.0;
+            for (int y = 0; y < 16; y++) {
+                double q = 0.0;
+                if (xin && y < ny) {
+                    T v = load_raw<KIND>(in, base + y * X);
+                    bad |= !isfinite((double)v);
+                    q = to_q<KIND>(v, two_eb);
+                }
+                const double cm = cprev;
+                double n_c = __shfl_up_sync(kFull, q, 1);
+                double n_cm = __shfl_up_sync(kFull, cm, 1);
+                if (!xl) n_c = n_cm = 0.0;
+                const double pred = __dsub_rn(__dadd_rn(cm, n_c), n_cm);
+                const double delta = __dsub_rn(q, pred);
+                cprev = q;
+                if (xin && y < ny) {
+                    uint32_t c = code_of_f64(delta, r);
+                    codes[base + y * X] = (uint16_t)c;
+                    hist_add(h, c);
+                }
+            }
+        }
+        hist_flush(h);
+    }
+    if (__any_sync(kFull, bad) && lane == 0) atomicOr(&st->flags, (unsigned long long)F_NONFINITE);
+    hist_finish(h);
+}
+
+// ----------------------------------------------------------------------------
+// 1D, block 32: task = 16 consecutive blocks (512 points)
+// ----------------------------------------------------------------------------
+template <int KIND>
+__global__ void __launch_bounds__(kThreads, 2) dq1d_kernel(const void* __restrict__ in, uint64_t X,
+                                                           uint32_t cap, DevStatus* st,
+                                                           uint16_t* __restrict__ codes,
+                                                           unsigned long long* ghist) {
+    using T = typename Raw<KIND>::T;
+    extern __shared__ uint32_t smem_hist[];
+    HistCtx h;
+    hist_init(h, smem_hist, ghist, cap);
+    const double two_eb = st->two_eb;
+    const int r = (int)(cap >> 1);
+    const uint32_t lane = lane_id();
+    const uint64_t ntask = ceil_div(X, 512);
+    bool bad = false;
+    for (uint64_t task = blockIdx.x * (uint64_t)kWarpsPerCta + (threadIdx.x >> 5); task < ntask;
+         task += (uint64_t)gridDim.x * kWarpsPerCta) {
+        const uint64_t base = task * 512 + lane;
+        bool use_int = false;
+        if (KIND == 0) {
+            float raw[16];
+            float mx = 0.f;
+#pragma unroll
+            for (int j = 0; j < 16; j++) {
+                float v = 0.f;
+                if (base + j * 32 < X) v = load_raw<0>(in, base + j * 32);
+                raw[j] = v;
+                mx = fmaxf(mx, fabsf(v));
+                bad |= !isfinite(v);
+            }
+            use_int = __all_sync(kFull, !bad && (double)mx / two_eb < kIntBound);
+            if (use_int) {
+#pragma unroll
+                for (int j = 0; j < 16; j++) {
+                    int v = (int)prequant((double)raw[j], two_eb);
+                    int left = __shfl_up_sync(kFull, v, 1);
+                    int delta = v - (lane ? left : 0);
+                    if (base + j * 32 < X) {
+                        uint32_t c = code_of_int(delta, r);
+                        codes[base + j * 32] = (uint16_t)c;
+                        hist_add(h, c);
+                    }
+                }
+            }
+        }
+        if (!use_int) {
+            for (int j = 0; j < 16; j++) {
+                const uint64_t i = base + j * 32;
+                double q = 0.0;
+                if (i < X) {
+                    T v = load_raw<KIND>(in, i);
+                    bad |= !isfinite((double)v);
+                    q = to_q<KIND>(v, two_eb);
+                }
+                double n_c = __shfl_up_sync(kFull, q, 1);
+                if (!lane) n_c = 0.0;
+                const double delta = __dsub_rn(q, n_c);
+                if (i < X) {
+                    uint32_t c = code_of_f64(delta, r);
+                    codes[i] = (uint16_t)c;
+                    hist_add(h, c);
+                }
+            }
+        }
+        hist_flush(h);
+    }
+    if (__any_sync(kFull, bad) && lane == 0) atomicOr(&st->flags, (unsigned long long)F_NONFINITE);
+    hist_finish(h);
+}
+
+// ----------------------------------------------------------------------------
+// Generic block shapes: one thread per point, fp64 reference order.
+// ----------------------------------------------------------------------------
+struct Geo {
+    int nd;
+    uint64_t dims[3];
+    uint32_t block[3];
+    uint64_t stride[3];
+};
+
+template <int KIND>
+__global__ void __launch_bounds__(kThreads) dq_generic_kernel(const void* __restrict__ in, Geo g,
+                                                              uint64_t n, uint32_t cap,
+                                                              DevStatus* st,
+                                                              uint16_t* __restrict__ codes,
+                                                              unsigned long long* ghist) {
+    extern __shared__ uint32_t smem_hist[];
+    HistCtx h;
+    hist_init(h, smem_hist, ghist, cap);
+    const double two_eb = st->two_eb;
+    const int r = (int)(cap >> 1);
+    bool bad = false;
+    uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+    uint64_t ntot = ceil_div(n, 32) * 32;   // keep whole warps alive for the flushes
+    uint32_t cnt = 0;
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < ntot; i += stride) {
+        if (i < n) {
+            uint64_t c[3] = {0, 0, 0}, rem = i;
+            bool lead[3] = {true, true, true};
+            for (int a = 0; a < g.nd; a++) {
+                c[a] = rem / g.stride[a];
+                rem -= c[a] * g.stride[a];
+                lead[a] = (c[a] % g.block[a]) == 0;   // neighbour at -1 is padding
+            }
+            auto val = [&](int da, int db, int dc) -> double {
+                int dd[3] = {da, db, dc};
+                uint64_t j = i;
+                for (int a = 0; a < g.nd; a++) {
+                    if (dd[a]) {
+                        if (lead[a]) return 0.0;
+                        j -= g.stride[a];
+                    }
+                }
+                return load_q<KIND>(in, j, two_eb, bad);
+            };
+            double q = val(0, 0, 0);
+            double pred;
+            if (g.nd == 1) {
+                pred = val(1, 0, 0);
+            } else if (g.nd == 2) {
+                pred = __dsub_rn(__dadd_rn(val(1, 0, 0), val(0, 1, 0)), val(1, 1, 0));
+            } else {
+                pred = __dadd_rn(val(1, 0, 0), val(0, 1, 0));
+                pred = __dadd_rn(pred, val(0, 0, 1));
+                pred = __dsub_rn(pred, val(1, 1, 0));
+                pred = __dsub_rn(pred, val(1, 0, 1));
+                pred = __dsub_rn(pred, val(0, 1, 1));
+                pred = __dadd_rn(pred, val(1, 1, 1));
+            }
+            uint32_t code = code_of_f64(__dsub_rn(q, pred), r);
+            codes[i] = (uint16_t)code;
+            hist_add(h, code);
+        }
+        if (++cnt == 200) {   // 8-bit packed counters: flush well before 255
+            hist_flush(h);
+            cnt = 0;
+        }
+    }
+    hist_flush(h);
+    if (__any_sync(kFull, bad) && lane_id() == 0) atomicOr(&st->flags, (unsigned long long)F_NONFINITE);
+    hist_finish(h);
+}
+
+__global__ void prequantize_kernel(const void* __restrict__ in, int dtype, uint64_t n,
+                                   const DevStatus* st, double* __restrict__ out) {
+    const double two_eb = st->two_eb;
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n;
+         i += (uint64_t)gridDim.x * blockDim.x) {
+        double v = dtype == 0 ? (double)((const float*)in)[i] : ((const double*)in)[i];
+        out[i] = prequant(v, two_eb);
+    }
+}
+
+template <int KIND>
+int launch_kind(sdqz_ctx* ctx, const void* d_in, int ndims, const uint64_t dims[3],
+                const uint32_t block[3], uint32_t cap, uint16_t* d_codes,
+                unsigned long long* d_hist) {
+    size_t smem = (d_hist && cap <= kSmemHistMax) ? cap * sizeof(uint32_t) : 0;
+    if (smem > 48 * 1024) {
+        cudaFuncSetAttribute(dq3d_kernel<KIND>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        cudaFuncSetAttribute(dq2d_kernel<KIND>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        cudaFuncSetAttribute(dq1d_kernel<KIND>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        cudaFuncSetAttribute(dq_generic_kernel<KIND>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    }
+    uint64_t n = dims[0] * dims[1] * dims[2];
+    int max_grid = ctx->num_sms * 8;
+    if (is_fast_shape(ndims, block)) {
+        uint64_t ntask;
+        if (ndims == 3) ntask = ceil_div(ceil_div(dims[2], 8), 4) * ceil_div(dims[1], 8) * ceil_div(dims[0], 8);
+        else if (ndims == 2) ntask = ceil_div(ceil_div(dims[1], 16), 2) * ceil_div(dims[0], 16);
+        else ntask = ceil_div(dims[0], 512);
+        uint64_t grid = ceil_div(ntask, kWarpsPerCta);
+        if (grid > (uint64_t)max_grid) grid = max_grid;
+        if (grid < 1) grid = 1;
+        if (ndims == 3)
+            dq3d_kernel<KIND><<<(unsigned)grid, kThreads, smem, ctx->stream>>>(
+                d_in, dims[0], dims[1], dims[2], cap, ctx->d_status, d_codes, d_hist);
+        else if (ndims == 2)
+            dq2d_kernel<KIND><<<(unsigned)grid, kThreads, smem, ctx->stream>>>(
+                d_in, dims[0], dims[1], cap, ctx->d_status, d_codes, d_hist);
+        else
+            dq1d_kernel<KIND><<<(unsigned)grid, kThreads, smem, ctx->stream>>>(
+                d_in, dims[0], cap, ctx->d_status, d_codes, d_hist);
+    } else {
+        Geo g;
+        g.nd = ndims;
+        for (int a = 0; a < 3; a++) { g.dims[a] = dims[a]; g.block[a] = block[a]; }
+        g.stride[ndims - 1] = 1;
+        for (int a = ndims - 2; a >= 0; a--) g.stride[a] = g.stride[a + 1] * dims[a + 1];
+        uint64_t grid = ceil_div(n, kThreads);
+        if (grid > (uint64_t)max_grid) grid = max_grid;
+        if (grid < 1) grid = 1;
+        dq_generic_kernel<KIND><<<(unsigned)grid, kThreads, smem, ctx->stream>>>(
+            d_in, g, n, cap, ctx->d_status, d_codes, d_hist);
+    }
+    SDQZ_LAUNCHED(ctx);
+    return SDQZ_OK;
+}
+
+}  // namespace
+
+bool is_fast_shape(int ndims, const uint32_t block[3]) {
+    if (ndims == 3) return block[0] == 8 && block[1] == 8 && block[2] == 8;
+    if (ndims == 2) return block[0] == 16 && block[1] == 16;
+    return ndims == 1 && block[0] == 32;
+}
+
+int launch_dualquant(sdqz_ctx* ctx, const void* d_in, int in_kind, int ndims,
+                     const uint64_t dims[3], const uint32_t block[3], uint32_t cap,
+                     uint16_t* d_codes, unsigned long long* d_hist) {
+    switch (in_kind) {
+        case 0: return launch_kind<0>(ctx, d_in, ndims, dims, block, cap, d_codes, d_hist);
+        case 1: return launch_kind<1>(ctx, d_in, ndims, dims, block, cap, d_codes, d_hist);
+        default: return launch_kind<2>(ctx, d_in, ndims, dims, block, cap, d_codes, d_hist);
+    }
+}
+
+int launch_prequantize(sdqz_ctx* ctx, const void* d_in, int dtype, uint64_t n, double* d_out) {
+    uint64_t grid = ceil_div(n, 256);
+    if (grid > (uint64_t)ctx->num_sms * 8) grid = ctx->num_sms * 8;
+    if (grid < 1) grid = 1;
+    prequantize_kernel<<<(unsigned)grid, 256, 0, ctx->stream>>>(d_in, dtype, n, ctx->d_status, d_out);
+    SDQZ_LAUNCHED(ctx);
+    return SDQZ_OK;
+}
+
+}  // namespace sdqz

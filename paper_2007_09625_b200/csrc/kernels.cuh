@@ -1,0 +1,87 @@
+// kernels.cuh -- host-side launchers shared between translation units.
+#pragma once
+#include "common.cuh"
+
+namespace sdqz {
+
+// describe.cu ---------------------------------------------------------------
+// min/max (ordered bits) and nonfinite flag into the status block.
+int launch_describe(sdqz_ctx* ctx, const void* d_in, int dtype, uint64_t n);
+// eb = magnitude (abs) or magnitude*(max-min) (valrel), computed on device
+// from the describe results; sets F_RANGE_ZERO / F_NONFINITE accordingly.
+int launch_resolve(sdqz_ctx* ctx, int dtype, int eb_mode, double magnitude);
+
+// dualquant.cu --------------------------------------------------------------
+// in_kind: 0 f32 data, 1 f64 data, 2 f64 prequantized units.  Reads two_eb from
+// the status block.  d_hist (uint64[cap]) must be zeroed by the caller.
+int launch_dualquant(sdqz_ctx* ctx, const void* d_in, int in_kind, int ndims,
+                     const uint64_t dims[3], const uint32_t block[3], uint32_t cap,
+                     uint16_t* d_codes, unsigned long long* d_hist);
+int launch_prequantize(sdqz_ctx* ctx, const void* d_in, int dtype, uint64_t n, double* d_out);
+
+// huffman.cu ----------------------------------------------------------------
+int launch_histogram_u32(sdqz_ctx* ctx, const uint32_t* codes, uint64_t n, uint32_t cap,
+                         unsigned long long* hist);
+// tree + canonical book from a histogram (uint64[cap]).  bw_only: stop after
+// the bitwidths (build_tree API).  from_bw: skip the tree, canonize d_bw.
+// err_format: report table errors as archive-format errors (deserialize).
+int launch_codebook(sdqz_ctx* ctx, const unsigned long long* d_hist, uint8_t* d_bw, uint32_t cap,
+                    const BookDev& book, bool build_tree, bool canon, bool err_format);
+// decode LUT from reverse tables (first/offsets/symbols, max_bw from status or arg)
+int launch_build_lut(sdqz_ctx* ctx, const uint64_t* first, const int64_t* offsets,
+                     const uint32_t* symbols, int max_bw_or_neg, uint32_t* lut);
+
+// chunked encode/deflate from uint16 codes + packed entries (unit from status).
+// Also compacts outliers (code 0) as interleaved {u64 idx, f64 value} records,
+// recomputing the value from the input (in_kind as in launch_dualquant);
+// d_in may be null when no outlier output is wanted.
+struct DeflateJob {
+    const uint16_t* codes = nullptr;     // source codes (uint16) ...
+    const void* units = nullptr;         // ... or packed units (stage API deflate)
+    int units_width = 0;                 // 32/64 when `units` is used
+    uint64_t n = 0;
+    uint32_t chunk = 0;
+    const uint64_t* entries = nullptr;   // codebook (when codes are used)
+    uint32_t cap = 0;
+    uint32_t* chunk_bits = nullptr;      // [C]
+    uint8_t* payload = nullptr;          // capacity payload_cap
+    uint64_t payload_cap = 0;
+    // outliers
+    const void* in = nullptr;
+    int in_kind = 0;
+    uint64_t in_split = ~0ull;           // indices >= in_split read from `in_tail`
+    const void* in_tail = nullptr;
+    uint64_t idx_base = 0;               // added to every emitted index
+    void* out_records = nullptr;         // {u64, f64}[max]
+    uint64_t out_cap = 0;
+    bool want_payload = true;
+};
+int launch_deflate(sdqz_ctx* ctx, const DeflateJob& job);
+
+int launch_encode_u32(sdqz_ctx* ctx, const uint32_t* codes, uint64_t n, const uint64_t* entries,
+                      uint32_t cap, int unit, void* units);
+
+// inflate into uint16 (or uint32 when out32) codes; counts zero codes.
+int launch_inflate(sdqz_ctx* ctx, const uint8_t* payload, uint64_t payload_bytes,
+                   const uint32_t* chunk_bits, uint64_t n_chunks, uint32_t chunk,
+                   const uint64_t* first, const int64_t* offsets, const uint32_t* symbols,
+                   const uint32_t* lut, int max_bw, uint64_t n, void* codes, bool out32);
+
+// reconstruct.cu ------------------------------------------------------------
+// Validate outlier records (range, order, code==0) and scatter their fp64
+// bits into `dense` (uint64[n]); flag blocks needing the fp64 path.
+int launch_outlier_scatter(sdqz_ctx* ctx, const void* records, const uint64_t* idx,
+                           const double* val, uint64_t k, uint64_t n, const uint16_t* codes,
+                           int ndims, const uint64_t dims[3], const uint32_t block[3],
+                           uint64_t* dense, uint8_t* blockflag, bool check_format);
+int launch_reconstruct(sdqz_ctx* ctx, const uint16_t* codes, const uint64_t* dense,
+                       const uint8_t* blockflag, bool any_slow, int ndims, const uint64_t dims[3],
+                       const uint32_t block[3], uint32_t cap, double two_eb, void* out,
+                       int out_kind);
+
+// helpers
+__host__ __device__ inline uint64_t ceil_div(uint64_t a, uint64_t b) { return (a + b - 1) / b; }
+uint32_t default_chunk_size(uint64_t n);
+bool is_fast_shape(int ndims, const uint32_t block[3]);
+
+}  // namespace sdqz

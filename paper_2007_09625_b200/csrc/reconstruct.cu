@@ -1,0 +1,406 @@
+// reconstruct.cu -- K6: reversed dual-quantization (dualquant.py:197-227,
+// :276-332) as exact integer prefix sums.
+//
+// Within a block the Lorenzo inverse is final = P_x P_y P_z delta', where
+// delta' is the residual field with the (unknown) true residual at each
+// outlier.  Streaming over planes z and rows y with lane = x:
+//     final(z,y,x) = u(x) + K(x),  K = f(z,y-1,x) + f(z-1,y,x) - f(z-1,y-1,x),
+//     u = P_x delta'  (segmented warp scan over the block's 8 / 16 / 32 lanes).
+// An outlier at p carries its final value v, so u(p) = v - K(p); to its right
+// (up to the next outlier) u(x) = S(x) - S(p) + v - K(p) with S = scan of the
+// in-cap residuals.  Each lane therefore takes the correction t = v - K - S of
+// the last outlier at or left of it in its segment (ballot + shuffle): O(1)
+// per point, no per-outlier loop, exact in int64.
+//
+// Outlier values are scattered beforehand into a dense fp64 side array at
+// their flat index (only those slots are ever read: code 0 <=> outlier,
+// validated).  A block whose outlier values are not integers below 2^40 (the
+// int64 path would no longer match fp64 rounding) is flagged and redone by a
+// generic kernel that replays the reference's fp64 operation order exactly
+// (cumsum per axis, then per-outlier box corrections in raster order); the
+// generic kernel also serves non-default block shapes.
+#include "kernels.cuh"
+
+namespace sdqz {
+
+namespace {
+
+constexpr int kThreads = 256;
+constexpr int kWarpsPerCta = kThreads / 32;
+constexpr double kExact = 1099511627776.0;   // 2^40
+
+struct Geo {
+    int nd;
+    uint64_t dims[3];
+    uint32_t block[3];
+    uint64_t stride[3];
+    uint64_t nblk[3];
+};
+
+__device__ __forceinline__ uint64_t block_of(const Geo& g, uint64_t idx) {
+    uint64_t rem = idx, b = 0;
+    for (int a = 0; a < g.nd; a++) {
+        uint64_t c = rem / g.stride[a];
+        rem -= c * g.stride[a];
+        b = b * g.nblk[a] + c / g.block[a];
+    }
+    return b;
+}
+
+__global__ void outlier_scatter_kernel(const unsigned long long* __restrict__ rec,
+                                       const uint64_t* __restrict__ idxs, const double* __restrict__ vals,
+                                       uint64_t k, uint64_t n, const uint16_t* __restrict__ codes, Geo g,
+                                       unsigned long long* __restrict__ dense, uint8_t* blockflag,
+                                       DevStatus* st) {
+    unsigned long long f = 0;
+    for (uint64_t j = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; j < k;
+         j += (uint64_t)gridDim.x * blockDim.x) {
+        uint64_t idx = rec ? rec[2 * j] : idxs[j];
+        unsigned long long vb = rec ? rec[2 * j + 1] : (unsigned long long)__double_as_longlong(vals[j]);
+        if (j > 0) {
+            uint64_t prev = rec ? rec[2 * (j - 1)] : idxs[j - 1];
+            if ((long long)idx - (long long)prev <= 0) f |= F_OUT_ORDER;
+        }
+        if (idx >= n) { f |= F_OUT_RANGE; continue; }
+        if (codes[idx] != 0) f |= F_OUT_NONZERO;
+        dense[idx] = vb;
+        double v = __longlong_as_double((long long)vb);
+        if (!(fabs(v) < kExact && v == floor(v))) {
+            blockflag[block_of(g, idx)] = 1;
+            f |= F_OUT_SLOW;
+        }
+    }
+    if (f) atomicOr(&st->flags, f);
+}
+
+__global__ void count_zero_kernel(const uint16_t* __restrict__ codes, uint64_t n, DevStatus* st) {
+    uint32_t z = 0;
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n;
+         i += (uint64_t)gridDim.x * blockDim.x)
+        z += codes[i] == 0;
+    z = __reduce_add_sync(kFull, z);
+    if (lane_id() == 0 && z) atomicAdd(&st->n_zero, (unsigned long long)z);
+}
+
+__global__ void narrow_codes_kernel(const uint32_t* __restrict__ in, uint64_t n, uint32_t cap,
+                                    uint16_t* __restrict__ out, DevStatus* st) {
+    bool bad = false;
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n;
+         i += (uint64_t)gridDim.x * blockDim.x) {
+        uint32_t c = in[i];
+        if (c >= cap) { bad = true; c = 1; }
+        out[i] = (uint16_t)c;
+    }
+    if (bad) atomicOr(&st->flags, (unsigned long long)F_CODE_RANGE);
+}
+
+template <int OUTK>
+__device__ __forceinline__ void store_out(void* out, uint64_t i, long long fin, double two_eb) {
+    double v = __dmul_rn((double)fin, two_eb);
+    if (OUTK == 0) ((float*)out)[i] = __double2float_rn(v);
+    else ((double*)out)[i] = v;
+}
+
+__device__ __forceinline__ long long outlier_int(const unsigned long long* dense, uint64_t i) {
+    return (long long)__longlong_as_double((long long)dense[i]);
+}
+
+// segmented (width W lanes) inclusive scan + last-outlier correction
+template <int W>
+__device__ __forceinline__ long long row_final(int dlt, bool isout, long long vout, long long K,
+                                               uint32_t lane) {
+    const uint32_t sl = lane & (W - 1);
+    int S = dlt;
+#pragma unroll
+    for (int o = 1; o < W; o <<= 1) {
+        int t = __shfl_up_sync(kFull, S, o);
+        if (sl >= (uint32_t)o) S += t;
+    }
+    long long t = isout ? (vout - K - (long long)S) : 0;
+    uint32_t m = __ballot_sync(kFull, isout);
+    uint32_t segmask = (W == 32) ? kFull : (((1u << W) - 1) << (lane & ~(W - 1)));
+    uint32_t mine = m & segmask & (lane == 31 ? kFull : ((2u << lane) - 1));
+    int src = mine ? 31 - __clz(mine) : (int)lane;
+    long long corr = __shfl_sync(kFull, t, src);
+    if (!mine) corr = 0;
+    return (long long)S + corr + K;
+}
+
+template <int OUTK>
+__global__ void __launch_bounds__(kThreads) rq3d_kernel(const uint16_t* __restrict__ codes,
+                                                        const unsigned long long* __restrict__ dense,
+                                                        const uint8_t* __restrict__ blockflag,
+                                                        int any_slow, uint64_t Z, uint64_t Y,
+                                                        uint64_t X, uint32_t cap, double two_eb,
+                                                        void* __restrict__ out) {
+    const int r = (int)(cap >> 1);
+    const uint32_t lane = lane_id();
+    const uint64_t nbx = ceil_div(X, 8), nbx4 = ceil_div(nbx, 4), nby = ceil_div(Y, 8), nbz = ceil_div(Z, 8);
+    const uint64_t ntask = nbx4 * nby * nbz;
+    const uint64_t YX = Y * X;
+    for (uint64_t task = blockIdx.x * (uint64_t)kWarpsPerCta + (threadIdx.x >> 5); task < ntask;
+         task += (uint64_t)gridDim.x * kWarpsPerCta) {
+        const uint64_t bx4 = task % nbx4, t2 = task / nbx4;
+        const uint64_t by = t2 % nby, bz = t2 / nby;
+        const uint64_t x = bx4 * 32 + lane, y0 = by * 8, z0 = bz * 8;
+        const bool xin = x < X;
+        bool skip = false;
+        if (any_slow && xin) skip = blockflag[(bz * nby + by) * nbx + (x >> 3)] != 0;
+        const int ny = (int)umin(8, Y - y0), nz = (int)umin(8, Z - z0);
+        long long F[8];
+#pragma unroll
+        for (int y = 0; y < 8; y++) F[y] = 0;
+        for (int z = 0; z < nz; z++) {
+            long long R = 0, lag = 0;
+#pragma unroll
+            for (int y = 0; y < 8; y++) {
+                const bool valid = xin && y < ny;
+                const uint64_t i = (z0 + z) * YX + (y0 + y) * X + x;
+                uint32_t code = valid ? codes[i] : (uint32_t)r;
+                const bool isout = valid && code == 0;
+                const int dlt = isout ? 0 : (int)code - r;
+                const long long vout = isout ? outlier_int(dense, i) : 0;
+                const long long K = R + F[y] - (y ? F[y - 1] : 0);
+                const long long fin = row_final<8>(dlt, isout, vout, K, lane);
+                R = fin;
+                if (y) F[y - 1] = lag;
+                lag = fin;
+                if (valid && !skip) store_out<OUTK>(out, i, fin, two_eb);
+            }
+            F[7] = lag;
+        }
+    }
+}
+
+template <int OUTK>
+__global__ void __launch_bounds__(kThreads) rq2d_kernel(const uint16_t* __restrict__ codes,
+                                                        const unsigned long long* __restrict__ dense,
+                                                        const uint8_t* __restrict__ blockflag,
+                                                        int any_slow, uint64_t Y, uint64_t X,
+                                                        uint32_t cap, double two_eb,
+                                                        void* __restrict__ out) {
+    const int r = (int)(cap >> 1);
+    const uint32_t lane = lane_id();
+    const uint64_t nbx = ceil_div(X, 16), nbx2 = ceil_div(nbx, 2), nby = ceil_div(Y, 16);
+    const uint64_t ntask = nbx2 * nby;
+    for (uint64_t task = blockIdx.x * (uint64_t)kWarpsPerCta + (threadIdx.x >> 5); task < ntask;
+         task += (uint64_t)gridDim.x * kWarpsPerCta) {
+        const uint64_t bx2 = task % nbx2, by = task / nbx2;
+        const uint64_t x = bx2 * 32 + lane, y0 = by * 16;
+        const bool xin = x < X;
+        bool skip = false;
+        if (any_slow && xin) skip = blockflag[by * nbx + (x >> 4)] != 0;
+        const int ny = (int)umin(16, Y - y0);
+        long long prev = 0;
+        for (int y = 0; y < ny; y++) {
+            const uint64_t i = (y0 + y) * X + x;
+            uint32_t code = xin ? codes[i] : (uint32_t)r;
+            const bool isout = xin && code == 0;
+            const int dlt = isout ? 0 : (int)code - r;
+            const long long vout = isout ? outlier_int(dense, i) : 0;
+            const long long fin = row_final<16>(dlt, isout, vout, prev, lane);
+            prev = fin;
+            if (xin && !skip) store_out<OUTK>(out, i, fin, two_eb);
+        }
+    }
+}
+
+template <int OUTK>
+__global__ void __launch_bounds__(kThreads) rq1d_kernel(const uint16_t* __restrict__ codes,
+                                                        const unsigned long long* __restrict__ dense,
+                                                        const uint8_t* __restrict__ blockflag,
+                                                        int any_slow, uint64_t X, uint32_t cap,
+                                                        double two_eb, void* __restrict__ out) {
+    const int r = (int)(cap >> 1);
+    const uint32_t lane = lane_id();
+    const uint64_t nb = ceil_div(X, 32);
+    for (uint64_t b = blockIdx.x * (uint64_t)kWarpsPerCta + (threadIdx.x >> 5); b < nb;
+         b += (uint64_t)gridDim.x * kWarpsPerCta) {
+        if (any_slow && blockflag[b]) continue;
+        const uint64_t i = b * 32 + lane;
+        const bool in = i < X;
+        uint32_t code = in ? codes[i] : (uint32_t)r;
+        const bool isout = in && code == 0;
+        const int dlt = isout ? 0 : (int)code - r;
+        const long long vout = isout ? outlier_int(dense, i) : 0;
+        const long long fin = row_final<32>(dlt, isout, vout, 0, lane);
+        if (in) store_out<OUTK>(out, i, fin, two_eb);
+    }
+}
+
+// Reference-order fp64 reconstruction, one thread per block (generic shapes
+// and flagged blocks).  `work` is an fp64 scratch array indexed like the field.
+template <int OUTK>
+__global__ void rq_generic_kernel(const uint16_t* __restrict__ codes,
+                                  const unsigned long long* __restrict__ dense,
+                                  const uint8_t* __restrict__ blockflag, int only_flagged, Geo g,
+                                  uint32_t cap, double two_eb, double* __restrict__ work,
+                                  void* __restrict__ out, const DevStatus* st) {
+    if (only_flagged && !(st->flags & F_OUT_SLOW)) return;
+    const double r = (double)(cap >> 1);
+    const uint64_t nblocks = g.nblk[0] * g.nblk[1] * g.nblk[2];
+    for (uint64_t b = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; b < nblocks;
+         b += (uint64_t)gridDim.x * blockDim.x) {
+        if (only_flagged && !blockflag[b]) continue;
+        uint64_t bc[3] = {0, 0, 0}, rem = b;
+        for (int a = g.nd - 1; a >= 0; a--) { bc[a] = rem % g.nblk[a]; rem /= g.nblk[a]; }
+        uint64_t o[3] = {0, 0, 0}, e[3] = {1, 1, 1};
+        for (int a = 0; a < g.nd; a++) {
+            o[a] = bc[a] * g.block[a];
+            e[a] = umin(g.block[a], g.dims[a] - o[a]);
+        }
+        uint64_t st0 = g.nd > 0 ? g.stride[0] : 1, st1 = g.nd > 1 ? g.stride[1] : 1,
+                 st2 = g.nd > 2 ? g.stride[2] : 1;
+        uint64_t base = o[0] * st0 + (g.nd > 1 ? o[1] * st1 : 0) + (g.nd > 2 ? o[2] * st2 : 0);
+        auto at = [&](uint64_t a, uint64_t bb, uint64_t c) { return base + a * st0 + bb * st1 + c * st2; };
+        // residuals
+        for (uint64_t a = 0; a < e[0]; a++)
+            for (uint64_t bb = 0; bb < e[1]; bb++)
+                for (uint64_t c = 0; c < e[2]; c++) {
+                    uint64_t i = at(a, bb, c);
+                    uint32_t code = codes[i];
+                    work[i] = code == 0 ? 0.0 : __dsub_rn((double)code, r);
+                }
+        // cumsum along block axis 0, then 1, then 2 (dualquant.py:215-217)
+        for (uint64_t bb = 0; bb < e[1]; bb++)
+            for (uint64_t c = 0; c < e[2]; c++)
+                for (uint64_t a = 1; a < e[0]; a++)
+                    work[at(a, bb, c)] = __dadd_rn(work[at(a, bb, c)], work[at(a - 1, bb, c)]);
+        if (g.nd > 1)
+            for (uint64_t a = 0; a < e[0]; a++)
+                for (uint64_t c = 0; c < e[2]; c++)
+                    for (uint64_t bb = 1; bb < e[1]; bb++)
+                        work[at(a, bb, c)] = __dadd_rn(work[at(a, bb, c)], work[at(a, bb - 1, c)]);
+        if (g.nd > 2)
+            for (uint64_t a = 0; a < e[0]; a++)
+                for (uint64_t bb = 0; bb < e[1]; bb++)
+                    for (uint64_t c = 1; c < e[2]; c++)
+                        work[at(a, bb, c)] = __dadd_rn(work[at(a, bb, c)], work[at(a, bb, c - 1)]);
+        // outliers in raster order: acc[box] += v - acc[p]   (dualquant.py:218-226)
+        for (uint64_t a = 0; a < e[0]; a++)
+            for (uint64_t bb = 0; bb < e[1]; bb++)
+                for (uint64_t c = 0; c < e[2]; c++) {
+                    uint64_t i = at(a, bb, c);
+                    if (codes[i] != 0) continue;
+                    double v = __longlong_as_double((long long)dense[i]);
+                    double d = __dsub_rn(v, work[i]);
+                    for (uint64_t a2 = a; a2 < e[0]; a2++)
+                        for (uint64_t b2 = bb; b2 < e[1]; b2++)
+                            for (uint64_t c2 = c; c2 < e[2]; c2++) {
+                                uint64_t j = at(a2, b2, c2);
+                                work[j] = __dadd_rn(work[j], d);
+                            }
+                }
+        for (uint64_t a = 0; a < e[0]; a++)
+            for (uint64_t bb = 0; bb < e[1]; bb++)
+                for (uint64_t c = 0; c < e[2]; c++) {
+                    uint64_t i = at(a, bb, c);
+                    double v = __dmul_rn(work[i], two_eb);
+                    if (OUTK == 0) ((float*)out)[i] = __double2float_rn(v);
+                    else ((double*)out)[i] = v;
+                }
+    }
+}
+
+Geo make_geo(int ndims, const uint64_t dims[3], const uint32_t block[3]) {
+    Geo g{};
+    g.nd = ndims;
+    for (int a = 0; a < 3; a++) {
+        g.dims[a] = a < ndims ? dims[a] : 1;
+        g.block[a] = a < ndims ? block[a] : 1;
+        g.nblk[a] = a < ndims ? ceil_div(dims[a], block[a]) : 1;
+    }
+    g.stride[ndims - 1] = 1;
+    for (int a = ndims - 2; a >= 0; a--) g.stride[a] = g.stride[a + 1] * g.dims[a + 1];
+    for (int a = ndims; a < 3; a++) g.stride[a] = 1;
+    return g;
+}
+
+}  // namespace
+
+int launch_outlier_scatter(sdqz_ctx* ctx, const void* records, const uint64_t* idx,
+                           const double* val, uint64_t k, uint64_t n, const uint16_t* codes,
+                           int ndims, const uint64_t dims[3], const uint32_t block[3],
+                           uint64_t* dense, uint8_t* blockflag, bool check_format) {
+    (void)check_format;
+    if (k == 0) return SDQZ_OK;
+    Geo g = make_geo(ndims, dims, block);
+    uint64_t grid = ceil_div(k, 256);
+    if (grid > (uint64_t)ctx->num_sms * 8) grid = ctx->num_sms * 8;
+    outlier_scatter_kernel<<<(unsigned)grid, 256, 0, ctx->stream>>>(
+        (const unsigned long long*)records, idx, val, k, n, codes, g, (unsigned long long*)dense,
+        blockflag, ctx->d_status);
+    SDQZ_LAUNCHED(ctx);
+    return SDQZ_OK;
+}
+
+int launch_count_zero(sdqz_ctx* ctx, const uint16_t* codes, uint64_t n) {
+    uint64_t grid = ceil_div(n, 256);
+    if (grid > (uint64_t)ctx->num_sms * 8) grid = ctx->num_sms * 8;
+    if (grid < 1) grid = 1;
+    count_zero_kernel<<<(unsigned)grid, 256, 0, ctx->stream>>>(codes, n, ctx->d_status);
+    SDQZ_LAUNCHED(ctx);
+    return SDQZ_OK;
+}
+
+int launch_narrow_codes(sdqz_ctx* ctx, const uint32_t* in, uint64_t n, uint32_t cap, uint16_t* out) {
+    uint64_t grid = ceil_div(n, 256);
+    if (grid > (uint64_t)ctx->num_sms * 8) grid = ctx->num_sms * 8;
+    if (grid < 1) grid = 1;
+    narrow_codes_kernel<<<(unsigned)grid, 256, 0, ctx->stream>>>(in, n, cap, out, ctx->d_status);
+    SDQZ_LAUNCHED(ctx);
+    return SDQZ_OK;
+}
+
+int launch_reconstruct(sdqz_ctx* ctx, const uint16_t* codes, const uint64_t* dense,
+                       const uint8_t* blockflag, bool any_slow, int ndims, const uint64_t dims[3],
+                       const uint32_t block[3], uint32_t cap, double two_eb, void* out,
+                       int out_kind) {
+    int rc = SDQZ_OK;
+    Geo g = make_geo(ndims, dims, block);
+    const unsigned long long* dn = (const unsigned long long*)dense;
+    uint64_t n = g.dims[0] * g.dims[1] * g.dims[2];
+    int max_grid = ctx->num_sms * 8;
+    bool fast = is_fast_shape(ndims, block);
+    if (fast) {
+        uint64_t ntask;
+        if (ndims == 3) ntask = ceil_div(ceil_div(dims[2], 8), 4) * ceil_div(dims[1], 8) * ceil_div(dims[0], 8);
+        else if (ndims == 2) ntask = ceil_div(ceil_div(dims[1], 16), 2) * ceil_div(dims[0], 16);
+        else ntask = ceil_div(dims[0], 32);
+        uint64_t grid = ceil_div(ntask, kWarpsPerCta);
+        if (grid > (uint64_t)max_grid) grid = max_grid;
+        if (grid < 1) grid = 1;
+        int slow = any_slow ? 1 : 0;
+#define RQ_LAUNCH(K)                                                                                 \
+        if (ndims == 3)                                                                              \
+            rq3d_kernel<K><<<(unsigned)grid, kThreads, 0, ctx->stream>>>(codes, dn, blockflag, slow,   \
+                                                                        dims[0], dims[1], dims[2], cap, two_eb, out); \
+        else if (ndims == 2)                                                                         \
+            rq2d_kernel<K><<<(unsigned)grid, kThreads, 0, ctx->stream>>>(codes, dn, blockflag, slow,   \
+                                                                        dims[0], dims[1], cap, two_eb, out); \
+        else                                                                                         \
+            rq1d_kernel<K><<<(unsigned)grid, kThreads, 0, ctx->stream>>>(codes, dn, blockflag, slow,   \
+                                                                        dims[0], cap, two_eb, out);
+        if (out_kind == 0) { RQ_LAUNCH(0) } else { RQ_LAUNCH(1) }
+#undef RQ_LAUNCH
+        SDQZ_LAUNCHED(ctx);
+        if (!any_slow) return SDQZ_OK;
+    }
+    double* work = scratch_as<double>(ctx, S_WORK, n, &rc);
+    if (!work) return rc;
+    uint64_t nblocks = g.nblk[0] * g.nblk[1] * g.nblk[2];
+    uint64_t grid = ceil_div(nblocks, 128);
+    if (grid > (uint64_t)max_grid) grid = max_grid;
+    if (grid < 1) grid = 1;
+    int only = fast ? 1 : 0;
+    if (out_kind == 0)
+        rq_generic_kernel<0><<<(unsigned)grid, 128, 0, ctx->stream>>>(codes, dn, blockflag, only, g, cap,
+                                                                    two_eb, work, out, ctx->d_status);
+    else
+        rq_generic_kernel<1><<<(unsigned)grid, 128, 0, ctx->stream>>>(codes, dn, blockflag, only, g, cap,
+                                                                    two_eb, work, out, ctx->d_status);
+    SDQZ_LAUNCHED(ctx);
+    return SDQZ_OK;
+}
+
+}  // namespace sdqz

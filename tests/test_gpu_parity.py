@@ -1,0 +1,282 @@
+"""GPU parity: every stage of the CUDA path against the reference's golden
+vectors (tests/golden) and the CPU oracle, bit-exact."""
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+if not torch.cuda.is_available():  # pragma: no cover
+    pytest.skip("needs a CUDA device", allow_module_level=True)
+
+import paper_2007_09625_b200 as S  # noqa: E402
+from oracle import sdqz_oracle as O  # noqa: E402
+
+
+def bits(a):
+    a = np.asarray(a)
+    return a.view(np.uint32 if a.dtype == np.float32 else np.uint64)
+
+
+class TestGoldenArchives:
+    def test_compress_bytes(self, golden):
+        for e, c in golden.cases():
+            blob = S.compress(c["data"], **e["kwargs"])
+            assert blob == c["blob"].tobytes(), e["name"]
+
+    def test_decompress_bits(self, golden):
+        for e, c in golden.cases():
+            out = S.decompress(c["blob"].tobytes())
+            assert out.dtype == c["out"].dtype and out.shape == c["out"].shape, e["name"]
+            assert np.array_equal(bits(out), bits(c["out"])), e["name"]
+
+    def test_device_resident_roundtrip(self, golden):
+        for e, c in golden.cases():
+            t = torch.from_numpy(np.ascontiguousarray(c["data"])).cuda()
+            dev = S.compress_device(t, **e["kwargs"])
+            assert dev.to_bytes() == c["blob"].tobytes(), e["name"]
+            out = S.decompress_device(dev).cpu().numpy()
+            assert np.array_equal(bits(out), bits(c["out"])), e["name"]
+
+
+class TestGoldenStages:
+    def test_compress_field(self, golden):
+        for e, c in golden.cases():
+            h = S.parse_header(c["blob"].tobytes())
+            cfg = S.QuantConfig(h.eb_resolved, h.cap, h.block_shape[:h.ndims])
+            fd = S.describe_field(c["data"], c["data"].shape)
+            q = S.compress_field(c["data"], fd, cfg)
+            assert q.codes.dtype == np.uint32
+            assert np.array_equal(q.codes, c["codes"]), e["name"]
+            assert np.array_equal(q.outlier_indices, c["oidx"]), e["name"]
+            assert np.array_equal(bits(q.outlier_values), bits(c["oval"])), e["name"]
+
+    def test_histogram_tree_canonize(self, golden):
+        for e, c in golden.cases():
+            cap = int(c["hist"].size)
+            h = S.histogram(c["codes"], cap)
+            assert h.dtype == np.int64 and np.array_equal(h, c["hist"]), e["name"]
+            bw = S.build_tree(h)
+            assert np.array_equal(bw, c["bw"]), e["name"]
+            cb, rb = S.canonize(bw)
+            assert cb.entries.dtype == c["entries"].dtype, e["name"]
+            assert np.array_equal(cb.entries, c["entries"]), e["name"]
+            ob = O.canonical_book(bw)
+            assert np.array_equal(rb.first_codes, ob.first) and np.array_equal(rb.offsets, ob.offsets)
+            assert np.array_equal(rb.symbols, ob.symbols) and rb.max_bitwidth == ob.max_bw
+
+    def test_encode_deflate_inflate(self, golden):
+        for e, c in golden.cases():
+            p = O.unpack_archive(c["blob"].tobytes())
+            cb, rb = S.canonize(c["bw"])
+            units = S.encode(c["codes"], cb)
+            assert np.array_equal(units, O.encode(c["codes"], O.canonical_book(c["bw"])))
+            ds = S.deflate(units, p.chunk)
+            assert np.array_equal(ds.chunk_bit_lengths, c["chunk_bits"]), e["name"]
+            assert ds.payload == p.payload, e["name"]
+            got = S.inflate(ds, rb, c["codes"].size)
+            assert got.dtype == np.uint32 and np.array_equal(got, c["codes"]), e["name"]
+
+    def test_reconstruct_field(self, golden):
+        for e, c in golden.cases():
+            h = S.parse_header(c["blob"].tobytes())
+            cfg = S.QuantConfig(h.eb_resolved, h.cap, h.block_shape[:h.ndims])
+            q = S.QuantOutput(c["codes"], c["oidx"], c["oval"], h.field_dims, cfg)
+            got = S.reconstruct_field(q)
+            want = O.reconstruct(c["codes"], c["oidx"], c["oval"], h.field_dims, h.eb_resolved,
+                                 h.cap, h.block_shape[:h.ndims])
+            assert np.array_equal(bits(got), bits(want)), e["name"]
+
+    def test_tree_vectors(self, golden):
+        g = golden.npz
+        off = 0
+        for n in g["tree_lens"].tolist():
+            f = g["tree_freq"][off:off + n]
+            assert np.array_equal(S.build_tree(f), g["tree_bw"][off:off + n])
+            off += n
+
+
+class TestKats:
+    """The reference suite's known answers (SURVEY.md §4 KAT table)."""
+
+    def test_prequantize(self):
+        assert S.prequantize(np.array([0.74]), eb=0.25).values[0] == 1.0
+        assert S.prequantize(np.array([-0.75, 0.75]), eb=0.25).values.tolist() == [-2.0, 2.0]
+        assert S.prequantize(np.array([-0.3]), eb=0.1).values.tolist() == [-1.0]
+        with pytest.raises(S.SdqzError, match="nonfinite"):
+            S.prequantize(np.array([1.0, np.inf]), eb=0.1)
+
+    def test_postquantize_block(self):
+        cfg = S.QuantConfig(eb=1.0, cap=16, block_shape=(2, 2))
+        codes, idx, _ = S.postquantize_block(S.pad_block(np.full((2, 2), 3.0)), cfg)
+        assert codes.tolist() == [[11, 8], [8, 8]] and idx.size == 0
+        cfg1 = S.QuantConfig(eb=1.0, cap=16, block_shape=(1,))
+        codes, idx, vals = S.postquantize_block(S.pad_block(np.array([8.0])), cfg1)
+        assert codes.tolist() == [0] and vals.tolist() == [8.0]
+        codes, idx, _ = S.postquantize_block(S.pad_block(np.array([-7.0])), cfg1)
+        assert codes.tolist() == [1] and idx.size == 0
+
+    def test_compress_field_kats(self):
+        d = np.zeros(64)
+        q = S.compress_field(d, S.describe_field(d, [64]), S.QuantConfig.for_rank(0.01, 1))
+        assert np.all(q.codes == 512) and q.n_outliers == 0
+        d = np.array([1.0])
+        q = S.compress_field(d, S.describe_field(d, [1]), S.QuantConfig.for_rank(0.25, 1))
+        assert q.codes.tolist() == [514]
+
+    def test_tree_and_book(self):
+        assert S.build_tree(np.array([5, 2, 1, 1])).tolist() == [1, 2, 3, 3]
+        assert S.build_tree(np.array([0, 9, 0, 0])).tolist() == [0, 1, 0, 0]
+        assert S.build_tree(np.array([1000, 1])).tolist() == [1, 1]
+        with pytest.raises(S.SdqzError, match="all-zero"):
+            S.build_tree(np.zeros(8, dtype=np.int64))
+        cb, rb = S.canonize(np.array([1, 2, 3, 3], dtype=np.uint8))
+        assert cb.codewords.tolist() == [0b0, 0b10, 0b110, 0b111]
+        assert int(cb.entries[2]) == 0x03000006 and cb.unit_width == 32
+        with pytest.raises(S.SdqzError, match="Kraft"):
+            S.canonize(np.array([1, 2, 3], dtype=np.uint8))
+
+    def test_deflate_inflate_kats(self):
+        units = np.array([(3 << 24) | 0b110, (2 << 24) | 0b01], dtype=np.uint32)
+        ds = S.deflate(units, chunk_size=16)
+        assert ds.chunk_bit_lengths.tolist() == [5] and ds.payload == bytes([0b11001000])
+        ds = S.deflate(units, chunk_size=1)
+        assert ds.chunk_bit_lengths.tolist() == [3, 2]
+        assert ds.payload == bytes([0b11000000, 0b01000000])
+        bw = S.build_tree(np.array([5, 2, 1, 1]))
+        cb, rb = S.canonize(bw)
+        ds = S.DeflatedStream(8, np.array([5], dtype=np.uint32), bytes([0b11010000]))
+        assert S.inflate(ds, rb, 2).tolist() == [2, 1]
+
+    def test_fibonacci_units(self):
+        fib = [1, 1]
+        while len(fib) < 30:
+            fib.append(fib[-1] + fib[-2])
+        freq = np.zeros(32, dtype=np.int64)
+        freq[:30] = fib
+        bw = S.build_tree(freq)
+        cb, rb = S.canonize(bw)
+        assert int(bw.max()) == 29 and cb.unit_width == 64 and cb.entries.dtype == np.uint64
+        codes = np.random.default_rng(5).integers(0, 30, 20_000, dtype=np.uint32)
+        ds = S.deflate(S.encode(codes, cb), 256)
+        assert np.array_equal(S.inflate(ds, rb, codes.size), codes)
+
+
+class TestErrors:
+    def test_corruption_messages(self):
+        bw = S.build_tree(np.array([5, 2, 1, 1]))
+        cb, rb = S.canonize(bw)
+        bad = S.DeflatedStream(8, np.array([5], dtype=np.uint32), bytes([0b11001000]))
+        with pytest.raises(S.CorruptionError, match="disagree"):
+            S.inflate(bad, rb, 2)
+        cb1, rb1 = S.canonize(S.build_tree(np.array([42, 0, 0, 0])))
+        ds = S.deflate(S.encode(np.zeros(100, np.uint32), cb1), 7)
+        assert np.array_equal(S.inflate(ds, rb1, 100), np.zeros(100, np.uint32))
+        with pytest.raises(S.CorruptionError, match="no codeword"):
+            S.inflate(S.DeflatedStream(7, ds.chunk_bit_lengths, b"\xff" + ds.payload[1:]), rb1, 100)
+        with pytest.raises(S.CorruptionError, match="outside"):
+            S.histogram(np.array([4]), 4)
+        _, cbz, _ = (None, *S.canonize(S.build_tree(np.array([5, 0, 3, 2, 0, 0, 0, 0]))))
+        with pytest.raises(S.CorruptionError, match="no codebook entry"):
+            S.encode(np.array([1]), cbz)
+
+    def test_reconstruct_validation(self):
+        d = np.full(8, 5.0)
+        cfg = S.QuantConfig.for_rank(0.01, 1)
+        q = S.compress_field(d, S.describe_field(d, [8]), cfg)
+        q.codes[3] = 0
+        with pytest.raises(S.CorruptionError, match="outlier"):
+            S.reconstruct_field(q)
+        q = S.compress_field(d, S.describe_field(d, [8]), cfg)
+        q.outlier_indices = np.array([2], dtype=np.uint64)
+        q.outlier_values = np.array([1.0])
+        with pytest.raises(S.CorruptionError, match="code is not 0"):
+            S.reconstruct_field(q)
+
+    def test_archive_errors_on_device_path(self):
+        blob = S.compress(np.linspace(0, 1, 64).reshape(8, 8), eb=0.01)
+        with pytest.raises(S.ArchiveFormatError, match="short read"):
+            S.decompress(b"")
+        b = bytearray(blob)
+        b[0] = ord("X")
+        with pytest.raises(S.ArchiveFormatError, match="bad magic"):
+            S.decompress(bytes(b))
+        with pytest.raises(S.ArchiveFormatError, match="trailing"):
+            S.decompress(blob + b"\0")
+        with pytest.raises(S.ArchiveFormatError, match="short read"):
+            S.decompress(blob[:-1])
+        h = S.parse_header(blob)
+        table = np.frombuffer(blob[S.HEADER_SIZE:S.HEADER_SIZE + h.cap], np.uint8)
+        b = bytearray(blob)
+        b[S.HEADER_SIZE + int(np.flatnonzero(table)[0])] += 1
+        with pytest.raises(S.ArchiveFormatError, match="Kraft"):
+            S.decompress(bytes(b))
+
+    def test_compress_errors(self):
+        with pytest.raises(S.SdqzError, match="NaN"):
+            S.compress(np.array([0.0, np.nan, 1.0], np.float32), eb=0.1)
+        with pytest.raises(S.SdqzError, match="NaN"):
+            S.compress(np.array([0.0, np.inf, 1.0], np.float32), eb=0.1, mode="valrel")
+        with pytest.raises(S.SdqzError, match="absolute"):
+            S.compress(np.full(16, 3.0, np.float32), eb=0.1, mode="valrel")
+        with pytest.raises(S.SdqzError, match="must be positive"):
+            S.compress(np.arange(16, dtype=np.float32), eb=0.0)
+        with pytest.raises(S.SdqzError, match="cap"):
+            S.compress(np.arange(16, dtype=np.float32), eb=0.1, cap=100)
+        with pytest.raises(S.SdqzError, match="NaN"):
+            S.compress(np.array([np.nan, 1.0], np.float32), eb=0.1, cap=100)
+        with pytest.raises(S.SdqzError, match="mode"):
+            S.compress(np.arange(16, dtype=np.float32), eb=0.1, mode="pointwise")
+
+
+class TestDifferential:
+    """Seeded random fields: GPU archive bytes and decompressed bits == oracle."""
+
+    @pytest.mark.parametrize("seed", range(40))
+    def test_random_fields(self, seed):
+        rng = np.random.default_rng(1000 + seed)
+        rank = int(rng.integers(1, 4))
+        dims = tuple(int(d) for d in rng.integers(1, [4000, 90, 40][rank - 1], rank))
+        kind = seed % 4
+        if kind == 0:
+            data = rng.normal(0, rng.uniform(0.5, 20), dims)
+        elif kind == 1:
+            data = np.cumsum(rng.normal(0, 1, dims), axis=-1)
+        elif kind == 2:
+            data = S.generate_field("smooth", dims, seed=seed)
+        else:
+            data = rng.normal(0, 1e4, dims)
+        data = data.astype(np.float32 if seed % 5 else np.float64)
+        cap = int(rng.choice([4, 16, 64, 256, 1024, 4096, 65536]))
+        block = None if seed % 3 else tuple(int(b) for b in rng.integers(1, 9, rank))
+        mode = "valrel" if seed % 2 else "abs"
+        eb = float(rng.uniform(1e-4, 1e-2)) if mode == "valrel" else float(rng.uniform(1e-3, 0.3))
+        chunk = None if seed % 4 else int(rng.integers(1, 5000))
+        kw = dict(eb=eb, mode=mode, cap=cap, block_shape=block, chunk_size=chunk)
+        blob = S.compress(data, **kw)
+        ref = O.compress(data, **kw)
+        assert blob == ref
+        assert np.array_equal(bits(S.decompress(blob)), bits(O.decompress(ref)))
+
+
+class TestConfigScale:
+    """Config-shaped fields at full size: bytes == oracle (Hurricane) and
+    size-independent properties for the larger configs."""
+
+    def test_hurricane_bit_exact(self):
+        f = S.generate_field("smooth", (100, 500, 500), seed=1).astype(np.float32)
+        blob = S.compress(f, eb=1e-4, mode="valrel")
+        assert blob == O.compress(f, eb=1e-4, mode="valrel")
+        out = S.decompress(blob)
+        h = S.parse_header(blob)
+        err = np.abs(out.astype(np.float64) - f.astype(np.float64))
+        assert err.max() <= h.eb_resolved * (1 + 1e-6) + 2 * np.spacing(np.abs(out).max())
+
+    def test_cesm_roundtrip(self):
+        f = S.generate_field("smooth", (1800, 3600), seed=1).astype(np.float32)
+        blob = S.compress(f, eb=1e-4, mode="valrel")
+        assert blob == O.compress(f, eb=1e-4, mode="valrel")
+        out = S.decompress(blob)
+        h = S.parse_header(blob)
+        assert np.abs(out.astype(np.float64) - f).max() <= h.eb_resolved + 2 * np.spacing(np.float32(8))
