@@ -73,8 +73,14 @@ SDQZ_API int sdqz_ctx_create(int device, void* stream, sdqz_ctx** out);
 SDQZ_API int sdqz_ctx_destroy(sdqz_ctx* ctx);
 SDQZ_API int sdqz_ctx_set_stream(sdqz_ctx* ctx, void* stream);
 SDQZ_API const char* sdqz_last_error(const sdqz_ctx* ctx);
-/* Kernels launched by the most recent call (evidence for the bench). */
+/* Total kernels launched through this context (evidence for the bench). */
 SDQZ_API uint64_t sdqz_kernel_launches(const sdqz_ctx* ctx);
+/* Per-kernel device timer: on=1 resets and starts accumulating CUDA-event
+ * intervals per kernel name on the context's stream; sdqz_kernel_times writes
+ * "name=ms;name=ms;..." (NUL-terminated, truncated to len) and returns the
+ * untruncated length. */
+SDQZ_API int sdqz_set_timing(sdqz_ctx* ctx, int on);
+SDQZ_API int sdqz_kernel_times(sdqz_ctx* ctx, char* buf, uint64_t len);
 
 /* ---- L1: field description (core.py:136-175) ---------------------------- */
 /* min/max in the input dtype (returned widened to double) + nonfinite flag. */

@@ -45,6 +45,8 @@ _SIGS = {
     "sdqz_ctx_set_stream": (c_int, [c_void_p, c_void_p]),
     "sdqz_last_error": (c_char_p, [c_void_p]),
     "sdqz_kernel_launches": (c_uint64, [c_void_p]),
+    "sdqz_set_timing": (c_int, [c_void_p, c_int]),
+    "sdqz_kernel_times": (c_int, [c_void_p, c_char_p, c_uint64]),
     "sdqz_describe": (c_int, [c_void_p, c_void_p, c_int, c_uint64, POINTER(c_double),
                               POINTER(c_double), POINTER(c_int)]),
     "sdqz_prequantize": (c_int, [c_void_p, c_void_p, c_int, c_uint64, c_double, c_void_p]),
@@ -140,6 +142,20 @@ class Context:
             msg = self.lib.sdqz_last_error(self.h).decode(errors="replace")
             raise _exc_for(rc, msg)
         return rc
+
+    def set_timing(self, on: bool) -> None:
+        self.lib.sdqz_set_timing(self.h, 1 if on else 0)
+
+    def kernel_times(self) -> dict:
+        """Accumulated device ms per kernel name since set_timing(True)."""
+        buf = ctypes.create_string_buffer(8192)
+        self.lib.sdqz_kernel_times(self.h, buf, 8192)
+        out = {}
+        for item in buf.value.decode().split(";"):
+            if "=" in item:
+                k, v = item.split("=")
+                out[k] = float(v)
+        return out
 
     @property
     def launches(self) -> int:

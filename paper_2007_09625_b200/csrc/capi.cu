@@ -71,20 +71,51 @@ __global__ void set_eb_kernel(DevStatus* st, double eb) {
 
 int reset_status(sdqz_ctx* ctx) {
     init_status_kernel<<<1, 1, 0, ctx->stream>>>(ctx->d_status);
-    SDQZ_LAUNCHED(ctx);
+    SDQZ_LAUNCHED_NAMED(ctx, "init_status_kernel");
     return SDQZ_OK;
 }
 
 int set_eb(sdqz_ctx* ctx, double eb) {
     set_eb_kernel<<<1, 1, 0, ctx->stream>>>(ctx->d_status, eb);
-    SDQZ_LAUNCHED(ctx);
+    SDQZ_LAUNCHED_NAMED(ctx, "set_eb_kernel");
     return SDQZ_OK;
+}
+
+void kt_mark(sdqz_ctx* ctx, const char* name) {
+    if (ctx->ev_used == ctx->ev_pool.size()) {
+        cudaEvent_t e;
+        if (cudaEventCreate(&e) != cudaSuccess) return;
+        ctx->ev_pool.push_back(e);
+    }
+    size_t i = ctx->ev_used++;
+    cudaEventRecord(ctx->ev_pool[i], ctx->stream);
+    ctx->marks.emplace_back(name, i);
+}
+
+// After a stream sync: attribute the time between consecutive marks to the
+// later mark's kernel, then restart the segment.
+static void kt_flush(sdqz_ctx* ctx) {
+    for (size_t i = 1; i < ctx->marks.size(); i++) {
+        float ms = 0.f;
+        cudaEventElapsedTime(&ms, ctx->ev_pool[ctx->marks[i - 1].second],
+                             ctx->ev_pool[ctx->marks[i].second]);
+        const char* name = ctx->marks[i].first;
+        bool found = false;
+        for (auto& t : ctx->ktotals)
+            if (t.first == name) { t.second += ms; found = true; break; }
+        if (!found) ctx->ktotals.emplace_back(name, (double)ms);
+    }
+    ctx->marks.clear();
+    ctx->ev_used = 0;
+    kt_mark(ctx, "(start)");
 }
 
 int fetch_status(sdqz_ctx* ctx) {
     SDQZ_CUDA(ctx, cudaMemcpyAsync(ctx->h_status, ctx->d_status, sizeof(DevStatus),
                                    cudaMemcpyDeviceToHost, ctx->stream));
+    if (ctx->timing) kt_mark(ctx, "status_readback");
     SDQZ_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
+    if (ctx->timing) kt_flush(ctx);
     return SDQZ_OK;
 }
 
@@ -303,6 +334,31 @@ int sdqz_ctx_set_stream(sdqz_ctx* ctx, void* stream) {
 const char* sdqz_last_error(const sdqz_ctx* ctx) { return ctx ? ctx->err.c_str() : "no context"; }
 
 uint64_t sdqz_kernel_launches(const sdqz_ctx* ctx) { return ctx ? ctx->launches : 0; }
+
+int sdqz_set_timing(sdqz_ctx* ctx, int on) {
+    cudaStreamSynchronize(ctx->stream);
+    ctx->marks.clear();
+    ctx->ev_used = 0;
+    ctx->ktotals.clear();
+    ctx->timing = on != 0;
+    if (ctx->timing) kt_mark(ctx, "(start)");
+    return SDQZ_OK;
+}
+
+int sdqz_kernel_times(sdqz_ctx* ctx, char* buf, uint64_t len) {
+    if (ctx->timing) {
+        cudaStreamSynchronize(ctx->stream);
+        kt_flush(ctx);
+    }
+    std::string s;
+    for (auto& t : ctx->ktotals) s += t.first + "=" + fmt("%.6f", t.second) + ";";
+    if (len) {
+        size_t n = std::min<size_t>(s.size(), len - 1);
+        memcpy(buf, s.data(), n);
+        buf[n] = 0;
+    }
+    return (int)s.size();
+}
 
 // ---------------------------------------------------------------------------
 int sdqz_describe(sdqz_ctx* ctx, const void* d_in, int dtype, uint64_t n, double* vmin,

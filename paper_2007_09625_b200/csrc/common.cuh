@@ -106,9 +106,31 @@ __device__ __forceinline__ double prequant(double v, double two_eb) {
     return copysign(r, x);
 }
 
-template <typename T>
-__device__ __forceinline__ double load_as_double(const T* p, uint64_t i) {
-    return (double)__ldg(p + i);
+// prequant() at a fraction of the FP64 cost, branch-free, for |v / 2eb| < 2^27
+// (the caller checks that bound per warp).  y = v * RN(1/2eb) is within 2.5
+// ulp of RN(v / 2eb); since |y| + 0.5 and its fraction are exact in fp64 here,
+// floor(|y| + 0.5) can differ from the reference only when that fraction is
+// within 2.5 ulp(2^27) < 2^-22 of 0 or 1.  Such a value ORs `amb`, and the
+// caller then redoes the whole task with exact division.
+__device__ __forceinline__ int prequant_int_fast(float v, double rcp, bool& amb) {
+    const double y = __dmul_rn((double)v, rcp);
+    const double t = __dadd_rn(fabs(y), 0.5);
+    const double fl = floor(t);
+    const double fr = __dsub_rn(t, fl);
+    amb |= (fr < 2.384185791015625e-07) | (fr > 1.0 - 2.384185791015625e-07);
+    const int m = (int)fl;
+    return y < 0.0 ? -m : m;
+}
+
+// Warp-collective: the fast path, with the (rare) tie-neighbourhood lanes
+// redone by exact division behind a warp-uniform branch.
+__device__ __forceinline__ int prequant_int(float v, double rcp, double two_eb) {
+    bool amb = false;
+    int d = prequant_int_fast(v, rcp, amb);
+    if (__any_sync(kFull, amb)) {
+        if (amb) d = (int)prequant((double)v, two_eb);
+    }
+    return d;
 }
 
 __device__ __forceinline__ int warp_excl_scan(int v, int* total) {
@@ -149,6 +171,13 @@ struct sdqz_ctx {
     // state of the last fused compress (sections live in scratch buffers)
     sdqz_header last_hdr{};
     bool have_archive = false;
+
+    // optional per-kernel device timer (bench / profiling)
+    bool timing = false;
+    std::vector<cudaEvent_t> ev_pool;
+    size_t ev_used = 0;
+    std::vector<std::pair<const char*, size_t>> marks;   // (name, event index)
+    std::vector<std::pair<std::string, double>> ktotals; // accumulated ms per kernel
 };
 
 namespace sdqz {
@@ -157,7 +186,7 @@ namespace sdqz {
 enum Slot : int {
     S_CODES = 0, S_HIST, S_BW, S_ENTRIES, S_FIRST, S_OFFSETS, S_SYMBOLS, S_LUT,
     S_CHUNK_BITS, S_CHUNK_AUX, S_BYTE_OFF, S_OUT_OFF, S_PAYLOAD, S_OUTREC, S_SORT,
-    S_TREE, S_STAGE, S_DENSE, S_WORK, S_BLOCKFLAG, S_MISC, S_NSLOTS
+    S_TREE, S_STAGE, S_DENSE, S_WORK, S_BLOCKFLAG, S_MISC, S_REDO, S_NSLOTS
 };
 
 int set_error(sdqz_ctx* ctx, int code, const std::string& msg);
@@ -172,11 +201,18 @@ int reset_status(sdqz_ctx* ctx);      // memset status on stream
         if (_e != cudaSuccess) return ::sdqz::cuda_check((ctx), _e, #expr);       \
     } while (0)
 
-#define SDQZ_LAUNCHED(ctx)                                                        \
+// After every kernel launch: count it, surface launch errors, and (when the
+// context's kernel timer is on) record an event named after the kernel.  The
+// time between consecutive marks on the context's single stream is that
+// kernel's device time (host gaps are marked separately at syncs).
+void kt_mark(sdqz_ctx* ctx, const char* name);
+
+#define SDQZ_LAUNCHED_NAMED(ctx, name)                                            \
     do {                                                                          \
         (ctx)->launches++;                                                        \
         cudaError_t _e = cudaGetLastError();                                      \
         if (_e != cudaSuccess) return ::sdqz::cuda_check((ctx), _e, "kernel launch"); \
+        if ((ctx)->timing) ::sdqz::kt_mark((ctx), (name));                        \
     } while (0)
 
 template <typename T>

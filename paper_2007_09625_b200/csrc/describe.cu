@@ -121,13 +121,13 @@ int launch_describe(sdqz_ctx* ctx, const void* d_in, int dtype, uint64_t n) {
         describe_kernel<float><<<grid, 256, 0, ctx->stream>>>((const float*)d_in, n, ctx->d_status);
     else
         describe_kernel<double><<<grid, 256, 0, ctx->stream>>>((const double*)d_in, n, ctx->d_status);
-    SDQZ_LAUNCHED(ctx);
+    SDQZ_LAUNCHED_NAMED(ctx, "describe_kernel");
     return SDQZ_OK;
 }
 
 int launch_resolve(sdqz_ctx* ctx, int dtype, int eb_mode, double magnitude) {
     resolve_kernel<<<1, 1, 0, ctx->stream>>>(ctx->d_status, dtype, eb_mode, magnitude);
-    SDQZ_LAUNCHED(ctx);
+    SDQZ_LAUNCHED_NAMED(ctx, "resolve_kernel");
     return SDQZ_OK;
 }
 

@@ -30,7 +30,6 @@ namespace {
 constexpr int kThreads = 256;
 constexpr int kWarpsPerCta = kThreads / 32;
 constexpr uint32_t kSmemHistMax = 16384;   // caps above this count in global memory
-constexpr double kIntSafe = 134217728.0;   // 2^27
 
 struct HistCtx {
     uint32_t* shist;                 // shared (or null => global)
@@ -130,6 +129,59 @@ __device__ __forceinline__ double to_q(typename Raw<KIND>::T v, double two_eb) {
 
 constexpr double kIntBound = 134217724.0;   // 2^27 - 4
 
+// fp64 task in the reference's term order (dualquant.py:125-129):
+// +(z-1,y,x) +(z,y-1,x) +(z,y,x-1) -(z-1,y-1,x) -(z-1,y,x-1) -(z,y-1,x-1) +(z-1,y-1,x-1).
+// Out of line so its registers do not inflate the int32 fast path; called
+// warp-uniformly, it counts into its own window and flushes before returning.
+template <int KIND>
+__device__ __noinline__ void dq3d_task_f64(const void* __restrict__ in, uint64_t base, uint64_t YX,
+                                           uint64_t X, bool xin, int nz, int ny, uint32_t xl,
+                                           double two_eb, int r, uint16_t* __restrict__ codes,
+                                           HistCtx hc, bool& bad) {
+    using T = typename Raw<KIND>::T;
+    HistCtx h = hc;
+    h.lo = h.hi = 0;
+    double P[8];
+#pragma unroll
+    for (int y = 0; y < 8; y++) P[y] = 0.0;
+    for (int z = 0; z < 8; z++) {
+        double cprev = 0.0, pold = 0.0;
+#pragma unroll
+        for (int y = 0; y < 8; y++) {
+            double q = 0.0;
+            if (xin && z < nz && y < ny) {
+                T v = load_raw<KIND>(in, base + z * YX + y * X);
+                bad |= !isfinite((double)v);
+                q = to_q<KIND>(v, two_eb);
+            }
+            const double pz = P[y];
+            const double pzm = pold;           // P_old[y-1] (0 for y == 0)
+            const double cm = cprev;           // (z, y-1, x)  (0 for y == 0)
+            double n_c = __shfl_up_sync(kFull, q, 1);
+            double n_pz = __shfl_up_sync(kFull, pz, 1);
+            double n_cm = __shfl_up_sync(kFull, cm, 1);
+            double n_pzm = __shfl_up_sync(kFull, pzm, 1);
+            if (!xl) n_c = n_pz = n_cm = n_pzm = 0.0;
+            double pred = __dadd_rn(pz, cm);
+            pred = __dadd_rn(pred, n_c);
+            pred = __dsub_rn(pred, pzm);
+            pred = __dsub_rn(pred, n_pz);
+            pred = __dsub_rn(pred, n_cm);
+            pred = __dadd_rn(pred, n_pzm);
+            const double delta = __dsub_rn(q, pred);
+            pold = pz;
+            P[y] = q;
+            cprev = q;
+            if (xin && z < nz && y < ny) {
+                uint32_t c = code_of_f64(delta, r);
+                codes[base + z * YX + y * X] = (uint16_t)c;
+                hist_add(h, c);
+            }
+        }
+    }
+    hist_flush(h);
+}
+
 // ----------------------------------------------------------------------------
 // 3D, block 8x8x8
 // ----------------------------------------------------------------------------
@@ -143,6 +195,7 @@ __global__ void __launch_bounds__(kThreads, 2) dq3d_kernel(const void* __restric
     HistCtx h;
     hist_init(h, smem_hist, ghist, cap);
     const double two_eb = st->two_eb;
+    const double rcp = __drcp_rn(two_eb);
     const int r = (int)(cap >> 1);
     const uint32_t lane = lane_id(), xl = lane & 7;
     const uint64_t nbx4 = ceil_div(ceil_div(X, 8), 4), nby = ceil_div(Y, 8), nbz = ceil_div(Z, 8);
@@ -173,13 +226,18 @@ __global__ void __launch_bounds__(kThreads, 2) dq3d_kernel(const void* __restric
                 }
             use_int = __all_sync(kFull, !bad && (double)mx / two_eb < kIntBound);
             if (use_int) {
+#pragma unroll
+                for (int z = 0; z < 8; z++)
+#pragma unroll
+                    for (int y = 0; y < 8; y++)
+                        raw[z][y] = __int_as_float(prequant_int(raw[z][y], rcp, two_eb));
                 int hprev[8];
 #pragma unroll
                 for (int z = 0; z < 8; z++) {
                     int gprev = 0;
 #pragma unroll
                     for (int y = 0; y < 8; y++) {
-                        int v = (int)prequant((double)raw[z][y], two_eb);
+                        int v = __float_as_int(raw[z][y]);
                         int left = __shfl_up_sync(kFull, v, 1);
                         int g = v - (xl ? left : 0);
                         int hh = g - gprev;
@@ -195,48 +253,7 @@ __global__ void __launch_bounds__(kThreads, 2) dq3d_kernel(const void* __restric
                 }
             }
         }
-        if (!use_int) {
-            // fp64, reference term order (dualquant.py:125-129):
-            // +(z-1,y,x) +(z,y-1,x) +(z,y,x-1) -(z-1,y-1,x) -(z-1,y,x-1) -(z,y-1,x-1) +(z-1,y-1,x-1)
-            double P[8];
-#pragma unroll
-            for (int y = 0; y < 8; y++) P[y] = 0.0;
-            for (int z = 0; z < 8; z++) {
-                double cprev = 0.0, pold = 0.0;
-#pragma unroll
-                for (int y = 0; y < 8; y++) {
-                    double q = 0.0;
-                    if (xin && z < nz && y < ny) {
-                        T v = load_raw<KIND>(in, base + z * YX + y * X);
-                        bad |= !isfinite((double)v);
-                        q = to_q<KIND>(v, two_eb);
-                    }
-                    const double pz = P[y];
-                    const double pzm = pold;           // P_old[y-1] (0 for y == 0)
-                    const double cm = cprev;           // (z, y-1, x)  (0 for y == 0)
-                    double n_c = __shfl_up_sync(kFull, q, 1);
-                    double n_pz = __shfl_up_sync(kFull, pz, 1);
-                    double n_cm = __shfl_up_sync(kFull, cm, 1);
-                    double n_pzm = __shfl_up_sync(kFull, pzm, 1);
-                    if (!xl) n_c = n_pz = n_cm = n_pzm = 0.0;
-                    double pred = __dadd_rn(pz, cm);
-                    pred = __dadd_rn(pred, n_c);
-                    pred = __dsub_rn(pred, pzm);
-                    pred = __dsub_rn(pred, n_pz);
-                    pred = __dsub_rn(pred, n_cm);
-                    pred = __dadd_rn(pred, n_pzm);
-                    const double delta = __dsub_rn(q, pred);
-                    pold = pz;
-                    P[y] = q;
-                    cprev = q;
-                    if (xin && z < nz && y < ny) {
-                        uint32_t c = code_of_f64(delta, r);
-                        codes[base + z * YX + y * X] = (uint16_t)c;
-                        hist_add(h, c);
-                    }
-                }
-            }
-        }
+        if (!use_int) dq3d_task_f64<KIND>(in, base, YX, X, xin, nz, ny, xl, two_eb, r, codes, h, bad);
         hist_flush(h);
     }
     if (__any_sync(kFull, bad) && lane == 0) atomicOr(&st->flags, (unsigned long long)F_NONFINITE);
@@ -256,6 +273,7 @@ __global__ void __launch_bounds__(kThreads, 2) dq2d_kernel(const void* __restric
     HistCtx h;
     hist_init(h, smem_hist, ghist, cap);
     const double two_eb = st->two_eb;
+    const double rcp = __drcp_rn(two_eb);
     const int r = (int)(cap >> 1);
     const uint32_t lane = lane_id(), xl = lane & 15;
     const uint64_t nbx2 = ceil_div(ceil_div(X, 16), 2), nby = ceil_div(Y, 16);
@@ -282,10 +300,12 @@ __global__ void __launch_bounds__(kThreads, 2) dq2d_kernel(const void* __restric
             }
             use_int = __all_sync(kFull, !bad && (double)mx / two_eb < kIntBound);
             if (use_int) {
+#pragma unroll
+                for (int y = 0; y < 16; y++) raw[y] = __int_as_float(prequant_int(raw[y], rcp, two_eb));
                 int gprev = 0;
 #pragma unroll
                 for (int y = 0; y < 16; y++) {
-                    int v = (int)prequant((double)raw[y], two_eb);
+                    int v = __float_as_int(raw[y]);
                     int left = __shfl_up_sync(kFull, v, 1);
                     int g = v - (xl ? left : 0);
                     int delta = g - gprev;
@@ -341,6 +361,7 @@ __global__ void __launch_bounds__(kThreads, 2) dq1d_kernel(const void* __restric
     HistCtx h;
     hist_init(h, smem_hist, ghist, cap);
     const double two_eb = st->two_eb;
+    const double rcp = __drcp_rn(two_eb);
     const int r = (int)(cap >> 1);
     const uint32_t lane = lane_id();
     const uint64_t ntask = ceil_div(X, 512);
@@ -363,8 +384,10 @@ __global__ void __launch_bounds__(kThreads, 2) dq1d_kernel(const void* __restric
             use_int = __all_sync(kFull, !bad && (double)mx / two_eb < kIntBound);
             if (use_int) {
 #pragma unroll
+                for (int j = 0; j < 16; j++) raw[j] = __int_as_float(prequant_int(raw[j], rcp, two_eb));
+#pragma unroll
                 for (int j = 0; j < 16; j++) {
-                    int v = (int)prequant((double)raw[j], two_eb);
+                    int v = __float_as_int(raw[j]);
                     int left = __shfl_up_sync(kFull, v, 1);
                     int delta = v - (lane ? left : 0);
                     if (base + j * 32 < X) {
@@ -420,6 +443,7 @@ __global__ void __launch_bounds__(kThreads) dq_generic_kernel(const void* __rest
     HistCtx h;
     hist_init(h, smem_hist, ghist, cap);
     const double two_eb = st->two_eb;
+    const double rcp = __drcp_rn(two_eb);
     const int r = (int)(cap >> 1);
     bool bad = false;
     uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
@@ -501,8 +525,10 @@ int launch_kind(sdqz_ctx* ctx, const void* d_in, int ndims, const uint64_t dims[
         if (ndims == 3) ntask = ceil_div(ceil_div(dims[2], 8), 4) * ceil_div(dims[1], 8) * ceil_div(dims[0], 8);
         else if (ndims == 2) ntask = ceil_div(ceil_div(dims[1], 16), 2) * ceil_div(dims[0], 16);
         else ntask = ceil_div(dims[0], 512);
+        // persistent: 2 resident CTAs per SM (__launch_bounds__(256, 2)), each
+        // walking many tasks, so the per-CTA histogram setup/merge amortizes
         uint64_t grid = ceil_div(ntask, kWarpsPerCta);
-        if (grid > (uint64_t)max_grid) grid = max_grid;
+        if (grid > (uint64_t)ctx->num_sms * 2) grid = ctx->num_sms * 2;
         if (grid < 1) grid = 1;
         if (ndims == 3)
             dq3d_kernel<KIND><<<(unsigned)grid, kThreads, smem, ctx->stream>>>(
@@ -525,7 +551,7 @@ int launch_kind(sdqz_ctx* ctx, const void* d_in, int ndims, const uint64_t dims[
         dq_generic_kernel<KIND><<<(unsigned)grid, kThreads, smem, ctx->stream>>>(
             d_in, g, n, cap, ctx->d_status, d_codes, d_hist);
     }
-    SDQZ_LAUNCHED(ctx);
+    SDQZ_LAUNCHED_NAMED(ctx, "dq_generic_kernel");
     return SDQZ_OK;
 }
 
@@ -552,7 +578,7 @@ int launch_prequantize(sdqz_ctx* ctx, const void* d_in, int dtype, uint64_t n, d
     if (grid > (uint64_t)ctx->num_sms * 8) grid = ctx->num_sms * 8;
     if (grid < 1) grid = 1;
     prequantize_kernel<<<(unsigned)grid, 256, 0, ctx->stream>>>(d_in, dtype, n, ctx->d_status, d_out);
-    SDQZ_LAUNCHED(ctx);
+    SDQZ_LAUNCHED_NAMED(ctx, "prequantize_kernel");
     return SDQZ_OK;
 }
 

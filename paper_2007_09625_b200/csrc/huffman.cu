@@ -120,38 +120,45 @@ __global__ void __launch_bounds__(kBookThreads) codebook_kernel(
             __syncthreads();
         } else {
             // ---- two-queue merge (thread 0) --------------------------------
-            unsigned long long* iw = small ? (smem + cap) : gs.iw;
-            uint32_t* im = small ? (uint32_t*)(smem + 2 * cap) : gs.im;
+            // Internal nodes are keyed like leaves, (weight << 16) | min symbol,
+            // so one u64 compare orders both queues exactly as the reference
+            // heap does.  Three-deep register windows over each queue keep the
+            // shared-memory loads off the sequential critical path.
+            unsigned long long* iq = small ? (smem + cap) : gs.iw;
             uint32_t* parent = small ? (uint32_t*)(smem + 2 * cap) + cap : gs.parent;
             if (tid == 0) {
+                constexpr unsigned long long NONE = ~0ull;
                 uint32_t li = 0, ii = 0, ni = 0;
-                unsigned long long lk = keys[0];
+                unsigned long long L0 = keys[0], L1 = keys[1], L2 = n > 2 ? keys[2] : NONE;
+                unsigned long long H0 = NONE, H1 = NONE, H2 = NONE;
                 for (uint32_t k = 0; k + 1 < n; k++) {
-                    unsigned long long w[2];
-                    uint32_t m[2], node[2];
+                    unsigned long long kk[2];
+                    uint32_t node[2];
 #pragma unroll
                     for (int t = 0; t < 2; t++) {
-                        bool take_leaf;
-                        unsigned long long lw = lk >> 16;
-                        uint32_t ls = (uint32_t)(lk & 0xFFFF);
-                        if (ii == ni) take_leaf = true;
-                        else if (li >= n) take_leaf = false;
-                        else {
-                            unsigned long long qw = iw[ii];
-                            uint32_t qm = im[ii];
-                            take_leaf = lw < qw || (lw == qw && ls < qm);
-                        }
-                        if (take_leaf) {
-                            w[t] = lw; m[t] = ls; node[t] = li;
-                            li++;
-                            lk = li < n ? keys[li] : ~0ull;
-                        } else {
-                            w[t] = iw[ii]; m[t] = im[ii]; node[t] = n + ii;
-                            ii++;
-                        }
+                        // branch-free pick; both candidate refills are loaded
+                        // every step
+                        const bool leaf = L0 < H0;
+                        const unsigned long long ln = (li + 3 < n) ? keys[li + 3] : NONE;
+                        const unsigned long long hn = (ii + 3 < ni) ? iq[ii + 3] : NONE;
+                        kk[t] = leaf ? L0 : H0;
+                        node[t] = leaf ? li : n + ii;
+                        L0 = leaf ? L1 : L0;
+                        L1 = leaf ? L2 : L1;
+                        L2 = leaf ? ln : L2;
+                        H0 = leaf ? H0 : H1;
+                        H1 = leaf ? H1 : H2;
+                        H2 = leaf ? H2 : hn;
+                        li += leaf;
+                        ii += !leaf;
                     }
-                    iw[ni] = w[0] + w[1];
-                    im[ni] = min(m[0], m[1]);
+                    const unsigned long long nk =
+                        (((kk[0] >> 16) + (kk[1] >> 16)) << 16) | min(kk[0] & 0xFFFF, kk[1] & 0xFFFF);
+                    iq[ni] = nk;
+                    const uint32_t d = ni - ii;
+                    if (d == 0) H0 = nk;
+                    else if (d == 1) H1 = nk;
+                    else if (d == 2) H2 = nk;
                     ni++;
                     parent[node[0]] = n + k;
                     parent[node[1]] = n + k;
@@ -362,12 +369,48 @@ __device__ __forceinline__ uint32_t unit_of(const DeflateArgs& a) {
     return a.unit ? a.unit : (a.st->max_bw <= 24 ? 32u : 64u);
 }
 
+// Eight consecutive codes per lane: one 16-byte load when the group is
+// aligned and complete, scalar loads otherwise.
+template <int SRC>
+__device__ __forceinline__ void load_group8(const DeflateArgs& a, uint64_t i0, uint64_t e,
+                                            uint32_t codes[8], bool& valid_all) {
+    if (SRC == SRC_CODES && (i0 & 7) == 0 && i0 + 8 <= e) {
+        uint4 v = __ldg(reinterpret_cast<const uint4*>((const uint16_t*)a.src + i0));
+        codes[0] = v.x & 0xFFFF; codes[1] = v.x >> 16;
+        codes[2] = v.y & 0xFFFF; codes[3] = v.y >> 16;
+        codes[4] = v.z & 0xFFFF; codes[5] = v.z >> 16;
+        codes[6] = v.w & 0xFFFF; codes[7] = v.w >> 16;
+        valid_all = true;
+        return;
+    }
+    valid_all = false;
+#pragma unroll
+    for (int k = 0; k < 8; k++) codes[k] = 0;
+}
+
+template <int SRC>
+__device__ __forceinline__ void unit_of_code(const DeflateArgs& a, const unsigned long long* tab,
+                                             uint64_t i, uint32_t code, bool have_code,
+                                             uint32_t unit, uint32_t& w, unsigned long long& cw,
+                                             uint32_t& c_out, bool& bad_range) {
+    if (SRC == SRC_CODES && have_code) {
+        c_out = code;
+        if (code >= a.cap) { bad_range = true; w = 0; cw = 0; return; }
+        if (!tab) { w = 0; cw = 0; return; }
+        unsigned long long u = tab[code];
+        w = (uint32_t)(u >> (unit - 8));
+        cw = u & ((1ull << (unit - 8)) - 1);
+        return;
+    }
+    fetch_unit<SRC>(a.src, tab, i, a.cap, unit, w, cw, c_out, bad_range);
+}
+
 // stats: warp per chunk -> bits, zero codes; flags range / absent-symbol errors
 template <int SRC>
 __global__ void __launch_bounds__(256) chunk_stats_kernel(DeflateArgs a) {
     extern __shared__ unsigned long long stable[];
     const uint32_t unit = unit_of(a);
-    const bool smem_tab = SRC == SRC_CODES && a.cap <= 4096;
+    const bool smem_tab = SRC == SRC_CODES && a.gtable && a.cap <= 4096;
     if (smem_tab)
         for (uint32_t i = threadIdx.x; i < a.cap; i += blockDim.x) stable[i] = a.gtable[i];
     __syncthreads();
@@ -375,15 +418,24 @@ __global__ void __launch_bounds__(256) chunk_stats_kernel(DeflateArgs a) {
     const uint32_t lane = lane_id();
     bool bad_range = false, bad_width = false;
     for (uint64_t c = blockIdx.x * 8ull + (threadIdx.x >> 5); c < a.nchunks; c += gridDim.x * 8ull) {
-        uint64_t s = c * a.chunk, e = umin(s + a.chunk, a.n);
+        const uint64_t s = c * a.chunk, e = umin(s + a.chunk, a.n);
         uint32_t bits = 0, zeros = 0;
-        for (uint64_t i = s + lane; i < e; i += 32) {
-            uint32_t w, code;
-            unsigned long long cw;
-            fetch_unit<SRC>(a.src, tab, i, a.cap, unit, w, cw, code, bad_range);
-            bits += w;
-            zeros += (SRC == SRC_CODES && code == 0);
-            if (w == 0 && (SRC != SRC_CODES || (tab && code < a.cap))) bad_width = true;
+        for (uint64_t g = s; g < e; g += 256) {
+            const uint64_t i0 = g + 8 * lane;
+            uint32_t codes[8];
+            bool vec;
+            load_group8<SRC>(a, i0, e, codes, vec);
+#pragma unroll
+            for (int k = 0; k < 8; k++) {
+                const uint64_t i = i0 + k;
+                if (!vec && i >= e) continue;
+                uint32_t w, code;
+                unsigned long long cw;
+                unit_of_code<SRC>(a, tab, i, codes[k], vec, unit, w, cw, code, bad_range);
+                bits += w;
+                zeros += (SRC == SRC_CODES && code == 0);
+                if (w == 0 && (SRC != SRC_CODES || (tab && code < a.cap))) bad_width = true;
+            }
         }
         bits = __reduce_add_sync(kFull, bits);
         zeros = __reduce_add_sync(kFull, zeros);
@@ -398,39 +450,69 @@ __global__ void __launch_bounds__(256) chunk_stats_kernel(DeflateArgs a) {
     if (f) atomicOr(&a.st->flags, f);
 }
 
-// exclusive scans over chunks (single CTA): byte offsets and outlier offsets
+// Exclusive scans over chunks (single CTA, 1024 threads): byte offsets
+// (ceil(bits/8)) and outlier offsets.  Tiles of 4096 chunks are staged in
+// shared memory with coalesced loads; each thread scans 4 consecutive entries.
 __global__ void __launch_bounds__(1024) chunk_scan_kernel(DeflateArgs a) {
-    __shared__ unsigned long long sb[1024], so[1024];
+    constexpr int kTile = 4096, kPer = kTile / 1024;
+    __shared__ uint32_t sbits[kTile], szero[kTile];
+    __shared__ unsigned long long wsb[32], wso[32];
     const uint64_t C = a.nchunks;
-    const uint64_t per = ceil_div(C, blockDim.x);
-    const uint64_t lo = umin(threadIdx.x * per, C), hi = umin(lo + per, C);
-    unsigned long long tb = 0, to = 0;
-    for (uint64_t c = lo; c < hi; c++) {
-        tb += (a.chunk_bits[c] + 7) >> 3;
-        if (a.chunk_zeros) to += a.chunk_zeros[c];
-    }
-    sb[threadIdx.x] = tb;
-    so[threadIdx.x] = to;
-    __syncthreads();
-    for (uint32_t o = 1; o < blockDim.x; o <<= 1) {
-        unsigned long long xb = threadIdx.x >= o ? sb[threadIdx.x - o] : 0;
-        unsigned long long xo = threadIdx.x >= o ? so[threadIdx.x - o] : 0;
+    const uint32_t tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+    unsigned long long carry_b = 0, carry_o = 0;
+    for (uint64_t t0 = 0; t0 < C; t0 += kTile) {
+        const uint32_t m = (uint32_t)umin(kTile, C - t0);
+        for (uint32_t i = tid; i < m; i += 1024) {
+            sbits[i] = (a.chunk_bits[t0 + i] + 7) >> 3;
+            szero[i] = a.chunk_zeros ? a.chunk_zeros[t0 + i] : 0;
+        }
         __syncthreads();
-        sb[threadIdx.x] += xb;
-        so[threadIdx.x] += xo;
+        unsigned long long tb = 0, to = 0;
+#pragma unroll
+        for (int q = 0; q < kPer; q++) {
+            uint32_t i = tid * kPer + q;
+            if (i < m) { tb += sbits[i]; to += szero[i]; }
+        }
+        // block exclusive scan of (tb, to)
+        unsigned long long xb = tb, xo = to;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            unsigned long long yb = __shfl_up_sync(kFull, xb, o), yo = __shfl_up_sync(kFull, xo, o);
+            if (lane >= (uint32_t)o) { xb += yb; xo += yo; }
+        }
+        if (lane == 31) { wsb[wid] = xb; wso[wid] = xo; }
+        __syncthreads();
+        if (wid == 0) {
+            unsigned long long vb = wsb[lane], vo = wso[lane];
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                unsigned long long yb = __shfl_up_sync(kFull, vb, o), yo = __shfl_up_sync(kFull, vo, o);
+                if (lane >= (uint32_t)o) { vb += yb; vo += yo; }
+            }
+            wsb[lane] = vb;
+            wso[lane] = vo;
+        }
+        __syncthreads();
+        unsigned long long rb = carry_b + (wid ? wsb[wid - 1] : 0) + xb - tb;
+        unsigned long long ro = carry_o + (wid ? wso[wid - 1] : 0) + xo - to;
+#pragma unroll
+        for (int q = 0; q < kPer; q++) {
+            uint32_t i = tid * kPer + q;
+            if (i < m) {
+                a.byte_off[t0 + i] = rb;
+                if (a.out_off) a.out_off[t0 + i] = ro;
+                rb += sbits[i];
+                ro += szero[i];
+            }
+        }
+        carry_b += wsb[31];
+        carry_o += wso[31];
         __syncthreads();
     }
-    unsigned long long rb = sb[threadIdx.x] - tb, ro = so[threadIdx.x] - to;
-    for (uint64_t c = lo; c < hi; c++) {
-        a.byte_off[c] = rb;
-        if (a.out_off) a.out_off[c] = ro;
-        rb += (a.chunk_bits[c] + 7) >> 3;
-        if (a.chunk_zeros) ro += a.chunk_zeros[c];
-    }
-    if (threadIdx.x == blockDim.x - 1) {
-        a.st->payload_bytes = sb[threadIdx.x];
-        a.st->n_outliers = so[threadIdx.x];
-        if (sb[threadIdx.x] > a.payload_cap || (a.records && so[threadIdx.x] > a.out_cap))
+    if (tid == 0) {
+        a.st->payload_bytes = carry_b;
+        a.st->n_outliers = carry_o;
+        if (carry_b > a.payload_cap || (a.records && carry_o > a.out_cap))
             atomicOr(&a.st->flags, (unsigned long long)F_OVERFLOW);
     }
 }
@@ -456,114 +538,126 @@ __device__ __forceinline__ double outlier_value(const DeflateArgs& a, uint64_t i
     return a.in_kind == 2 ? v : prequant(v, two_eb);
 }
 
-// pack: warp per chunk.  Lanes take 4 consecutive codes each and build a
-// <=64-bit left-aligned segment; segments are concatenated by the owner-lane
-// word assembly below (falls back to 1 code per lane when 4 codes overflow).
+// Per-warp bit-stream writer for one chunk.  Each call appends one <=64-bit
+// left-aligned segment per lane, in lane order.  Output word j of the call
+// is assembled by lane j % 32 from the few segments that overlap it: lanes
+// mark the word whose first bit they cover, so the owner starts at the right
+// segment without searching; no atomics, coalesced 32-bit stores.
+struct WarpBitWriter {
+    uint8_t* payload;
+    uint64_t B, Bend;          // chunk byte range
+    uint64_t wbyte;            // global byte address of the current word 0
+    uint32_t carry_bits;       // bits already in carry_word
+    uint32_t carry_word;
+    unsigned long long* seg_s; // [32]
+    uint32_t* off_s;           // [33]
+    uint8_t* first_s;          // [68]
+
+    __device__ __forceinline__ void emit(unsigned long long seg, uint32_t len, uint32_t lane) {
+        int total_l;
+        const uint32_t off = (uint32_t)warp_excl_scan((int)len, &total_l) + carry_bits;
+        const uint32_t total = carry_bits + (uint32_t)total_l;
+        seg_s[lane] = seg;
+        off_s[lane] = off;
+        if (lane == 31) off_s[32] = total;
+        if (len) {
+            uint32_t w = (off + 31) >> 5;                 // first word starting inside [off, off+len)
+            if (32 * w < off + len) first_s[w] = (uint8_t)lane;
+            if (32 * (w + 1) < off + len) first_s[w + 1] = (uint8_t)lane;
+        }
+        __syncwarp();
+        const uint32_t nw = (total + 31) >> 5, full = total >> 5;
+        uint32_t new_carry = 0;
+        for (uint32_t j = lane; j < nw; j += 32) {
+            const uint32_t ws = 32 * j, we = ws + 32;
+            uint32_t word = j ? 0u : carry_word;
+            for (uint32_t i = j ? first_s[j] : 0; i < 32; i++) {
+                const uint32_t o = off_s[i];
+                if (o >= we) break;
+                if (off_s[i + 1] <= ws) continue;
+                const unsigned long long sg = seg_s[i];
+                word |= (o >= ws) ? ((uint32_t)(sg >> 32) >> (o - ws))
+                                  : (uint32_t)((sg << (ws - o)) >> 32);
+            }
+            if (j < full) store_word(payload, wbyte + 4ull * j, word, B, Bend);
+            else new_carry = word;
+        }
+        const uint32_t pc = __shfl_sync(kFull, new_carry, (nw - 1) & 31);
+        __syncwarp();
+        carry_word = (total & 31) ? pc : 0;
+        wbyte += 4ull * full;
+        carry_bits = total & 31;
+    }
+};
+
+// pack: warp per chunk.  Lanes take 8 consecutive codes and build a <=64-bit
+// segment (falling back to one code per lane per call when 8 codes overflow
+// 64 bits); outliers (code 0) are compacted in row-major order.
 template <int SRC, bool PAYLOAD>
 __global__ void __launch_bounds__(256) chunk_pack_kernel(DeflateArgs a) {
     extern __shared__ unsigned long long stable[];
     __shared__ unsigned long long s_seg[8][32];
     __shared__ uint32_t s_off[8][33];
+    __shared__ uint8_t s_first[8][68];
     if (a.st->flags & (F_CODE_RANGE | F_ABSENT_SYM | F_ZERO_WIDTH | F_OVERFLOW | F_BW_TOO_BIG |
                        F_KRAFT | F_NO_PRESENT | F_ALL_ZERO_HIST))
         return;
     const uint32_t unit = unit_of(a);
-    const bool smem_tab = SRC == SRC_CODES && a.cap <= 4096;
+    const bool smem_tab = SRC == SRC_CODES && a.gtable && a.cap <= 4096;
     if (smem_tab)
         for (uint32_t i = threadIdx.x; i < a.cap; i += blockDim.x) stable[i] = a.gtable[i];
     __syncthreads();
     const unsigned long long* tab = smem_tab ? stable : a.gtable;
     const double two_eb = a.st->two_eb;
     const uint32_t lane = lane_id(), wid = threadIdx.x >> 5;
-    unsigned long long* seg_s = s_seg[wid];
-    uint32_t* off_s = s_off[wid];
     bool dummy = false;
 
     for (uint64_t c = blockIdx.x * 8ull + wid; c < a.nchunks; c += gridDim.x * 8ull) {
         const uint64_t s = c * a.chunk, e = umin(s + a.chunk, a.n);
-        const uint64_t B = a.byte_off[c];
-        const uint64_t Bend = B + ((a.chunk_bits[c] + 7) >> 3);
-        uint64_t wbyte = B & ~3ull;                 // global byte of the current word 0
-        uint32_t carry_bits = (uint32_t)(B & 3) * 8;
-        uint32_t carry_word = 0;
+        WarpBitWriter wr;
+        wr.payload = a.payload;
+        wr.B = a.byte_off[c];
+        wr.Bend = wr.B + ((a.chunk_bits[c] + 7) >> 3);
+        wr.wbyte = wr.B & ~3ull;
+        wr.carry_bits = (uint32_t)(wr.B & 3) * 8;
+        wr.carry_word = 0;
+        wr.seg_s = s_seg[wid];
+        wr.off_s = s_off[wid];
+        wr.first_s = s_first[wid];
         uint64_t orec = a.out_off ? a.out_off[c] : 0;
 
-        auto emit = [&](unsigned long long seg, uint32_t len) {
-            // concatenate the 32 lanes' segments onto the stream
-            int total_l;
-            uint32_t off = (uint32_t)warp_excl_scan((int)len, &total_l) + carry_bits;
-            uint32_t total = carry_bits + (uint32_t)total_l;
-            seg_s[lane] = seg;
-            off_s[lane] = off;
-            if (lane == 31) off_s[32] = total;
-            __syncwarp();
-            uint32_t nw = (total + 31) >> 5, full = total >> 5;
-            uint32_t new_carry = 0;
-            for (uint32_t j = lane; j < nw; j += 32) {
-                uint32_t ws = 32 * j, we = ws + 32;
-                uint32_t word = (j == 0) ? carry_word : 0;
-                // first lane whose segment reaches past ws
-                int lo = 0, hi = 31;
-                while (lo < hi) {   // largest i with off[i] <= ws
-                    int mid = (lo + hi + 1) >> 1;
-                    if (off_s[mid] <= ws) lo = mid; else hi = mid - 1;
-                }
-                for (int i = lo; i < 32; i++) {
-                    uint32_t o = off_s[i];
-                    if (o >= we) break;
-                    uint32_t oend = (i < 31) ? off_s[i + 1] : total;
-                    if (oend <= ws) continue;
-                    unsigned long long sg = seg_s[i];
-                    uint32_t piece;
-                    if (o >= ws) piece = (uint32_t)(sg >> 32) >> (o - ws);
-                    else piece = (uint32_t)((sg << (ws - o)) >> 32);
-                    word |= piece;
-                }
-                if (j < full) {
-                    if (PAYLOAD) store_word(a.payload, wbyte + 4ull * j, word, B, Bend);
-                } else {
-                    new_carry = word;
-                }
-            }
-            // broadcast the partial word from its owner
-            uint32_t owner = (nw - 1) & 31;
-            uint32_t pc = __shfl_sync(kFull, new_carry, owner);
-            __syncwarp();
-            if (total & 31) carry_word = pc; else carry_word = 0;
-            wbyte += 4ull * full;
-            carry_bits = total & 31;
-        };
-
-        for (uint64_t g = s; g < e; g += 128) {
-            // lane owns codes g + 4*lane .. +3
+        for (uint64_t g = s; g < e; g += 256) {
+            const uint64_t i0 = g + 8 * lane;
+            uint32_t codes[8];
+            bool vec;
+            load_group8<SRC>(a, i0, e, codes, vec);
             unsigned long long seg = 0;
             uint32_t len = 0, zc = 0;
             bool over = false;
-            uint32_t codes4[4];
+            uint32_t code8[8];
 #pragma unroll
-            for (int k = 0; k < 4; k++) {
-                uint64_t i = g + 4 * lane + k;
-                codes4[k] = 1;
-                if (i < e) {
-                    uint32_t w, code;
-                    unsigned long long cw;
-                    fetch_unit<SRC>(a.src, tab, i, a.cap, unit, w, cw, code, dummy);
-                    codes4[k] = code;
-                    if (SRC == SRC_CODES && code == 0) zc++;
-                    if (len + w <= 64) {
-                        if (w) seg |= cw << (64 - len - w);
-                    } else {
-                        over = true;
-                    }
-                    len += w;
+            for (int k = 0; k < 8; k++) {
+                const uint64_t i = i0 + k;
+                code8[k] = 1;
+                if (!vec && i >= e) continue;
+                uint32_t w, code;
+                unsigned long long cw;
+                unit_of_code<SRC>(a, tab, i, codes[k], vec, unit, w, cw, code, dummy);
+                code8[k] = code;
+                if (SRC == SRC_CODES && code == 0) zc++;
+                if (len + w <= 64) {
+                    if (w) seg |= cw << (64 - len - w);
+                } else {
+                    over = true;
                 }
+                len += w;
             }
             if (PAYLOAD) {
                 if (!__any_sync(kFull, over)) {
-                    emit(seg, len);
+                    wr.emit(seg, len, lane);
                 } else {
-                    for (int k = 0; k < 4; k++) {
-                        uint64_t i = g + 32 * k + lane;
+                    for (int k = 0; k < 8; k++) {
+                        const uint64_t i = g + 32 * k + lane;
                         unsigned long long sg = 0;
                         uint32_t w = 0;
                         if (i < e) {
@@ -572,32 +666,30 @@ __global__ void __launch_bounds__(256) chunk_pack_kernel(DeflateArgs a) {
                             fetch_unit<SRC>(a.src, tab, i, a.cap, unit, w, cw, code, dummy);
                             sg = w ? (cw << (64 - w)) : 0;
                         }
-                        emit(sg, w);
+                        wr.emit(sg, w, lane);
                     }
                 }
             }
             // outliers in row-major order
-            if (SRC == SRC_CODES && a.records) {
+            if (SRC == SRC_CODES && a.records && __any_sync(kFull, zc)) {
                 int ztot;
                 uint32_t zoff = (uint32_t)warp_excl_scan((int)zc, &ztot);
-                if (zc) {
-                    uint64_t slot = orec + zoff;
+                uint64_t slot = orec + zoff;
 #pragma unroll
-                    for (int k = 0; k < 4; k++) {
-                        uint64_t i = g + 4 * lane + k;
-                        if (i < e && codes4[k] == 0) {
-                            double v = outlier_value(a, i, two_eb);
-                            a.records[2 * slot] = i + a.idx_base;
-                            a.records[2 * slot + 1] = (unsigned long long)__double_as_longlong(v);
-                            slot++;
-                        }
+                for (int k = 0; k < 8; k++) {
+                    const uint64_t i = i0 + k;
+                    if (i < e && code8[k] == 0) {
+                        double v = outlier_value(a, i, two_eb);
+                        a.records[2 * slot] = i + a.idx_base;
+                        a.records[2 * slot + 1] = (unsigned long long)__double_as_longlong(v);
+                        slot++;
                     }
                 }
                 orec += (uint64_t)ztot;
             }
         }
-        // flush the final partial word
-        if (PAYLOAD && carry_bits && lane == 0) store_word(a.payload, wbyte, carry_word, B, Bend);
+        if (PAYLOAD && wr.carry_bits && lane == 0)
+            store_word(a.payload, wr.wbyte, wr.carry_word, wr.B, wr.Bend);
         __syncwarp();
     }
 }
@@ -632,48 +724,109 @@ __device__ __forceinline__ uint32_t load_be(const uint32_t* w, uint64_t i, uint6
     return i < nw ? bswap32(__ldg(w + i)) : 0u;   // zeros past the payload (huffman.py:338)
 }
 
+// MSB-first bit reader over the payload with a software-pipelined 16-byte
+// prefetch: the block after the one being consumed is always in flight, so
+// the ~1 us global-load latency is hidden behind ~40 decoded codewords and
+// never stalls the lockstep warp (one lane refilling would stall all 32).
+struct BitReader {
+    const uint4* blk;
+    uint64_t nblk;                 // readable 16 B blocks (payload + zero padding)
+    unsigned long long buf;        // left-aligned valid bits
+    int nb;
+    unsigned long long qhi, qlo;   // queued big-endian words
+    int qw;
+    uint4 nxt;                     // prefetched block
+    uint64_t next_idx;
+
+    __device__ __forceinline__ uint4 load(uint64_t i) const {
+        return i < nblk ? __ldg(blk + i) : make_uint4(0, 0, 0, 0);
+    }
+    __device__ __forceinline__ void take(const uint4& v) {
+        qhi = ((unsigned long long)bswap32(v.x) << 32) | bswap32(v.y);
+        qlo = ((unsigned long long)bswap32(v.z) << 32) | bswap32(v.w);
+        qw = 4;
+    }
+    __device__ __forceinline__ uint32_t pop() {
+        if (qw == 0) {
+            take(nxt);
+            nxt = load(next_idx++);
+        }
+        uint32_t w = (uint32_t)(qhi >> 32);
+        qhi = (qhi << 32) | (qlo >> 32);
+        qlo <<= 32;
+        qw--;
+        return w;
+    }
+    __device__ __forceinline__ void refill() {   // steady state: nb > 0, one pop suffices
+        if (nb <= 32) {
+            buf |= (unsigned long long)pop() << (32 - nb);
+            nb += 32;
+        }
+    }
+    __device__ __forceinline__ void init(uint64_t bit) {
+        uint64_t b = bit >> 7;
+        take(load(b));
+        nxt = load(b + 1);
+        next_idx = b + 2;
+        uint32_t off = (uint32_t)(bit & 127);
+        for (uint32_t s = 0; s < (off >> 5); s++) pop();
+        buf = 0;
+        nb = 0;
+        refill();
+        refill();
+        uint32_t sh = off & 31;
+        buf <<= sh;
+        nb -= (int)sh;
+        refill();
+    }
+    __device__ __forceinline__ void skip(uint32_t len) {
+        buf = len < 64 ? (buf << len) : 0;
+        nb -= (int)len;
+    }
+};
+
 template <bool OUT32>
 __global__ void __launch_bounds__(64) inflate_kernel(
     const uint8_t* __restrict__ payload, uint64_t nwords, const uint32_t* __restrict__ chunk_bits,
     const unsigned long long* __restrict__ byte_off, uint64_t nchunks, uint32_t chunk, uint64_t n,
     const uint64_t* __restrict__ gfirst, const int64_t* __restrict__ goffsets,
     const uint32_t* __restrict__ symbols, const uint32_t* __restrict__ glut, int max_bw_arg,
-    void* out, DevStatus* st) {
+    void* out, DevStatus* st, const uint8_t* __restrict__ only) {
+    // `only` != null: decode just the chunks the warp-parallel decoder handed
+    // back (tiny chunks, corrupt streams -> exact reference error semantics)
+    const uint64_t c = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+    if (only && !__any_sync(kFull, c < nchunks && only[c])) return;
     __shared__ uint32_t lut[1 << kLutBits];
     __shared__ unsigned long long first[58];
     __shared__ long long offs[59];
-    for (uint32_t i = threadIdx.x; i < (1u << kLutBits); i += blockDim.x) lut[i] = glut[i];
-    for (uint32_t i = threadIdx.x; i < 58; i += blockDim.x) first[i] = gfirst[i];
-    for (uint32_t i = threadIdx.x; i < 59; i += blockDim.x) offs[i] = goffsets[i];
-    __syncthreads();
+    for (uint32_t i = lane_id(); i < (1u << kLutBits); i += 32) lut[i] = glut[i];
+    for (uint32_t i = lane_id(); i < 58; i += 32) first[i] = gfirst[i];
+    for (uint32_t i = lane_id(); i < 59; i += 32) offs[i] = goffsets[i];
+    __syncwarp();
     const int mx = max_bw_arg > 0 ? max_bw_arg : (int)st->max_bw;
     if (mx < 1 || mx > kMaxBw) return;
     const int lb = mx < kLutBits ? mx : kLutBits;
     const long long nsym = offs[mx + 1];
-    const uint64_t c = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
     uint32_t zeros = 0;
-    if (c < nchunks) {
+    if (c < nchunks && (!only || only[c])) {
         const uint32_t* words = reinterpret_cast<const uint32_t*>(payload);
         const uint64_t sbit = byte_off[c] * 8;
         const uint32_t budget = chunk_bits[c];
         const uint64_t base = c * chunk;
         const uint64_t cnt = umin(chunk, n - base);
-        uint64_t wi = sbit >> 5;
-        uint32_t sh = (uint32_t)(sbit & 31);
-        unsigned long long buf = (((unsigned long long)load_be(words, wi, nwords) << 32) |
-                                  load_be(words, wi + 1, nwords)) << sh;
-        int nb = 64 - (int)sh;
-        wi += 2;
+        const bool vec = !OUT32 && (base & 7) == 0;
+        uint16_t* out16 = (uint16_t*)out + base;
+        BitReader rd;
+        rd.blk = reinterpret_cast<const uint4*>(payload);
+        rd.nblk = nwords / 4;
+        rd.init(sbit);
         uint32_t pos = 0;
         unsigned long long err = ~0ull;
+        unsigned long long acc0 = 0, acc1 = 0;   // 8 pending uint16 codes
         uint64_t k = 0;
         for (; k < cnt; k++) {
-            if (nb <= 32) {
-                buf |= (unsigned long long)load_be(words, wi, nwords) << (32 - nb);
-                nb += 32;
-                wi++;
-            }
-            uint32_t e = lut[buf >> (64 - lb)];
+            rd.refill();
+            uint32_t e = lut[rd.buf >> (64 - lb)];
             uint32_t len = (e >> 16) & 0xFF;
             uint32_t sym = e & 0xFFFF;
             if (len == 0) {
@@ -681,7 +834,8 @@ __global__ void __launch_bounds__(64) inflate_kernel(
                 uint64_t p = sbit + pos;
                 uint64_t pw = p >> 5;
                 uint32_t ps = (uint32_t)(p & 31);
-                unsigned long long hi64 = ((unsigned long long)load_be(words, pw, nwords) << 32) | load_be(words, pw + 1, nwords);
+                unsigned long long hi64 = ((unsigned long long)load_be(words, pw, nwords) << 32) |
+                                          load_be(words, pw + 1, nwords);
                 uint32_t w2 = load_be(words, pw + 2, nwords);
                 unsigned long long peek64 = ps ? ((hi64 << ps) | (w2 >> (32 - ps))) : hi64;
                 unsigned long long peek = peek64 >> (64 - mx);
@@ -701,19 +855,30 @@ __global__ void __launch_bounds__(64) inflate_kernel(
             }
             if (len == 255) { err = k * 4 + DK_NO_CODEWORD; break; }
             if (pos + len > budget) { err = k * 4 + DK_EXHAUSTED; break; }
-            if (OUT32) ((uint32_t*)out)[base + k] = sym;
-            else ((uint16_t*)out)[base + k] = (uint16_t)sym;
             zeros += (sym == 0);
             pos += len;
-            if (len < 64) buf <<= len; else buf = 0;
-            nb -= (int)len;
-            if (nb < 0) {   // only after a long codeword: resync the window from memory
-                uint64_t p = sbit + pos;
-                wi = p >> 5;
-                sh = (uint32_t)(p & 31);
-                buf = (((unsigned long long)load_be(words, wi, nwords) << 32) | load_be(words, wi + 1, nwords)) << sh;
-                nb = 64 - (int)sh;
-                wi += 2;
+            if (OUT32) {
+                ((uint32_t*)out)[base + k] = sym;
+            } else if (vec) {
+                const uint32_t j = (uint32_t)(k & 7);
+                if (j < 4) acc0 |= (unsigned long long)sym << (16 * j);
+                else acc1 |= (unsigned long long)sym << (16 * (j - 4));
+                if (j == 7) {
+                    *reinterpret_cast<uint4*>(out16 + k - 7) =
+                        make_uint4((uint32_t)acc0, (uint32_t)(acc0 >> 32), (uint32_t)acc1,
+                                   (uint32_t)(acc1 >> 32));
+                    acc0 = acc1 = 0;
+                }
+            } else {
+                out16[k] = (uint16_t)sym;
+            }
+            if ((int)len <= rd.nb) rd.skip(len);
+            else rd.init(sbit + pos);   // a codeword longer than the window: resync
+        }
+        if (vec && err == ~0ull) {
+            for (uint64_t j = k & ~7ull; j < k; j++) {
+                uint32_t t = (uint32_t)(j & 7);
+                out16[j] = (uint16_t)((t < 4 ? acc0 >> (16 * t) : acc1 >> (16 * (t - 4))) & 0xFFFF);
             }
         }
         if (err == ~0ull && pos != budget) err = (0x3fffffffffffffffull << 2) | DK_DISAGREE;
@@ -723,6 +888,236 @@ __global__ void __launch_bounds__(64) inflate_kernel(
     if (lane_id() == 0 && zeros) atomicAdd(&st->n_zero, (unsigned long long)zeros);
 }
 
+// --------------------------------------------------------------------------
+// K5': warp-parallel inflate of one chunk (self-synchronising decode).
+//
+// The archive fixes ~1e4-6e4 chunks (huffman.py:206-212), too few threads for
+// a thread-per-chunk decoder.  Here a warp splits chunk c's bit range into L
+// lane slices.  Phase 1: each lane decodes from its slice start (usually
+// mid-codeword) to the first codeword boundary at/after the next slice start
+// (its exit), remembering which bit offsets within 64 bits of its start were
+// codeword boundaries.  Phase 2: lane 0 started at a true boundary; lane l is
+// synchronised when lane l-1's exit is one of its recorded boundaries (from
+// there on both decodes coincide, so lane l's exit is a true boundary too).
+// Unsynchronised lanes redo from their predecessor's exit until the whole
+// warp is consistent.  Phase 3: a prefix sum of per-lane symbol counts gives
+// output offsets and every lane decodes its true span again, storing codes.
+// Anything unusual (short chunks, invalid bit patterns, count or length
+// mismatch) hands the chunk to the sequential decoder, which reproduces the
+// reference's exact error semantics.
+// --------------------------------------------------------------------------
+struct DecodeTables {
+    const uint32_t* lut;                 // shared
+    const unsigned long long* first;     // shared
+    const long long* offs;               // shared
+    const uint32_t* symbols;
+    const uint32_t* words;
+    uint64_t nwords;
+    long long nsym;
+    int lb, mx;
+};
+
+__device__ __noinline__ uint32_t long_codeword(const DecodeTables& d, uint64_t p, uint32_t& sym) {
+    const uint64_t pw = p >> 5;
+    const uint32_t ps = (uint32_t)(p & 31);
+    const unsigned long long hi64 = ((unsigned long long)load_be(d.words, pw, d.nwords) << 32) |
+                                    load_be(d.words, pw + 1, d.nwords);
+    const uint32_t w2 = load_be(d.words, pw + 2, d.nwords);
+    const unsigned long long peek64 = ps ? ((hi64 << ps) | (w2 >> (32 - ps))) : hi64;
+    const unsigned long long peek = peek64 >> (64 - d.mx);
+    for (int b = d.lb + 1; b <= d.mx; b++) {
+        const unsigned long long top = peek >> (d.mx - b);
+        const unsigned long long cntb = (unsigned long long)(d.offs[b + 1] - d.offs[b]);
+        if (top < d.first[b] + cntb) {
+            long long idx = d.offs[b] + (long long)(top - d.first[b]);
+            if (idx < 0) idx = 0;
+            if (idx >= d.nsym) idx = d.nsym ? d.nsym - 1 : 0;
+            sym = d.symbols[idx];
+            return (uint32_t)b;
+        }
+    }
+    return 255;
+}
+
+// one codeword at absolute bit `p` (the reader's position); 255 = invalid
+__device__ __forceinline__ uint32_t decode_one(const DecodeTables& d, BitReader& rd, uint64_t p,
+                                               uint32_t& sym) {
+    rd.refill();
+    const uint32_t e = d.lut[rd.buf >> (64 - d.lb)];
+    uint32_t len = (e >> 16) & 0xFF;
+    sym = e & 0xFFFF;
+    if (len == 0) len = long_codeword(d, p, sym);
+    if (len != 255) {
+        if ((int)len <= rd.nb) rd.skip(len);
+        else rd.init(p + len);
+    }
+    return len;
+}
+
+// decode from `start` (relative) until the position reaches `stop`; records
+// boundaries within [start, start + 64) in `mask`; returns false on an invalid pattern
+__device__ __forceinline__ bool decode_span(const DecodeTables& d, uint64_t sbit, uint32_t start,
+                                            uint32_t stop, uint32_t& exit_pos, uint32_t& count,
+                                            unsigned long long& mask) {
+    BitReader rd;
+    rd.blk = reinterpret_cast<const uint4*>(d.words);
+    rd.nblk = d.nwords / 4;
+    rd.init(sbit + start);
+    uint32_t pos = start, k = 0;
+    unsigned long long m = 0;
+    bool ok = true;
+    while (pos < stop) {
+        const uint32_t rel = pos - start;
+        if (rel < 64) m |= 1ull << rel;
+        uint32_t sym;
+        const uint32_t len = decode_one(d, rd, sbit + pos, sym);
+        if (len == 255) { ok = false; break; }
+        pos += len;
+        k++;
+    }
+    exit_pos = pos;
+    count = k;
+    mask = m;
+    return ok;
+}
+
+constexpr uint32_t kMinSliceBits = 128;
+
+__global__ void __launch_bounds__(256) inflate_warp_kernel(
+    const uint8_t* __restrict__ payload, uint64_t nwords, const uint32_t* __restrict__ chunk_bits,
+    const unsigned long long* __restrict__ byte_off, uint64_t nchunks, uint32_t chunk, uint64_t n,
+    const uint64_t* __restrict__ gfirst, const int64_t* __restrict__ goffsets,
+    const uint32_t* __restrict__ symbols, const uint32_t* __restrict__ glut, int max_bw_arg,
+    uint16_t* __restrict__ out, uint8_t* __restrict__ redo, DevStatus* st) {
+    __shared__ uint32_t lut[1 << kLutBits];
+    __shared__ unsigned long long first[58];
+    __shared__ long long offs[59];
+    for (uint32_t i = threadIdx.x; i < (1u << kLutBits); i += blockDim.x) lut[i] = glut[i];
+    for (uint32_t i = threadIdx.x; i < 58; i += blockDim.x) first[i] = gfirst[i];
+    for (uint32_t i = threadIdx.x; i < 59; i += blockDim.x) offs[i] = goffsets[i];
+    __syncthreads();
+    const int mx = max_bw_arg > 0 ? max_bw_arg : (int)st->max_bw;
+    if (mx < 1 || mx > kMaxBw) return;
+    DecodeTables d;
+    d.lut = lut;
+    d.first = first;
+    d.offs = offs;
+    d.symbols = symbols;
+    d.words = reinterpret_cast<const uint32_t*>(payload);
+    d.nwords = nwords;
+    d.nsym = offs[mx + 1];
+    d.mx = mx;
+    d.lb = mx < kLutBits ? mx : kLutBits;
+    const uint32_t lane = lane_id();
+    uint32_t zeros_total = 0;
+
+    for (uint64_t c = blockIdx.x * 8ull + (threadIdx.x >> 5); c < nchunks; c += gridDim.x * 8ull) {
+        const uint32_t B = chunk_bits[c];
+        const uint64_t sbit = byte_off[c] * 8;
+        const uint64_t base = c * chunk;
+        const uint32_t cnt = (uint32_t)umin(chunk, n - base);
+        uint32_t L = B / kMinSliceBits;
+        if (L > 32) L = 32;
+        if (L < 2 || (base & 7)) {
+            if (lane == 0) redo[c] = 1;
+            continue;
+        }
+        const bool active = lane < L;
+        uint32_t s = active ? (uint32_t)(((uint64_t)lane * B) / L) : B;
+        const uint32_t s_next = active ? (uint32_t)(((uint64_t)(lane + 1) * B) / L) : B;
+        uint32_t e = B, k = 0;
+        unsigned long long mask = 1;
+        bool ok = true;
+        if (active) ok = decode_span(d, sbit, s, s_next, e, k, mask);
+        // phase 2: propagate synchronisation from lane 0
+        bool good = false;
+        uint32_t cstart = 0;
+        for (int round = 0; round <= 32; round++) {
+            const uint32_t pe = __shfl_up_sync(kFull, e, 1);
+            const bool pok = __shfl_up_sync(kFull, ok, 1);
+            cstart = lane ? pe : 0;
+            bool sync = true;
+            if (active) {
+                if (lane == 0) sync = ok;
+                else sync = ok && pok && cstart >= s && cstart - s < 64 && ((mask >> (cstart - s)) & 1);
+            }
+            if (__all_sync(kFull, sync)) { good = true; break; }
+            // redo from the predecessor's exit; a lane whose predecessor is
+            // itself invalid waits for a later round
+            if (active && !sync && pok && cstart < s_next) {
+                s = cstart;
+                ok = decode_span(d, sbit, s, s_next, e, k, mask);
+            }
+        }
+        const uint32_t last_e = __shfl_sync(kFull, e, L - 1);
+        uint32_t nsym_l = 0;
+        if (active) {
+            const uint32_t rel = cstart - s;   // < 64 when synchronised
+            nsym_l = k - (rel ? __popcll(mask & ((1ull << rel) - 1)) : 0);
+        }
+        int total;
+        const uint32_t o = (uint32_t)warp_excl_scan((int)nsym_l, &total);
+        if (!good || last_e != B || (uint32_t)total != cnt) {
+            if (lane == 0) redo[c] = 1;
+            continue;
+        }
+        // phase 3: decode the true span [cstart, e) and store nsym_l codes at o
+        bool ok3 = true;
+        uint32_t zeros = 0;
+        if (active && nsym_l) {
+            BitReader rd;
+            rd.blk = reinterpret_cast<const uint4*>(payload);
+            rd.nblk = nwords / 4;
+            rd.init(sbit + cstart);
+            uint32_t pos = cstart;
+            uint16_t* dst = out + base + o;
+            uint32_t j = 0;
+            // scalar head up to 8-code alignment
+            const uint32_t head = umin((8 - ((base + o) & 7)) & 7, nsym_l);
+            for (; j < head; j++) {
+                uint32_t sym;
+                const uint32_t len = decode_one(d, rd, sbit + pos, sym);
+                if (len == 255) { ok3 = false; break; }
+                pos += len;
+                dst[j] = (uint16_t)sym;
+                zeros += sym == 0;
+            }
+            unsigned long long acc0 = 0, acc1 = 0;
+            for (; ok3 && j + 8 <= nsym_l; j += 8) {
+#pragma unroll
+                for (int t = 0; t < 8; t++) {
+                    uint32_t sym;
+                    const uint32_t len = decode_one(d, rd, sbit + pos, sym);
+                    ok3 &= len != 255;
+                    pos += len;
+                    zeros += sym == 0;
+                    if (t < 4) acc0 |= (unsigned long long)sym << (16 * t);
+                    else acc1 |= (unsigned long long)sym << (16 * (t - 4));
+                }
+                *reinterpret_cast<uint4*>(dst + j) = make_uint4((uint32_t)acc0, (uint32_t)(acc0 >> 32),
+                                                                (uint32_t)acc1, (uint32_t)(acc1 >> 32));
+                acc0 = acc1 = 0;
+            }
+            for (; ok3 && j < nsym_l; j++) {
+                uint32_t sym;
+                const uint32_t len = decode_one(d, rd, sbit + pos, sym);
+                if (len == 255) { ok3 = false; break; }
+                pos += len;
+                dst[j] = (uint16_t)sym;
+                zeros += sym == 0;
+            }
+            ok3 &= pos == e;
+        }
+        if (!__all_sync(kFull, ok3)) {
+            if (lane == 0) redo[c] = 1;
+            continue;
+        }
+        zeros_total += zeros;
+    }
+    zeros_total = __reduce_add_sync(kFull, zeros_total);
+    if (lane == 0 && zeros_total) atomicAdd(&st->n_zero, (unsigned long long)zeros_total);
+}
+
 template <int SRC>
 int run_deflate(sdqz_ctx* ctx, DeflateArgs& a, bool payload) {
     size_t smem = (SRC == SRC_CODES && a.cap <= 4096) ? a.cap * 8 : 0;
@@ -730,14 +1125,14 @@ int run_deflate(sdqz_ctx* ctx, DeflateArgs& a, bool payload) {
     if (grid > (uint64_t)ctx->num_sms * 16) grid = ctx->num_sms * 16;
     if (grid < 1) grid = 1;
     chunk_stats_kernel<SRC><<<(unsigned)grid, 256, smem, ctx->stream>>>(a);
-    SDQZ_LAUNCHED(ctx);
+    SDQZ_LAUNCHED_NAMED(ctx, "chunk_stats_kernel");
     chunk_scan_kernel<<<1, 1024, 0, ctx->stream>>>(a);
-    SDQZ_LAUNCHED(ctx);
+    SDQZ_LAUNCHED_NAMED(ctx, "chunk_scan_kernel");
     if (payload)
         chunk_pack_kernel<SRC, true><<<(unsigned)grid, 256, smem, ctx->stream>>>(a);
     else
         chunk_pack_kernel<SRC, false><<<(unsigned)grid, 256, smem, ctx->stream>>>(a);
-    SDQZ_LAUNCHED(ctx);
+    SDQZ_LAUNCHED_NAMED(ctx, "chunk_pack_kernel");
     return SDQZ_OK;
 }
 
@@ -752,7 +1147,7 @@ int launch_histogram_u32(sdqz_ctx* ctx, const uint32_t* codes, uint64_t n, uint3
     if (grid > (uint64_t)ctx->num_sms * 4) grid = ctx->num_sms * 4;
     if (grid < 1) grid = 1;
     hist_u32_kernel<<<(unsigned)grid, 256, smem, ctx->stream>>>(codes, n, cap, hist, ctx->d_status);
-    SDQZ_LAUNCHED(ctx);
+    SDQZ_LAUNCHED_NAMED(ctx, "hist_u32_kernel");
     return SDQZ_OK;
 }
 
@@ -780,14 +1175,14 @@ int launch_codebook(sdqz_ctx* ctx, const unsigned long long* d_hist, uint8_t* d_
         cudaFuncSetAttribute(codebook_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     codebook_kernel<<<1, kBookThreads, smem, ctx->stream>>>(d_hist, d_bw, cap, book, ctx->d_status,
                                                            build_tree ? 1 : 0, canon ? 1 : 0, gs);
-    SDQZ_LAUNCHED(ctx);
+    SDQZ_LAUNCHED_NAMED(ctx, "codebook_kernel");
     return SDQZ_OK;
 }
 
 int launch_build_lut(sdqz_ctx* ctx, const uint64_t* first, const int64_t* offsets,
                      const uint32_t* symbols, int max_bw_or_neg, uint32_t* lut) {
     lut_kernel<<<16, 256, 0, ctx->stream>>>(first, offsets, symbols, max_bw_or_neg, ctx->d_status, lut);
-    SDQZ_LAUNCHED(ctx);
+    SDQZ_LAUNCHED_NAMED(ctx, "lut_kernel");
     return SDQZ_OK;
 }
 
@@ -837,7 +1232,7 @@ int launch_encode_u32(sdqz_ctx* ctx, const uint32_t* codes, uint64_t n, const ui
     if (grid < 1) grid = 1;
     encode_kernel<<<(unsigned)grid, 256, 0, ctx->stream>>>(codes, n, (const unsigned long long*)entries,
                                                           cap, unit, units, ctx->d_status);
-    SDQZ_LAUNCHED(ctx);
+    SDQZ_LAUNCHED_NAMED(ctx, "encode_kernel");
     return SDQZ_OK;
 }
 
@@ -861,17 +1256,29 @@ int launch_inflate(sdqz_ctx* ctx, const uint8_t* payload, uint64_t payload_bytes
     a.byte_off = scratch_as<unsigned long long>(ctx, S_BYTE_OFF, n_chunks, &rc);
     if (!a.byte_off) return rc;
     chunk_scan_kernel<<<1, 1024, 0, ctx->stream>>>(a);
-    SDQZ_LAUNCHED(ctx);
+    SDQZ_LAUNCHED_NAMED(ctx, "chunk_scan_kernel");
     uint64_t grid = ceil_div(n_chunks, 64);
-    if (out32)
+    if (out32) {
         inflate_kernel<true><<<(unsigned)grid, 64, 0, ctx->stream>>>(
             payload, nwords, chunk_bits, a.byte_off, n_chunks, chunk, n, first, offsets, symbols, lut,
-            max_bw, codes, ctx->d_status);
-    else
-        inflate_kernel<false><<<(unsigned)grid, 64, 0, ctx->stream>>>(
-            payload, nwords, chunk_bits, a.byte_off, n_chunks, chunk, n, first, offsets, symbols, lut,
-            max_bw, codes, ctx->d_status);
-    SDQZ_LAUNCHED(ctx);
+            max_bw, codes, ctx->d_status, nullptr);
+        SDQZ_LAUNCHED_NAMED(ctx, "inflate_kernel");
+        return SDQZ_OK;
+    }
+    // warp-parallel decode; chunks it hands back are redone sequentially
+    uint8_t* redo = scratch_as<uint8_t>(ctx, S_REDO, n_chunks, &rc);
+    if (!redo) return rc;
+    SDQZ_CUDA(ctx, cudaMemsetAsync(redo, 0, n_chunks, ctx->stream));
+    uint64_t wgrid = ceil_div(n_chunks, 8);
+    if (wgrid > (uint64_t)ctx->num_sms * 8) wgrid = ctx->num_sms * 8;
+    inflate_warp_kernel<<<(unsigned)wgrid, 256, 0, ctx->stream>>>(
+        payload, nwords, chunk_bits, a.byte_off, n_chunks, chunk, n, first, offsets, symbols, lut,
+        max_bw, (uint16_t*)codes, redo, ctx->d_status);
+    SDQZ_LAUNCHED_NAMED(ctx, "inflate_warp_kernel");
+    inflate_kernel<false><<<(unsigned)grid, 64, 0, ctx->stream>>>(
+        payload, nwords, chunk_bits, a.byte_off, n_chunks, chunk, n, first, offsets, symbols, lut,
+        max_bw, codes, ctx->d_status, redo);
+    SDQZ_LAUNCHED_NAMED(ctx, "inflate_kernel");
     return SDQZ_OK;
 }
 

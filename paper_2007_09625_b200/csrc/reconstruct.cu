@@ -330,7 +330,7 @@ int launch_outlier_scatter(sdqz_ctx* ctx, const void* records, const uint64_t* i
     outlier_scatter_kernel<<<(unsigned)grid, 256, 0, ctx->stream>>>(
         (const unsigned long long*)records, idx, val, k, n, codes, g, (unsigned long long*)dense,
         blockflag, ctx->d_status);
-    SDQZ_LAUNCHED(ctx);
+    SDQZ_LAUNCHED_NAMED(ctx, "outlier_scatter_kernel");
     return SDQZ_OK;
 }
 
@@ -339,7 +339,7 @@ int launch_count_zero(sdqz_ctx* ctx, const uint16_t* codes, uint64_t n) {
     if (grid > (uint64_t)ctx->num_sms * 8) grid = ctx->num_sms * 8;
     if (grid < 1) grid = 1;
     count_zero_kernel<<<(unsigned)grid, 256, 0, ctx->stream>>>(codes, n, ctx->d_status);
-    SDQZ_LAUNCHED(ctx);
+    SDQZ_LAUNCHED_NAMED(ctx, "count_zero_kernel");
     return SDQZ_OK;
 }
 
@@ -348,7 +348,7 @@ int launch_narrow_codes(sdqz_ctx* ctx, const uint32_t* in, uint64_t n, uint32_t 
     if (grid > (uint64_t)ctx->num_sms * 8) grid = ctx->num_sms * 8;
     if (grid < 1) grid = 1;
     narrow_codes_kernel<<<(unsigned)grid, 256, 0, ctx->stream>>>(in, n, cap, out, ctx->d_status);
-    SDQZ_LAUNCHED(ctx);
+    SDQZ_LAUNCHED_NAMED(ctx, "narrow_codes_kernel");
     return SDQZ_OK;
 }
 
@@ -383,7 +383,7 @@ int launch_reconstruct(sdqz_ctx* ctx, const uint16_t* codes, const uint64_t* den
                                                                         dims[0], cap, two_eb, out);
         if (out_kind == 0) { RQ_LAUNCH(0) } else { RQ_LAUNCH(1) }
 #undef RQ_LAUNCH
-        SDQZ_LAUNCHED(ctx);
+        SDQZ_LAUNCHED_NAMED(ctx, "rq_fast");
         if (!any_slow) return SDQZ_OK;
     }
     double* work = scratch_as<double>(ctx, S_WORK, n, &rc);
@@ -399,7 +399,7 @@ int launch_reconstruct(sdqz_ctx* ctx, const uint16_t* codes, const uint64_t* den
     else
         rq_generic_kernel<1><<<(unsigned)grid, 128, 0, ctx->stream>>>(codes, dn, blockflag, only, g, cap,
                                                                     two_eb, work, out, ctx->d_status);
-    SDQZ_LAUNCHED(ctx);
+    SDQZ_LAUNCHED_NAMED(ctx, "rq_generic_kernel");
     return SDQZ_OK;
 }
 

@@ -224,8 +224,9 @@ def inflate(ds: DeflatedStream, rb: ReverseCodebook, n_codes: int,
     syms = np.asarray(rb.symbols, dtype=np.uint32)
     dsym = _device.upload(np.concatenate([syms, np.zeros(1, np.uint32)]).view(np.int32))
     out = _device.empty(n_codes, torch.int32)
+    dfirst = _device.upload(first.view(np.int64))   # keep references alive across the call
+    doffs = _device.upload(offs)
     _lib.context().call("sdqz_inflate", _lib.ptr(dpay), len(ds.payload), _lib.ptr(dbits), n_chunks,
-                        int(ds.chunk_size), _lib.ptr(_device.upload(first.view(np.int64))),
-                        _lib.ptr(_device.upload(offs)), _lib.ptr(dsym), int(rb.max_bitwidth),
-                        int(n_codes), _lib.ptr(out))
+                        int(ds.chunk_size), _lib.ptr(dfirst), _lib.ptr(doffs), _lib.ptr(dsym),
+                        int(rb.max_bitwidth), int(n_codes), _lib.ptr(out))
     return _device.download(out, n_codes).view(np.uint32).astype(CODE_DTYPE)

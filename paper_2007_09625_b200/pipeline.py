@@ -231,3 +231,41 @@ def decompress_archive(ar: Archive, workers: int | None = None) -> np.ndarray:
 
 __all__ = ["compress", "decompress", "decompress_archive", "compress_device",
            "decompress_device", "DeviceArchive", "DEFAULT_BLOCK_SHAPES"]
+
+
+class CompressPlan:
+    """Pre-validated compress of one device-resident field: `run()` is a single
+    C-ABI call (no per-call Python validation) -- used by the bench's
+    device-level figure and by repeated compression of a resident field."""
+
+    def __init__(self, t, dims, *, eb, mode="abs", cap=1024, block_shape=None, chunk_size=None):
+        dims, block, pending = _check_request(t, dims, eb, mode, cap, block_shape, chunk_size)
+        if pending is not None:
+            raise pending
+        self.t, dt = _device.to_device(t)
+        self.ctx = _lib.context()
+        self.args = (_lib.ptr(self.t), 0 if dt == np.float32 else 1, len(dims), _lib.dims3(dims),
+                     _lib.block3(block), 0 if mode == "abs" else 1, float(eb), int(cap),
+                     int(chunk_size or 0))
+        self.hdr = _lib.Header()
+
+    def run(self) -> DeviceArchive:
+        self.ctx.call("sdqz_compress", *self.args, ctypes.byref(self.hdr))
+        return DeviceArchive(self.hdr, self.ctx)
+
+
+class DecompressPlan:
+    """Device-resident decompress of the context's last archive into a
+    preallocated output tensor (single C-ABI call per run)."""
+
+    def __init__(self, dev: DeviceArchive):
+        self.dev = dev
+        self.out = _out_tensor(dev.header)
+
+    def run(self):
+        ctx, h = self.dev.ctx, self.dev.header
+        bw, rec, cb, pay = (ctypes.c_void_p() for _ in range(4))
+        ctx.call("sdqz_archive_sections", ctypes.byref(bw), ctypes.byref(rec), ctypes.byref(cb),
+                 ctypes.byref(pay))
+        ctx.call("sdqz_decompress_sections", ctypes.byref(h), bw, rec, cb, pay, _lib.ptr(self.out))
+        return self.out
