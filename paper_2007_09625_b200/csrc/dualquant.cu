@@ -22,6 +22,7 @@
 // codes outside that window use shared-memory atomics; each CTA merges its
 // shared histogram into the global uint64 histogram once.
 #include "kernels.cuh"
+#include "tma.cuh"
 
 namespace sdqz {
 
@@ -255,6 +256,108 @@ __global__ void __launch_bounds__(kThreads, 2) dq3d_kernel(const void* __restric
         }
         if (!use_int) dq3d_task_f64<KIND>(in, base, YX, X, xin, nz, ny, xl, two_eb, r, codes, h, bad);
         hist_flush(h);
+    }
+    if (__any_sync(kFull, bad) && lane == 0) atomicOr(&st->flags, (unsigned long long)F_NONFINITE);
+    hist_finish(h);
+}
+
+// ----------------------------------------------------------------------------
+// 3D, block 8x8x8, fp32 input staged by TMA.  A CTA is 4 warps; each warp
+// streams its own tasks through a 2-stage shared-memory ring: the tile of
+// task t+1 (32 x 8 x 8 floats, OOB zero-filled by the TMA unit) is in flight
+// while task t is computed from shared memory, so the field is read once at
+// full bandwidth with no per-element address arithmetic or registers held
+// for loads.
+// ----------------------------------------------------------------------------
+constexpr int kTmaWarps = 4;
+constexpr uint32_t kTile3 = 32 * 8 * 8;          // floats per 3D task tile
+
+__global__ void __launch_bounds__(kTmaWarps * 32) dq3d_tma_kernel(
+    const __grid_constant__ CUtensorMap tmap, const float* __restrict__ in, uint64_t Z, uint64_t Y,
+    uint64_t X, uint32_t cap, DevStatus* st, uint16_t* __restrict__ codes,
+    unsigned long long* ghist) {
+    extern __shared__ __align__(128) unsigned char dsm[];
+    float* tiles = reinterpret_cast<float*>(dsm);                              // [warp][2][kTile3]
+    uint64_t* bars = reinterpret_cast<uint64_t*>(dsm + kTmaWarps * 2 * kTile3 * 4);
+    uint32_t* shist_base = reinterpret_cast<uint32_t*>(bars + kTmaWarps * 2);
+    HistCtx h;
+    hist_init(h, shist_base, ghist, cap);
+    const double two_eb = st->two_eb;
+    const double rcp = __drcp_rn(two_eb);
+    const int r = (int)(cap >> 1);
+    const uint32_t lane = lane_id(), wid = threadIdx.x >> 5, xl = lane & 7;
+    const uint64_t nbx4 = ceil_div(ceil_div(X, 8), 4), nby = ceil_div(Y, 8), nbz = ceil_div(Z, 8);
+    const uint64_t ntask = nbx4 * nby * nbz;
+    const uint64_t YX = Y * X;
+    float* mytiles = tiles + (size_t)wid * 2 * kTile3;
+    uint64_t* mybar = bars + wid * 2;
+    if (lane == 0) {
+        mbar_init(&mybar[0], 1);
+        mbar_init(&mybar[1], 1);
+        fence_mbar_init();
+    }
+    __syncwarp();
+    auto issue = [&](uint64_t task, int stage) {
+        const uint64_t bx4 = task % nbx4, t2 = task / nbx4;
+        const uint64_t by = t2 % nby, bz = t2 / nby;
+        mbar_expect_tx(&mybar[stage], kTile3 * 4);
+        tma_load_3d(mytiles + stage * kTile3, &tmap, (int)(bx4 * 32), (int)(by * 8), (int)(bz * 8),
+                    &mybar[stage]);
+    };
+    const uint64_t stride = (uint64_t)gridDim.x * kTmaWarps;
+    uint64_t task = blockIdx.x * (uint64_t)kTmaWarps + wid;
+    if (lane == 0 && task < ntask) issue(task, 0);
+    uint32_t phase0 = 0, phase1 = 0;
+    bool bad = false;
+    for (int it = 0; task < ntask; task += stride, it++) {
+        const int stage = it & 1;
+        if (lane == 0 && task + stride < ntask) issue(task + stride, stage ^ 1);
+        if (stage == 0) { mbar_wait(&mybar[0], phase0); phase0 ^= 1; }
+        else { mbar_wait(&mybar[1], phase1); phase1 ^= 1; }
+        const float* tile = mytiles + stage * kTile3;
+        const uint64_t bx4 = task % nbx4, t2 = task / nbx4;
+        const uint64_t by = t2 % nby, bz = t2 / nby;
+        const uint64_t x = bx4 * 32 + lane, y0 = by * 8, z0 = bz * 8;
+        const bool xin = x < X;
+        const int ny = (int)umin(8, Y - y0), nz = (int)umin(8, Z - z0);
+        const uint64_t base = z0 * YX + y0 * X + x;
+        float mx = 0.f;
+        bool tbad = false;
+#pragma unroll 16
+        for (int k = 0; k < 64; k++) {
+            const float v = tile[k * 32 + lane];
+            mx = fmaxf(mx, fabsf(v));
+            tbad |= !isfinite(v);
+        }
+        bad |= tbad;
+        const bool use_int = __all_sync(kFull, !tbad && (double)mx / two_eb < kIntBound);
+        if (use_int) {
+            int hprev[8];
+#pragma unroll
+            for (int z = 0; z < 8; z++) {
+                int gprev = 0;
+                uint16_t* crow = codes + base + z * YX;
+#pragma unroll
+                for (int y = 0; y < 8; y++) {
+                    const int v = prequant_int(tile[(z * 8 + y) * 32 + lane], rcp, two_eb);
+                    const int left = __shfl_up_sync(kFull, v, 1);
+                    const int g = v - (xl ? left : 0);
+                    const int hh = g - gprev;
+                    gprev = g;
+                    const int delta = hh - (z ? hprev[y] : 0);
+                    hprev[y] = hh;
+                    const uint32_t c = code_of_int(delta, r);
+                    if (xin && z < nz && y < ny) {
+                        crow[y * X] = (uint16_t)c;
+                        hist_add(h, c);
+                    }
+                }
+            }
+        } else {
+            dq3d_task_f64<0>(in, base, YX, X, xin, nz, ny, xl, two_eb, r, codes, h, bad);
+        }
+        hist_flush(h);
+        __syncwarp();   // every lane is done with this stage before it is refilled
     }
     if (__any_sync(kFull, bad) && lane == 0) atomicOr(&st->flags, (unsigned long long)F_NONFINITE);
     hist_finish(h);
@@ -520,6 +623,35 @@ int launch_kind(sdqz_ctx* ctx, const void* d_in, int ndims, const uint64_t dims[
     }
     uint64_t n = dims[0] * dims[1] * dims[2];
     int max_grid = ctx->num_sms * 8;
+    // TMA-fed 3D path: fp32, 16-byte aligned base and row pitch, extents TMA can address
+    if (KIND == 0 && ndims == 3 && is_fast_shape(ndims, block) && dims[2] % 4 == 0 &&
+        ((uintptr_t)d_in & 15) == 0 && dims[2] < (1ull << 31) && dims[1] < (1ull << 31) &&
+        dims[0] < (1ull << 31) && !env_disabled("SDQZ_NO_TMA")) {
+        CUtensorMap map;
+        const uint64_t gd[3] = {dims[2], dims[1], dims[0]};
+        const uint64_t gs[2] = {dims[2] * 4, dims[2] * dims[1] * 4};
+        const uint32_t box[3] = {32, 8, 8};
+        if (make_tensor_map(&map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, d_in, gd, gs, box)) {
+            const size_t tsm = kTmaWarps * 2 * kTile3 * 4 + kTmaWarps * 2 * 8 + smem;
+            static bool attr_done = false;
+            if (!attr_done) {
+                cudaFuncSetAttribute(dq3d_tma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     64 * 1024 + 16 * 4096 + 64);
+                attr_done = true;
+            }
+            const uint64_t ntask =
+                ceil_div(ceil_div(dims[2], 8), 4) * ceil_div(dims[1], 8) * ceil_div(dims[0], 8);
+            int per_sm = 1;
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, dq3d_tma_kernel, kTmaWarps * 32, tsm);
+            if (per_sm < 1) per_sm = 1;
+            uint64_t grid = ceil_div(ntask, kTmaWarps);
+            if (grid > (uint64_t)ctx->num_sms * per_sm) grid = (uint64_t)ctx->num_sms * per_sm;
+            dq3d_tma_kernel<<<(unsigned)grid, kTmaWarps * 32, tsm, ctx->stream>>>(
+                map, (const float*)d_in, dims[0], dims[1], dims[2], cap, ctx->d_status, d_codes, d_hist);
+            SDQZ_LAUNCHED_NAMED(ctx, "dq3d_tma_kernel");
+            return SDQZ_OK;
+        }
+    }
     if (is_fast_shape(ndims, block)) {
         uint64_t ntask;
         if (ndims == 3) ntask = ceil_div(ceil_div(dims[2], 8), 4) * ceil_div(dims[1], 8) * ceil_div(dims[0], 8);
@@ -556,6 +688,40 @@ int launch_kind(sdqz_ctx* ctx, const void* d_in, int ndims, const uint64_t dims[
 }
 
 }  // namespace
+
+bool env_disabled(const char* name) {
+    const char* v = getenv(name);
+    return v && v[0] && v[0] != '0';
+}
+
+bool make_tensor_map(CUtensorMap* map, CUtensorMapDataType dtype, uint32_t rank, const void* base,
+                     const uint64_t* dims, const uint64_t* strides_bytes, const uint32_t* box) {
+    static PFN_cuTensorMapEncodeTiled_v12000 encode = nullptr;
+    static bool tried = false;
+    if (!tried) {
+        tried = true;
+        void* fn = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            encode = (PFN_cuTensorMapEncodeTiled_v12000)fn;
+        else
+            cudaGetLastError();
+    }
+    if (!encode) return false;
+    cuuint64_t gd[5], gs[4];
+    cuuint32_t bx[5], es[5];
+    for (uint32_t i = 0; i < rank; i++) {
+        gd[i] = dims[i];
+        bx[i] = box[i];
+        es[i] = 1;
+        if (i + 1 < rank) gs[i] = strides_bytes[i];
+    }
+    CUresult r = encode(map, dtype, rank, const_cast<void*>(base), gd, gs, bx, es,
+                        CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                        CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    return r == CUDA_SUCCESS;
+}
 
 bool is_fast_shape(int ndims, const uint32_t block[3]) {
     if (ndims == 3) return block[0] == 8 && block[1] == 8 && block[2] == 8;

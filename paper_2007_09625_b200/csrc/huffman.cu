@@ -87,11 +87,14 @@ struct TreeScratch {       // global scratch for caps above the smem limit
     uint32_t* jmp;              // [2*cap] x2
 };
 
+template <bool SMALL>
 __global__ void __launch_bounds__(kBookThreads) codebook_kernel(
     const unsigned long long* __restrict__ hist, uint8_t* __restrict__ bw, uint32_t cap,
     BookDev book, DevStatus* st, int build_tree, int canon, TreeScratch gs) {
     extern __shared__ unsigned long long smem[];
-    const bool small = cap <= kSmemSortMax;
+    // SMALL (cap <= 4096): every table lives in shared memory; the template
+    // keeps the pointers in the shared address space (no generic accesses)
+    constexpr bool small = SMALL;
     unsigned long long* keys = small ? smem : gs.keys;
     __shared__ uint32_t s_n, s_max, s_cnt[64], s_err;
     __shared__ unsigned long long s_first[64];
@@ -406,20 +409,40 @@ __device__ __forceinline__ void unit_of_code(const DeflateArgs& a, const unsigne
 }
 
 // stats: warp per chunk -> bits, zero codes; flags range / absent-symbol errors
-template <int SRC>
+// TS: the codebook (cap <= 4096) is staged in shared memory; as a template
+// parameter it keeps table reads in the shared address space.
+template <int SRC, bool TS>
 __global__ void __launch_bounds__(256) chunk_stats_kernel(DeflateArgs a) {
     extern __shared__ unsigned long long stable[];
     const uint32_t unit = unit_of(a);
-    const bool smem_tab = SRC == SRC_CODES && a.gtable && a.cap <= 4096;
-    if (smem_tab)
+    if (TS)
         for (uint32_t i = threadIdx.x; i < a.cap; i += blockDim.x) stable[i] = a.gtable[i];
     __syncthreads();
-    const unsigned long long* tab = smem_tab ? stable : a.gtable;
+    const unsigned long long* tab = TS ? stable : a.gtable;
     const uint32_t lane = lane_id();
     bool bad_range = false, bad_width = false;
     for (uint64_t c = blockIdx.x * 8ull + (threadIdx.x >> 5); c < a.nchunks; c += gridDim.x * 8ull) {
         const uint64_t s = c * a.chunk, e = umin(s + a.chunk, a.n);
         uint32_t bits = 0, zeros = 0;
+        if (SRC == SRC_CODES && ((s | e) & 7) == 0) {
+            // aligned chunk: 16-byte loads of 8 codes, branch-free accumulation
+            const uint16_t* src = (const uint16_t*)a.src;
+            const uint32_t wshift = unit - 8;
+            for (uint64_t i0 = s + 8 * lane; i0 < e; i0 += 256) {
+                const uint4 v = __ldg(reinterpret_cast<const uint4*>(src + i0));
+                const uint32_t wv[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+                for (int k = 0; k < 8; k++) {
+                    const uint32_t code = (wv[k >> 1] >> (16 * (k & 1))) & 0xFFFF;
+                    const bool inr = code < a.cap;
+                    const unsigned long long u = (inr && tab) ? tab[code] : 0ull;
+                    bad_range |= !inr;
+                    bad_width |= tab && inr && u == 0;
+                    bits += (uint32_t)(u >> wshift);
+                    zeros += code == 0;
+                }
+            }
+        } else
         for (uint64_t g = s; g < e; g += 256) {
             const uint64_t i0 = g + 8 * lane;
             uint32_t codes[8];
@@ -593,7 +616,7 @@ struct WarpBitWriter {
 // pack: warp per chunk.  Lanes take 8 consecutive codes and build a <=64-bit
 // segment (falling back to one code per lane per call when 8 codes overflow
 // 64 bits); outliers (code 0) are compacted in row-major order.
-template <int SRC, bool PAYLOAD>
+template <int SRC, bool PAYLOAD, bool TS>
 __global__ void __launch_bounds__(256) chunk_pack_kernel(DeflateArgs a) {
     extern __shared__ unsigned long long stable[];
     __shared__ unsigned long long s_seg[8][32];
@@ -603,11 +626,10 @@ __global__ void __launch_bounds__(256) chunk_pack_kernel(DeflateArgs a) {
                        F_KRAFT | F_NO_PRESENT | F_ALL_ZERO_HIST))
         return;
     const uint32_t unit = unit_of(a);
-    const bool smem_tab = SRC == SRC_CODES && a.gtable && a.cap <= 4096;
-    if (smem_tab)
+    if (TS)
         for (uint32_t i = threadIdx.x; i < a.cap; i += blockDim.x) stable[i] = a.gtable[i];
     __syncthreads();
-    const unsigned long long* tab = smem_tab ? stable : a.gtable;
+    const unsigned long long* tab = TS ? stable : a.gtable;
     const double two_eb = a.st->two_eb;
     const uint32_t lane = lane_id(), wid = threadIdx.x >> 5;
     bool dummy = false;
@@ -690,6 +712,154 @@ __global__ void __launch_bounds__(256) chunk_pack_kernel(DeflateArgs a) {
         }
         if (PAYLOAD && wr.carry_bits && lane == 0)
             store_word(a.payload, wr.wbyte, wr.carry_word, wr.B, wr.Bend);
+        __syncwarp();
+    }
+}
+
+// --------------------------------------------------------------------------
+// pack (fused path, uint16 codes): warp per chunk, rounds of 32 x kRun codes.
+// Lane l owns the run of kRun consecutive codes [g + kRun*l, +kRun): pass A
+// looks the codewords up (shared table) and sums their widths; one warp scan
+// gives each run its bit offset; pass B streams the run MSB-first through a
+// 64-bit accumulator into a per-warp shared word buffer.  Words strictly
+// inside a run have a single writer (plain store); a run's first and last
+// words are shared with its neighbours and merged with atomicOr (two per run,
+// i.e. per 16 codes).  Completed words go to global memory coalesced; the
+// trailing partial word carries into the next round.
+// --------------------------------------------------------------------------
+constexpr int kRun = 16;
+constexpr int kRoundCodes = 32 * kRun;
+constexpr int kBufWords = kRoundCodes * kMaxBw / 32 + 4;   // worst case 56 bits per code
+
+template <bool TS>
+__global__ void __launch_bounds__(256) chunk_pack_run_kernel(DeflateArgs a, int want_payload) {
+    extern __shared__ unsigned long long stable[];
+    __shared__ uint32_t s_buf[8][kBufWords];
+    if (a.st->flags & (F_CODE_RANGE | F_ABSENT_SYM | F_ZERO_WIDTH | F_OVERFLOW | F_BW_TOO_BIG |
+                       F_KRAFT | F_NO_PRESENT | F_ALL_ZERO_HIST))
+        return;
+    const uint32_t unit = unit_of(a);
+    const uint32_t wshift = unit - 8;
+    const unsigned long long cwmask = (1ull << wshift) - 1;
+    if (TS)
+        for (uint32_t i = threadIdx.x; i < a.cap; i += blockDim.x) stable[i] = a.gtable[i];
+    __syncthreads();
+    const unsigned long long* tab = TS ? stable : a.gtable;
+    const double two_eb = a.st->two_eb;
+    const uint32_t lane = lane_id(), wid = threadIdx.x >> 5;
+    uint32_t* buf = s_buf[wid];
+    const uint16_t* src = (const uint16_t*)a.src;
+    const bool payload = want_payload != 0 && a.gtable != nullptr;
+
+    for (uint64_t c = blockIdx.x * 8ull + wid; c < a.nchunks; c += gridDim.x * 8ull) {
+        const uint64_t s = c * a.chunk, e = umin(s + a.chunk, a.n);
+        const uint64_t B = a.byte_off[c];
+        const uint64_t Bend = B + ((a.chunk_bits[c] + 7) >> 3);
+        uint64_t wbyte = B & ~3ull;
+        uint32_t carry = (uint32_t)(B & 3) * 8;
+        uint64_t orec = a.out_off ? a.out_off[c] : 0;
+        for (uint32_t i = lane; i < kBufWords; i += 32) buf[i] = 0;
+        __syncwarp();
+        for (uint64_t g = s; g < e; g += kRoundCodes) {
+            const uint64_t i0 = g + (uint64_t)kRun * lane;
+            const uint32_t cnt = i0 < e ? (uint32_t)umin(kRun, e - i0) : 0;
+            // pass A: codes, widths, zero count
+            uint32_t code[kRun];
+            if (cnt == kRun && (i0 & 7) == 0) {
+                const uint4 v0 = __ldg(reinterpret_cast<const uint4*>(src + i0));
+                const uint4 v1 = __ldg(reinterpret_cast<const uint4*>(src + i0) + 1);
+                const uint32_t wv[8] = {v0.x, v0.y, v0.z, v0.w, v1.x, v1.y, v1.z, v1.w};
+#pragma unroll
+                for (int k = 0; k < 8; k++) {
+                    code[2 * k] = wv[k] & 0xFFFF;
+                    code[2 * k + 1] = wv[k] >> 16;
+                }
+            } else {
+#pragma unroll
+                for (int k = 0; k < kRun; k++) code[k] = (uint32_t)k < cnt ? src[i0 + k] : 1u;
+            }
+            uint32_t bits = 0, zc = 0;
+            unsigned long long u[kRun];
+#pragma unroll
+            for (int k = 0; k < kRun; k++) {
+                u[k] = ((uint32_t)k < cnt && payload) ? tab[code[k]] : 0ull;
+                bits += (uint32_t)(u[k] >> wshift);
+                zc += ((uint32_t)k < cnt) & (code[k] == 0);
+            }
+            int total_l;
+            const uint32_t off = (uint32_t)warp_excl_scan((int)bits, &total_l) + carry;
+            const uint32_t total = carry + (uint32_t)total_l;
+            // pass B: stream the run into the word buffer
+            if (payload && bits) {
+                uint32_t wi = off >> 5;
+                uint32_t nacc = off & 31;            // leading bits belong to earlier runs
+                unsigned long long acc = 0;          // left-aligned pending bits
+                bool first = true;
+#pragma unroll
+                for (int k = 0; k < kRun; k++) {
+                    uint32_t w = (uint32_t)(u[k] >> wshift);
+                    unsigned long long cw = u[k] & cwmask;
+                    if (w > 32) {                    // 64-bit units: emit the high part first
+                        const uint32_t wh = w - 32;
+                        acc |= (cw >> 32) << (64 - nacc - wh);
+                        nacc += wh;
+                        cw &= 0xFFFFFFFFull;
+                        w = 32;
+                        if (nacc >= 32) {
+                            const uint32_t word = (uint32_t)(acc >> 32);
+                            if (first) atomicOr(&buf[wi], word); else buf[wi] = word;
+                            first = false;
+                            wi++;
+                            acc <<= 32;
+                            nacc -= 32;
+                        }
+                    }
+                    if (w) acc |= cw << (64 - nacc - w);
+                    nacc += w;
+                    if (nacc >= 32) {
+                        const uint32_t word = (uint32_t)(acc >> 32);
+                        if (first) atomicOr(&buf[wi], word); else buf[wi] = word;
+                        first = false;
+                        wi++;
+                        acc <<= 32;
+                        nacc -= 32;
+                    }
+                }
+                if (nacc) atomicOr(&buf[wi], (uint32_t)(acc >> 32));
+            }
+            __syncwarp();
+            if (payload) {
+                const uint32_t full = total >> 5;
+                for (uint32_t j = lane; j < full; j += 32) store_word(a.payload, wbyte + 4ull * j, buf[j], B, Bend);
+                __syncwarp();
+                const uint32_t used = (total + 31) >> 5;
+                const uint32_t cw_last = (total & 31) ? buf[full] : 0u;
+                for (uint32_t j = lane; j < used; j += 32) buf[j] = 0;
+                __syncwarp();
+                if (lane == 0) buf[0] = cw_last;
+                __syncwarp();
+                wbyte += 4ull * full;
+                carry = total & 31;
+            }
+            // outliers (code 0) in row-major order
+            if (a.records && __any_sync(kFull, zc)) {
+                int ztot;
+                const uint32_t zoff = (uint32_t)warp_excl_scan((int)zc, &ztot);
+                uint64_t slot = orec + zoff;
+#pragma unroll
+                for (int k = 0; k < kRun; k++) {
+                    if ((uint32_t)k < cnt && code[k] == 0) {
+                        const uint64_t i = i0 + k;
+                        const double v = outlier_value(a, i, two_eb);
+                        a.records[2 * slot] = i + a.idx_base;
+                        a.records[2 * slot + 1] = (unsigned long long)__double_as_longlong(v);
+                        slot++;
+                    }
+                }
+                orec += (uint64_t)ztot;
+            }
+        }
+        if (payload && carry && lane == 0) store_word(a.payload, wbyte, buf[0], B, Bend);
         __syncwarp();
     }
 }
@@ -906,10 +1076,14 @@ __global__ void __launch_bounds__(64) inflate_kernel(
 // mismatch) hands the chunk to the sequential decoder, which reproduces the
 // reference's exact error semantics.
 // --------------------------------------------------------------------------
+// decode tables of the warp decoder: file-scope shared arrays, so every
+// access compiles to LDS (no generic-pointer address conversion per symbol)
+__shared__ uint32_t dl_lut[1 << kLutBits];
+__shared__ unsigned long long dl_first[58];
+__shared__ long long dl_offs[59];
+
 struct DecodeTables {
-    const uint32_t* lut;                 // shared
-    const unsigned long long* first;     // shared
-    const long long* offs;               // shared
+    uint32_t lut_s;                      // shared-space address of dl_lut
     const uint32_t* symbols;
     const uint32_t* words;
     uint64_t nwords;
@@ -917,36 +1091,42 @@ struct DecodeTables {
     int lb, mx;
 };
 
-__device__ __noinline__ uint32_t long_codeword(const DecodeTables& d, uint64_t p, uint32_t& sym) {
+// canonical decode of a codeword longer than the LUT; returns sym | len << 16
+// (len 255: no codeword of any width matches)
+__device__ __forceinline__ uint32_t long_codeword(const uint32_t* words, uint64_t nwords,
+                                                  const uint32_t* symbols, long long nsym, int lb,
+                                                  int mx, uint64_t p) {
     const uint64_t pw = p >> 5;
     const uint32_t ps = (uint32_t)(p & 31);
-    const unsigned long long hi64 = ((unsigned long long)load_be(d.words, pw, d.nwords) << 32) |
-                                    load_be(d.words, pw + 1, d.nwords);
-    const uint32_t w2 = load_be(d.words, pw + 2, d.nwords);
+    const unsigned long long hi64 = ((unsigned long long)load_be(words, pw, nwords) << 32) |
+                                    load_be(words, pw + 1, nwords);
+    const uint32_t w2 = load_be(words, pw + 2, nwords);
     const unsigned long long peek64 = ps ? ((hi64 << ps) | (w2 >> (32 - ps))) : hi64;
-    const unsigned long long peek = peek64 >> (64 - d.mx);
-    for (int b = d.lb + 1; b <= d.mx; b++) {
-        const unsigned long long top = peek >> (d.mx - b);
-        const unsigned long long cntb = (unsigned long long)(d.offs[b + 1] - d.offs[b]);
-        if (top < d.first[b] + cntb) {
-            long long idx = d.offs[b] + (long long)(top - d.first[b]);
+    const unsigned long long peek = peek64 >> (64 - mx);
+    for (int b = lb + 1; b <= mx; b++) {
+        const unsigned long long top = peek >> (mx - b);
+        const unsigned long long cntb = (unsigned long long)(dl_offs[b + 1] - dl_offs[b]);
+        if (top < dl_first[b] + cntb) {
+            long long idx = dl_offs[b] + (long long)(top - dl_first[b]);
             if (idx < 0) idx = 0;
-            if (idx >= d.nsym) idx = d.nsym ? d.nsym - 1 : 0;
-            sym = d.symbols[idx];
-            return (uint32_t)b;
+            if (idx >= nsym) idx = nsym ? nsym - 1 : 0;
+            return (symbols[idx] & 0xFFFF) | ((uint32_t)b << 16);
         }
     }
-    return 255;
+    return 255u << 16;
 }
 
 // one codeword at absolute bit `p` (the reader's position); 255 = invalid
 __device__ __forceinline__ uint32_t decode_one(const DecodeTables& d, BitReader& rd, uint64_t p,
                                                uint32_t& sym) {
     rd.refill();
-    const uint32_t e = d.lut[rd.buf >> (64 - d.lb)];
-    uint32_t len = (e >> 16) & 0xFF;
+    // explicit 32-bit shared address: keeps the shared-window base out of the loop
+    uint32_t e;
+    asm("ld.shared.u32 %0, [%1];" : "=r"(e) : "r"(d.lut_s + ((uint32_t)(rd.buf >> (64 - d.lb)) << 2)));
+    if ((e & 0xFF0000u) == 0)   // longer than the LUT (rare)
+        e = long_codeword(d.words, d.nwords, d.symbols, d.nsym, d.lb, d.mx, p);
+    const uint32_t len = (e >> 16) & 0xFF;
     sym = e & 0xFFFF;
-    if (len == 0) len = long_codeword(d, p, sym);
     if (len != 255) {
         if ((int)len <= rd.nb) rd.skip(len);
         else rd.init(p + len);
@@ -989,23 +1169,20 @@ __global__ void __launch_bounds__(256) inflate_warp_kernel(
     const uint64_t* __restrict__ gfirst, const int64_t* __restrict__ goffsets,
     const uint32_t* __restrict__ symbols, const uint32_t* __restrict__ glut, int max_bw_arg,
     uint16_t* __restrict__ out, uint8_t* __restrict__ redo, DevStatus* st) {
-    __shared__ uint32_t lut[1 << kLutBits];
-    __shared__ unsigned long long first[58];
-    __shared__ long long offs[59];
-    for (uint32_t i = threadIdx.x; i < (1u << kLutBits); i += blockDim.x) lut[i] = glut[i];
-    for (uint32_t i = threadIdx.x; i < 58; i += blockDim.x) first[i] = gfirst[i];
-    for (uint32_t i = threadIdx.x; i < 59; i += blockDim.x) offs[i] = goffsets[i];
+    for (uint32_t i = threadIdx.x; i < (1u << kLutBits); i += blockDim.x) dl_lut[i] = glut[i];
+    for (uint32_t i = threadIdx.x; i < 58; i += blockDim.x) dl_first[i] = gfirst[i];
+    for (uint32_t i = threadIdx.x; i < 59; i += blockDim.x) dl_offs[i] = goffsets[i];
     __syncthreads();
     const int mx = max_bw_arg > 0 ? max_bw_arg : (int)st->max_bw;
     if (mx < 1 || mx > kMaxBw) return;
     DecodeTables d;
-    d.lut = lut;
-    d.first = first;
-    d.offs = offs;
+    // opaque copy: stops ptxas rematerialising the shared-window base (an
+    // S2R SR_CgaCtaId on the decode critical path) at every lookup
+    asm volatile("mov.u32 %0, %1;" : "=r"(d.lut_s) : "r"((uint32_t)__cvta_generic_to_shared(dl_lut)));
     d.symbols = symbols;
     d.words = reinterpret_cast<const uint32_t*>(payload);
     d.nwords = nwords;
-    d.nsym = offs[mx + 1];
+    d.nsym = dl_offs[mx + 1];
     d.mx = mx;
     d.lb = mx < kLutBits ? mx : kLutBits;
     const uint32_t lane = lane_id();
@@ -1120,18 +1297,22 @@ __global__ void __launch_bounds__(256) inflate_warp_kernel(
 
 template <int SRC>
 int run_deflate(sdqz_ctx* ctx, DeflateArgs& a, bool payload) {
-    size_t smem = (SRC == SRC_CODES && a.cap <= 4096) ? a.cap * 8 : 0;
+    const bool ts = SRC == SRC_CODES && a.gtable && a.cap <= 4096;
+    size_t smem = ts ? a.cap * 8 : 0;
     uint64_t grid = ceil_div(a.nchunks, 8);
     if (grid > (uint64_t)ctx->num_sms * 16) grid = ctx->num_sms * 16;
     if (grid < 1) grid = 1;
-    chunk_stats_kernel<SRC><<<(unsigned)grid, 256, smem, ctx->stream>>>(a);
+    if (ts) chunk_stats_kernel<SRC, true><<<(unsigned)grid, 256, smem, ctx->stream>>>(a);
+    else chunk_stats_kernel<SRC, false><<<(unsigned)grid, 256, 0, ctx->stream>>>(a);
     SDQZ_LAUNCHED_NAMED(ctx, "chunk_stats_kernel");
     chunk_scan_kernel<<<1, 1024, 0, ctx->stream>>>(a);
     SDQZ_LAUNCHED_NAMED(ctx, "chunk_scan_kernel");
-    if (payload)
-        chunk_pack_kernel<SRC, true><<<(unsigned)grid, 256, smem, ctx->stream>>>(a);
-    else
-        chunk_pack_kernel<SRC, false><<<(unsigned)grid, 256, smem, ctx->stream>>>(a);
+    if (SRC == SRC_CODES) {
+        if (ts) chunk_pack_run_kernel<true><<<(unsigned)grid, 256, smem, ctx->stream>>>(a, payload ? 1 : 0);
+        else chunk_pack_run_kernel<false><<<(unsigned)grid, 256, 0, ctx->stream>>>(a, payload ? 1 : 0);
+    } else {
+        chunk_pack_kernel<SRC, true, false><<<(unsigned)grid, 256, 0, ctx->stream>>>(a);
+    }
     SDQZ_LAUNCHED_NAMED(ctx, "chunk_pack_kernel");
     return SDQZ_OK;
 }
@@ -1172,9 +1353,13 @@ int launch_codebook(sdqz_ctx* ctx, const unsigned long long* d_hist, uint8_t* d_
         gs.jmp = u + 7 * cap;
     }
     if (smem > 48 * 1024)
-        cudaFuncSetAttribute(codebook_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    codebook_kernel<<<1, kBookThreads, smem, ctx->stream>>>(d_hist, d_bw, cap, book, ctx->d_status,
-                                                           build_tree ? 1 : 0, canon ? 1 : 0, gs);
+        cudaFuncSetAttribute(codebook_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (cap <= kSmemSortMax)
+        codebook_kernel<true><<<1, kBookThreads, smem, ctx->stream>>>(d_hist, d_bw, cap, book, ctx->d_status,
+                                                                   build_tree ? 1 : 0, canon ? 1 : 0, gs);
+    else
+        codebook_kernel<false><<<1, kBookThreads, 0, ctx->stream>>>(d_hist, d_bw, cap, book, ctx->d_status,
+                                                                    build_tree ? 1 : 0, canon ? 1 : 0, gs);
     SDQZ_LAUNCHED_NAMED(ctx, "codebook_kernel");
     return SDQZ_OK;
 }

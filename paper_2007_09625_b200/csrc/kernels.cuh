@@ -83,5 +83,6 @@ int launch_reconstruct(sdqz_ctx* ctx, const uint16_t* codes, const uint64_t* den
 __host__ __device__ inline uint64_t ceil_div(uint64_t a, uint64_t b) { return (a + b - 1) / b; }
 uint32_t default_chunk_size(uint64_t n);
 bool is_fast_shape(int ndims, const uint32_t block[3]);
+bool env_disabled(const char* name);   // env var set and not "0"
 
 }  // namespace sdqz
