@@ -220,7 +220,7 @@ int decompress_core(sdqz_ctx* ctx, const sdqz_header* hdr, const uint8_t* d_bw, 
     const bool chunks_ok = C == ceil_div(n, hdr->chunk_size) && geom_ok && eb_ok;
     BookDev book;
     if ((rc = book_tables(ctx, cap, &book))) return rc;
-    uint16_t* codes = scratch_as<uint16_t>(ctx, S_CODES, n + 8, &rc);
+    uint16_t* codes = scratch_as<uint16_t>(ctx, S_CODES, n + 64, &rc);
     uint64_t* dense = scratch_as<uint64_t>(ctx, S_DENSE, n, &rc);
     uint64_t nblocks = 1;
     for (int a = 0; a < hdr->ndims; a++) nblocks *= ceil_div(hdr->dims[a], hdr->block[a] ? hdr->block[a] : 1);
@@ -440,7 +440,7 @@ int sdqz_reconstruct(sdqz_ctx* ctx, const void* d_codes, int code_bytes, uint64_
     const uint16_t* codes = (const uint16_t*)d_codes;
     if ((rc = reset_status(ctx)) || (rc = set_eb(ctx, eb))) return rc;
     if (code_bytes == 4) {
-        uint16_t* c16 = scratch_as<uint16_t>(ctx, S_CODES, n + 8, &rc);
+        uint16_t* c16 = scratch_as<uint16_t>(ctx, S_CODES, n + 64, &rc);
         if (!c16) return rc;
         if ((rc = launch_narrow_codes(ctx, (const uint32_t*)d_codes, n, cap, c16))) return rc;
         codes = c16;
@@ -590,7 +590,7 @@ int sdqz_compress(sdqz_ctx* ctx, const void* d_in, int dtype, int ndims, const u
     const uint64_t C = ceil_div(n, cs);
     const int in_kind = dtype;
 
-    uint16_t* codes = scratch_as<uint16_t>(ctx, S_CODES, n + 8, &rc);
+    uint16_t* codes = scratch_as<uint16_t>(ctx, S_CODES, n + 64, &rc);
     unsigned long long* hist = scratch_as<unsigned long long>(ctx, S_HIST, cap, &rc);
     uint32_t* cbits = scratch_as<uint32_t>(ctx, S_CHUNK_BITS, C, &rc);
     BookDev book;

@@ -51,6 +51,19 @@ __device__ __forceinline__ void hist_add(HistCtx& h, uint32_t code) {
     }
 }
 
+// Branch-free window update; codes outside the window go to a shared
+// `red` (rare).  Requires the shared histogram (cap <= kSmemHistMax) or none.
+__device__ __forceinline__ void hist_add_fast(HistCtx& h, uint32_t code) {
+    const uint32_t dw = code - h.wbase;
+    const unsigned long long inc = dw < 16u ? (1ull << ((dw & 7u) << 3)) : 0ull;
+    h.lo += dw < 8u ? inc : 0ull;
+    h.hi += dw < 8u ? 0ull : inc;
+    if (dw >= 16u) {
+        if (h.shist) atomicAdd(&h.shist[code], 1u);
+        else if (h.ghist) atomicAdd(&h.ghist[code], 1ull);
+    }
+}
+
 __device__ __forceinline__ void hist_flush(HistCtx& h) {
 #pragma unroll
     for (int k = 0; k < 16; k++) {
@@ -321,37 +334,48 @@ __global__ void __launch_bounds__(kTmaWarps * 32) dq3d_tma_kernel(
         const bool xin = x < X;
         const int ny = (int)umin(8, Y - y0), nz = (int)umin(8, Z - z0);
         const uint64_t base = z0 * YX + y0 * X + x;
+        // pass 1: prequantize the tile in place (fp32 -> int32 bits), branch-free;
+        // the task-wide vote falls back to the exact fp64 path on a bound
+        // violation, a non-finite value or a rounding-tie neighbourhood
         float mx = 0.f;
-        bool tbad = false;
-#pragma unroll 16
+        bool tbad = false, amb = false;
+        int* itile = reinterpret_cast<int*>(const_cast<float*>(tile));
+#pragma unroll 8
         for (int k = 0; k < 64; k++) {
             const float v = tile[k * 32 + lane];
             mx = fmaxf(mx, fabsf(v));
             tbad |= !isfinite(v);
+            itile[k * 32 + lane] = prequant_int_fast(v, rcp, amb);
         }
         bad |= tbad;
-        const bool use_int = __all_sync(kFull, !tbad && (double)mx / two_eb < kIntBound);
+        const bool use_int = __all_sync(kFull, !tbad && !amb && (double)mx / two_eb < kIntBound);
         if (use_int) {
+            // pass 2: D_z D_y D_x Lorenzo residual in int32, codes, histogram
             int hprev[8];
 #pragma unroll
+            for (int y = 0; y < 8; y++) hprev[y] = 0;
+            uint16_t* crow = codes + base;
+#pragma unroll 1
             for (int z = 0; z < 8; z++) {
                 int gprev = 0;
-                uint16_t* crow = codes + base + z * YX;
+                const bool zin = xin && z < nz;
 #pragma unroll
                 for (int y = 0; y < 8; y++) {
-                    const int v = prequant_int(tile[(z * 8 + y) * 32 + lane], rcp, two_eb);
+                    const int v = itile[(z * 8 + y) * 32 + lane];
                     const int left = __shfl_up_sync(kFull, v, 1);
                     const int g = v - (xl ? left : 0);
                     const int hh = g - gprev;
                     gprev = g;
-                    const int delta = hh - (z ? hprev[y] : 0);
+                    const int delta = hh - hprev[y];
                     hprev[y] = hh;
-                    const uint32_t c = code_of_int(delta, r);
-                    if (xin && z < nz && y < ny) {
+                    const uint32_t u = (uint32_t)(delta + r);
+                    const uint32_t c = (u - 1u) < (uint32_t)(2 * r - 1) ? u : 0u;   // -r < delta < r
+                    if (zin && y < ny) {
                         crow[y * X] = (uint16_t)c;
-                        hist_add(h, c);
+                        hist_add_fast(h, c);
                     }
                 }
+                crow += YX;
             }
         } else {
             dq3d_task_f64<0>(in, base, YX, X, xin, nz, ny, xl, two_eb, r, codes, h, bad);

@@ -1308,6 +1308,12 @@ int run_deflate(sdqz_ctx* ctx, DeflateArgs& a, bool payload) {
     chunk_scan_kernel<<<1, 1024, 0, ctx->stream>>>(a);
     SDQZ_LAUNCHED_NAMED(ctx, "chunk_scan_kernel");
     if (SRC == SRC_CODES) {
+        static bool attr = false;   // 28.8 KB static + up to 32 KB table > the 48 KB default
+        if (!attr) {
+            cudaFuncSetAttribute(chunk_pack_run_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 4096 * 8);
+            attr = true;
+        }
         if (ts) chunk_pack_run_kernel<true><<<(unsigned)grid, 256, smem, ctx->stream>>>(a, payload ? 1 : 0);
         else chunk_pack_run_kernel<false><<<(unsigned)grid, 256, 0, ctx->stream>>>(a, payload ? 1 : 0);
     } else {

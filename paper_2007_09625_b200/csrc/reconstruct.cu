@@ -126,8 +126,147 @@ __device__ __forceinline__ long long row_final(int dlt, bool isout, long long vo
     return (long long)S + corr + K;
 }
 
+// int32 variant of row_final; the caller guarantees |K| < 3*2^28 and |v| < 2^27
+template <int W>
+__device__ __forceinline__ int row_final32(int dlt, bool isout, int vout, int K, uint32_t lane) {
+    const uint32_t sl = lane & (W - 1);
+    int S = dlt;
+#pragma unroll
+    for (int o = 1; o < W; o <<= 1) {
+        const int t = __shfl_up_sync(kFull, S, o);
+        if (sl >= (uint32_t)o) S += t;
+    }
+    const int t = isout ? (vout - K - S) : 0;
+    const uint32_t m = __ballot_sync(kFull, isout);
+    const uint32_t segmask = (W == 32) ? kFull : (((1u << W) - 1) << (lane & ~(W - 1)));
+    const uint32_t mine = m & segmask & (lane == 31 ? kFull : ((2u << lane) - 1));
+    const int src = mine ? 31 - __clz(mine) : (int)lane;
+    const int corr = __shfl_sync(kFull, t, src);
+    return S + (mine ? corr : 0) + K;
+}
+
+// 3D block 8x8x8 reconstruction.  The task's 64 codes per lane are loaded up
+// front (64 independent coalesced row loads in flight), then the Lorenzo
+// inverse runs in int32 with an overflow guard (every final and outlier value
+// below 2^28 / 2^27 keeps every intermediate inside int32); a task that trips
+// the guard is recomputed in int64 (rq3d_task64).
+template <int OUTK>
+__device__ __noinline__ void rq3d_task64(const uint16_t* __restrict__ codes,
+                                         const unsigned long long* __restrict__ dense,
+                                         uint64_t base, uint64_t YX, uint64_t X, bool xin, bool skip,
+                                         int ny, int nz, int r, double two_eb, uint32_t lane,
+                                         void* __restrict__ out) {
+    long long F[8];
+#pragma unroll
+    for (int y = 0; y < 8; y++) F[y] = 0;
+    for (int z = 0; z < nz; z++) {
+        long long R = 0, lag = 0;
+#pragma unroll
+        for (int y = 0; y < 8; y++) {
+            const bool valid = xin && y < ny;
+            const uint64_t i = base + z * YX + y * X;
+            const uint32_t code = valid ? codes[i] : (uint32_t)r;
+            const bool isout = valid && code == 0;
+            const int dlt = isout ? 0 : (int)code - r;
+            const long long vout = isout ? outlier_int(dense, i) : 0;
+            const long long K = R + F[y] - (y ? F[y - 1] : 0);
+            const long long fin = row_final<8>(dlt, isout, vout, K, lane);
+            R = fin;
+            if (y) F[y - 1] = lag;
+            lag = fin;
+            if (valid && !skip) store_out<OUTK>(out, i, fin, two_eb);
+        }
+        F[7] = lag;
+    }
+}
+
 template <int OUTK>
 __global__ void __launch_bounds__(kThreads) rq3d_kernel(const uint16_t* __restrict__ codes,
+                                                        const unsigned long long* __restrict__ dense,
+                                                        const uint8_t* __restrict__ blockflag,
+                                                        int any_slow, uint64_t Z, uint64_t Y,
+                                                        uint64_t X, uint32_t cap, double two_eb,
+                                                        void* __restrict__ out) {
+    __shared__ __align__(16) uint16_t s_codes[kWarpsPerCta][64 * 32];
+    const int r = (int)(cap >> 1);
+    const uint32_t lane = lane_id();
+    const uint64_t nbx = ceil_div(X, 8), nbx4 = ceil_div(nbx, 4), nby = ceil_div(Y, 8), nbz = ceil_div(Z, 8);
+    const uint64_t ntask = nbx4 * nby * nbz;
+    const uint64_t YX = Y * X;
+    for (uint64_t task = blockIdx.x * (uint64_t)kWarpsPerCta + (threadIdx.x >> 5); task < ntask;
+         task += (uint64_t)gridDim.x * kWarpsPerCta) {
+        const uint64_t bx4 = task % nbx4, t2 = task / nbx4;
+        const uint64_t by = t2 % nby, bz = t2 / nby;
+        const uint64_t x = bx4 * 32 + lane, y0 = by * 8, z0 = bz * 8;
+        const bool xin = x < X;
+        bool skip = false;
+        if (any_slow && xin) skip = blockflag[(bz * nby + by) * nbx + (x >> 3)] != 0;
+        const int ny = (int)umin(8, Y - y0), nz = (int)umin(8, Z - z0);
+        const uint64_t base = z0 * YX + y0 * X + x;
+        // stage the task's 8x8 rows of 32 codes in shared memory with
+        // cp.async (4-byte pieces, 16 lanes per row, two rows per instruction)
+        uint16_t* tile = s_codes[threadIdx.x >> 5];
+        {
+            const uint64_t row0 = z0 * YX + y0 * X + bx4 * 32;
+            const uint32_t half = lane >> 4, piece = lane & 15;
+#pragma unroll 8
+            for (int k = 0; k < 32; k++) {
+                const int row = 2 * k + half, z = row >> 3, y = row & 7;
+                if (z < nz && y < ny) {
+                    const uint16_t* src = codes + row0 + z * YX + y * X + 2 * piece;
+                    asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(
+                                     (uint32_t)__cvta_generic_to_shared(tile + row * 32 + 2 * piece)),
+                                 "l"(src)
+                                 : "memory");
+                }
+            }
+            asm volatile("cp.async.wait_all;" ::: "memory");
+            __syncwarp();
+        }
+        int F[8];
+#pragma unroll
+        for (int y = 0; y < 8; y++) F[y] = 0;
+        bool ovf = false;
+        float* outf = (float*)out;
+        double* outd = (double*)out;
+#pragma unroll 1
+        for (int z = 0; z < nz; z++) {
+            int R = 0, lag = 0;
+            const uint64_t zoff = base + z * YX;
+#pragma unroll
+            for (int y = 0; y < 8; y++) {
+                const bool valid = xin && y < ny;
+                const uint32_t code = valid ? tile[(z * 8 + y) * 32 + lane] : (uint32_t)r;
+                const bool isout = valid && code == 0;
+                const int dlt = isout ? 0 : (int)code - r;
+                int vout = 0;
+                if (isout) {
+                    const long long v = outlier_int(dense, zoff + y * X);
+                    ovf |= v >= (1ll << 27) || v <= -(1ll << 27);
+                    vout = (int)v;
+                }
+                const int K = R + F[y] - (y ? F[y - 1] : 0);
+                const int fin = row_final32<8>(dlt, isout, vout, K, lane);
+                ovf |= fin >= (1 << 28) || fin <= -(1 << 28);
+                R = fin;
+                if (y) F[y - 1] = lag;
+                lag = fin;
+                if (valid && !skip) {
+                    const double v = __dmul_rn((double)fin, two_eb);
+                    if (OUTK == 0) outf[zoff + y * X] = __double2float_rn(v);
+                    else outd[zoff + y * X] = v;
+                }
+            }
+            F[7] = lag;
+        }
+        if (__any_sync(kFull, ovf))
+            rq3d_task64<OUTK>(codes, dense, base, YX, X, xin, skip, ny, nz, r, two_eb, lane, out);
+        __syncwarp();   // tile reused by the next task
+    }
+}
+
+template <int OUTK>
+__global__ void __launch_bounds__(kThreads) rq3d_kernel_old(const uint16_t* __restrict__ codes,
                                                         const unsigned long long* __restrict__ dense,
                                                         const uint8_t* __restrict__ blockflag,
                                                         int any_slow, uint64_t Z, uint64_t Y,
@@ -371,9 +510,14 @@ int launch_reconstruct(sdqz_ctx* ctx, const uint16_t* codes, const uint64_t* den
         if (grid > (uint64_t)max_grid) grid = max_grid;
         if (grid < 1) grid = 1;
         int slow = any_slow ? 1 : 0;
+        // cp.async staging needs 4-byte aligned code rows
+        const bool staged = dims[2] % 2 == 0 && ((uintptr_t)codes & 3) == 0;
 #define RQ_LAUNCH(K)                                                                                 \
-        if (ndims == 3)                                                                              \
+        if (ndims == 3 && staged)                                                                    \
             rq3d_kernel<K><<<(unsigned)grid, kThreads, 0, ctx->stream>>>(codes, dn, blockflag, slow,   \
+                                                                        dims[0], dims[1], dims[2], cap, two_eb, out); \
+        else if (ndims == 3)                                                                         \
+            rq3d_kernel_old<K><<<(unsigned)grid, kThreads, 0, ctx->stream>>>(codes, dn, blockflag, slow, \
                                                                         dims[0], dims[1], dims[2], cap, two_eb, out); \
         else if (ndims == 2)                                                                         \
             rq2d_kernel<K><<<(unsigned)grid, kThreads, 0, ctx->stream>>>(codes, dn, blockflag, slow,   \
