@@ -129,12 +129,98 @@ __global__ void __launch_bounds__(kBookThreads) codebook_kernel(
             // shared-memory loads off the sequential critical path.
             unsigned long long* iq = small ? (smem + cap) : gs.iw;
             uint32_t* parent = small ? (uint32_t*)(smem + 2 * cap) + cap : gs.parent;
+            constexpr unsigned long long NONE = ~0ull;
+            // -- parallel rounds.  With t = the first node the sequential merge
+            // would create (sum of the two smallest frontier keys), every
+            // frontier element below t is popped before t, pairwise in sorted
+            // order; so the first 2*floor(m/2) of the m elements below t can be
+            // merged in one round, exactly as the heap would.  Rounds continue
+            // while they stay productive; the tail runs sequentially.
+            __shared__ uint32_t r_li, r_ii, r_ni, r_p, r_mL, r_mI;
+            __shared__ unsigned long long r_t;
+            unsigned long long* fk = small ? (unsigned long long*)((uint32_t*)(smem + 2 * cap) + 3 * cap)
+                                           : (unsigned long long*)gs.dep;
+            uint32_t* fid = small ? (uint32_t*)(smem + 2 * cap) + 5 * cap : gs.jmp;
+            if (tid == 0) { r_li = 0; r_ii = 0; r_ni = 0; }
+            __syncthreads();
+            auto lower = [](const unsigned long long* a, uint32_t lo, uint32_t hi,
+                            unsigned long long key) {
+                while (lo < hi) {
+                    const uint32_t mid = (lo + hi) >> 1;
+                    if (a[mid] < key) lo = mid + 1; else hi = mid;
+                }
+                return lo;
+            };
+            while (true) {
+                const uint32_t li = r_li, ii = r_ii, ni = r_ni;
+                if (ni + 1 >= n) break;
+                if (tid == 0) {
+                    const unsigned long long LH = li < n ? keys[li] : NONE, IH = ii < ni ? iq[ii] : NONE;
+                    unsigned long long f0, f1;
+                    if (LH < IH) {
+                        f0 = LH;
+                        const unsigned long long L1 = li + 1 < n ? keys[li + 1] : NONE;
+                        f1 = L1 < IH ? L1 : IH;
+                    } else {
+                        f0 = IH;
+                        const unsigned long long I1 = ii + 1 < ni ? iq[ii + 1] : NONE;
+                        f1 = LH < I1 ? LH : I1;
+                    }
+                    const unsigned long long t =
+                        (((f0 >> 16) + (f1 >> 16)) << 16) | min(f0 & 0xFFFF, f1 & 0xFFFF);
+                    const uint32_t mL = lower(keys, li, n, t) - li, mI = lower(iq, ii, ni, t) - ii;
+                    r_t = t;
+                    r_mL = mL;
+                    r_mI = mI;
+                    r_p = (mL + mI) / 2;
+                }
+                __syncthreads();
+                const uint32_t p = r_p, mL = r_mL, mI = r_mI;
+                if (p < 4) break;   // unproductive: finish sequentially
+                // merged position of every element below t
+                for (uint32_t j = tid; j < mL + mI; j += blockDim.x) {
+                    unsigned long long key;
+                    uint32_t pos, id;
+                    if (j < mL) {
+                        key = keys[li + j];
+                        pos = j + (lower(iq, ii, ii + mI, key) - ii);
+                        id = li + j;
+                    } else {
+                        const uint32_t q = j - mL;
+                        key = iq[ii + q];
+                        pos = q + (lower(keys, li, li + mL, key) - li);
+                        id = n + ii + q;
+                    }
+                    if (pos < 2 * p) { fk[pos] = key; fid[pos] = id; }
+                }
+                __syncthreads();
+                for (uint32_t j = tid; j < p; j += blockDim.x) {
+                    const unsigned long long a = fk[2 * j], b = fk[2 * j + 1];
+                    iq[ni + j] = (((a >> 16) + (b >> 16)) << 16) | min(a & 0xFFFF, b & 0xFFFF);
+                    parent[fid[2 * j]] = n + ni + j;
+                    parent[fid[2 * j + 1]] = n + ni + j;
+                }
+                if (tid == 0) {
+                    uint32_t cL = mL, cI = mI;
+                    if ((mL + mI) & 1) {   // the largest element below t waits for the next round
+                        const bool last_leaf =
+                            mL > 0 && (mI == 0 || keys[li + mL - 1] > iq[ii + mI - 1]);
+                        if (last_leaf) cL--; else cI--;
+                    }
+                    r_li = li + cL;
+                    r_ii = ii + cI;
+                    r_ni = ni + p;
+                }
+                __syncthreads();
+            }
+            // -- sequential tail (thread 0): two-queue merge from (li, ii, ni)
             if (tid == 0) {
-                constexpr unsigned long long NONE = ~0ull;
-                uint32_t li = 0, ii = 0, ni = 0;
-                unsigned long long L0 = keys[0], L1 = keys[1], L2 = n > 2 ? keys[2] : NONE;
-                unsigned long long H0 = NONE, H1 = NONE, H2 = NONE;
-                for (uint32_t k = 0; k + 1 < n; k++) {
+                uint32_t li = r_li, ii = r_ii, ni = r_ni;
+                auto lk = [&](uint32_t i) { return i < n ? keys[i] : NONE; };
+                auto ik = [&](uint32_t i) { return i < ni ? iq[i] : NONE; };
+                unsigned long long L0 = lk(li), L1 = lk(li + 1), L2 = lk(li + 2);
+                unsigned long long H0 = ik(ii), H1 = ik(ii + 1), H2 = ik(ii + 2);
+                for (uint32_t k = ni; k + 1 < n; k++) {
                     unsigned long long kk[2];
                     uint32_t node[2];
 #pragma unroll
@@ -166,6 +252,7 @@ __global__ void __launch_bounds__(kBookThreads) codebook_kernel(
                     parent[node[0]] = n + k;
                     parent[node[1]] = n + k;
                 }
+                (void)ni;
             }
             __syncthreads();
             // ---- depths by pointer jumping (root = 2n-2) -------------------
@@ -1081,6 +1168,9 @@ __global__ void __launch_bounds__(64) inflate_kernel(
 __shared__ uint32_t dl_lut[1 << kLutBits];
 __shared__ unsigned long long dl_first[58];
 __shared__ long long dl_offs[59];
+__shared__ unsigned long long dl_lim[58];     // (first[b] + count[b]) << (mx - b)
+constexpr uint32_t kSymSmem = 8192;
+__shared__ uint16_t dl_sym[kSymSmem];         // symbols by (width, symbol), if they fit
 
 struct DecodeTables {
     uint32_t lut_s;                      // shared-space address of dl_lut
@@ -1090,6 +1180,23 @@ struct DecodeTables {
     long long nsym;
     int lb, mx;
 };
+
+// canonical decode (huffman.py:295-305) of a codeword longer than the LUT from
+// a left-aligned `mx`-bit peek; shared tables only.  Returns sym | len << 16
+// (len 255: no codeword of any width matches).
+__device__ __forceinline__ uint32_t long_from_peek(const DecodeTables& d, unsigned long long peek) {
+    for (int b = d.lb + 1; b <= d.mx; b++) {
+        if (peek < dl_lim[b]) {
+            const unsigned long long top = peek >> (d.mx - b);
+            long long idx = dl_offs[b] + (long long)(top - dl_first[b]);
+            if (idx < 0) idx = 0;
+            if (idx >= d.nsym) idx = d.nsym ? d.nsym - 1 : 0;
+            const uint32_t sym = d.nsym <= (long long)kSymSmem ? dl_sym[idx] : d.symbols[idx];
+            return (sym & 0xFFFF) | ((uint32_t)b << 16);
+        }
+    }
+    return 255u << 16;
+}
 
 // canonical decode of a codeword longer than the LUT; returns sym | len << 16
 // (len 255: no codeword of any width matches)
@@ -1123,8 +1230,11 @@ __device__ __forceinline__ uint32_t decode_one(const DecodeTables& d, BitReader&
     // explicit 32-bit shared address: keeps the shared-window base out of the loop
     uint32_t e;
     asm("ld.shared.u32 %0, [%1];" : "=r"(e) : "r"(d.lut_s + ((uint32_t)(rd.buf >> (64 - d.lb)) << 2)));
-    if ((e & 0xFF0000u) == 0)   // longer than the LUT (rare)
-        e = long_codeword(d.words, d.nwords, d.symbols, d.nsym, d.lb, d.mx, p);
+    if ((e & 0xFF0000u) == 0) {   // longer than the LUT
+        // after refill the window holds >= 33 valid bits: enough for mx <= 32
+        e = d.mx <= 32 ? long_from_peek(d, rd.buf >> (64 - d.mx))
+                       : long_codeword(d.words, d.nwords, d.symbols, d.nsym, d.lb, d.mx, p);
+    }
     const uint32_t len = (e >> 16) & 0xFF;
     sym = e & 0xFFFF;
     if (len != 255) {
@@ -1161,6 +1271,89 @@ __device__ __forceinline__ bool decode_span(const DecodeTables& d, uint64_t sbit
     return ok;
 }
 
+// Phase-1 decode of one lane slice [start, stop), continued to stop2 (the
+// 64-bit synchronisation window of the next slice).  maskA: boundaries in
+// [start, start+64); maskB: boundaries in [stop, stop+64); kpre: codewords
+// starting before stop; exit: first boundary >= stop.
+__device__ __forceinline__ bool decode_window(const DecodeTables& d, uint64_t sbit, uint32_t start,
+                                              uint32_t stop, uint32_t stop2, uint32_t& exit_pos,
+                                              uint32_t& kpre, unsigned long long& maskA,
+                                              unsigned long long& maskB) {
+    BitReader rd;
+    rd.blk = reinterpret_cast<const uint4*>(d.words);
+    rd.nblk = d.nwords / 4;
+    rd.init(sbit + start);
+    uint32_t pos = start, k = 0, ex = 0;
+    unsigned long long ma = 0, mb = 0;
+    bool ok = true, have = false;
+    while (pos < stop2) {
+        const uint32_t ra = pos - start;
+        if (ra < 64) ma |= 1ull << ra;
+        if (pos >= stop) {
+            if (!have) { ex = pos; have = true; }
+            const uint32_t rb = pos - stop;
+            if (rb < 64) mb |= 1ull << rb;
+        } else {
+            k++;
+        }
+        uint32_t sym;
+        const uint32_t len = decode_one(d, rd, sbit + pos, sym);
+        if (len == 255) { ok = false; break; }
+        pos += len;
+    }
+    exit_pos = have ? ex : pos;
+    kpre = k;
+    maskA = ma;
+    maskB = mb;
+    return ok;
+}
+
+// Decode `count` codewords from relative bit `start`, which must end exactly
+// at `end`; store them at dst (16-byte stores once 8-code aligned).
+__device__ __forceinline__ bool decode_store(const DecodeTables& d, uint64_t sbit, uint32_t start,
+                                             uint32_t end, uint32_t count, uint16_t* dst,
+                                             uint32_t& zeros) {
+    BitReader rd;
+    rd.blk = reinterpret_cast<const uint4*>(d.words);
+    rd.nblk = d.nwords / 4;
+    rd.init(sbit + start);
+    uint32_t pos = start, j = 0;
+    bool ok = true;
+    const uint32_t head = (uint32_t)umin((8 - (((uintptr_t)dst >> 1) & 7)) & 7, count);
+    for (; j < head; j++) {
+        uint32_t sym;
+        const uint32_t len = decode_one(d, rd, sbit + pos, sym);
+        if (len == 255) { ok = false; break; }
+        pos += len;
+        dst[j] = (uint16_t)sym;
+        zeros += sym == 0;
+    }
+    for (; ok && j + 8 <= count; j += 8) {
+        unsigned long long acc0 = 0, acc1 = 0;
+#pragma unroll
+        for (int t = 0; t < 8; t++) {
+            uint32_t sym;
+            const uint32_t len = decode_one(d, rd, sbit + pos, sym);
+            ok &= len != 255;
+            pos += len;
+            zeros += sym == 0;
+            if (t < 4) acc0 |= (unsigned long long)sym << (16 * t);
+            else acc1 |= (unsigned long long)sym << (16 * (t - 4));
+        }
+        *reinterpret_cast<uint4*>(dst + j) =
+            make_uint4((uint32_t)acc0, (uint32_t)(acc0 >> 32), (uint32_t)acc1, (uint32_t)(acc1 >> 32));
+    }
+    for (; ok && j < count; j++) {
+        uint32_t sym;
+        const uint32_t len = decode_one(d, rd, sbit + pos, sym);
+        if (len == 255) { ok = false; break; }
+        pos += len;
+        dst[j] = (uint16_t)sym;
+        zeros += sym == 0;
+    }
+    return ok && pos == end;
+}
+
 constexpr uint32_t kMinSliceBits = 128;
 
 __global__ void __launch_bounds__(256) inflate_warp_kernel(
@@ -1172,9 +1365,19 @@ __global__ void __launch_bounds__(256) inflate_warp_kernel(
     for (uint32_t i = threadIdx.x; i < (1u << kLutBits); i += blockDim.x) dl_lut[i] = glut[i];
     for (uint32_t i = threadIdx.x; i < 58; i += blockDim.x) dl_first[i] = gfirst[i];
     for (uint32_t i = threadIdx.x; i < 59; i += blockDim.x) dl_offs[i] = goffsets[i];
-    __syncthreads();
     const int mx = max_bw_arg > 0 ? max_bw_arg : (int)st->max_bw;
     if (mx < 1 || mx > kMaxBw) return;
+    __syncthreads();
+    {
+        const long long ns = dl_offs[mx + 1];
+        if (ns <= (long long)kSymSmem)
+            for (uint32_t i = threadIdx.x; i < ns; i += blockDim.x) dl_sym[i] = (uint16_t)symbols[i];
+        for (uint32_t b = threadIdx.x; b < 58; b += blockDim.x)
+            dl_lim[b] = (b >= 1 && (int)b <= mx)
+                            ? (dl_first[b] + (unsigned long long)(dl_offs[b + 1] - dl_offs[b])) << (mx - b)
+                            : 0ull;
+    }
+    __syncthreads();
     DecodeTables d;
     // opaque copy: stops ptxas rematerialising the shared-window base (an
     // S2R SR_CgaCtaId on the decode critical path) at every lookup
@@ -1205,8 +1408,44 @@ __global__ void __launch_bounds__(256) inflate_warp_kernel(
         uint32_t e = B, k = 0;
         unsigned long long mask = 1;
         bool ok = true;
+        // phase 1 + window synchronisation: lane l-1 continues 64 bits into
+        // slice l; the first boundary both paths share is a true boundary
+        // (lane 0 is true from bit 0, so by induction every lane is)
+        {
+            unsigned long long mB = 0;
+            uint32_t kpre = 0;
+            if (active) ok = decode_window(d, sbit, s, s_next, lane + 1 == L ? B : s_next + 64, e, kpre, mask, mB);
+            const unsigned long long pmB = __shfl_up_sync(kFull, mB, 1);
+            const bool pok = __shfl_up_sync(kFull, ok, 1);
+            const unsigned long long cand = lane ? (mask & pmB) : 1ull;
+            const bool sync = !active || (ok && cand != 0 && (lane == 0 || pok));
+            const uint32_t rel = cand ? (uint32_t)(__ffsll((long long)cand) - 1) : 0;
+            const uint32_t nrel = __shfl_down_sync(kFull, rel, 1);
+            const uint32_t last_e = __shfl_sync(kFull, e, L - 1);
+            if (__all_sync(kFull, sync) && last_e == B) {
+                uint32_t nl = 0;
+                if (active) {
+                    nl = kpre - (rel ? __popcll(mask & ((1ull << rel) - 1)) : 0);
+                    if (lane + 1 < L) nl += nrel ? __popcll(mB & ((1ull << nrel) - 1)) : 0;
+                }
+                int total;
+                const uint32_t o = (uint32_t)warp_excl_scan((int)nl, &total);
+                if ((uint32_t)total == cnt) {
+                    const uint32_t cs = s + rel;
+                    const uint32_t ce = lane + 1 < L ? s_next + nrel : B;
+                    bool ok3 = true;
+                    uint32_t zeros = 0;
+                    if (active && nl) ok3 = decode_store(d, sbit, cs, ce, nl, out + base + o, zeros);
+                    if (__all_sync(kFull, ok3)) {
+                        zeros_total += zeros;
+                        continue;
+                    }
+                }
+            }
+        }
         if (active) ok = decode_span(d, sbit, s, s_next, e, k, mask);
-        // phase 2: propagate synchronisation from lane 0
+        // fallback phase 2: propagate synchronisation from lane 0 by redoing
+        // lanes from their predecessor's exit
         bool good = false;
         uint32_t cstart = 0;
         for (int round = 0; round <= 32; round++) {
@@ -1241,50 +1480,7 @@ __global__ void __launch_bounds__(256) inflate_warp_kernel(
         // phase 3: decode the true span [cstart, e) and store nsym_l codes at o
         bool ok3 = true;
         uint32_t zeros = 0;
-        if (active && nsym_l) {
-            BitReader rd;
-            rd.blk = reinterpret_cast<const uint4*>(payload);
-            rd.nblk = nwords / 4;
-            rd.init(sbit + cstart);
-            uint32_t pos = cstart;
-            uint16_t* dst = out + base + o;
-            uint32_t j = 0;
-            // scalar head up to 8-code alignment
-            const uint32_t head = umin((8 - ((base + o) & 7)) & 7, nsym_l);
-            for (; j < head; j++) {
-                uint32_t sym;
-                const uint32_t len = decode_one(d, rd, sbit + pos, sym);
-                if (len == 255) { ok3 = false; break; }
-                pos += len;
-                dst[j] = (uint16_t)sym;
-                zeros += sym == 0;
-            }
-            unsigned long long acc0 = 0, acc1 = 0;
-            for (; ok3 && j + 8 <= nsym_l; j += 8) {
-#pragma unroll
-                for (int t = 0; t < 8; t++) {
-                    uint32_t sym;
-                    const uint32_t len = decode_one(d, rd, sbit + pos, sym);
-                    ok3 &= len != 255;
-                    pos += len;
-                    zeros += sym == 0;
-                    if (t < 4) acc0 |= (unsigned long long)sym << (16 * t);
-                    else acc1 |= (unsigned long long)sym << (16 * (t - 4));
-                }
-                *reinterpret_cast<uint4*>(dst + j) = make_uint4((uint32_t)acc0, (uint32_t)(acc0 >> 32),
-                                                                (uint32_t)acc1, (uint32_t)(acc1 >> 32));
-                acc0 = acc1 = 0;
-            }
-            for (; ok3 && j < nsym_l; j++) {
-                uint32_t sym;
-                const uint32_t len = decode_one(d, rd, sbit + pos, sym);
-                if (len == 255) { ok3 = false; break; }
-                pos += len;
-                dst[j] = (uint16_t)sym;
-                zeros += sym == 0;
-            }
-            ok3 &= pos == e;
-        }
+        if (active && nsym_l) ok3 = decode_store(d, sbit, cstart, e, nsym_l, out + base + o, zeros);
         if (!__all_sync(kFull, ok3)) {
             if (lane == 0) redo[c] = 1;
             continue;
