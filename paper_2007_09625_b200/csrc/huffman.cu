@@ -1271,28 +1271,39 @@ __device__ __forceinline__ bool decode_span(const DecodeTables& d, uint64_t sbit
     return ok;
 }
 
+// 128-bit boundary window (two u64 halves)
+struct Win128 {
+    unsigned long long lo, hi;
+    __device__ __forceinline__ void set(uint32_t r) {
+        if (r < 64) lo |= 1ull << r;
+        else if (r < 128) hi |= 1ull << (r - 64);
+    }
+    __device__ __forceinline__ uint32_t below(uint32_t r) const {   // set bits in [0, r)
+        if (r == 0) return 0;
+        if (r <= 64) return __popcll(r == 64 ? lo : (lo & ((1ull << r) - 1)));
+        return __popcll(lo) + __popcll(hi & ((1ull << (r - 64)) - 1));
+    }
+};
+
 // Phase-1 decode of one lane slice [start, stop), continued to stop2 (the
-// 64-bit synchronisation window of the next slice).  maskA: boundaries in
-// [start, start+64); maskB: boundaries in [stop, stop+64); kpre: codewords
+// 128-bit synchronisation window of the next slice).  wa: boundaries in
+// [start, start+128); wb: boundaries in [stop, stop+128); kpre: codewords
 // starting before stop; exit: first boundary >= stop.
 __device__ __forceinline__ bool decode_window(const DecodeTables& d, uint64_t sbit, uint32_t start,
                                               uint32_t stop, uint32_t stop2, uint32_t& exit_pos,
-                                              uint32_t& kpre, unsigned long long& maskA,
-                                              unsigned long long& maskB) {
+                                              uint32_t& kpre, Win128& wa, Win128& wb) {
     BitReader rd;
     rd.blk = reinterpret_cast<const uint4*>(d.words);
     rd.nblk = d.nwords / 4;
     rd.init(sbit + start);
     uint32_t pos = start, k = 0, ex = 0;
-    unsigned long long ma = 0, mb = 0;
+    wa.lo = wa.hi = wb.lo = wb.hi = 0;
     bool ok = true, have = false;
     while (pos < stop2) {
-        const uint32_t ra = pos - start;
-        if (ra < 64) ma |= 1ull << ra;
+        wa.set(pos - start);
         if (pos >= stop) {
             if (!have) { ex = pos; have = true; }
-            const uint32_t rb = pos - stop;
-            if (rb < 64) mb |= 1ull << rb;
+            wb.set(pos - stop);
         } else {
             k++;
         }
@@ -1303,8 +1314,6 @@ __device__ __forceinline__ bool decode_window(const DecodeTables& d, uint64_t sb
     }
     exit_pos = have ? ex : pos;
     kpre = k;
-    maskA = ma;
-    maskB = mb;
     return ok;
 }
 
@@ -1403,84 +1412,67 @@ __global__ void __launch_bounds__(256) inflate_warp_kernel(
             continue;
         }
         const bool active = lane < L;
-        uint32_t s = active ? (uint32_t)(((uint64_t)lane * B) / L) : B;
+        const uint32_t s0 = active ? (uint32_t)(((uint64_t)lane * B) / L) : B;
         const uint32_t s_next = active ? (uint32_t)(((uint64_t)(lane + 1) * B) / L) : B;
-        uint32_t e = B, k = 0;
-        unsigned long long mask = 1;
+        const uint32_t stop2 = lane + 1 == L ? B : s_next + 128;
+        // phase 1: every lane decodes its slice plus a 128-bit window of the next
+        uint32_t start = s0, e = B, kpre = 0;
+        Win128 wa{0, 0}, wb{0, 0};
         bool ok = true;
-        // phase 1 + window synchronisation: lane l-1 continues 64 bits into
-        // slice l; the first boundary both paths share is a true boundary
-        // (lane 0 is true from bit 0, so by induction every lane is)
-        {
-            unsigned long long mB = 0;
-            uint32_t kpre = 0;
-            if (active) ok = decode_window(d, sbit, s, s_next, lane + 1 == L ? B : s_next + 64, e, kpre, mask, mB);
-            const unsigned long long pmB = __shfl_up_sync(kFull, mB, 1);
-            const bool pok = __shfl_up_sync(kFull, ok, 1);
-            const unsigned long long cand = lane ? (mask & pmB) : 1ull;
-            const bool sync = !active || (ok && cand != 0 && (lane == 0 || pok));
-            const uint32_t rel = cand ? (uint32_t)(__ffsll((long long)cand) - 1) : 0;
-            const uint32_t nrel = __shfl_down_sync(kFull, rel, 1);
-            const uint32_t last_e = __shfl_sync(kFull, e, L - 1);
-            if (__all_sync(kFull, sync) && last_e == B) {
-                uint32_t nl = 0;
-                if (active) {
-                    nl = kpre - (rel ? __popcll(mask & ((1ull << rel) - 1)) : 0);
-                    if (lane + 1 < L) nl += nrel ? __popcll(mB & ((1ull << nrel) - 1)) : 0;
-                }
-                int total;
-                const uint32_t o = (uint32_t)warp_excl_scan((int)nl, &total);
-                if ((uint32_t)total == cnt) {
-                    const uint32_t cs = s + rel;
-                    const uint32_t ce = lane + 1 < L ? s_next + nrel : B;
-                    bool ok3 = true;
-                    uint32_t zeros = 0;
-                    if (active && nl) ok3 = decode_store(d, sbit, cs, ce, nl, out + base + o, zeros);
-                    if (__all_sync(kFull, ok3)) {
-                        zeros_total += zeros;
-                        continue;
-                    }
-                }
-            }
-        }
-        if (active) ok = decode_span(d, sbit, s, s_next, e, k, mask);
-        // fallback phase 2: propagate synchronisation from lane 0 by redoing
-        // lanes from their predecessor's exit
+        if (active) ok = decode_window(d, sbit, start, s_next, stop2, e, kpre, wa, wb);
+        // phase 2: truth propagates from lane 0.  A lane whose predecessor is
+        // true synchronises at the first boundary both paths share inside the
+        // window (a true boundary); failing that, it redecodes from the
+        // predecessor's exit, which is a true boundary.
+        bool tru = !active || (lane == 0 && ok);
+        uint32_t sync = start;   // absolute (chunk-relative) start of the lane's true span
         bool good = false;
-        uint32_t cstart = 0;
-        for (int round = 0; round <= 32; round++) {
+        for (uint32_t round = 0; round <= L; round++) {
+            const bool ptru = __shfl_up_sync(kFull, tru, 1);
+            const unsigned long long pb_lo = __shfl_up_sync(kFull, wb.lo, 1);
+            const unsigned long long pb_hi = __shfl_up_sync(kFull, wb.hi, 1);
             const uint32_t pe = __shfl_up_sync(kFull, e, 1);
-            const bool pok = __shfl_up_sync(kFull, ok, 1);
-            cstart = lane ? pe : 0;
-            bool sync = true;
-            if (active) {
-                if (lane == 0) sync = ok;
-                else sync = ok && pok && cstart >= s && cstart - s < 64 && ((mask >> (cstart - s)) & 1);
+            if (active && !tru && ptru && lane > 0) {
+                // wb of lane-1 and wa of this lane share the origin s0 only
+                // while this lane still starts at s0
+                const unsigned long long c_lo = start == s0 ? (wa.lo & pb_lo) : 0ull;
+                const unsigned long long c_hi = start == s0 ? (wa.hi & pb_hi) : 0ull;
+                if (ok && (c_lo | c_hi)) {
+                    sync = s0 + (c_lo ? (uint32_t)(__ffsll((long long)c_lo) - 1)
+                                      : 64u + (uint32_t)(__ffsll((long long)c_hi) - 1));
+                    tru = true;
+                } else if (pe < s_next) {
+                    start = pe;
+                    sync = pe;
+                    ok = decode_window(d, sbit, start, s_next, stop2, e, kpre, wa, wb);
+                    tru = ok;
+                } else {
+                    ok = false;
+                }
             }
-            if (__all_sync(kFull, sync)) { good = true; break; }
-            // redo from the predecessor's exit; a lane whose predecessor is
-            // itself invalid waits for a later round
-            if (active && !sync && pok && cstart < s_next) {
-                s = cstart;
-                ok = decode_span(d, sbit, s, s_next, e, k, mask);
-            }
+            if (__all_sync(kFull, tru)) { good = true; break; }
         }
+        // symbols of each true span [sync_l, sync_{l+1})
+        const uint32_t nsync = __shfl_down_sync(kFull, sync, 1);
         const uint32_t last_e = __shfl_sync(kFull, e, L - 1);
-        uint32_t nsym_l = 0;
+        uint32_t nl = 0, ce = B;
         if (active) {
-            const uint32_t rel = cstart - s;   // < 64 when synchronised
-            nsym_l = k - (rel ? __popcll(mask & ((1ull << rel) - 1)) : 0);
+            nl = kpre - wa.below(sync - start);
+            if (lane + 1 < L) {
+                ce = nsync;
+                nl += wb.below(nsync - s_next);
+            }
         }
         int total;
-        const uint32_t o = (uint32_t)warp_excl_scan((int)nsym_l, &total);
+        const uint32_t o = (uint32_t)warp_excl_scan((int)nl, &total);
         if (!good || last_e != B || (uint32_t)total != cnt) {
             if (lane == 0) redo[c] = 1;
             continue;
         }
-        // phase 3: decode the true span [cstart, e) and store nsym_l codes at o
+        // phase 3: decode each true span again and store its codes at o
         bool ok3 = true;
         uint32_t zeros = 0;
-        if (active && nsym_l) ok3 = decode_store(d, sbit, cstart, e, nsym_l, out + base + o, zeros);
+        if (active && nl) ok3 = decode_store(d, sbit, sync, ce, nl, out + base + o, zeros);
         if (!__all_sync(kFull, ok3)) {
             if (lane == 0) redo[c] = 1;
             continue;
