@@ -80,6 +80,9 @@ SDQZ_API uint64_t sdqz_kernel_launches(const sdqz_ctx* ctx);
  * "name=ms;name=ms;..." (NUL-terminated, truncated to len) and returns the
  * untruncated length. */
 SDQZ_API int sdqz_set_timing(sdqz_ctx* ctx, int on);
+/* Diagnostics of the last call (inflate: lane redecodes, unsynchronised
+ * chunks, chunks decoded by the sequential path). */
+SDQZ_API int sdqz_debug_counters(sdqz_ctx* ctx, uint64_t* out, int n);
 SDQZ_API int sdqz_kernel_times(sdqz_ctx* ctx, char* buf, uint64_t len);
 
 /* ---- L1: field description (core.py:136-175) ---------------------------- */

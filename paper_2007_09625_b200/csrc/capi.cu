@@ -335,6 +335,12 @@ const char* sdqz_last_error(const sdqz_ctx* ctx) { return ctx ? ctx->err.c_str()
 
 uint64_t sdqz_kernel_launches(const sdqz_ctx* ctx) { return ctx ? ctx->launches : 0; }
 
+int sdqz_debug_counters(sdqz_ctx* ctx, uint64_t* out, int n) {
+    const unsigned long long* p = ctx->h_status->pad;
+    for (int i = 0; i < n && i < 3; i++) out[i] = p[i];
+    return SDQZ_OK;
+}
+
 int sdqz_set_timing(sdqz_ctx* ctx, int on) {
     cudaStreamSynchronize(ctx->stream);
     ctx->marks.clear();

@@ -399,7 +399,20 @@ __global__ void lut_kernel(const uint64_t* __restrict__ first, const int64_t* __
                     found = true;
                 }
             }
-            if (!found) e = (lb == mx) ? (255u << 16) : 0u;
+            if (!found && lb == mx) {
+                e = 255u << 16;
+            } else if (!found) {
+                // longer than the LUT: record the shortest width any codeword
+                // with this prefix can have, so the decoder's canonical search
+                // starts there (len field 0, hint in the symbol field)
+                const unsigned long long pmin = (unsigned long long)i << (mx - lb);
+                uint32_t b0 = (uint32_t)mx + 1;
+                for (int b = lb + 1; b <= mx; b++) {
+                    const unsigned long long cnt = (unsigned long long)(offsets[b + 1] - offsets[b]);
+                    if (pmin < ((first[b] + cnt) << (mx - b))) { b0 = (uint32_t)b; break; }
+                }
+                e = b0;
+            }
         }
         lut[i] = e;
     }
@@ -1066,6 +1079,7 @@ __global__ void __launch_bounds__(64) inflate_kernel(
     const long long nsym = offs[mx + 1];
     uint32_t zeros = 0;
     if (c < nchunks && (!only || only[c])) {
+        if (only) atomicAdd(&st->pad[2], 1ull);   // diagnostics: chunks handed back
         const uint32_t* words = reinterpret_cast<const uint32_t*>(payload);
         const uint64_t sbit = byte_off[c] * 8;
         const uint32_t budget = chunk_bits[c];
@@ -1184,8 +1198,9 @@ struct DecodeTables {
 // canonical decode (huffman.py:295-305) of a codeword longer than the LUT from
 // a left-aligned `mx`-bit peek; shared tables only.  Returns sym | len << 16
 // (len 255: no codeword of any width matches).
-__device__ __forceinline__ uint32_t long_from_peek(const DecodeTables& d, unsigned long long peek) {
-    for (int b = d.lb + 1; b <= d.mx; b++) {
+__device__ __forceinline__ uint32_t long_from_peek(const DecodeTables& d, unsigned long long peek,
+                                                   int b0) {
+    for (int b = b0; b <= d.mx; b++) {
         if (peek < dl_lim[b]) {
             const unsigned long long top = peek >> (d.mx - b);
             long long idx = dl_offs[b] + (long long)(top - dl_first[b]);
@@ -1232,7 +1247,7 @@ __device__ __forceinline__ uint32_t decode_one(const DecodeTables& d, BitReader&
     asm("ld.shared.u32 %0, [%1];" : "=r"(e) : "r"(d.lut_s + ((uint32_t)(rd.buf >> (64 - d.lb)) << 2)));
     if ((e & 0xFF0000u) == 0) {   // longer than the LUT
         // after refill the window holds >= 33 valid bits: enough for mx <= 32
-        e = d.mx <= 32 ? long_from_peek(d, rd.buf >> (64 - d.mx))
+        e = d.mx <= 32 ? long_from_peek(d, rd.buf >> (64 - d.mx), (int)(e & 0xFFFF))
                        : long_codeword(d.words, d.nwords, d.symbols, d.nsym, d.lb, d.mx, p);
     }
     const uint32_t len = (e >> 16) & 0xFF;
@@ -1363,6 +1378,160 @@ __device__ __forceinline__ bool decode_store(const DecodeTables& d, uint64_t sbi
     return ok && pos == end;
 }
 
+// ---- lean branch-free reader for the warp decoder -------------------------
+// 64-bit left-aligned window + one preloaded next word.  The refill is
+// predicated (no divergence when lanes refill at different symbols) and the
+// next word's load is issued ~10 codewords before it is consumed.
+struct LeanReader {
+    const uint32_t* w;
+    uint64_t last;                 // last readable word index
+    uint64_t wi;                   // index of the word in `nxt`
+    unsigned long long buf;
+    int nb;
+    uint32_t nxt;
+
+    __device__ __forceinline__ uint32_t ldw(uint64_t i) const {
+        return bswap32(__ldg(w + (i < last ? i : last)));
+    }
+    __device__ __forceinline__ void init(uint64_t bit) {
+        const uint64_t i = bit >> 5;
+        const uint32_t sh = (uint32_t)(bit & 31);
+        buf = (((unsigned long long)ldw(i) << 32) | ldw(i + 1)) << sh;
+        nb = 64 - (int)sh;
+        wi = i + 2;
+        nxt = ldw(wi);
+    }
+    __device__ __forceinline__ void refill() {
+        const bool need = nb <= 32;
+        const uint32_t sft = (uint32_t)(32 - nb) & 63;
+        buf |= need ? ((unsigned long long)nxt << sft) : 0ull;
+        nb += need ? 32 : 0;
+        wi += need ? 1 : 0;
+        uint32_t v = nxt;
+        const uint32_t* p = w + (wi < last ? wi : last);
+        asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.u32 q, %2, 0;\n\t@q ld.global.nc.u32 %0, [%1];\n\t}"
+                     : "+r"(v)
+                     : "l"(p), "r"((uint32_t)need));
+        nxt = need ? bswap32(v) : nxt;
+    }
+};
+
+// One codeword at relative position `pos` (absolute bit sbit + pos).  Returns
+// sym | len << 16 with len in 1..56, or len 255 for an invalid pattern (the
+// reader then advances one bit so loops stay bounded; the caller discards).
+__device__ __forceinline__ uint32_t lean_step(const DecodeTables& d, LeanReader& rd, uint64_t abs) {
+    rd.refill();
+    uint32_t e;
+    asm("ld.shared.u32 %0, [%1];" : "=r"(e) : "r"(d.lut_s + ((uint32_t)(rd.buf >> (64 - d.lb)) << 2)));
+    if ((e & 0xFF0000u) == 0) {   // longer than the LUT (rare, hint in the low bits)
+        e = d.mx <= 32 ? long_from_peek(d, rd.buf >> (64 - d.mx), (int)(e & 0xFFFF))
+                       : long_codeword(d.words, d.nwords, d.symbols, d.nsym, d.lb, d.mx, abs);
+    }
+    uint32_t len = (e >> 16) & 0xFF;
+    const uint32_t adv = len == 255 ? 1u : len;
+    if ((int)adv <= rd.nb) {
+        rd.buf <<= adv;
+        rd.nb -= (int)adv;
+    } else {
+        rd.init(abs + adv);   // only after a codeword wider than 32 bits
+    }
+    return (e & 0xFFFF) | (len << 16);
+}
+
+// Phase 1 of a lane: decode [start, stop2); record boundaries of the first
+// 128 bits (wa) and of [stop, stop+128) (wb), codewords starting before
+// stop (kpre) and the first boundary >= stop (exit).
+__device__ __noinline__ bool lean_window(const DecodeTables& d, uint64_t sbit, uint32_t start,
+                                         uint32_t stop, uint32_t stop2, uint32_t* exit_pos,
+                                         uint32_t* kpre, Win128* wa, Win128* wb) {
+    LeanReader rd;
+    rd.w = d.words;
+    rd.last = d.nwords - 1;
+    rd.init(sbit + start);
+    uint32_t pos = start, k = 0;
+    unsigned long long alo = 0, ahi = 0, blo = 0, bhi = 0;
+    bool ok = true;
+    // head: boundaries relative to start (first 128 bits, never past stop)
+    const uint32_t hend = start + 128 < stop ? start + 128 : stop;
+    while (pos < hend) {
+        const uint32_t r = pos - start;
+        alo |= r < 64 ? (1ull << (r & 63)) : 0ull;
+        ahi |= r >= 64 ? (1ull << (r & 63)) : 0ull;
+        const uint32_t e = lean_step(d, rd, sbit + pos);
+        ok &= (e >> 16) != 255;
+        pos += (e >> 16) == 255 ? 1u : (e >> 16);
+        k++;
+    }
+    // body
+    while (pos < stop) {
+        const uint32_t e = lean_step(d, rd, sbit + pos);
+        ok &= (e >> 16) != 255;
+        pos += (e >> 16) == 255 ? 1u : (e >> 16);
+        k++;
+    }
+    const uint32_t ex = pos;
+    // tail window [stop, stop2)
+    while (pos < stop2) {
+        const uint32_t r = pos - stop;
+        blo |= r < 64 ? (1ull << (r & 63)) : 0ull;
+        bhi |= (r >= 64 && r < 128) ? (1ull << (r & 63)) : 0ull;
+        const uint32_t e = lean_step(d, rd, sbit + pos);
+        ok &= (e >> 16) != 255;
+        pos += (e >> 16) == 255 ? 1u : (e >> 16);
+    }
+    *exit_pos = ex;
+    *kpre = k;
+    wa->lo = alo;
+    wa->hi = ahi;
+    wb->lo = blo;
+    wb->hi = bhi;
+    return ok;
+}
+
+// Phase 3 of a lane: decode `count` codewords from `start` (must end exactly
+// at `end`) and store them at dst; 16-byte stores once 8-code aligned.
+__device__ __noinline__ bool lean_store(const DecodeTables& d, uint64_t sbit, uint32_t start,
+                                        uint32_t end, uint32_t count, uint16_t* dst,
+                                        uint32_t* zeros_out) {
+    LeanReader rd;
+    rd.w = d.words;
+    rd.last = d.nwords - 1;
+    rd.init(sbit + start);
+    uint32_t pos = start, j = 0, zeros = 0;
+    bool ok = true;
+    const uint32_t head = (uint32_t)umin((8 - (((uintptr_t)dst >> 1) & 7)) & 7, count);
+    for (; j < head; j++) {
+        const uint32_t e = lean_step(d, rd, sbit + pos);
+        ok &= (e >> 16) != 255;
+        pos += (e >> 16) == 255 ? 1u : (e >> 16);
+        dst[j] = (uint16_t)e;
+        zeros += (e & 0xFFFF) == 0;
+    }
+    for (; j + 8 <= count; j += 8) {
+        unsigned long long acc0 = 0, acc1 = 0;
+        for (int t = 0; t < 8; t++) {
+            const uint32_t e = lean_step(d, rd, sbit + pos);
+            ok &= (e >> 16) != 255;
+            pos += (e >> 16) == 255 ? 1u : (e >> 16);
+            const unsigned long long s = e & 0xFFFF;
+            zeros += s == 0;
+            acc0 |= t < 4 ? (s << (16 * (t & 3))) : 0ull;
+            acc1 |= t >= 4 ? (s << (16 * (t & 3))) : 0ull;
+        }
+        *reinterpret_cast<uint4*>(dst + j) =
+            make_uint4((uint32_t)acc0, (uint32_t)(acc0 >> 32), (uint32_t)acc1, (uint32_t)(acc1 >> 32));
+    }
+    for (; j < count; j++) {
+        const uint32_t e = lean_step(d, rd, sbit + pos);
+        ok &= (e >> 16) != 255;
+        pos += (e >> 16) == 255 ? 1u : (e >> 16);
+        dst[j] = (uint16_t)e;
+        zeros += (e & 0xFFFF) == 0;
+    }
+    *zeros_out += zeros;
+    return ok && pos == end;
+}
+
 constexpr uint32_t kMinSliceBits = 128;
 
 __global__ void __launch_bounds__(256) inflate_warp_kernel(
@@ -1419,7 +1588,7 @@ __global__ void __launch_bounds__(256) inflate_warp_kernel(
         uint32_t start = s0, e = B, kpre = 0;
         Win128 wa{0, 0}, wb{0, 0};
         bool ok = true;
-        if (active) ok = decode_window(d, sbit, start, s_next, stop2, e, kpre, wa, wb);
+        if (active) ok = lean_window(d, sbit, start, s_next, stop2, &e, &kpre, &wa, &wb);
         // phase 2: truth propagates from lane 0.  A lane whose predecessor is
         // true synchronises at the first boundary both paths share inside the
         // window (a true boundary); failing that, it redecodes from the
@@ -1444,14 +1613,16 @@ __global__ void __launch_bounds__(256) inflate_warp_kernel(
                 } else if (pe < s_next) {
                     start = pe;
                     sync = pe;
-                    ok = decode_window(d, sbit, start, s_next, stop2, e, kpre, wa, wb);
+                    ok = lean_window(d, sbit, start, s_next, stop2, &e, &kpre, &wa, &wb);
                     tru = ok;
+                    atomicAdd(&st->pad[0], 1ull);   // diagnostics: lane redecodes
                 } else {
                     ok = false;
                 }
             }
             if (__all_sync(kFull, tru)) { good = true; break; }
         }
+        if (lane == 0 && !good) atomicAdd(&st->pad[1], 1ull);
         // symbols of each true span [sync_l, sync_{l+1})
         const uint32_t nsync = __shfl_down_sync(kFull, sync, 1);
         const uint32_t last_e = __shfl_sync(kFull, e, L - 1);
@@ -1472,7 +1643,7 @@ __global__ void __launch_bounds__(256) inflate_warp_kernel(
         // phase 3: decode each true span again and store its codes at o
         bool ok3 = true;
         uint32_t zeros = 0;
-        if (active && nl) ok3 = decode_store(d, sbit, sync, ce, nl, out + base + o, zeros);
+        if (active && nl) ok3 = lean_store(d, sbit, sync, ce, nl, out + base + o, &zeros);
         if (!__all_sync(kFull, ok3)) {
             if (lane == 0) redo[c] = 1;
             continue;
