@@ -204,6 +204,7 @@ def algorithmic_bytes(kernel: str, n: int, k: int, c: int, p: int) -> int | None
         "dq3d": 6 * n, "dq2d": 6 * n, "dq1d": 6 * n, "dualquant": 6 * n,
         "chunk_stats_kernel": 2 * n + 4 * c,
         "chunk_pack_kernel": 2 * n + p + 16 * k + 4 * k + 8 * c,
+        "inflate_warp_kernel": p + 4 * c + 8 * c + 2 * n,
         "inflate_kernel": p + 4 * c + 8 * c + 2 * n,
         "rq_fast": 2 * n + 4 * n + 8 * k,
         "outlier_scatter_kernel": 16 * k + 8 * k + 2 * k,

@@ -183,7 +183,7 @@ def decompress(blob: bytes, workers: int | None = None) -> np.ndarray:
     except SdqzError as e:
         _rewrite_geometry_error(e, blob)
         raise
-    return t.cpu().numpy()
+    return _device.download(t)
 
 
 def _rewrite_geometry_error(e, blob):
@@ -226,7 +226,7 @@ def decompress_archive(ar: Archive, workers: int | None = None) -> np.ndarray:
     _lib.context().call("sdqz_decompress_sections", ctypes.byref(ch), _lib.ptr(d_bw),
                         _lib.ptr(d_rec), _lib.ptr(d_cb), _lib.ptr(d_pay), _lib.ptr(o))
     del torch
-    return o.view(*_dims_of(ch)).cpu().numpy()
+    return _device.download(o.view(*_dims_of(ch)))
 
 
 __all__ = ["compress", "decompress", "decompress_archive", "compress_device",
