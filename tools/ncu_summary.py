@@ -30,7 +30,7 @@ for r in rows[2:]:
         v = float(r[i].replace(",", "")) if r[i] else 0.0
         return v * SCALE.get(units[i], 1)
     name = r[h.index("Kernel Name")].replace("(anonymous namespace)::", "").split("(")[0]
-    name = name.replace("void ", "").replace("sdqz::", "").replace("<unnamed>::", "")
+    name = name.replace("void ", "").replace("sdqz::", "").replace("<unnamed>::", "").replace("unnamed>::", "")
     dur = g(M[0])
     rd, wr = g(M[1]), g(M[2])
     lines.append(f"{name} | {dur*1e6:.1f} | {rd/1e6:.1f} | {wr/1e6:.1f} | {g(M[3]):.1f} | {g(M[4]):.1f} | "
