@@ -11,7 +11,7 @@ agg = collections.defaultdict(list)
 for r in rows[hi + 1:]:
     if len(r) <= vi:
         continue
-    name = r[ki].replace('void ', '').replace('sdqz::', '').replace('<', '').split('(')[0]
+    name = r[ki].replace('void ', '').replace('sdqz::', '').replace('<unnamed>::', '').replace('unnamed>::', '').split('(')[0]
     v = float(r[vi].replace(',', ''))
     scale = {'ns': 1e-3, 'nsecond': 1e-3, 'us': 1, 'usecond': 1, 'ms': 1e3, 'msecond': 1e3}[r[ui]]
     agg[name].append(v * scale)
