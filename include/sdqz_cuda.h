@@ -143,6 +143,14 @@ SDQZ_API int sdqz_deflate_units(sdqz_ctx* ctx, const void* d_units, int unit_wid
                        uint32_t chunk, uint32_t* d_chunk_bits, uint8_t* d_payload,
                        uint64_t payload_cap, uint64_t* payload_bytes);
 
+/* encode + deflate (huffman.py:193-269) of uint16 codes with a packed codebook
+ * (d_entries uint64[cap] from sdqz_canonize): the fused path's K4 without the
+ * outlier compaction.  Used per shard by the multi-GPU compress. */
+SDQZ_API int sdqz_encode_deflate(sdqz_ctx* ctx, const uint16_t* d_codes, uint64_t n,
+                        const uint64_t* d_entries, uint32_t cap, uint32_t chunk,
+                        uint32_t* d_chunk_bits, uint8_t* d_payload, uint64_t payload_cap,
+                        uint64_t* payload_bytes);
+
 /* inflate (huffman.py:311-356) with the canonical reverse tables. */
 SDQZ_API int sdqz_inflate(sdqz_ctx* ctx, const uint8_t* d_payload, uint64_t payload_bytes,
                  const uint32_t* d_chunk_bits, uint64_t n_chunks, uint32_t chunk,

@@ -67,6 +67,8 @@ _SIGS = {
                                 c_void_p]),
     "sdqz_deflate_units": (c_int, [c_void_p, c_void_p, c_int, c_uint64, c_uint32, c_void_p,
                                    c_void_p, c_uint64, POINTER(c_uint64)]),
+    "sdqz_encode_deflate": (c_int, [c_void_p, c_void_p, c_uint64, c_void_p, c_uint32, c_uint32,
+                                    c_void_p, c_void_p, c_uint64, POINTER(c_uint64)]),
     "sdqz_inflate": (c_int, [c_void_p, c_void_p, c_uint64, c_void_p, c_uint64, c_uint32,
                              c_void_p, c_void_p, c_void_p, c_int, c_uint64, c_void_p]),
     "sdqz_compress": (c_int, [c_void_p, c_void_p, c_int, c_int, POINTER(c_uint64),

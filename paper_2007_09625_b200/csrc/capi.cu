@@ -563,6 +563,35 @@ int sdqz_deflate_units(sdqz_ctx* ctx, const void* d_units, int unit_width, uint6
     return SDQZ_OK;
 }
 
+int sdqz_encode_deflate(sdqz_ctx* ctx, const uint16_t* d_codes, uint64_t n, const uint64_t* d_entries,
+                        uint32_t cap, uint32_t chunk, uint32_t* d_chunk_bits, uint8_t* d_payload,
+                        uint64_t payload_cap, uint64_t* payload_bytes) {
+    int rc;
+    *payload_bytes = 0;
+    if (chunk < 1) return set_error(ctx, SDQZ_EINVAL, "chunk_size must be >= 1");
+    if (!valid_cap(cap)) return set_error(ctx, SDQZ_EINVAL, "bad cap");
+    if (n == 0) return SDQZ_OK;
+    if ((rc = reset_status(ctx))) return rc;
+    DeflateJob job;
+    job.codes = d_codes;
+    job.n = n;
+    job.chunk = chunk;
+    job.entries = d_entries;
+    job.cap = cap;
+    job.chunk_bits = d_chunk_bits;
+    job.payload = d_payload;
+    job.payload_cap = payload_cap;
+    if ((rc = launch_deflate(ctx, job))) return rc;
+    if ((rc = fetch_status(ctx))) return rc;
+    const DevStatus& s = *ctx->h_status;
+    if (s.flags & F_CODE_RANGE) return set_error(ctx, SDQZ_ECORRUPT, fmt("quantization code outside [0, %u)", cap));
+    if (s.flags & F_ABSENT_SYM)
+        return set_error(ctx, SDQZ_ECORRUPT, "code has no codebook entry (zero frequency at build time)");
+    if (s.flags & F_OVERFLOW) return set_error(ctx, SDQZ_EINVAL, "payload capacity exceeded");
+    *payload_bytes = s.payload_bytes;
+    return SDQZ_OK;
+}
+
 int sdqz_inflate(sdqz_ctx* ctx, const uint8_t* d_payload, uint64_t payload_bytes,
                  const uint32_t* d_chunk_bits, uint64_t n_chunks, uint32_t chunk,
                  const uint64_t* d_first, const int64_t* d_offsets, const uint32_t* d_symbols,
