@@ -1159,501 +1159,6 @@ __global__ void __launch_bounds__(64) inflate_kernel(
     if (lane_id() == 0 && zeros) atomicAdd(&st->n_zero, (unsigned long long)zeros);
 }
 
-// --------------------------------------------------------------------------
-// K5': warp-parallel inflate of one chunk (self-synchronising decode).
-//
-// The archive fixes ~1e4-6e4 chunks (huffman.py:206-212), too few threads for
-// a thread-per-chunk decoder.  Here a warp splits chunk c's bit range into L
-// lane slices.  Phase 1: each lane decodes from its slice start (usually
-// mid-codeword) to the first codeword boundary at/after the next slice start
-// (its exit), remembering which bit offsets within 64 bits of its start were
-// codeword boundaries.  Phase 2: lane 0 started at a true boundary; lane l is
-// synchronised when lane l-1's exit is one of its recorded boundaries (from
-// there on both decodes coincide, so lane l's exit is a true boundary too).
-// Unsynchronised lanes redo from their predecessor's exit until the whole
-// warp is consistent.  Phase 3: a prefix sum of per-lane symbol counts gives
-// output offsets and every lane decodes its true span again, storing codes.
-// Anything unusual (short chunks, invalid bit patterns, count or length
-// mismatch) hands the chunk to the sequential decoder, which reproduces the
-// reference's exact error semantics.
-// --------------------------------------------------------------------------
-// decode tables of the warp decoder: file-scope shared arrays, so every
-// access compiles to LDS (no generic-pointer address conversion per symbol)
-__shared__ uint32_t dl_lut[1 << kLutBits];
-__shared__ unsigned long long dl_first[58];
-__shared__ long long dl_offs[59];
-__shared__ unsigned long long dl_lim[58];     // (first[b] + count[b]) << (mx - b)
-constexpr uint32_t kSymSmem = 8192;
-__shared__ uint16_t dl_sym[kSymSmem];         // symbols by (width, symbol), if they fit
-
-struct DecodeTables {
-    uint32_t lut_s;                      // shared-space address of dl_lut
-    const uint32_t* symbols;
-    const uint32_t* words;
-    uint64_t nwords;
-    long long nsym;
-    int lb, mx;
-};
-
-// canonical decode (huffman.py:295-305) of a codeword longer than the LUT from
-// a left-aligned `mx`-bit peek; shared tables only.  Returns sym | len << 16
-// (len 255: no codeword of any width matches).
-__device__ __forceinline__ uint32_t long_from_peek(const DecodeTables& d, unsigned long long peek,
-                                                   int b0) {
-    for (int b = b0; b <= d.mx; b++) {
-        if (peek < dl_lim[b]) {
-            const unsigned long long top = peek >> (d.mx - b);
-            long long idx = dl_offs[b] + (long long)(top - dl_first[b]);
-            if (idx < 0) idx = 0;
-            if (idx >= d.nsym) idx = d.nsym ? d.nsym - 1 : 0;
-            const uint32_t sym = d.nsym <= (long long)kSymSmem ? dl_sym[idx] : d.symbols[idx];
-            return (sym & 0xFFFF) | ((uint32_t)b << 16);
-        }
-    }
-    return 255u << 16;
-}
-
-// canonical decode of a codeword longer than the LUT; returns sym | len << 16
-// (len 255: no codeword of any width matches)
-__device__ __forceinline__ uint32_t long_codeword(const uint32_t* words, uint64_t nwords,
-                                                  const uint32_t* symbols, long long nsym, int lb,
-                                                  int mx, uint64_t p) {
-    const uint64_t pw = p >> 5;
-    const uint32_t ps = (uint32_t)(p & 31);
-    const unsigned long long hi64 = ((unsigned long long)load_be(words, pw, nwords) << 32) |
-                                    load_be(words, pw + 1, nwords);
-    const uint32_t w2 = load_be(words, pw + 2, nwords);
-    const unsigned long long peek64 = ps ? ((hi64 << ps) | (w2 >> (32 - ps))) : hi64;
-    const unsigned long long peek = peek64 >> (64 - mx);
-    for (int b = lb + 1; b <= mx; b++) {
-        const unsigned long long top = peek >> (mx - b);
-        const unsigned long long cntb = (unsigned long long)(dl_offs[b + 1] - dl_offs[b]);
-        if (top < dl_first[b] + cntb) {
-            long long idx = dl_offs[b] + (long long)(top - dl_first[b]);
-            if (idx < 0) idx = 0;
-            if (idx >= nsym) idx = nsym ? nsym - 1 : 0;
-            return (symbols[idx] & 0xFFFF) | ((uint32_t)b << 16);
-        }
-    }
-    return 255u << 16;
-}
-
-// one codeword at absolute bit `p` (the reader's position); 255 = invalid
-__device__ __forceinline__ uint32_t decode_one(const DecodeTables& d, BitReader& rd, uint64_t p,
-                                               uint32_t& sym) {
-    rd.refill();
-    // explicit 32-bit shared address: keeps the shared-window base out of the loop
-    uint32_t e;
-    asm("ld.shared.u32 %0, [%1];" : "=r"(e) : "r"(d.lut_s + ((uint32_t)(rd.buf >> (64 - d.lb)) << 2)));
-    if ((e & 0xFF0000u) == 0) {   // longer than the LUT
-        // after refill the window holds >= 33 valid bits: enough for mx <= 32
-        e = d.mx <= 32 ? long_from_peek(d, rd.buf >> (64 - d.mx), (int)(e & 0xFFFF))
-                       : long_codeword(d.words, d.nwords, d.symbols, d.nsym, d.lb, d.mx, p);
-    }
-    const uint32_t len = (e >> 16) & 0xFF;
-    sym = e & 0xFFFF;
-    if (len != 255) {
-        if ((int)len <= rd.nb) rd.skip(len);
-        else rd.init(p + len);
-    }
-    return len;
-}
-
-// decode from `start` (relative) until the position reaches `stop`; records
-// boundaries within [start, start + 64) in `mask`; returns false on an invalid pattern
-__device__ __forceinline__ bool decode_span(const DecodeTables& d, uint64_t sbit, uint32_t start,
-                                            uint32_t stop, uint32_t& exit_pos, uint32_t& count,
-                                            unsigned long long& mask) {
-    BitReader rd;
-    rd.blk = reinterpret_cast<const uint4*>(d.words);
-    rd.nblk = d.nwords / 4;
-    rd.init(sbit + start);
-    uint32_t pos = start, k = 0;
-    unsigned long long m = 0;
-    bool ok = true;
-    while (pos < stop) {
-        const uint32_t rel = pos - start;
-        if (rel < 64) m |= 1ull << rel;
-        uint32_t sym;
-        const uint32_t len = decode_one(d, rd, sbit + pos, sym);
-        if (len == 255) { ok = false; break; }
-        pos += len;
-        k++;
-    }
-    exit_pos = pos;
-    count = k;
-    mask = m;
-    return ok;
-}
-
-// 128-bit boundary window (two u64 halves)
-struct Win128 {
-    unsigned long long lo, hi;
-    __device__ __forceinline__ void set(uint32_t r) {
-        if (r < 64) lo |= 1ull << r;
-        else if (r < 128) hi |= 1ull << (r - 64);
-    }
-    __device__ __forceinline__ uint32_t below(uint32_t r) const {   // set bits in [0, r)
-        if (r == 0) return 0;
-        if (r <= 64) return __popcll(r == 64 ? lo : (lo & ((1ull << r) - 1)));
-        return __popcll(lo) + __popcll(hi & ((1ull << (r - 64)) - 1));
-    }
-};
-
-// Phase-1 decode of one lane slice [start, stop), continued to stop2 (the
-// 128-bit synchronisation window of the next slice).  wa: boundaries in
-// [start, start+128); wb: boundaries in [stop, stop+128); kpre: codewords
-// starting before stop; exit: first boundary >= stop.
-__device__ __forceinline__ bool decode_window(const DecodeTables& d, uint64_t sbit, uint32_t start,
-                                              uint32_t stop, uint32_t stop2, uint32_t& exit_pos,
-                                              uint32_t& kpre, Win128& wa, Win128& wb) {
-    BitReader rd;
-    rd.blk = reinterpret_cast<const uint4*>(d.words);
-    rd.nblk = d.nwords / 4;
-    rd.init(sbit + start);
-    uint32_t pos = start, k = 0, ex = 0;
-    wa.lo = wa.hi = wb.lo = wb.hi = 0;
-    bool ok = true, have = false;
-    while (pos < stop2) {
-        wa.set(pos - start);
-        if (pos >= stop) {
-            if (!have) { ex = pos; have = true; }
-            wb.set(pos - stop);
-        } else {
-            k++;
-        }
-        uint32_t sym;
-        const uint32_t len = decode_one(d, rd, sbit + pos, sym);
-        if (len == 255) { ok = false; break; }
-        pos += len;
-    }
-    exit_pos = have ? ex : pos;
-    kpre = k;
-    return ok;
-}
-
-// Decode `count` codewords from relative bit `start`, which must end exactly
-// at `end`; store them at dst (16-byte stores once 8-code aligned).
-__device__ __forceinline__ bool decode_store(const DecodeTables& d, uint64_t sbit, uint32_t start,
-                                             uint32_t end, uint32_t count, uint16_t* dst,
-                                             uint32_t& zeros) {
-    BitReader rd;
-    rd.blk = reinterpret_cast<const uint4*>(d.words);
-    rd.nblk = d.nwords / 4;
-    rd.init(sbit + start);
-    uint32_t pos = start, j = 0;
-    bool ok = true;
-    const uint32_t head = (uint32_t)umin((8 - (((uintptr_t)dst >> 1) & 7)) & 7, count);
-    for (; j < head; j++) {
-        uint32_t sym;
-        const uint32_t len = decode_one(d, rd, sbit + pos, sym);
-        if (len == 255) { ok = false; break; }
-        pos += len;
-        dst[j] = (uint16_t)sym;
-        zeros += sym == 0;
-    }
-    for (; ok && j + 8 <= count; j += 8) {
-        unsigned long long acc0 = 0, acc1 = 0;
-#pragma unroll
-        for (int t = 0; t < 8; t++) {
-            uint32_t sym;
-            const uint32_t len = decode_one(d, rd, sbit + pos, sym);
-            ok &= len != 255;
-            pos += len;
-            zeros += sym == 0;
-            if (t < 4) acc0 |= (unsigned long long)sym << (16 * t);
-            else acc1 |= (unsigned long long)sym << (16 * (t - 4));
-        }
-        *reinterpret_cast<uint4*>(dst + j) =
-            make_uint4((uint32_t)acc0, (uint32_t)(acc0 >> 32), (uint32_t)acc1, (uint32_t)(acc1 >> 32));
-    }
-    for (; ok && j < count; j++) {
-        uint32_t sym;
-        const uint32_t len = decode_one(d, rd, sbit + pos, sym);
-        if (len == 255) { ok = false; break; }
-        pos += len;
-        dst[j] = (uint16_t)sym;
-        zeros += sym == 0;
-    }
-    return ok && pos == end;
-}
-
-// ---- lean branch-free reader for the warp decoder -------------------------
-// 64-bit left-aligned window + one preloaded next word.  The refill is
-// predicated (no divergence when lanes refill at different symbols) and the
-// next word's load is issued ~10 codewords before it is consumed.
-struct LeanReader {
-    const uint32_t* w;
-    uint64_t last;                 // last readable word index
-    uint64_t wi;                   // index of the word in `nxt`
-    unsigned long long buf;
-    int nb;
-    uint32_t nxt;
-
-    __device__ __forceinline__ uint32_t ldw(uint64_t i) const {
-        return bswap32(__ldg(w + (i < last ? i : last)));
-    }
-    __device__ __forceinline__ void init(uint64_t bit) {
-        const uint64_t i = bit >> 5;
-        const uint32_t sh = (uint32_t)(bit & 31);
-        buf = (((unsigned long long)ldw(i) << 32) | ldw(i + 1)) << sh;
-        nb = 64 - (int)sh;
-        wi = i + 2;
-        nxt = ldw(wi);
-    }
-    __device__ __forceinline__ void refill() {
-        const bool need = nb <= 32;
-        const uint32_t sft = (uint32_t)(32 - nb) & 63;
-        buf |= need ? ((unsigned long long)nxt << sft) : 0ull;
-        nb += need ? 32 : 0;
-        wi += need ? 1 : 0;
-        uint32_t v = nxt;
-        const uint32_t* p = w + (wi < last ? wi : last);
-        asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.u32 q, %2, 0;\n\t@q ld.global.nc.u32 %0, [%1];\n\t}"
-                     : "+r"(v)
-                     : "l"(p), "r"((uint32_t)need));
-        nxt = need ? bswap32(v) : nxt;
-    }
-};
-
-// One codeword at relative position `pos` (absolute bit sbit + pos).  Returns
-// sym | len << 16 with len in 1..56, or len 255 for an invalid pattern (the
-// reader then advances one bit so loops stay bounded; the caller discards).
-__device__ __forceinline__ uint32_t lean_step(const DecodeTables& d, LeanReader& rd, uint64_t abs) {
-    rd.refill();
-    uint32_t e;
-    asm("ld.shared.u32 %0, [%1];" : "=r"(e) : "r"(d.lut_s + ((uint32_t)(rd.buf >> (64 - d.lb)) << 2)));
-    if ((e & 0xFF0000u) == 0) {   // longer than the LUT (rare, hint in the low bits)
-        e = d.mx <= 32 ? long_from_peek(d, rd.buf >> (64 - d.mx), (int)(e & 0xFFFF))
-                       : long_codeword(d.words, d.nwords, d.symbols, d.nsym, d.lb, d.mx, abs);
-    }
-    uint32_t len = (e >> 16) & 0xFF;
-    const uint32_t adv = len == 255 ? 1u : len;
-    if ((int)adv <= rd.nb) {
-        rd.buf <<= adv;
-        rd.nb -= (int)adv;
-    } else {
-        rd.init(abs + adv);   // only after a codeword wider than 32 bits
-    }
-    return (e & 0xFFFF) | (len << 16);
-}
-
-// Phase 1 of a lane: decode [start, stop2); record boundaries of the first
-// 128 bits (wa) and of [stop, stop+128) (wb), codewords starting before
-// stop (kpre) and the first boundary >= stop (exit).
-__device__ __noinline__ bool lean_window(const DecodeTables& d, uint64_t sbit, uint32_t start,
-                                         uint32_t stop, uint32_t stop2, uint32_t* exit_pos,
-                                         uint32_t* kpre, Win128* wa, Win128* wb) {
-    LeanReader rd;
-    rd.w = d.words;
-    rd.last = d.nwords - 1;
-    rd.init(sbit + start);
-    uint32_t pos = start, k = 0;
-    unsigned long long alo = 0, ahi = 0, blo = 0, bhi = 0;
-    bool ok = true;
-    // head: boundaries relative to start (first 128 bits, never past stop)
-    const uint32_t hend = start + 128 < stop ? start + 128 : stop;
-    while (pos < hend) {
-        const uint32_t r = pos - start;
-        alo |= r < 64 ? (1ull << (r & 63)) : 0ull;
-        ahi |= r >= 64 ? (1ull << (r & 63)) : 0ull;
-        const uint32_t e = lean_step(d, rd, sbit + pos);
-        ok &= (e >> 16) != 255;
-        pos += (e >> 16) == 255 ? 1u : (e >> 16);
-        k++;
-    }
-    // body
-    while (pos < stop) {
-        const uint32_t e = lean_step(d, rd, sbit + pos);
-        ok &= (e >> 16) != 255;
-        pos += (e >> 16) == 255 ? 1u : (e >> 16);
-        k++;
-    }
-    const uint32_t ex = pos;
-    // tail window [stop, stop2)
-    while (pos < stop2) {
-        const uint32_t r = pos - stop;
-        blo |= r < 64 ? (1ull << (r & 63)) : 0ull;
-        bhi |= (r >= 64 && r < 128) ? (1ull << (r & 63)) : 0ull;
-        const uint32_t e = lean_step(d, rd, sbit + pos);
-        ok &= (e >> 16) != 255;
-        pos += (e >> 16) == 255 ? 1u : (e >> 16);
-    }
-    *exit_pos = ex;
-    *kpre = k;
-    wa->lo = alo;
-    wa->hi = ahi;
-    wb->lo = blo;
-    wb->hi = bhi;
-    return ok;
-}
-
-// Phase 3 of a lane: decode `count` codewords from `start` (must end exactly
-// at `end`) and store them at dst; 16-byte stores once 8-code aligned.
-__device__ __noinline__ bool lean_store(const DecodeTables& d, uint64_t sbit, uint32_t start,
-                                        uint32_t end, uint32_t count, uint16_t* dst,
-                                        uint32_t* zeros_out) {
-    LeanReader rd;
-    rd.w = d.words;
-    rd.last = d.nwords - 1;
-    rd.init(sbit + start);
-    uint32_t pos = start, j = 0, zeros = 0;
-    bool ok = true;
-    const uint32_t head = (uint32_t)umin((8 - (((uintptr_t)dst >> 1) & 7)) & 7, count);
-    for (; j < head; j++) {
-        const uint32_t e = lean_step(d, rd, sbit + pos);
-        ok &= (e >> 16) != 255;
-        pos += (e >> 16) == 255 ? 1u : (e >> 16);
-        dst[j] = (uint16_t)e;
-        zeros += (e & 0xFFFF) == 0;
-    }
-    for (; j + 8 <= count; j += 8) {
-        unsigned long long acc0 = 0, acc1 = 0;
-        for (int t = 0; t < 8; t++) {
-            const uint32_t e = lean_step(d, rd, sbit + pos);
-            ok &= (e >> 16) != 255;
-            pos += (e >> 16) == 255 ? 1u : (e >> 16);
-            const unsigned long long s = e & 0xFFFF;
-            zeros += s == 0;
-            acc0 |= t < 4 ? (s << (16 * (t & 3))) : 0ull;
-            acc1 |= t >= 4 ? (s << (16 * (t & 3))) : 0ull;
-        }
-        *reinterpret_cast<uint4*>(dst + j) =
-            make_uint4((uint32_t)acc0, (uint32_t)(acc0 >> 32), (uint32_t)acc1, (uint32_t)(acc1 >> 32));
-    }
-    for (; j < count; j++) {
-        const uint32_t e = lean_step(d, rd, sbit + pos);
-        ok &= (e >> 16) != 255;
-        pos += (e >> 16) == 255 ? 1u : (e >> 16);
-        dst[j] = (uint16_t)e;
-        zeros += (e & 0xFFFF) == 0;
-    }
-    *zeros_out += zeros;
-    return ok && pos == end;
-}
-
-constexpr uint32_t kMinSliceBits = 128;
-
-__global__ void __launch_bounds__(256) inflate_warp_kernel(
-    const uint8_t* __restrict__ payload, uint64_t nwords, const uint32_t* __restrict__ chunk_bits,
-    const unsigned long long* __restrict__ byte_off, uint64_t nchunks, uint32_t chunk, uint64_t n,
-    const uint64_t* __restrict__ gfirst, const int64_t* __restrict__ goffsets,
-    const uint32_t* __restrict__ symbols, const uint32_t* __restrict__ glut, int max_bw_arg,
-    uint16_t* __restrict__ out, uint8_t* __restrict__ redo, DevStatus* st) {
-    for (uint32_t i = threadIdx.x; i < (1u << kLutBits); i += blockDim.x) dl_lut[i] = glut[i];
-    for (uint32_t i = threadIdx.x; i < 58; i += blockDim.x) dl_first[i] = gfirst[i];
-    for (uint32_t i = threadIdx.x; i < 59; i += blockDim.x) dl_offs[i] = goffsets[i];
-    const int mx = max_bw_arg > 0 ? max_bw_arg : (int)st->max_bw;
-    if (mx < 1 || mx > kMaxBw) return;
-    __syncthreads();
-    {
-        const long long ns = dl_offs[mx + 1];
-        if (ns <= (long long)kSymSmem)
-            for (uint32_t i = threadIdx.x; i < ns; i += blockDim.x) dl_sym[i] = (uint16_t)symbols[i];
-        for (uint32_t b = threadIdx.x; b < 58; b += blockDim.x)
-            dl_lim[b] = (b >= 1 && (int)b <= mx)
-                            ? (dl_first[b] + (unsigned long long)(dl_offs[b + 1] - dl_offs[b])) << (mx - b)
-                            : 0ull;
-    }
-    __syncthreads();
-    DecodeTables d;
-    // opaque copy: stops ptxas rematerialising the shared-window base (an
-    // S2R SR_CgaCtaId on the decode critical path) at every lookup
-    asm volatile("mov.u32 %0, %1;" : "=r"(d.lut_s) : "r"((uint32_t)__cvta_generic_to_shared(dl_lut)));
-    d.symbols = symbols;
-    d.words = reinterpret_cast<const uint32_t*>(payload);
-    d.nwords = nwords;
-    d.nsym = dl_offs[mx + 1];
-    d.mx = mx;
-    d.lb = mx < kLutBits ? mx : kLutBits;
-    const uint32_t lane = lane_id();
-    uint32_t zeros_total = 0;
-
-    for (uint64_t c = blockIdx.x * 8ull + (threadIdx.x >> 5); c < nchunks; c += gridDim.x * 8ull) {
-        const uint32_t B = chunk_bits[c];
-        const uint64_t sbit = byte_off[c] * 8;
-        const uint64_t base = c * chunk;
-        const uint32_t cnt = (uint32_t)umin(chunk, n - base);
-        uint32_t L = B / kMinSliceBits;
-        if (L > 32) L = 32;
-        if (L < 2 || (base & 7)) {
-            if (lane == 0) redo[c] = 1;
-            continue;
-        }
-        const bool active = lane < L;
-        const uint32_t s0 = active ? (uint32_t)(((uint64_t)lane * B) / L) : B;
-        const uint32_t s_next = active ? (uint32_t)(((uint64_t)(lane + 1) * B) / L) : B;
-        const uint32_t stop2 = lane + 1 == L ? B : s_next + 128;
-        // phase 1: every lane decodes its slice plus a 128-bit window of the next
-        uint32_t start = s0, e = B, kpre = 0;
-        Win128 wa{0, 0}, wb{0, 0};
-        bool ok = true;
-        if (active) ok = lean_window(d, sbit, start, s_next, stop2, &e, &kpre, &wa, &wb);
-        // phase 2: truth propagates from lane 0.  A lane whose predecessor is
-        // true synchronises at the first boundary both paths share inside the
-        // window (a true boundary); failing that, it redecodes from the
-        // predecessor's exit, which is a true boundary.
-        bool tru = !active || (lane == 0 && ok);
-        uint32_t sync = start;   // absolute (chunk-relative) start of the lane's true span
-        bool good = false;
-        for (uint32_t round = 0; round <= L; round++) {
-            const bool ptru = __shfl_up_sync(kFull, tru, 1);
-            const unsigned long long pb_lo = __shfl_up_sync(kFull, wb.lo, 1);
-            const unsigned long long pb_hi = __shfl_up_sync(kFull, wb.hi, 1);
-            const uint32_t pe = __shfl_up_sync(kFull, e, 1);
-            if (active && !tru && ptru && lane > 0) {
-                // wb of lane-1 and wa of this lane share the origin s0 only
-                // while this lane still starts at s0
-                const unsigned long long c_lo = start == s0 ? (wa.lo & pb_lo) : 0ull;
-                const unsigned long long c_hi = start == s0 ? (wa.hi & pb_hi) : 0ull;
-                if (ok && (c_lo | c_hi)) {
-                    sync = s0 + (c_lo ? (uint32_t)(__ffsll((long long)c_lo) - 1)
-                                      : 64u + (uint32_t)(__ffsll((long long)c_hi) - 1));
-                    tru = true;
-                } else if (pe < s_next) {
-                    start = pe;
-                    sync = pe;
-                    ok = lean_window(d, sbit, start, s_next, stop2, &e, &kpre, &wa, &wb);
-                    tru = ok;
-                    atomicAdd(&st->pad[0], 1ull);   // diagnostics: lane redecodes
-                } else {
-                    ok = false;
-                }
-            }
-            if (__all_sync(kFull, tru)) { good = true; break; }
-        }
-        if (lane == 0 && !good) atomicAdd(&st->pad[1], 1ull);
-        // symbols of each true span [sync_l, sync_{l+1})
-        const uint32_t nsync = __shfl_down_sync(kFull, sync, 1);
-        const uint32_t last_e = __shfl_sync(kFull, e, L - 1);
-        uint32_t nl = 0, ce = B;
-        if (active) {
-            nl = kpre - wa.below(sync - start);
-            if (lane + 1 < L) {
-                ce = nsync;
-                nl += wb.below(nsync - s_next);
-            }
-        }
-        int total;
-        const uint32_t o = (uint32_t)warp_excl_scan((int)nl, &total);
-        if (!good || last_e != B || (uint32_t)total != cnt) {
-            if (lane == 0) redo[c] = 1;
-            continue;
-        }
-        // phase 3: decode each true span again and store its codes at o
-        bool ok3 = true;
-        uint32_t zeros = 0;
-        if (active && nl) ok3 = lean_store(d, sbit, sync, ce, nl, out + base + o, &zeros);
-        if (!__all_sync(kFull, ok3)) {
-            if (lane == 0) redo[c] = 1;
-            continue;
-        }
-        zeros_total += zeros;
-    }
-    zeros_total = __reduce_add_sync(kFull, zeros_total);
-    if (lane == 0 && zeros_total) atomicAdd(&st->n_zero, (unsigned long long)zeros_total);
-}
-
 template <int SRC>
 int run_deflate(sdqz_ctx* ctx, DeflateArgs& a, bool payload) {
     const bool ts = SRC == SRC_CODES && a.gtable && a.cap <= 4096;
@@ -1819,12 +1324,11 @@ int launch_inflate(sdqz_ctx* ctx, const uint8_t* payload, uint64_t payload_bytes
     uint8_t* redo = scratch_as<uint8_t>(ctx, S_REDO, n_chunks, &rc);
     if (!redo) return rc;
     SDQZ_CUDA(ctx, cudaMemsetAsync(redo, 0, n_chunks, ctx->stream));
-    uint64_t wgrid = ceil_div(n_chunks, 8);
-    if (wgrid > (uint64_t)ctx->num_sms * 8) wgrid = ctx->num_sms * 8;
-    inflate_warp_kernel<<<(unsigned)wgrid, 256, 0, ctx->stream>>>(
-        payload, nwords, chunk_bits, a.byte_off, n_chunks, chunk, n, first, offsets, symbols, lut,
-        max_bw, (uint16_t*)codes, redo, ctx->d_status);
-    SDQZ_LAUNCHED_NAMED(ctx, "inflate_warp_kernel");
+    uint32_t* tab = nullptr;
+    if ((rc = launch_decode_tables(ctx, first, offsets, symbols, max_bw, &tab))) return rc;
+    if ((rc = launch_inflate_fast(ctx, payload, nwords, chunk_bits, a.byte_off, n_chunks, chunk, n,
+                                  first, offsets, symbols, tab, max_bw, (uint16_t*)codes, redo)))
+        return rc;
     inflate_kernel<false><<<(unsigned)grid, 64, 0, ctx->stream>>>(
         payload, nwords, chunk_bits, a.byte_off, n_chunks, chunk, n, first, offsets, symbols, lut,
         max_bw, codes, ctx->d_status, redo);

@@ -67,6 +67,16 @@ int launch_inflate(sdqz_ctx* ctx, const uint8_t* payload, uint64_t payload_bytes
                    const uint64_t* first, const int64_t* offsets, const uint32_t* symbols,
                    const uint32_t* lut, int max_bw, uint64_t n, void* codes, bool out32);
 
+// inflate.cu: decode tables (primary 12-bit + second level) and the warp-per-chunk
+// self-synchronising decoder; chunks it cannot finish are flagged in `redo`.
+int launch_decode_tables(sdqz_ctx* ctx, const uint64_t* first, const int64_t* offsets,
+                         const uint32_t* symbols, int max_bw, uint32_t** tab_out);
+int launch_inflate_fast(sdqz_ctx* ctx, const uint8_t* payload, uint64_t nwords,
+                        const uint32_t* chunk_bits, const unsigned long long* byte_off,
+                        uint64_t n_chunks, uint32_t chunk, uint64_t n, const uint64_t* first,
+                        const int64_t* offsets, const uint32_t* symbols, const uint32_t* tab,
+                        int max_bw, uint16_t* codes, uint8_t* redo);
+
 // reconstruct.cu ------------------------------------------------------------
 // Validate outlier records (range, order, code==0) and scatter their fp64
 // bits into `dense` (uint64[n]); flag blocks needing the fp64 path.
