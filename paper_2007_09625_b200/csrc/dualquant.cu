@@ -51,19 +51,6 @@ __device__ __forceinline__ void hist_add(HistCtx& h, uint32_t code) {
     }
 }
 
-// Branch-free window update; codes outside the window go to a shared
-// `red` (rare).  Requires the shared histogram (cap <= kSmemHistMax) or none.
-__device__ __forceinline__ void hist_add_fast(HistCtx& h, uint32_t code) {
-    const uint32_t dw = code - h.wbase;
-    const unsigned long long inc = dw < 16u ? (1ull << ((dw & 7u) << 3)) : 0ull;
-    h.lo += dw < 8u ? inc : 0ull;
-    h.hi += dw < 8u ? 0ull : inc;
-    if (dw >= 16u) {
-        if (h.shist) atomicAdd(&h.shist[code], 1u);
-        else if (h.ghist) atomicAdd(&h.ghist[code], 1ull);
-    }
-}
-
 __device__ __forceinline__ void hist_flush(HistCtx& h) {
 #pragma unroll
     for (int k = 0; k < 16; k++) {
@@ -281,109 +268,167 @@ __global__ void __launch_bounds__(kThreads, 2) dq3d_kernel(const void* __restric
 // while task t is computed from shared memory, so the field is read once at
 // full bandwidth with no per-element address arithmetic or registers held
 // for loads.
+//
+// One pass per task: every point is prequantized (fp64 reciprocal multiply,
+// exact division only in the 2^-22 rounding-tie neighbourhood), D_x D_y D_z
+// differenced in int32, coded and counted.  The 16 histogram bins around the
+// radius are lane-private shared counters (bank = lane: conflict-free atomics,
+// merged once per CTA); other codes go to the CTA's shared histogram.  A task
+// holding a value too large for the int32 path (|x / 2eb| >= 2^27 - 4) or a
+// non-finite value is rare: its counts are taken back and the task is redone
+// in fp64 in the reference's term order.
 // ----------------------------------------------------------------------------
-constexpr int kTmaWarps = 4;
-constexpr uint32_t kTile3 = 32 * 8 * 8;          // floats per 3D task tile
+constexpr int kTmaWarps = 8;
+constexpr int kStages = 3;                       // ring of plane-pair tiles per warp
+constexpr uint32_t kPair = 32 * 8 * 2;           // floats per stage: 32 x, 8 y, 2 z
+constexpr uint32_t kHot = 16;                    // lane-private bins per warp
 
-__global__ void __launch_bounds__(kTmaWarps * 32) dq3d_tma_kernel(
+__device__ __forceinline__ void hot_add(uint32_t hot_s, uint32_t c, uint32_t wbase, HistCtx& h) {
+    const uint32_t dw = c - wbase;
+    if (dw < kHot) {
+        asm volatile("red.shared.add.u32 [%0], 1;" ::"r"(hot_s + dw * 128u) : "memory");
+    } else if (h.shist) {
+        atomicAdd(&h.shist[c], 1u);
+    } else if (h.ghist) {
+        atomicAdd(&h.ghist[c], 1ull);
+    }
+}
+
+// take back the counts of a task's fast-path codes (read from global memory)
+__device__ __noinline__ void dq3d_uncount(const uint16_t* __restrict__ codes, uint64_t base, uint64_t YX,
+                                          uint64_t X, bool xin, int nz, int ny, uint32_t hot_s,
+                                          uint32_t wbase, HistCtx h) {
+    for (int z = 0; z < nz; z++)
+        for (int y = 0; y < ny; y++) {
+            if (!xin) continue;
+            const uint32_t c = codes[base + z * YX + y * X];
+            const uint32_t dw = c - wbase;
+            if (dw < kHot) {
+                asm volatile("red.shared.add.u32 [%0], -1;" ::"r"(hot_s + dw * 128u) : "memory");
+            } else if (h.shist) {
+                atomicSub(&h.shist[c], 1u);
+            } else if (h.ghist) {
+                atomicAdd(&h.ghist[c], ~0ull);   // -1 mod 2^64
+            }
+        }
+}
+
+__global__ void __launch_bounds__(kTmaWarps * 32, 3) dq3d_tma_kernel(
     const __grid_constant__ CUtensorMap tmap, const float* __restrict__ in, uint64_t Z, uint64_t Y,
     uint64_t X, uint32_t cap, DevStatus* st, uint16_t* __restrict__ codes,
     unsigned long long* ghist) {
     extern __shared__ __align__(128) unsigned char dsm[];
-    float* tiles = reinterpret_cast<float*>(dsm);                              // [warp][2][kTile3]
-    uint64_t* bars = reinterpret_cast<uint64_t*>(dsm + kTmaWarps * 2 * kTile3 * 4);
-    uint32_t* shist_base = reinterpret_cast<uint32_t*>(bars + kTmaWarps * 2);
+    float* tiles = reinterpret_cast<float*>(dsm);                              // [warp][stage][kPair]
+    uint64_t* bars = reinterpret_cast<uint64_t*>(dsm + kTmaWarps * kStages * kPair * 4);
+    uint32_t* hot = reinterpret_cast<uint32_t*>(bars + kTmaWarps * kStages);   // [warp][kHot][32]
+    uint32_t* shist_base = hot + kTmaWarps * kHot * 32;
+    for (uint32_t i = threadIdx.x; i < kTmaWarps * kHot * 32; i += blockDim.x) hot[i] = 0;
     HistCtx h;
-    hist_init(h, shist_base, ghist, cap);
+    hist_init(h, shist_base, ghist, cap);   // (syncs)
     const double two_eb = st->two_eb;
     const double rcp = __drcp_rn(two_eb);
     const int r = (int)(cap >> 1);
+    const uint32_t wbase = cap >= 2 * kHot ? (uint32_t)r - kHot / 2 : 0u;
     const uint32_t lane = lane_id(), wid = threadIdx.x >> 5, xl = lane & 7;
+    const uint32_t hot_s = smem_u32(hot + wid * kHot * 32 + lane);
     const uint64_t nbx4 = ceil_div(ceil_div(X, 8), 4), nby = ceil_div(Y, 8), nbz = ceil_div(Z, 8);
     const uint64_t ntask = nbx4 * nby * nbz;
     const uint64_t YX = Y * X;
-    float* mytiles = tiles + (size_t)wid * 2 * kTile3;
-    uint64_t* mybar = bars + wid * 2;
+    float* mytiles = tiles + (size_t)wid * kStages * kPair;
+    uint64_t* mybar = bars + wid * kStages;
     if (lane == 0) {
-        mbar_init(&mybar[0], 1);
-        mbar_init(&mybar[1], 1);
+        for (int q = 0; q < kStages; q++) mbar_init(&mybar[q], 1);
         fence_mbar_init();
     }
     __syncwarp();
-    auto issue = [&](uint64_t task, int stage) {
+    const uint64_t stride = (uint64_t)gridDim.x * kTmaWarps;
+    const uint64_t first = blockIdx.x * (uint64_t)kTmaWarps + wid;
+    // unit u = (task first + (u >> 2) * stride, z planes 2(u & 3) .. +1)
+    auto issue = [&](uint64_t u) {
+        const uint64_t task = first + (u >> 2) * stride;
+        if (task >= ntask) return;
         const uint64_t bx4 = task % nbx4, t2 = task / nbx4;
         const uint64_t by = t2 % nby, bz = t2 / nby;
-        mbar_expect_tx(&mybar[stage], kTile3 * 4);
-        tma_load_3d(mytiles + stage * kTile3, &tmap, (int)(bx4 * 32), (int)(by * 8), (int)(bz * 8),
-                    &mybar[stage]);
+        const uint32_t q = (uint32_t)(u % kStages);
+        mbar_expect_tx(&mybar[q], kPair * 4);
+        tma_load_3d(mytiles + q * kPair, &tmap, (int)(bx4 * 32), (int)(by * 8),
+                    (int)(bz * 8 + 2 * (u & 3)), &mybar[q]);
     };
-    const uint64_t stride = (uint64_t)gridDim.x * kTmaWarps;
-    uint64_t task = blockIdx.x * (uint64_t)kTmaWarps + wid;
-    if (lane == 0 && task < ntask) issue(task, 0);
-    uint32_t phase0 = 0, phase1 = 0;
+    if (lane == 0)
+        for (int q = 0; q < kStages - 1; q++) issue(q);
+    uint32_t phase = 0;   // bit q: parity of stage q
+    uint64_t u = 0;
     bool bad = false;
-    for (int it = 0; task < ntask; task += stride, it++) {
-        const int stage = it & 1;
-        if (lane == 0 && task + stride < ntask) issue(task + stride, stage ^ 1);
-        if (stage == 0) { mbar_wait(&mybar[0], phase0); phase0 ^= 1; }
-        else { mbar_wait(&mybar[1], phase1); phase1 ^= 1; }
-        const float* tile = mytiles + stage * kTile3;
+    for (uint64_t task = first; task < ntask; task += stride) {
         const uint64_t bx4 = task % nbx4, t2 = task / nbx4;
         const uint64_t by = t2 % nby, bz = t2 / nby;
         const uint64_t x = bx4 * 32 + lane, y0 = by * 8, z0 = bz * 8;
         const bool xin = x < X;
         const int ny = (int)umin(8, Y - y0), nz = (int)umin(8, Z - z0);
         const uint64_t base = z0 * YX + y0 * X + x;
-        // pass 1: prequantize the tile in place (fp32 -> int32 bits), branch-free;
-        // the task-wide vote falls back to the exact fp64 path on a bound
-        // violation, a non-finite value or a rounding-tie neighbourhood
-        float mx = 0.f;
-        bool tbad = false, amb = false;
-        int* itile = reinterpret_cast<int*>(const_cast<float*>(tile));
-#pragma unroll 8
-        for (int k = 0; k < 64; k++) {
-            const float v = tile[k * 32 + lane];
-            mx = fmaxf(mx, fabsf(v));
-            tbad |= !isfinite(v);
-            itile[k * 32 + lane] = prequant_int_fast(v, rcp, amb);
-        }
-        bad |= tbad;
-        const bool use_int = __all_sync(kFull, !tbad && !amb && (double)mx / two_eb < kIntBound);
-        if (use_int) {
-            // pass 2: D_z D_y D_x Lorenzo residual in int32, codes, histogram
-            int hprev[8];
+        int hprev[8];
 #pragma unroll
-            for (int y = 0; y < 8; y++) hprev[y] = 0;
-            uint16_t* crow = codes + base;
+        for (int y = 0; y < 8; y++) hprev[y] = 0;
+        bool big = false;
+        uint16_t* crow = codes + base;
 #pragma unroll 1
-            for (int z = 0; z < 8; z++) {
+        for (int pr = 0; pr < 4; pr++, u++) {
+            if (lane == 0) issue(u + kStages - 1);
+            const uint32_t q = (uint32_t)(u % kStages);
+            mbar_wait(&mybar[q], (phase >> q) & 1u);
+            phase ^= 1u << q;
+            const float* tile = mytiles + q * kPair;
+#pragma unroll
+            for (int zz = 0; zz < 2; zz++) {
                 int gprev = 0;
-                const bool zin = xin && z < nz;
+                const bool zin = xin && 2 * pr + zz < nz;
 #pragma unroll
                 for (int y = 0; y < 8; y++) {
-                    const int v = itile[(z * 8 + y) * 32 + lane];
-                    const int left = __shfl_up_sync(kFull, v, 1);
-                    const int g = v - (xl ? left : 0);
+                    const float v = tile[(zz * 8 + y) * 32 + lane];
+                    const double yv = __dmul_rn((double)v, rcp);
+                    const double t = __dadd_rn(fabs(yv), 0.5);
+                    const double fl = floor(t);
+                    const double fr = __dsub_rn(t, fl);
+                    big |= !(t < kIntBound);
+                    int qv = (int)fl;
+                    qv = yv < 0.0 ? -qv : qv;
+                    if ((fr < 2.384185791015625e-07) | (fr > 1.0 - 2.384185791015625e-07))
+                        qv = (int)prequant((double)v, two_eb);   // rounding-tie neighbourhood: exact
+                    const int left = __shfl_up_sync(kFull, qv, 1);
+                    const int g = qv - (xl ? left : 0);
                     const int hh = g - gprev;
                     gprev = g;
                     const int delta = hh - hprev[y];
                     hprev[y] = hh;
-                    const uint32_t u = (uint32_t)(delta + r);
-                    const uint32_t c = (u - 1u) < (uint32_t)(2 * r - 1) ? u : 0u;   // -r < delta < r
+                    const uint32_t uu = (uint32_t)(delta + r);
+                    const uint32_t c = (uu - 1u) < (uint32_t)(2 * r - 1) ? uu : 0u;   // -r < delta < r
                     if (zin && y < ny) {
                         crow[y * X] = (uint16_t)c;
-                        hist_add_fast(h, c);
+                        hot_add(hot_s, c, wbase, h);
                     }
                 }
                 crow += YX;
             }
-        } else {
+            __syncwarp();   // the stage is refilled two units later
+        }
+        if (__any_sync(kFull, big)) {
+            dq3d_uncount(codes, base, YX, X, xin, nz, ny, hot_s, wbase, h);
             dq3d_task_f64<0>(in, base, YX, X, xin, nz, ny, xl, two_eb, r, codes, h, bad);
         }
-        hist_flush(h);
-        __syncwarp();   // every lane is done with this stage before it is refilled
     }
     if (__any_sync(kFull, bad) && lane == 0) atomicOr(&st->flags, (unsigned long long)F_NONFINITE);
+    __syncthreads();
+    // merge the lane-private hot bins: warp w sums bins w, w+8, ... over all warps' lanes
+    for (uint32_t j = wid; j < kHot; j += kTmaWarps) {
+        uint32_t v = 0;
+#pragma unroll
+        for (int w = 0; w < kTmaWarps; w++) v += hot[(w * kHot + j) * 32 + lane];
+        v = __reduce_add_sync(kFull, v);
+        if (lane == 0 && v && wbase + j < cap) {
+            if (h.shist) atomicAdd(&h.shist[wbase + j], v);
+            else if (h.ghist) atomicAdd(&h.ghist[wbase + j], (unsigned long long)v);
+        }
+    }
     hist_finish(h);
 }
 
@@ -654,13 +699,14 @@ int launch_kind(sdqz_ctx* ctx, const void* d_in, int ndims, const uint64_t dims[
         CUtensorMap map;
         const uint64_t gd[3] = {dims[2], dims[1], dims[0]};
         const uint64_t gs[2] = {dims[2] * 4, dims[2] * dims[1] * 4};
-        const uint32_t box[3] = {32, 8, 8};
+        const uint32_t box[3] = {32, 8, 2};
         if (make_tensor_map(&map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, d_in, gd, gs, box)) {
-            const size_t tsm = kTmaWarps * 2 * kTile3 * 4 + kTmaWarps * 2 * 8 + smem;
+            const size_t tsm = kTmaWarps * kStages * kPair * 4 + kTmaWarps * kStages * 8 +
+                               kTmaWarps * kHot * 32 * 4 + smem;
             static bool attr_done = false;
             if (!attr_done) {
                 cudaFuncSetAttribute(dq3d_tma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     64 * 1024 + 16 * 4096 + 64);
+                                     kTmaWarps * kStages * kPair * 4 + 16 * 1024 + 16 * 4096 + 256);
                 attr_done = true;
             }
             const uint64_t ntask =

@@ -78,6 +78,29 @@ __device__ void bitonic_sort(unsigned long long* a, uint32_t m) {
     }
 }
 
+// Bitonic sort of 1024 u64 keys held one per thread (blockDim == 1024):
+// strides < 32 exchange through shuffles, larger ones through `a` (smem).
+__device__ unsigned long long bitonic_sort_1024(unsigned long long x, unsigned long long* a) {
+    const uint32_t i = threadIdx.x;
+    for (uint32_t k = 2; k <= 1024; k <<= 1) {
+        for (uint32_t j = k >> 1; j > 0; j >>= 1) {
+            unsigned long long y;
+            if (j >= 32) {
+                a[i] = x;
+                __syncthreads();
+                y = a[i ^ j];
+                __syncthreads();
+            } else {
+                y = __shfl_xor_sync(kFull, x, j);
+            }
+            const bool asc = (i & k) == 0, low = (i & j) == 0;
+            const unsigned long long mn = x < y ? x : y, mxv = x < y ? y : x;
+            x = (low == asc) ? mn : mxv;
+        }
+    }
+    return x;
+}
+
 struct TreeScratch {       // global scratch for caps above the smem limit
     unsigned long long* keys;   // [cap]
     unsigned long long* iw;     // [cap]
@@ -87,10 +110,16 @@ struct TreeScratch {       // global scratch for caps above the smem limit
     uint32_t* jmp;              // [2*cap] x2
 };
 
+#ifdef SDQZ_DEBUG_TIMING
+#define BOOK_T(i) do { __syncthreads(); if (threadIdx.x == 0) tclk[i] = clock64(); } while (0)
+#else
+#define BOOK_T(i) do {} while (0)
+#endif
+
 template <bool SMALL>
 __global__ void __launch_bounds__(kBookThreads) codebook_kernel(
     const unsigned long long* __restrict__ hist, uint8_t* __restrict__ bw, uint32_t cap,
-    BookDev book, DevStatus* st, int build_tree, int canon, TreeScratch gs) {
+    BookDev book, DevStatus* st, int build_tree, int canon, TreeScratch gs, uint32_t round_min) {
     extern __shared__ unsigned long long smem[];
     // SMALL (cap <= 4096): every table lives in shared memory; the template
     // keeps the pointers in the shared address space (no generic accesses)
@@ -100,6 +129,11 @@ __global__ void __launch_bounds__(kBookThreads) codebook_kernel(
     __shared__ unsigned long long s_first[64];
     __shared__ long long s_off[66];
     const uint32_t tid = threadIdx.x;
+#ifdef SDQZ_DEBUG_TIMING
+    __shared__ long long tclk[8];
+    if (tid < 8) tclk[tid] = 0;
+#endif
+    BOOK_T(0);
 
     if (build_tree) {
         // ---- leaves sorted by (freq, symbol) -------------------------------
@@ -117,7 +151,17 @@ __global__ void __launch_bounds__(kBookThreads) codebook_kernel(
             if (tid == 0) atomicOr(&st->flags, (unsigned long long)F_ALL_ZERO_HIST);
             return;
         }
-        bitonic_sort(keys, cap);
+        BOOK_T(1);
+        if (cap <= 1024 && blockDim.x == 1024) {
+            __shared__ unsigned long long xbuf[1024];
+            const unsigned long long x = bitonic_sort_1024(tid < cap ? keys[tid] : ~0ull, xbuf);
+            __syncthreads();
+            if (tid < cap) keys[tid] = x;
+            __syncthreads();
+        } else {
+            bitonic_sort(keys, cap);
+        }
+        BOOK_T(2);
         if (n == 1) {
             if (tid == 0) bw[keys[0] & 0xFFFF] = 1;
             __syncthreads();
@@ -176,7 +220,7 @@ __global__ void __launch_bounds__(kBookThreads) codebook_kernel(
                 }
                 __syncthreads();
                 const uint32_t p = r_p, mL = r_mL, mI = r_mI;
-                if (p < 4) break;   // unproductive: finish sequentially
+                if (p < round_min) break;   // unproductive: finish sequentially
                 // merged position of every element below t
                 for (uint32_t j = tid; j < mL + mI; j += blockDim.x) {
                     unsigned long long key;
@@ -213,6 +257,7 @@ __global__ void __launch_bounds__(kBookThreads) codebook_kernel(
                 }
                 __syncthreads();
             }
+            BOOK_T(3);
             // -- sequential tail (thread 0): two-queue merge from (li, ii, ni)
             if (tid == 0) {
                 uint32_t li = r_li, ii = r_ii, ni = r_ni;
@@ -255,6 +300,7 @@ __global__ void __launch_bounds__(kBookThreads) codebook_kernel(
                 (void)ni;
             }
             __syncthreads();
+            BOOK_T(4);
             // ---- depths by pointer jumping (root = 2n-2) -------------------
             // d[v] = hops from v to jmp[v]; doubling: d += d[jmp], jmp = jmp[jmp].
             const uint32_t nodes = 2 * n - 1, root = 2 * n - 2;
@@ -307,6 +353,7 @@ __global__ void __launch_bounds__(kBookThreads) codebook_kernel(
             __syncthreads();
         }
     }
+    BOOK_T(5);
     if (!canon) return;
     __syncthreads();
 
@@ -358,20 +405,46 @@ __global__ void __launch_bounds__(kBookThreads) codebook_kernel(
     const uint32_t unit = mx <= 24 ? 32 : 64;
     for (uint32_t b = tid; b < 58; b += blockDim.x) book.first[b] = s_first[b];
     for (uint32_t b = tid; b < 59; b += blockDim.x) book.offsets[b] = s_off[b];
-    // order symbols by (bitwidth, symbol)
-    for (uint32_t s = tid; s < cap; s += blockDim.x) {
-        uint32_t b = bw[s];
-        keys[s] = b ? (((unsigned long long)b << 16) | s) : ~0ull;
+    // order symbols by (bitwidth, symbol) without sorting: a symbol's rank in
+    // its bitwidth group = same-width symbols before it (match_any within the
+    // warp + per-(warp, width) counts scanned down the warps), tile by tile
+    __shared__ uint32_t wcnt[32][64];
+    __shared__ uint32_t run[64];
+    if (tid < 64) run[tid] = 0;
+    const uint32_t lane = tid & 31, wid = tid >> 5;
+    BOOK_T(6);
+    for (uint32_t base = 0; base < cap; base += blockDim.x) {
+        const uint32_t s = base + tid;
+        const uint32_t b = s < cap ? bw[s] : 0;
+        const uint32_t m = __match_any_sync(kFull, b);
+        const uint32_t rk = __popc(m & ((1u << lane) - 1));
+        for (uint32_t i = tid; i < 32 * 64; i += blockDim.x) (&wcnt[0][0])[i] = 0;
+        __syncthreads();
+        if (rk == 0 && b < 64) wcnt[wid][b] = __popc(m);
+        __syncthreads();
+        if (tid < 64) {
+            uint32_t acc = run[tid];
+            for (uint32_t w = 0; w < blockDim.x / 32; w++) {
+                const uint32_t v = wcnt[w][tid];
+                wcnt[w][tid] = acc;
+                acc += v;
+            }
+            run[tid] = acc;
+        }
+        __syncthreads();
+        if (b && b < 64) {
+            const uint32_t i = (uint32_t)s_off[b] + wcnt[wid][b] + rk;
+            book.entries[s] = ((unsigned long long)b << (unit - 8)) |
+                              (s_first[b] + (unsigned long long)(i - (uint32_t)s_off[b]));
+            book.symbols[i] = s;
+        }
+        __syncthreads();
     }
-    __syncthreads();
-    bitonic_sort(keys, cap);
-    for (uint32_t i = tid; i < n; i += blockDim.x) {
-        unsigned long long k = keys[i];
-        uint32_t s = (uint32_t)(k & 0xFFFF), b = (uint32_t)(k >> 16);
-        unsigned long long cw = s_first[b] + (unsigned long long)(i - (uint32_t)s_off[b]);
-        book.entries[s] = ((unsigned long long)b << (unit - 8)) | cw;
-        book.symbols[i] = s;
-    }
+    BOOK_T(7);
+#ifdef SDQZ_DEBUG_TIMING
+    if (tid == 0) printf("codebook phases(cycles): keys %lld sort %lld merge-rounds %lld tail %lld depths %lld canon-prep %lld canon-rank %lld\n",
+                         tclk[1]-tclk[0], tclk[2]-tclk[1], tclk[3]-tclk[2], tclk[4]-tclk[3], tclk[5]-tclk[4], tclk[6]-tclk[5], tclk[7]-tclk[6]);
+#endif
 }
 
 // decode LUT: entry = sym | len << 16; len 0 = longer than the LUT, 255 = no codeword
@@ -577,26 +650,48 @@ __global__ void __launch_bounds__(256) chunk_stats_kernel(DeflateArgs a) {
 // (ceil(bits/8)) and outlier offsets.  Tiles of 4096 chunks are staged in
 // shared memory with coalesced loads; each thread scans 4 consecutive entries.
 __global__ void __launch_bounds__(1024) chunk_scan_kernel(DeflateArgs a) {
-    constexpr int kTile = 4096, kPer = kTile / 1024;
-    __shared__ uint32_t sbits[kTile], szero[kTile];
+    // one CTA; tiles of 16384 chunks, 16 consecutive chunks per thread, all of
+    // a tile's loads issued before the first use (one memory latency per tile)
+    constexpr int kPer = 16, kTile = 1024 * kPer;
     __shared__ unsigned long long wsb[32], wso[32];
     const uint64_t C = a.nchunks;
     const uint32_t tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
     unsigned long long carry_b = 0, carry_o = 0;
     for (uint64_t t0 = 0; t0 < C; t0 += kTile) {
-        const uint32_t m = (uint32_t)umin(kTile, C - t0);
-        for (uint32_t i = tid; i < m; i += 1024) {
-            sbits[i] = (a.chunk_bits[t0 + i] + 7) >> 3;
-            szero[i] = a.chunk_zeros ? a.chunk_zeros[t0 + i] : 0;
+        const uint64_t i0 = t0 + (uint64_t)tid * kPer;
+        uint32_t vb[kPer], vz[kPer];
+        const bool vec = (((uintptr_t)a.chunk_bits | (uintptr_t)a.chunk_zeros) & 15) == 0;
+        if (vec && i0 + kPer <= C) {
+#pragma unroll
+            for (int q = 0; q < kPer; q += 4) {
+                const uint4 u = *reinterpret_cast<const uint4*>(a.chunk_bits + i0 + q);
+                vb[q] = u.x; vb[q + 1] = u.y; vb[q + 2] = u.z; vb[q + 3] = u.w;
+            }
+            if (a.chunk_zeros) {
+#pragma unroll
+                for (int q = 0; q < kPer; q += 4) {
+                    const uint4 u = *reinterpret_cast<const uint4*>(a.chunk_zeros + i0 + q);
+                    vz[q] = u.x; vz[q + 1] = u.y; vz[q + 2] = u.z; vz[q + 3] = u.w;
+                }
+            } else {
+#pragma unroll
+                for (int q = 0; q < kPer; q++) vz[q] = 0;
+            }
+        } else {
+#pragma unroll
+            for (int q = 0; q < kPer; q++) {
+                const bool in = i0 + q < C;
+                vb[q] = in ? a.chunk_bits[i0 + q] : 0;
+                vz[q] = in && a.chunk_zeros ? a.chunk_zeros[i0 + q] : 0;
+            }
         }
-        __syncthreads();
         unsigned long long tb = 0, to = 0;
 #pragma unroll
         for (int q = 0; q < kPer; q++) {
-            uint32_t i = tid * kPer + q;
-            if (i < m) { tb += sbits[i]; to += szero[i]; }
+            vb[q] = (vb[q] + 7) >> 3;
+            tb += vb[q];
+            to += vz[q];
         }
-        // block exclusive scan of (tb, to)
         unsigned long long xb = tb, xo = to;
 #pragma unroll
         for (int o = 1; o < 32; o <<= 1) {
@@ -606,27 +701,26 @@ __global__ void __launch_bounds__(1024) chunk_scan_kernel(DeflateArgs a) {
         if (lane == 31) { wsb[wid] = xb; wso[wid] = xo; }
         __syncthreads();
         if (wid == 0) {
-            unsigned long long vb = wsb[lane], vo = wso[lane];
+            unsigned long long ub = wsb[lane], uo = wso[lane];
 #pragma unroll
             for (int o = 1; o < 32; o <<= 1) {
-                unsigned long long yb = __shfl_up_sync(kFull, vb, o), yo = __shfl_up_sync(kFull, vo, o);
-                if (lane >= (uint32_t)o) { vb += yb; vo += yo; }
+                unsigned long long yb = __shfl_up_sync(kFull, ub, o), yo = __shfl_up_sync(kFull, uo, o);
+                if (lane >= (uint32_t)o) { ub += yb; uo += yo; }
             }
-            wsb[lane] = vb;
-            wso[lane] = vo;
+            wsb[lane] = ub;
+            wso[lane] = uo;
         }
         __syncthreads();
         unsigned long long rb = carry_b + (wid ? wsb[wid - 1] : 0) + xb - tb;
         unsigned long long ro = carry_o + (wid ? wso[wid - 1] : 0) + xo - to;
 #pragma unroll
         for (int q = 0; q < kPer; q++) {
-            uint32_t i = tid * kPer + q;
-            if (i < m) {
-                a.byte_off[t0 + i] = rb;
-                if (a.out_off) a.out_off[t0 + i] = ro;
-                rb += sbits[i];
-                ro += szero[i];
+            if (i0 + q < C) {
+                a.byte_off[i0 + q] = rb;
+                if (a.out_off) a.out_off[i0 + q] = ro;
             }
+            rb += vb[q];
+            ro += vz[q];
         }
         carry_b += wsb[31];
         carry_o += wso[31];
@@ -1222,14 +1316,25 @@ int launch_codebook(sdqz_ctx* ctx, const unsigned long long* d_hist, uint8_t* d_
         gs.dep = u + 3 * cap;
         gs.jmp = u + 7 * cap;
     }
-    if (smem > 48 * 1024)
+    static size_t attr_smem = 0;   // static shared memory (~17 KB) + dynamic can pass 48 KB
+    if (smem > attr_smem) {
         cudaFuncSetAttribute(codebook_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        attr_smem = smem;
+    }
+    static uint32_t round_min = 0;
+    if (!round_min) {
+        const char* e = getenv("SDQZ_ROUND_MIN");
+        round_min = e ? (uint32_t)atoi(e) : 4u;
+        if (!round_min) round_min = 1;
+    }
     if (cap <= kSmemSortMax)
         codebook_kernel<true><<<1, kBookThreads, smem, ctx->stream>>>(d_hist, d_bw, cap, book, ctx->d_status,
-                                                                   build_tree ? 1 : 0, canon ? 1 : 0, gs);
+                                                                   build_tree ? 1 : 0, canon ? 1 : 0, gs,
+                                                                   round_min);
     else
         codebook_kernel<false><<<1, kBookThreads, 0, ctx->stream>>>(d_hist, d_bw, cap, book, ctx->d_status,
-                                                                    build_tree ? 1 : 0, canon ? 1 : 0, gs);
+                                                                    build_tree ? 1 : 0, canon ? 1 : 0, gs,
+                                                                    round_min);
     SDQZ_LAUNCHED_NAMED(ctx, "codebook_kernel");
     return SDQZ_OK;
 }
