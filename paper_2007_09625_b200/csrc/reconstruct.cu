@@ -265,6 +265,340 @@ __global__ void __launch_bounds__(kThreads) rq3d_kernel(const uint16_t* __restri
     }
 }
 
+// ----------------------------------------------------------------------------
+// 3D block 8x8x8, one thread per block.  With H = prefix_x(delta),
+// G = H + G(row y-1), F = G + F(plane z-1) the Lorenzo inverse costs three
+// integer adds per point and needs no communication: F of the previous plane
+// (64 values) and G of the previous row (8) live in registers.  An outlier
+// fixes F = v and re-derives G and H from it, which is exactly the
+// reference's per-outlier box correction applied in raster order
+// (dualquant.py:218-226).  A warp covers 32 consecutive blocks along x, so
+// every row of 8 codes (16 B) and 8 outputs (32 B) is part of one contiguous
+// warp-wide access.  int32 arithmetic with a magnitude guard (|F| < 2^28
+// keeps every intermediate exact); a block that trips it is redone in int64.
+// ----------------------------------------------------------------------------
+// one row of 8 points: x-prefix, then the y and z recurrences; outliers
+// (code 0) take their stored value.  Returns false on the magnitude guard.
+template <bool OUT>
+__device__ __forceinline__ void rq_row8(const uint32_t (&cw)[8], int r, int (&Gp)[8], int (&Fr)[8],
+                                        const unsigned long long* __restrict__ dense, uint64_t rb,
+                                        int& mn, int& mx) {
+    int H = 0;
+#pragma unroll
+    for (int x = 0; x < 8; x++) {
+        H += (int)cw[x] - r;
+        int G = H + Gp[x];
+        int f = G + Fr[x];
+        if (OUT && cw[x] == 0) {   // outlier: its final value is stored verbatim
+            const long long v = outlier_int(dense, rb + x);
+            const bool fits = v < (1ll << 28) && v > -(1ll << 28);
+            f = fits ? (int)v : (1 << 29);   // out of int32 range: trip the guard
+            G = f - Fr[x];
+            H = G - Gp[x];
+        }
+        mx = max(mx, f);
+        mn = min(mn, f);
+        Gp[x] = G;
+        Fr[x] = f;
+    }
+}
+
+template <int OUTK>
+__device__ __forceinline__ void rq_store8(void* __restrict__ out, uint64_t rb, const int (&F)[8],
+                                          double two_eb, int nx, bool vec) {
+    if (OUTK == 0) {
+        float o[8];
+#pragma unroll
+        for (int x = 0; x < 8; x++) o[x] = __double2float_rn(__dmul_rn((double)F[x], two_eb));
+        float* op = (float*)out + rb;
+        if (vec) {
+            *reinterpret_cast<float4*>(op) = make_float4(o[0], o[1], o[2], o[3]);
+            *reinterpret_cast<float4*>(op + 4) = make_float4(o[4], o[5], o[6], o[7]);
+        } else {
+#pragma unroll
+            for (int x = 0; x < 8; x++)
+                if (x < nx) op[x] = o[x];
+        }
+    } else {
+        double* op = (double*)out + rb;
+#pragma unroll
+        for (int x = 0; x < 8; x++)
+            if (vec || x < nx) op[x] = __dmul_rn((double)F[x], two_eb);
+    }
+}
+
+__device__ __forceinline__ bool has_zero16(uint32_t w) {   // either 16-bit half == 0
+    return ((w - 0x00010001u) & ~w & 0x80008000u) != 0;
+}
+
+// One half-row (4 points) of a block row whose other half lives in the
+// neighbouring lane.  Computed with a zero x-carry, then corrected: the true
+// x-prefix adds the left half's final H (`carry`) to every point before this
+// half's first outlier (an outlier resets the prefix).
+template <int OUTK, bool VEC>
+__device__ __forceinline__ void rq_half_row(uint2 w, int r, uint32_t h, int (&Gp)[4], int (&Fr)[4],
+                                            const unsigned long long* __restrict__ dense, uint64_t rb,
+                                            double two_eb, void* __restrict__ out, bool store, int nv,
+                                            int& mn, int& mx) {
+    const uint32_t cw[4] = {w.x & 0xFFFF, w.x >> 16, w.y & 0xFFFF, w.y >> 16};
+    int H = 0, G[4], F[4];
+    int fo = 4;   // first outlier position in this half
+    if (has_zero16(w.x) | has_zero16(w.y)) {
+#pragma unroll
+        for (int x = 3; x >= 0; x--)
+            if (cw[x] == 0) fo = x;
+#pragma unroll
+        for (int x = 0; x < 4; x++) {
+            H += (int)cw[x] - r;
+            G[x] = H + Gp[x];
+            F[x] = G[x] + Fr[x];
+            if (cw[x] == 0) {   // outlier: its final value is stored verbatim
+                const long long v = outlier_int(dense, rb + x);
+                F[x] = (v < (1ll << 28) && v > -(1ll << 28)) ? (int)v : (1 << 29);   // guard trips
+                G[x] = F[x] - Fr[x];
+                H = G[x] - Gp[x];
+            }
+        }
+    } else {
+#pragma unroll
+        for (int x = 0; x < 4; x++) {
+            H += (int)cw[x] - r;
+            G[x] = H + Gp[x];
+            F[x] = G[x] + Fr[x];
+        }
+    }
+    // x-carry from the left half (after its own outliers)
+    const int hl = __shfl_xor_sync(kFull, H, 1);
+    const int carry = h ? hl : 0;
+#pragma unroll
+    for (int x = 0; x < 4; x++) {
+        const int cx = x < fo ? carry : 0;
+        G[x] += cx;
+        F[x] += cx;
+        Gp[x] = G[x];
+        Fr[x] = F[x];
+        mx = max(mx, F[x]);
+        mn = min(mn, F[x]);
+    }
+    if (store) {
+        if (OUTK == 0) {
+            float o[4];
+#pragma unroll
+            for (int x = 0; x < 4; x++) o[x] = __double2float_rn(__dmul_rn((double)F[x], two_eb));
+            if (VEC) {
+                *reinterpret_cast<float4*>((float*)out + rb) = make_float4(o[0], o[1], o[2], o[3]);
+            } else {
+#pragma unroll
+                for (int x = 0; x < 4; x++)
+                    if (x < nv) ((float*)out)[rb + x] = o[x];
+            }
+        } else {
+            double* op = (double*)out + rb;
+#pragma unroll
+            for (int x = 0; x < 4; x++)
+                if (VEC || x < nv) op[x] = __dmul_rn((double)F[x], two_eb);
+        }
+    }
+}
+
+// 4 codes of a half row; missing points (x >= nv) read as residual 0 (code r)
+template <bool VEC>
+__device__ __forceinline__ uint2 load_half(const uint16_t* __restrict__ codes, uint64_t i, int nv, int r) {
+    if (VEC) return __ldg(reinterpret_cast<const uint2*>(codes + i));
+    uint32_t c[4];
+#pragma unroll
+    for (int x = 0; x < 4; x++) c[x] = x < nv ? codes[i + x] : (uint32_t)r;
+    return make_uint2(c[0] | (c[1] << 16), c[2] | (c[3] << 16));
+}
+
+// Block of full x-extent (8), two lanes per block (x 0-3 / 4-7); the next
+// plane's 8 row loads are in flight while the current plane is processed.
+// Rows past the field (ny < 8) load a clamped row and are never stored;
+// their values only feed later rows, so stored values are unaffected.
+template <int OUTK, bool VEC>
+__device__ __forceinline__ bool rq3d_half_block(const uint16_t* __restrict__ codes,
+                                                const unsigned long long* __restrict__ dense,
+                                                uint64_t base, uint64_t YX, uint64_t X, int nx, int ny,
+                                                int nz, int r, double two_eb, void* __restrict__ out,
+                                                uint32_t h, bool active) {
+    const int nv = VEC ? 4 : (active ? nx - 4 * (int)h : 0);   // valid points of this half
+    int Fp[8][4];
+#pragma unroll
+    for (int y = 0; y < 8; y++)
+#pragma unroll
+        for (int x = 0; x < 4; x++) Fp[y][x] = 0;
+    int mx = 0, mn = 0;
+    const uint64_t hb = base + 4 * h;
+    uint2 cur[8];
+#pragma unroll
+    for (int y = 0; y < 8; y++)
+        cur[y] = active ? load_half<VEC>(codes, hb + (uint64_t)min(y, ny - 1) * X, nv, r) : make_uint2(0, 0);
+#pragma unroll 1
+    for (int z = 0; z < nz; z++) {
+        uint2 nxt[8];
+        const uint64_t zb = hb + (uint64_t)z * YX;
+        if (z + 1 < nz && active) {
+#pragma unroll
+            for (int y = 0; y < 8; y++)
+                nxt[y] = load_half<VEC>(codes, zb + YX + (uint64_t)min(y, ny - 1) * X, nv, r);
+        }
+        int Gp[4] = {0, 0, 0, 0};
+#pragma unroll
+        for (int y = 0; y < 8; y++)
+            rq_half_row<OUTK, VEC>(cur[y], r, h, Gp, Fp[y], dense, zb + (uint64_t)y * X, two_eb, out,
+                                   active && y < ny && nv > 0, nv, mn, mx);
+#pragma unroll
+        for (int y = 0; y < 8; y++) cur[y] = nxt[y];
+    }
+    return mx < (1 << 28) && mn > -(1 << 28);
+}
+
+// One thread per block (full x-extent, 8-byte aligned rows): F of the previous
+// plane lives in shared memory, transposed ([y][x/4][thread] int4) so the
+// per-row reads/writes are conflict-free, which keeps registers for the
+// prefetched next plane.
+constexpr int kRqThreads = 64;
+
+__device__ __forceinline__ void cp_async8(uint32_t dst, const void* src) {
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(dst), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait1() { asm volatile("cp.async.wait_group 1;" ::: "memory"); }
+
+// The thread's block rows stream through shared memory: plane z+1's 16
+// eight-byte row halves are copied by cp.async while plane z is processed.
+// Shared layouts are [slot][thread] so a warp's accesses are contiguous.
+template <int OUTK>
+__device__ __forceinline__ bool rq3d_block_smem(const uint16_t* __restrict__ codes,
+                                                const unsigned long long* __restrict__ dense,
+                                                uint64_t base, uint64_t YX, uint64_t X, int nx, int ny,
+                                                int nz, int r, double two_eb, void* __restrict__ out,
+                                                int4* __restrict__ fp, uint2* __restrict__ cs, bool vec,
+                                                bool vec_out) {
+    // vec: 8-byte aligned rows whose 16-byte reads stay inside the array
+    // (cp.async); otherwise rows are gathered with guarded scalar loads.
+    // x >= nx (partial edge block): the row read runs into the next row; those
+    // codes are replaced by residual 0 and their values are never stored.
+    // Rows past the field (ny < 8) load a clamped row and are never stored.
+#pragma unroll
+    for (int i = 0; i < 16; i++) fp[i * kRqThreads] = make_int4(0, 0, 0, 0);
+    int mx = 0, mn = 0;
+    const bool edge = nx < 8;
+    auto fetch = [&](int z) {
+        const int buf = z & 1;
+        for (int y = 0; y < 8; y++) {
+            const uint16_t* src = codes + base + (uint64_t)z * YX + (uint64_t)min(y, ny - 1) * X;
+            uint2* d0 = cs + ((buf * 8 + y) * 2) * kRqThreads;
+            uint2* d1 = d0 + kRqThreads;
+            if (vec) {
+                cp_async8((uint32_t)__cvta_generic_to_shared(d0), src);
+                cp_async8((uint32_t)__cvta_generic_to_shared(d1), src + 4);
+            } else {
+                uint32_t c[8];
+#pragma unroll
+                for (int x = 0; x < 8; x++) c[x] = x < nx ? src[x] : (uint32_t)r;
+                *d0 = make_uint2(c[0] | (c[1] << 16), c[2] | (c[3] << 16));
+                *d1 = make_uint2(c[4] | (c[5] << 16), c[6] | (c[7] << 16));
+            }
+        }
+        cp_async_commit();
+    };
+    fetch(0);
+#pragma unroll 1
+    for (int z = 0; z < nz; z++) {
+        if (z + 1 < nz) fetch(z + 1);
+        else cp_async_commit();   // empty group keeps the wait count uniform
+        cp_async_wait1();
+        const uint64_t zb = base + (uint64_t)z * YX;
+        const uint2* cz = cs + ((z & 1) * 8 * 2) * kRqThreads;
+        int Gp[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+#pragma unroll 1
+        for (int y = 0; y < 8; y++) {
+            const uint2 u0 = cz[(y * 2) * kRqThreads], u1 = cz[(y * 2 + 1) * kRqThreads];
+            uint32_t cw[8] = {u0.x & 0xFFFF, u0.x >> 16, u0.y & 0xFFFF, u0.y >> 16,
+                              u1.x & 0xFFFF, u1.x >> 16, u1.y & 0xFFFF, u1.y >> 16};
+            if (edge) {
+#pragma unroll
+                for (int x = 0; x < 8; x++) cw[x] = x < nx ? cw[x] : (uint32_t)r;
+            }
+            const uint64_t rb = zb + (uint64_t)y * X;
+            const int4 a = fp[(y * 2) * kRqThreads], b = fp[(y * 2 + 1) * kRqThreads];
+            const int F0[8] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
+            int F[8], G[8];
+            int H = 0;
+#pragma unroll
+            for (int x = 0; x < 8; x++) {
+                H += (int)cw[x] - r;
+                G[x] = H + Gp[x];
+                F[x] = G[x] + F0[x];
+            }
+            bool anyz = false;
+#pragma unroll
+            for (int x = 0; x < 8; x++) anyz |= cw[x] == 0;
+            if (anyz) {   // rare: redo the row with its outliers
+                H = 0;
+#pragma unroll
+                for (int x = 0; x < 8; x++) {
+                    H += (int)cw[x] - r;
+                    G[x] = H + Gp[x];
+                    F[x] = G[x] + F0[x];
+                    if (cw[x] == 0) {   // outlier: its final value is stored verbatim
+                        const long long v = outlier_int(dense, rb + x);
+                        F[x] = (v < (1ll << 28) && v > -(1ll << 28)) ? (int)v : (1 << 29);
+                        G[x] = F[x] - F0[x];
+                        H = G[x] - Gp[x];
+                    }
+                }
+            }
+#pragma unroll
+            for (int x = 0; x < 8; x++) {
+                Gp[x] = G[x];
+                mx = max(mx, F[x]);
+                mn = min(mn, F[x]);
+            }
+            fp[(y * 2) * kRqThreads] = make_int4(F[0], F[1], F[2], F[3]);
+            fp[(y * 2 + 1) * kRqThreads] = make_int4(F[4], F[5], F[6], F[7]);
+            if (y < ny) rq_store8<OUTK>(out, rb, F, two_eb, nx, OUTK == 0 && !edge && vec_out);
+        }
+    }
+    cp_async_wait1();
+    return mx < (1 << 28) && mn > -(1 << 28);
+}
+
+template <int OUTK>
+__global__ void __launch_bounds__(kRqThreads) rq3d_block_kernel(const uint16_t* __restrict__ codes,
+                                                         const unsigned long long* __restrict__ dense,
+                                                         uint8_t* __restrict__ blockflag,
+                                                         int any_slow, uint64_t Z, uint64_t Y,
+                                                         uint64_t X, uint32_t cap, double two_eb,
+                                                         void* __restrict__ out, DevStatus* st) {
+    __shared__ int4 s_fp[16 * kRqThreads];
+    __shared__ uint2 s_cs[2 * 16 * kRqThreads];
+    const int r = (int)(cap >> 1);
+    const uint64_t nbx = ceil_div(X, 8), nby = ceil_div(Y, 8), nbz = ceil_div(Z, 8);
+    const uint64_t nblk = nbx * nby * nbz;
+    const uint64_t YX = Y * X;
+    const bool vec_ok = (X & 3) == 0 && ((uintptr_t)codes & 7) == 0;
+    const bool vec_out = (X & 3) == 0 && ((uintptr_t)out & 15) == 0;
+    for (uint64_t b = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; b < nblk;
+         b += (uint64_t)gridDim.x * blockDim.x) {
+        if (any_slow && blockflag[b]) continue;   // the fp64 replay kernel owns it
+        const uint64_t bx = b % nbx, t2 = b / nbx, by = t2 % nby, bz = t2 / nby;
+        const int nx = (int)umin(8, X - bx * 8), ny = (int)umin(8, Y - by * 8), nz = (int)umin(8, Z - bz * 8);
+        const uint64_t base = bz * 8 * YX + by * 8 * X + bx * 8;
+        // cp.async rows need 8-byte alignment and the last row's 16-byte read
+        // inside the code array
+        const bool inside = base + (uint64_t)(nz - 1) * YX + (uint64_t)(ny - 1) * X + 8 <= Z * YX;
+        const bool ok = rq3d_block_smem<OUTK>(codes, dense, base, YX, X, nx, ny, nz, r, two_eb, out,
+                                              s_fp + threadIdx.x, s_cs + threadIdx.x, vec_ok && inside,
+                                              vec_out);
+        if (!ok) {   // magnitude guard: the fp64 replay kernel redoes the block
+            blockflag[b] = 1;
+            atomicOr(&st->flags, (unsigned long long)F_OUT_SLOW);
+        }
+    }
+}
+
 template <int OUTK>
 __global__ void __launch_bounds__(kThreads) rq3d_kernel_old(const uint16_t* __restrict__ codes,
                                                         const unsigned long long* __restrict__ dense,
@@ -512,8 +846,14 @@ int launch_reconstruct(sdqz_ctx* ctx, const uint16_t* codes, const uint64_t* den
         int slow = any_slow ? 1 : 0;
         // cp.async staging needs 4-byte aligned code rows
         const bool staged = dims[2] % 2 == 0 && ((uintptr_t)codes & 3) == 0;
+        const uint64_t nblk3 = ndims == 3 ? ceil_div(dims[0], 8) * ceil_div(dims[1], 8) * ceil_div(dims[2], 8) : 1;
+        uint64_t bgrid = ceil_div(nblk3, 64);
+        if (bgrid > (uint64_t)ctx->num_sms * 16) bgrid = (uint64_t)ctx->num_sms * 16;
 #define RQ_LAUNCH(K)                                                                                 \
-        if (ndims == 3 && staged)                                                                    \
+        if (ndims == 3 && !env_disabled("SDQZ_RQ_WARP"))                                             \
+            rq3d_block_kernel<K><<<(unsigned)bgrid, 64, 0, ctx->stream>>>(codes, dn, const_cast<uint8_t*>(blockflag), slow, \
+                                                                        dims[0], dims[1], dims[2], cap, two_eb, out, ctx->d_status); \
+        else if (ndims == 3 && staged)                                                               \
             rq3d_kernel<K><<<(unsigned)grid, kThreads, 0, ctx->stream>>>(codes, dn, blockflag, slow,   \
                                                                         dims[0], dims[1], dims[2], cap, two_eb, out); \
         else if (ndims == 3)                                                                         \
