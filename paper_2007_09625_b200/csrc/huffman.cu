@@ -925,6 +925,140 @@ constexpr int kRun = 16;
 constexpr int kRoundCodes = 32 * kRun;
 constexpr int kBufWords = kRoundCodes * kMaxBw / 32 + 4;   // worst case 56 bits per code
 
+// 32-bit units (every codeword <= 24 bits, the common case): the codebook is
+// re-encoded as left-aligned codeword | width (width in the low 5 bits, which
+// a <= 24-bit codeword leaves free), so appending a code is two funnel shifts
+// into a 64-bit pending window; no 64-bit variable shifts, no branches.
+__device__ __forceinline__ uint32_t entry32(unsigned long long u) {
+    const uint32_t w = (uint32_t)(u >> 24);
+    const uint32_t cw = (uint32_t)(u & 0xFFFFFFull);
+    return w ? ((cw << (32 - w)) | w) : 0u;
+}
+
+__device__ __forceinline__ bool zero_half(uint32_t w) {   // either 16-bit half == 0
+    return ((w - 0x00010001u) & ~w & 0x80008000u) != 0;
+}
+
+template <bool TS>
+__global__ void __launch_bounds__(256) chunk_pack32_kernel(DeflateArgs a) {
+    __shared__ uint32_t s_tab[TS ? 4096 : 1];
+    __shared__ uint32_t s_buf[8][kRoundCodes * 24 / 32 + 4];
+    if (a.st->flags & (F_CODE_RANGE | F_ABSENT_SYM | F_ZERO_WIDTH | F_OVERFLOW | F_BW_TOO_BIG |
+                       F_KRAFT | F_NO_PRESENT | F_ALL_ZERO_HIST))
+        return;
+    if (unit_of(a) != 32) return;   // 64-bit units: chunk_pack_run_kernel
+    if (TS)
+        for (uint32_t i = threadIdx.x; i < a.cap; i += blockDim.x) s_tab[i] = entry32(a.gtable[i]);
+    __syncthreads();
+    const double two_eb = a.st->two_eb;
+    const uint32_t lane = lane_id(), wid = threadIdx.x >> 5;
+    uint32_t* buf = s_buf[wid];
+    const uint16_t* src = (const uint16_t*)a.src;
+    auto lookup = [&](uint32_t code) -> uint32_t {
+        return TS ? s_tab[code] : entry32(__ldg(a.gtable + code));
+    };
+    for (uint64_t c = blockIdx.x * 8ull + wid; c < a.nchunks; c += gridDim.x * 8ull) {
+        const uint64_t s = c * a.chunk, e = umin(s + a.chunk, a.n);
+        const uint64_t B = a.byte_off[c];
+        const uint64_t Bend = B + ((a.chunk_bits[c] + 7) >> 3);
+        uint64_t wbyte = B & ~3ull;
+        uint32_t carry = (uint32_t)(B & 3) * 8;
+        uint32_t carry_word = 0;
+        uint64_t orec = a.out_off ? a.out_off[c] : 0;
+        for (uint64_t g = s; g < e; g += kRoundCodes) {
+            const uint64_t i0 = g + (uint64_t)kRun * lane;
+            const uint32_t cnt = i0 < e ? (uint32_t)umin(kRun, e - i0) : 0;
+            uint32_t code[kRun];
+            bool anyz;
+            if (cnt == kRun && (i0 & 7) == 0) {
+                const uint4 v0 = __ldg(reinterpret_cast<const uint4*>(src + i0));
+                const uint4 v1 = __ldg(reinterpret_cast<const uint4*>(src + i0) + 1);
+                const uint32_t wv[8] = {v0.x, v0.y, v0.z, v0.w, v1.x, v1.y, v1.z, v1.w};
+                anyz = false;
+#pragma unroll
+                for (int k = 0; k < 8; k++) {
+                    code[2 * k] = wv[k] & 0xFFFF;
+                    code[2 * k + 1] = wv[k] >> 16;
+                    anyz |= zero_half(wv[k]);
+                }
+            } else {
+                anyz = false;
+#pragma unroll
+                for (int k = 0; k < kRun; k++) {
+                    code[k] = (uint32_t)k < cnt ? src[i0 + k] : 1u;
+                    anyz |= code[k] == 0;
+                }
+            }
+            uint32_t ent[kRun], bits = 0;
+#pragma unroll
+            for (int k = 0; k < kRun; k++) {
+                ent[k] = (uint32_t)k < cnt ? lookup(code[k]) : 0u;
+                bits += ent[k] & 31u;
+            }
+            int total_l;
+            const uint32_t off = (uint32_t)warp_excl_scan((int)bits, &total_l) + carry;
+            const uint32_t total = carry + (uint32_t)total_l;
+            // the previous round's trailing partial word seeds word 0
+            if (lane == 0) buf[0] = carry_word;
+            for (uint32_t j = lane + 1; j < (total + 31) >> 5; j += 32) buf[j] = 0;
+            __syncwarp();
+            if (bits) {
+                uint32_t wi = off >> 5, nacc = off & 31;
+                uint32_t hi = 0, lo = 0;             // pending window, left-aligned
+                const uint32_t wfirst = wi;
+                uint32_t first_word = 0;
+                bool have_first = false;
+#pragma unroll
+                for (int k = 0; k < kRun; k++) {
+                    const uint32_t al = ent[k] & ~31u;    // codeword, left-aligned
+                    hi |= al >> nacc;
+                    lo |= __funnelshift_r(0u, al, nacc);
+                    nacc += ent[k] & 31u;
+                    const bool emit = nacc >= 32;
+                    if (emit && have_first) buf[wi] = hi;
+                    first_word = (emit && !have_first) ? hi : first_word;
+                    have_first |= emit;
+                    wi += emit ? 1u : 0u;
+                    hi = emit ? lo : hi;
+                    lo = emit ? 0u : lo;
+                    nacc -= emit ? 32u : 0u;
+                }
+                if (have_first) atomicOr(&buf[wfirst], first_word);
+                if (nacc) atomicOr(&buf[wi], hi);
+            }
+            __syncwarp();
+            const uint32_t full = total >> 5;
+            for (uint32_t j = lane; j < full; j += 32) store_word(a.payload, wbyte + 4ull * j, buf[j], B, Bend);
+            carry_word = (total & 31) ? buf[full] : 0u;
+            __syncwarp();
+            wbyte += 4ull * full;
+            carry = total & 31;
+            // outliers (code 0) in row-major order
+            if (a.records && __any_sync(kFull, anyz)) {
+                uint32_t zc = 0;
+#pragma unroll
+                for (int k = 0; k < kRun; k++) zc += ((uint32_t)k < cnt) & (code[k] == 0);
+                int ztot;
+                const uint32_t zoff = (uint32_t)warp_excl_scan((int)zc, &ztot);
+                uint64_t slot = orec + zoff;
+#pragma unroll
+                for (int k = 0; k < kRun; k++) {
+                    if ((uint32_t)k < cnt && code[k] == 0) {
+                        const uint64_t i = i0 + k;
+                        const double v = outlier_value(a, i, two_eb);
+                        a.records[2 * slot] = i + a.idx_base;
+                        a.records[2 * slot + 1] = (unsigned long long)__double_as_longlong(v);
+                        slot++;
+                    }
+                }
+                orec += (uint64_t)ztot;
+            }
+        }
+        if (carry && lane == 0) store_word(a.payload, wbyte, carry_word, B, Bend);
+        __syncwarp();
+    }
+}
+
 template <bool TS>
 __global__ void __launch_bounds__(256) chunk_pack_run_kernel(DeflateArgs a, int want_payload) {
     extern __shared__ unsigned long long stable[];
@@ -933,6 +1067,8 @@ __global__ void __launch_bounds__(256) chunk_pack_run_kernel(DeflateArgs a, int 
                        F_KRAFT | F_NO_PRESENT | F_ALL_ZERO_HIST))
         return;
     const uint32_t unit = unit_of(a);
+    const bool payload = want_payload != 0 && a.gtable != nullptr;
+    if (payload && unit == 32) return;   // chunk_pack32_kernel packs it
     const uint32_t wshift = unit - 8;
     const unsigned long long cwmask = (1ull << wshift) - 1;
     if (TS)
@@ -943,7 +1079,6 @@ __global__ void __launch_bounds__(256) chunk_pack_run_kernel(DeflateArgs a, int 
     const uint32_t lane = lane_id(), wid = threadIdx.x >> 5;
     uint32_t* buf = s_buf[wid];
     const uint16_t* src = (const uint16_t*)a.src;
-    const bool payload = want_payload != 0 && a.gtable != nullptr;
 
     for (uint64_t c = blockIdx.x * 8ull + wid; c < a.nchunks; c += gridDim.x * 8ull) {
         const uint64_t s = c * a.chunk, e = umin(s + a.chunk, a.n);
@@ -983,17 +1118,22 @@ __global__ void __launch_bounds__(256) chunk_pack_run_kernel(DeflateArgs a, int 
             int total_l;
             const uint32_t off = (uint32_t)warp_excl_scan((int)bits, &total_l) + carry;
             const uint32_t total = carry + (uint32_t)total_l;
-            // pass B: stream the run into the word buffer
+            // pass B: stream the run into the word buffer.  Branch-free: a
+            // completed word is a predicated plain store, except the run's
+            // first and last words, which neighbouring runs share and which are
+            // OR-ed in after the loop (two shared atomics per 16 codes).
             if (payload && bits) {
                 uint32_t wi = off >> 5;
                 uint32_t nacc = off & 31;            // leading bits belong to earlier runs
                 unsigned long long acc = 0;          // left-aligned pending bits
-                bool first = true;
+                const uint32_t wfirst = wi;
+                uint32_t first_word = 0;
+                bool have_first = false;
 #pragma unroll
                 for (int k = 0; k < kRun; k++) {
                     uint32_t w = (uint32_t)(u[k] >> wshift);
                     unsigned long long cw = u[k] & cwmask;
-                    if (w > 32) {                    // 64-bit units: emit the high part first
+                    if (unit > 32 && w > 32) {       // 64-bit units: emit the high part first
                         const uint32_t wh = w - 32;
                         acc |= (cw >> 32) << (64 - nacc - wh);
                         nacc += wh;
@@ -1001,24 +1141,27 @@ __global__ void __launch_bounds__(256) chunk_pack_run_kernel(DeflateArgs a, int 
                         w = 32;
                         if (nacc >= 32) {
                             const uint32_t word = (uint32_t)(acc >> 32);
-                            if (first) atomicOr(&buf[wi], word); else buf[wi] = word;
-                            first = false;
+                            if (have_first) buf[wi] = word; else first_word = word;
+                            have_first = true;
                             wi++;
                             acc <<= 32;
                             nacc -= 32;
                         }
                     }
-                    if (w) acc |= cw << (64 - nacc - w);
+                    acc |= w ? (cw << (64 - nacc - w)) : 0ull;
                     nacc += w;
-                    if (nacc >= 32) {
-                        const uint32_t word = (uint32_t)(acc >> 32);
-                        if (first) atomicOr(&buf[wi], word); else buf[wi] = word;
-                        first = false;
-                        wi++;
-                        acc <<= 32;
-                        nacc -= 32;
-                    }
+                    const bool emit = nacc >= 32;
+                    const uint32_t word = (uint32_t)(acc >> 32);
+                    if (emit && have_first) buf[wi] = word;
+                    first_word = (emit && !have_first) ? word : first_word;
+                    have_first |= emit;
+                    wi += emit ? 1u : 0u;
+                    acc = emit ? (acc << 32) : acc;
+                    nacc -= emit ? 32u : 0u;
                 }
+                // (the shared ORs below are atomic: no ordering against the
+                // neighbours' plain stores is needed -- those words differ)
+                if (have_first) atomicOr(&buf[wfirst], first_word);
                 if (nacc) atomicOr(&buf[wi], (uint32_t)(acc >> 32));
             }
             __syncwarp();
@@ -1271,6 +1414,11 @@ int run_deflate(sdqz_ctx* ctx, DeflateArgs& a, bool payload) {
             cudaFuncSetAttribute(chunk_pack_run_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  4096 * 8);
             attr = true;
+        }
+        if (payload && a.gtable) {   // 32-bit units (device-decided; no-op otherwise)
+            if (ts) chunk_pack32_kernel<true><<<(unsigned)grid, 256, 0, ctx->stream>>>(a);
+            else chunk_pack32_kernel<false><<<(unsigned)grid, 256, 0, ctx->stream>>>(a);
+            SDQZ_LAUNCHED_NAMED(ctx, "chunk_pack32_kernel");
         }
         if (ts) chunk_pack_run_kernel<true><<<(unsigned)grid, 256, smem, ctx->stream>>>(a, payload ? 1 : 0);
         else chunk_pack_run_kernel<false><<<(unsigned)grid, 256, 0, ctx->stream>>>(a, payload ? 1 : 0);
