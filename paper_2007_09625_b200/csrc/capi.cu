@@ -70,6 +70,9 @@ __global__ void set_eb_kernel(DevStatus* st, double eb) {
 }  // namespace
 
 int reset_status(sdqz_ctx* ctx) {
+    // host time since the last sync (Python, argument checks) is "(host)", not
+    // the first kernel's
+    if (ctx->timing) kt_mark(ctx, "(host)");
     init_status_kernel<<<1, 1, 0, ctx->stream>>>(ctx->d_status);
     SDQZ_LAUNCHED_NAMED(ctx, "init_status_kernel");
     return SDQZ_OK;
