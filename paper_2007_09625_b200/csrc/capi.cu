@@ -237,7 +237,7 @@ int decompress_core(sdqz_ctx* ctx, const sdqz_header* hdr, const uint8_t* d_bw, 
     // canonical tables from the stored bitwidths (deserialize checks + canonize)
     if ((rc = launch_codebook(ctx, nullptr, const_cast<uint8_t*>(d_bw), cap, book, false, true, true)))
         return rc;
-    if ((rc = launch_build_lut(ctx, book.first, book.offsets, book.symbols, -1, book.lut))) return rc;
+    // (the sequential decoder's LUT is built with the fast decoder's tables)
     if (chunks_ok) {
         if ((rc = launch_inflate(ctx, d_payload, payload_alloc, d_cbits, C, hdr->chunk_size,
                                  book.first, book.offsets, book.symbols, book.lut, -1, n, codes,

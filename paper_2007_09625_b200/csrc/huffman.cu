@@ -1578,7 +1578,9 @@ int launch_inflate(sdqz_ctx* ctx, const uint8_t* payload, uint64_t payload_bytes
     if (!redo) return rc;
     SDQZ_CUDA(ctx, cudaMemsetAsync(redo, 0, n_chunks, ctx->stream));
     uint32_t* tab = nullptr;
-    if ((rc = launch_decode_tables(ctx, first, offsets, symbols, max_bw, &tab))) return rc;
+    if ((rc = launch_decode_tables(ctx, first, offsets, symbols, max_bw, &tab,
+                                   const_cast<uint32_t*>(lut))))
+        return rc;
     if ((rc = launch_inflate_fast(ctx, payload, nwords, chunk_bits, a.byte_off, n_chunks, chunk, n,
                                   first, offsets, symbols, tab, max_bw, (uint16_t*)codes, redo)))
         return rc;

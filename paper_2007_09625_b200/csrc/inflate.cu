@@ -5,66 +5,106 @@
 // its bit range is cut into L <= 32 equal lane slices (>= kSliceMin bits).
 //
 //   phase 1  every lane decodes from its slice start (usually mid-codeword)
-//            to the first codeword boundary at/after its slice end (its exit),
-//            counting codewords, and records the codeword boundaries of the
-//            first kWin bits of its slice (wa) and of the first kWin bits of
-//            the NEXT slice (wb, decoding on past its end).
-//   phase 2  lane 0 starts on a true boundary.  Lane l is synchronised with
-//            lane l-1 when wa_l & wb_{l-1} != 0: from that first common
-//            boundary on both paths coincide (Huffman decoding is a function
-//            of the position), so lane l's path is the true path.  Lanes are
-//            checked all at once with a ballot; the first unsynchronised lane
-//            redecodes from its predecessor's exit (a true boundary) and the
-//            ballot is repeated -- at most L rounds, usually one.
-//   phase 3  a warp scan of the per-lane true-symbol counts gives output
-//            offsets and every lane decodes its true span again, packing codes
-//            into 16-byte stores.
+//            to the first codeword start at/after its slice end (its exit),
+//            counting codewords and recording the codeword starts of the first
+//            kWin bits of its slice (head mask).  It then decodes on into the
+//            next slice until one of its codeword starts is also in the next
+//            lane's head mask: from that synchronisation point on both paths
+//            coincide (decoding is a function of the position).
+//   phase 2  lane 0 starts on a true boundary; lane l is on the true path if
+//            lane l-1 is and l-1 synchronised with it.  The first lane that
+//            did not sync redecodes from its predecessor's exit (a true
+//            boundary) -- rare with a 128-bit window.
+//   phase 3  a warp scan of the per-lane true-span symbol counts gives output
+//            offsets and every lane decodes its span again, storing codes.
 //
-// Decode step: a 32-bit peek is a funnel shift of two big-endian payload
-// words held in registers (a third is prefetched); a 12-bit primary table in
-// shared memory resolves codewords <= 12 bits, longer ones go through a
-// per-prefix second-level table (also shared; sized 2^(max len under the
-// prefix - 12)) or, if that does not fit, a canonical limit search.  Chunks
-// whose codes exceed 32 bits, or whose decode fails any check, are handed to
-// the sequential decoder (huffman.cu inflate_kernel), which reproduces the
-// reference's exact error semantics.
+// Tables (shared memory, built once per call by dtab_kernel from the
+// canonical codebook) are indexed by the next 12 payload bits and resolve
+// SEVERAL codewords per lookup: T1 gives the total length, count and the
+// codeword-start mask of the greedy decode of the 12-bit window (phase 1
+// needs no symbols); T3 gives up to three symbols with their cumulative
+// lengths (phase 3).  Codewords longer than 12 bits go through a second-level
+// table (or, past its budget, a canonical limit search).  With ~2-4 bits per
+// code this decodes ~3 codewords per table step.
+//
+// Chunks whose codes exceed 32 bits, or whose decode fails any check, are
+// handed to the sequential decoder (huffman.cu inflate_kernel), which
+// reproduces the reference's exact error semantics.
 #include "kernels.cuh"
 
 namespace sdqz {
 
 namespace {
 
-constexpr int kL1 = 12;                    // primary table bits
+constexpr int kL1 = 12;                    // table index bits
 constexpr uint32_t kL1Size = 1u << kL1;
-constexpr uint32_t kL2Max = 4096;          // second-level entries
+constexpr uint32_t kL2Max = 4096;          // second-level entries (long codes)
 constexpr uint32_t kSliceMin = 192;        // bits per lane slice (> kWin)
 constexpr uint32_t kWin = 128;             // synchronisation window (bits)
-constexpr uint32_t kTabWords = kL1Size + kL2Max;
+// layout of the table block (u32 words): T1 | L2 | T3 (u64)
+constexpr uint32_t kOffL2 = kL1Size;
+constexpr uint32_t kOffT3 = kL1Size + kL2Max;
+constexpr uint32_t kTabWords = kOffT3 + 2 * kL1Size;
 
-// entry: short/full  sym << 16 | len            (len 1..32)
-//        second level base << 16 | k << 8 | 0x40 (len field 0, k extra bits)
-//        slow         0                          (canonical limit search)
-//        invalid      0x80 | 1                   (no codeword: incomplete code)
-constexpr uint32_t kInvalid = 0x81;          // len 1 + flag: loops stay bounded
+// T1 entry:  len (0-3) | count (4-7) | codeword-start mask (8-19) | invalid (20)
+//            count 0 = first codeword longer than 12 bits (or invalid)
+// T3 entry:  sym0 (0-15) | sym1 (16-31) | sym2 (32-47) | n (48-49) | len1 (50-53)
+//            | len12 (54-57) | len123 (58-61) | zeros (62-63)
+//            n 0 = long: bits 0-11 second-level base, 12-16 extra bits k,
+//            17 second level present, 18 invalid
+// L2 entry:  sym << 16 | len
+constexpr uint32_t kT1Invalid = 1u << 20;
+constexpr uint32_t kLongInvalid = 0x81;    // len 1 + flag (sym|len form)
 
 // ---------------------------------------------------------------------------
-// decode tables: one CTA builds primary + second-level tables in global memory
+// decode tables: one CTA
 // ---------------------------------------------------------------------------
 __global__ void __launch_bounds__(1024) dtab_kernel(const uint64_t* __restrict__ first,
                                                     const int64_t* __restrict__ offsets,
                                                     const uint32_t* __restrict__ symbols,
                                                     int max_bw_arg, const DevStatus* st,
-                                                    uint32_t* __restrict__ tab) {
+                                                    uint32_t* __restrict__ tab,
+                                                    uint32_t* __restrict__ old_lut) {
     __shared__ uint32_t pmax[kL1Size];
-    __shared__ uint32_t pbase[kL1Size];
+    __shared__ uint32_t s_one[kL1Size];   // first codeword of a 12-bit window: sym << 16 | len
+    __shared__ uint16_t pbase[kL1Size];   // second-level base, 0xFFFF = none
     __shared__ unsigned long long s_first[34];
     __shared__ long long s_off[35];
     const int mx = max_bw_arg > 0 ? max_bw_arg : (int)st->max_bw;
-    if (mx < 1 || mx > 32) return;                // > 32: the warp decoder is not used
+    if (mx < 1 || mx > kMaxBw) return;
+    if (mx > 32) {   // 64-bit codes: only the sequential decoder's table (lut_kernel's rule)
+        if (!old_lut) return;
+        const long long ns = offsets[mx + 1];
+        for (uint32_t i = threadIdx.x; i < (1u << kLutBits); i += blockDim.x) {
+            uint32_t e = 0;
+            bool found = false;
+            for (int b = 1; b <= kLutBits && !found; b++) {
+                const unsigned long long top = i >> (kLutBits - b);
+                const unsigned long long cnt = (unsigned long long)(offsets[b + 1] - offsets[b]);
+                if (top >= first[b] && top < first[b] + cnt) {
+                    long long idx = offsets[b] + (long long)(top - first[b]);
+                    if (idx >= ns) idx = ns ? ns - 1 : 0;
+                    e = (symbols[idx] & 0xFFFF) | ((uint32_t)b << 16);
+                    found = true;
+                }
+            }
+            if (!found) {
+                const unsigned long long pmin = (unsigned long long)i << (mx - kLutBits);
+                uint32_t b0 = (uint32_t)mx + 1;
+                for (int b = kLutBits + 1; b <= mx; b++) {
+                    const unsigned long long cnt = (unsigned long long)(offsets[b + 1] - offsets[b]);
+                    if (pmin < ((first[b] + cnt) << (mx - b))) { b0 = (uint32_t)b; break; }
+                }
+                e = b0;
+            }
+            old_lut[i] = e;
+        }
+        return;
+    }
     for (int b = threadIdx.x; b < 34; b += blockDim.x) s_first[b] = b <= mx ? first[b] : 0;
     for (int b = threadIdx.x; b < 35; b += blockDim.x) s_off[b] = b <= mx + 1 ? offsets[b] : offsets[mx + 1];
     for (uint32_t i = threadIdx.x; i < kL1Size; i += blockDim.x) pmax[i] = 0;
-    for (uint32_t i = threadIdx.x; i < kL2Max; i += blockDim.x) tab[kL1Size + i] = kInvalid;
+    for (uint32_t i = threadIdx.x; i < kL2Max; i += blockDim.x) tab[kOffL2 + i] = kLongInvalid;
     __syncthreads();
     const long long nsym = s_off[mx + 1];
     // longest code under each 12-bit prefix
@@ -108,28 +148,88 @@ __global__ void __launch_bounds__(1024) dtab_kernel(const uint64_t* __restrict__
         uint32_t acc = x - run + ((t >> 5) ? wsum[(t >> 5) - 1] : 0u);
 #pragma unroll
         for (uint32_t j = 0; j < per; j++) {
-            pbase[t * per + j] = (sz[j] && acc + sz[j] <= kL2Max) ? acc : ~0u;
+            pbase[t * per + j] = (sz[j] && acc + sz[j] <= kL2Max) ? (uint16_t)acc : (uint16_t)0xFFFF;
             acc += sz[j];
         }
     }
     __syncthreads();
-    // primary entries
+    // first codeword of every 12-bit window (0: longer than 12 bits / none)
     for (uint32_t i = threadIdx.x; i < kL1Size; i += blockDim.x) {
-        uint32_t e = kInvalid;
-        bool found = false;
-        for (int b = 1; b <= kL1 && b <= mx && !found; b++) {
+        uint32_t e = 0;
+        for (int b = 1; b <= kL1 && b <= mx; b++) {
             const unsigned long long top = i >> (kL1 - b);
             const unsigned long long cnt = (unsigned long long)(s_off[b + 1] - s_off[b]);
             if (top >= s_first[b] && top < s_first[b] + cnt) {
-                const long long idx = s_off[b] + (long long)(top - s_first[b]);
-                e = (symbols[idx] << 16) | (uint32_t)b;
-                found = true;
+                e = (symbols[s_off[b] + (long long)(top - s_first[b])] << 16) | (uint32_t)b;
+                break;
             }
         }
-        if (!found && pmax[i]) {
-            e = pbase[i] != ~0u ? ((pbase[i] << 16) | ((pmax[i] - kL1) << 8) | 0x40u) : 0u;
+        s_one[i] = e;
+    }
+    __syncthreads();
+    // the sequential fallback decoder's table (huffman.cu lut_kernel format)
+    if (old_lut) {
+        const int lb = mx < kLutBits ? mx : kLutBits;
+        for (uint32_t i = threadIdx.x; i < (1u << kLutBits); i += blockDim.x) {
+            uint32_t e = 0;
+            if (i < (1u << lb)) {
+                const uint32_t one = s_one[(i << (kL1 - lb)) & (kL1Size - 1)];
+                if (one && (int)(one & 63u) <= lb) {
+                    e = (one >> 16) | ((one & 63u) << 16);
+                } else if (lb == mx) {
+                    e = 255u << 16;
+                } else {   // longer than the LUT: shortest possible width as the search hint
+                    const unsigned long long pmin = (unsigned long long)i << (mx - lb);
+                    uint32_t b0 = (uint32_t)mx + 1;
+                    for (int b = lb + 1; b <= mx; b++) {
+                        const unsigned long long cnt = (unsigned long long)(s_off[b + 1] - s_off[b]);
+                        if (pmin < ((s_first[b] + cnt) << (mx - b))) { b0 = (uint32_t)b; break; }
+                    }
+                    e = b0;
+                }
+            }
+            old_lut[i] = e;
         }
-        tab[i] = e;
+    }
+    __syncthreads();
+    // T1 / T3: greedy decode of each 12-bit window, one table lookup per codeword
+    for (uint32_t i = threadIdx.x; i < kL1Size; i += blockDim.x) {
+        uint32_t o = 0, m = 0, mask = 0, zeros = 0, sym[3] = {0, 0, 0}, cum[3] = {0, 0, 0};
+        while (o < (uint32_t)kL1) {
+            const uint32_t one = s_one[(i << o) & (kL1Size - 1)];
+            const uint32_t b = one & 63u;
+            if (!b || b > kL1 - o) break;
+            const uint32_t sv = one >> 16;
+            mask |= 1u << o;
+            if (m < 3) {
+                sym[m] = sv;
+                cum[m] = o + b;
+                zeros += sv == 0;
+            }
+            m++;
+            o += b;
+        }
+        uint32_t t1;
+        unsigned long long t3;
+        if (m) {
+            t1 = o | (m << 4) | (mask << 8);
+            const uint32_t n3 = m < 3 ? m : 3;
+            t3 = (unsigned long long)sym[0] | ((unsigned long long)sym[1] << 16) |
+                 ((unsigned long long)sym[2] << 32) | ((unsigned long long)n3 << 48) |
+                 ((unsigned long long)cum[0] << 50) | ((unsigned long long)cum[n3 > 1 ? 1 : 0] << 54) |
+                 ((unsigned long long)cum[n3 - 1] << 58) | ((unsigned long long)zeros << 62);
+        } else if (pmax[i]) {   // the codeword is longer than 12 bits
+            t1 = 1u << 8;
+            t3 = pbase[i] != 0xFFFF ? ((unsigned long long)pbase[i] | ((unsigned long long)(pmax[i] - kL1) << 12) |
+                                    (1ull << 17))
+                                 : 0ull;
+        } else {                // no codeword has this prefix (incomplete code)
+            t1 = (1u << 8) | kT1Invalid;
+            t3 = 1ull << 18;
+        }
+        tab[i] = t1;
+        tab[kOffT3 + 2 * i] = (uint32_t)t3;
+        tab[kOffT3 + 2 * i + 1] = (uint32_t)(t3 >> 32);
     }
     // second-level entries
     for (long long i = lo + threadIdx.x; i < nsym; i += blockDim.x) {
@@ -137,12 +237,12 @@ __global__ void __launch_bounds__(1024) dtab_kernel(const uint64_t* __restrict__
         while (b < mx && i >= s_off[b + 1]) b++;
         const unsigned long long code = s_first[b] + (unsigned long long)(i - s_off[b]);
         const uint32_t p = (uint32_t)(code >> (b - kL1));
-        if (pbase[p] == ~0u) continue;
+        if (pbase[p] == 0xFFFF) continue;
         const uint32_t k = pmax[p] - kL1, extra = (uint32_t)b - kL1;
         const uint32_t low = (uint32_t)(code & ((1ull << extra) - 1));
         const uint32_t start = pbase[p] + (low << (k - extra));
         const uint32_t e = (symbols[i] << 16) | (uint32_t)b;
-        for (uint32_t j = 0; j < (1u << (k - extra)); j++) tab[kL1Size + start + j] = e;
+        for (uint32_t j = 0; j < (1u << (k - extra)); j++) tab[kOffL2 + start + j] = e;
     }
 }
 
@@ -150,7 +250,7 @@ __global__ void __launch_bounds__(1024) dtab_kernel(const uint64_t* __restrict__
 // shared decode state
 // ---------------------------------------------------------------------------
 struct Tabs {
-    uint32_t tab_s;           // shared address of the tables
+    uint32_t tab_s;           // shared address of the table block
     const uint32_t* symbols;  // global, slow path only
     int mx;
 };
@@ -159,52 +259,66 @@ __shared__ unsigned long long sh_lim[34];   // (first[b] + count[b]), b <= 32
 __shared__ unsigned long long sh_first[34];
 __shared__ long long sh_off[35];
 
-__device__ __noinline__ uint32_t slow_entry(const Tabs& t, uint32_t peek) {
-    for (int b = kL1 + 1; b <= t.mx; b++) {
-        const unsigned long long top = peek >> (32 - b);
-        if (top < sh_lim[b]) {
-            if (top < sh_first[b]) return kInvalid;
-            return (t.symbols[sh_off[b] + (long long)(top - sh_first[b])] << 16) | (uint32_t)b;
-        }
-    }
-    return kInvalid;
-}
-
 __device__ __forceinline__ uint32_t lds32(uint32_t addr) {
     uint32_t v;
     asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(addr));
     return v;
 }
-
-// table entry of the codeword at the top of `peek`
-__device__ __forceinline__ uint32_t lookup(const Tabs& t, uint32_t peek) {
-    uint32_t e = lds32(t.tab_s + ((peek >> (32 - kL1)) << 2));
-    if ((e & 63u) == 0) {
-        if (e & 0x40u) {
-            const uint32_t k = (e >> 8) & 31u;
-            e = lds32(t.tab_s + ((kL1Size + (e >> 16) + ((peek << kL1) >> (32 - k))) << 2));
-        } else {
-            e = slow_entry(t, peek);
-        }
-    }
-    return e;
+__device__ __forceinline__ unsigned long long lds64(uint32_t addr) {
+    unsigned long long v;
+    asm volatile("ld.shared.u64 %0, [%1];" : "=l"(v) : "r"(addr));
+    return v;
 }
 
-// Chunk bits staged in shared memory (big-endian words): a step is two LDS of
-// the words under the bit position, a funnel shift and the table lookup.
-// Positions are absolute bits of the staged window.
+// codeword longer than 12 bits at the top of `peek` -> sym << 16 | len
+__device__ __noinline__ uint32_t long_entry(const Tabs& t, uint32_t peek) {
+    const unsigned long long e3 = lds64(t.tab_s + (kOffT3 + 2 * (peek >> (32 - kL1))) * 4);
+    if (e3 & (1ull << 18)) return kLongInvalid;
+    if (e3 & (1ull << 17)) {
+        const uint32_t k = (uint32_t)(e3 >> 12) & 31u;
+        const uint32_t idx = (uint32_t)(e3 & 0xFFF) + ((peek << kL1) >> (32 - k));
+        return lds32(t.tab_s + (kOffL2 + idx) * 4);
+    }
+    for (int b = kL1 + 1; b <= t.mx; b++) {   // canonical limit search
+        const unsigned long long top = peek >> (32 - b);
+        if (top < sh_lim[b]) {
+            if (top < sh_first[b]) return kLongInvalid;
+            return (t.symbols[sh_off[b] + (long long)(top - sh_first[b])] << 16) | (uint32_t)b;
+        }
+    }
+    return kLongInvalid;
+}
+
+// one phase-1 table step at `peek`: total length, codeword count, start mask
+__device__ __forceinline__ void step1(const Tabs& t, uint32_t peek, uint32_t& len, uint32_t& m,
+                                      uint32_t& mask, uint32_t& bad) {
+    const uint32_t e = lds32(t.tab_s + ((peek >> (32 - kL1)) << 2));
+    if (e & 15u) {
+        len = e & 15u;
+        m = (e >> 4) & 15u;
+        mask = (e >> 8) & 0xFFFu;
+    } else {
+        const uint32_t ee = (e & kT1Invalid) ? kLongInvalid : long_entry(t, peek);
+        bad |= ee & 0x80u;
+        len = ee & 63u;
+        m = 1;
+        mask = 1;
+    }
+}
+
+// Chunk bits staged in shared memory (big-endian words): the peek is two LDS
+// of the words under the bit position and a funnel shift.  Positions are
+// absolute bits of the staged window.
 struct SmemReader {
     uint32_t base_s;   // shared address of word 0
     uint32_t a;        // bit position
-    __device__ __forceinline__ void init(uint32_t bit) { a = bit; }
+    __device__ __forceinline__ void seek(uint32_t bit) { a = bit; }
     __device__ __forceinline__ uint32_t pos() const { return a; }
-    __device__ __forceinline__ uint32_t step(const Tabs& t) {
+    __device__ __forceinline__ uint32_t peek() const {
         const uint32_t wa = base_s + ((a >> 5) << 2);
-        const uint32_t peek = __funnelshift_l(lds32(wa + 4), lds32(wa), a);
-        const uint32_t e = lookup(t, peek);
-        a += e & 63u;
-        return e;
+        return __funnelshift_l(lds32(wa + 4), lds32(wa), a);
     }
+    __device__ __forceinline__ void adv(uint32_t n) { a += n; }
 };
 
 // Chunk bits read from global memory: two words in registers + one prefetched.
@@ -217,7 +331,7 @@ struct GlobalReader {
     __device__ __forceinline__ uint32_t ld(uint32_t i) const {
         return bswap32(__ldg(w + (i < last ? i : last)));
     }
-    __device__ __forceinline__ void init(uint32_t bit) {
+    __device__ __forceinline__ void seek(uint32_t bit) {
         const uint32_t i = bit >> 5;
         p = bit;
         s = bit & 31u;
@@ -227,11 +341,10 @@ struct GlobalReader {
         w2 = ld(wi);
     }
     __device__ __forceinline__ uint32_t pos() const { return p; }
-    __device__ __forceinline__ uint32_t step(const Tabs& t) {
-        const uint32_t e = lookup(t, __funnelshift_l(w1, w0, s));
-        const uint32_t len = e & 63u;
-        const uint32_t s2 = s + len;
-        p += len;
+    __device__ __forceinline__ uint32_t peek() const { return __funnelshift_l(w1, w0, s); }
+    __device__ __forceinline__ void adv(uint32_t n) {   // n <= 32
+        const uint32_t s2 = s + n;
+        p += n;
         if (s2 >= 32) {
             w0 = w1;
             w1 = w2;
@@ -239,57 +352,81 @@ struct GlobalReader {
             w2 = ld(wi);
         }
         s = s2 & 31u;
-        return e;
     }
 };
 
-// Phase 1a: decode [A0, H) (H <= A0 + kWin) recording codeword starts
-// relative to A0 in (lo, hi); counts into k, ORs entries into fl.
+// 128-bit (lo, hi) view of `mask` (<= 12 bits) shifted left by r < 128
+__device__ __forceinline__ void shl128(uint32_t mask, uint32_t r, unsigned long long& lo,
+                                       unsigned long long& hi) {
+    const unsigned long long mm = mask;
+    lo = r < 64 ? (mm << r) : 0ull;
+    hi = r >= 64 ? (mm << (r - 64)) : (r > 52 ? (mm >> (64 - r)) : 0ull);
+}
+
+// Phase 1a: decode [A0, H) recording codeword starts relative to A0 in (lo, hi)
 template <class Rd>
 __device__ __forceinline__ void lane_head(const Tabs& t, Rd& rd, uint32_t A0, uint32_t H,
-                                          uint32_t& k, uint32_t& fl, unsigned long long& lo,
+                                          uint32_t& k, uint32_t& bad, unsigned long long& lo,
                                           unsigned long long& hi) {
-    const uint32_t h1 = A0 + 64 < H ? A0 + 64 : H;
     unsigned long long l = 0, h = 0;
-    while (rd.pos() < h1) {
-        l |= 1ull << (rd.pos() - A0);
-        fl |= rd.step(t);
-        k++;
-    }
     while (rd.pos() < H) {
-        h |= 1ull << (rd.pos() - A0 - 64);
-        fl |= rd.step(t);
-        k++;
+        uint32_t len, m, mask;
+        step1(t, rd.peek(), len, m, mask, bad);
+        unsigned long long a, b;
+        shl128(mask, rd.pos() - A0, a, b);
+        l |= a;
+        h |= b;
+        k += m;
+        rd.adv(len);
     }
     lo = l;
     hi = h;
 }
 
-// Phase 1b: decode to the slice end S (exit = first codeword start >= S),
-// then on into the next slice until a codeword start coincides with one of the
-// next lane's head boundaries (nlo, nhi, relative to S) -- the synchronisation
+// Phase 1b: decode to the slice end S (counting codewords that start before
+// S; exit = first codeword start >= S), then on until a codeword start is in
+// the next lane's head mask (nlo, nhi, relative to S) -- the synchronisation
 // point -- or T is reached.  kt counts the codewords in [exit, sync).
 template <class Rd>
 __device__ __forceinline__ bool lane_rest(const Tabs& t, Rd& rd, uint32_t S, uint32_t T,
                                           unsigned long long nlo, unsigned long long nhi,
-                                          uint32_t& k, uint32_t& fl, uint32_t& exit_pos,
+                                          uint32_t& k, uint32_t& bad, uint32_t& exit_pos,
                                           uint32_t& sync_pos, uint32_t& kt) {
     while (rd.pos() < S) {
-        fl |= rd.step(t);
-        k++;
+        const uint32_t p = rd.pos();
+        uint32_t len, m, mask;
+        step1(t, rd.peek(), len, m, mask, bad);
+        if (p + len <= S) {
+            k += m;
+            rd.adv(len);
+        } else {   // the step crosses S: count starts before S, stop at the first >= S
+            const uint32_t d = S - p;
+            k += __popc(mask & ((1u << d) - 1));
+            const uint32_t mh = mask >> d;
+            rd.adv(mh ? d + (uint32_t)__ffs(mh) - 1 : len);
+            break;
+        }
     }
     exit_pos = rd.pos();
     uint32_t n = 0;
     bool found = false;
     while (rd.pos() < T) {
         const uint32_t r = rd.pos() - S;
-        const unsigned long long m = r < 64 ? (nlo >> r) : (nhi >> (r - 64));
-        if (m & 1ull) {
+        uint32_t len, m, mask;
+        step1(t, rd.peek(), len, m, mask, bad);
+        unsigned long long a, b;
+        shl128(mask, r, a, b);
+        a &= nlo;
+        b &= nhi;
+        if (a | b) {
+            const uint32_t q = a ? (uint32_t)(__ffsll((long long)a) - 1) : 64u + (uint32_t)(__ffsll((long long)b) - 1);
+            n += __popc(mask & ((1u << (q - r)) - 1));
+            rd.adv(q - r);
             found = true;
             break;
         }
-        fl |= rd.step(t);
-        n++;
+        n += m;
+        rd.adv(len);
     }
     sync_pos = rd.pos();
     kt = n;
@@ -303,47 +440,84 @@ __device__ __forceinline__ uint32_t below(unsigned long long lo, unsigned long l
     return __popcll(lo) + __popcll(r >= 128 ? hi : (hi & ((1ull << (r - 64)) - 1)));
 }
 
-// phase 3 of one lane: `count` codewords from `start`, must end at `end`
+// Phase 3 of one lane: `count` codewords from `start` (must end at `end`) into
+// dst.  Symbols go through a 16-slot per-lane ring in shared memory; every
+// completed 16-byte output vector is written with one store.
 template <class Rd>
 __device__ __forceinline__ bool lane_store(const Tabs& t, Rd& rd, uint32_t start, uint32_t end,
-                                           uint32_t count, uint16_t* dst, uint32_t& zeros) {
-    rd.init(start);
-    uint32_t j = 0, z = 0, fl = 0;
-    const uint32_t head = (uint32_t)umin((8u - (((uint32_t)(uintptr_t)dst >> 1) & 7u)) & 7u, count);
-    for (; j < head; j++) {
-        const uint32_t e = rd.step(t);
-        fl |= e;
-        dst[j] = (uint16_t)(e >> 16);
-        z += e < 0x10000u;
-    }
-    for (; j + 8 <= count; j += 8) {
-        uint32_t v[4];
-#pragma unroll
-        for (int q = 0; q < 8; q++) {
-            const uint32_t e = rd.step(t);
-            fl |= e;
-            z += e < 0x10000u;
-            if (q & 1) v[q >> 1] |= e & 0xFFFF0000u;
-            else v[q >> 1] = e >> 16;
+                                           uint32_t count, uint16_t* dst, uint32_t ring_s,
+                                           uint32_t& zeros) {
+    rd.seek(start);
+    const uint32_t aoff = (uint32_t)((uintptr_t)dst >> 1) & 7u;   // slots before dst in its vector
+    uint16_t* const dal = dst - aoff;                               // 16-byte aligned
+    uint32_t P = aoff;              // next ring slot (absolute)
+    uint32_t nextv = 8;             // slot count at which vector (nextv/8 - 1) completes
+    uint32_t j = 0, bad = 0, z = 0;
+    while (j < count) {
+        const uint32_t peek = rd.peek();
+        unsigned long long e3 = lds64(t.tab_s + (kOffT3 + 2 * (peek >> (32 - kL1))) * 4);
+        uint32_t n3 = (uint32_t)(e3 >> 48) & 3u, len;
+        if (n3 == 0) {   // long codeword (or invalid pattern)
+            const uint32_t ee = long_entry(t, peek);
+            bad |= ee & 0x80u;
+            len = ee & 63u;
+            e3 = ee >> 16;
+            n3 = 1;
+            z += (ee >> 16) == 0;
+        } else if (j + n3 > count) {   // the span ends inside this step
+            const uint32_t take = count - j;
+            len = take == 1 ? (uint32_t)(e3 >> 50) & 15u : (uint32_t)(e3 >> 54) & 15u;
+            z += ((e3 & 0xFFFF) == 0) + (take > 1 && ((e3 >> 16) & 0xFFFF) == 0);
+            n3 = take;
+        } else {
+            len = (uint32_t)(e3 >> 58) & 15u;
+            z += (uint32_t)(e3 >> 62);
         }
-        *reinterpret_cast<uint4*>(dst + j) = make_uint4(v[0], v[1], v[2], v[3]);
+#pragma unroll
+        for (uint32_t q = 0; q < 3; q++) {
+            if (q < n3) {
+                asm volatile("st.shared.u16 [%0], %1;" ::"r"(ring_s + ((P + q) & 15u) * 2),
+                             "h"((unsigned short)(e3 >> (16 * q))));
+            }
+        }
+        P += n3;
+        j += n3;
+        rd.adv(len);
+        if (P >= nextv) {   // vector v = nextv/8 - 1 complete (lane-private ring)
+            const uint32_t v = nextv / 8 - 1;
+            const uint32_t rs = ring_s + ((8 * v) & 15u) * 2;
+            uint4 qv;
+            asm volatile("ld.shared.v2.u32 {%0, %1}, [%2];" : "=r"(qv.x), "=r"(qv.y) : "r"(rs));
+            asm volatile("ld.shared.v2.u32 {%0, %1}, [%2];" : "=r"(qv.z), "=r"(qv.w) : "r"(rs + 8));
+            if (v == 0 && aoff) {
+                const uint32_t h[8] = {qv.x & 0xFFFF, qv.x >> 16, qv.y & 0xFFFF, qv.y >> 16,
+                                       qv.z & 0xFFFF, qv.z >> 16, qv.w & 0xFFFF, qv.w >> 16};
+#pragma unroll
+                for (uint32_t s = 1; s < 8; s++)
+                    if (s >= aoff) dal[s] = (uint16_t)h[s];
+            } else {
+                *reinterpret_cast<uint4*>(dal + 8 * v) = qv;
+            }
+            nextv += 8;
+        }
     }
-    for (; j < count; j++) {
-        const uint32_t e = rd.step(t);
-        fl |= e;
-        dst[j] = (uint16_t)(e >> 16);
-        z += e < 0x10000u;
+    // trailing partial vector
+    const uint32_t v = nextv / 8 - 1;
+    for (uint32_t s = (v == 0 ? aoff : 0); 8 * v + s < P; s++) {
+        unsigned short h;
+        asm volatile("ld.shared.u16 %0, [%1];" : "=h"(h) : "r"(ring_s + ((8 * v + s) & 15u) * 2));
+        dal[8 * v + s] = h;
     }
     zeros += z;
-    return !(fl & 0x80u) && rd.pos() == end;
+    return !bad && rd.pos() == end;
 }
 
 // Phases 1-3 of one chunk by one warp; positions are absolute bits (the chunk
 // occupies [sbit, sbit + B)).  false = hand the chunk back.
 template <class Rd>
 __device__ __forceinline__ bool decode_chunk(const Tabs& t, Rd rd, uint32_t sbit, uint32_t B,
-                                             uint32_t cnt, uint16_t* out, uint32_t& zeros,
-                                             DevStatus* st) {
+                                             uint32_t cnt, uint16_t* out, uint32_t ring_s,
+                                             uint32_t& zeros, DevStatus* st) {
     const uint32_t lane = lane_id();
     uint32_t L = B / kSliceMin;
     L = L < 1 ? 1 : (L > 32 ? 32 : L);
@@ -352,17 +526,17 @@ __device__ __forceinline__ bool decode_chunk(const Tabs& t, Rd rd, uint32_t sbit
     const uint32_t s0 = sbit + (active ? (uint32_t)(((uint64_t)lane * B) / L) : B);
     const uint32_t s1 = sbit + (active ? (uint32_t)(((uint64_t)(lane + 1) * B) / L) : B);
     const uint32_t T = last || !active ? s1 : (s1 + kWin < sbit + B ? s1 + kWin : sbit + B);
-    uint32_t k = 0, fl = 0, ex = s1, sp = s1, kt = 0, start = s0;
+    uint32_t k = 0, bad = 0, ex = s1, sp = s1, kt = 0, start = s0;
     unsigned long long lo = 0, hi = 0;
     bool fwd = false;   // this lane's tail met the next lane's path
     if (active) {
-        rd.init(s0);
-        lane_head(t, rd, s0, s0 + kWin < s1 ? s0 + kWin : s1, k, fl, lo, hi);
+        rd.seek(s0);
+        lane_head(t, rd, s0, s0 + kWin < s1 ? s0 + kWin : s1, k, bad, lo, hi);
     }
     const unsigned long long nlo = __shfl_down_sync(kFull, lo, 1);
     const unsigned long long nhi = __shfl_down_sync(kFull, hi, 1);
-    if (active) fwd = lane_rest(t, rd, s1, T, nlo, nhi, k, fl, ex, sp, kt);
-    bool ok = !(fl & 0x80u);
+    if (active) fwd = lane_rest(t, rd, s1, T, nlo, nhi, k, bad, ex, sp, kt);
+    bool ok = bad == 0;
     // phase 2: lane l is on the true path if lane l-1 is and l-1's tail met it;
     // the first lane that is not redecodes from its predecessor's exit
     bool restarted = lane == 0;
@@ -372,21 +546,21 @@ __device__ __forceinline__ bool decode_chunk(const Tabs& t, Rd rd, uint32_t sbit
         const uint32_t pe = __shfl_up_sync(kFull, ex, 1);
         const uint32_t psp = __shfl_up_sync(kFull, sp, 1);
         const bool synced = !active || (ok && (restarted || pfwd));
-        const unsigned bad = __ballot_sync(kFull, !synced);
-        if (bad == 0) {
+        const unsigned badl = __ballot_sync(kFull, !synced);
+        if (badl == 0) {
             if (active && !restarted) q = psp;
             break;
         }
-        const uint32_t f = (uint32_t)(__ffs(bad) - 1);
+        const uint32_t f = (uint32_t)(__ffs(badl) - 1);
         if (f == 0 || round >= L) return false;
         if (lane == f) {
             restarted = true;
             q = start = pe;
             k = 0;
-            fl = 0;
-            rd.init(pe);
-            fwd = lane_rest(t, rd, s1, T, nlo, nhi, k, fl, ex, sp, kt);
-            ok = !(fl & 0x80u);
+            bad = 0;
+            rd.seek(pe);
+            fwd = lane_rest(t, rd, s1, T, nlo, nhi, k, bad, ex, sp, kt);
+            ok = bad == 0;
             atomicAdd(&st->pad[0], 1ull);   // diagnostics: lane redecodes
         }
         if (!__shfl_sync(kFull, ok ? 1u : 0u, f)) return false;
@@ -408,16 +582,17 @@ __device__ __forceinline__ bool decode_chunk(const Tabs& t, Rd rd, uint32_t sbit
     bool ok3 = true;
     uint32_t z = 0;
     const uint32_t end = last ? sbit + B : nq;
-    if (active && nl) ok3 = lane_store(t, rd, q, end, nl, out + o, z);
+    if (active && nl) ok3 = lane_store(t, rd, q, end, nl, out + o, ring_s, z);
     if (!__all_sync(kFull, ok3)) return false;
     zeros += z;
     return true;
 }
 
-constexpr int kWarps = 8;
+constexpr int kWarps = 32;            // one CTA per SM shares one copy of the tables
+constexpr uint32_t kRingStride = 40;   // 16 u16 slots per lane + 8 bytes: 2-way bank conflicts
 
-// dynamic shared memory: tables (kTabWords) then one staging buffer of
-// `stage_words` words per warp
+// dynamic shared memory: tables (kTabWords) | per-lane rings | one staging
+// buffer of `stage_words` words per warp
 __global__ void __launch_bounds__(kWarps * 32) inflate_fast_kernel(
     const uint8_t* __restrict__ payload, uint64_t nwords, const uint32_t* __restrict__ chunk_bits,
     const unsigned long long* __restrict__ byte_off, uint64_t nchunks, uint32_t chunk, uint64_t n,
@@ -451,7 +626,8 @@ __global__ void __launch_bounds__(kWarps * 32) inflate_fast_kernel(
     t.symbols = symbols;
     t.mx = mx;
     const uint32_t lane = lane_id(), wid = threadIdx.x >> 5;
-    uint32_t* stage = s_tab + kTabWords + wid * stage_words;
+    const uint32_t ring_s = smem_base + kTabWords * 4 + threadIdx.x * kRingStride;
+    uint32_t* stage = s_tab + kTabWords + (kWarps * 32 * kRingStride) / 4 + wid * stage_words;
     const uint32_t* words = reinterpret_cast<const uint32_t*>(payload);
     const uint4* words4 = reinterpret_cast<const uint4*>(payload);
     uint32_t zeros_total = 0;
@@ -480,14 +656,15 @@ __global__ void __launch_bounds__(kWarps * 32) inflate_fast_kernel(
             __syncwarp();
             SmemReader rd;
             rd.base_s = (uint32_t)__cvta_generic_to_shared(stage);
-            good = decode_chunk(t, rd, sbit, B, cnt, out + base, zeros_total, st);
+            good = decode_chunk(t, rd, sbit, B, cnt, out + base, ring_s, zeros_total, st);
             __syncwarp();   // the stage is refilled by the next chunk
         } else {
             const uint64_t wbase = boff >> 2;
             GlobalReader rd;
             rd.w = words + wbase;
             rd.last = (uint32_t)umin(nwords > wbase ? nwords - 1 - wbase : 0, 0xFFFFFFFFull);
-            good = decode_chunk(t, rd, (uint32_t)(boff & 3) * 8, B, cnt, out + base, zeros_total, st);
+            good = decode_chunk(t, rd, (uint32_t)(boff & 3) * 8, B, cnt, out + base, ring_s,
+                                zeros_total, st);
         }
         if (!good && lane == 0) {
             redo[c] = 1;
@@ -502,11 +679,12 @@ __global__ void __launch_bounds__(kWarps * 32) inflate_fast_kernel(
 }  // namespace
 
 int launch_decode_tables(sdqz_ctx* ctx, const uint64_t* first, const int64_t* offsets,
-                         const uint32_t* symbols, int max_bw, uint32_t** tab_out) {
+                         const uint32_t* symbols, int max_bw, uint32_t** tab_out, uint32_t* old_lut) {
     int rc = SDQZ_OK;
     uint32_t* tab = scratch_as<uint32_t>(ctx, S_DTAB, kTabWords, &rc);
     if (!tab) return rc;
-    dtab_kernel<<<1, 1024, 0, ctx->stream>>>(first, offsets, symbols, max_bw, ctx->d_status, tab);
+    dtab_kernel<<<1, 1024, 0, ctx->stream>>>(first, offsets, symbols, max_bw, ctx->d_status, tab,
+                                             old_lut);
     SDQZ_LAUNCHED_NAMED(ctx, "dtab_kernel");
     *tab_out = tab;
     return SDQZ_OK;
@@ -523,9 +701,13 @@ int launch_inflate_fast(sdqz_ctx* ctx, const uint8_t* payload, uint64_t nwords,
     SDQZ_CUDA(ctx, cudaMemsetAsync(counter, 0, sizeof(unsigned int), ctx->stream));
     // per-warp staging: room for ~2x the average chunk (bigger chunks read global memory)
     const uint64_t avg = n_chunks ? (nwords * 4) / n_chunks : 0;
-    uint32_t stage_words = 256;
-    while (stage_words < 2048 && stage_words * 4 < 2 * avg + 64) stage_words <<= 1;
-    const size_t smem = (kTabWords + (size_t)kWarps * stage_words) * 4;
+    const size_t fixed = (size_t)kTabWords * 4 + (size_t)kWarps * 32 * kRingStride;
+    int smem_max = 0;
+    cudaDeviceGetAttribute(&smem_max, cudaDevAttrMaxSharedMemoryPerBlockOptin, ctx->device);
+    const uint32_t room = (uint32_t)(((size_t)smem_max - 1024 - fixed) / (kWarps * 4)) & ~15u;
+    uint32_t stage_words = (uint32_t)umin(((2 * avg + 64) / 4 + 15) & ~15ull, room);
+    if (stage_words < 64) stage_words = 64;
+    const size_t smem = fixed + (size_t)kWarps * stage_words * 4;
     static size_t attr_smem = 0;
     if (smem > attr_smem) {
         cudaFuncSetAttribute(inflate_fast_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
