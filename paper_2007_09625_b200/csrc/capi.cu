@@ -55,32 +55,27 @@ void* scratch(sdqz_ctx* ctx, int slot, size_t bytes, cudaError_t* e) {
 
 namespace {
 
-__global__ void init_status_kernel(DevStatus* st) {
+__global__ void init_status_kernel(DevStatus* st, double eb, int has_eb) {
     memset(st, 0, sizeof(DevStatus));
     st->decode_key = ~0ull;
     st->vmin_bits = ~0ull;
     st->vmax_bits = 0;
-}
-
-__global__ void set_eb_kernel(DevStatus* st, double eb) {
-    st->eb = eb;
-    st->two_eb = __dmul_rn(2.0, eb);
+    if (has_eb) {   // a known absolute bound (decompress / stage calls)
+        st->eb = eb;
+        st->two_eb = __dmul_rn(2.0, eb);
+    }
 }
 
 }  // namespace
 
-int reset_status(sdqz_ctx* ctx) {
+int reset_status(sdqz_ctx* ctx) { return reset_status_eb(ctx, 0.0, false); }
+
+int reset_status_eb(sdqz_ctx* ctx, double eb, bool has_eb) {
     // host time since the last sync (Python, argument checks) is "(host)", not
     // the first kernel's
     if (ctx->timing) kt_mark(ctx, "(host)");
-    init_status_kernel<<<1, 1, 0, ctx->stream>>>(ctx->d_status);
+    init_status_kernel<<<1, 1, 0, ctx->stream>>>(ctx->d_status, eb, has_eb ? 1 : 0);
     SDQZ_LAUNCHED_NAMED(ctx, "init_status_kernel");
-    return SDQZ_OK;
-}
-
-int set_eb(sdqz_ctx* ctx, double eb) {
-    set_eb_kernel<<<1, 1, 0, ctx->stream>>>(ctx->d_status, eb);
-    SDQZ_LAUNCHED_NAMED(ctx, "set_eb_kernel");
     return SDQZ_OK;
 }
 
@@ -231,8 +226,7 @@ int decompress_core(sdqz_ctx* ctx, const sdqz_header* hdr, const uint8_t* d_bw, 
     if (!codes || !dense || !bflag) return rc;
     uint32_t safe_block[3];
     for (int a = 0; a < 3; a++) safe_block[a] = hdr->block[a] ? hdr->block[a] : 1;
-    if ((rc = reset_status(ctx))) return rc;
-    if ((rc = set_eb(ctx, hdr->eb_resolved))) return rc;
+    if ((rc = reset_status_eb(ctx, hdr->eb_resolved, true))) return rc;
     SDQZ_CUDA(ctx, cudaMemsetAsync(bflag, 0, nblocks, ctx->stream));
     // canonical tables from the stored bitwidths (deserialize checks + canonize)
     if ((rc = launch_codebook(ctx, nullptr, const_cast<uint8_t*>(d_bw), cap, book, false, true, true)))
@@ -391,7 +385,7 @@ int sdqz_describe(sdqz_ctx* ctx, const void* d_in, int dtype, uint64_t n, double
 int sdqz_prequantize(sdqz_ctx* ctx, const void* d_in, int dtype, uint64_t n, double eb,
                      double* d_out) {
     int rc;
-    if ((rc = reset_status(ctx)) || (rc = set_eb(ctx, eb))) return rc;
+    if ((rc = reset_status_eb(ctx, eb, true))) return rc;
     if ((rc = launch_prequantize(ctx, d_in, dtype, n, d_out))) return rc;
     return fetch_status(ctx);
 }
@@ -401,7 +395,7 @@ int sdqz_dualquant(sdqz_ctx* ctx, const void* d_in, int in_kind, int ndims, cons
                    uint64_t* d_hist, int* nonfinite) {
     int rc;
     if (ndims < 1 || ndims > 3 || !valid_cap(cap)) return set_error(ctx, SDQZ_EINVAL, "bad geometry");
-    if ((rc = reset_status(ctx)) || (rc = set_eb(ctx, eb))) return rc;
+    if ((rc = reset_status_eb(ctx, eb, true))) return rc;
     if (d_hist) SDQZ_CUDA(ctx, cudaMemsetAsync(d_hist, 0, cap * 8ull, ctx->stream));
     if ((rc = launch_dualquant(ctx, d_in, in_kind, ndims, dims, block, cap, d_codes,
                                (unsigned long long*)d_hist)))
@@ -416,7 +410,7 @@ int sdqz_outliers(sdqz_ctx* ctx, const void* d_in, int in_kind, const uint16_t* 
     int rc;
     *k_out = 0;
     if (n == 0) return SDQZ_OK;
-    if ((rc = reset_status(ctx)) || (rc = set_eb(ctx, eb))) return rc;
+    if ((rc = reset_status_eb(ctx, eb, true))) return rc;
     uint32_t* cbits = scratch_as<uint32_t>(ctx, S_CHUNK_BITS, ceil_div(n, 4096), &rc);
     if (!cbits) return rc;
     DeflateJob job;
@@ -447,7 +441,7 @@ int sdqz_reconstruct(sdqz_ctx* ctx, const void* d_codes, int code_bytes, uint64_
                      void* d_out, int out_kind) {
     int rc = SDQZ_OK;
     const uint16_t* codes = (const uint16_t*)d_codes;
-    if ((rc = reset_status(ctx)) || (rc = set_eb(ctx, eb))) return rc;
+    if ((rc = reset_status_eb(ctx, eb, true))) return rc;
     if (code_bytes == 4) {
         uint16_t* c16 = scratch_as<uint16_t>(ctx, S_CODES, n + 64, &rc);
         if (!c16) return rc;

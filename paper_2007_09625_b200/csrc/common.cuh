@@ -194,6 +194,7 @@ int cuda_check(sdqz_ctx* ctx, cudaError_t e, const char* what);
 void* scratch(sdqz_ctx* ctx, int slot, size_t bytes, cudaError_t* e);
 int fetch_status(sdqz_ctx* ctx);      // D2H of the status block + sync
 int reset_status(sdqz_ctx* ctx);      // memset status on stream
+int reset_status_eb(sdqz_ctx* ctx, double eb, bool has_eb);   // ... and set eb / 2eb
 
 #define SDQZ_CUDA(ctx, expr)                                                      \
     do {                                                                          \

@@ -12,6 +12,7 @@
 //       shared memory, canonical fallback for longer codewords, the
 //       reference's error checks in lockstep priority order.
 #include "kernels.cuh"
+#include "scan.cuh"
 
 namespace sdqz {
 
@@ -650,88 +651,8 @@ __global__ void __launch_bounds__(256) chunk_stats_kernel(DeflateArgs a) {
 // (ceil(bits/8)) and outlier offsets.  Tiles of 4096 chunks are staged in
 // shared memory with coalesced loads; each thread scans 4 consecutive entries.
 __global__ void __launch_bounds__(1024) chunk_scan_kernel(DeflateArgs a) {
-    // one CTA; tiles of 16384 chunks, 16 consecutive chunks per thread, all of
-    // a tile's loads issued before the first use (one memory latency per tile)
-    constexpr int kPer = 16, kTile = 1024 * kPer;
-    __shared__ unsigned long long wsb[32], wso[32];
-    const uint64_t C = a.nchunks;
-    const uint32_t tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
-    unsigned long long carry_b = 0, carry_o = 0;
-    for (uint64_t t0 = 0; t0 < C; t0 += kTile) {
-        const uint64_t i0 = t0 + (uint64_t)tid * kPer;
-        uint32_t vb[kPer], vz[kPer];
-        const bool vec = (((uintptr_t)a.chunk_bits | (uintptr_t)a.chunk_zeros) & 15) == 0;
-        if (vec && i0 + kPer <= C) {
-#pragma unroll
-            for (int q = 0; q < kPer; q += 4) {
-                const uint4 u = *reinterpret_cast<const uint4*>(a.chunk_bits + i0 + q);
-                vb[q] = u.x; vb[q + 1] = u.y; vb[q + 2] = u.z; vb[q + 3] = u.w;
-            }
-            if (a.chunk_zeros) {
-#pragma unroll
-                for (int q = 0; q < kPer; q += 4) {
-                    const uint4 u = *reinterpret_cast<const uint4*>(a.chunk_zeros + i0 + q);
-                    vz[q] = u.x; vz[q + 1] = u.y; vz[q + 2] = u.z; vz[q + 3] = u.w;
-                }
-            } else {
-#pragma unroll
-                for (int q = 0; q < kPer; q++) vz[q] = 0;
-            }
-        } else {
-#pragma unroll
-            for (int q = 0; q < kPer; q++) {
-                const bool in = i0 + q < C;
-                vb[q] = in ? a.chunk_bits[i0 + q] : 0;
-                vz[q] = in && a.chunk_zeros ? a.chunk_zeros[i0 + q] : 0;
-            }
-        }
-        unsigned long long tb = 0, to = 0;
-#pragma unroll
-        for (int q = 0; q < kPer; q++) {
-            vb[q] = (vb[q] + 7) >> 3;
-            tb += vb[q];
-            to += vz[q];
-        }
-        unsigned long long xb = tb, xo = to;
-#pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-            unsigned long long yb = __shfl_up_sync(kFull, xb, o), yo = __shfl_up_sync(kFull, xo, o);
-            if (lane >= (uint32_t)o) { xb += yb; xo += yo; }
-        }
-        if (lane == 31) { wsb[wid] = xb; wso[wid] = xo; }
-        __syncthreads();
-        if (wid == 0) {
-            unsigned long long ub = wsb[lane], uo = wso[lane];
-#pragma unroll
-            for (int o = 1; o < 32; o <<= 1) {
-                unsigned long long yb = __shfl_up_sync(kFull, ub, o), yo = __shfl_up_sync(kFull, uo, o);
-                if (lane >= (uint32_t)o) { ub += yb; uo += yo; }
-            }
-            wsb[lane] = ub;
-            wso[lane] = uo;
-        }
-        __syncthreads();
-        unsigned long long rb = carry_b + (wid ? wsb[wid - 1] : 0) + xb - tb;
-        unsigned long long ro = carry_o + (wid ? wso[wid - 1] : 0) + xo - to;
-#pragma unroll
-        for (int q = 0; q < kPer; q++) {
-            if (i0 + q < C) {
-                a.byte_off[i0 + q] = rb;
-                if (a.out_off) a.out_off[i0 + q] = ro;
-            }
-            rb += vb[q];
-            ro += vz[q];
-        }
-        carry_b += wsb[31];
-        carry_o += wso[31];
-        __syncthreads();
-    }
-    if (tid == 0) {
-        a.st->payload_bytes = carry_b;
-        a.st->n_outliers = carry_o;
-        if (carry_b > a.payload_cap || (a.records && carry_o > a.out_cap))
-            atomicOr(&a.st->flags, (unsigned long long)F_OVERFLOW);
-    }
+    block_chunk_scan(a.chunk_bits, a.chunk_zeros, a.nchunks, a.byte_off, a.out_off, a.payload_cap,
+                     a.records != nullptr, a.out_cap, a.st);
 }
 
 __device__ __forceinline__ void store_word(uint8_t* payload, uint64_t wbyte, uint32_t word,
@@ -1563,10 +1484,10 @@ int launch_inflate(sdqz_ctx* ctx, const uint8_t* payload, uint64_t payload_bytes
     a.st = ctx->d_status;
     a.byte_off = scratch_as<unsigned long long>(ctx, S_BYTE_OFF, n_chunks, &rc);
     if (!a.byte_off) return rc;
-    chunk_scan_kernel<<<1, 1024, 0, ctx->stream>>>(a);
-    SDQZ_LAUNCHED_NAMED(ctx, "chunk_scan_kernel");
     uint64_t grid = ceil_div(n_chunks, 64);
     if (out32) {
+        chunk_scan_kernel<<<1, 1024, 0, ctx->stream>>>(a);
+        SDQZ_LAUNCHED_NAMED(ctx, "chunk_scan_kernel");
         inflate_kernel<true><<<(unsigned)grid, 64, 0, ctx->stream>>>(
             payload, nwords, chunk_bits, a.byte_off, n_chunks, chunk, n, first, offsets, symbols, lut,
             max_bw, codes, ctx->d_status, nullptr);
@@ -1576,10 +1497,10 @@ int launch_inflate(sdqz_ctx* ctx, const uint8_t* payload, uint64_t payload_bytes
     // warp-parallel decode; chunks it hands back are redone sequentially
     uint8_t* redo = scratch_as<uint8_t>(ctx, S_REDO, n_chunks, &rc);
     if (!redo) return rc;
-    SDQZ_CUDA(ctx, cudaMemsetAsync(redo, 0, n_chunks, ctx->stream));
+    // one launch: decode tables (+ the fallback LUT) | chunk byte offsets + clears
     uint32_t* tab = nullptr;
-    if ((rc = launch_decode_tables(ctx, first, offsets, symbols, max_bw, &tab,
-                                   const_cast<uint32_t*>(lut))))
+    if ((rc = launch_decode_prep(ctx, first, offsets, symbols, max_bw, &tab, const_cast<uint32_t*>(lut),
+                                 chunk_bits, n_chunks, a.byte_off, redo)))
         return rc;
     if ((rc = launch_inflate_fast(ctx, payload, nwords, chunk_bits, a.byte_off, n_chunks, chunk, n,
                                   first, offsets, symbols, tab, max_bw, (uint16_t*)codes, redo)))

@@ -31,6 +31,7 @@
 // handed to the sequential decoder (huffman.cu inflate_kernel), which
 // reproduces the reference's exact error semantics.
 #include "kernels.cuh"
+#include "scan.cuh"
 
 namespace sdqz {
 
@@ -59,12 +60,11 @@ constexpr uint32_t kLongInvalid = 0x81;    // len 1 + flag (sym|len form)
 // ---------------------------------------------------------------------------
 // decode tables: one CTA
 // ---------------------------------------------------------------------------
-__global__ void __launch_bounds__(1024) dtab_kernel(const uint64_t* __restrict__ first,
-                                                    const int64_t* __restrict__ offsets,
-                                                    const uint32_t* __restrict__ symbols,
-                                                    int max_bw_arg, const DevStatus* st,
-                                                    uint32_t* __restrict__ tab,
-                                                    uint32_t* __restrict__ old_lut) {
+__device__ __forceinline__ void dtab_body(const uint64_t* __restrict__ first,
+                                          const int64_t* __restrict__ offsets,
+                                          const uint32_t* __restrict__ symbols, int max_bw_arg,
+                                          const DevStatus* st, uint32_t* __restrict__ tab,
+                                          uint32_t* __restrict__ old_lut) {
     __shared__ uint32_t pmax[kL1Size];
     __shared__ uint32_t s_one[kL1Size];   // first codeword of a 12-bit window: sym << 16 | len
     __shared__ uint16_t pbase[kL1Size];   // second-level base, 0xFFFF = none
@@ -243,6 +243,31 @@ __global__ void __launch_bounds__(1024) dtab_kernel(const uint64_t* __restrict__
         const uint32_t start = pbase[p] + (low << (k - extra));
         const uint32_t e = (symbols[i] << 16) | (uint32_t)b;
         for (uint32_t j = 0; j < (1u << (k - extra)); j++) tab[kOffL2 + start + j] = e;
+    }
+}
+
+__global__ void __launch_bounds__(1024) dtab_kernel(const uint64_t* __restrict__ first,
+                                                    const int64_t* __restrict__ offsets,
+                                                    const uint32_t* __restrict__ symbols,
+                                                    int max_bw_arg, const DevStatus* st,
+                                                    uint32_t* __restrict__ tab,
+                                                    uint32_t* __restrict__ old_lut) {
+    dtab_body(first, offsets, symbols, max_bw_arg, st, tab, old_lut);
+}
+
+// decompress prep in one launch: CTA 0 builds the decode tables, CTA 1 scans the
+// chunk byte offsets and clears the hand-back flags and the chunk counter
+__global__ void __launch_bounds__(1024) decode_prep_kernel(
+    const uint64_t* __restrict__ first, const int64_t* __restrict__ offsets,
+    const uint32_t* __restrict__ symbols, int max_bw_arg, DevStatus* st, uint32_t* __restrict__ tab,
+    uint32_t* __restrict__ old_lut, const uint32_t* __restrict__ chunk_bits, uint64_t C,
+    unsigned long long* __restrict__ byte_off, uint8_t* __restrict__ redo, unsigned int* counter) {
+    if (blockIdx.x == 0) {
+        dtab_body(first, offsets, symbols, max_bw_arg, st, tab, old_lut);
+    } else {
+        for (uint64_t i = threadIdx.x; i < C; i += blockDim.x) redo[i] = 0;
+        if (threadIdx.x == 0) *counter = 0;
+        block_chunk_scan(chunk_bits, nullptr, C, byte_off, nullptr, ~0ull, false, 0, st);
     }
 }
 
@@ -690,15 +715,30 @@ int launch_decode_tables(sdqz_ctx* ctx, const uint64_t* first, const int64_t* of
     return SDQZ_OK;
 }
 
+int launch_decode_prep(sdqz_ctx* ctx, const uint64_t* first, const int64_t* offsets,
+                       const uint32_t* symbols, int max_bw, uint32_t** tab_out, uint32_t* old_lut,
+                       const uint32_t* chunk_bits, uint64_t n_chunks, unsigned long long* byte_off,
+                       uint8_t* redo) {
+    int rc = SDQZ_OK;
+    uint32_t* tab = scratch_as<uint32_t>(ctx, S_DTAB, kTabWords, &rc);
+    unsigned int* counter = scratch_as<unsigned int>(ctx, S_COUNTER, 4, &rc);
+    if (!tab || !counter) return rc;
+    decode_prep_kernel<<<2, 1024, 0, ctx->stream>>>(first, offsets, symbols, max_bw, ctx->d_status, tab,
+                                                    old_lut, chunk_bits, n_chunks, byte_off, redo,
+                                                    counter);
+    SDQZ_LAUNCHED_NAMED(ctx, "decode_prep_kernel");
+    *tab_out = tab;
+    return SDQZ_OK;
+}
+
 int launch_inflate_fast(sdqz_ctx* ctx, const uint8_t* payload, uint64_t nwords,
                         const uint32_t* chunk_bits, const unsigned long long* byte_off,
                         uint64_t n_chunks, uint32_t chunk, uint64_t n, const uint64_t* first,
                         const int64_t* offsets, const uint32_t* symbols, const uint32_t* tab,
                         int max_bw, uint16_t* codes, uint8_t* redo) {
     int rc = SDQZ_OK;
-    unsigned int* counter = scratch_as<unsigned int>(ctx, S_COUNTER, 4, &rc);
+    unsigned int* counter = scratch_as<unsigned int>(ctx, S_COUNTER, 4, &rc);   // cleared by the prep kernel
     if (!counter) return rc;
-    SDQZ_CUDA(ctx, cudaMemsetAsync(counter, 0, sizeof(unsigned int), ctx->stream));
     // per-warp staging: room for ~2x the average chunk (bigger chunks read global memory)
     const uint64_t avg = n_chunks ? (nwords * 4) / n_chunks : 0;
     const size_t fixed = (size_t)kTabWords * 4 + (size_t)kWarps * 32 * kRingStride;

@@ -72,6 +72,10 @@ int launch_inflate(sdqz_ctx* ctx, const uint8_t* payload, uint64_t payload_bytes
 // (old_lut, if non-null, also receives the sequential decoder's 12-bit table)
 int launch_decode_tables(sdqz_ctx* ctx, const uint64_t* first, const int64_t* offsets,
                          const uint32_t* symbols, int max_bw, uint32_t** tab_out, uint32_t* old_lut);
+int launch_decode_prep(sdqz_ctx* ctx, const uint64_t* first, const int64_t* offsets,
+                       const uint32_t* symbols, int max_bw, uint32_t** tab_out, uint32_t* old_lut,
+                       const uint32_t* chunk_bits, uint64_t n_chunks, unsigned long long* byte_off,
+                       uint8_t* redo);
 int launch_inflate_fast(sdqz_ctx* ctx, const uint8_t* payload, uint64_t nwords,
                         const uint32_t* chunk_bits, const unsigned long long* byte_off,
                         uint64_t n_chunks, uint32_t chunk, uint64_t n, const uint64_t* first,
