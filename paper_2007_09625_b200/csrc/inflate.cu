@@ -295,16 +295,10 @@ __device__ __forceinline__ unsigned long long lds64(uint32_t addr) {
     return v;
 }
 
-// codeword longer than 12 bits at the top of `peek` -> sym << 16 | len
-__device__ __noinline__ uint32_t long_entry(const Tabs& t, uint32_t peek) {
-    const unsigned long long e3 = lds64(t.tab_s + (kOffT3 + 2 * (peek >> (32 - kL1))) * 4);
-    if (e3 & (1ull << 18)) return kLongInvalid;
-    if (e3 & (1ull << 17)) {
-        const uint32_t k = (uint32_t)(e3 >> 12) & 31u;
-        const uint32_t idx = (uint32_t)(e3 & 0xFFF) + ((peek << kL1) >> (32 - k));
-        return lds32(t.tab_s + (kOffL2 + idx) * 4);
-    }
-    for (int b = kL1 + 1; b <= t.mx; b++) {   // canonical limit search
+// codeword longer than 12 bits at the top of `peek`, past the second-level
+// budget: canonical limit search -> sym << 16 | len
+__device__ __noinline__ uint32_t long_search(const Tabs& t, uint32_t peek) {
+    for (int b = kL1 + 1; b <= t.mx; b++) {
         const unsigned long long top = peek >> (32 - b);
         if (top < sh_lim[b]) {
             if (top < sh_first[b]) return kLongInvalid;
@@ -312,6 +306,22 @@ __device__ __noinline__ uint32_t long_entry(const Tabs& t, uint32_t peek) {
         }
     }
     return kLongInvalid;
+}
+
+// codeword longer than 12 bits at the top of `peek` -> sym << 16 | len, given
+// the window's T3 entry (second-level pointer)
+__device__ __forceinline__ uint32_t long_entry3(const Tabs& t, uint32_t peek, unsigned long long e3) {
+    if (e3 & (1ull << 17)) {
+        const uint32_t k = (uint32_t)(e3 >> 12) & 31u;
+        const uint32_t idx = (uint32_t)(e3 & 0xFFF) + ((peek << kL1) >> (32 - k));
+        return lds32(t.tab_s + (kOffL2 + idx) * 4);
+    }
+    if (e3 & (1ull << 18)) return kLongInvalid;
+    return long_search(t, peek);
+}
+
+__device__ __forceinline__ uint32_t long_entry(const Tabs& t, uint32_t peek) {
+    return long_entry3(t, peek, lds64(t.tab_s + (kOffT3 + 2 * (peek >> (32 - kL1))) * 4));
 }
 
 // one phase-1 table step at `peek`: total length, codeword count, start mask
@@ -388,19 +398,35 @@ __device__ __forceinline__ void shl128(uint32_t mask, uint32_t r, unsigned long 
     hi = r >= 64 ? (mm << (r - 64)) : (r > 52 ? (mm >> (64 - r)) : 0ull);
 }
 
-// Phase 1a: decode [A0, H) recording codeword starts relative to A0 in (lo, hi)
+// Phase 1a: decode [A0, H) recording codeword starts relative to A0 in (lo, hi).
+// The position only grows, so the 128-bit record splits into three loops with
+// plain 64-bit shifts: steps wholly inside lo, steps straddling 64, steps in hi.
 template <class Rd>
 __device__ __forceinline__ void lane_head(const Tabs& t, Rd& rd, uint32_t A0, uint32_t H,
                                           uint32_t& k, uint32_t& bad, unsigned long long& lo,
                                           unsigned long long& hi) {
     unsigned long long l = 0, h = 0;
+    const uint32_t h52 = A0 + 52 < H ? A0 + 52 : H, h64 = A0 + 64 < H ? A0 + 64 : H;
+    while (rd.pos() < h52) {   // mask (12 bits) << r stays below bit 64
+        uint32_t len, m, mask;
+        step1(t, rd.peek(), len, m, mask, bad);
+        l |= (unsigned long long)mask << (rd.pos() - A0);
+        k += m;
+        rd.adv(len);
+    }
+    while (rd.pos() < h64) {
+        uint32_t len, m, mask;
+        step1(t, rd.peek(), len, m, mask, bad);
+        const uint32_t r = rd.pos() - A0;
+        l |= (unsigned long long)mask << r;
+        h |= (unsigned long long)mask >> (64 - r);
+        k += m;
+        rd.adv(len);
+    }
     while (rd.pos() < H) {
         uint32_t len, m, mask;
         step1(t, rd.peek(), len, m, mask, bad);
-        unsigned long long a, b;
-        shl128(mask, rd.pos() - A0, a, b);
-        l |= a;
-        h |= b;
+        h |= (unsigned long long)mask << (rd.pos() - A0 - 64);
         k += m;
         rd.adv(len);
     }
@@ -435,7 +461,25 @@ __device__ __forceinline__ bool lane_rest(const Tabs& t, Rd& rd, uint32_t S, uin
     exit_pos = rd.pos();
     uint32_t n = 0;
     bool found = false;
-    while (rd.pos() < T) {
+    // synchronisation usually comes within a few codewords: steps that start
+    // below bit 52 of the window compare against nlo alone
+    const uint32_t t52 = S + 52 < T ? S + 52 : T;
+    while (rd.pos() < t52) {
+        const uint32_t r = rd.pos() - S;
+        uint32_t len, m, mask;
+        step1(t, rd.peek(), len, m, mask, bad);
+        const unsigned long long a = ((unsigned long long)mask << r) & nlo;
+        if (a) {
+            const uint32_t q = (uint32_t)(__ffsll((long long)a) - 1);
+            n += __popc(mask & ((1u << (q - r)) - 1));
+            rd.adv(q - r);
+            found = true;
+            break;
+        }
+        n += m;
+        rd.adv(len);
+    }
+    while (!found && rd.pos() < T) {
         const uint32_t r = rd.pos() - S;
         uint32_t len, m, mask;
         step1(t, rd.peek(), len, m, mask, bad);
@@ -483,7 +527,7 @@ __device__ __forceinline__ bool lane_store(const Tabs& t, Rd& rd, uint32_t start
         unsigned long long e3 = lds64(t.tab_s + (kOffT3 + 2 * (peek >> (32 - kL1))) * 4);
         uint32_t n3 = (uint32_t)(e3 >> 48) & 3u, len;
         if (n3 == 0) {   // long codeword (or invalid pattern)
-            const uint32_t ee = long_entry(t, peek);
+            const uint32_t ee = long_entry3(t, peek, e3);
             bad |= ee & 0x80u;
             len = ee & 63u;
             e3 = ee >> 16;
