@@ -208,7 +208,9 @@ def algorithmic_bytes(kernel: str, n: int, k: int, c: int, p: int) -> int | None
         "chunk_pack32_kernel": 2 * n + p + 20 * k + 12 * c,  # codes, payload, outliers (+ input reads)
         "chunk_pack_kernel": 2 * n + p + 20 * k + 12 * c,
         "inflate_fast_kernel": p + 12 * c + 2 * n,         # payload, chunk bits + offsets, codes written
-        "rq_fast": 2 * n + 4 * n + 8 * k,                  # codes read, field written, outlier values
+        "rq3d_block_kernel": 2 * n + 4 * n + 8 * k,        # codes read, field written, outlier values
+        "rq2d_kernel": 2 * n + 4 * n + 8 * k,
+        "rq1d_kernel": 2 * n + 4 * n + 8 * k,
         "outlier_scatter_kernel": 16 * k + 8 * k + 2 * k,
     }
     for key, v in table.items():
@@ -226,12 +228,17 @@ def load_peak():
 
 
 def load_traffic(config: str, kernel: str):
+    """dram read+write bytes per launch from the committed ncu --set full
+    capture (profiles/ncu_traffic.json, tools/ncu_summary.py)."""
     p = ROOT / "profiles" / "ncu_traffic.json"
     try:
-        t = json.loads(p.read_text())
-        return t.get(config, {}).get(kernel)
+        t = json.loads(p.read_text()).get(config, {})
     except (OSError, ValueError):
         return None
+    for name, v in t.items():
+        if name == kernel or name.startswith(kernel) or kernel.startswith(name):
+            return v
+    return None
 
 
 # --------------------------------------------------------------------------

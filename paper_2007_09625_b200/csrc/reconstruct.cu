@@ -867,7 +867,9 @@ int launch_reconstruct(sdqz_ctx* ctx, const uint16_t* codes, const uint64_t* den
                                                                         dims[0], cap, two_eb, out);
         if (out_kind == 0) { RQ_LAUNCH(0) } else { RQ_LAUNCH(1) }
 #undef RQ_LAUNCH
-        SDQZ_LAUNCHED_NAMED(ctx, "rq_fast");
+        if (ndims == 3) SDQZ_LAUNCHED_NAMED(ctx, "rq3d_block_kernel");
+        else if (ndims == 2) SDQZ_LAUNCHED_NAMED(ctx, "rq2d_kernel");
+        else SDQZ_LAUNCHED_NAMED(ctx, "rq1d_kernel");
         if (!any_slow) return SDQZ_OK;
     }
     double* work = scratch_as<double>(ctx, S_WORK, n, &rc);

@@ -13,18 +13,40 @@ __device__ __forceinline__ void block_chunk_scan(const uint32_t* __restrict__ ch
                                                  unsigned long long* __restrict__ out_off,
                                                  unsigned long long payload_cap, bool records,
                                                  unsigned long long out_cap, DevStatus* st) {
+    // rows of 4096 chunks, 4 consecutive per thread (one 16-byte load, two
+    // 16-byte stores per array: a warp's accesses are contiguous)
     __shared__ unsigned long long wsb[32], wso[32];
     const uint32_t tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+    const bool vec = (((uintptr_t)chunk_bits | (uintptr_t)chunk_zeros | (uintptr_t)byte_off |
+                       (uintptr_t)out_off) & 15) == 0;
     unsigned long long carry_b = 0, carry_o = 0;
-    uint32_t nb = tid < C ? chunk_bits[tid] : 0;
-    uint32_t nz = (tid < C && chunk_zeros) ? chunk_zeros[tid] : 0;
-    for (uint64_t r0 = 0; r0 < C; r0 += 1024) {
-        const uint64_t i = r0 + tid;
-        const uint32_t vb = (nb + 7) >> 3, vz = nz;
-        const uint64_t ni = i + 1024;
-        nb = ni < C ? chunk_bits[ni] : 0;
-        nz = (ni < C && chunk_zeros) ? chunk_zeros[ni] : 0;
-        unsigned long long xb = vb, xo = vz;
+    for (uint64_t r0 = 0; r0 < C; r0 += 4096) {
+        const uint64_t i0 = r0 + 4 * (uint64_t)tid;
+        uint32_t vb[4], vz[4];
+        if (vec && i0 + 4 <= C) {
+            const uint4 u = *reinterpret_cast<const uint4*>(chunk_bits + i0);
+            vb[0] = u.x; vb[1] = u.y; vb[2] = u.z; vb[3] = u.w;
+            if (chunk_zeros) {
+                const uint4 z = *reinterpret_cast<const uint4*>(chunk_zeros + i0);
+                vz[0] = z.x; vz[1] = z.y; vz[2] = z.z; vz[3] = z.w;
+            } else {
+                vz[0] = vz[1] = vz[2] = vz[3] = 0;
+            }
+        } else {
+#pragma unroll
+            for (int q = 0; q < 4; q++) {
+                vb[q] = i0 + q < C ? chunk_bits[i0 + q] : 0;
+                vz[q] = (i0 + q < C && chunk_zeros) ? chunk_zeros[i0 + q] : 0;
+            }
+        }
+        unsigned long long tb = 0, to = 0;
+#pragma unroll
+        for (int q = 0; q < 4; q++) {
+            vb[q] = (vb[q] + 7) >> 3;
+            tb += vb[q];
+            to += vz[q];
+        }
+        unsigned long long xb = tb, xo = to;
 #pragma unroll
         for (int o = 1; o < 32; o <<= 1) {
             const unsigned long long yb = __shfl_up_sync(kFull, xb, o), yo = __shfl_up_sync(kFull, xo, o);
@@ -43,9 +65,29 @@ __device__ __forceinline__ void block_chunk_scan(const uint32_t* __restrict__ ch
             wso[lane] = uo;
         }
         __syncthreads();
-        if (i < C) {
-            byte_off[i] = carry_b + (wid ? wsb[wid - 1] : 0) + xb - vb;
-            if (out_off) out_off[i] = carry_o + (wid ? wso[wid - 1] : 0) + xo - vz;
+        unsigned long long rb[4], ro[4];
+        rb[0] = carry_b + (wid ? wsb[wid - 1] : 0) + xb - tb;
+        ro[0] = carry_o + (wid ? wso[wid - 1] : 0) + xo - to;
+#pragma unroll
+        for (int q = 1; q < 4; q++) {
+            rb[q] = rb[q - 1] + vb[q - 1];
+            ro[q] = ro[q - 1] + vz[q - 1];
+        }
+        if (vec && i0 + 4 <= C) {
+            reinterpret_cast<ulonglong2*>(byte_off + i0)[0] = make_ulonglong2(rb[0], rb[1]);
+            reinterpret_cast<ulonglong2*>(byte_off + i0)[1] = make_ulonglong2(rb[2], rb[3]);
+            if (out_off) {
+                reinterpret_cast<ulonglong2*>(out_off + i0)[0] = make_ulonglong2(ro[0], ro[1]);
+                reinterpret_cast<ulonglong2*>(out_off + i0)[1] = make_ulonglong2(ro[2], ro[3]);
+            }
+        } else {
+#pragma unroll
+            for (int q = 0; q < 4; q++) {
+                if (i0 + q < C) {
+                    byte_off[i0 + q] = rb[q];
+                    if (out_off) out_off[i0 + q] = ro[q];
+                }
+            }
         }
         carry_b += wsb[31];
         carry_o += wso[31];
