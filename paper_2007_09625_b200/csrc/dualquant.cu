@@ -331,9 +331,13 @@ __global__ void __launch_bounds__(kTmaWarps * 32, 3) dq3d_tma_kernel(
     const uint32_t wbase = cap >= 2 * kHot ? (uint32_t)r - kHot / 2 : 0u;
     const uint32_t lane = lane_id(), wid = threadIdx.x >> 5, xl = lane & 7;
     const uint32_t hot_s = smem_u32(hot + wid * kHot * 32 + lane);
-    const uint64_t nbx4 = ceil_div(ceil_div(X, 8), 4), nby = ceil_div(Y, 8), nbz = ceil_div(Z, 8);
-    const uint64_t ntask = nbx4 * nby * nbz;
+    // task indices and in-task offsets fit 32 bits (TMA extents < 2^31, a task
+    // spans < 8 planes): 32-bit index math, one wide multiply-add per address
+    const uint32_t nbx4 = (uint32_t)ceil_div(ceil_div(X, 8), 4), nby = (uint32_t)ceil_div(Y, 8),
+                   nbz = (uint32_t)ceil_div(Z, 8);
+    const uint32_t ntask = nbx4 * nby * nbz;
     const uint64_t YX = Y * X;
+    const uint32_t X32 = (uint32_t)X, YX32 = (uint32_t)umin(YX, 0xFFFFFFFFull);
     float* mytiles = tiles + (size_t)wid * kStages * kPair;
     uint64_t* mybar = bars + wid * kStages;
     if (lane == 0) {
@@ -341,40 +345,43 @@ __global__ void __launch_bounds__(kTmaWarps * 32, 3) dq3d_tma_kernel(
         fence_mbar_init();
     }
     __syncwarp();
-    const uint64_t stride = (uint64_t)gridDim.x * kTmaWarps;
-    const uint64_t first = blockIdx.x * (uint64_t)kTmaWarps + wid;
+    // shared-address view of the CTA histogram (codes outside the hot window)
+    const bool use_s = h.shist != nullptr;
+    const uint32_t shist_s = use_s ? smem_u32(h.shist) : 0u;
+    const uint32_t stride = gridDim.x * kTmaWarps;
+    const uint32_t first = blockIdx.x * kTmaWarps + wid;
     // unit u = (task first + (u >> 2) * stride, z planes 2(u & 3) .. +1)
-    auto issue = [&](uint64_t u) {
-        const uint64_t task = first + (u >> 2) * stride;
+    auto issue = [&](uint32_t u) {
+        const uint32_t task = first + (u >> 2) * stride;
         if (task >= ntask) return;
-        const uint64_t bx4 = task % nbx4, t2 = task / nbx4;
-        const uint64_t by = t2 % nby, bz = t2 / nby;
-        const uint32_t q = (uint32_t)(u % kStages);
+        const uint32_t bx4 = task % nbx4, t2 = task / nbx4;
+        const uint32_t by = t2 % nby, bz = t2 / nby;
+        const uint32_t q = u % kStages;
         mbar_expect_tx(&mybar[q], kPair * 4);
         tma_load_3d(mytiles + q * kPair, &tmap, (int)(bx4 * 32), (int)(by * 8),
                     (int)(bz * 8 + 2 * (u & 3)), &mybar[q]);
     };
     if (lane == 0)
-        for (int q = 0; q < kStages - 1; q++) issue(q);
+        for (uint32_t q = 0; q < kStages - 1; q++) issue(q);
     uint32_t phase = 0;   // bit q: parity of stage q
-    uint64_t u = 0;
+    uint32_t u = 0;
     bool bad = false;
-    for (uint64_t task = first; task < ntask; task += stride) {
-        const uint64_t bx4 = task % nbx4, t2 = task / nbx4;
-        const uint64_t by = t2 % nby, bz = t2 / nby;
-        const uint64_t x = bx4 * 32 + lane, y0 = by * 8, z0 = bz * 8;
+    for (uint32_t task = first; task < ntask; task += stride) {
+        const uint32_t bx4 = task % nbx4, t2 = task / nbx4;
+        const uint32_t by = t2 % nby, bz = t2 / nby;
+        const uint64_t x = (uint64_t)bx4 * 32 + lane, y0 = (uint64_t)by * 8, z0 = (uint64_t)bz * 8;
         const bool xin = x < X;
         const int ny = (int)umin(8, Y - y0), nz = (int)umin(8, Z - z0);
         const uint64_t base = z0 * YX + y0 * X + x;
+        uint16_t* const tb = codes + base;
         int hprev[8];
 #pragma unroll
         for (int y = 0; y < 8; y++) hprev[y] = 0;
         bool big = false;
-        uint16_t* crow = codes + base;
 #pragma unroll 1
         for (int pr = 0; pr < 4; pr++, u++) {
             if (lane == 0) issue(u + kStages - 1);
-            const uint32_t q = (uint32_t)(u % kStages);
+            const uint32_t q = u % kStages;
             mbar_wait(&mybar[q], (phase >> q) & 1u);
             phase ^= 1u << q;
             const float* tile = mytiles + q * kPair;
@@ -382,18 +389,22 @@ __global__ void __launch_bounds__(kTmaWarps * 32, 3) dq3d_tma_kernel(
             for (int zz = 0; zz < 2; zz++) {
                 int gprev = 0;
                 const bool zin = xin && 2 * pr + zz < nz;
+                const uint32_t zoff = (uint32_t)(2 * pr + zz) * YX32;
 #pragma unroll
                 for (int y = 0; y < 8; y++) {
                     const float v = tile[(zz * 8 + y) * 32 + lane];
-                    const double yv = __dmul_rn((double)v, rcp);
-                    const double t = __dadd_rn(fabs(yv), 0.5);
+                    // |x / 2eb| by reciprocal multiply; exact division only in the
+                    // 2^-22 neighbourhood of a rounding tie (warp-uniform branch)
+                    const double t = __dadd_rn(__dmul_rn((double)fabsf(v), rcp), 0.5);
                     const double fl = floor(t);
                     const double fr = __dsub_rn(t, fl);
-                    big |= !(t < kIntBound);
-                    int qv = (int)fl;
-                    qv = yv < 0.0 ? -qv : qv;
-                    if ((fr < 2.384185791015625e-07) | (fr > 1.0 - 2.384185791015625e-07))
-                        qv = (int)prequant((double)v, two_eb);   // rounding-tie neighbourhood: exact
+                    int m = (int)fl;
+                    const bool amb = (fr < 2.384185791015625e-07) | (fr > 1.0 - 2.384185791015625e-07);
+                    if (__any_sync(kFull, amb)) {
+                        if (amb) m = (int)floor(__dadd_rn(fabs(__ddiv_rn((double)v, two_eb)), 0.5));
+                    }
+                    big |= !(t < kIntBound);   // also NaN / Inf
+                    const int qv = v < 0.f ? -m : m;
                     const int left = __shfl_up_sync(kFull, qv, 1);
                     const int g = qv - (xl ? left : 0);
                     const int hh = g - gprev;
@@ -403,11 +414,16 @@ __global__ void __launch_bounds__(kTmaWarps * 32, 3) dq3d_tma_kernel(
                     const uint32_t uu = (uint32_t)(delta + r);
                     const uint32_t c = (uu - 1u) < (uint32_t)(2 * r - 1) ? uu : 0u;   // -r < delta < r
                     if (zin && y < ny) {
-                        crow[y * X] = (uint16_t)c;
-                        hot_add(hot_s, c, wbase, h);
+                        tb[zoff + (uint32_t)y * X32] = (uint16_t)c;
+                        const uint32_t dw = c - wbase;
+                        if (use_s) {   // one shared reduction: lane-private hot bin or CTA bin
+                            const uint32_t addr = dw < kHot ? hot_s + dw * 128u : shist_s + c * 4u;
+                            asm volatile("red.shared.add.u32 [%0], 1;" ::"r"(addr) : "memory");
+                        } else {
+                            hot_add(hot_s, c, wbase, h);
+                        }
                     }
                 }
-                crow += YX;
             }
             __syncwarp();   // the stage is refilled two units later
         }
@@ -695,7 +711,7 @@ int launch_kind(sdqz_ctx* ctx, const void* d_in, int ndims, const uint64_t dims[
     // TMA-fed 3D path: fp32, 16-byte aligned base and row pitch, extents TMA can address
     if (KIND == 0 && ndims == 3 && is_fast_shape(ndims, block) && dims[2] % 4 == 0 &&
         ((uintptr_t)d_in & 15) == 0 && dims[2] < (1ull << 31) && dims[1] < (1ull << 31) &&
-        dims[0] < (1ull << 31) && !env_disabled("SDQZ_NO_TMA")) {
+        dims[0] < (1ull << 31) && dims[1] * dims[2] < (1ull << 28) && !env_disabled("SDQZ_NO_TMA")) {
         CUtensorMap map;
         const uint64_t gd[3] = {dims[2], dims[1], dims[0]};
         const uint64_t gs[2] = {dims[2] * 4, dims[2] * dims[1] * 4};
