@@ -289,7 +289,7 @@ def ours_arm(args, cfg, world, rank, local_rank):
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
-    launches0 = ctx.launches
+    launches0, replays0 = ctx.launches, ctx.graph_replays
     with Clocks(local_rank) as clk:
         for i in range(args.steps):
             flush.zero_()                       # evict the field/archive from L2
@@ -300,6 +300,7 @@ def ours_arm(args, cfg, world, rank, local_rank):
     if world > 1:
         dist.barrier()
     launches = ctx.launches - launches0
+    replays = ctx.graph_replays - replays0
     step_ms = [s.elapsed_time(e) for s, e in zip(starts, ends)]
     t_local = sum(step_ms) / 1e3
     t = torch.tensor([t_local], dtype=torch.float64, device="cuda")
@@ -391,6 +392,7 @@ def ours_arm(args, cfg, world, rank, local_rank):
                          "traffic": load_traffic(args.config, dom)},
             "e2e": e2e,
             "gpu_launches": launches,
+            "graph_replays": replays,
             "clocks": clk.summary(),
             "cpu_baseline": base,
         }

@@ -75,6 +75,10 @@ SDQZ_API int sdqz_ctx_set_stream(sdqz_ctx* ctx, void* stream);
 SDQZ_API const char* sdqz_last_error(const sdqz_ctx* ctx);
 /* Total kernels launched through this context (evidence for the bench). */
 SDQZ_API uint64_t sdqz_kernel_launches(const sdqz_ctx* ctx);
+/* Compress / decompress calls served by replaying a captured CUDA graph (a
+ * call repeating the previous call's pointers and parameters is captured once,
+ * then replayed; disabled while the kernel timer runs or SDQZ_NO_GRAPH=1). */
+SDQZ_API uint64_t sdqz_graph_replays(const sdqz_ctx* ctx);
 /* Per-kernel device timer: on=1 resets and starts accumulating CUDA-event
  * intervals per kernel name on the context's stream; sdqz_kernel_times writes
  * "name=ms;name=ms;..." (NUL-terminated, truncated to len) and returns the

@@ -45,6 +45,7 @@ _SIGS = {
     "sdqz_ctx_set_stream": (c_int, [c_void_p, c_void_p]),
     "sdqz_last_error": (c_char_p, [c_void_p]),
     "sdqz_kernel_launches": (c_uint64, [c_void_p]),
+    "sdqz_graph_replays": (c_uint64, [c_void_p]),
     "sdqz_set_timing": (c_int, [c_void_p, c_int]),
     "sdqz_debug_counters": (c_int, [c_void_p, POINTER(c_uint64), c_int]),
     "sdqz_kernel_times": (c_int, [c_void_p, c_char_p, c_uint64]),
@@ -163,6 +164,10 @@ class Context:
     @property
     def launches(self) -> int:
         return int(self.lib.sdqz_kernel_launches(self.h))
+
+    @property
+    def graph_replays(self) -> int:
+        return int(self.lib.sdqz_graph_replays(self.h))
 
     def __del__(self):  # pragma: no cover - interpreter shutdown order varies
         try:

@@ -31,6 +31,7 @@ void* scratch(sdqz_ctx* ctx, int slot, size_t bytes, cudaError_t* e) {
     auto& b = ctx->bufs[slot];
     if (bytes == 0) bytes = 16;
     if (b.bytes >= bytes) return b.p;
+    ctx->gen++;   // device pointers change: captured graphs are stale
     if (b.p) {
         cudaStreamSynchronize(ctx->stream);
         cudaFree(b.p);
@@ -108,13 +109,23 @@ static void kt_flush(sdqz_ctx* ctx) {
     kt_mark(ctx, "(start)");
 }
 
-int fetch_status(sdqz_ctx* ctx) {
+int enqueue_status_copy(sdqz_ctx* ctx) {
     SDQZ_CUDA(ctx, cudaMemcpyAsync(ctx->h_status, ctx->d_status, sizeof(DevStatus),
                                    cudaMemcpyDeviceToHost, ctx->stream));
     if (ctx->timing) kt_mark(ctx, "status_readback");
+    return SDQZ_OK;
+}
+
+int sync_status(sdqz_ctx* ctx) {
     SDQZ_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
     if (ctx->timing) kt_flush(ctx);
     return SDQZ_OK;
+}
+
+int fetch_status(sdqz_ctx* ctx) {
+    int rc;
+    if ((rc = enqueue_status_copy(ctx))) return rc;
+    return sync_status(ctx);
 }
 
 }  // namespace sdqz
@@ -205,49 +216,9 @@ uint64_t archive_total(const sdqz_header& h) {
 }
 
 // Shared decompress core over device-resident sections.
-int decompress_core(sdqz_ctx* ctx, const sdqz_header* hdr, const uint8_t* d_bw, const void* d_rec,
-                    const uint32_t* d_cbits, const uint8_t* d_payload, uint64_t payload_alloc,
-                    void* d_out) {
-    int rc = SDQZ_OK;
-    const uint64_t n = prod3(hdr->dims);
-    const uint32_t cap = hdr->cap;
-    const uint64_t C = hdr->n_chunks, k = hdr->n_outliers;
-    bool geom_ok = true;    // QuantConfig checks (core.py:87-94) come after deserialize
-    for (int a = 0; a < hdr->ndims; a++) geom_ok &= hdr->block[a] >= 1;
-    const bool eb_ok = hdr->eb_resolved > 0 && std::isfinite(hdr->eb_resolved);
-    const bool chunks_ok = C == ceil_div(n, hdr->chunk_size) && geom_ok && eb_ok;
-    BookDev book;
-    if ((rc = book_tables(ctx, cap, &book))) return rc;
-    uint16_t* codes = scratch_as<uint16_t>(ctx, S_CODES, n + 64, &rc);
-    uint64_t* dense = scratch_as<uint64_t>(ctx, S_DENSE, n, &rc);
-    uint64_t nblocks = 1;
-    for (int a = 0; a < hdr->ndims; a++) nblocks *= ceil_div(hdr->dims[a], hdr->block[a] ? hdr->block[a] : 1);
-    uint8_t* bflag = scratch_as<uint8_t>(ctx, S_BLOCKFLAG, nblocks, &rc);
-    if (!codes || !dense || !bflag) return rc;
-    uint32_t safe_block[3];
-    for (int a = 0; a < 3; a++) safe_block[a] = hdr->block[a] ? hdr->block[a] : 1;
-    if ((rc = reset_status_eb(ctx, hdr->eb_resolved, true))) return rc;
-    SDQZ_CUDA(ctx, cudaMemsetAsync(bflag, 0, nblocks, ctx->stream));
-    // canonical tables from the stored bitwidths (deserialize checks + canonize)
-    if ((rc = launch_codebook(ctx, nullptr, const_cast<uint8_t*>(d_bw), cap, book, false, true, true)))
-        return rc;
-    // (the sequential decoder's LUT is built with the fast decoder's tables)
-    if (chunks_ok) {
-        if ((rc = launch_inflate(ctx, d_payload, payload_alloc, d_cbits, C, hdr->chunk_size,
-                                 book.first, book.offsets, book.symbols, book.lut, -1, n, codes,
-                                 false)))
-            return rc;
-    }
-    if ((rc = launch_outlier_scatter(ctx, d_rec, nullptr, nullptr, k, n, codes, hdr->ndims,
-                                     hdr->dims, safe_block, dense, bflag, true)))
-        return rc;
-    if (chunks_ok) {
-        double two_eb = 2.0 * hdr->eb_resolved;
-        if ((rc = launch_reconstruct(ctx, codes, dense, bflag, true, hdr->ndims, hdr->dims,
-                                     hdr->block, cap, two_eb, d_out, hdr->dtype_code)))
-            return rc;
-    }
-    if ((rc = fetch_status(ctx))) return rc;
+int decompress_checks(sdqz_ctx* ctx, const sdqz_header* hdr, bool chunks_ok, bool geom_ok, bool eb_ok,
+                      uint64_t n, uint64_t C, uint64_t k) {
+    int rc;
     const DevStatus& s = *ctx->h_status;
     // deserialize order (archive.py:204-237)
     if ((rc = table_error(ctx, s.flags, true))) return rc;
@@ -275,6 +246,282 @@ int decompress_core(sdqz_ctx* ctx, const sdqz_header* hdr, const uint8_t* d_bw, 
         return set_error(ctx, SDQZ_ECORRUPT, fmt("%llu zero codes but %llu outlier entries", s.n_zero,
                                                  (unsigned long long)k));
     return SDQZ_OK;
+}
+
+template <typename T>
+void key_put(std::string& k, const T& v) {
+    k.append(reinterpret_cast<const char*>(&v), sizeof(T));
+}
+
+// Record the enqueue sequence into a graph (nothing executes while capturing);
+// any failure simply leaves graphs off for this key.
+template <typename Enq>
+void capture_graph(sdqz_ctx* ctx, sdqz_ctx::Graph& g, const std::string& key, Enq enqueue) {
+    if (g.exec) {
+        cudaGraphExecDestroy(g.exec);
+        g.exec = nullptr;
+    }
+    cudaGraph_t graph = nullptr;
+    // capture on a private stream (the caller's may be the legacy default
+    // stream, which cannot be captured); nothing executes while capturing
+    if (!ctx->cap_stream && cudaStreamCreateWithFlags(&ctx->cap_stream, cudaStreamNonBlocking) != cudaSuccess) {
+        cudaGetLastError();
+        ctx->cap_stream = nullptr;
+        return;
+    }
+    cudaStream_t user = ctx->stream;
+    ctx->stream = ctx->cap_stream;
+    if (cudaStreamBeginCapture(ctx->stream, cudaStreamCaptureModeThreadLocal) != cudaSuccess) {
+        cudaGetLastError();
+        ctx->stream = user;
+        return;
+    }
+    const uint64_t l0 = ctx->launches;
+    const std::string err0 = ctx->err;
+    const int rc = enqueue();
+    const cudaError_t ec = cudaStreamEndCapture(ctx->stream, &graph);
+    ctx->stream = user;
+    g.nlaunch = ctx->launches - l0;
+    ctx->launches = l0;
+    ctx->err = err0;
+    if (rc != SDQZ_OK || ec != cudaSuccess || !graph) {
+        cudaGetLastError();
+        if (graph) cudaGraphDestroy(graph);
+        return;
+    }
+    cudaGraphExec_t exec = nullptr;
+    if (cudaGraphInstantiate(&exec, graph, 0) == cudaSuccess) {
+        g.exec = exec;
+        g.key = key;
+        g.gen = ctx->gen;
+    } else {
+        cudaGetLastError();
+    }
+    cudaGraphDestroy(graph);
+}
+
+bool graphs_on(const sdqz_ctx* ctx) { return !ctx->timing && !env_disabled("SDQZ_NO_GRAPH"); }
+
+// Shared decompress core over device-resident sections.  The enqueue part (all
+// launches + the status copy) replays as a CUDA graph when a call repeats the
+// previous one's pointers and header; the checks run on the host after sync.
+int decompress_core(sdqz_ctx* ctx, const sdqz_header* hdr, const uint8_t* d_bw, const void* d_rec,
+                    const uint32_t* d_cbits, const uint8_t* d_payload, uint64_t payload_alloc,
+                    void* d_out) {
+    int rc = SDQZ_OK;
+    const uint64_t n = prod3(hdr->dims);
+    const uint32_t cap = hdr->cap;
+    const uint64_t C = hdr->n_chunks, k = hdr->n_outliers;
+    bool geom_ok = true;    // QuantConfig checks (core.py:87-94) come after deserialize
+    for (int a = 0; a < hdr->ndims; a++) geom_ok &= hdr->block[a] >= 1;
+    const bool eb_ok = hdr->eb_resolved > 0 && std::isfinite(hdr->eb_resolved);
+    const bool chunks_ok = C == ceil_div(n, hdr->chunk_size) && geom_ok && eb_ok;
+    BookDev book;
+    if ((rc = book_tables(ctx, cap, &book))) return rc;
+    uint16_t* codes = scratch_as<uint16_t>(ctx, S_CODES, n + 64, &rc);
+    uint64_t* dense = scratch_as<uint64_t>(ctx, S_DENSE, n, &rc);
+    uint64_t nblocks = 1;
+    for (int a = 0; a < hdr->ndims; a++) nblocks *= ceil_div(hdr->dims[a], hdr->block[a] ? hdr->block[a] : 1);
+    uint8_t* bflag = scratch_as<uint8_t>(ctx, S_BLOCKFLAG, nblocks, &rc);
+    if (!codes || !dense || !bflag) return rc;
+    uint32_t safe_block[3];
+    for (int a = 0; a < 3; a++) safe_block[a] = hdr->block[a] ? hdr->block[a] : 1;
+    auto enqueue = [&]() -> int {
+        int r2;
+        if ((r2 = reset_status_eb(ctx, hdr->eb_resolved, true))) return r2;
+        SDQZ_CUDA(ctx, cudaMemsetAsync(bflag, 0, nblocks, ctx->stream));
+        // canonical tables from the stored bitwidths (deserialize checks + canonize)
+        if ((r2 = launch_codebook(ctx, nullptr, const_cast<uint8_t*>(d_bw), cap, book, false, true, true)))
+            return r2;
+        // (the sequential decoder's LUT is built with the fast decoder's tables)
+        if (chunks_ok) {
+            if ((r2 = launch_inflate(ctx, d_payload, payload_alloc, d_cbits, C, hdr->chunk_size,
+                                     book.first, book.offsets, book.symbols, book.lut, -1, n, codes,
+                                     false)))
+                return r2;
+        }
+        if ((r2 = launch_outlier_scatter(ctx, d_rec, nullptr, nullptr, k, n, codes, hdr->ndims,
+                                         hdr->dims, safe_block, dense, bflag, true)))
+            return r2;
+        if (chunks_ok) {
+            double two_eb = 2.0 * hdr->eb_resolved;
+            if ((r2 = launch_reconstruct(ctx, codes, dense, bflag, true, hdr->ndims, hdr->dims,
+                                         hdr->block, cap, two_eb, d_out, hdr->dtype_code)))
+                return r2;
+        }
+        return enqueue_status_copy(ctx);
+    };
+    std::string key;
+    key_put(key, *hdr);
+    key_put(key, d_bw);
+    key_put(key, d_rec);
+    key_put(key, d_cbits);
+    key_put(key, d_payload);
+    key_put(key, payload_alloc);
+    key_put(key, d_out);
+    const bool graphs = graphs_on(ctx);
+    bool capture = false;
+    if (graphs && ctx->g_decomp.exec && ctx->g_decomp.key == key && ctx->g_decomp.gen == ctx->gen) {
+        SDQZ_CUDA(ctx, cudaGraphLaunch(ctx->g_decomp.exec, ctx->stream));
+        ctx->launches += ctx->g_decomp.nlaunch;
+        ctx->graph_replays++;
+    } else {
+        const uint64_t gen0 = ctx->gen;
+        if ((rc = enqueue())) return rc;
+        capture = graphs && ctx->last_decomp_key == key && ctx->gen == gen0;
+    }
+    ctx->last_decomp_key = key;
+    if ((rc = sync_status(ctx))) return rc;
+    if ((rc = decompress_checks(ctx, hdr, chunks_ok, geom_ok, eb_ok, n, C, k))) return rc;
+    if (capture) capture_graph(ctx, ctx->g_decomp, key, enqueue);
+    return SDQZ_OK;
+}
+
+struct CompressState {
+    const void* d_in;
+    int dtype, ndims, eb_mode;
+    uint64_t dims[3];
+    uint32_t block[3];
+    double eb;
+    uint32_t cap, cs;
+    uint64_t n, C;
+    uint16_t* codes;
+    unsigned long long* hist;
+    uint32_t* cbits;
+    BookDev book;
+    uint64_t pay_cap, rec_cap;
+    uint8_t* payload;
+    unsigned long long* rec;
+    DeflateJob job;
+};
+
+// ---------------------------------------------------------------------------
+// fused compress: prepare (scratch) / enqueue (all launches + status copy) /
+// finish (sync, checks in the reference's order, overflow redo, header)
+// ---------------------------------------------------------------------------
+int compress_prepare(sdqz_ctx* ctx, CompressState& c) {
+    int rc = SDQZ_OK;
+    c.codes = scratch_as<uint16_t>(ctx, S_CODES, c.n + 64, &rc);
+    c.hist = scratch_as<unsigned long long>(ctx, S_HIST, c.cap, &rc);
+    c.cbits = scratch_as<uint32_t>(ctx, S_CHUNK_BITS, c.C, &rc);
+    if (!c.codes || !c.hist || !c.cbits) return rc;
+    if ((rc = book_tables(ctx, c.cap, &c.book))) return rc;
+    // first-guess capacities; exact sizes are known after the chunk scan
+    c.pay_cap = ctx->bufs[S_PAYLOAD].bytes ? ctx->bufs[S_PAYLOAD].bytes : (c.n / 2 + c.C + 4096);
+    c.rec_cap = ctx->bufs[S_OUTREC].bytes ? ctx->bufs[S_OUTREC].bytes / 16 : (c.n / 32 + 1024);
+    c.payload = scratch_as<uint8_t>(ctx, S_PAYLOAD, c.pay_cap, &rc);
+    c.rec = scratch_as<unsigned long long>(ctx, S_OUTREC, 2 * c.rec_cap, &rc);
+    if (!c.payload || !c.rec) return rc;
+    c.job = DeflateJob{};
+    c.job.codes = c.codes;
+    c.job.n = c.n;
+    c.job.chunk = c.cs;
+    c.job.entries = c.book.entries;
+    c.job.cap = c.cap;
+    c.job.chunk_bits = c.cbits;
+    c.job.payload = c.payload;
+    c.job.payload_cap = c.pay_cap;
+    c.job.in = c.d_in;
+    c.job.in_kind = c.dtype;
+    c.job.out_records = c.rec;
+    c.job.out_cap = c.rec_cap;
+    return SDQZ_OK;
+}
+
+int compress_enqueue(sdqz_ctx* ctx, const CompressState& c) {
+    int rc;
+    if ((rc = reset_status(ctx))) return rc;
+    if (c.eb_mode == 1 || !(c.eb > 0 && std::isfinite(c.eb))) {
+        if ((rc = launch_describe(ctx, c.d_in, c.dtype, c.n))) return rc;
+    }
+    if ((rc = launch_resolve(ctx, c.dtype, c.eb_mode, c.eb))) return rc;
+    SDQZ_CUDA(ctx, cudaMemsetAsync(c.hist, 0, c.cap * 8ull, ctx->stream));
+    if ((rc = launch_dualquant(ctx, c.d_in, c.dtype, c.ndims, c.dims, c.block, c.cap, c.codes, c.hist)))
+        return rc;
+    if ((rc = launch_codebook(ctx, c.hist, c.book.bw, c.cap, c.book, true, true, false))) return rc;
+    if ((rc = launch_deflate(ctx, c.job))) return rc;
+    return enqueue_status_copy(ctx);
+}
+
+int compress_finish(sdqz_ctx* ctx, CompressState& c, sdqz_header* hdr) {
+    int rc;
+    if ((rc = sync_status(ctx))) return rc;
+    uint64_t f = ctx->h_status->flags;
+    // resolve_error_bound / QuantConfig order (core.py:161-175, :87-89)
+    if (f & F_NONFINITE)
+        return set_error(ctx, SDQZ_EINVAL, "field contains NaN/Inf values and cannot be compressed");
+    if (!(c.eb > 0 && std::isfinite(c.eb))) return set_error(ctx, SDQZ_EINVAL, "error bound must be positive");
+    if (f & F_RANGE_ZERO)
+        return set_error(ctx, SDQZ_EINVAL,
+                         "value-range-relative bound is undefined on a constant field; use an "
+                         "absolute error bound instead");
+    double ebr = ctx->h_status->eb;
+    if (!(ebr > 0 && std::isfinite(ebr)))
+        return set_error(ctx, SDQZ_EINVAL, "error bound must be positive and finite");
+    if ((rc = table_error(ctx, f, false))) return rc;
+    if (f & F_OVERFLOW) {
+        // grow to the exact sizes and redo the deflate stage only
+        uint64_t P = ctx->h_status->payload_bytes, K = ctx->h_status->n_outliers;
+        c.payload = scratch_as<uint8_t>(ctx, S_PAYLOAD, P + 64, &rc);
+        c.rec = scratch_as<unsigned long long>(ctx, S_OUTREC, 2 * (K + 1), &rc);
+        if (!c.payload || !c.rec) return rc;
+        c.job.payload = c.payload;
+        c.job.payload_cap = ctx->bufs[S_PAYLOAD].bytes;
+        c.job.out_records = c.rec;
+        c.job.out_cap = ctx->bufs[S_OUTREC].bytes / 16;
+        // clear the overflow flag, keep eb / max_bw
+        SDQZ_CUDA(ctx, cudaMemsetAsync(&ctx->d_status->flags, 0, 8, ctx->stream));
+        if ((rc = launch_deflate(ctx, c.job))) return rc;
+        if ((rc = fetch_status(ctx))) return rc;
+        if (ctx->h_status->flags & F_OVERFLOW)
+            return set_error(ctx, SDQZ_EINVAL, "internal: capacity still exceeded");
+    }
+    const DevStatus& s = *ctx->h_status;
+    // zero padding after the payload: decoders peek past the last chunk (huffman.py:338)
+    {
+        auto& pb = ctx->bufs[S_PAYLOAD];
+        uint64_t pad = std::min<uint64_t>(64, pb.bytes - s.payload_bytes);
+        SDQZ_CUDA(ctx, cudaMemsetAsync((uint8_t*)pb.p + s.payload_bytes, 0, pad, ctx->stream));
+    }
+    sdqz_header h{};
+    h.dtype_code = (uint8_t)c.dtype;
+    h.ndims = (uint8_t)c.ndims;
+    h.eb_mode = (uint8_t)c.eb_mode;
+    h.unit_width = (uint8_t)unit_for((uint32_t)s.max_bw);
+    for (int a = 0; a < 3; a++) {
+        h.dims[a] = a < c.ndims ? c.dims[a] : 1;
+        h.block[a] = a < c.ndims ? c.block[a] : 1;
+    }
+    h.eb_resolved = s.eb;
+    h.eb_specified = c.eb;
+    h.cap = c.cap;
+    h.chunk_size = c.cs;
+    h.n_outliers = s.n_outliers;
+    h.n_chunks = c.C;
+    h.payload_bytes = s.payload_bytes;
+    ctx->last_hdr = h;
+    ctx->have_archive = true;
+    if (hdr) *hdr = h;
+    return SDQZ_OK;
+}
+
+std::string compress_key(const CompressState& c) {
+    std::string k;
+    key_put(k, c.d_in);
+    key_put(k, c.dtype);
+    key_put(k, c.ndims);
+    for (int a = 0; a < 3; a++) { key_put(k, c.dims[a]); key_put(k, c.block[a]); }
+    key_put(k, c.eb_mode);
+    key_put(k, c.eb);
+    key_put(k, c.cap);
+    key_put(k, c.cs);
+    key_put(k, c.pay_cap);
+    key_put(k, c.rec_cap);
+    return k;
+}
+
+void capture_compress(sdqz_ctx* ctx, const CompressState& c, const std::string& key) {
+    capture_graph(ctx, ctx->g_comp, key, [&] { return compress_enqueue(ctx, c); });
 }
 
 }  // namespace
@@ -311,6 +558,9 @@ int sdqz_ctx_destroy(sdqz_ctx* ctx) {
     cudaStreamSynchronize(ctx->stream);
     for (auto& b : ctx->bufs)
         if (b.p) cudaFree(b.p);
+    if (ctx->g_comp.exec) cudaGraphExecDestroy(ctx->g_comp.exec);
+    if (ctx->cap_stream) cudaStreamDestroy(ctx->cap_stream);
+    if (ctx->g_decomp.exec) cudaGraphExecDestroy(ctx->g_decomp.exec);
     if (ctx->d_status) cudaFree(ctx->d_status);
     if (ctx->h_status) cudaFreeHost(ctx->h_status);
     if (ctx->own_stream) cudaStreamDestroy(ctx->stream);
@@ -331,6 +581,8 @@ int sdqz_ctx_set_stream(sdqz_ctx* ctx, void* stream) {
 const char* sdqz_last_error(const sdqz_ctx* ctx) { return ctx ? ctx->err.c_str() : "no context"; }
 
 uint64_t sdqz_kernel_launches(const sdqz_ctx* ctx) { return ctx ? ctx->launches : 0; }
+
+uint64_t sdqz_graph_replays(const sdqz_ctx* ctx) { return ctx ? ctx->graph_replays : 0; }
 
 int sdqz_debug_counters(sdqz_ctx* ctx, uint64_t* out, int n) {
     const unsigned long long* p = ctx->h_status->pad;
@@ -618,102 +870,34 @@ int sdqz_compress(sdqz_ctx* ctx, const void* d_in, int dtype, int ndims, const u
     if (!valid_cap(cap)) return set_error(ctx, SDQZ_EINVAL, "bad cap");
     const uint64_t n = prod3(dims);
     if (n == 0) return set_error(ctx, SDQZ_EINVAL, "empty field");
-    const uint32_t cs = chunk ? chunk : default_chunk_size(n);
-    const uint64_t C = ceil_div(n, cs);
-    const int in_kind = dtype;
-
-    uint16_t* codes = scratch_as<uint16_t>(ctx, S_CODES, n + 64, &rc);
-    unsigned long long* hist = scratch_as<unsigned long long>(ctx, S_HIST, cap, &rc);
-    uint32_t* cbits = scratch_as<uint32_t>(ctx, S_CHUNK_BITS, C, &rc);
-    BookDev book;
-    if (!codes || !hist || !cbits) return rc;
-    if ((rc = book_tables(ctx, cap, &book))) return rc;
-    // first-guess capacities; exact sizes are known after the chunk scan
-    uint64_t pay_cap = ctx->bufs[S_PAYLOAD].bytes ? ctx->bufs[S_PAYLOAD].bytes : (n / 2 + C + 4096);
-    uint64_t rec_cap = ctx->bufs[S_OUTREC].bytes ? ctx->bufs[S_OUTREC].bytes / 16 : (n / 32 + 1024);
-    uint8_t* payload = scratch_as<uint8_t>(ctx, S_PAYLOAD, pay_cap, &rc);
-    unsigned long long* rec = scratch_as<unsigned long long>(ctx, S_OUTREC, 2 * rec_cap, &rc);
-    if (!payload || !rec) return rc;
-
-    if ((rc = reset_status(ctx))) return rc;
-    if (eb_mode == 1 || !(eb > 0 && std::isfinite(eb))) {
-        if ((rc = launch_describe(ctx, d_in, dtype, n))) return rc;
+    CompressState cst;
+    cst.d_in = d_in;
+    cst.dtype = dtype;
+    cst.ndims = ndims;
+    for (int a = 0; a < 3; a++) { cst.dims[a] = dims[a]; cst.block[a] = block[a]; }
+    cst.eb_mode = eb_mode;
+    cst.eb = eb;
+    cst.cap = cap;
+    cst.n = n;
+    cst.cs = chunk ? chunk : default_chunk_size(n);
+    cst.C = ceil_div(n, cst.cs);
+    if ((rc = compress_prepare(ctx, cst))) return rc;
+    // Graph replay: a call identical to the previous one (same pointers and
+    // parameters, unchanged scratch arena) re-launches the captured pipeline
+    // in one cudaGraphLaunch.  The second identical call captures it.
+    const std::string key = compress_key(cst);
+    const bool graphs = graphs_on(ctx);
+    if (graphs && ctx->g_comp.exec && ctx->g_comp.key == key && ctx->g_comp.gen == ctx->gen) {
+        SDQZ_CUDA(ctx, cudaGraphLaunch(ctx->g_comp.exec, ctx->stream));
+        ctx->launches += ctx->g_comp.nlaunch;
+        ctx->graph_replays++;
+        return compress_finish(ctx, cst, hdr);
     }
-    if ((rc = launch_resolve(ctx, dtype, eb_mode, eb))) return rc;
-    SDQZ_CUDA(ctx, cudaMemsetAsync(hist, 0, cap * 8ull, ctx->stream));
-    if ((rc = launch_dualquant(ctx, d_in, in_kind, ndims, dims, block, cap, codes, hist))) return rc;
-    if ((rc = launch_codebook(ctx, hist, book.bw, cap, book, true, true, false))) return rc;
-    DeflateJob job;
-    job.codes = codes;
-    job.n = n;
-    job.chunk = cs;
-    job.entries = book.entries;
-    job.cap = cap;
-    job.chunk_bits = cbits;
-    job.payload = payload;
-    job.payload_cap = pay_cap;
-    job.in = d_in;
-    job.in_kind = in_kind;
-    job.out_records = rec;
-    job.out_cap = rec_cap;
-    if ((rc = launch_deflate(ctx, job))) return rc;
-    if ((rc = fetch_status(ctx))) return rc;
-    uint64_t f = ctx->h_status->flags;
-    // resolve_error_bound / QuantConfig order (core.py:161-175, :87-89)
-    if (f & F_NONFINITE)
-        return set_error(ctx, SDQZ_EINVAL, "field contains NaN/Inf values and cannot be compressed");
-    if (!(eb > 0 && std::isfinite(eb))) return set_error(ctx, SDQZ_EINVAL, "error bound must be positive");
-    if (f & F_RANGE_ZERO)
-        return set_error(ctx, SDQZ_EINVAL,
-                         "value-range-relative bound is undefined on a constant field; use an "
-                         "absolute error bound instead");
-    double ebr = ctx->h_status->eb;
-    if (!(ebr > 0 && std::isfinite(ebr)))
-        return set_error(ctx, SDQZ_EINVAL, "error bound must be positive and finite");
-    if ((rc = table_error(ctx, f, false))) return rc;
-    if (f & F_OVERFLOW) {
-        // grow to the exact sizes and redo the deflate stage only
-        uint64_t P = ctx->h_status->payload_bytes, K = ctx->h_status->n_outliers;
-        payload = scratch_as<uint8_t>(ctx, S_PAYLOAD, P + 64, &rc);
-        rec = scratch_as<unsigned long long>(ctx, S_OUTREC, 2 * (K + 1), &rc);
-        if (!payload || !rec) return rc;
-        job.payload = payload;
-        job.payload_cap = ctx->bufs[S_PAYLOAD].bytes;
-        job.out_records = rec;
-        job.out_cap = ctx->bufs[S_OUTREC].bytes / 16;
-        // clear the overflow flag, keep eb / max_bw
-        SDQZ_CUDA(ctx, cudaMemsetAsync(&ctx->d_status->flags, 0, 8, ctx->stream));
-        if ((rc = launch_deflate(ctx, job))) return rc;
-        if ((rc = fetch_status(ctx))) return rc;
-        if (ctx->h_status->flags & F_OVERFLOW)
-            return set_error(ctx, SDQZ_EINVAL, "internal: capacity still exceeded");
-    }
-    const DevStatus& s = *ctx->h_status;
-    // zero padding after the payload: decoders peek past the last chunk (huffman.py:338)
-    {
-        auto& pb = ctx->bufs[S_PAYLOAD];
-        uint64_t pad = std::min<uint64_t>(64, pb.bytes - s.payload_bytes);
-        SDQZ_CUDA(ctx, cudaMemsetAsync((uint8_t*)pb.p + s.payload_bytes, 0, pad, ctx->stream));
-    }
-    sdqz_header h{};
-    h.dtype_code = (uint8_t)dtype;
-    h.ndims = (uint8_t)ndims;
-    h.eb_mode = (uint8_t)eb_mode;
-    h.unit_width = (uint8_t)unit_for((uint32_t)s.max_bw);
-    for (int a = 0; a < 3; a++) {
-        h.dims[a] = a < ndims ? dims[a] : 1;
-        h.block[a] = a < ndims ? block[a] : 1;
-    }
-    h.eb_resolved = s.eb;
-    h.eb_specified = eb;
-    h.cap = cap;
-    h.chunk_size = cs;
-    h.n_outliers = s.n_outliers;
-    h.n_chunks = C;
-    h.payload_bytes = s.payload_bytes;
-    ctx->last_hdr = h;
-    ctx->have_archive = true;
-    if (hdr) *hdr = h;
+    const uint64_t gen0 = ctx->gen;
+    if ((rc = compress_enqueue(ctx, cst))) return rc;
+    if ((rc = compress_finish(ctx, cst, hdr))) return rc;
+    if (graphs && ctx->last_comp_key == key && ctx->gen == gen0) capture_compress(ctx, cst, key);
+    ctx->last_comp_key = key;
     return SDQZ_OK;
 }
 

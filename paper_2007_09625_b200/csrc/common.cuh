@@ -172,6 +172,20 @@ struct sdqz_ctx {
     sdqz_header last_hdr{};
     bool have_archive = false;
 
+    // captured pipelines (CUDA graphs), valid while the scratch arena's
+    // generation is unchanged
+    struct Graph {
+        cudaGraphExec_t exec = nullptr;
+        std::string key;
+        uint64_t gen = 0;
+        uint64_t nlaunch = 0;
+    };
+    uint64_t gen = 0;
+    Graph g_comp, g_decomp;
+    std::string last_comp_key, last_decomp_key;
+    uint64_t graph_replays = 0;
+    cudaStream_t cap_stream = nullptr;   // capture stream
+
     // optional per-kernel device timer (bench / profiling)
     bool timing = false;
     std::vector<cudaEvent_t> ev_pool;
@@ -194,6 +208,8 @@ int cuda_check(sdqz_ctx* ctx, cudaError_t e, const char* what);
 void* scratch(sdqz_ctx* ctx, int slot, size_t bytes, cudaError_t* e);
 int fetch_status(sdqz_ctx* ctx);      // D2H of the status block + sync
 int reset_status(sdqz_ctx* ctx);      // memset status on stream
+int enqueue_status_copy(sdqz_ctx* ctx);   // D2H of the status block (no sync)
+int sync_status(sdqz_ctx* ctx);           // stream sync (+ timer flush)
 int reset_status_eb(sdqz_ctx* ctx, double eb, bool has_eb);   // ... and set eb / 2eb
 
 #define SDQZ_CUDA(ctx, expr)                                                      \
