@@ -425,6 +425,7 @@ int compress_prepare(sdqz_ctx* ctx, CompressState& c) {
     c.job.in_kind = c.dtype;
     c.job.out_records = c.rec;
     c.job.out_cap = c.rec_cap;
+    c.job.trusted = true;   // K2's codes: < cap and all present in the book
     return SDQZ_OK;
 }
 

@@ -540,6 +540,7 @@ struct DeflateArgs {
     unsigned long long* records;         // {idx, f64 bits} pairs
     unsigned long long out_cap;
     DevStatus* st;
+    bool trusted;
 };
 
 __device__ __forceinline__ uint32_t unit_of(const DeflateArgs& a) {
@@ -580,6 +581,54 @@ __device__ __forceinline__ void unit_of_code(const DeflateArgs& a, const unsigne
         return;
     }
     fetch_unit<SRC>(a.src, tab, i, a.cap, unit, w, cw, c_out, bad_range);
+}
+
+__device__ __forceinline__ bool zero_half16(uint32_t w) {   // either 16-bit half == 0
+    return ((w - 0x00010001u) & ~w & 0x80008000u) != 0;
+}
+
+// stats for codes produced by K2 (always < cap, every symbol present in the
+// book): a byte table of widths, two lookups per 32-bit word, zero codes
+// counted exactly only in words that hold one (rare)
+__global__ void __launch_bounds__(256) chunk_stats_fast_kernel(DeflateArgs a) {
+    __shared__ uint8_t s_w[4096];
+    const uint32_t wshift = unit_of(a) - 8;
+    for (uint32_t i = threadIdx.x; i < a.cap; i += blockDim.x) s_w[i] = (uint8_t)(a.gtable[i] >> wshift);
+    __syncthreads();
+    const uint32_t lane = lane_id();
+    const uint16_t* src = (const uint16_t*)a.src;
+    for (uint64_t c = blockIdx.x * 8ull + (threadIdx.x >> 5); c < a.nchunks; c += gridDim.x * 8ull) {
+        const uint64_t s = c * a.chunk, e = umin(s + a.chunk, a.n);
+        uint32_t bits = 0, zeros = 0;
+        uint64_t i0 = s + 8 * lane;
+        if ((s & 7) == 0) {
+            for (; i0 + 8 <= e; i0 += 256) {
+                const uint4 v = __ldg(reinterpret_cast<const uint4*>(src + i0));
+                const uint32_t wv[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+                for (int k = 0; k < 4; k++) {
+                    bits += (uint32_t)s_w[wv[k] & 0xFFFF] + (uint32_t)s_w[wv[k] >> 16];
+                    if (zero_half16(wv[k])) zeros += ((wv[k] & 0xFFFF) == 0) + ((wv[k] >> 16) == 0);
+                }
+            }
+        }
+        for (; i0 < e; i0 += 256) {   // unaligned chunk or ragged tail
+#pragma unroll
+            for (int k = 0; k < 8; k++) {
+                if (i0 + k < e) {
+                    const uint32_t code = src[i0 + k];
+                    bits += s_w[code];
+                    zeros += code == 0;
+                }
+            }
+        }
+        bits = __reduce_add_sync(kFull, bits);
+        zeros = __reduce_add_sync(kFull, zeros);
+        if (lane == 0) {
+            a.chunk_bits[c] = bits;
+            if (a.chunk_zeros) a.chunk_zeros[c] = zeros;
+        }
+    }
 }
 
 // stats: warp per chunk -> bits, zero codes; flags range / absent-symbol errors
@@ -861,7 +910,7 @@ __device__ __forceinline__ bool zero_half(uint32_t w) {   // either 16-bit half 
 }
 
 template <bool TS>
-__global__ void __launch_bounds__(256) chunk_pack32_kernel(DeflateArgs a) {
+__global__ void __launch_bounds__(256, 3) chunk_pack32_kernel(DeflateArgs a) {
     __shared__ uint32_t s_tab[TS ? 4096 : 1];
     __shared__ uint32_t s_buf[8][kRoundCodes * 24 / 32 + 4];
     if (a.st->flags & (F_CODE_RANGE | F_ABSENT_SYM | F_ZERO_WIDTH | F_OVERFLOW | F_BW_TOO_BIG |
@@ -886,14 +935,25 @@ __global__ void __launch_bounds__(256) chunk_pack32_kernel(DeflateArgs a) {
         uint32_t carry = (uint32_t)(B & 3) * 8;
         uint32_t carry_word = 0;
         uint64_t orec = a.out_off ? a.out_off[c] : 0;
+        // the next round's 16 codes per lane are in flight while this round packs
+        auto fetch = [&](uint64_t g, uint4& v0, uint4& v1) -> bool {
+            const uint64_t i0 = g + (uint64_t)kRun * lane;
+            if (i0 + kRun > e || (i0 & 7)) return false;
+            v0 = __ldg(reinterpret_cast<const uint4*>(src + i0));
+            v1 = __ldg(reinterpret_cast<const uint4*>(src + i0) + 1);
+            return true;
+        };
+        uint4 n0 = make_uint4(0, 0, 0, 0), n1 = n0;
+        bool nvalid = fetch(s, n0, n1);
         for (uint64_t g = s; g < e; g += kRoundCodes) {
             const uint64_t i0 = g + (uint64_t)kRun * lane;
             const uint32_t cnt = i0 < e ? (uint32_t)umin(kRun, e - i0) : 0;
+            const uint4 v0 = n0, v1 = n1;
+            const bool valid = nvalid;
+            nvalid = g + kRoundCodes < e && fetch(g + kRoundCodes, n0, n1);
             uint32_t code[kRun];
             bool anyz;
-            if (cnt == kRun && (i0 & 7) == 0) {
-                const uint4 v0 = __ldg(reinterpret_cast<const uint4*>(src + i0));
-                const uint4 v1 = __ldg(reinterpret_cast<const uint4*>(src + i0) + 1);
+            if (valid) {
                 const uint32_t wv[8] = {v0.x, v0.y, v0.z, v0.w, v1.x, v1.y, v1.z, v1.w};
                 anyz = false;
 #pragma unroll
@@ -1324,9 +1384,14 @@ int run_deflate(sdqz_ctx* ctx, DeflateArgs& a, bool payload) {
     uint64_t grid = ceil_div(a.nchunks, 8);
     if (grid > (uint64_t)ctx->num_sms * 16) grid = ctx->num_sms * 16;
     if (grid < 1) grid = 1;
-    if (ts) chunk_stats_kernel<SRC, true><<<(unsigned)grid, 256, smem, ctx->stream>>>(a);
-    else chunk_stats_kernel<SRC, false><<<(unsigned)grid, 256, 0, ctx->stream>>>(a);
-    SDQZ_LAUNCHED_NAMED(ctx, "chunk_stats_kernel");
+    if (SRC == SRC_CODES && a.gtable && a.trusted && a.cap <= 4096) {
+        chunk_stats_fast_kernel<<<(unsigned)grid, 256, 0, ctx->stream>>>(a);
+        SDQZ_LAUNCHED_NAMED(ctx, "chunk_stats_kernel");
+    } else {
+        if (ts) chunk_stats_kernel<SRC, true><<<(unsigned)grid, 256, smem, ctx->stream>>>(a);
+        else chunk_stats_kernel<SRC, false><<<(unsigned)grid, 256, 0, ctx->stream>>>(a);
+        SDQZ_LAUNCHED_NAMED(ctx, "chunk_stats_kernel");
+    }
     chunk_scan_kernel<<<1, 1024, 0, ctx->stream>>>(a);
     SDQZ_LAUNCHED_NAMED(ctx, "chunk_scan_kernel");
     if (SRC == SRC_CODES) {
@@ -1433,6 +1498,7 @@ int launch_deflate(sdqz_ctx* ctx, const DeflateJob& job) {
     a.idx_base = job.idx_base;
     a.records = (unsigned long long*)job.out_records;
     a.out_cap = job.out_cap;
+    a.trusted = job.trusted;
     a.st = ctx->d_status;
     if (a.nchunks == 0) return SDQZ_OK;
     a.byte_off = scratch_as<unsigned long long>(ctx, S_BYTE_OFF, a.nchunks, &rc);

@@ -55,6 +55,7 @@ struct DeflateJob {
     void* out_records = nullptr;         // {u64, f64}[max]
     uint64_t out_cap = 0;
     bool want_payload = true;
+    bool trusted = false;                // codes came from K2 (< cap, all present in the book)
 };
 int launch_deflate(sdqz_ctx* ctx, const DeflateJob& job);
 
