@@ -313,9 +313,11 @@ __global__ void __launch_bounds__(kBookThreads) codebook_kernel(
             }
             __syncthreads();
             if (nodes <= 8 * blockDim.x) {
-                // in place, staged through registers (<= 8 nodes per thread)
+                // in place, staged through registers (<= 8 nodes per thread);
+                // stops once every node points at the root (~log2 of the depth)
                 for (int it = 0; it < 13; it++) {
                     uint32_t dv[8], jv[8];
+                    bool done = true;
 #pragma unroll
                     for (int q = 0; q < 8; q++) {
                         uint32_t v = tid + q * blockDim.x;
@@ -323,9 +325,10 @@ __global__ void __launch_bounds__(kBookThreads) codebook_kernel(
                             uint32_t j = jc[v];
                             dv[q] = dc[v] + dc[j];
                             jv[q] = jc[j];
+                            done &= j == root;
                         }
                     }
-                    __syncthreads();
+                    if (__syncthreads_and(done)) break;
 #pragma unroll
                     for (int q = 0; q < 8; q++) {
                         uint32_t v = tid + q * blockDim.x;
