@@ -60,11 +60,14 @@ constexpr uint32_t kLongInvalid = 0x81;    // len 1 + flag (sym|len form)
 // ---------------------------------------------------------------------------
 // decode tables: one CTA
 // ---------------------------------------------------------------------------
+// part 0: T1/T3 tables; part 1: second-level table + the fallback LUT;
+// part -1: everything (both parts compute the shared preliminaries)
 __device__ __forceinline__ void dtab_body(const uint64_t* __restrict__ first,
                                           const int64_t* __restrict__ offsets,
                                           const uint32_t* __restrict__ symbols, int max_bw_arg,
                                           const DevStatus* st, uint32_t* __restrict__ tab,
-                                          uint32_t* __restrict__ old_lut) {
+                                          uint32_t* __restrict__ old_lut, int part) {
+    const bool p0 = part != 1, p1 = part != 0;
     __shared__ uint32_t pmax[kL1Size];
     __shared__ uint32_t s_one[kL1Size];   // first codeword of a 12-bit window: sym << 16 | len
     __shared__ uint16_t pbase[kL1Size];   // second-level base, 0xFFFF = none
@@ -73,7 +76,7 @@ __device__ __forceinline__ void dtab_body(const uint64_t* __restrict__ first,
     const int mx = max_bw_arg > 0 ? max_bw_arg : (int)st->max_bw;
     if (mx < 1 || mx > kMaxBw) return;
     if (mx > 32) {   // 64-bit codes: only the sequential decoder's table (lut_kernel's rule)
-        if (!old_lut) return;
+        if (!old_lut || !p1) return;
         const long long ns = offsets[mx + 1];
         for (uint32_t i = threadIdx.x; i < (1u << kLutBits); i += blockDim.x) {
             uint32_t e = 0;
@@ -104,7 +107,8 @@ __device__ __forceinline__ void dtab_body(const uint64_t* __restrict__ first,
     for (int b = threadIdx.x; b < 34; b += blockDim.x) s_first[b] = b <= mx ? first[b] : 0;
     for (int b = threadIdx.x; b < 35; b += blockDim.x) s_off[b] = b <= mx + 1 ? offsets[b] : offsets[mx + 1];
     for (uint32_t i = threadIdx.x; i < kL1Size; i += blockDim.x) pmax[i] = 0;
-    for (uint32_t i = threadIdx.x; i < kL2Max; i += blockDim.x) tab[kOffL2 + i] = kLongInvalid;
+    if (p1)
+        for (uint32_t i = threadIdx.x; i < kL2Max; i += blockDim.x) tab[kOffL2 + i] = kLongInvalid;
     __syncthreads();
     const long long nsym = s_off[mx + 1];
     // longest code under each 12-bit prefix
@@ -168,7 +172,7 @@ __device__ __forceinline__ void dtab_body(const uint64_t* __restrict__ first,
     }
     __syncthreads();
     // the sequential fallback decoder's table (huffman.cu lut_kernel format)
-    if (old_lut) {
+    if (old_lut && p1) {
         const int lb = mx < kLutBits ? mx : kLutBits;
         for (uint32_t i = threadIdx.x; i < (1u << kLutBits); i += blockDim.x) {
             uint32_t e = 0;
@@ -193,7 +197,7 @@ __device__ __forceinline__ void dtab_body(const uint64_t* __restrict__ first,
     }
     __syncthreads();
     // T1 / T3: greedy decode of each 12-bit window, one table lookup per codeword
-    for (uint32_t i = threadIdx.x; i < kL1Size; i += blockDim.x) {
+    for (uint32_t i = threadIdx.x; p0 && i < kL1Size; i += blockDim.x) {
         uint32_t o = 0, m = 0, mask = 0, zeros = 0, sym[3] = {0, 0, 0}, cum[3] = {0, 0, 0};
         while (o < (uint32_t)kL1) {
             const uint32_t one = s_one[(i << o) & (kL1Size - 1)];
@@ -232,7 +236,7 @@ __device__ __forceinline__ void dtab_body(const uint64_t* __restrict__ first,
         tab[kOffT3 + 2 * i + 1] = (uint32_t)(t3 >> 32);
     }
     // second-level entries
-    for (long long i = lo + threadIdx.x; i < nsym; i += blockDim.x) {
+    for (long long i = lo + threadIdx.x; p1 && i < nsym; i += blockDim.x) {
         int b = kL1 + 1;
         while (b < mx && i >= s_off[b + 1]) b++;
         const unsigned long long code = s_first[b] + (unsigned long long)(i - s_off[b]);
@@ -252,18 +256,19 @@ __global__ void __launch_bounds__(1024) dtab_kernel(const uint64_t* __restrict__
                                                     int max_bw_arg, const DevStatus* st,
                                                     uint32_t* __restrict__ tab,
                                                     uint32_t* __restrict__ old_lut) {
-    dtab_body(first, offsets, symbols, max_bw_arg, st, tab, old_lut);
+    dtab_body(first, offsets, symbols, max_bw_arg, st, tab, old_lut, -1);
 }
 
-// decompress prep in one launch: CTA 0 builds the decode tables, CTA 1 scans the
+// decompress prep in one launch: CTAs 0/1 build the decode tables (T1/T3 | second
+// level + fallback LUT), CTA 2 scans the
 // chunk byte offsets and clears the hand-back flags and the chunk counter
 __global__ void __launch_bounds__(1024) decode_prep_kernel(
     const uint64_t* __restrict__ first, const int64_t* __restrict__ offsets,
     const uint32_t* __restrict__ symbols, int max_bw_arg, DevStatus* st, uint32_t* __restrict__ tab,
     uint32_t* __restrict__ old_lut, const uint32_t* __restrict__ chunk_bits, uint64_t C,
     unsigned long long* __restrict__ byte_off, uint8_t* __restrict__ redo, unsigned int* counter) {
-    if (blockIdx.x == 0) {
-        dtab_body(first, offsets, symbols, max_bw_arg, st, tab, old_lut);
+    if (blockIdx.x < 2) {
+        dtab_body(first, offsets, symbols, max_bw_arg, st, tab, old_lut, (int)blockIdx.x);
     } else {
         for (uint64_t i = threadIdx.x; i < C; i += blockDim.x) redo[i] = 0;
         if (threadIdx.x == 0) *counter = 0;
@@ -767,7 +772,7 @@ int launch_decode_prep(sdqz_ctx* ctx, const uint64_t* first, const int64_t* offs
     uint32_t* tab = scratch_as<uint32_t>(ctx, S_DTAB, kTabWords, &rc);
     unsigned int* counter = scratch_as<unsigned int>(ctx, S_COUNTER, 4, &rc);
     if (!tab || !counter) return rc;
-    decode_prep_kernel<<<2, 1024, 0, ctx->stream>>>(first, offsets, symbols, max_bw, ctx->d_status, tab,
+    decode_prep_kernel<<<3, 1024, 0, ctx->stream>>>(first, offsets, symbols, max_bw, ctx->d_status, tab,
                                                     old_lut, chunk_bits, n_chunks, byte_off, redo,
                                                     counter);
     SDQZ_LAUNCHED_NAMED(ctx, "decode_prep_kernel");

@@ -20,9 +20,8 @@ __device__ __forceinline__ void block_chunk_scan(const uint32_t* __restrict__ ch
     const bool vec = (((uintptr_t)chunk_bits | (uintptr_t)chunk_zeros | (uintptr_t)byte_off |
                        (uintptr_t)out_off) & 15) == 0;
     unsigned long long carry_b = 0, carry_o = 0;
-    for (uint64_t r0 = 0; r0 < C; r0 += 4096) {
-        const uint64_t i0 = r0 + 4 * (uint64_t)tid;
-        uint32_t vb[4], vz[4];
+    // row r+1's loads are issued before row r is scanned
+    auto load = [&](uint64_t i0, uint32_t (&vb)[4], uint32_t (&vz)[4]) {
         if (vec && i0 + 4 <= C) {
             const uint4 u = *reinterpret_cast<const uint4*>(chunk_bits + i0);
             vb[0] = u.x; vb[1] = u.y; vb[2] = u.z; vb[3] = u.w;
@@ -39,6 +38,15 @@ __device__ __forceinline__ void block_chunk_scan(const uint32_t* __restrict__ ch
                 vz[q] = (i0 + q < C && chunk_zeros) ? chunk_zeros[i0 + q] : 0;
             }
         }
+    };
+    uint32_t nb[4], nz[4];
+    load(4 * (uint64_t)tid, nb, nz);
+    for (uint64_t r0 = 0; r0 < C; r0 += 4096) {
+        const uint64_t i0 = r0 + 4 * (uint64_t)tid;
+        uint32_t vb[4], vz[4];
+#pragma unroll
+        for (int q = 0; q < 4; q++) { vb[q] = nb[q]; vz[q] = nz[q]; }
+        if (r0 + 4096 < C) load(i0 + 4096, nb, nz);
         unsigned long long tb = 0, to = 0;
 #pragma unroll
         for (int q = 0; q < 4; q++) {
