@@ -262,55 +262,101 @@ __global__ void __launch_bounds__(kThreads, 2) dq3d_kernel(const void* __restric
 }
 
 // ----------------------------------------------------------------------------
-// 3D, block 8x8x8, fp32 input staged by TMA.  A CTA is 4 warps; each warp
-// streams its own tasks through a 2-stage shared-memory ring: the tile of
-// task t+1 (32 x 8 x 8 floats, OOB zero-filled by the TMA unit) is in flight
-// while task t is computed from shared memory, so the field is read once at
-// full bandwidth with no per-element address arithmetic or registers held
-// for loads.
+// 3D, block 8x8x8, fp32 input staged by TMA.  Each warp streams its own tasks
+// (4 blocks side by side along x, lane = x) through a 3-stage ring of
+// 32 x 8 x 2 tiles (OOB zero-filled by the TMA unit): the next two plane
+// pairs are in flight while one is computed from shared memory.
 //
-// One pass per task: every point is prequantized (fp64 reciprocal multiply,
-// exact division only in the 2^-22 rounding-tie neighbourhood), D_x D_y D_z
-// differenced in int32, coded and counted.  The 16 histogram bins around the
-// radius are lane-private shared counters (bank = lane: conflict-free atomics,
-// merged once per CTA); other codes go to the CTA's shared histogram.  A task
-// holding a value too large for the int32 path (|x / 2eb| >= 2^27 - 4) or a
-// non-finite value is rare: its counts are taken back and the task is redone
-// in fp64 in the reference's term order.
+// Prequantization in fixed point.  One fp64 FMA  R = |v| * RN(1/2eb) + C  with
+// C = 1.5 * 2^30 + 0.5 + 2^-21 lands in the binade [2^30, 2^31) whenever
+// |v / 2eb| < 2^29, where the ulp is 2^-22: the mantissa holds
+// x = round((|v|/2eb + 0.5) * 2^22) + 2 as a 52-bit integer, so
+// floor(|v| / 2eb + 0.5) is just bits [22, 51) of R (one funnel shift, no
+// float->int conversion).  The FMA is within 0.57 units of 2^-22 of the exact
+// value, so the result can differ from the reference's
+// floor(RN(RN(|v| / 2eb) + 0.5)) only when x mod 2^22 < 4 (a value within a
+// few 2^-22 of a rounding tie, probability ~1e-6).  Such values, and any
+// |v / 2eb| >= 2^27 - 2048 (high word of R at or above the bound; includes
+// NaN/Inf), mark the task; a marked task's counts are taken back and it is
+// redone in fp64 with exact division in the reference's term order.
+//
+// D_x D_y D_z are int32 differences (exact below 2^27); the code and its
+// histogram bin follow.  The 16 bins around the radius are lane-private
+// shared counters ([warp][lane][17]: odd stride, conflict-free), other codes
+// go to the CTA histogram: one red.shared per point either way.
 // ----------------------------------------------------------------------------
 constexpr int kTmaWarps = 8;
 constexpr int kStages = 3;                       // ring of plane-pair tiles per warp
 constexpr uint32_t kPair = 32 * 8 * 2;           // floats per stage: 32 x, 8 y, 2 z
 constexpr uint32_t kHot = 16;                    // lane-private bins per warp
+constexpr uint32_t kHotStride = 17;              // u32 per lane (odd: conflict-free)
+constexpr double kFixC = 1610612736.0 + 0.5 + 4.76837158203125e-07;   // 1.5*2^30 + 0.5 + 2^-21
+constexpr double kFixBound = 134215680.0;                             // 2^27 - 2048
 
-__device__ __forceinline__ void hot_add(uint32_t hot_s, uint32_t c, uint32_t wbase, HistCtx& h) {
-    const uint32_t dw = c - wbase;
-    if (dw < kHot) {
-        asm volatile("red.shared.add.u32 [%0], 1;" ::"r"(hot_s + dw * 128u) : "memory");
+// hot bin of code c for this lane: hb + 4c (hb = lane base - 4 wbase)
+__device__ __forceinline__ void hot_add(uint32_t hb, uint32_t c, uint32_t wbase, HistCtx& h, int by) {
+    if (c - wbase < kHot) {
+        asm volatile("red.shared.add.u32 [%0], %1;" ::"r"(hb + c * 4u), "r"(by) : "memory");
     } else if (h.shist) {
-        atomicAdd(&h.shist[c], 1u);
+        atomicAdd(&h.shist[c], (uint32_t)by);
     } else if (h.ghist) {
-        atomicAdd(&h.ghist[c], 1ull);
+        atomicAdd(&h.ghist[c], (unsigned long long)(long long)by);
     }
 }
 
-// take back the counts of a task's fast-path codes (read from global memory)
+// take back the counts of a task's fast-path codes (read back from global
+// memory: each lane reads the column it wrote)
 __device__ __noinline__ void dq3d_uncount(const uint16_t* __restrict__ codes, uint64_t base, uint64_t YX,
-                                          uint64_t X, bool xin, int nz, int ny, uint32_t hot_s,
+                                          uint64_t X, bool xin, int nz, int ny, uint32_t hb,
                                           uint32_t wbase, HistCtx h) {
+    if (!xin) return;
     for (int z = 0; z < nz; z++)
-        for (int y = 0; y < ny; y++) {
-            if (!xin) continue;
-            const uint32_t c = codes[base + z * YX + y * X];
-            const uint32_t dw = c - wbase;
-            if (dw < kHot) {
-                asm volatile("red.shared.add.u32 [%0], -1;" ::"r"(hot_s + dw * 128u) : "memory");
-            } else if (h.shist) {
-                atomicSub(&h.shist[c], 1u);
-            } else if (h.ghist) {
-                atomicAdd(&h.ghist[c], ~0ull);   // -1 mod 2^64
+        for (int y = 0; y < ny; y++) hot_add(hb, codes[base + z * YX + y * X], wbase, h, -1);
+}
+
+__device__ __forceinline__ uint16_t* row_ptr(uint16_t* p, uint32_t rowbytes, uint32_t y) {
+    return (uint16_t*)((char*)p + (y * rowbytes));
+}
+
+// one plane pair (2 z x 8 y) of a task.  FULL: every point is inside the
+// field (no predicates); SH: the CTA histogram is in shared memory.
+template <bool FULL, bool SH>
+__device__ __forceinline__ void dq3d_pair(const float* __restrict__ tile, uint32_t lane, uint32_t xl,
+                                          double rcp, uint32_t hi_bound, int r, uint32_t wbase,
+                                          uint32_t hb, uint32_t shist_s, HistCtx& h, int (&hprev)[8],
+                                          bool& mark, uint16_t* tbz0, uint16_t* tbz1, uint32_t rowbytes,
+                                          bool zin0, bool zin1, int ny) {
+#pragma unroll
+    for (int zz = 0; zz < 2; zz++) {
+        int gprev = 0;
+        uint16_t* const tbz = zz ? tbz1 : tbz0;
+        const bool zin = zz ? zin1 : zin0;
+#pragma unroll
+        for (int y = 0; y < 8; y++) {
+            const float v = tile[(zz * 8 + y) * 32 + lane];
+            const double R = __fma_rn((double)fabsf(v), rcp, kFixC);
+            const uint32_t lo = (uint32_t)__double2loint(R), hi = (uint32_t)__double2hiint(R);
+            mark |= ((lo & 0x3FFFFCu) == 0u) | (hi >= hi_bound);
+            const int s = __float_as_int(v) >> 31;
+            const int qv = (int)((__funnelshift_r(lo, hi, 22) & 0x1FFFFFFFu) ^ (uint32_t)s) - s;
+            const int left = __shfl_up_sync(kFull, qv, 1);
+            const int g = qv - (xl ? left : 0);
+            const int hh = g - gprev;
+            gprev = g;
+            const uint32_t uu = (uint32_t)(hh - hprev[y] + r);
+            hprev[y] = hh;
+            const uint32_t c = (uu - 1u) < (uint32_t)(2 * r - 1) ? uu : 0u;   // -r < delta < r
+            if (FULL || (zin && y < ny)) {
+                *row_ptr(tbz, rowbytes, (uint32_t)y) = (uint16_t)c;
+                if (SH) {   // one shared reduction: lane-private hot bin or CTA bin
+                    const uint32_t addr = (c - wbase < kHot ? hb : shist_s) + c * 4u;
+                    asm volatile("red.shared.add.u32 [%0], 1;" ::"r"(addr) : "memory");
+                } else {
+                    hot_add(hb, c, wbase, h, 1);
+                }
             }
         }
+    }
 }
 
 __global__ void __launch_bounds__(kTmaWarps * 32, 3) dq3d_tma_kernel(
@@ -320,24 +366,25 @@ __global__ void __launch_bounds__(kTmaWarps * 32, 3) dq3d_tma_kernel(
     extern __shared__ __align__(128) unsigned char dsm[];
     float* tiles = reinterpret_cast<float*>(dsm);                              // [warp][stage][kPair]
     uint64_t* bars = reinterpret_cast<uint64_t*>(dsm + kTmaWarps * kStages * kPair * 4);
-    uint32_t* hot = reinterpret_cast<uint32_t*>(bars + kTmaWarps * kStages);   // [warp][kHot][32]
-    uint32_t* shist_base = hot + kTmaWarps * kHot * 32;
-    for (uint32_t i = threadIdx.x; i < kTmaWarps * kHot * 32; i += blockDim.x) hot[i] = 0;
+    uint32_t* hot = reinterpret_cast<uint32_t*>(bars + kTmaWarps * kStages);   // [warp][lane][17]
+    uint32_t* shist_base = hot + kTmaWarps * 32 * kHotStride;
+    for (uint32_t i = threadIdx.x; i < kTmaWarps * 32 * kHotStride; i += blockDim.x) hot[i] = 0;
     HistCtx h;
     hist_init(h, shist_base, ghist, cap);   // (syncs)
     const double two_eb = st->two_eb;
     const double rcp = __drcp_rn(two_eb);
+    const uint32_t hi_bound = (uint32_t)__double2hiint(kFixC + kFixBound);
     const int r = (int)(cap >> 1);
     const uint32_t wbase = cap >= 2 * kHot ? (uint32_t)r - kHot / 2 : 0u;
     const uint32_t lane = lane_id(), wid = threadIdx.x >> 5, xl = lane & 7;
-    const uint32_t hot_s = smem_u32(hot + wid * kHot * 32 + lane);
+    const uint32_t hb = smem_u32(hot + (wid * 32 + lane) * kHotStride) - wbase * 4u;
     // task indices and in-task offsets fit 32 bits (TMA extents < 2^31, a task
-    // spans < 8 planes): 32-bit index math, one wide multiply-add per address
+    // spans < 8 planes): 32-bit index math
     const uint32_t nbx4 = (uint32_t)ceil_div(ceil_div(X, 8), 4), nby = (uint32_t)ceil_div(Y, 8),
                    nbz = (uint32_t)ceil_div(Z, 8);
     const uint32_t ntask = nbx4 * nby * nbz;
     const uint64_t YX = Y * X;
-    const uint32_t X32 = (uint32_t)X, YX32 = (uint32_t)umin(YX, 0xFFFFFFFFull);
+    const uint32_t rowbytes = (uint32_t)X * 2u, planebytes = (uint32_t)umin(YX * 2, 0xFFFFFFFFull);
     float* mytiles = tiles + (size_t)wid * kStages * kPair;
     uint64_t* mybar = bars + wid * kStages;
     if (lane == 0) {
@@ -345,7 +392,6 @@ __global__ void __launch_bounds__(kTmaWarps * 32, 3) dq3d_tma_kernel(
         fence_mbar_init();
     }
     __syncwarp();
-    // shared-address view of the CTA histogram (codes outside the hot window)
     const bool use_s = h.shist != nullptr;
     const uint32_t shist_s = use_s ? smem_u32(h.shist) : 0u;
     const uint32_t stride = gridDim.x * kTmaWarps;
@@ -374,10 +420,11 @@ __global__ void __launch_bounds__(kTmaWarps * 32, 3) dq3d_tma_kernel(
         const int ny = (int)umin(8, Y - y0), nz = (int)umin(8, Z - z0);
         const uint64_t base = z0 * YX + y0 * X + x;
         uint16_t* const tb = codes + base;
+        const bool full = __all_sync(kFull, xin) && ny == 8 && nz == 8;   // warp-uniform
         int hprev[8];
 #pragma unroll
         for (int y = 0; y < 8; y++) hprev[y] = 0;
-        bool big = false;
+        bool mark = false;
 #pragma unroll 1
         for (int pr = 0; pr < 4; pr++, u++) {
             if (lane == 0) issue(u + kStages - 1);
@@ -385,50 +432,28 @@ __global__ void __launch_bounds__(kTmaWarps * 32, 3) dq3d_tma_kernel(
             mbar_wait(&mybar[q], (phase >> q) & 1u);
             phase ^= 1u << q;
             const float* tile = mytiles + q * kPair;
-#pragma unroll
-            for (int zz = 0; zz < 2; zz++) {
-                int gprev = 0;
-                const bool zin = xin && 2 * pr + zz < nz;
-                const uint32_t zoff = (uint32_t)(2 * pr + zz) * YX32;
-#pragma unroll
-                for (int y = 0; y < 8; y++) {
-                    const float v = tile[(zz * 8 + y) * 32 + lane];
-                    // |x / 2eb| by reciprocal multiply; exact division only in the
-                    // 2^-22 neighbourhood of a rounding tie (warp-uniform branch)
-                    const double t = __dadd_rn(__dmul_rn((double)fabsf(v), rcp), 0.5);
-                    const double fl = floor(t);
-                    const double fr = __dsub_rn(t, fl);
-                    int m = (int)fl;
-                    const bool amb = (fr < 2.384185791015625e-07) | (fr > 1.0 - 2.384185791015625e-07);
-                    if (__any_sync(kFull, amb)) {
-                        if (amb) m = (int)floor(__dadd_rn(fabs(__ddiv_rn((double)v, two_eb)), 0.5));
-                    }
-                    big |= !(t < kIntBound);   // also NaN / Inf
-                    const int qv = v < 0.f ? -m : m;
-                    const int left = __shfl_up_sync(kFull, qv, 1);
-                    const int g = qv - (xl ? left : 0);
-                    const int hh = g - gprev;
-                    gprev = g;
-                    const int delta = hh - hprev[y];
-                    hprev[y] = hh;
-                    const uint32_t uu = (uint32_t)(delta + r);
-                    const uint32_t c = (uu - 1u) < (uint32_t)(2 * r - 1) ? uu : 0u;   // -r < delta < r
-                    if (zin && y < ny) {
-                        tb[zoff + (uint32_t)y * X32] = (uint16_t)c;
-                        const uint32_t dw = c - wbase;
-                        if (use_s) {   // one shared reduction: lane-private hot bin or CTA bin
-                            const uint32_t addr = dw < kHot ? hot_s + dw * 128u : shist_s + c * 4u;
-                            asm volatile("red.shared.add.u32 [%0], 1;" ::"r"(addr) : "memory");
-                        } else {
-                            hot_add(hot_s, c, wbase, h);
-                        }
-                    }
-                }
+            uint16_t* tbz0 = (uint16_t*)((char*)tb + (uint64_t)(2 * pr) * planebytes);
+            uint16_t* tbz1 = (uint16_t*)((char*)tbz0 + planebytes);
+            const bool zin0 = xin && 2 * pr < nz, zin1 = xin && 2 * pr + 1 < nz;
+            if (full) {
+                if (use_s)
+                    dq3d_pair<true, true>(tile, lane, xl, rcp, hi_bound, r, wbase, hb, shist_s, h, hprev,
+                                          mark, tbz0, tbz1, rowbytes, zin0, zin1, ny);
+                else
+                    dq3d_pair<true, false>(tile, lane, xl, rcp, hi_bound, r, wbase, hb, shist_s, h, hprev,
+                                           mark, tbz0, tbz1, rowbytes, zin0, zin1, ny);
+            } else {
+                if (use_s)
+                    dq3d_pair<false, true>(tile, lane, xl, rcp, hi_bound, r, wbase, hb, shist_s, h, hprev,
+                                           mark, tbz0, tbz1, rowbytes, zin0, zin1, ny);
+                else
+                    dq3d_pair<false, false>(tile, lane, xl, rcp, hi_bound, r, wbase, hb, shist_s, h,
+                                            hprev, mark, tbz0, tbz1, rowbytes, zin0, zin1, ny);
             }
             __syncwarp();   // the stage is refilled two units later
         }
-        if (__any_sync(kFull, big)) {
-            dq3d_uncount(codes, base, YX, X, xin, nz, ny, hot_s, wbase, h);
+        if (__any_sync(kFull, mark)) {
+            dq3d_uncount(codes, base, YX, X, xin, nz, ny, hb, wbase, h);
             dq3d_task_f64<0>(in, base, YX, X, xin, nz, ny, xl, two_eb, r, codes, h, bad);
         }
     }
@@ -438,7 +463,7 @@ __global__ void __launch_bounds__(kTmaWarps * 32, 3) dq3d_tma_kernel(
     for (uint32_t j = wid; j < kHot; j += kTmaWarps) {
         uint32_t v = 0;
 #pragma unroll
-        for (int w = 0; w < kTmaWarps; w++) v += hot[(w * kHot + j) * 32 + lane];
+        for (int w = 0; w < kTmaWarps; w++) v += hot[(w * 32 + lane) * kHotStride + j];
         v = __reduce_add_sync(kFull, v);
         if (lane == 0 && v && wbase + j < cap) {
             if (h.shist) atomicAdd(&h.shist[wbase + j], v);
@@ -718,11 +743,11 @@ int launch_kind(sdqz_ctx* ctx, const void* d_in, int ndims, const uint64_t dims[
         const uint32_t box[3] = {32, 8, 2};
         if (make_tensor_map(&map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, d_in, gd, gs, box)) {
             const size_t tsm = kTmaWarps * kStages * kPair * 4 + kTmaWarps * kStages * 8 +
-                               kTmaWarps * kHot * 32 * 4 + smem;
+                               kTmaWarps * 32 * kHotStride * 4 + smem;
             static bool attr_done = false;
             if (!attr_done) {
                 cudaFuncSetAttribute(dq3d_tma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     kTmaWarps * kStages * kPair * 4 + 16 * 1024 + 16 * 4096 + 256);
+                                     kTmaWarps * kStages * kPair * 4 + kTmaWarps * 32 * kHotStride * 4 + 16 * 4096 + 256);
                 attr_done = true;
             }
             const uint64_t ntask =

@@ -311,3 +311,56 @@ class TestCorruptStreams:
                 S.decompress(blob)
             assert str(ei.value) == str(werr)
             assert isinstance(ei.value, S.CorruptionError) == isinstance(werr, O.OracleCorruption)
+
+
+class TestDualquant3DPaths:
+    """The TMA-fed 3D dual-quant kernel (row pitch a multiple of 4 floats):
+    partial tasks at every edge, the task redo path (magnitudes at or above
+    2^27 units of 2eb, values on prequantization rounding ties), the shared
+    and global histogram variants."""
+
+    @staticmethod
+    def check(data, **kw):
+        blob = S.compress(data, **kw)
+        ref = O.compress(data, **kw)
+        assert blob == ref
+        assert np.array_equal(bits(S.decompress(blob)), bits(O.decompress(ref)))
+
+    @pytest.mark.parametrize("dims", [(8, 8, 32), (13, 17, 36), (9, 8, 64), (3, 5, 4), (17, 9, 100),
+                                      (24, 40, 128)])
+    def test_edges(self, dims):
+        f = S.generate_field("smooth", dims, seed=7).astype(np.float32)
+        self.check(f, eb=1e-3, mode="valrel")
+
+    @pytest.mark.parametrize("cap", [4, 16, 32, 1024, 65536])
+    def test_caps(self, cap):
+        rng = np.random.default_rng(cap)
+        f = np.cumsum(rng.normal(0, 1, (12, 20, 40)), axis=-1).astype(np.float32)
+        self.check(f, eb=0.05, mode="abs", cap=cap)
+
+    def test_big_magnitudes_redo(self):
+        rng = np.random.default_rng(11)
+        f = rng.normal(0, 1.0, (16, 24, 64)).astype(np.float32)
+        f[3:5, 2:9, 10:50] *= 3e8            # |x / 2eb| well above 2^27 in some tasks
+        f[12, 20, 63] = 2.0 ** 27 * 2e-3     # one value right at the int32 bound
+        self.check(f, eb=1e-3, mode="abs")
+
+    def test_rounding_ties(self):
+        rng = np.random.default_rng(5)
+        two_eb = 0.25
+        k = rng.integers(-4000, 4000, (16, 16, 32)).astype(np.float64)
+        f = ((k + 0.5) * two_eb).astype(np.float32)          # exact ties
+        f[::2] = np.nextafter(f[::2], np.float32(np.inf))    # one ulp off the tie
+        f[1::4] = np.nextafter(f[1::4], np.float32(-np.inf))
+        self.check(f, eb=two_eb / 2, mode="abs")
+        g = (k * 0.3 + 0.15).astype(np.float32)               # near-ties for a non-dyadic bound
+        self.check(g, eb=0.15, mode="abs")
+
+    def test_nonfinite_abs_mode(self):
+        f = np.zeros((8, 8, 32), np.float32)
+        f[4, 4, 17] = np.inf
+        with pytest.raises(S.SdqzError, match="NaN"):
+            S.compress(f, eb=0.1, mode="abs")
+        f[4, 4, 17] = np.nan
+        with pytest.raises(S.SdqzError, match="NaN"):
+            S.compress(f, eb=0.1, mode="abs")
