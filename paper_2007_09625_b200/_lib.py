@@ -17,7 +17,8 @@ from pathlib import Path
 
 from .core import CorruptionError, SdqzError
 
-LIB_PATH = Path(__file__).resolve().parent / "libsdqz_cuda.so"
+# SDQZ_LIB_PATH: load another build of the same library (A/B kernel experiments)
+LIB_PATH = Path(os.environ.get("SDQZ_LIB_PATH") or Path(__file__).resolve().parent / "libsdqz_cuda.so")
 
 SDQZ_OK, SDQZ_EINVAL, SDQZ_ECORRUPT, SDQZ_EFORMAT, SDQZ_ECUDA = range(5)
 HEADER_SIZE = 93

@@ -275,28 +275,28 @@ __global__ void __launch_bounds__(kThreads, 2) dq3d_kernel(const void* __restric
 // float->int conversion).  The FMA is within 0.57 units of 2^-22 of the exact
 // value, so the result can differ from the reference's
 // floor(RN(RN(|v| / 2eb) + 0.5)) only when x mod 2^22 < 4 (a value within a
-// few 2^-22 of a rounding tie, probability ~1e-6).  Such values, and any
+// few 2^-22 of a rounding tie, probability ~1e-6).  Such values are redone
+// in place with exact division (one warp vote per plane row set).  Any
 // |v / 2eb| >= 2^27 - 2048 (high word of R at or above the bound; includes
-// NaN/Inf), mark the task; a marked task's counts are taken back and it is
+// NaN/Inf) marks the task; a marked task's counts are taken back and it is
 // redone in fp64 with exact division in the reference's term order.
 //
 // D_x D_y D_z are int32 differences (exact below 2^27); the code and its
 // histogram bin follow.  The 16 bins around the radius are lane-private
-// shared counters ([warp][lane][17]: odd stride, conflict-free), other codes
-// go to the CTA histogram: one red.shared per point either way.
+// shared counters ([warp][bin][lane]: bank = lane, conflict-free), other
+// codes go to the CTA histogram: one red.shared per point either way.
 // ----------------------------------------------------------------------------
 constexpr int kTmaWarps = 8;
 constexpr int kStages = 3;                       // ring of plane-pair tiles per warp
 constexpr uint32_t kPair = 32 * 8 * 2;           // floats per stage: 32 x, 8 y, 2 z
 constexpr uint32_t kHot = 16;                    // lane-private bins per warp
-constexpr uint32_t kHotStride = 17;              // u32 per lane (odd: conflict-free)
 constexpr double kFixC = 1610612736.0 + 0.5 + 4.76837158203125e-07;   // 1.5*2^30 + 0.5 + 2^-21
 constexpr double kFixBound = 134215680.0;                             // 2^27 - 2048
 
-// hot bin of code c for this lane: hb + 4c (hb = lane base - 4 wbase)
+// hot bin of code c for this lane: hb + 128c (hb = lane base - 128 wbase)
 __device__ __forceinline__ void hot_add(uint32_t hb, uint32_t c, uint32_t wbase, HistCtx& h, int by) {
     if (c - wbase < kHot) {
-        asm volatile("red.shared.add.u32 [%0], %1;" ::"r"(hb + c * 4u), "r"(by) : "memory");
+        asm volatile("red.shared.add.u32 [%0], %1;" ::"r"(hb + c * 128u), "r"(by) : "memory");
     } else if (h.shist) {
         atomicAdd(&h.shist[c], (uint32_t)by);
     } else if (h.ghist) {
@@ -322,34 +322,60 @@ __device__ __forceinline__ uint16_t* row_ptr(uint16_t* p, uint32_t rowbytes, uin
 // field (no predicates); SH: the CTA histogram is in shared memory.
 template <bool FULL, bool SH>
 __device__ __forceinline__ void dq3d_pair(const float* __restrict__ tile, uint32_t lane, uint32_t xl,
-                                          double rcp, uint32_t hi_bound, int r, uint32_t wbase,
+                                          double rcp, double two_eb, uint32_t hi_bound, int r, uint32_t wbase,
                                           uint32_t hb, uint32_t shist_s, HistCtx& h, int (&hprev)[8],
                                           bool& mark, uint16_t* tbz0, uint16_t* tbz1, uint32_t rowbytes,
                                           bool zin0, bool zin1, int ny) {
+    // phases keep the 8 rows of a plane independent until the y recurrence:
+    // loads / prequantization / shuffles of all rows are in flight together
 #pragma unroll
     for (int zz = 0; zz < 2; zz++) {
-        int gprev = 0;
         uint16_t* const tbz = zz ? tbz1 : tbz0;
         const bool zin = zz ? zin1 : zin0;
+        int qv[8], left[8];
+        bool amb = false;
 #pragma unroll
         for (int y = 0; y < 8; y++) {
             const float v = tile[(zz * 8 + y) * 32 + lane];
             const double R = __fma_rn((double)fabsf(v), rcp, kFixC);
             const uint32_t lo = (uint32_t)__double2loint(R), hi = (uint32_t)__double2hiint(R);
-            mark |= ((lo & 0x3FFFFCu) == 0u) | (hi >= hi_bound);
+            amb |= (lo & 0x3FFFFCu) == 0u;
+            mark |= hi >= hi_bound;
             const int s = __float_as_int(v) >> 31;
-            const int qv = (int)((__funnelshift_r(lo, hi, 22) & 0x1FFFFFFFu) ^ (uint32_t)s) - s;
-            const int left = __shfl_up_sync(kFull, qv, 1);
-            const int g = qv - (xl ? left : 0);
+            qv[y] = (int)((__funnelshift_r(lo, hi, 22) & 0x1FFFFFFFu) ^ (uint32_t)s) - s;
+        }
+        if (__any_sync(kFull, amb)) {   // rare: exact division near a rounding tie
+#pragma unroll
+            for (int y = 0; y < 8; y++) {
+                const float v = tile[(zz * 8 + y) * 32 + lane];
+                const double R = __fma_rn((double)fabsf(v), rcp, kFixC);
+                if (((uint32_t)__double2loint(R) & 0x3FFFFCu) == 0u) {
+                    const int m = (int)floor(__dadd_rn(fabs(__ddiv_rn((double)v, two_eb)), 0.5));
+                    qv[y] = v < 0.f ? -m : m;
+                }
+            }
+        }
+#pragma unroll
+        for (int y = 0; y < 8; y++) left[y] = __shfl_up_sync(kFull, qv[y], 1);
+        int gprev = 0;
+        uint32_t cc[8];
+#pragma unroll
+        for (int y = 0; y < 8; y++) {
+            const int g = qv[y] - (xl ? left[y] : 0);
             const int hh = g - gprev;
             gprev = g;
             const uint32_t uu = (uint32_t)(hh - hprev[y] + r);
             hprev[y] = hh;
-            const uint32_t c = (uu - 1u) < (uint32_t)(2 * r - 1) ? uu : 0u;   // -r < delta < r
+            cc[y] = (uu - 1u) < (uint32_t)(2 * r - 1) ? uu : 0u;   // -r < delta < r
+        }
+#pragma unroll
+        for (int y = 0; y < 8; y++) {
+            const uint32_t c = cc[y];
             if (FULL || (zin && y < ny)) {
                 *row_ptr(tbz, rowbytes, (uint32_t)y) = (uint16_t)c;
                 if (SH) {   // one shared reduction: lane-private hot bin or CTA bin
-                    const uint32_t addr = (c - wbase < kHot ? hb : shist_s) + c * 4u;
+                    const bool hot = c - wbase < kHot;
+                    const uint32_t addr = c * (hot ? 128u : 4u) + (hot ? hb : shist_s);
                     asm volatile("red.shared.add.u32 [%0], 1;" ::"r"(addr) : "memory");
                 } else {
                     hot_add(hb, c, wbase, h, 1);
@@ -366,9 +392,9 @@ __global__ void __launch_bounds__(kTmaWarps * 32, 3) dq3d_tma_kernel(
     extern __shared__ __align__(128) unsigned char dsm[];
     float* tiles = reinterpret_cast<float*>(dsm);                              // [warp][stage][kPair]
     uint64_t* bars = reinterpret_cast<uint64_t*>(dsm + kTmaWarps * kStages * kPair * 4);
-    uint32_t* hot = reinterpret_cast<uint32_t*>(bars + kTmaWarps * kStages);   // [warp][lane][17]
-    uint32_t* shist_base = hot + kTmaWarps * 32 * kHotStride;
-    for (uint32_t i = threadIdx.x; i < kTmaWarps * 32 * kHotStride; i += blockDim.x) hot[i] = 0;
+    uint32_t* hot = reinterpret_cast<uint32_t*>(bars + kTmaWarps * kStages);   // [warp][kHot][32]
+    uint32_t* shist_base = hot + kTmaWarps * kHot * 32;
+    for (uint32_t i = threadIdx.x; i < kTmaWarps * kHot * 32; i += blockDim.x) hot[i] = 0;
     HistCtx h;
     hist_init(h, shist_base, ghist, cap);   // (syncs)
     const double two_eb = st->two_eb;
@@ -377,7 +403,7 @@ __global__ void __launch_bounds__(kTmaWarps * 32, 3) dq3d_tma_kernel(
     const int r = (int)(cap >> 1);
     const uint32_t wbase = cap >= 2 * kHot ? (uint32_t)r - kHot / 2 : 0u;
     const uint32_t lane = lane_id(), wid = threadIdx.x >> 5, xl = lane & 7;
-    const uint32_t hb = smem_u32(hot + (wid * 32 + lane) * kHotStride) - wbase * 4u;
+    const uint32_t hb = smem_u32(hot + wid * kHot * 32 + lane) - wbase * 128u;
     // task indices and in-task offsets fit 32 bits (TMA extents < 2^31, a task
     // spans < 8 planes): 32-bit index math
     const uint32_t nbx4 = (uint32_t)ceil_div(ceil_div(X, 8), 4), nby = (uint32_t)ceil_div(Y, 8),
@@ -396,25 +422,36 @@ __global__ void __launch_bounds__(kTmaWarps * 32, 3) dq3d_tma_kernel(
     const uint32_t shist_s = use_s ? smem_u32(h.shist) : 0u;
     const uint32_t stride = gridDim.x * kTmaWarps;
     const uint32_t first = blockIdx.x * kTmaWarps + wid;
-    // unit u = (task first + (u >> 2) * stride, z planes 2(u & 3) .. +1)
-    auto issue = [&](uint32_t u) {
-        const uint32_t task = first + (u >> 2) * stride;
-        if (task >= ntask) return;
-        const uint32_t bx4 = task % nbx4, t2 = task / nbx4;
-        const uint32_t by = t2 % nby, bz = t2 / nby;
-        const uint32_t q = u % kStages;
+    // unit = (task, plane pair); the ring runs two units ahead: while pair pr
+    // of a task is computed, pair pr + 2 (of this task or the next) loads
+    auto issue = [&](uint32_t q, uint32_t bx4, uint32_t by, uint32_t z) {
         mbar_expect_tx(&mybar[q], kPair * 4);
-        tma_load_3d(mytiles + q * kPair, &tmap, (int)(bx4 * 32), (int)(by * 8),
-                    (int)(bz * 8 + 2 * (u & 3)), &mybar[q]);
+        tma_load_3d(mytiles + q * kPair, &tmap, (int)(bx4 * 32), (int)(by * 8), (int)z, &mybar[q]);
     };
-    if (lane == 0)
-        for (uint32_t q = 0; q < kStages - 1; q++) issue(q);
-    uint32_t phase = 0;   // bit q: parity of stage q
-    uint32_t u = 0;
+    uint32_t cbx = 0, cby = 0, cbz = 0;   // coordinates of the current task
+    if (first < ntask) {
+        cbx = first % nbx4;
+        const uint32_t t2 = first / nbx4;
+        cby = t2 % nby;
+        cbz = t2 / nby;
+        if (lane == 0) {
+            issue(0, cbx, cby, cbz * 8);
+            issue(1, cbx, cby, cbz * 8 + 2);
+        }
+    }
+    uint32_t phase = 0;    // bit q: parity of stage q
+    uint32_t qc = 0;       // stage of the unit being computed
     bool bad = false;
     for (uint32_t task = first; task < ntask; task += stride) {
-        const uint32_t bx4 = task % nbx4, t2 = task / nbx4;
-        const uint32_t by = t2 % nby, bz = t2 / nby;
+        const uint32_t bx4 = cbx, by = cby, bz = cbz;
+        const uint32_t nt = task + stride;
+        const bool has_next = nt < ntask;
+        if (has_next) {
+            cbx = nt % nbx4;
+            const uint32_t t2 = nt / nbx4;
+            cby = t2 % nby;
+            cbz = t2 / nby;
+        }
         const uint64_t x = (uint64_t)bx4 * 32 + lane, y0 = (uint64_t)by * 8, z0 = (uint64_t)bz * 8;
         const bool xin = x < X;
         const int ny = (int)umin(8, Y - y0), nz = (int)umin(8, Z - z0);
@@ -426,28 +463,32 @@ __global__ void __launch_bounds__(kTmaWarps * 32, 3) dq3d_tma_kernel(
         for (int y = 0; y < 8; y++) hprev[y] = 0;
         bool mark = false;
 #pragma unroll 1
-        for (int pr = 0; pr < 4; pr++, u++) {
-            if (lane == 0) issue(u + kStages - 1);
-            const uint32_t q = u % kStages;
-            mbar_wait(&mybar[q], (phase >> q) & 1u);
-            phase ^= 1u << q;
-            const float* tile = mytiles + q * kPair;
+        for (uint32_t pr = 0; pr < 4; pr++) {
+            if (lane == 0) {
+                const uint32_t qn = qc == 0 ? 2 : qc - 1;   // (qc + 2) % 3
+                if (pr < 2) issue(qn, bx4, by, bz * 8 + 2 * (pr + 2));
+                else if (has_next) issue(qn, cbx, cby, cbz * 8 + 2 * (pr - 2));
+            }
+            mbar_wait(&mybar[qc], (phase >> qc) & 1u);
+            phase ^= 1u << qc;
+            const float* tile = mytiles + qc * kPair;
+            qc = qc == 2 ? 0 : qc + 1;
             uint16_t* tbz0 = (uint16_t*)((char*)tb + (uint64_t)(2 * pr) * planebytes);
             uint16_t* tbz1 = (uint16_t*)((char*)tbz0 + planebytes);
-            const bool zin0 = xin && 2 * pr < nz, zin1 = xin && 2 * pr + 1 < nz;
+            const bool zin0 = xin && (int)(2 * pr) < nz, zin1 = xin && (int)(2 * pr + 1) < nz;
             if (full) {
                 if (use_s)
-                    dq3d_pair<true, true>(tile, lane, xl, rcp, hi_bound, r, wbase, hb, shist_s, h, hprev,
+                    dq3d_pair<true, true>(tile, lane, xl, rcp, two_eb, hi_bound, r, wbase, hb, shist_s, h, hprev,
                                           mark, tbz0, tbz1, rowbytes, zin0, zin1, ny);
                 else
-                    dq3d_pair<true, false>(tile, lane, xl, rcp, hi_bound, r, wbase, hb, shist_s, h, hprev,
+                    dq3d_pair<true, false>(tile, lane, xl, rcp, two_eb, hi_bound, r, wbase, hb, shist_s, h, hprev,
                                            mark, tbz0, tbz1, rowbytes, zin0, zin1, ny);
             } else {
                 if (use_s)
-                    dq3d_pair<false, true>(tile, lane, xl, rcp, hi_bound, r, wbase, hb, shist_s, h, hprev,
+                    dq3d_pair<false, true>(tile, lane, xl, rcp, two_eb, hi_bound, r, wbase, hb, shist_s, h, hprev,
                                            mark, tbz0, tbz1, rowbytes, zin0, zin1, ny);
                 else
-                    dq3d_pair<false, false>(tile, lane, xl, rcp, hi_bound, r, wbase, hb, shist_s, h,
+                    dq3d_pair<false, false>(tile, lane, xl, rcp, two_eb, hi_bound, r, wbase, hb, shist_s, h,
                                             hprev, mark, tbz0, tbz1, rowbytes, zin0, zin1, ny);
             }
             __syncwarp();   // the stage is refilled two units later
@@ -463,7 +504,7 @@ __global__ void __launch_bounds__(kTmaWarps * 32, 3) dq3d_tma_kernel(
     for (uint32_t j = wid; j < kHot; j += kTmaWarps) {
         uint32_t v = 0;
 #pragma unroll
-        for (int w = 0; w < kTmaWarps; w++) v += hot[(w * 32 + lane) * kHotStride + j];
+        for (int w = 0; w < kTmaWarps; w++) v += hot[(w * kHot + j) * 32 + lane];
         v = __reduce_add_sync(kFull, v);
         if (lane == 0 && v && wbase + j < cap) {
             if (h.shist) atomicAdd(&h.shist[wbase + j], v);
@@ -743,11 +784,11 @@ int launch_kind(sdqz_ctx* ctx, const void* d_in, int ndims, const uint64_t dims[
         const uint32_t box[3] = {32, 8, 2};
         if (make_tensor_map(&map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, d_in, gd, gs, box)) {
             const size_t tsm = kTmaWarps * kStages * kPair * 4 + kTmaWarps * kStages * 8 +
-                               kTmaWarps * 32 * kHotStride * 4 + smem;
+                               kTmaWarps * kHot * 32 * 4 + smem;
             static bool attr_done = false;
             if (!attr_done) {
                 cudaFuncSetAttribute(dq3d_tma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     kTmaWarps * kStages * kPair * 4 + kTmaWarps * 32 * kHotStride * 4 + 16 * 4096 + 256);
+                                     kTmaWarps * kStages * kPair * 4 + kTmaWarps * kHot * 32 * 4 + 16 * 4096 + 256);
                 attr_done = true;
             }
             const uint64_t ntask =
