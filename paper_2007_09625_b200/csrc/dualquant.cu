@@ -267,19 +267,21 @@ __global__ void __launch_bounds__(kThreads, 2) dq3d_kernel(const void* __restric
 // 32 x 8 x 2 tiles (OOB zero-filled by the TMA unit): the next two plane
 // pairs are in flight while one is computed from shared memory.
 //
-// Prequantization in fixed point.  One fp64 FMA  R = |v| * RN(1/2eb) + C  with
-// C = 1.5 * 2^30 + 0.5 + 2^-21 lands in the binade [2^30, 2^31) whenever
+// Prequantization in fixed point.  One fp64 FMA  R = v * RN(1/2eb) + C  with
+// C = 1.5 * 2^30 + 0.5 + 2^-21 stays in the binade [2^30, 2^31) whenever
 // |v / 2eb| < 2^29, where the ulp is 2^-22: the mantissa holds
-// x = round((|v|/2eb + 0.5) * 2^22) + 2 as a 52-bit integer, so
-// floor(|v| / 2eb + 0.5) is just bits [22, 51) of R (one funnel shift, no
-// float->int conversion).  The FMA is within 0.57 units of 2^-22 of the exact
-// value, so the result can differ from the reference's
-// floor(RN(RN(|v| / 2eb) + 0.5)) only when x mod 2^22 < 4 (a value within a
-// few 2^-22 of a rounding tie, probability ~1e-6).  Such values are redone
-// in place with exact division (one warp vote per plane row set).  Any
-// |v / 2eb| >= 2^27 - 2048 (high word of R at or above the bound; includes
-// NaN/Inf) marks the task; a marked task's counts are taken back and it is
-// redone in fp64 with exact division in the reference's term order.
+// x = round((v/2eb + 0.5) * 2^22) + 2^51 + 2 as an integer, so the rounded
+// quotient is bits [22, 51) of R plus a constant bias K (one funnel shift, no
+// float->int conversion, no sign handling: the bias cancels in the Lorenzo
+// differences and is subtracted only at the x edge of a block).  The FMA is
+// within 0.57 units of 2^-22 of the exact value, so the result can differ
+// from the reference's copysign(floor(RN(RN(|v| / 2eb) + 0.5)), v) only when
+// x mod 2^22 < 4 (a value within a few 2^-22 of a rounding tie, probability
+// ~1e-6).  Such values are redone in place with exact division (one warp vote
+// per plane).  Any |v / 2eb| >= 2^27 - 2048 (high word of R outside the
+// bound; includes NaN/Inf) marks the task; a marked task's counts are taken
+// back and it is redone in fp64 with exact division in the reference's term
+// order.
 //
 // D_x D_y D_z are int32 differences (exact below 2^27); the code and its
 // histogram bin follow.  The 16 bins around the radius are lane-private
@@ -292,6 +294,7 @@ constexpr uint32_t kPair = 32 * 8 * 2;           // floats per stage: 32 x, 8 y,
 constexpr uint32_t kHot = 16;                    // lane-private bins per warp
 constexpr double kFixC = 1610612736.0 + 0.5 + 4.76837158203125e-07;   // 1.5*2^30 + 0.5 + 2^-21
 constexpr double kFixBound = 134215680.0;                             // 2^27 - 2048
+constexpr int kFixK = 0x60000000;   // bits [22, 53) of C - 0.5 - 2^-21 (exponent bit 52 + 2^51)
 
 // hot bin of code c for this lane: hb + 128c (hb = lane base - 128 wbase)
 __device__ __forceinline__ void hot_add(uint32_t hb, uint32_t c, uint32_t wbase, HistCtx& h, int by) {
@@ -322,7 +325,7 @@ __device__ __forceinline__ uint16_t* row_ptr(uint16_t* p, uint32_t rowbytes, uin
 // field (no predicates); SH: the CTA histogram is in shared memory.
 template <bool FULL, bool SH>
 __device__ __forceinline__ void dq3d_pair(const float* __restrict__ tile, uint32_t lane, uint32_t xl,
-                                          double rcp, double two_eb, uint32_t hi_bound, int r, uint32_t wbase,
+                                          double rcp, double two_eb, uint32_t hi_lo, uint32_t hi_span, int r, uint32_t wbase,
                                           uint32_t hb, uint32_t shist_s, HistCtx& h, int (&hprev)[8],
                                           bool& mark, uint16_t* tbz0, uint16_t* tbz1, uint32_t rowbytes,
                                           bool zin0, bool zin1, int ny) {
@@ -332,26 +335,25 @@ __device__ __forceinline__ void dq3d_pair(const float* __restrict__ tile, uint32
     for (int zz = 0; zz < 2; zz++) {
         uint16_t* const tbz = zz ? tbz1 : tbz0;
         const bool zin = zz ? zin1 : zin0;
-        int qv[8], left[8];
+        int qv[8], left[8];   // rounded quotients + kFixK
         bool amb = false;
 #pragma unroll
         for (int y = 0; y < 8; y++) {
             const float v = tile[(zz * 8 + y) * 32 + lane];
-            const double R = __fma_rn((double)fabsf(v), rcp, kFixC);
+            const double R = __fma_rn((double)v, rcp, kFixC);
             const uint32_t lo = (uint32_t)__double2loint(R), hi = (uint32_t)__double2hiint(R);
             amb |= (lo & 0x3FFFFCu) == 0u;
-            mark |= hi >= hi_bound;
-            const int s = __float_as_int(v) >> 31;
-            qv[y] = (int)((__funnelshift_r(lo, hi, 22) & 0x1FFFFFFFu) ^ (uint32_t)s) - s;
+            mark |= (hi - hi_lo) >= hi_span;
+            qv[y] = (int)__funnelshift_r(lo, hi, 22);
         }
         if (__any_sync(kFull, amb)) {   // rare: exact division near a rounding tie
 #pragma unroll
             for (int y = 0; y < 8; y++) {
                 const float v = tile[(zz * 8 + y) * 32 + lane];
-                const double R = __fma_rn((double)fabsf(v), rcp, kFixC);
+                const double R = __fma_rn((double)v, rcp, kFixC);
                 if (((uint32_t)__double2loint(R) & 0x3FFFFCu) == 0u) {
                     const int m = (int)floor(__dadd_rn(fabs(__ddiv_rn((double)v, two_eb)), 0.5));
-                    qv[y] = v < 0.f ? -m : m;
+                    qv[y] = (v < 0.f ? -m : m) + kFixK;
                 }
             }
         }
@@ -361,7 +363,7 @@ __device__ __forceinline__ void dq3d_pair(const float* __restrict__ tile, uint32
         uint32_t cc[8];
 #pragma unroll
         for (int y = 0; y < 8; y++) {
-            const int g = qv[y] - (xl ? left[y] : 0);
+            const int g = qv[y] - (xl ? left[y] : kFixK);
             const int hh = g - gprev;
             gprev = g;
             const uint32_t uu = (uint32_t)(hh - hprev[y] + r);
@@ -385,7 +387,7 @@ __device__ __forceinline__ void dq3d_pair(const float* __restrict__ tile, uint32
     }
 }
 
-__global__ void __launch_bounds__(kTmaWarps * 32, 3) dq3d_tma_kernel(
+__global__ void __launch_bounds__(kTmaWarps * 32, 2) dq3d_tma_kernel(
     const __grid_constant__ CUtensorMap tmap, const float* __restrict__ in, uint64_t Z, uint64_t Y,
     uint64_t X, uint32_t cap, DevStatus* st, uint16_t* __restrict__ codes,
     unsigned long long* ghist) {
@@ -399,7 +401,9 @@ __global__ void __launch_bounds__(kTmaWarps * 32, 3) dq3d_tma_kernel(
     hist_init(h, shist_base, ghist, cap);   // (syncs)
     const double two_eb = st->two_eb;
     const double rcp = __drcp_rn(two_eb);
-    const uint32_t hi_bound = (uint32_t)__double2hiint(kFixC + kFixBound);
+    // in bounds: hi(C - B) < hi(R) < hi(C + B), one unsigned compare
+    const uint32_t hi_lo = (uint32_t)__double2hiint(kFixC - kFixBound) + 1u;
+    const uint32_t hi_span = (uint32_t)__double2hiint(kFixC + kFixBound) - hi_lo;
     const int r = (int)(cap >> 1);
     const uint32_t wbase = cap >= 2 * kHot ? (uint32_t)r - kHot / 2 : 0u;
     const uint32_t lane = lane_id(), wid = threadIdx.x >> 5, xl = lane & 7;
@@ -478,17 +482,17 @@ __global__ void __launch_bounds__(kTmaWarps * 32, 3) dq3d_tma_kernel(
             const bool zin0 = xin && (int)(2 * pr) < nz, zin1 = xin && (int)(2 * pr + 1) < nz;
             if (full) {
                 if (use_s)
-                    dq3d_pair<true, true>(tile, lane, xl, rcp, two_eb, hi_bound, r, wbase, hb, shist_s, h, hprev,
+                    dq3d_pair<true, true>(tile, lane, xl, rcp, two_eb, hi_lo, hi_span, r, wbase, hb, shist_s, h, hprev,
                                           mark, tbz0, tbz1, rowbytes, zin0, zin1, ny);
                 else
-                    dq3d_pair<true, false>(tile, lane, xl, rcp, two_eb, hi_bound, r, wbase, hb, shist_s, h, hprev,
+                    dq3d_pair<true, false>(tile, lane, xl, rcp, two_eb, hi_lo, hi_span, r, wbase, hb, shist_s, h, hprev,
                                            mark, tbz0, tbz1, rowbytes, zin0, zin1, ny);
             } else {
                 if (use_s)
-                    dq3d_pair<false, true>(tile, lane, xl, rcp, two_eb, hi_bound, r, wbase, hb, shist_s, h, hprev,
+                    dq3d_pair<false, true>(tile, lane, xl, rcp, two_eb, hi_lo, hi_span, r, wbase, hb, shist_s, h, hprev,
                                            mark, tbz0, tbz1, rowbytes, zin0, zin1, ny);
                 else
-                    dq3d_pair<false, false>(tile, lane, xl, rcp, two_eb, hi_bound, r, wbase, hb, shist_s, h,
+                    dq3d_pair<false, false>(tile, lane, xl, rcp, two_eb, hi_lo, hi_span, r, wbase, hb, shist_s, h,
                                             hprev, mark, tbz0, tbz1, rowbytes, zin0, zin1, ny);
             }
             __syncwarp();   // the stage is refilled two units later
