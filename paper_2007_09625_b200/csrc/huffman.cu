@@ -702,9 +702,9 @@ __global__ void __launch_bounds__(256) chunk_stats_kernel(DeflateArgs a) {
 // Exclusive scans over chunks (single CTA, 1024 threads): byte offsets
 // (ceil(bits/8)) and outlier offsets.  Tiles of 4096 chunks are staged in
 // shared memory with coalesced loads; each thread scans 4 consecutive entries.
-__global__ void __launch_bounds__(1024) chunk_scan_kernel(DeflateArgs a) {
-    block_chunk_scan(a.chunk_bits, a.chunk_zeros, a.nchunks, a.byte_off, a.out_off, a.payload_cap,
-                     a.records != nullptr, a.out_cap, a.st);
+__global__ void __cluster_dims__(kScanCtas, 1, 1) __launch_bounds__(1024) chunk_scan_kernel(DeflateArgs a) {
+    cluster_chunk_scan(blockIdx.x, a.chunk_bits, a.chunk_zeros, a.nchunks, a.byte_off, a.out_off,
+                       a.payload_cap, a.records != nullptr, a.out_cap, a.st);
 }
 
 __device__ __forceinline__ void store_word(uint8_t* payload, uint64_t wbyte, uint32_t word,
@@ -1395,7 +1395,7 @@ int run_deflate(sdqz_ctx* ctx, DeflateArgs& a, bool payload) {
         else chunk_stats_kernel<SRC, false><<<(unsigned)grid, 256, 0, ctx->stream>>>(a);
         SDQZ_LAUNCHED_NAMED(ctx, "chunk_stats_kernel");
     }
-    chunk_scan_kernel<<<1, 1024, 0, ctx->stream>>>(a);
+    chunk_scan_kernel<<<kScanCtas, 1024, 0, ctx->stream>>>(a);
     SDQZ_LAUNCHED_NAMED(ctx, "chunk_scan_kernel");
     if (SRC == SRC_CODES) {
         static bool attr = false;   // 28.8 KB static + up to 32 KB table > the 48 KB default
@@ -1555,7 +1555,7 @@ int launch_inflate(sdqz_ctx* ctx, const uint8_t* payload, uint64_t payload_bytes
     if (!a.byte_off) return rc;
     uint64_t grid = ceil_div(n_chunks, 64);
     if (out32) {
-        chunk_scan_kernel<<<1, 1024, 0, ctx->stream>>>(a);
+        chunk_scan_kernel<<<kScanCtas, 1024, 0, ctx->stream>>>(a);
         SDQZ_LAUNCHED_NAMED(ctx, "chunk_scan_kernel");
         inflate_kernel<true><<<(unsigned)grid, 64, 0, ctx->stream>>>(
             payload, nwords, chunk_bits, a.byte_off, n_chunks, chunk, n, first, offsets, symbols, lut,

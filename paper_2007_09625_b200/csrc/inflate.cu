@@ -259,20 +259,20 @@ __global__ void __launch_bounds__(1024) dtab_kernel(const uint64_t* __restrict__
     dtab_body(first, offsets, symbols, max_bw_arg, st, tab, old_lut, -1);
 }
 
-// decompress prep in one launch: CTAs 0/1 build the decode tables (T1/T3 | second
-// level + fallback LUT), CTA 2 scans the
-// chunk byte offsets and clears the hand-back flags and the chunk counter
-__global__ void __launch_bounds__(1024) decode_prep_kernel(
+// decompress prep in one launch of two clusters: cluster 0 scans the chunk
+// byte offsets and clears the hand-back flags and the chunk counter; CTAs 0/1
+// of cluster 1 build the decode tables (T1/T3 | second level + fallback LUT)
+__global__ void __cluster_dims__(kScanCtas, 1, 1) __launch_bounds__(1024) decode_prep_kernel(
     const uint64_t* __restrict__ first, const int64_t* __restrict__ offsets,
     const uint32_t* __restrict__ symbols, int max_bw_arg, DevStatus* st, uint32_t* __restrict__ tab,
     uint32_t* __restrict__ old_lut, const uint32_t* __restrict__ chunk_bits, uint64_t C,
     unsigned long long* __restrict__ byte_off, uint8_t* __restrict__ redo, unsigned int* counter) {
-    if (blockIdx.x < 2) {
-        dtab_body(first, offsets, symbols, max_bw_arg, st, tab, old_lut, (int)blockIdx.x);
-    } else {
-        for (uint64_t i = threadIdx.x; i < C; i += blockDim.x) redo[i] = 0;
-        if (threadIdx.x == 0) *counter = 0;
-        block_chunk_scan(chunk_bits, nullptr, C, byte_off, nullptr, ~0ull, false, 0, st);
+    if (blockIdx.x < kScanCtas) {   // cluster 0: chunk byte offsets, flag clears
+        for (uint64_t i = blockIdx.x * 1024ull + threadIdx.x; i < C; i += kScanCtas * 1024ull) redo[i] = 0;
+        if (blockIdx.x == 0 && threadIdx.x == 0) *counter = 0;
+        cluster_chunk_scan(blockIdx.x, chunk_bits, nullptr, C, byte_off, nullptr, ~0ull, false, 0, st);
+    } else if (blockIdx.x < kScanCtas + 2) {   // cluster 1: decode tables
+        dtab_body(first, offsets, symbols, max_bw_arg, st, tab, old_lut, (int)(blockIdx.x - kScanCtas));
     }
 }
 
@@ -772,7 +772,7 @@ int launch_decode_prep(sdqz_ctx* ctx, const uint64_t* first, const int64_t* offs
     uint32_t* tab = scratch_as<uint32_t>(ctx, S_DTAB, kTabWords, &rc);
     unsigned int* counter = scratch_as<unsigned int>(ctx, S_COUNTER, 4, &rc);
     if (!tab || !counter) return rc;
-    decode_prep_kernel<<<3, 1024, 0, ctx->stream>>>(first, offsets, symbols, max_bw, ctx->d_status, tab,
+    decode_prep_kernel<<<2 * kScanCtas, 1024, 0, ctx->stream>>>(first, offsets, symbols, max_bw, ctx->d_status, tab,
                                                     old_lut, chunk_bits, n_chunks, byte_off, redo,
                                                     counter);
     SDQZ_LAUNCHED_NAMED(ctx, "decode_prep_kernel");
