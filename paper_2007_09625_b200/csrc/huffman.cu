@@ -181,13 +181,13 @@ __global__ void __launch_bounds__(kBookThreads) codebook_kernel(
             // order; so the first 2*floor(m/2) of the m elements below t can be
             // merged in one round, exactly as the heap would.  Rounds continue
             // while they stay productive; the tail runs sequentially.
-            __shared__ uint32_t r_li, r_ii, r_ni, r_p, r_mL, r_mI;
-            __shared__ unsigned long long r_t;
+            // The frontier state (li, ii, ni) is block-uniform and kept in every
+            // thread's registers; t and the counts below t are computed by all
+            // threads (broadcast reads + barrier counts), so a round has no
+            // serial section.
             unsigned long long* fk = small ? (unsigned long long*)((uint32_t*)(smem + 2 * cap) + 3 * cap)
                                            : (unsigned long long*)gs.dep;
             uint32_t* fid = small ? (uint32_t*)(smem + 2 * cap) + 5 * cap : gs.jmp;
-            if (tid == 0) { r_li = 0; r_ii = 0; r_ni = 0; }
-            __syncthreads();
             auto lower = [](const unsigned long long* a, uint32_t lo, uint32_t hi,
                             unsigned long long key) {
                 while (lo < hi) {
@@ -196,31 +196,33 @@ __global__ void __launch_bounds__(kBookThreads) codebook_kernel(
                 }
                 return lo;
             };
-            while (true) {
-                const uint32_t li = r_li, ii = r_ii, ni = r_ni;
-                if (ni + 1 >= n) break;
-                if (tid == 0) {
-                    const unsigned long long LH = li < n ? keys[li] : NONE, IH = ii < ni ? iq[ii] : NONE;
-                    unsigned long long f0, f1;
-                    if (LH < IH) {
-                        f0 = LH;
-                        const unsigned long long L1 = li + 1 < n ? keys[li + 1] : NONE;
-                        f1 = L1 < IH ? L1 : IH;
-                    } else {
-                        f0 = IH;
-                        const unsigned long long I1 = ii + 1 < ni ? iq[ii + 1] : NONE;
-                        f1 = LH < I1 ? LH : I1;
-                    }
-                    const unsigned long long t =
-                        (((f0 >> 16) + (f1 >> 16)) << 16) | min(f0 & 0xFFFF, f1 & 0xFFFF);
-                    const uint32_t mL = lower(keys, li, n, t) - li, mI = lower(iq, ii, ni, t) - ii;
-                    r_t = t;
-                    r_mL = mL;
-                    r_mI = mI;
-                    r_p = (mL + mI) / 2;
+            uint32_t li = 0, ii = 0, ni = 0;
+            __shared__ uint32_t r_li, r_ii, r_ni;
+            while (ni + 1 < n) {
+                const unsigned long long LH = li < n ? keys[li] : NONE, IH = ii < ni ? iq[ii] : NONE;
+                unsigned long long f0, f1;
+                if (LH < IH) {
+                    f0 = LH;
+                    const unsigned long long L1 = li + 1 < n ? keys[li + 1] : NONE;
+                    f1 = L1 < IH ? L1 : IH;
+                } else {
+                    f0 = IH;
+                    const unsigned long long I1 = ii + 1 < ni ? iq[ii + 1] : NONE;
+                    f1 = LH < I1 ? LH : I1;
                 }
-                __syncthreads();
-                const uint32_t p = r_p, mL = r_mL, mI = r_mI;
+                const unsigned long long t =
+                    (((f0 >> 16) + (f1 >> 16)) << 16) | min(f0 & 0xFFFF, f1 & 0xFFFF);
+                // elements below t in each (sorted) queue
+                uint32_t mL = 0, mI = 0;
+                for (uint32_t j0 = 0; j0 < n - li; j0 += blockDim.x) {
+                    const uint32_t j = li + j0 + tid;
+                    mL += __syncthreads_count(j < n && keys[j] < t);
+                }
+                for (uint32_t j0 = 0; j0 < ni - ii; j0 += blockDim.x) {
+                    const uint32_t j = ii + j0 + tid;
+                    mI += __syncthreads_count(j < ni && iq[j] < t);
+                }
+                const uint32_t p = (mL + mI) / 2;
                 if (p < round_min) break;   // unproductive: finish sequentially
                 // merged position of every element below t
                 for (uint32_t j = tid; j < mL + mI; j += blockDim.x) {
@@ -238,6 +240,11 @@ __global__ void __launch_bounds__(kBookThreads) codebook_kernel(
                     }
                     if (pos < 2 * p) { fk[pos] = key; fid[pos] = id; }
                 }
+                uint32_t cL = mL, cI = mI;
+                if ((mL + mI) & 1) {   // the largest element below t waits for the next round
+                    const bool last_leaf = mL > 0 && (mI == 0 || keys[li + mL - 1] > iq[ii + mI - 1]);
+                    if (last_leaf) cL--; else cI--;
+                }
                 __syncthreads();
                 for (uint32_t j = tid; j < p; j += blockDim.x) {
                     const unsigned long long a = fk[2 * j], b = fk[2 * j + 1];
@@ -245,19 +252,13 @@ __global__ void __launch_bounds__(kBookThreads) codebook_kernel(
                     parent[fid[2 * j]] = n + ni + j;
                     parent[fid[2 * j + 1]] = n + ni + j;
                 }
-                if (tid == 0) {
-                    uint32_t cL = mL, cI = mI;
-                    if ((mL + mI) & 1) {   // the largest element below t waits for the next round
-                        const bool last_leaf =
-                            mL > 0 && (mI == 0 || keys[li + mL - 1] > iq[ii + mI - 1]);
-                        if (last_leaf) cL--; else cI--;
-                    }
-                    r_li = li + cL;
-                    r_ii = ii + cI;
-                    r_ni = ni + p;
-                }
+                li += cL;
+                ii += cI;
+                ni += p;
                 __syncthreads();
             }
+            if (tid == 0) { r_li = li; r_ii = ii; r_ni = ni; }
+            __syncthreads();
             BOOK_T(3);
             // -- sequential tail (thread 0): two-queue merge from (li, ii, ni)
             if (tid == 0) {

@@ -60,6 +60,15 @@ constexpr uint32_t kLongInvalid = 0x81;    // len 1 + flag (sym|len form)
 // ---------------------------------------------------------------------------
 // decode tables: one CTA
 // ---------------------------------------------------------------------------
+// s_one is stored swizzled: the greedy decode reads window (i << o) mod 2^12,
+// whose low o bits are zero for every lane, so a plain layout puts a warp's
+// reads in one bank for o >= 5; XOR-folding the high bits into the bank bits
+// spreads them (conflict-free up to o = 7).
+__device__ __forceinline__ uint32_t swz12(uint32_t w) {
+    const uint32_t h = w >> 5;
+    return w ^ ((h ^ (h >> 5)) & 31u);
+}
+
 // part 0: T1/T3 tables; part 1: second-level table + the fallback LUT;
 // part -1: everything (both parts compute the shared preliminaries)
 __device__ __forceinline__ void dtab_body(const uint64_t* __restrict__ first,
@@ -168,7 +177,7 @@ __device__ __forceinline__ void dtab_body(const uint64_t* __restrict__ first,
                 break;
             }
         }
-        s_one[i] = e;
+        s_one[swz12(i)] = e;
     }
     __syncthreads();
     // the sequential fallback decoder's table (huffman.cu lut_kernel format)
@@ -177,7 +186,7 @@ __device__ __forceinline__ void dtab_body(const uint64_t* __restrict__ first,
         for (uint32_t i = threadIdx.x; i < (1u << kLutBits); i += blockDim.x) {
             uint32_t e = 0;
             if (i < (1u << lb)) {
-                const uint32_t one = s_one[(i << (kL1 - lb)) & (kL1Size - 1)];
+                const uint32_t one = s_one[swz12((i << (kL1 - lb)) & (kL1Size - 1))];
                 if (one && (int)(one & 63u) <= lb) {
                     e = (one >> 16) | ((one & 63u) << 16);
                 } else if (lb == mx) {
@@ -200,7 +209,7 @@ __device__ __forceinline__ void dtab_body(const uint64_t* __restrict__ first,
     for (uint32_t i = threadIdx.x; p0 && i < kL1Size; i += blockDim.x) {
         uint32_t o = 0, m = 0, mask = 0, zeros = 0, sym[3] = {0, 0, 0}, cum[3] = {0, 0, 0};
         while (o < (uint32_t)kL1) {
-            const uint32_t one = s_one[(i << o) & (kL1Size - 1)];
+            const uint32_t one = s_one[swz12((i << o) & (kL1Size - 1))];
             const uint32_t b = one & 63u;
             if (!b || b > kL1 - o) break;
             const uint32_t sv = one >> 16;
