@@ -44,16 +44,25 @@ __global__ void __launch_bounds__(256) describe_kernel(const T* __restrict__ in,
     for (uint64_t i = tid; i < head; i += stride) acc(in[i], mn, mx, bad);
     const V* vin = reinterpret_cast<const V*>(in + head);
     uint64_t nv = (n - head) / W;
-#pragma unroll 4
-    for (uint64_t i = tid; i < nv; i += stride) {
-        V v = __ldg(vin + i);
+    auto accv = [&](const V& v) {
         if constexpr (W == 4) {
             acc(v.x, mn, mx, bad); acc(v.y, mn, mx, bad);
             acc(v.z, mn, mx, bad); acc(v.w, mn, mx, bad);
         } else {
             acc(v.x, mn, mx, bad); acc(v.y, mn, mx, bad);
         }
+    };
+    // full batches of kBatch unconditional loads in flight per thread
+    constexpr int kBatch = 8;
+    uint64_t i = tid;
+    for (; i + (kBatch - 1) * stride < nv; i += kBatch * stride) {
+        V v[kBatch];
+#pragma unroll
+        for (int k = 0; k < kBatch; k++) v[k] = __ldg(vin + i + k * stride);
+#pragma unroll
+        for (int k = 0; k < kBatch; k++) accv(v[k]);
     }
+    for (; i < nv; i += stride) accv(__ldg(vin + i));
     for (uint64_t i = head + nv * W + tid; i < n; i += stride) acc(in[i], mn, mx, bad);
 
 #pragma unroll

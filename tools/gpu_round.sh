@@ -9,7 +9,7 @@ timeout 600 python bench.py --steps 20 --warmup 5 > $OUT/bench.json 2> $OUT/benc
 for c in ${CONFIGS:-cesm nyx hacc}; do
   timeout 600 python bench.py --steps 10 --warmup 3 --config $c --no-cpu-baseline > $OUT/bench_$c.json 2> $OUT/bench_$c.err; echo "bench_$c=$?"
 done
-timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 60 --csv --log-file $OUT/launches.csv python tools/profile_step.py hurricane 2 > /dev/null 2>&1
+timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -k regex:"describe|dq|codebook|chunk|inflate|rq|outlier|init_status|resolve|decode_prep|lut" -c 60 --csv --log-file $OUT/launches.csv python tools/profile_step.py hurricane 2 > /dev/null 2>&1
 echo "ncu_launch=$?"
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:"${NCU_KERNELS:-inflate_fast|dq3d_tma|rq3d_block|chunk_pack32|chunk_stats|describe|codebook}" -s 8 -c 8 -o $OUT/prof_full python tools/profile_step.py hurricane 2 > /dev/null 2>&1
 echo "ncu_full=$?"
