@@ -975,10 +975,18 @@ __global__ void __launch_bounds__(256, 3) chunk_pack32_kernel(DeflateArgs a) {
                 }
             }
             uint32_t ent[kRun], bits = 0;
+            if (cnt == kRun) {
 #pragma unroll
-            for (int k = 0; k < kRun; k++) {
-                ent[k] = (uint32_t)k < cnt ? lookup(code[k]) : 0u;
-                bits += ent[k] & 31u;
+                for (int k = 0; k < kRun; k++) {
+                    ent[k] = lookup(code[k]);
+                    bits += ent[k] & 31u;
+                }
+            } else {
+#pragma unroll
+                for (int k = 0; k < kRun; k++) {
+                    ent[k] = (uint32_t)k < cnt ? lookup(code[k]) : 0u;
+                    bits += ent[k] & 31u;
+                }
             }
             int total_l;
             const uint32_t off = (uint32_t)warp_excl_scan((int)bits, &total_l) + carry;
@@ -987,29 +995,22 @@ __global__ void __launch_bounds__(256, 3) chunk_pack32_kernel(DeflateArgs a) {
             if (lane == 0) buf[0] = carry_word;
             for (uint32_t j = lane + 1; j < (total + 31) >> 5; j += 32) buf[j] = 0;
             __syncwarp();
-            if (bits) {
-                uint32_t wi = off >> 5, nacc = off & 31;
-                uint32_t hi = 0, lo = 0;             // pending window, left-aligned
-                const uint32_t wfirst = wi;
-                uint32_t first_word = 0;
-                bool have_first = false;
+            // every codeword is OR-ed into the (at most two) words it touches:
+            // no per-code branches or selects, one or two shared reductions
+            {
+                const uint32_t bufs = smem_u32(buf);
+                uint32_t p = off;
 #pragma unroll
                 for (int k = 0; k < kRun; k++) {
-                    const uint32_t al = ent[k] & ~31u;    // codeword, left-aligned
-                    hi |= al >> nacc;
-                    lo |= __funnelshift_r(0u, al, nacc);
-                    nacc += ent[k] & 31u;
-                    const bool emit = nacc >= 32;
-                    if (emit && have_first) buf[wi] = hi;
-                    first_word = (emit && !have_first) ? hi : first_word;
-                    have_first |= emit;
-                    wi += emit ? 1u : 0u;
-                    hi = emit ? lo : hi;
-                    lo = emit ? 0u : lo;
-                    nacc -= emit ? 32u : 0u;
+                    const uint32_t al = ent[k] & ~31u, w = ent[k] & 31u;
+                    const uint32_t sh = p & 31u, addr = bufs + ((p >> 5) << 2);
+                    // (w == 0 past a partial run: OR-ing 0 is harmless)
+                    asm volatile("red.shared.or.b32 [%0], %1;" ::"r"(addr), "r"(al >> sh) : "memory");
+                    asm volatile("{\n\t.reg .pred p;\n\tsetp.gt.u32 p, %2, 32;\n\t"
+                                 "@p red.shared.or.b32 [%0], %1;\n\t}"
+                                 ::"r"(addr + 4), "r"(__funnelshift_r(0u, al, sh)), "r"(sh + w) : "memory");
+                    p += w;
                 }
-                if (have_first) atomicOr(&buf[wfirst], first_word);
-                if (nacc) atomicOr(&buf[wi], hi);
             }
             __syncwarp();
             const uint32_t full = total >> 5;
