@@ -993,6 +993,7 @@ __global__ void __launch_bounds__(256, 3) chunk_pack32_kernel(DeflateArgs a) {
             const uint32_t total = carry + (uint32_t)total_l;
             // the previous round's trailing partial word seeds word 0
             if (lane == 0) buf[0] = carry_word;
+#pragma unroll 1
             for (uint32_t j = lane + 1; j < (total + 31) >> 5; j += 32) buf[j] = 0;
             __syncwarp();
             // every codeword is OR-ed into the (at most two) words it touches:
@@ -1004,11 +1005,13 @@ __global__ void __launch_bounds__(256, 3) chunk_pack32_kernel(DeflateArgs a) {
                 for (int k = 0; k < kRun; k++) {
                     const uint32_t al = ent[k] & ~31u, w = ent[k] & 31u;
                     const uint32_t sh = p & 31u, addr = bufs + ((p >> 5) << 2);
-                    // (w == 0 past a partial run: OR-ing 0 is harmless)
+                    (void)w;
+                    // the spill into the next word is 0 unless sh + w > 32, and
+                    // w == 0 past a partial run: OR-ing 0 is harmless, so both
+                    // reductions are unconditional (no branches)
                     asm volatile("red.shared.or.b32 [%0], %1;" ::"r"(addr), "r"(al >> sh) : "memory");
-                    asm volatile("{\n\t.reg .pred p;\n\tsetp.gt.u32 p, %2, 32;\n\t"
-                                 "@p red.shared.or.b32 [%0], %1;\n\t}"
-                                 ::"r"(addr + 4), "r"(__funnelshift_r(0u, al, sh)), "r"(sh + w) : "memory");
+                    asm volatile("red.shared.or.b32 [%0], %1;" ::"r"(addr + 4), "r"(__funnelshift_r(0u, al, sh))
+                                 : "memory");
                     p += w;
                 }
             }
