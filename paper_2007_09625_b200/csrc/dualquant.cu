@@ -446,16 +446,15 @@ __global__ void __launch_bounds__(kTmaWarps * 32, 2) dq3d_tma_kernel(
     uint32_t phase = 0;    // bit q: parity of stage q
     uint32_t qc = 0;       // stage of the unit being computed
     bool bad = false;
-    for (uint32_t task = first; task < ntask; task += stride) {
+    // tasks past the first wave are claimed dynamically (the status block's
+    // zeroed scratch word), so warps on busier SMs take fewer of them
+    unsigned long long* const ctr = &st->pad[2];
+    uint32_t nt = 0;
+    for (uint32_t task = first; task < ntask; task = nt) {
         const uint32_t bx4 = cbx, by = cby, bz = cbz;
-        const uint32_t nt = task + stride;
-        const bool has_next = nt < ntask;
-        if (has_next) {
-            cbx = nt % nbx4;
-            const uint32_t t2 = nt / nbx4;
-            cby = t2 % nby;
-            cbz = t2 / nby;
-        }
+        uint32_t claim = 0;
+        if (lane == 0) claim = (uint32_t)atomicAdd(ctr, 1ull);   // consumed at pair 2
+        bool has_next = false;
         const uint64_t x = (uint64_t)bx4 * 32 + lane, y0 = (uint64_t)by * 8, z0 = (uint64_t)bz * 8;
         const bool xin = x < X;
         const int ny = (int)umin(8, Y - y0), nz = (int)umin(8, Z - z0);
@@ -468,6 +467,16 @@ __global__ void __launch_bounds__(kTmaWarps * 32, 2) dq3d_tma_kernel(
         bool mark = false;
 #pragma unroll 1
         for (uint32_t pr = 0; pr < 4; pr++) {
+            if (pr == 2) {   // the next task: its first two pairs load during pairs 2, 3
+                nt = stride + __shfl_sync(kFull, claim, 0);
+                has_next = nt < ntask;
+                if (has_next) {
+                    cbx = nt % nbx4;
+                    const uint32_t t2 = nt / nbx4;
+                    cby = t2 % nby;
+                    cbz = t2 / nby;
+                }
+            }
             if (lane == 0) {
                 const uint32_t qn = qc == 0 ? 2 : qc - 1;   // (qc + 2) % 3
                 if (pr < 2) issue(qn, bx4, by, bz * 8 + 2 * (pr + 2));
