@@ -211,6 +211,7 @@ def algorithmic_bytes(kernel: str, n: int, k: int, c: int, p: int) -> int | None
         "rq3d_block_kernel": 2 * n + 4 * n + 8 * k,        # codes read, field written, outlier values
         "rq2d_kernel": 2 * n + 4 * n + 8 * k,
         "rq1d_kernel": 2 * n + 4 * n + 8 * k,
+        "rq1d_vec_kernel": 2 * n + 4 * n + 8 * k,
         "outlier_scatter_kernel": 16 * k + 8 * k + 2 * k,
     }
     for key, v in table.items():

@@ -691,6 +691,152 @@ __global__ void __launch_bounds__(kThreads, 2) dq1d_kernel(const void* __restric
 }
 
 // ----------------------------------------------------------------------------
+// 1D, block 32, fp32, whole 1024-point tasks.  Lane l holds points 4l..4l+3 of
+// each of the task's 8 rows of 128 (float4 loads, 8 in flight per lane; one
+// uint2 store of 4 codes), a block spans 8 lanes.  Prequantization is the
+// fixed-point FMA of dq3d_tma_kernel (bias kFixK cancels in the differences;
+// the left neighbour of a block's first point is the bias itself, i.e. the
+// zero pad of dualquant.py:81-86), with the same exact tie-neighbourhood
+// redo.  A task holding any |v / 2eb| >= 2^27 - 2048 (or a non-finite value)
+// is computed in fp64 with exact division instead (dualquant.py:76-77, 1D
+// predictor d[a-1]).  Histogram: lane-private hot bins + CTA bins (one shared
+// reduction per point).
+// ----------------------------------------------------------------------------
+constexpr uint32_t kVecTask = 1024;
+
+template <bool SH>
+__device__ __forceinline__ void dq1d_count(uint32_t c, uint32_t wbase, uint32_t hb, uint32_t shist_s,
+                                           HistCtx& h) {
+    if (SH) {
+        const bool hot = c - wbase < kHot;
+        const uint32_t addr = c * (hot ? 128u : 4u) + (hot ? hb : shist_s);
+        asm volatile("red.shared.add.u32 [%0], 1;" ::"r"(addr) : "memory");
+    } else {
+        hot_add(hb, c, wbase, h, 1);
+    }
+}
+
+// exact fp64 task (dualquant.py:76-77, predictor d[a-1]), reloading its values
+template <bool SH>
+__device__ __noinline__ void dq1d_task_f64(const float4* __restrict__ src, uint2* __restrict__ dst,
+                                           uint32_t lane, double two_eb, int r, uint32_t wbase,
+                                           uint32_t hb, uint32_t shist_s, HistCtx h, bool& bad) {
+    const bool lead = (lane & 7) == 0;
+    for (int j = 0; j < 8; j++) {
+        const float4 w = __ldg(src + 32 * j);
+        const float e[4] = {w.x, w.y, w.z, w.w};
+        double d[4];
+#pragma unroll
+        for (int c = 0; c < 4; c++) {
+            bad |= !isfinite(e[c]);
+            d[c] = prequant((double)e[c], two_eb);
+        }
+        double left = __shfl_up_sync(kFull, d[3], 1);
+        if (lead) left = 0.0;
+        uint32_t cc[4];
+#pragma unroll
+        for (int c = 0; c < 4; c++) {
+            cc[c] = code_of_f64(__dsub_rn(d[c], c ? d[c - 1] : left), r);
+            dq1d_count<SH>(cc[c], wbase, hb, shist_s, h);
+        }
+        dst[32 * j] = make_uint2(cc[0] | (cc[1] << 16), cc[2] | (cc[3] << 16));
+    }
+}
+
+template <bool SH>
+__global__ void __launch_bounds__(kThreads, 2) dq1d_vec_kernel(const float* __restrict__ in, uint64_t ntask,
+                                                               uint32_t cap, DevStatus* st,
+                                                               uint16_t* __restrict__ codes,
+                                                               unsigned long long* ghist) {
+    extern __shared__ __align__(16) uint32_t dsm1[];
+    uint32_t* hot = dsm1;   // [warp][kHot][32]
+    for (uint32_t i = threadIdx.x; i < kWarpsPerCta * kHot * 32; i += blockDim.x) hot[i] = 0;
+    HistCtx h;
+    hist_init(h, hot + kWarpsPerCta * kHot * 32, ghist, cap);   // (syncs)
+    const double two_eb = st->two_eb;
+    const double rcp = __drcp_rn(two_eb);
+    const uint32_t hi_lo = (uint32_t)__double2hiint(kFixC - kFixBound) + 1u;
+    const uint32_t hi_span = (uint32_t)__double2hiint(kFixC + kFixBound) - hi_lo;
+    const int r = (int)(cap >> 1);
+    const uint32_t wbase = cap >= 2 * kHot ? (uint32_t)r - kHot / 2 : 0u;
+    const uint32_t lane = lane_id(), wid = threadIdx.x >> 5;
+    const uint32_t hb = smem_u32(hot + wid * kHot * 32 + lane) - wbase * 128u;
+    const uint32_t shist_s = SH ? smem_u32(h.shist) : 0u;
+    const bool lead = (lane & 7) == 0;   // first lane of a 32-point block
+    bool bad = false;
+    for (uint64_t task = blockIdx.x * (uint64_t)kWarpsPerCta + wid; task < ntask;
+         task += (uint64_t)gridDim.x * kWarpsPerCta) {
+        const float4* src = reinterpret_cast<const float4*>(in + task * kVecTask) + lane;
+        uint2* dst = reinterpret_cast<uint2*>(codes + task * kVecTask) + lane;
+        float4 v[8];
+#pragma unroll
+        for (int j = 0; j < 8; j++) v[j] = __ldcs(src + 32 * j);
+        int q[8][4];
+        bool amb = false, mark = false;
+#pragma unroll
+        for (int j = 0; j < 8; j++) {
+            const float e[4] = {v[j].x, v[j].y, v[j].z, v[j].w};
+#pragma unroll
+            for (int c = 0; c < 4; c++) {
+                const double R = __fma_rn((double)e[c], rcp, kFixC);
+                const uint32_t lo = (uint32_t)__double2loint(R), hi = (uint32_t)__double2hiint(R);
+                amb |= (lo & 0x3FFFFCu) == 0u;
+                mark |= (hi - hi_lo) >= hi_span;
+                q[j][c] = (int)__funnelshift_r(lo, hi, 22);
+            }
+        }
+        if (__any_sync(kFull, mark)) {   // rare: huge magnitudes or non-finite values
+            dq1d_task_f64<SH>(src, dst, lane, two_eb, r, wbase, hb, shist_s, h, bad);
+            continue;
+        }
+        if (__any_sync(kFull, amb)) {   // rare: exact division near a rounding tie
+#pragma unroll 1
+            for (int j = 0; j < 8; j++) {
+                const float4 w = __ldg(src + 32 * j);
+                const float e[4] = {w.x, w.y, w.z, w.w};
+#pragma unroll
+                for (int c = 0; c < 4; c++) {
+                    const double R = __fma_rn((double)e[c], rcp, kFixC);
+                    if (((uint32_t)__double2loint(R) & 0x3FFFFCu) == 0u) {
+                        const int m = (int)floor(__dadd_rn(fabs(__ddiv_rn((double)e[c], two_eb)), 0.5));
+                        const int qq = (e[c] < 0.f ? -m : m) + kFixK;
+#pragma unroll
+                        for (int jj = 0; jj < 8; jj++)
+                            if (jj == j) q[jj][c] = qq;
+                    }
+                }
+            }
+        }
+#pragma unroll
+        for (int j = 0; j < 8; j++) {
+            int left = __shfl_up_sync(kFull, q[j][3], 1);
+            if (lead) left = kFixK;
+            uint32_t cc[4];
+#pragma unroll
+            for (int c = 0; c < 4; c++) {
+                const uint32_t uu = (uint32_t)(q[j][c] - (c ? q[j][c - 1] : left) + r);
+                cc[c] = (uu - 1u) < (uint32_t)(2 * r - 1) ? uu : 0u;   // -r < delta < r
+                dq1d_count<SH>(cc[c], wbase, hb, shist_s, h);
+            }
+            dst[32 * j] = make_uint2(cc[0] | (cc[1] << 16), cc[2] | (cc[3] << 16));
+        }
+    }
+    if (__any_sync(kFull, bad) && lane == 0) atomicOr(&st->flags, (unsigned long long)F_NONFINITE);
+    __syncthreads();
+    for (uint32_t j = wid; j < kHot; j += kWarpsPerCta) {
+        uint32_t s = 0;
+#pragma unroll
+        for (int w = 0; w < kWarpsPerCta; w++) s += hot[(w * kHot + j) * 32 + lane];
+        s = __reduce_add_sync(kFull, s);
+        if (lane == 0 && s && wbase + j < cap) {
+            if (h.shist) atomicAdd(&h.shist[wbase + j], s);
+            else if (h.ghist) atomicAdd(&h.ghist[wbase + j], (unsigned long long)s);
+        }
+    }
+    hist_finish(h);
+}
+
+// ----------------------------------------------------------------------------
 // Generic block shapes: one thread per point, fp64 reference order.
 // ----------------------------------------------------------------------------
 struct Geo {
@@ -817,6 +963,35 @@ int launch_kind(sdqz_ctx* ctx, const void* d_in, int ndims, const uint64_t dims[
             return SDQZ_OK;
         }
     }
+    // vectorised 1D path: whole 1024-point tasks, then the tail by dq1d_kernel
+    if (KIND == 0 && ndims == 1 && is_fast_shape(ndims, block) && dims[0] >= kVecTask &&
+        ((uintptr_t)d_in & 15) == 0 && ((uintptr_t)d_codes & 7) == 0 && !env_disabled("SDQZ_NO_VEC1D")) {
+        const uint64_t nt = dims[0] / kVecTask;
+        const size_t vsm = kWarpsPerCta * kHot * 32 * 4 + smem;
+        static bool vattr = false;
+        if (!vattr) {
+            const int mx = kWarpsPerCta * kHot * 32 * 4 + kSmemHistMax * 4;
+            cudaFuncSetAttribute(dq1d_vec_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
+            cudaFuncSetAttribute(dq1d_vec_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
+            vattr = true;
+        }
+        uint64_t grid = ceil_div(nt, kWarpsPerCta);
+        if (grid > (uint64_t)ctx->num_sms * 2) grid = (uint64_t)ctx->num_sms * 2;
+        if (smem)
+            dq1d_vec_kernel<true><<<(unsigned)grid, kThreads, vsm, ctx->stream>>>(
+                (const float*)d_in, nt, cap, ctx->d_status, d_codes, d_hist);
+        else
+            dq1d_vec_kernel<false><<<(unsigned)grid, kThreads, vsm, ctx->stream>>>(
+                (const float*)d_in, nt, cap, ctx->d_status, d_codes, d_hist);
+        SDQZ_LAUNCHED_NAMED(ctx, "dq1d_vec_kernel");
+        const uint64_t off = nt * kVecTask;
+        if (off < dims[0]) {
+            dq1d_kernel<0><<<1, kThreads, smem, ctx->stream>>>((const float*)d_in + off, dims[0] - off,
+                                                               cap, ctx->d_status, d_codes + off, d_hist);
+            SDQZ_LAUNCHED_NAMED(ctx, "dq1d_kernel");
+        }
+        return SDQZ_OK;
+    }
     if (is_fast_shape(ndims, block)) {
         uint64_t ntask;
         if (ndims == 3) ntask = ceil_div(ceil_div(dims[2], 8), 4) * ceil_div(dims[1], 8) * ceil_div(dims[0], 8);
@@ -848,7 +1023,8 @@ int launch_kind(sdqz_ctx* ctx, const void* d_in, int ndims, const uint64_t dims[
         dq_generic_kernel<KIND><<<(unsigned)grid, kThreads, smem, ctx->stream>>>(
             d_in, g, n, cap, ctx->d_status, d_codes, d_hist);
     }
-    SDQZ_LAUNCHED_NAMED(ctx, "dq_generic_kernel");
+    SDQZ_LAUNCHED_NAMED(ctx, !is_fast_shape(ndims, block) ? "dq_generic_kernel"
+                             : ndims == 3 ? "dq3d_kernel" : ndims == 2 ? "dq2d_kernel" : "dq1d_kernel");
     return SDQZ_OK;
 }
 

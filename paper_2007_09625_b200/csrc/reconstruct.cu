@@ -701,6 +701,110 @@ __global__ void __launch_bounds__(kThreads) rq1d_kernel(const uint16_t* __restri
     }
 }
 
+// 1D block 32, whole 1024-point tasks: lane l holds points 4l..4l+3 of each of
+// the task's 8 rows of 128 (uint2 code loads, all 8 in flight; float4
+// stores), a block spans 8 lanes.  Per lane: T = sum of the residuals after
+// its last outlier (reset to the outlier's value v there).  Inclusive scan P
+// of T over the block's lanes; a lane's carry-in is P(l-1) - P(s-1), s the
+// last lane left of it (in the block) holding an outlier -- the reference's
+// per-outlier box correction (dualquant.py:218-226) as a reset scan.  The
+// scan runs in int32: partial sums wrap, but the carry and every final value
+// are exact whenever |v| < 2^30 (then |final| < 2^30 + 32 r < 2^31); a task
+// with a larger outlier value takes the int64 instantiation.
+template <typename V, int OUTK>
+__device__ __forceinline__ void rq1d_vec_row(uint2 cw, const unsigned long long* __restrict__ dense,
+                                             uint64_t i0, int r, uint32_t lane, double two_eb,
+                                             void* __restrict__ out, bool store) {
+    const uint32_t c[4] = {cw.x & 0xFFFFu, cw.x >> 16, cw.y & 0xFFFFu, cw.y >> 16};
+    V fin[4];
+    V t = 0;
+    bool f = false;
+#pragma unroll
+    for (int k = 0; k < 4; k++) {
+        if (c[k] == 0) {
+            t = (V)__longlong_as_double((long long)dense[i0 + k]);
+            f = true;
+        } else {
+            t += (V)((int)c[k] - r);
+        }
+        fin[k] = t;   // local value (carry added below)
+    }
+    // inclusive scan of t over the block's 8 lanes
+    const uint32_t sl = lane & 7;
+    V P = t;
+#pragma unroll
+    for (int o = 1; o < 8; o <<= 1) {
+        const V y = __shfl_up_sync(kFull, P, o);
+        if (sl >= (uint32_t)o) P += y;
+    }
+    const V E = P - t;   // exclusive
+    const uint32_t m = __ballot_sync(kFull, f) & (((1u << sl) - 1u) << (lane & ~7u));
+    const int s = m ? 31 - __clz(m) : (int)(lane & ~7u);
+    const V Es = __shfl_sync(kFull, E, s);
+    const V carry = E - Es;
+    bool hit = false;
+#pragma unroll
+    for (int k = 0; k < 4; k++) {
+        hit |= c[k] == 0;
+        if (!hit) fin[k] += carry;
+    }
+    if (!store) return;
+    if (OUTK == 0) {
+        float4 o4;
+        o4.x = __double2float_rn(__dmul_rn((double)fin[0], two_eb));
+        o4.y = __double2float_rn(__dmul_rn((double)fin[1], two_eb));
+        o4.z = __double2float_rn(__dmul_rn((double)fin[2], two_eb));
+        o4.w = __double2float_rn(__dmul_rn((double)fin[3], two_eb));
+        __stcs(reinterpret_cast<float4*>((float*)out + i0), o4);
+    } else {
+        double* o = (double*)out + i0;
+#pragma unroll
+        for (int k = 0; k < 4; k++) o[k] = __dmul_rn((double)fin[k], two_eb);
+    }
+}
+
+template <int OUTK>
+__global__ void __launch_bounds__(kThreads) rq1d_vec_kernel(const uint16_t* __restrict__ codes,
+                                                            const unsigned long long* __restrict__ dense,
+                                                            const uint8_t* __restrict__ blockflag,
+                                                            int any_slow, uint64_t ntask, uint32_t cap,
+                                                            double two_eb, void* __restrict__ out) {
+    const int r = (int)(cap >> 1);
+    const uint32_t lane = lane_id();
+    for (uint64_t task = blockIdx.x * (uint64_t)kWarpsPerCta + (threadIdx.x >> 5); task < ntask;
+         task += (uint64_t)gridDim.x * kWarpsPerCta) {
+        const uint64_t t0 = task * 1024;
+        const uint2* src = reinterpret_cast<const uint2*>(codes + t0) + lane;
+        uint2 cw[8];
+#pragma unroll
+        for (int j = 0; j < 8; j++) cw[j] = __ldcs(src + 32 * j);
+        // an outlier value at or beyond 2^30 in magnitude sends the task to int64
+        bool big = false;
+#pragma unroll
+        for (int j = 0; j < 8; j++) {
+            const uint32_t z = __vcmpeq2(cw[j].x, 0u) | __vcmpeq2(cw[j].y, 0u);
+            if (z) {
+#pragma unroll
+                for (int k = 0; k < 4; k++) {
+                    const uint32_t cc = k < 2 ? (cw[j].x >> (16 * k)) & 0xFFFFu : (cw[j].y >> (16 * (k - 2))) & 0xFFFFu;
+                    if (cc == 0) {
+                        const double v = __longlong_as_double((long long)dense[t0 + j * 128 + lane * 4 + k]);
+                        big |= !(fabs(v) < 1073741824.0);
+                    }
+                }
+            }
+        }
+        const bool wide = __any_sync(kFull, big);
+#pragma unroll
+        for (int j = 0; j < 8; j++) {
+            const uint64_t i0 = t0 + j * 128 + lane * 4;
+            const bool store = !(any_slow && blockflag[i0 >> 5]);
+            if (wide) rq1d_vec_row<long long, OUTK>(cw[j], dense, i0, r, lane, two_eb, out, store);
+            else rq1d_vec_row<int, OUTK>(cw[j], dense, i0, r, lane, two_eb, out, store);
+        }
+    }
+}
+
 // Reference-order fp64 reconstruction, one thread per block (generic shapes
 // and flagged blocks).  `work` is an fp64 scratch array indexed like the field.
 template <int OUTK>
@@ -849,6 +953,13 @@ int launch_reconstruct(sdqz_ctx* ctx, const uint16_t* codes, const uint64_t* den
         const uint64_t nblk3 = ndims == 3 ? ceil_div(dims[0], 8) * ceil_div(dims[1], 8) * ceil_div(dims[2], 8) : 1;
         uint64_t bgrid = ceil_div(nblk3, 64);
         if (bgrid > (uint64_t)ctx->num_sms * 16) bgrid = (uint64_t)ctx->num_sms * 16;
+        // vectorised 1D: whole 1024-point tasks (8-byte code rows, 16-byte output rows)
+        const bool vec1d = ndims == 1 && dims[0] >= 1024 && ((uintptr_t)codes & 7) == 0 &&
+                           ((uintptr_t)out & 15) == 0 && !env_disabled("SDQZ_NO_VEC1D");
+        const uint64_t nt1 = ndims == 1 ? dims[0] / 1024 : 0, off1 = nt1 * 1024;
+        uint64_t vgrid = ceil_div(nt1, kWarpsPerCta);
+        if (vgrid > (uint64_t)ctx->num_sms * 8) vgrid = (uint64_t)ctx->num_sms * 8;
+        if (vgrid < 1) vgrid = 1;
 #define RQ_LAUNCH(K)                                                                                 \
         if (ndims == 3 && !env_disabled("SDQZ_RQ_WARP"))                                             \
             rq3d_block_kernel<K><<<(unsigned)bgrid, 64, 0, ctx->stream>>>(codes, dn, const_cast<uint8_t*>(blockflag), slow, \
@@ -862,14 +973,21 @@ int launch_reconstruct(sdqz_ctx* ctx, const uint16_t* codes, const uint64_t* den
         else if (ndims == 2)                                                                         \
             rq2d_kernel<K><<<(unsigned)grid, kThreads, 0, ctx->stream>>>(codes, dn, blockflag, slow,   \
                                                                         dims[0], dims[1], cap, two_eb, out); \
-        else                                                                                         \
+        else if (vec1d) {                                                                            \
+            rq1d_vec_kernel<K><<<(unsigned)vgrid, kThreads, 0, ctx->stream>>>(codes, dn, blockflag, slow, \
+                                                                             nt1, cap, two_eb, out); \
+            if (off1 < dims[0])                                                                      \
+                rq1d_kernel<K><<<1, kThreads, 0, ctx->stream>>>(codes + off1, dn + off1,            \
+                    blockflag + off1 / 32, slow, dims[0] - off1, cap, two_eb,                        \
+                    (char*)out + off1 * (K == 0 ? 4 : 8));                                           \
+        } else                                                                                       \
             rq1d_kernel<K><<<(unsigned)grid, kThreads, 0, ctx->stream>>>(codes, dn, blockflag, slow,   \
                                                                         dims[0], cap, two_eb, out);
         if (out_kind == 0) { RQ_LAUNCH(0) } else { RQ_LAUNCH(1) }
 #undef RQ_LAUNCH
         if (ndims == 3) SDQZ_LAUNCHED_NAMED(ctx, "rq3d_block_kernel");
         else if (ndims == 2) SDQZ_LAUNCHED_NAMED(ctx, "rq2d_kernel");
-        else SDQZ_LAUNCHED_NAMED(ctx, "rq1d_kernel");
+        else SDQZ_LAUNCHED_NAMED(ctx, vec1d ? "rq1d_vec_kernel" : "rq1d_kernel");
         if (!any_slow) return SDQZ_OK;
     }
     double* work = scratch_as<double>(ctx, S_WORK, n, &rc);

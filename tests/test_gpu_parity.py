@@ -364,3 +364,54 @@ class TestDualquant3DPaths:
         f[4, 4, 17] = np.nan
         with pytest.raises(S.SdqzError, match="NaN"):
             S.compress(f, eb=0.1, mode="abs")
+
+
+class TestVec1DPaths:
+    """The vectorised 1D kernels (dq1d_vec / rq1d_vec: whole 1024-point tasks,
+    tail by the scalar kernels): tails, caps, the fp64 task redo, rounding
+    ties, outlier values beyond the int32 reset-scan range."""
+
+    check = staticmethod(TestDualquant3DPaths.check)
+
+    @pytest.mark.parametrize("n", [1024, 1025, 2047, 5000, 100_003, 3_000_000])
+    def test_lengths(self, n):
+        f = S.generate_field("smooth", (n,), seed=3).astype(np.float32)
+        self.check(f, eb=1e-4, mode="valrel")
+
+    @pytest.mark.parametrize("cap", [4, 16, 32, 1024, 65536])
+    def test_caps(self, cap):
+        rng = np.random.default_rng(cap)
+        f = np.cumsum(rng.normal(0, 1, 9000)).astype(np.float32)
+        self.check(f, eb=0.05, mode="abs", cap=cap)
+
+    def test_big_magnitudes_redo(self):
+        rng = np.random.default_rng(12)
+        f = rng.normal(0, 1.0, 8192).astype(np.float32)
+        f[1500:1700] *= 3e8                  # fp64 task redo in dq, int64 rows in rq
+        f[5000] = 2.0 ** 27 * 2e-3           # right at the int32 bound
+        f[6000:6040] = 2.0 ** 31 * 2e-3      # outlier values beyond 2^30 units
+        self.check(f, eb=1e-3, mode="abs")
+
+    def test_outlier_dense(self):
+        rng = np.random.default_rng(13)
+        f = rng.normal(0, 50.0, 20000).astype(np.float32)    # most points are outliers
+        self.check(f, eb=0.01, mode="abs", cap=16)
+
+    def test_rounding_ties(self):
+        rng = np.random.default_rng(6)
+        k = rng.integers(-4000, 4000, 4096).astype(np.float64)
+        f = ((k + 0.5) * 0.25).astype(np.float32)
+        f[::2] = np.nextafter(f[::2], np.float32(np.inf))
+        self.check(f, eb=0.125, mode="abs")
+        g = (k * 0.3 + 0.15).astype(np.float32)
+        self.check(g, eb=0.15, mode="abs")
+
+    def test_nonfinite(self):
+        f = np.zeros(4096, np.float32)
+        f[3000] = np.nan
+        with pytest.raises(S.SdqzError, match="NaN"):
+            S.compress(f, eb=0.1, mode="abs")
+
+    def test_float64_output_path(self):
+        f = S.generate_field("smooth", (10_000,), seed=4)   # f64 in / out: scalar dq, vec rq
+        self.check(f, eb=1e-4, mode="valrel")
