@@ -8,6 +8,10 @@
 #include <cstring>
 #include <sstream>
 
+#include <vector>
+
+#include <omp.h>
+
 #include "kernels.cuh"
 
 namespace sdqz {
@@ -527,6 +531,92 @@ void capture_compress(sdqz_ctx* ctx, const CompressState& c, const std::string& 
 
 }  // namespace
 
+// ---------------------------------------------------------------------------
+// Host-buffer section copies.  Archive bytes live in pageable memory (a Python
+// bytes object): a DMA from/to pageable memory runs through the driver's
+// bounce buffer at a fraction of PCIe rate, and a fresh bytes object first-
+// touch faults every page.  Sections are therefore staged through one pinned
+// buffer (full-rate DMA) and moved between it and the pageable side by a
+// multi-threaded memcpy (page faults taken in parallel).
+// ---------------------------------------------------------------------------
+constexpr uint64_t kStageMax = 256ull << 20;   // pinned window
+constexpr uint64_t kStageMin = 1ull << 20;     // below this: direct copies
+
+// memcpy in 1 MB pieces across the OpenMP team (<= 16 threads)
+void par_memcpy(void* dst, const void* src, uint64_t n) {
+    constexpr uint64_t piece = 1ull << 20;
+    const long np = (long)((n + piece - 1) / piece);
+    int nt = omp_get_max_threads();
+    nt = nt < 1 ? 1 : (nt > 16 ? 16 : nt);
+    if (np < 2 || nt < 2) {
+        memcpy(dst, src, n);
+        return;
+    }
+#pragma omp parallel for schedule(static) num_threads(nt)
+    for (long i = 0; i < np; i++) {
+        const uint64_t o = (uint64_t)i * piece;
+        memcpy((char*)dst + o, (const char*)src + o, std::min(piece, n - o));
+    }
+}
+
+uint8_t* host_stage(sdqz_ctx* ctx, uint64_t bytes) {
+    if (ctx->h_stage_bytes < bytes) {
+        if (ctx->h_stage) cudaFreeHost(ctx->h_stage);
+        ctx->h_stage = nullptr;
+        ctx->h_stage_bytes = 0;
+        if (cudaHostAlloc(&ctx->h_stage, bytes, cudaHostAllocDefault) != cudaSuccess) {
+            cudaGetLastError();
+            ctx->h_stage = nullptr;
+            return nullptr;
+        }
+        ctx->h_stage_bytes = bytes;
+    }
+    return (uint8_t*)ctx->h_stage;
+}
+
+struct Seg {
+    void* dev;
+    uint64_t len;
+};
+
+// Copy the concatenation of `segs` (device buffers) to / from the contiguous
+// host range `host`; synchronous on return.
+int staged_copy(sdqz_ctx* ctx, uint8_t* host, const Seg* segs, int nseg, bool d2h) {
+    uint64_t total = 0;
+    for (int i = 0; i < nseg; i++) total += segs[i].len;
+    const auto kind = d2h ? cudaMemcpyDeviceToHost : cudaMemcpyHostToDevice;
+    uint8_t* stage = total >= kStageMin ? host_stage(ctx, std::min(total, kStageMax)) : nullptr;
+    if (!stage) {   // small (or no pinned memory): direct copies
+        uint64_t o = 0;
+        for (int i = 0; i < nseg; i++) {
+            if (segs[i].len)
+                SDQZ_CUDA(ctx, d2h ? cudaMemcpyAsync(host + o, segs[i].dev, segs[i].len, kind, ctx->stream)
+                                   : cudaMemcpyAsync(segs[i].dev, host + o, segs[i].len, kind, ctx->stream));
+            o += segs[i].len;
+        }
+        SDQZ_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
+        return SDQZ_OK;
+    }
+    const uint64_t W = std::min(total, kStageMax);
+    for (uint64_t off = 0; off < total; off += W) {
+        const uint64_t w = std::min(W, total - off);
+        if (!d2h) par_memcpy(stage, host + off, w);
+        uint64_t base = 0;
+        for (int i = 0; i < nseg; i++) {
+            const uint64_t a = std::max(base, off), b = std::min(base + segs[i].len, off + w);
+            if (a < b) {
+                char* dv = (char*)segs[i].dev + (a - base);
+                SDQZ_CUDA(ctx, d2h ? cudaMemcpyAsync(stage + (a - off), dv, b - a, kind, ctx->stream)
+                                   : cudaMemcpyAsync(dv, stage + (a - off), b - a, kind, ctx->stream));
+            }
+            base += segs[i].len;
+        }
+        SDQZ_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
+        if (d2h) par_memcpy(host + off, stage, w);
+    }
+    return SDQZ_OK;
+}
+
 extern "C" {
 
 int sdqz_ctx_create(int device, void* stream, sdqz_ctx** out) {
@@ -564,6 +654,7 @@ int sdqz_ctx_destroy(sdqz_ctx* ctx) {
     if (ctx->g_decomp.exec) cudaGraphExecDestroy(ctx->g_decomp.exec);
     if (ctx->d_status) cudaFree(ctx->d_status);
     if (ctx->h_status) cudaFreeHost(ctx->h_status);
+    if (ctx->h_stage) cudaFreeHost(ctx->h_stage);
     if (ctx->own_stream) cudaStreamDestroy(ctx->stream);
     delete ctx;
     return SDQZ_OK;
@@ -923,20 +1014,11 @@ int sdqz_archive_write(sdqz_ctx* ctx, uint8_t* h_dst, uint64_t capacity) {
     if (capacity < total) return set_error(ctx, SDQZ_EINVAL, "destination too small");
     put_header(h_dst, h);
     uint8_t* p = h_dst + SDQZ_HEADER_SIZE;
-    SDQZ_CUDA(ctx, cudaMemcpyAsync(p, ctx->bufs[S_BW].p, h.cap, cudaMemcpyDeviceToHost, ctx->stream));
-    p += h.cap;
-    if (h.n_outliers)
-        SDQZ_CUDA(ctx, cudaMemcpyAsync(p, ctx->bufs[S_OUTREC].p, 16 * h.n_outliers,
-                                       cudaMemcpyDeviceToHost, ctx->stream));
-    p += 16 * h.n_outliers;
-    SDQZ_CUDA(ctx, cudaMemcpyAsync(p, ctx->bufs[S_CHUNK_BITS].p, 4 * h.n_chunks,
-                                   cudaMemcpyDeviceToHost, ctx->stream));
-    p += 4 * h.n_chunks;
-    if (h.payload_bytes)
-        SDQZ_CUDA(ctx, cudaMemcpyAsync(p, ctx->bufs[S_PAYLOAD].p, h.payload_bytes,
-                                       cudaMemcpyDeviceToHost, ctx->stream));
-    SDQZ_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
-    return SDQZ_OK;
+    const Seg segs[4] = {{ctx->bufs[S_BW].p, h.cap},
+                         {ctx->bufs[S_OUTREC].p, 16 * h.n_outliers},
+                         {ctx->bufs[S_CHUNK_BITS].p, 4ull * h.n_chunks},
+                         {ctx->bufs[S_PAYLOAD].p, h.payload_bytes}};
+    return staged_copy(ctx, p, segs, 4, true);
 }
 
 int sdqz_parse_header(sdqz_ctx* ctx, const uint8_t* b, uint64_t len, sdqz_header* h) {
@@ -1008,17 +1090,10 @@ int sdqz_decompress(sdqz_ctx* ctx, const uint8_t* h, uint64_t len, void* d_out) 
     uint32_t* cb = scratch_as<uint32_t>(ctx, S_CHUNK_AUX, hdr.n_chunks + 4, &rc);
     uint8_t* pay = scratch_as<uint8_t>(ctx, S_SORT, hdr.payload_bytes + 64, &rc);
     if (!bw || !rec || !cb || !pay) return rc;
-    SDQZ_CUDA(ctx, cudaMemcpyAsync(bw, p, hdr.cap, cudaMemcpyHostToDevice, ctx->stream));
-    p += hdr.cap;
-    if (hdr.n_outliers)
-        SDQZ_CUDA(ctx, cudaMemcpyAsync(rec, p, 16 * hdr.n_outliers, cudaMemcpyHostToDevice, ctx->stream));
-    p += 16 * hdr.n_outliers;
-    if (hdr.n_chunks)
-        SDQZ_CUDA(ctx, cudaMemcpyAsync(cb, p, 4 * hdr.n_chunks, cudaMemcpyHostToDevice, ctx->stream));
-    p += 4 * hdr.n_chunks;
     SDQZ_CUDA(ctx, cudaMemsetAsync(pay + hdr.payload_bytes, 0, 64, ctx->stream));
-    if (hdr.payload_bytes)
-        SDQZ_CUDA(ctx, cudaMemcpyAsync(pay, p, hdr.payload_bytes, cudaMemcpyHostToDevice, ctx->stream));
+    const Seg segs[4] = {{bw, hdr.cap}, {rec, 16 * hdr.n_outliers}, {cb, 4ull * hdr.n_chunks},
+                         {pay, hdr.payload_bytes}};
+    if ((rc = staged_copy(ctx, const_cast<uint8_t*>(p), segs, 4, false))) return rc;
     return sdqz_decompress_sections(ctx, &hdr, bw, rec, cb, pay, d_out);
 }
 

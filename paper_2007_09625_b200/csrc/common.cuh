@@ -161,6 +161,8 @@ struct sdqz_ctx {
 
     sdqz::DevStatus* d_status = nullptr;   // device
     sdqz::DevStatus* h_status = nullptr;   // pinned host mirror
+    void* h_stage = nullptr;               // pinned staging for host-buffer section copies
+    size_t h_stage_bytes = 0;
 
     struct Buf {
         void* p = nullptr;
