@@ -344,6 +344,13 @@ int decompress_core(sdqz_ctx* ctx, const sdqz_header* hdr, const uint8_t* d_bw, 
                                      false)))
                 return r2;
         }
+        if (chunks_ok && rq1d_records_ok(hdr->ndims, hdr->dims, hdr->block, codes, d_out, d_rec)) {
+            // 1D: outlier values straight from the sorted records (no dense scatter)
+            return (r2 = launch_reconstruct_1d_records(ctx, codes, d_rec, k, n, cap, 2.0 * hdr->eb_resolved,
+                                                       d_out, hdr->dtype_code, dense, bflag))
+                       ? r2
+                       : enqueue_status_copy(ctx);
+        }
         if ((r2 = launch_outlier_scatter(ctx, d_rec, nullptr, nullptr, k, n, codes, hdr->ndims,
                                          hdr->dims, safe_block, dense, bflag, true)))
             return r2;

@@ -51,7 +51,11 @@ __global__ void outlier_scatter_kernel(const unsigned long long* __restrict__ re
                                        const uint64_t* __restrict__ idxs, const double* __restrict__ vals,
                                        uint64_t k, uint64_t n, const uint16_t* __restrict__ codes, Geo g,
                                        unsigned long long* __restrict__ dense, uint8_t* blockflag,
-                                       DevStatus* st) {
+                                       DevStatus* st, int check_only) {
+    // check_only (1D records path): order / range / fp64-path checks; the
+    // codes[idx] == 0 check and the outlier values are taken by the
+    // reconstruct kernel from the records, so only the records of a flagged
+    // (fp64-path) block are scattered, for rq_generic_kernel
     unsigned long long f = 0;
     for (uint64_t j = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; j < k;
          j += (uint64_t)gridDim.x * blockDim.x) {
@@ -62,12 +66,21 @@ __global__ void outlier_scatter_kernel(const unsigned long long* __restrict__ re
             if ((long long)idx - (long long)prev <= 0) f |= F_OUT_ORDER;
         }
         if (idx >= n) { f |= F_OUT_RANGE; continue; }
-        if (codes[idx] != 0) f |= F_OUT_NONZERO;
-        dense[idx] = vb;
+        if (!check_only) {
+            if (codes[idx] != 0) f |= F_OUT_NONZERO;
+            dense[idx] = vb;
+        }
         double v = __longlong_as_double((long long)vb);
         if (!(fabs(v) < kExact && v == floor(v))) {
             blockflag[block_of(g, idx)] = 1;
             f |= F_OUT_SLOW;
+            if (check_only && rec) {   // every record of this 32-point block
+                const uint64_t b = idx >> 5;
+                for (uint64_t q = j; q > 0 && j - q < 32 && (rec[2 * (q - 1)] >> 5) == b; q--)
+                    if (rec[2 * (q - 1)] < n) dense[rec[2 * (q - 1)]] = rec[2 * (q - 1) + 1];
+                for (uint64_t q = j; q < k && q - j < 32 && (rec[2 * q] >> 5) == b; q++)
+                    if (rec[2 * q] < n) dense[rec[2 * q]] = rec[2 * q + 1];
+            }
         }
     }
     if (f) atomicOr(&st->flags, f);
@@ -711,6 +724,186 @@ __global__ void __launch_bounds__(kThreads) rq1d_kernel(const uint16_t* __restri
 // scan runs in int32: partial sums wrap, but the carry and every final value
 // are exact whenever |v| < 2^30 (then |final| < 2^30 + 32 r < 2^31); a task
 // with a larger outlier value takes the int64 instantiation.
+// reset scan of one row given the outlier values of its zero codes (vout[k]);
+// positions >= nvalid are not stored
+template <typename V, int OUTK>
+__device__ __forceinline__ void rq1d_rec_row(const uint32_t (&c)[4], const V (&vout)[4], uint64_t i0,
+                                             uint32_t nvalid, int r, uint32_t lane, double two_eb,
+                                             void* __restrict__ out, bool store) {
+    V fin[4];
+    V t = 0;
+    bool f = false;
+#pragma unroll
+    for (int k = 0; k < 4; k++) {
+        t = c[k] == 0 ? vout[k] : t + (V)((int)c[k] - r);
+        f |= c[k] == 0;
+        fin[k] = t;
+    }
+    const uint32_t sl = lane & 7;
+    V P = t;
+#pragma unroll
+    for (int o = 1; o < 8; o <<= 1) {
+        const V y = __shfl_up_sync(kFull, P, o);
+        if (sl >= (uint32_t)o) P += y;
+    }
+    const V E = P - t;
+    const uint32_t m = __ballot_sync(kFull, f) & (((1u << sl) - 1u) << (lane & ~7u));
+    const int s = m ? 31 - __clz(m) : (int)(lane & ~7u);
+    const V carry = E - __shfl_sync(kFull, E, s);
+    bool hit = false;
+#pragma unroll
+    for (int k = 0; k < 4; k++) {
+        hit |= c[k] == 0;
+        if (!hit) fin[k] += carry;
+    }
+    if (!store) return;
+    if (OUTK == 0 && nvalid >= 4) {
+        float4 o4;
+        o4.x = __double2float_rn(__dmul_rn((double)fin[0], two_eb));
+        o4.y = __double2float_rn(__dmul_rn((double)fin[1], two_eb));
+        o4.z = __double2float_rn(__dmul_rn((double)fin[2], two_eb));
+        o4.w = __double2float_rn(__dmul_rn((double)fin[3], two_eb));
+        __stcs(reinterpret_cast<float4*>((float*)out + i0), o4);
+    } else {
+#pragma unroll
+        for (int k = 0; k < 4; k++)
+            if ((uint32_t)k < nvalid) store_out<OUTK>(out, i0 + k, (long long)fin[k], two_eb);
+    }
+}
+
+// start[t] = first record with index >= 1024 t (lower bound; t <= ntask)
+__global__ void task_bounds_kernel(const unsigned long long* __restrict__ rec, uint64_t k, uint64_t ntask,
+                                   unsigned long long* __restrict__ start) {
+    for (uint64_t t = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; t <= ntask;
+         t += (uint64_t)gridDim.x * blockDim.x) {
+        const unsigned long long key = t * 1024ull;
+        uint64_t lo = 0, hi = k;
+        while (lo < hi) {
+            const uint64_t mid = (lo + hi) >> 1;
+            if (rec[2 * mid] < key) lo = mid + 1; else hi = mid;
+        }
+        start[t] = lo;
+    }
+}
+
+// the 8 rows of a task; zero codes take the value of the task record of the
+// same rank (task-relative ranks, first kVals values staged in `vals`)
+constexpr uint32_t kVals = 64;
+template <bool FULL, typename V, int OUTK>
+__device__ __forceinline__ void rq1d_rec_rows(const uint2 (&cw)[8], const double* vals,
+                                              const unsigned long long* __restrict__ trec, uint32_t m,
+                                              uint64_t t0, uint64_t n, const uint8_t* __restrict__ blockflag,
+                                              bool any_slow, int r, uint32_t lane, double two_eb,
+                                              void* __restrict__ out) {
+    const uint32_t lt = (1u << lane) - 1u;
+    uint32_t base = 0;
+#pragma unroll
+    for (int j = 0; j < 8; j++) {
+        const uint64_t i0 = t0 + j * 128 + lane * 4;
+        const uint32_t nvalid = FULL ? 4u : (i0 >= n ? 0u : (uint32_t)umin(4, n - i0));
+        const uint32_t c[4] = {cw[j].x & 0xFFFFu, cw[j].x >> 16, cw[j].y & 0xFFFFu, cw[j].y >> 16};
+        bool z[4];
+#pragma unroll
+        for (int q = 0; q < 4; q++) z[q] = c[q] == 0 && (FULL || (uint32_t)q < nvalid);
+        const bool store = (FULL || nvalid) && !(any_slow && blockflag[i0 >> 5]);
+        const uint32_t b0 = __ballot_sync(kFull, z[0]), b1 = __ballot_sync(kFull, z[1]),
+                       b2 = __ballot_sync(kFull, z[2]), b3 = __ballot_sync(kFull, z[3]);
+        V v4[4] = {0, 0, 0, 0};
+        if (b0 | b1 | b2 | b3) {
+            uint32_t rk = base + __popc(b0 & lt) + __popc(b1 & lt) + __popc(b2 & lt) + __popc(b3 & lt);
+#pragma unroll
+            for (int q = 0; q < 4; q++) {
+                if (z[q]) {
+                    const double v = rk < kVals ? (rk < m ? vals[rk] : 0.0)
+                                                : (rk < m ? __longlong_as_double((long long)trec[2 * rk + 1]) : 0.0);
+                    v4[q] = (V)v;
+                    rk++;
+                }
+            }
+            base += __popc(b0) + __popc(b1) + __popc(b2) + __popc(b3);
+        }
+        rq1d_rec_row<V, OUTK>(c, v4, i0, FULL ? 4u : nvalid, r, lane, two_eb, out, store);
+    }
+}
+
+// 1D block 32 from the archive's sorted outlier records (no dense scatter):
+// task t = points [1024 t, 1024 t + 1024) owns records [start[t], start[t+1]).
+// Each record's code is fetched from the lanes holding the task's codes
+// (codes[idx] == 0, dualquant.py:290-291); a zero code's value is the record
+// of the same rank among the task's zero codes (equal sets once the count
+// check of dualquant.py:292-294 passes, which the host makes after this).
+template <int OUTK>
+__global__ void __launch_bounds__(kThreads) rq1d_rec_kernel(const uint16_t* __restrict__ codes,
+                                                            const unsigned long long* __restrict__ rec,
+                                                            const unsigned long long* __restrict__ start,
+                                                            uint64_t k, const uint8_t* __restrict__ blockflag,
+                                                            uint64_t n, uint32_t cap, double two_eb,
+                                                            void* __restrict__ out, DevStatus* st) {
+    __shared__ double s_vals[kWarpsPerCta][kVals];
+    const int r = (int)(cap >> 1);
+    const uint32_t lane = lane_id(), lt = (1u << lane) - 1u;
+    double* const vals = s_vals[threadIdx.x >> 5];
+    const uint64_t ntask = ceil_div(n, 1024);
+    const bool any_slow = (st->flags & F_OUT_SLOW) != 0;
+    bool nz = false;
+    for (uint64_t task = blockIdx.x * (uint64_t)kWarpsPerCta + (threadIdx.x >> 5); task < ntask;
+         task += (uint64_t)gridDim.x * kWarpsPerCta) {
+        const uint64_t t0 = task * 1024;
+        const bool full = t0 + 1024 <= n;
+        uint2 cw[8];
+        if (full) {
+            const uint2* src = reinterpret_cast<const uint2*>(codes + t0) + lane;
+#pragma unroll
+            for (int j = 0; j < 8; j++) cw[j] = __ldcs(src + 32 * j);
+        } else {
+#pragma unroll
+            for (int j = 0; j < 8; j++) {
+                const uint64_t i0 = t0 + j * 128 + lane * 4;
+                uint32_t h[4];
+#pragma unroll
+                for (int q = 0; q < 4; q++) h[q] = i0 + q < n ? codes[i0 + q] : (uint32_t)r;
+                cw[j] = make_uint2(h[0] | (h[1] << 16), h[2] | (h[3] << 16));
+            }
+        }
+        uint64_t s0 = start[task], s1 = start[task + 1];
+        s0 = s0 < k ? s0 : k;
+        s1 = s1 < s0 ? s0 : (s1 < k ? s1 : k);
+        // the task's records: code at each index must be 0; values beyond
+        // 2^30 in magnitude send the task to int64
+        bool big = false;
+        for (uint64_t b = s0; b < s1; b += 32) {
+            const uint64_t q = b + lane;
+            const bool has = q < s1;
+            const unsigned long long idx = has ? rec[2 * q] : t0;
+            const double v = has ? __longlong_as_double((long long)rec[2 * q + 1]) : 0.0;
+            const uint64_t p = idx - t0;
+            const uint32_t row = (uint32_t)(p >> 7) & 7u, src = (uint32_t)(p >> 2) & 31u, kk = (uint32_t)p & 3u;
+            uint32_t word = 0;
+#pragma unroll
+            for (int jj = 0; jj < 8; jj++) {
+                const uint32_t wx = __shfl_sync(kFull, cw[jj].x, src), wy = __shfl_sync(kFull, cw[jj].y, src);
+                if ((uint32_t)jj == row) word = kk < 2 ? wx : wy;
+            }
+            const uint32_t code = (word >> (16 * (kk & 1))) & 0xFFFFu;
+            nz |= has && p < 1024 && code != 0;
+            big |= has && !(fabs(v) < 1073741824.0);
+            if (has && q - s0 < kVals) vals[q - s0] = v;
+        }
+        __syncwarp();
+        const bool wide = __any_sync(kFull, big);
+        const uint32_t m = (uint32_t)(s1 - s0);   // records of the task (< 2^31: <= 1024 if consistent)
+        if (full) {
+            if (wide) rq1d_rec_rows<true, long long, OUTK>(cw, vals, rec + 2 * s0, m, t0, n, blockflag, any_slow, r, lane, two_eb, out);
+            else rq1d_rec_rows<true, int, OUTK>(cw, vals, rec + 2 * s0, m, t0, n, blockflag, any_slow, r, lane, two_eb, out);
+        } else {
+            if (wide) rq1d_rec_rows<false, long long, OUTK>(cw, vals, rec + 2 * s0, m, t0, n, blockflag, any_slow, r, lane, two_eb, out);
+            else rq1d_rec_rows<false, int, OUTK>(cw, vals, rec + 2 * s0, m, t0, n, blockflag, any_slow, r, lane, two_eb, out);
+        }
+        __syncwarp();
+    }
+    if (__any_sync(kFull, nz) && lane == 0) atomicOr(&st->flags, (unsigned long long)F_OUT_NONZERO);
+}
+
 template <typename V, int OUTK>
 __device__ __forceinline__ void rq1d_vec_row(uint2 cw, const unsigned long long* __restrict__ dense,
                                              uint64_t i0, int r, uint32_t lane, double two_eb,
@@ -906,8 +1099,65 @@ int launch_outlier_scatter(sdqz_ctx* ctx, const void* records, const uint64_t* i
     if (grid > (uint64_t)ctx->num_sms * 8) grid = ctx->num_sms * 8;
     outlier_scatter_kernel<<<(unsigned)grid, 256, 0, ctx->stream>>>(
         (const unsigned long long*)records, idx, val, k, n, codes, g, (unsigned long long*)dense,
-        blockflag, ctx->d_status);
+        blockflag, ctx->d_status, 0);
     SDQZ_LAUNCHED_NAMED(ctx, "outlier_scatter_kernel");
+    return SDQZ_OK;
+}
+
+bool rq1d_records_ok(int ndims, const uint64_t dims[3], const uint32_t block[3], const void* codes,
+                     const void* out, const void* records) {
+    return records && ndims == 1 && block[0] == 32 && dims[0] >= 1 && ((uintptr_t)codes & 7) == 0 &&
+           ((uintptr_t)out & 15) == 0 && !env_disabled("SDQZ_NO_VEC1D");
+}
+
+// 1D block-32 decompress tail: record checks (+ fp64-path blocks scattered),
+// per-task record ranges, reconstruct from the records, fp64 replay of flagged blocks
+int launch_reconstruct_1d_records(sdqz_ctx* ctx, const uint16_t* codes, const void* records, uint64_t k,
+                                  uint64_t n, uint32_t cap, double two_eb, void* out, int out_kind,
+                                  uint64_t* dense, uint8_t* blockflag) {
+    int rc = SDQZ_OK;
+    const unsigned long long* rec = (const unsigned long long*)records;
+    const uint64_t dims[3] = {n, 1, 1};
+    const uint32_t block[3] = {32, 1, 1};
+    Geo g = make_geo(1, dims, block);
+    if (k) {
+        uint64_t grid = ceil_div(k, 256);
+        if (grid > (uint64_t)ctx->num_sms * 8) grid = ctx->num_sms * 8;
+        outlier_scatter_kernel<<<(unsigned)grid, 256, 0, ctx->stream>>>(
+            rec, nullptr, nullptr, k, n, codes, g, (unsigned long long*)dense, blockflag, ctx->d_status, 1);
+        SDQZ_LAUNCHED_NAMED(ctx, "outlier_check_kernel");
+    }
+    const uint64_t ntask = ceil_div(n, 1024);
+    unsigned long long* start = scratch_as<unsigned long long>(ctx, S_OUT_OFF, ntask + 1, &rc);
+    if (!start) return rc;
+    {
+        uint64_t grid = ceil_div(ntask + 1, 256);
+        if (grid > (uint64_t)ctx->num_sms * 8) grid = ctx->num_sms * 8;
+        task_bounds_kernel<<<(unsigned)grid, 256, 0, ctx->stream>>>(rec, k, ntask, start);
+        SDQZ_LAUNCHED_NAMED(ctx, "task_bounds_kernel");
+    }
+    uint64_t grid = ceil_div(ntask, kWarpsPerCta);
+    if (grid > (uint64_t)ctx->num_sms * 8) grid = ctx->num_sms * 8;
+    if (grid < 1) grid = 1;
+    if (out_kind == 0)
+        rq1d_rec_kernel<0><<<(unsigned)grid, kThreads, 0, ctx->stream>>>(codes, rec, start, k, blockflag, n, cap,
+                                                                       two_eb, out, ctx->d_status);
+    else
+        rq1d_rec_kernel<1><<<(unsigned)grid, kThreads, 0, ctx->stream>>>(codes, rec, start, k, blockflag, n, cap,
+                                                                       two_eb, out, ctx->d_status);
+    SDQZ_LAUNCHED_NAMED(ctx, "rq1d_rec_kernel");
+    double* work = scratch_as<double>(ctx, S_WORK, n, &rc);
+    if (!work) return rc;
+    uint64_t gg = ceil_div(g.nblk[0], 128);
+    if (gg > (uint64_t)ctx->num_sms) gg = ctx->num_sms;
+    if (gg < 1) gg = 1;
+    if (out_kind == 0)
+        rq_generic_kernel<0><<<(unsigned)gg, 128, 0, ctx->stream>>>(codes, (const unsigned long long*)dense, blockflag, 1,
+                                                                  g, cap, two_eb, work, out, ctx->d_status);
+    else
+        rq_generic_kernel<1><<<(unsigned)gg, 128, 0, ctx->stream>>>(codes, (const unsigned long long*)dense, blockflag, 1,
+                                                                  g, cap, two_eb, work, out, ctx->d_status);
+    SDQZ_LAUNCHED_NAMED(ctx, "rq_generic_kernel");
     return SDQZ_OK;
 }
 

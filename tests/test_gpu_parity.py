@@ -415,3 +415,61 @@ class TestVec1DPaths:
     def test_float64_output_path(self):
         f = S.generate_field("smooth", (10_000,), seed=4)   # f64 in / out: scalar dq, vec rq
         self.check(f, eb=1e-4, mode="valrel")
+
+
+class TestRecords1D:
+    """1D decompress takes outlier values straight from the archive records
+    (rank among a task's zero codes): edited records must raise what the
+    oracle raises, or decode identically (non-integer values: fp64 path)."""
+
+    @staticmethod
+    def archive():
+        rng = np.random.default_rng(21)
+        f = np.cumsum(rng.normal(0, 1, 50_000)).astype(np.float32)
+        f[::97] += 40.0                      # regular outliers
+        blob = S.compress(f, eb=0.05, mode="abs", cap=64)
+        h = S.parse_header(blob)
+        off = S.HEADER_SIZE + h.cap
+        return bytearray(blob), h, off
+
+    @staticmethod
+    def outcome(blob):
+        try:
+            return O.decompress(bytes(blob)), None
+        except O.OracleError as e:
+            return None, e
+
+    def check(self, blob):
+        want, werr = self.outcome(blob)
+        if werr is None:
+            assert np.array_equal(bits(S.decompress(bytes(blob))), bits(want))
+        else:
+            with pytest.raises(S.SdqzError) as ei:
+                S.decompress(bytes(blob))
+            assert str(ei.value) == str(werr)
+
+    def test_roundtrip(self):
+        blob, h, off = self.archive()
+        assert h.n_outliers > 100
+        self.check(blob)
+
+    @pytest.mark.parametrize("edit", ["shift", "swap", "range", "fraction", "huge", "drop_last"])
+    def test_edited_records(self, edit):
+        blob, h, off = self.archive()
+        rec = np.frombuffer(bytes(blob[off:off + 16 * h.n_outliers]), np.uint64).reshape(-1, 2).copy()
+        j = h.n_outliers // 2
+        if edit == "shift":
+            rec[j, 0] += 1
+        elif edit == "swap":
+            rec[[j, j + 1], 0] = rec[[j + 1, j], 0]
+        elif edit == "range":
+            rec[-1, 0] = 10 ** 9
+        elif edit == "fraction":
+            v = np.array([rec[j, 1]], np.uint64).view(np.float64)[0] + 0.25
+            rec[j, 1] = np.array([v]).view(np.uint64)[0]
+        elif edit == "huge":
+            rec[j, 1] = np.array([3.0 * 2 ** 31]).view(np.uint64)[0]
+        elif edit == "drop_last":
+            rec[-1, 0] += 1
+        blob[off:off + 16 * h.n_outliers] = rec.tobytes()
+        self.check(blob)
