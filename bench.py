@@ -212,6 +212,8 @@ def algorithmic_bytes(kernel: str, n: int, k: int, c: int, p: int) -> int | None
         "rq2d_kernel": 2 * n + 4 * n + 8 * k,
         "rq1d_kernel": 2 * n + 4 * n + 8 * k,
         "rq1d_vec_kernel": 2 * n + 4 * n + 8 * k,
+        "rq1d_rec_kernel": 2 * n + 4 * n + 16 * k,         # codes read, field written, outlier records
+        "outlier_check_kernel": 16 * k,
         "outlier_scatter_kernel": 16 * k + 8 * k + 2 * k,
     }
     for key, v in table.items():
@@ -391,6 +393,12 @@ def ours_arm(args, cfg, world, rank, local_rank):
                          "frac": achieved / peak if achieved else None,
                          "algorithmic_bytes": abytes, "ms": kernels[dom],
                          "traffic": load_traffic(args.config, dom)},
+            "kernel_roofline": {
+                kname: {"ms": round(kms, 5), "algorithmic_bytes": ab,
+                        "gbs": round(ab / (kms / 1e3) / 1e9, 1),
+                        "frac": round(ab / (kms / 1e3) / 1e9 / peak, 3)}
+                for kname, kms in sorted(kernels.items(), key=lambda x: -x[1])
+                if (ab := algorithmic_bytes(kname, n, K, C, P)) and kms > 0},
             "e2e": e2e,
             "gpu_launches": launches,
             "graph_replays": replays,

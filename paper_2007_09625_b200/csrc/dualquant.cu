@@ -837,6 +837,163 @@ __global__ void __launch_bounds__(kThreads, 2) dq1d_vec_kernel(const float* __re
 }
 
 // ----------------------------------------------------------------------------
+// 2D, block 16x16, fp32, row pitch a multiple of 4 floats.  A task is 16 rows
+// x 128 columns (8 blocks side by side); lane l holds columns 4l..4l+3 of
+// each row (float4 loads, uint2 code stores), a block spans 4 lanes.  The
+// task's 64 prequantized values per lane (fixed-point FMA as in
+// dq3d_tma_kernel) stay in registers; D_x by one shuffle per row, D_y against
+// the previous row.  A task holding any |v / 2eb| >= 2^27 - 2048 (or a
+// non-finite value) is computed in fp64 with exact division in the
+// reference's term order (dualquant.py:123-124); values near a rounding tie
+// are redone with exact division.
+// ----------------------------------------------------------------------------
+template <bool SH>
+__device__ __noinline__ void dq2d_task_f64(const float* __restrict__ in, uint16_t* __restrict__ codes,
+                                           uint64_t X, uint64_t y0, int ny, uint64_t x0, bool xin,
+                                           uint32_t lane, double two_eb, int r, uint32_t wbase, uint32_t hb,
+                                           uint32_t shist_s, HistCtx h, bool& bad) {
+    const bool lead = (lane & 3) == 0;
+    double prev[4] = {0.0, 0.0, 0.0, 0.0};
+    for (int y = 0; y < 16; y++) {
+        const bool row = xin && y < ny;
+        float4 w = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (row) w = __ldg(reinterpret_cast<const float4*>(in + (y0 + y) * X + x0));
+        const float e[4] = {w.x, w.y, w.z, w.w};
+        double q[4];
+#pragma unroll
+        for (int c = 0; c < 4; c++) {
+            bad |= row && !isfinite(e[c]);
+            q[c] = row ? prequant((double)e[c], two_eb) : 0.0;
+        }
+        double lq = __shfl_up_sync(kFull, q[3], 1), lp = __shfl_up_sync(kFull, prev[3], 1);
+        if (lead) lq = lp = 0.0;
+        uint32_t cc[4];
+#pragma unroll
+        for (int c = 0; c < 4; c++) {
+            const double nc = c ? q[c - 1] : lq, ncm = c ? prev[c - 1] : lp;
+            const double pred = __dsub_rn(__dadd_rn(prev[c], nc), ncm);
+            cc[c] = code_of_f64(__dsub_rn(q[c], pred), r);
+        }
+#pragma unroll
+        for (int c = 0; c < 4; c++) prev[c] = q[c];
+        if (row) {
+#pragma unroll
+            for (int c = 0; c < 4; c++) dq1d_count<SH>(cc[c], wbase, hb, shist_s, h);
+            *reinterpret_cast<uint2*>(codes + (y0 + y) * X + x0) =
+                make_uint2(cc[0] | (cc[1] << 16), cc[2] | (cc[3] << 16));
+        }
+    }
+}
+
+template <bool SH>
+__global__ void __launch_bounds__(kThreads, 2) dq2d_vec_kernel(const float* __restrict__ in, uint64_t Y,
+                                                               uint64_t X, uint32_t cap, DevStatus* st,
+                                                               uint16_t* __restrict__ codes,
+                                                               unsigned long long* ghist) {
+    extern __shared__ __align__(16) uint32_t dsm2[];
+    uint32_t* hot = dsm2;   // [warp][kHot][32]
+    for (uint32_t i = threadIdx.x; i < kWarpsPerCta * kHot * 32; i += blockDim.x) hot[i] = 0;
+    HistCtx h;
+    hist_init(h, hot + kWarpsPerCta * kHot * 32, ghist, cap);   // (syncs)
+    const double two_eb = st->two_eb;
+    const double rcp = __drcp_rn(two_eb);
+    const uint32_t hi_lo = (uint32_t)__double2hiint(kFixC - kFixBound) + 1u;
+    const uint32_t hi_span = (uint32_t)__double2hiint(kFixC + kFixBound) - hi_lo;
+    const int r = (int)(cap >> 1);
+    const uint32_t wbase = cap >= 2 * kHot ? (uint32_t)r - kHot / 2 : 0u;
+    const uint32_t lane = lane_id(), wid = threadIdx.x >> 5;
+    const uint32_t hb = smem_u32(hot + wid * kHot * 32 + lane) - wbase * 128u;
+    const uint32_t shist_s = SH ? smem_u32(h.shist) : 0u;
+    const bool lead = (lane & 3) == 0;   // first lane of a 16-column block
+    const uint64_t ntx = ceil_div(X, 128), nty = ceil_div(Y, 16), ntask = ntx * nty;
+    bool bad = false;
+    for (uint64_t task = blockIdx.x * (uint64_t)kWarpsPerCta + wid; task < ntask;
+         task += (uint64_t)gridDim.x * kWarpsPerCta) {
+        const uint64_t tx = task % ntx, ty = task / ntx;
+        const uint64_t x0 = tx * 128 + lane * 4, y0 = ty * 16;
+        const bool xin = x0 < X;
+        const int ny = (int)umin(16, Y - y0);
+        const float* src = in + y0 * X + x0;
+        int q[16][4];
+        bool amb = false, mark = false;
+#pragma unroll
+        for (int hh = 0; hh < 4; hh++) {
+            float4 v[4];
+#pragma unroll
+            for (int y = 0; y < 4; y++) {
+                v[y] = make_float4(0.f, 0.f, 0.f, 0.f);
+                if (xin && hh * 4 + y < ny) v[y] = __ldcs(reinterpret_cast<const float4*>(src + (hh * 4 + y) * X));
+            }
+#pragma unroll
+            for (int y = 0; y < 4; y++) {
+                const float e[4] = {v[y].x, v[y].y, v[y].z, v[y].w};
+#pragma unroll
+                for (int c = 0; c < 4; c++) {
+                    const double R = __fma_rn((double)e[c], rcp, kFixC);
+                    const uint32_t lo = (uint32_t)__double2loint(R), hi = (uint32_t)__double2hiint(R);
+                    amb |= (lo & 0x3FFFFCu) == 0u;
+                    mark |= (hi - hi_lo) >= hi_span;
+                    q[hh * 4 + y][c] = (int)__funnelshift_r(lo, hi, 22);
+                }
+            }
+        }
+        if (__any_sync(kFull, mark)) {   // rare: huge magnitudes or non-finite values
+            dq2d_task_f64<SH>(in, codes, X, y0, ny, x0, xin, lane, two_eb, r, wbase, hb, shist_s, h, bad);
+            continue;
+        }
+        if (__any_sync(kFull, amb)) {   // rare: exact division near a rounding tie
+#pragma unroll
+            for (int y = 0; y < 16; y++) {
+                if (!(xin && y < ny)) continue;
+                const float4 w = __ldg(reinterpret_cast<const float4*>(src + y * X));
+                const float e[4] = {w.x, w.y, w.z, w.w};
+#pragma unroll
+                for (int c = 0; c < 4; c++) {
+                    const double R = __fma_rn((double)e[c], rcp, kFixC);
+                    if (((uint32_t)__double2loint(R) & 0x3FFFFCu) == 0u) {
+                        const int m = (int)floor(__dadd_rn(fabs(__ddiv_rn((double)e[c], two_eb)), 0.5));
+                        q[y][c] = (e[c] < 0.f ? -m : m) + kFixK;
+                    }
+                }
+            }
+        }
+        int gprev[4] = {0, 0, 0, 0};
+#pragma unroll
+        for (int y = 0; y < 16; y++) {
+            int left = __shfl_up_sync(kFull, q[y][3], 1);
+            if (lead) left = kFixK;
+            uint32_t cc[4];
+#pragma unroll
+            for (int c = 0; c < 4; c++) {
+                const int g = q[y][c] - (c ? q[y][c - 1] : left);
+                const uint32_t uu = (uint32_t)(g - gprev[c] + r);
+                gprev[c] = g;
+                cc[c] = (uu - 1u) < (uint32_t)(2 * r - 1) ? uu : 0u;   // -r < delta < r
+            }
+            if (xin && y < ny) {
+#pragma unroll
+                for (int c = 0; c < 4; c++) dq1d_count<SH>(cc[c], wbase, hb, shist_s, h);
+                *reinterpret_cast<uint2*>(codes + (y0 + y) * X + x0) =
+                    make_uint2(cc[0] | (cc[1] << 16), cc[2] | (cc[3] << 16));
+            }
+        }
+    }
+    if (__any_sync(kFull, bad) && lane == 0) atomicOr(&st->flags, (unsigned long long)F_NONFINITE);
+    __syncthreads();
+    for (uint32_t j = wid; j < kHot; j += kWarpsPerCta) {
+        uint32_t sum = 0;
+#pragma unroll
+        for (int w = 0; w < kWarpsPerCta; w++) sum += hot[(w * kHot + j) * 32 + lane];
+        sum = __reduce_add_sync(kFull, sum);
+        if (lane == 0 && sum && wbase + j < cap) {
+            if (h.shist) atomicAdd(&h.shist[wbase + j], sum);
+            else if (h.ghist) atomicAdd(&h.ghist[wbase + j], (unsigned long long)sum);
+        }
+    }
+    hist_finish(h);
+}
+
+// ----------------------------------------------------------------------------
 // Generic block shapes: one thread per point, fp64 reference order.
 // ----------------------------------------------------------------------------
 struct Geo {
@@ -990,6 +1147,29 @@ int launch_kind(sdqz_ctx* ctx, const void* d_in, int ndims, const uint64_t dims[
                                                                cap, ctx->d_status, d_codes + off, d_hist);
             SDQZ_LAUNCHED_NAMED(ctx, "dq1d_kernel");
         }
+        return SDQZ_OK;
+    }
+    // vectorised 2D path (16-byte aligned rows)
+    if (KIND == 0 && ndims == 2 && is_fast_shape(ndims, block) && dims[1] % 4 == 0 &&
+        ((uintptr_t)d_in & 15) == 0 && ((uintptr_t)d_codes & 7) == 0 && !env_disabled("SDQZ_NO_VEC2D")) {
+        const uint64_t nt = ceil_div(dims[1], 128) * ceil_div(dims[0], 16);
+        const size_t vsm = kWarpsPerCta * kHot * 32 * 4 + smem;
+        static bool vattr = false;
+        if (!vattr) {
+            const int mx = kWarpsPerCta * kHot * 32 * 4 + kSmemHistMax * 4;
+            cudaFuncSetAttribute(dq2d_vec_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
+            cudaFuncSetAttribute(dq2d_vec_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
+            vattr = true;
+        }
+        uint64_t grid = ceil_div(nt, kWarpsPerCta);
+        if (grid > (uint64_t)ctx->num_sms * 2) grid = (uint64_t)ctx->num_sms * 2;
+        if (smem)
+            dq2d_vec_kernel<true><<<(unsigned)grid, kThreads, vsm, ctx->stream>>>(
+                (const float*)d_in, dims[0], dims[1], cap, ctx->d_status, d_codes, d_hist);
+        else
+            dq2d_vec_kernel<false><<<(unsigned)grid, kThreads, vsm, ctx->stream>>>(
+                (const float*)d_in, dims[0], dims[1], cap, ctx->d_status, d_codes, d_hist);
+        SDQZ_LAUNCHED_NAMED(ctx, "dq2d_vec_kernel");
         return SDQZ_OK;
     }
     if (is_fast_shape(ndims, block)) {

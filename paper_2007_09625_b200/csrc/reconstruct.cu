@@ -691,6 +691,117 @@ __global__ void __launch_bounds__(kThreads) rq2d_kernel(const uint16_t* __restri
     }
 }
 
+// 2D block 16x16, row pitch a multiple of 4: a task is 16 rows x 128 columns
+// (8 blocks), lane l holds columns 4l..4l+3 (uint2 code loads, all 16 rows in
+// flight; float4 stores), a block spans 4 lanes.  Row recurrence
+// F(y, x) = F(y-1, x) + S_y(x), S_y = x-prefix of the residuals restarted at an
+// outlier p with S_y(p) = v - F(y-1, p) -- the reference's per-outlier box
+// correction (dualquant.py:218-226) in raster order -- as a reset scan over
+// the block's 4 lanes.  int32 unless an outlier value of the task reaches
+// 2^29 (then |F| < 2^29 + 256 r keeps every result exact; wrapped partial sums
+// cancel).
+template <typename V, int OUTK>
+__device__ __forceinline__ void rq2d_vec_rows(const uint2 (&cw)[16], const unsigned long long* __restrict__ dense,
+                                              uint64_t X, uint64_t y0, int ny, uint64_t x0, bool xin, bool store,
+                                              int r, uint32_t lane, double two_eb, void* __restrict__ out) {
+    V K[4] = {0, 0, 0, 0};
+    const uint32_t sl = lane & 3;
+    const uint32_t below = ((1u << sl) - 1u) << (lane & ~3u);
+#pragma unroll
+    for (int y = 0; y < 16; y++) {
+        const bool row = xin && y < ny;
+        const uint64_t i0 = (y0 + y) * X + x0;
+        const uint32_t c[4] = {cw[y].x & 0xFFFFu, cw[y].x >> 16, cw[y].y & 0xFFFFu, cw[y].y >> 16};
+        V loc[4], t = 0;
+        bool f = false;
+#pragma unroll
+        for (int k = 0; k < 4; k++) {
+            if (c[k] == 0) {
+                t = (V)__longlong_as_double((long long)dense[i0 + k]) - K[k];
+                f = true;
+            } else {
+                t += (V)((int)c[k] - r);
+            }
+            loc[k] = t;
+        }
+        V P = t;
+#pragma unroll
+        for (int o = 1; o < 4; o <<= 1) {
+            const V yv = __shfl_up_sync(kFull, P, o);
+            if (sl >= (uint32_t)o) P += yv;
+        }
+        const V E = P - t;
+        const uint32_t m = __ballot_sync(kFull, f) & below;
+        const int src = m ? 31 - __clz(m) : (int)(lane & ~3u);
+        const V carry = E - __shfl_sync(kFull, E, src);
+        bool hit = false;
+#pragma unroll
+        for (int k = 0; k < 4; k++) {
+            hit |= c[k] == 0;
+            K[k] += loc[k] + (hit ? (V)0 : carry);
+        }
+        if (row && store) {
+            if (OUTK == 0) {
+                float4 o4;
+                o4.x = __double2float_rn(__dmul_rn((double)K[0], two_eb));
+                o4.y = __double2float_rn(__dmul_rn((double)K[1], two_eb));
+                o4.z = __double2float_rn(__dmul_rn((double)K[2], two_eb));
+                o4.w = __double2float_rn(__dmul_rn((double)K[3], two_eb));
+                __stcs(reinterpret_cast<float4*>((float*)out + i0), o4);
+            } else {
+#pragma unroll
+                for (int k = 0; k < 4; k++) ((double*)out)[i0 + k] = __dmul_rn((double)K[k], two_eb);
+            }
+        }
+    }
+}
+
+template <int OUTK>
+__global__ void __launch_bounds__(kThreads) rq2d_vec_kernel(const uint16_t* __restrict__ codes,
+                                                            const unsigned long long* __restrict__ dense,
+                                                            const uint8_t* __restrict__ blockflag,
+                                                            int any_slow, uint64_t Y, uint64_t X,
+                                                            uint32_t cap, double two_eb,
+                                                            void* __restrict__ out) {
+    const int r = (int)(cap >> 1);
+    const uint32_t lane = lane_id();
+    const uint64_t nbx = ceil_div(X, 16), ntx = ceil_div(X, 128), nty = ceil_div(Y, 16);
+    const uint64_t ntask = ntx * nty;
+    for (uint64_t task = blockIdx.x * (uint64_t)kWarpsPerCta + (threadIdx.x >> 5); task < ntask;
+         task += (uint64_t)gridDim.x * kWarpsPerCta) {
+        const uint64_t tx = task % ntx, ty = task / ntx;
+        const uint64_t x0 = tx * 128 + lane * 4, y0 = ty * 16;
+        const bool xin = x0 < X;
+        const int ny = (int)umin(16, Y - y0);
+        uint2 cw[16];
+#pragma unroll
+        for (int y = 0; y < 16; y++) {
+            // rows past the field read as residual 0 (code r) and are never stored
+            cw[y] = make_uint2((uint32_t)r | ((uint32_t)r << 16), (uint32_t)r | ((uint32_t)r << 16));
+            if (xin && y < ny) cw[y] = __ldcs(reinterpret_cast<const uint2*>(codes + (y0 + y) * X + x0));
+        }
+        const bool store = !(any_slow && xin && blockflag[ty * nbx + (x0 >> 4)]);
+        bool big = false;
+#pragma unroll
+        for (int y = 0; y < 16; y++) {
+            if (__vcmpeq2(cw[y].x, 0u) | __vcmpeq2(cw[y].y, 0u)) {
+#pragma unroll
+                for (int k = 0; k < 4; k++) {
+                    const uint32_t cc = (k < 2 ? cw[y].x : cw[y].y) >> (16 * (k & 1)) & 0xFFFFu;
+                    if (cc == 0) {
+                        const double v = __longlong_as_double((long long)dense[(y0 + y) * X + x0 + k]);
+                        big |= !(fabs(v) < 536870912.0);
+                    }
+                }
+            }
+        }
+        if (__any_sync(kFull, big))
+            rq2d_vec_rows<long long, OUTK>(cw, dense, X, y0, ny, x0, xin, store, r, lane, two_eb, out);
+        else
+            rq2d_vec_rows<int, OUTK>(cw, dense, X, y0, ny, x0, xin, store, r, lane, two_eb, out);
+    }
+}
+
 template <int OUTK>
 __global__ void __launch_bounds__(kThreads) rq1d_kernel(const uint16_t* __restrict__ codes,
                                                         const unsigned long long* __restrict__ dense,
@@ -1203,6 +1314,12 @@ int launch_reconstruct(sdqz_ctx* ctx, const uint16_t* codes, const uint64_t* den
         const uint64_t nblk3 = ndims == 3 ? ceil_div(dims[0], 8) * ceil_div(dims[1], 8) * ceil_div(dims[2], 8) : 1;
         uint64_t bgrid = ceil_div(nblk3, 64);
         if (bgrid > (uint64_t)ctx->num_sms * 16) bgrid = (uint64_t)ctx->num_sms * 16;
+        // vectorised 2D: 16 x 128 tasks (8-byte code rows, 16-byte output rows)
+        const bool vec2d = ndims == 2 && dims[1] % 4 == 0 && ((uintptr_t)codes & 7) == 0 &&
+                           ((uintptr_t)out & 15) == 0 && !env_disabled("SDQZ_NO_VEC2D");
+        uint64_t grid2 = ndims == 2 ? ceil_div(ceil_div(dims[1], 128) * ceil_div(dims[0], 16), kWarpsPerCta) : 1;
+        if (grid2 > (uint64_t)ctx->num_sms * 8) grid2 = (uint64_t)ctx->num_sms * 8;
+        if (grid2 < 1) grid2 = 1;
         // vectorised 1D: whole 1024-point tasks (8-byte code rows, 16-byte output rows)
         const bool vec1d = ndims == 1 && dims[0] >= 1024 && ((uintptr_t)codes & 7) == 0 &&
                            ((uintptr_t)out & 15) == 0 && !env_disabled("SDQZ_NO_VEC1D");
@@ -1220,6 +1337,9 @@ int launch_reconstruct(sdqz_ctx* ctx, const uint16_t* codes, const uint64_t* den
         else if (ndims == 3)                                                                         \
             rq3d_kernel_old<K><<<(unsigned)grid, kThreads, 0, ctx->stream>>>(codes, dn, blockflag, slow, \
                                                                         dims[0], dims[1], dims[2], cap, two_eb, out); \
+        else if (vec2d)                                                                              \
+            rq2d_vec_kernel<K><<<(unsigned)grid2, kThreads, 0, ctx->stream>>>(codes, dn, blockflag, slow, \
+                                                                             dims[0], dims[1], cap, two_eb, out); \
         else if (ndims == 2)                                                                         \
             rq2d_kernel<K><<<(unsigned)grid, kThreads, 0, ctx->stream>>>(codes, dn, blockflag, slow,   \
                                                                         dims[0], dims[1], cap, two_eb, out); \
@@ -1236,7 +1356,7 @@ int launch_reconstruct(sdqz_ctx* ctx, const uint16_t* codes, const uint64_t* den
         if (out_kind == 0) { RQ_LAUNCH(0) } else { RQ_LAUNCH(1) }
 #undef RQ_LAUNCH
         if (ndims == 3) SDQZ_LAUNCHED_NAMED(ctx, "rq3d_block_kernel");
-        else if (ndims == 2) SDQZ_LAUNCHED_NAMED(ctx, "rq2d_kernel");
+        else if (ndims == 2) SDQZ_LAUNCHED_NAMED(ctx, vec2d ? "rq2d_vec_kernel" : "rq2d_kernel");
         else SDQZ_LAUNCHED_NAMED(ctx, vec1d ? "rq1d_vec_kernel" : "rq1d_kernel");
         if (!any_slow) return SDQZ_OK;
     }

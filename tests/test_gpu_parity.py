@@ -473,3 +473,69 @@ class TestRecords1D:
             rec[-1, 0] += 1
         blob[off:off + 16 * h.n_outliers] = rec.tobytes()
         self.check(blob)
+
+
+class TestVec2DPaths:
+    """The vectorised 2D kernels (dq2d_vec / rq2d_vec: 16 x 128 tasks, rows a
+    multiple of 4 floats): edges, caps, the fp64 task redo, rounding ties,
+    outliers beyond the int32 range, fp64 fields."""
+
+    check = staticmethod(TestDualquant3DPaths.check)
+
+    @pytest.mark.parametrize("dims", [(16, 128), (17, 132), (1, 4), (40, 300), (123, 1028), (1800, 3600)])
+    def test_shapes(self, dims):
+        f = S.generate_field("smooth", dims, seed=9).astype(np.float32)
+        self.check(f, eb=1e-4, mode="valrel")
+
+    @pytest.mark.parametrize("cap", [4, 16, 32, 1024, 65536])
+    def test_caps(self, cap):
+        rng = np.random.default_rng(cap + 1)
+        f = np.cumsum(rng.normal(0, 1, (40, 200)), axis=1).astype(np.float32)
+        self.check(f, eb=0.05, mode="abs", cap=cap)
+
+    def test_big_magnitudes(self):
+        rng = np.random.default_rng(14)
+        f = rng.normal(0, 1.0, (48, 256)).astype(np.float32)
+        f[5:9, 10:90] *= 3e8                 # fp64 task redo in dq, int64 rows in rq
+        f[30, 200] = 2.0 ** 27 * 2e-3
+        f[40:42, 100:140] = 2.0 ** 30 * 2e-3   # outlier values beyond 2^29 units
+        self.check(f, eb=1e-3, mode="abs")
+
+    def test_outlier_dense(self):
+        rng = np.random.default_rng(15)
+        f = rng.normal(0, 50.0, (64, 320)).astype(np.float32)
+        self.check(f, eb=0.01, mode="abs", cap=16)
+
+    def test_rounding_ties(self):
+        rng = np.random.default_rng(16)
+        k = rng.integers(-4000, 4000, (32, 256)).astype(np.float64)
+        f = ((k + 0.5) * 0.25).astype(np.float32)
+        f[:, ::2] = np.nextafter(f[:, ::2], np.float32(np.inf))
+        self.check(f, eb=0.125, mode="abs")
+        g = (k * 0.3 + 0.15).astype(np.float32)
+        self.check(g, eb=0.15, mode="abs")
+
+    def test_nonfinite(self):
+        f = np.zeros((32, 128), np.float32)
+        f[20, 77] = np.inf
+        with pytest.raises(S.SdqzError, match="NaN"):
+            S.compress(f, eb=0.1, mode="abs")
+
+    def test_float64_field(self):
+        f = S.generate_field("smooth", (50, 400), seed=5)
+        self.check(f, eb=1e-4, mode="valrel")
+
+    def test_fraction_outlier_block(self):
+        # a non-integer outlier value sends its block to the fp64 replay
+        rng = np.random.default_rng(17)
+        f = np.cumsum(rng.normal(0, 1, (32, 256)), axis=1).astype(np.float32)
+        f[::7, ::11] += 30.0
+        blob = bytearray(S.compress(f, eb=0.05, mode="abs", cap=64))
+        h = S.parse_header(bytes(blob))
+        off = S.HEADER_SIZE + h.cap
+        rec = np.frombuffer(bytes(blob[off:off + 16 * h.n_outliers]), np.uint64).reshape(-1, 2).copy()
+        v = rec[:, 1].copy().view(np.float64)
+        v[h.n_outliers // 2] += 0.25
+        rec[:, 1] = v.view(np.uint64)
+        blob[off:off + 16 * h.n_outliers] = rec.tobytes()
+        assert np.array_equal(bits(S.decompress(bytes(blob))), bits(O.decompress(bytes(blob))))
