@@ -94,6 +94,12 @@ SDQZ_API int sdqz_kernel_times(sdqz_ctx* ctx, char* buf, uint64_t len);
 SDQZ_API int sdqz_describe(sdqz_ctx* ctx, const void* d_in, int dtype, uint64_t n,
                   double* vmin, double* vmax, int* nonfinite);
 
+/* Reconstruction quality (metrics.py:52-76) in one fp64 pass over both
+ * device arrays: out = {sum (a-b)^2, max |a-b|, min a, max a, nonfinite(a)}.
+ * Replaces the reference's numpy reductions in quality() / rd_sweep(). */
+SDQZ_API int sdqz_quality(sdqz_ctx* ctx, const void* d_orig, int orig_dtype, const void* d_recon,
+                          int recon_dtype, uint64_t n, double* out);
+
 /* ---- L2 lossy stage (dualquant.py) --------------------------------------- */
 /* prequantize (dualquant.py:62-78): d_out[i] = copysign(floor(|x/(2eb)|+.5), x/(2eb)). */
 SDQZ_API int sdqz_prequantize(sdqz_ctx* ctx, const void* d_in, int dtype, uint64_t n, double eb,

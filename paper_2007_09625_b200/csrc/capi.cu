@@ -733,6 +733,19 @@ int sdqz_describe(sdqz_ctx* ctx, const void* d_in, int dtype, uint64_t n, double
     return SDQZ_OK;
 }
 
+int sdqz_quality(sdqz_ctx* ctx, const void* d_orig, int orig_dtype, const void* d_recon, int recon_dtype,
+                 uint64_t n, double* out) {
+    int rc = SDQZ_OK;
+    if (n == 0) return set_error(ctx, SDQZ_EINVAL, "cannot score empty arrays");
+    double* part = scratch_as<double>(ctx, S_QUAL, 5 * 592 + 8, &rc);
+    if (!part) return rc;
+    if ((rc = launch_quality(ctx, d_orig, orig_dtype, d_recon, recon_dtype, n, part, part + 5 * 592)))
+        return rc;
+    SDQZ_CUDA(ctx, cudaMemcpyAsync(out, part + 5 * 592, 5 * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
+    SDQZ_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
+    return SDQZ_OK;
+}
+
 int sdqz_prequantize(sdqz_ctx* ctx, const void* d_in, int dtype, uint64_t n, double eb,
                      double* d_out) {
     int rc;

@@ -120,7 +120,83 @@ __global__ void resolve_kernel(DevStatus* st, int dtype, int eb_mode, double mag
     st->two_eb = __dmul_rn(2.0, eb);
 }
 
+// quality (metrics.py:52-76): one pass over (orig, recon) in fp64 -> per-CTA
+// partials {sum d^2, max |d|, min a, max a, nonfinite(a)}; a single CTA then
+// folds the partials in a fixed order (deterministic result).
+constexpr int kQualCtas = 592;
+template <typename A, typename B>
+__global__ void __launch_bounds__(256) quality_partial_kernel(const A* __restrict__ a, const B* __restrict__ b,
+                                                              uint64_t n, double* __restrict__ part) {
+    double ss = 0.0, mx = 0.0, amin = INFINITY, amax = -INFINITY;
+    bool bad = false;
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n;
+         i += (uint64_t)gridDim.x * blockDim.x) {
+        const double x = (double)__ldcs(a + i), y = (double)__ldcs(b + i);
+        const double d = __dsub_rn(x, y);
+        ss = __fma_rn(d, d, ss);
+        mx = fmax(mx, fabs(d));
+        amin = fmin(amin, x);
+        amax = fmax(amax, x);
+        bad |= !isfinite(x);
+        mx = isnan(d) ? d : mx;   // a NaN difference propagates (numpy max)
+    }
+    __shared__ double s[5][8];
+    const uint32_t lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+#pragma unroll
+    for (int o = 16; o; o >>= 1) {
+        ss += __shfl_down_sync(kFull, ss, o);
+        const double m2 = __shfl_down_sync(kFull, mx, o);
+        mx = isnan(m2) ? m2 : fmax(mx, m2);
+        amin = fmin(amin, __shfl_down_sync(kFull, amin, o));
+        amax = fmax(amax, __shfl_down_sync(kFull, amax, o));
+    }
+    const bool wbad = __any_sync(kFull, bad);
+    if (lane == 0) { s[0][w] = ss; s[1][w] = mx; s[2][w] = amin; s[3][w] = amax; s[4][w] = wbad ? 1.0 : 0.0; }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double r0 = 0.0, r1 = 0.0, r2 = INFINITY, r3 = -INFINITY, r4 = 0.0;
+        for (int k = 0; k < 8; k++) {
+            r0 += s[0][k];
+            r1 = isnan(s[1][k]) ? s[1][k] : fmax(r1, s[1][k]);
+            r2 = fmin(r2, s[2][k]);
+            r3 = fmax(r3, s[3][k]);
+            r4 = fmax(r4, s[4][k]);
+        }
+        double* p = part + 5 * blockIdx.x;
+        p[0] = r0; p[1] = r1; p[2] = r2; p[3] = r3; p[4] = r4;
+    }
+}
+
+__global__ void quality_final_kernel(const double* __restrict__ part, int nparts, double* __restrict__ out) {
+    double r0 = 0.0, r1 = 0.0, r2 = INFINITY, r3 = -INFINITY, r4 = 0.0;
+    for (int k = 0; k < nparts; k++) {
+        const double* p = part + 5 * k;
+        r0 += p[0];
+        r1 = isnan(p[1]) ? p[1] : fmax(r1, p[1]);
+        r2 = fmin(r2, p[2]);
+        r3 = fmax(r3, p[3]);
+        r4 = fmax(r4, p[4]);
+    }
+    out[0] = r0; out[1] = r1; out[2] = r2; out[3] = r3; out[4] = r4;
+}
+
 }  // namespace
+
+int launch_quality(sdqz_ctx* ctx, const void* a, int a_dtype, const void* b, int b_dtype, uint64_t n,
+                   double* d_part, double* d_out) {
+    uint64_t g = ceil_div(n, 256 * 4);
+    const int grid = (int)(g < 1 ? 1 : (g > (uint64_t)kQualCtas ? kQualCtas : g));
+#define QK(TA, TB) quality_partial_kernel<TA, TB><<<grid, 256, 0, ctx->stream>>>((const TA*)a, (const TB*)b, n, d_part)
+    if (a_dtype == 0 && b_dtype == 0) QK(float, float);
+    else if (a_dtype == 0) QK(float, double);
+    else if (b_dtype == 0) QK(double, float);
+    else QK(double, double);
+#undef QK
+    SDQZ_LAUNCHED_NAMED(ctx, "quality_partial_kernel");
+    quality_final_kernel<<<1, 1, 0, ctx->stream>>>(d_part, grid, d_out);
+    SDQZ_LAUNCHED_NAMED(ctx, "quality_final_kernel");
+    return SDQZ_OK;
+}
 
 int launch_describe(sdqz_ctx* ctx, const void* d_in, int dtype, uint64_t n) {
     int grid = ctx->num_sms * 4;

@@ -539,3 +539,54 @@ class TestVec2DPaths:
         rec[:, 1] = v.view(np.uint64)
         blob[off:off + 16 * h.n_outliers] = rec.tobytes()
         assert np.array_equal(bits(S.decompress(bytes(blob))), bits(O.decompress(bytes(blob))))
+
+
+class TestQualityKernel:
+    """metrics.quality through sdqz_quality (reference test_metrics.py:10-60)."""
+
+    @staticmethod
+    def numpy_quality(a, b):
+        a = np.asarray(a, np.float64).ravel()
+        b = np.asarray(b, np.float64).ravel()
+        d = a - b
+        return float(np.sqrt(np.mean(d * d))), float(np.abs(d).max()), float(a.max() - a.min())
+
+    def test_psnr_formula(self):
+        orig = np.array([0.0, 1.0])
+        q = S.quality(orig, orig + 1e-4)
+        assert q.psnr_db == pytest.approx(80.0, abs=1e-9)
+        assert q.rmse == pytest.approx(1e-4) and q.max_abs_error == pytest.approx(1e-4)
+
+    def test_identical(self):
+        q = S.quality(np.arange(5.0), np.arange(5.0))
+        assert q.rmse == 0.0 and np.isinf(q.psnr_db)
+
+    @pytest.mark.parametrize("dt", [np.float32, np.float64])
+    def test_against_numpy(self, dt):
+        rng = np.random.default_rng(3)
+        a = rng.normal(0, 3, 1_234_567).astype(dt)
+        b = (a + rng.uniform(-1e-3, 1e-3, a.size)).astype(np.float32)
+        q = S.quality(a, b)
+        rmse, mx, rg = self.numpy_quality(a, b)
+        assert q.max_abs_error == mx and q.value_range == rg
+        assert q.rmse == pytest.approx(rmse, rel=1e-12)
+
+    def test_errors(self):
+        with pytest.raises(S.SdqzError, match="length"):
+            S.quality(np.zeros(3), np.zeros(4))
+        with pytest.raises(S.SdqzError, match="zero value range"):
+            S.quality(np.zeros(4), np.ones(4))
+        with pytest.raises(S.SdqzError, match="nonfinite"):
+            S.quality(np.array([0.0, np.nan]), np.zeros(2))
+
+    def test_rd_sweep_matches_decompress(self):
+        f = S.generate_field("smooth", (24, 40, 56), seed=2).astype(np.float32)
+        fd = S.describe_field(f, f.shape)
+        rows = S.rd_sweep(f, fd, [S.ErrorBoundSpec("valrel", e) for e in (1e-2, 1e-3, 1e-4)])
+        for r, e in zip(rows, (1e-2, 1e-3, 1e-4)):
+            blob = O.compress(f, eb=e, mode="valrel")
+            rec = O.decompress(blob)
+            rmse, mx, rg = self.numpy_quality(f, rec)
+            assert r.error is None and r.max_abs_err == mx
+            assert r.psnr_db == pytest.approx(20 * np.log10(rg / rmse), abs=1e-9)
+            assert r.cr == pytest.approx(f.nbytes / len(blob))
