@@ -210,6 +210,7 @@ def algorithmic_bytes(kernel: str, n: int, k: int, c: int, p: int) -> int | None
         "inflate_fast_kernel": p + 12 * c + 2 * n,         # payload, chunk bits + offsets, codes written
         "rq3d_block_kernel": 2 * n + 4 * n + 8 * k,        # codes read, field written, outlier values
         "rq2d_kernel": 2 * n + 4 * n + 8 * k,
+        "rq2d_vec_kernel": 2 * n + 4 * n + 8 * k,
         "rq1d_kernel": 2 * n + 4 * n + 8 * k,
         "rq1d_vec_kernel": 2 * n + 4 * n + 8 * k,
         "rq1d_rec_kernel": 2 * n + 4 * n + 16 * k,         # codes read, field written, outlier records
