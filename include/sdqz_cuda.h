@@ -94,6 +94,10 @@ SDQZ_API int sdqz_kernel_times(sdqz_ctx* ctx, char* buf, uint64_t len);
 SDQZ_API int sdqz_describe(sdqz_ctx* ctx, const void* d_in, int dtype, uint64_t n,
                   double* vmin, double* vmax, int* nonfinite);
 
+/* Host -> device copy of a pageable host buffer through the context's pinned
+ * staging (parallel host copy overlapped with the DMA); synchronous. */
+SDQZ_API int sdqz_upload(sdqz_ctx* ctx, const void* h_src, uint64_t bytes, void* d_dst);
+
 /* Reconstruction quality (metrics.py:52-76) in one fp64 pass over both
  * device arrays: out = {sum (a-b)^2, max |a-b|, min a, max a, nonfinite(a)}.
  * Replaces the reference's numpy reductions in quality() / rd_sweep(). */

@@ -2,6 +2,8 @@
 
 from __future__ import annotations
 
+import ctypes
+
 import numpy as np
 
 from . import _lib
@@ -58,7 +60,13 @@ def to_device(arr, dtype=None):
         a = np.ascontiguousarray(arr, dtype=dt).reshape(-1)
         if not a.flags.writeable:
             a = a.copy()
-        t = torch.from_numpy(a).to(dev, non_blocking=False)
+        h = torch.from_numpy(a)
+        if a.nbytes >= _STAGED_MIN_BYTES and not h.is_pinned():
+            # pageable source: pinned staging + parallel host copy (sdqz_upload)
+            t = torch.empty(a.size, dtype=tdt, device=dev)
+            _lib.context().call("sdqz_upload", ctypes.c_void_p(a.ctypes.data), a.nbytes, _lib.ptr(t))
+        else:
+            t = h.to(dev, non_blocking=False)
     return t, dt
 
 
@@ -82,6 +90,7 @@ def zeros(n: int, dtype):
 
 
 _PINNED_MIN_BYTES = 1 << 20
+_STAGED_MIN_BYTES = 1 << 20
 
 
 def download(t, n: int | None = None) -> np.ndarray:

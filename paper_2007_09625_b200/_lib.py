@@ -53,6 +53,7 @@ _SIGS = {
     "sdqz_describe": (c_int, [c_void_p, c_void_p, c_int, c_uint64, POINTER(c_double),
                               POINTER(c_double), POINTER(c_int)]),
     "sdqz_prequantize": (c_int, [c_void_p, c_void_p, c_int, c_uint64, c_double, c_void_p]),
+    "sdqz_upload": (c_int, [c_void_p, c_void_p, c_uint64, c_void_p]),
     "sdqz_quality": (c_int, [c_void_p, c_void_p, c_int, c_void_p, c_int, c_uint64, POINTER(c_double)]),
     "sdqz_dualquant": (c_int, [c_void_p, c_void_p, c_int, c_int, POINTER(c_uint64),
                                POINTER(c_uint32), c_double, c_uint32, c_void_p, c_void_p,

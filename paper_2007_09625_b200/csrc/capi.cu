@@ -626,16 +626,21 @@ int staged_copy(sdqz_ctx* ctx, uint8_t* host, const Seg* segs, int nseg, bool d2
     const uint64_t W = std::min(total, kStageMax);
     for (uint64_t off = 0; off < total; off += W) {
         const uint64_t w = std::min(W, total - off);
-        if (!d2h) par_memcpy(stage, host + off, w);
-        uint64_t base = 0;
-        for (int i = 0; i < nseg; i++) {
-            const uint64_t a = std::max(base, off), b = std::min(base + segs[i].len, off + w);
-            if (a < b) {
-                char* dv = (char*)segs[i].dev + (a - base);
-                SDQZ_CUDA(ctx, d2h ? cudaMemcpyAsync(stage + (a - off), dv, b - a, kind, ctx->stream)
-                                   : cudaMemcpyAsync(dv, stage + (a - off), b - a, kind, ctx->stream));
+        // H2D: 8 MB pieces, the DMA of one overlaps the host copy of the next
+        const uint64_t piece = d2h ? w : (8ull << 20);
+        for (uint64_t lo = 0; lo < w; lo += piece) {
+            const uint64_t hi = std::min(w, lo + piece);
+            if (!d2h) par_memcpy(stage + lo, host + off + lo, hi - lo);
+            uint64_t base = 0;
+            for (int i = 0; i < nseg; i++) {
+                const uint64_t a = std::max(base, off + lo), b = std::min(base + segs[i].len, off + hi);
+                if (a < b) {
+                    char* dv = (char*)segs[i].dev + (a - base);
+                    SDQZ_CUDA(ctx, d2h ? cudaMemcpyAsync(stage + (a - off), dv, b - a, kind, ctx->stream)
+                                       : cudaMemcpyAsync(dv, stage + (a - off), b - a, kind, ctx->stream));
+                }
+                base += segs[i].len;
             }
-            base += segs[i].len;
         }
         if (d2h) par_populate(host + off, w);
         SDQZ_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
@@ -751,6 +756,11 @@ int sdqz_describe(sdqz_ctx* ctx, const void* d_in, int dtype, uint64_t n, double
     }
     *nonfinite = (s.flags & F_NONFINITE) ? 1 : 0;
     return SDQZ_OK;
+}
+
+int sdqz_upload(sdqz_ctx* ctx, const void* h_src, uint64_t bytes, void* d_dst) {
+    const Seg seg{d_dst, bytes};
+    return staged_copy(ctx, (uint8_t*)const_cast<void*>(h_src), &seg, 1, false);
 }
 
 int sdqz_quality(sdqz_ctx* ctx, const void* d_orig, int orig_dtype, const void* d_recon, int recon_dtype,
