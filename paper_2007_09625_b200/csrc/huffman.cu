@@ -1291,6 +1291,7 @@ __global__ void __launch_bounds__(64) inflate_kernel(
     // `only` != null: decode just the chunks the warp-parallel decoder handed
     // back (tiny chunks, corrupt streams -> exact reference error semantics)
     const uint64_t c = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+    if (only && st->pad[1] == 0) return;   // the warp-parallel decoder handed nothing back
     if (only && !__any_sync(kFull, c < nchunks && only[c])) return;
     __shared__ uint32_t lut[1 << kLutBits];
     __shared__ unsigned long long first[58];
@@ -1414,8 +1415,11 @@ int run_deflate(sdqz_ctx* ctx, DeflateArgs& a, bool payload) {
             else chunk_pack32_kernel<false><<<(unsigned)grid, 256, 0, ctx->stream>>>(a);
             SDQZ_LAUNCHED_NAMED(ctx, "chunk_pack32_kernel");
         }
-        if (ts) chunk_pack_run_kernel<true><<<(unsigned)grid, 256, smem, ctx->stream>>>(a, payload ? 1 : 0);
-        else chunk_pack_run_kernel<false><<<(unsigned)grid, 256, 0, ctx->stream>>>(a, payload ? 1 : 0);
+        // 64-bit units (or no payload): device-decided, usually an idle launch;
+        // two CTAs per SM walk the chunks
+        const unsigned rgrid = (unsigned)umin(grid, (uint64_t)ctx->num_sms * 2);
+        if (ts) chunk_pack_run_kernel<true><<<rgrid, 256, smem, ctx->stream>>>(a, payload ? 1 : 0);
+        else chunk_pack_run_kernel<false><<<rgrid, 256, 0, ctx->stream>>>(a, payload ? 1 : 0);
     } else {
         chunk_pack_kernel<SRC, true, false><<<(unsigned)grid, 256, 0, ctx->stream>>>(a);
     }

@@ -689,6 +689,7 @@ __global__ void __launch_bounds__(kWarps * 32) inflate_fast_kernel(
         for (uint64_t c = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; c < nchunks;
              c += (uint64_t)gridDim.x * blockDim.x)
             redo[c] = 1;
+        if (blockIdx.x == 0 && threadIdx.x == 0 && nchunks) atomicAdd(&st->pad[1], 1ull);
         return;
     }
     {

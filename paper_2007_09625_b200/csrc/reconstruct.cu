@@ -1364,6 +1364,9 @@ int launch_reconstruct(sdqz_ctx* ctx, const uint16_t* codes, const uint64_t* den
     if (!work) return rc;
     uint64_t nblocks = g.nblk[0] * g.nblk[1] * g.nblk[2];
     uint64_t grid = ceil_div(nblocks, 128);
+    // flagged-blocks-only replay: usually nothing to do (the kernel exits on
+    // the status word), so one CTA per SM bounds the idle launch cost
+    if (fast && grid > (uint64_t)ctx->num_sms) grid = ctx->num_sms;
     if (grid > (uint64_t)max_grid) grid = max_grid;
     if (grid < 1) grid = 1;
     int only = fast ? 1 : 0;
