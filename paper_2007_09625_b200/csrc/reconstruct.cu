@@ -28,6 +28,7 @@ namespace {
 constexpr int kThreads = 256;
 constexpr int kWarpsPerCta = kThreads / 32;
 constexpr double kExact = 1099511627776.0;   // 2^40
+constexpr uint64_t kSlotPts = 512;            // per-thread replay slot (largest fast block shape)
 
 struct Geo {
     int nd;
@@ -1133,14 +1134,19 @@ __global__ void rq_generic_kernel(const uint16_t* __restrict__ codes,
         uint64_t st0 = g.nd > 0 ? g.stride[0] : 1, st1 = g.nd > 1 ? g.stride[1] : 1,
                  st2 = g.nd > 2 ? g.stride[2] : 1;
         uint64_t base = o[0] * st0 + (g.nd > 1 ? o[1] * st1 : 0) + (g.nd > 2 ? o[2] * st2 : 0);
-        auto at = [&](uint64_t a, uint64_t bb, uint64_t c) { return base + a * st0 + bb * st1 + c * st2; };
+        auto gat = [&](uint64_t a, uint64_t bb, uint64_t c) { return base + a * st0 + bb * st1 + c * st2; };
+        // work: the whole-field array (all blocks), or this thread's block-sized
+        // slot when only flagged blocks of a <= 512-point shape are replayed
+        const uint64_t wbase = only_flagged ? (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) * kSlotPts : 0;
+        auto at = [&](uint64_t a, uint64_t bb, uint64_t c) {
+            return only_flagged ? wbase + (a * e[1] + bb) * e[2] + c : gat(a, bb, c);
+        };
         // residuals
         for (uint64_t a = 0; a < e[0]; a++)
             for (uint64_t bb = 0; bb < e[1]; bb++)
                 for (uint64_t c = 0; c < e[2]; c++) {
-                    uint64_t i = at(a, bb, c);
-                    uint32_t code = codes[i];
-                    work[i] = code == 0 ? 0.0 : __dsub_rn((double)code, r);
+                    const uint32_t code = codes[gat(a, bb, c)];
+                    work[at(a, bb, c)] = code == 0 ? 0.0 : __dsub_rn((double)code, r);
                 }
         // cumsum along block axis 0, then 1, then 2 (dualquant.py:215-217)
         for (uint64_t bb = 0; bb < e[1]; bb++)
@@ -1161,10 +1167,10 @@ __global__ void rq_generic_kernel(const uint16_t* __restrict__ codes,
         for (uint64_t a = 0; a < e[0]; a++)
             for (uint64_t bb = 0; bb < e[1]; bb++)
                 for (uint64_t c = 0; c < e[2]; c++) {
-                    uint64_t i = at(a, bb, c);
-                    if (codes[i] != 0) continue;
-                    double v = __longlong_as_double((long long)dense[i]);
-                    double d = __dsub_rn(v, work[i]);
+                    const uint64_t gi = gat(a, bb, c);
+                    if (codes[gi] != 0) continue;
+                    double v = __longlong_as_double((long long)dense[gi]);
+                    double d = __dsub_rn(v, work[at(a, bb, c)]);
                     for (uint64_t a2 = a; a2 < e[0]; a2++)
                         for (uint64_t b2 = bb; b2 < e[1]; b2++)
                             for (uint64_t c2 = c; c2 < e[2]; c2++) {
@@ -1175,10 +1181,10 @@ __global__ void rq_generic_kernel(const uint16_t* __restrict__ codes,
         for (uint64_t a = 0; a < e[0]; a++)
             for (uint64_t bb = 0; bb < e[1]; bb++)
                 for (uint64_t c = 0; c < e[2]; c++) {
-                    uint64_t i = at(a, bb, c);
-                    double v = __dmul_rn(work[i], two_eb);
-                    if (OUTK == 0) ((float*)out)[i] = __double2float_rn(v);
-                    else ((double*)out)[i] = v;
+                    const uint64_t gi = gat(a, bb, c);
+                    double v = __dmul_rn(work[at(a, bb, c)], two_eb);
+                    if (OUTK == 0) ((float*)out)[gi] = __double2float_rn(v);
+                    else ((double*)out)[gi] = v;
                 }
     }
 }
@@ -1257,11 +1263,11 @@ int launch_reconstruct_1d_records(sdqz_ctx* ctx, const uint16_t* codes, const vo
         rq1d_rec_kernel<1><<<(unsigned)grid, kThreads, 0, ctx->stream>>>(codes, rec, start, k, blockflag, n, cap,
                                                                        two_eb, out, ctx->d_status);
     SDQZ_LAUNCHED_NAMED(ctx, "rq1d_rec_kernel");
-    double* work = scratch_as<double>(ctx, S_WORK, n, &rc);
-    if (!work) return rc;
     uint64_t gg = ceil_div(g.nblk[0], 128);
     if (gg > (uint64_t)ctx->num_sms) gg = ctx->num_sms;
     if (gg < 1) gg = 1;
+    double* work = scratch_as<double>(ctx, S_WORK, gg * 128 * kSlotPts, &rc);
+    if (!work) return rc;
     if (out_kind == 0)
         rq_generic_kernel<0><<<(unsigned)gg, 128, 0, ctx->stream>>>(codes, (const unsigned long long*)dense, blockflag, 1,
                                                                   g, cap, two_eb, work, out, ctx->d_status);
@@ -1360,8 +1366,6 @@ int launch_reconstruct(sdqz_ctx* ctx, const uint16_t* codes, const uint64_t* den
         else SDQZ_LAUNCHED_NAMED(ctx, vec1d ? "rq1d_vec_kernel" : "rq1d_kernel");
         if (!any_slow) return SDQZ_OK;
     }
-    double* work = scratch_as<double>(ctx, S_WORK, n, &rc);
-    if (!work) return rc;
     uint64_t nblocks = g.nblk[0] * g.nblk[1] * g.nblk[2];
     uint64_t grid = ceil_div(nblocks, 128);
     // flagged-blocks-only replay: usually nothing to do (the kernel exits on
@@ -1369,6 +1373,9 @@ int launch_reconstruct(sdqz_ctx* ctx, const uint16_t* codes, const uint64_t* den
     if (fast && grid > (uint64_t)ctx->num_sms) grid = ctx->num_sms;
     if (grid > (uint64_t)max_grid) grid = max_grid;
     if (grid < 1) grid = 1;
+    // whole-field fp64 scratch for generic shapes; per-thread block slots otherwise
+    double* work = scratch_as<double>(ctx, S_WORK, fast ? grid * 128 * kSlotPts : n, &rc);
+    if (!work) return rc;
     int only = fast ? 1 : 0;
     if (out_kind == 0)
         rq_generic_kernel<0><<<(unsigned)grid, 128, 0, ctx->stream>>>(codes, dn, blockflag, only, g, cap,
