@@ -40,7 +40,7 @@ namespace {
 constexpr int kL1 = 12;                    // table index bits
 constexpr uint32_t kL1Size = 1u << kL1;
 constexpr uint32_t kL2Max = 4096;          // second-level entries (long codes)
-constexpr uint32_t kSliceMin = 192;        // bits per lane slice (> kWin)
+constexpr uint32_t kSliceMin = 64;         // bits per lane slice (short chunks keep more lanes busy)
 constexpr uint32_t kWin = 128;             // synchronisation window (bits)
 // layout of the table block (u32 words): T1 | L2 | T3 (u64)
 constexpr uint32_t kOffL2 = kL1Size;
@@ -614,7 +614,10 @@ __device__ __forceinline__ bool decode_chunk(const Tabs& t, Rd rd, uint32_t sbit
     bool fwd = false;   // this lane's tail met the next lane's path
     if (active) {
         rd.seek(s0);
-        lane_head(t, rd, s0, s0 + kWin < s1 ? s0 + kWin : s1, k, bad, lo, hi);
+        // the head window ends >= 12 bits (one table step) before the slice end,
+        // so its last step cannot run past S (lane_rest counts exactly to S)
+        const uint32_t hend = s1 > s0 + 12 ? (s0 + kWin < s1 - 12 ? s0 + kWin : s1 - 12) : s0;
+        lane_head(t, rd, s0, hend, k, bad, lo, hi);
     }
     const unsigned long long nlo = __shfl_down_sync(kFull, lo, 1);
     const unsigned long long nhi = __shfl_down_sync(kFull, hi, 1);
