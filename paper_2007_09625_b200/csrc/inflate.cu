@@ -69,14 +69,19 @@ __device__ __forceinline__ uint32_t swz12(uint32_t w) {
     return w ^ ((h ^ (h >> 5)) & 31u);
 }
 
-// part 0: T1/T3 tables; part 1: second-level table + the fallback LUT;
+// parts 0-3: a quarter of the T1/T3 windows each; part 4: second-level table;
+// part 5: the fallback LUT;
 // part -1: everything (both parts compute the shared preliminaries)
 __device__ __forceinline__ void dtab_body(const uint64_t* __restrict__ first,
                                           const int64_t* __restrict__ offsets,
                                           const uint32_t* __restrict__ symbols, int max_bw_arg,
                                           const DevStatus* st, uint32_t* __restrict__ tab,
                                           uint32_t* __restrict__ old_lut, int part) {
-    const bool p0 = part != 1, p1 = part != 0;
+    constexpr int kT13Parts = 4;
+    // p0: T1/T3 windows [w0, w1); pl2: second-level table; plut: fallback LUT
+    const bool p0 = part < kT13Parts, pl2 = part < 0 || part == kT13Parts, plut = part < 0 || part == kT13Parts + 1;
+    const uint32_t w0 = part >= 0 && part < kT13Parts ? (uint32_t)part * (kL1Size / kT13Parts) : 0u;
+    const uint32_t w1 = part >= 0 && part < kT13Parts ? w0 + kL1Size / kT13Parts : kL1Size;
     __shared__ uint32_t pmax[kL1Size];
     __shared__ uint32_t s_one[kL1Size];   // first codeword of a 12-bit window: sym << 16 | len
     __shared__ uint16_t pbase[kL1Size];   // second-level base, 0xFFFF = none
@@ -85,7 +90,7 @@ __device__ __forceinline__ void dtab_body(const uint64_t* __restrict__ first,
     const int mx = max_bw_arg > 0 ? max_bw_arg : (int)st->max_bw;
     if (mx < 1 || mx > kMaxBw) return;
     if (mx > 32) {   // 64-bit codes: only the sequential decoder's table (lut_kernel's rule)
-        if (!old_lut || !p1) return;
+        if (!old_lut || !plut) return;
         const long long ns = offsets[mx + 1];
         for (uint32_t i = threadIdx.x; i < (1u << kLutBits); i += blockDim.x) {
             uint32_t e = 0;
@@ -116,7 +121,7 @@ __device__ __forceinline__ void dtab_body(const uint64_t* __restrict__ first,
     for (int b = threadIdx.x; b < 34; b += blockDim.x) s_first[b] = b <= mx ? first[b] : 0;
     for (int b = threadIdx.x; b < 35; b += blockDim.x) s_off[b] = b <= mx + 1 ? offsets[b] : offsets[mx + 1];
     for (uint32_t i = threadIdx.x; i < kL1Size; i += blockDim.x) pmax[i] = 0;
-    if (p1)
+    if (pl2)
         for (uint32_t i = threadIdx.x; i < kL2Max; i += blockDim.x) tab[kOffL2 + i] = kLongInvalid;
     __syncthreads();
     const long long nsym = s_off[mx + 1];
@@ -181,7 +186,7 @@ __device__ __forceinline__ void dtab_body(const uint64_t* __restrict__ first,
     }
     __syncthreads();
     // the sequential fallback decoder's table (huffman.cu lut_kernel format)
-    if (old_lut && p1) {
+    if (old_lut && plut) {
         const int lb = mx < kLutBits ? mx : kLutBits;
         for (uint32_t i = threadIdx.x; i < (1u << kLutBits); i += blockDim.x) {
             uint32_t e = 0;
@@ -206,7 +211,7 @@ __device__ __forceinline__ void dtab_body(const uint64_t* __restrict__ first,
     }
     __syncthreads();
     // T1 / T3: greedy decode of each 12-bit window, one table lookup per codeword
-    for (uint32_t i = threadIdx.x; p0 && i < kL1Size; i += blockDim.x) {
+    for (uint32_t i = w0 + threadIdx.x; p0 && i < w1; i += blockDim.x) {
         uint32_t o = 0, m = 0, mask = 0, zeros = 0, sym[3] = {0, 0, 0}, cum[3] = {0, 0, 0};
         while (o < (uint32_t)kL1) {
             const uint32_t one = s_one[swz12((i << o) & (kL1Size - 1))];
@@ -245,7 +250,7 @@ __device__ __forceinline__ void dtab_body(const uint64_t* __restrict__ first,
         tab[kOffT3 + 2 * i + 1] = (uint32_t)(t3 >> 32);
     }
     // second-level entries
-    for (long long i = lo + threadIdx.x; p1 && i < nsym; i += blockDim.x) {
+    for (long long i = lo + threadIdx.x; pl2 && i < nsym; i += blockDim.x) {
         int b = kL1 + 1;
         while (b < mx && i >= s_off[b + 1]) b++;
         const unsigned long long code = s_first[b] + (unsigned long long)(i - s_off[b]);
@@ -280,7 +285,7 @@ __global__ void __cluster_dims__(kScanCtas, 1, 1) __launch_bounds__(1024) decode
         for (uint64_t i = blockIdx.x * 1024ull + threadIdx.x; i < C; i += kScanCtas * 1024ull) redo[i] = 0;
         if (blockIdx.x == 0 && threadIdx.x == 0) *counter = 0;
         cluster_chunk_scan(blockIdx.x, chunk_bits, nullptr, C, byte_off, nullptr, ~0ull, false, 0, st);
-    } else if (blockIdx.x < kScanCtas + 2) {   // cluster 1: decode tables
+    } else if (blockIdx.x < kScanCtas + 6) {   // cluster 1: decode tables (4 x T1/T3 quarter | L2 | LUT)
         dtab_body(first, offsets, symbols, max_bw_arg, st, tab, old_lut, (int)(blockIdx.x - kScanCtas));
     }
 }
