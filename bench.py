@@ -404,7 +404,8 @@ def ours_arm(args, cfg, world, rank, local_rank):
                 if (ab := algorithmic_bytes(kname, n, K, C, P)) and kms > 0
                 # a label whose launch skipped the work (e.g. the 64-bit-unit packer
                 # when units are 32 bits, a 1D tail kernel) is not a roofline entry
-                and ab / (kms / 1e3) / 1e9 <= 1.2 * peak},
+                and ab / (kms / 1e3) / 1e9 <= 1.2 * peak
+                and not (kname.startswith("chunk_pack_kernel") and int(hdr.unit_width) == 32)},
             "e2e": e2e,
             "gpu_launches": launches,
             "graph_replays": replays,
