@@ -590,3 +590,39 @@ class TestQualityKernel:
             assert r.error is None and r.max_abs_err == mx
             assert r.psnr_db == pytest.approx(20 * np.log10(rg / rmse), abs=1e-9)
             assert r.cr == pytest.approx(f.nbytes / len(blob))
+
+
+class TestLargeChunks:
+    """Chunks larger than the decoder's shared staging buffer (~4 KB) are read
+    from global memory (GlobalReader4): HACC- and large-config-sized chunks."""
+
+    @pytest.mark.parametrize("chunk", [16384, 65536])
+    def test_big_chunks(self, chunk):
+        rng = np.random.default_rng(chunk)
+        f = np.cumsum(rng.normal(0, 1, 400_000)).astype(np.float32)
+        kw = dict(eb=0.02, mode="abs", chunk_size=chunk)
+        blob = S.compress(f, **kw)
+        assert blob == O.compress(f, **kw)
+        h = S.parse_header(blob)
+        assert h.payload_bytes / h.n_chunks > 8192
+        assert np.array_equal(bits(S.decompress(blob)), bits(O.decompress(blob)))
+
+    def test_big_chunk_bitflips(self):
+        rng = np.random.default_rng(99)
+        f = np.cumsum(rng.normal(0, 1, 200_000)).astype(np.float32)
+        blob = bytearray(S.compress(f, eb=0.02, mode="abs", chunk_size=65536))
+        h = S.parse_header(bytes(blob))
+        p0 = len(blob) - h.payload_bytes
+        for pos in (p0 + 100, p0 + h.payload_bytes // 2, len(blob) - 50):
+            b2 = bytearray(blob)
+            b2[pos] ^= 0x10
+            try:
+                want, werr = O.decompress(bytes(b2)), None
+            except O.OracleError as e:
+                want, werr = None, e
+            if werr is None:
+                assert np.array_equal(bits(S.decompress(bytes(b2))), bits(want))
+            else:
+                with pytest.raises(S.SdqzError) as ei:
+                    S.decompress(bytes(b2))
+                assert str(ei.value) == str(werr)
