@@ -341,10 +341,6 @@ __device__ __forceinline__ void rq_store8(void* __restrict__ out, uint64_t rb, c
     }
 }
 
-__device__ __forceinline__ bool has_zero16(uint32_t w) {   // either 16-bit half == 0
-    return ((w - 0x00010001u) & ~w & 0x80008000u) != 0;
-}
-
 // One half-row (4 points) of a block row whose other half lives in the
 // neighbouring lane.  Computed with a zero x-carry, then corrected: the true
 // x-prefix adds the left half's final H (`carry`) to every point before this
@@ -953,7 +949,7 @@ __global__ void __launch_bounds__(kThreads) rq1d_rec_kernel(const uint16_t* __re
                                                             void* __restrict__ out, DevStatus* st) {
     __shared__ double s_vals[kWarpsPerCta][kVals];
     const int r = (int)(cap >> 1);
-    const uint32_t lane = lane_id(), lt = (1u << lane) - 1u;
+    const uint32_t lane = lane_id();
     double* const vals = s_vals[threadIdx.x >> 5];
     const uint64_t ntask = ceil_div(n, 1024);
     const bool any_slow = (st->flags & F_OUT_SLOW) != 0;
