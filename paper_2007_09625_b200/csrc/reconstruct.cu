@@ -341,6 +341,10 @@ __device__ __forceinline__ void rq_store8(void* __restrict__ out, uint64_t rb, c
     }
 }
 
+__device__ __forceinline__ __attribute__((unused)) bool has_zero16(uint32_t w) {   // either 16-bit half == 0
+    return ((w - 0x00010001u) & ~w & 0x80008000u) != 0;
+}
+
 // One half-row (4 points) of a block row whose other half lives in the
 // neighbouring lane.  Computed with a zero x-carry, then corrected: the true
 // x-prefix adds the left half's final H (`carry`) to every point before this
