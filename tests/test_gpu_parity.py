@@ -626,3 +626,21 @@ class TestLargeChunks:
                 with pytest.raises(S.SdqzError) as ei:
                     S.decompress(bytes(b2))
                 assert str(ei.value) == str(werr)
+
+
+class TestHostStaging:
+    """Host-buffer copies through the pinned staging window (256 MB): a pageable
+    field larger than the window uploads in two windows and gives the same
+    archive as the device-resident field; the archive round-trips through bytes."""
+
+    def test_pageable_upload_two_windows(self):
+        n = 80_000_000                                   # 320 MB fp32 > one staging window
+        x = np.linspace(0.0, 40.0, n, dtype=np.float64)
+        f = (np.sin(x) + 0.25 * np.sin(7.3 * x)).astype(np.float32)
+        blob = S.compress(f, eb=1e-3, mode="abs")        # pageable numpy -> sdqz_upload
+        t = torch.from_numpy(f).cuda()
+        dev = S.compress_device(t, eb=1e-3, mode="abs")
+        assert blob == dev.to_bytes()
+        out = S.decompress(blob)
+        err = np.abs(out.astype(np.float64) - f.astype(np.float64)).max()
+        assert err <= 1e-3 * (1 + 1e-9) + 2 * np.spacing(np.float32(1.25))
