@@ -199,6 +199,18 @@ SDQZ_API int sdqz_decompress_sections(sdqz_ctx* ctx, const sdqz_header* hdr, con
                              const void* d_outliers, const uint32_t* d_chunk_bits,
                              const uint8_t* d_payload, void* d_out);
 
+/* Multi-GPU slab decompress: inflate the chunk range
+ * [c0, c0 + n_chunks) covering this rank's slab (device sections: the range's
+ * chunk bit lengths and payload bytes, zero padded by >= 64 bytes), then
+ * reconstruct the slab whose first code is `lo` codes into the range, with
+ * the slab's outlier records (indices slab-local, ascending).  Checks as
+ * decompress for the slab: decode errors, record range/order, codes[idx] == 0,
+ * zero-code count of the slab.  Replaces the per-rank pipeline.py:42-58. */
+SDQZ_API int sdqz_decompress_slab(sdqz_ctx* ctx, const sdqz_header* hdr, const uint8_t* d_bw,
+                                  const void* d_rec, uint64_t k, const uint32_t* d_chunk_bits,
+                                  uint64_t n_chunks, const uint8_t* d_payload, uint64_t payload_bytes,
+                                  uint64_t n_range, uint64_t lo, const uint64_t local_dims[3], void* d_out);
+
 #ifdef __cplusplus
 }
 #endif

@@ -86,6 +86,9 @@ _SIGS = {
     "sdqz_decompress": (c_int, [c_void_p, c_void_p, c_uint64, c_void_p]),
     "sdqz_decompress_sections": (c_int, [c_void_p, POINTER(Header), c_void_p, c_void_p,
                                          c_void_p, c_void_p, c_void_p]),
+    "sdqz_decompress_slab": (c_int, [c_void_p, POINTER(Header), c_void_p, c_void_p, c_uint64, c_void_p,
+                                     c_uint64, c_void_p, c_uint64, c_uint64, c_uint64,
+                                     POINTER(c_uint64), c_void_p]),
 }
 
 EXPORTS = tuple(_SIGS)

@@ -1122,6 +1122,60 @@ int sdqz_decompress_sections(sdqz_ctx* ctx, const sdqz_header* hdr, const uint8_
                            d_out);
 }
 
+int sdqz_decompress_slab(sdqz_ctx* ctx, const sdqz_header* hdr, const uint8_t* d_bw, const void* d_rec,
+                         uint64_t k, const uint32_t* d_chunk_bits, uint64_t n_chunks, const uint8_t* d_payload,
+                         uint64_t payload_bytes, uint64_t n_range, uint64_t lo, const uint64_t local_dims[3],
+                         void* d_out) {
+    int rc = SDQZ_OK;
+    const uint32_t cap = hdr->cap;
+    uint64_t ldims[3] = {1, 1, 1};
+    uint64_t n_local = 1, nblocks = 1;
+    uint32_t block[3] = {1, 1, 1};
+    for (int a = 0; a < hdr->ndims; a++) {
+        ldims[a] = local_dims[a];
+        block[a] = hdr->block[a] ? hdr->block[a] : 1;
+        n_local *= ldims[a];
+        nblocks *= ceil_div(ldims[a], block[a]);
+    }
+    if (lo + n_local > n_range) return set_error(ctx, SDQZ_EINVAL, "slab outside the chunk range");
+    if (n_local == 0) return SDQZ_OK;
+    BookDev book;
+    if ((rc = book_tables(ctx, cap, &book))) return rc;
+    uint16_t* codes = scratch_as<uint16_t>(ctx, S_CODES, n_range + 64, &rc);
+    uint64_t* dense = scratch_as<uint64_t>(ctx, S_DENSE, n_local, &rc);
+    uint8_t* bflag = scratch_as<uint8_t>(ctx, S_BLOCKFLAG, nblocks, &rc);
+    if (!codes || !dense || !bflag) return rc;
+    if ((rc = reset_status_eb(ctx, hdr->eb_resolved, true))) return rc;
+    SDQZ_CUDA(ctx, cudaMemsetAsync(bflag, 0, nblocks, ctx->stream));
+    if ((rc = launch_codebook(ctx, nullptr, const_cast<uint8_t*>(d_bw), cap, book, false, true, true))) return rc;
+    if (n_chunks &&
+        (rc = launch_inflate(ctx, d_payload, payload_bytes, d_chunk_bits, n_chunks, hdr->chunk_size, book.first,
+                             book.offsets, book.symbols, book.lut, -1, n_range, codes, false)))
+        return rc;
+    // zero codes of the slab alone (the decoder counted the whole chunk range)
+    SDQZ_CUDA(ctx, cudaMemsetAsync(&ctx->d_status->n_zero, 0, sizeof(unsigned long long), ctx->stream));
+    if ((rc = launch_count_zero(ctx, codes + lo, n_local))) return rc;
+    if ((rc = launch_outlier_scatter(ctx, d_rec, nullptr, nullptr, k, n_local, codes + lo, hdr->ndims, ldims,
+                                     block, dense, bflag, true)))
+        return rc;
+    if ((rc = launch_reconstruct(ctx, codes + lo, dense, bflag, true, hdr->ndims, ldims, block, cap,
+                                 2.0 * hdr->eb_resolved, d_out, hdr->dtype_code)))
+        return rc;
+    if ((rc = enqueue_status_copy(ctx))) return rc;
+    if ((rc = sync_status(ctx))) return rc;
+    const DevStatus& s = *ctx->h_status;
+    if ((rc = table_error(ctx, s.flags, true))) return rc;
+    if (s.flags & F_OUT_RANGE) return set_error(ctx, SDQZ_EFORMAT, "outlier index out of range");
+    if (s.flags & F_OUT_ORDER) return set_error(ctx, SDQZ_EFORMAT, "outlier indices not strictly ascending");
+    if ((rc = decode_error(ctx))) return rc;
+    if (s.flags & F_OUT_NONZERO)
+        return set_error(ctx, SDQZ_ECORRUPT, "outlier entry at a position whose code is not 0");
+    if (s.n_zero != k)
+        return set_error(ctx, SDQZ_ECORRUPT, fmt("%llu zero codes but %llu outlier entries", s.n_zero,
+                                                 (unsigned long long)k));
+    return SDQZ_OK;
+}
+
 int sdqz_decompress(sdqz_ctx* ctx, const uint8_t* h, uint64_t len, void* d_out) {
     int rc = SDQZ_OK;
     sdqz_header hdr;

@@ -30,6 +30,7 @@ drive it with a gloo group and a checker backend.
 
 from __future__ import annotations
 
+import ctypes
 import math
 from dataclasses import dataclass
 
@@ -125,6 +126,38 @@ class DeviceShardOps:
         from .huffman import DeflatedStream, canonize, inflate
         _, rb = canonize(bitwidths)
         return inflate(DeflatedStream(chunk, chunk_bits, payload.tobytes()), rb, n_codes)
+
+    def decompress_slab(self, h: ArchiveHeader, bw: np.ndarray, rec: np.ndarray, bits: np.ndarray,
+                        payload: np.ndarray, n_range: int, lo: int, local_dims) -> np.ndarray:
+        """Device-resident slab decompress (sdqz_decompress_slab): the chunk range's
+        sections go to the GPU once; decode tables, the warp-parallel decoder and
+        the reconstruct run there, and only the slab comes back."""
+        torch = _device._torch()
+        ch = _lib.Header()
+        ch.dtype_code, ch.ndims, ch.eb_mode, ch.unit_width = h.dtype_code, h.ndims, h.eb_mode, h.unit_width
+        for a in range(3):
+            ch.dims[a] = h.dims[a]
+            ch.block[a] = h.block_shape[a]
+        ch.eb_resolved, ch.eb_specified, ch.cap, ch.chunk_size = (h.eb_resolved, h.eb_specified, h.cap,
+                                                                  h.chunk_size)
+        ch.n_outliers, ch.n_chunks, ch.payload_bytes = len(rec), len(bits), len(payload)
+        bwp = np.zeros(h.cap + 16, np.uint8)
+        bwp[: h.cap] = bw
+        r = np.empty((max(len(rec), 1), 2), np.uint64)
+        r[: len(rec), 0] = rec["index"]
+        r[: len(rec), 1] = rec["value"].view(np.uint64)
+        pay = np.zeros(len(payload) + 64, np.uint8)
+        pay[: len(payload)] = payload
+        d_bw = _device.upload(bwp)
+        d_rec = _device.upload(r.reshape(-1).view(np.int64))
+        d_bits = _device.upload(np.concatenate([bits.astype(np.uint32), np.zeros(4, np.uint32)]).view(np.int32))
+        d_pay = _device.upload(pay)
+        n = math.prod(local_dims)
+        out = _device.empty(n, torch.float32 if h.dtype_code == 0 else torch.float64)
+        _lib.context().call("sdqz_decompress_slab", ctypes.byref(ch), _lib.ptr(d_bw), _lib.ptr(d_rec),
+                            len(rec), _lib.ptr(d_bits), len(bits), _lib.ptr(d_pay), len(payload),
+                            int(n_range), int(lo), _lib.dims3(local_dims), _lib.ptr(out))
+        return _device.download(out, n).reshape(local_dims)
 
     def reconstruct(self, codes: np.ndarray, idx: np.ndarray, vals: np.ndarray, local_dims,
                     cfg: QuantConfig, dtype) -> np.ndarray:
@@ -362,11 +395,16 @@ def decompress_sharded(blob, *, group=None, rows: list[int] | None = None, ops=N
     c0, c1 = o // cs, -(-(o + n_local) // cs)
     payload = np.frombuffer(buf, np.uint8, int(offs[c1] - offs[c0]), p + int(offs[c0]))
     n_range = min(c1 * cs, n_global) - c0 * cs
-    codes = ops.inflate(payload, bits[c0:c1].copy(), cs, n_range, bw.copy())
     lo = o - c0 * cs
-    codes = np.asarray(codes)[lo: lo + n_local]
     idx = rec["index"]
     a, b = np.searchsorted(idx, o), np.searchsorted(idx, o + n_local)
+    if hasattr(ops, "decompress_slab"):   # device backend: one device-resident pass
+        srec = np.empty(b - a, _RECORD)
+        srec["index"] = idx[a:b] - np.uint64(o)
+        srec["value"] = rec["value"][a:b]
+        return ops.decompress_slab(h, bw.copy(), srec, bits[c0:c1].copy(), payload, n_range, lo, local_dims)
+    codes = ops.inflate(payload, bits[c0:c1].copy(), cs, n_range, bw.copy())
+    codes = np.asarray(codes)[lo: lo + n_local]
     return ops.reconstruct(codes, (idx[a:b] - np.uint64(o)).astype(np.uint64),
                            rec["value"][a:b].astype(np.float64), local_dims, cfg, h.np_dtype)
 

@@ -172,3 +172,20 @@ def test_sharded_device_two_ranks_one_gpu():
     assert blobs[0] == ref and blobs[1] == ref
     got = np.concatenate(slabs, axis=0)
     assert np.array_equal(got.view(np.uint32), O.decompress(ref).view(np.uint32))
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("name,dims,rows,kw", CASES, ids=[c[0] for c in CASES])
+def test_sharded_device_cases(name, dims, rows, kw):
+    """Every protocol case through the device backend (sdqz_decompress_slab):
+    straddling chunks, a chunk spanning three slabs, an empty slab, outliers."""
+    data = _smooth(dims)
+    if name.startswith("3d-cap64"):
+        data = data + np.random.default_rng(3).normal(0, 0.3, data.shape).astype(np.float32)
+    ref = O.compress(data, dims, **kw)
+    blobs, slabs = run_sharded((data.reshape(-1), dims, rows, kw), len(rows), backend="device")
+    for b in blobs:
+        assert b == ref
+    dec = O.decompress(ref)
+    got = np.concatenate([s.reshape((-1,) + tuple(dims[1:])) for s in slabs], axis=0)
+    assert np.array_equal(got.reshape(dec.shape).view(np.uint32), dec.view(np.uint32))
