@@ -679,11 +679,14 @@ __device__ __forceinline__ bool decode_chunk(const Tabs& t, Rd rd, uint32_t sbit
     return true;
 }
 
-constexpr int kWarps = 32;            // one CTA per SM shares one copy of the tables
+// one CTA per SM shares one copy of the tables: 32 warps, or 24 for chunks of
+// >= 16384 codes (longer lane spans: the register budget of 1024-thread CTAs
+// is the limit there, and fewer warps leave more staging per warp)
 constexpr uint32_t kRingStride = 40;   // 16 u16 slots per lane + 8 bytes: 2-way bank conflicts
 
 // dynamic shared memory: tables (kTabWords) | per-lane rings | one staging
 // buffer of `stage_words` words per warp
+template <int kWarps>
 __global__ void __launch_bounds__(kWarps * 32) inflate_fast_kernel(
     const uint8_t* __restrict__ payload, uint64_t nwords, const uint32_t* __restrict__ chunk_bits,
     const unsigned long long* __restrict__ byte_off, uint64_t nchunks, uint32_t chunk, uint64_t n,
@@ -798,14 +801,11 @@ int launch_decode_prep(sdqz_ctx* ctx, const uint64_t* first, const int64_t* offs
     return SDQZ_OK;
 }
 
-int launch_inflate_fast(sdqz_ctx* ctx, const uint8_t* payload, uint64_t nwords,
-                        const uint32_t* chunk_bits, const unsigned long long* byte_off,
-                        uint64_t n_chunks, uint32_t chunk, uint64_t n, const uint64_t* first,
-                        const int64_t* offsets, const uint32_t* symbols, const uint32_t* tab,
-                        int max_bw, uint16_t* codes, uint8_t* redo) {
-    int rc = SDQZ_OK;
-    unsigned int* counter = scratch_as<unsigned int>(ctx, S_COUNTER, 4, &rc);   // cleared by the prep kernel
-    if (!counter) return rc;
+template <int kWarps>
+void launch_inflate_fast_w(sdqz_ctx* ctx, const uint8_t* payload, uint64_t nwords, const uint32_t* chunk_bits,
+                           const unsigned long long* byte_off, uint64_t n_chunks, uint32_t chunk, uint64_t n,
+                           const uint64_t* first, const int64_t* offsets, const uint32_t* symbols,
+                           const uint32_t* tab, int max_bw, uint16_t* codes, uint8_t* redo, unsigned int* counter) {
     // per-warp staging: room for ~2x the average chunk (bigger chunks read global memory)
     const uint64_t avg = n_chunks ? (nwords * 4) / n_chunks : 0;
     const size_t fixed = (size_t)kTabWords * 4 + (size_t)kWarps * 32 * kRingStride;
@@ -817,19 +817,35 @@ int launch_inflate_fast(sdqz_ctx* ctx, const uint8_t* payload, uint64_t nwords,
     const size_t smem = fixed + (size_t)kWarps * stage_words * 4;
     static size_t attr_smem = 0;
     if (smem > attr_smem) {
-        cudaFuncSetAttribute(inflate_fast_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        cudaFuncSetAttribute(inflate_fast_kernel<kWarps>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         attr_smem = smem;
     }
     int per_sm = 1;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, inflate_fast_kernel, kWarps * 32, smem);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, inflate_fast_kernel<kWarps>, kWarps * 32, smem);
     if (per_sm < 1) per_sm = 1;
     uint64_t grid = ceil_div(n_chunks, kWarps);
     const uint64_t cap = (uint64_t)ctx->num_sms * per_sm;
     if (grid > cap) grid = cap;
     if (grid < 1) grid = 1;
-    inflate_fast_kernel<<<(unsigned)grid, kWarps * 32, smem, ctx->stream>>>(
+    inflate_fast_kernel<kWarps><<<(unsigned)grid, kWarps * 32, smem, ctx->stream>>>(
         payload, nwords, chunk_bits, byte_off, n_chunks, chunk, n, first, offsets, symbols, tab,
         max_bw, codes, redo, counter, stage_words, ctx->d_status);
+}
+
+int launch_inflate_fast(sdqz_ctx* ctx, const uint8_t* payload, uint64_t nwords,
+                        const uint32_t* chunk_bits, const unsigned long long* byte_off,
+                        uint64_t n_chunks, uint32_t chunk, uint64_t n, const uint64_t* first,
+                        const int64_t* offsets, const uint32_t* symbols, const uint32_t* tab,
+                        int max_bw, uint16_t* codes, uint8_t* redo) {
+    int rc = SDQZ_OK;
+    unsigned int* counter = scratch_as<unsigned int>(ctx, S_COUNTER, 4, &rc);   // cleared by the prep kernel
+    if (!counter) return rc;
+    if (chunk >= 16384)
+        launch_inflate_fast_w<24>(ctx, payload, nwords, chunk_bits, byte_off, n_chunks, chunk, n, first, offsets,
+                                  symbols, tab, max_bw, codes, redo, counter);
+    else
+        launch_inflate_fast_w<32>(ctx, payload, nwords, chunk_bits, byte_off, n_chunks, chunk, n, first, offsets,
+                                  symbols, tab, max_bw, codes, redo, counter);
     SDQZ_LAUNCHED_NAMED(ctx, "inflate_fast_kernel");
     return SDQZ_OK;
 }
