@@ -182,7 +182,8 @@ def reference_arm(args, cfg, world, rank):
 def cpu_baseline(data, dims, cfg):
     """Oracle port, one thread, on a bounded sample of the same field."""
     from oracle import sdqz_oracle as O
-    rows = max(1, min(dims[0], int(math.ceil(4e6 / max(1, math.prod(dims[1:]))))))
+    # up to 2.5e7 points: the whole Hurricane workload (~5-10 s of one core)
+    rows = max(1, min(dims[0], int(math.ceil(2.5e7 / max(1, math.prod(dims[1:]))))))
     sdims = (rows,) + tuple(dims[1:])
     sample = data.reshape(dims)[:rows].copy()
     t0 = time.perf_counter()
