@@ -606,15 +606,23 @@ __global__ void __launch_bounds__(256) chunk_stats_fast_kernel(DeflateArgs a) {
         uint32_t bits = 0, zeros = 0;
         uint64_t i0 = s + 8 * lane;
         if ((s & 7) == 0) {
-            for (; i0 + 8 <= e; i0 += 256) {
-                const uint4 v = __ldg(reinterpret_cast<const uint4*>(src + i0));
+            auto acc4 = [&](const uint4& v) {
                 const uint32_t wv[4] = {v.x, v.y, v.z, v.w};
 #pragma unroll
                 for (int k = 0; k < 4; k++) {
                     bits += (uint32_t)s_w[wv[k] & 0xFFFF] + (uint32_t)s_w[wv[k] >> 16];
                     if (zero_half16(wv[k])) zeros += ((wv[k] & 0xFFFF) == 0) + ((wv[k] >> 16) == 0);
                 }
+            };
+            // four 16-byte loads per lane in flight (a chunk is a few such rounds)
+            for (; i0 + 3 * 256 + 8 <= e; i0 += 4 * 256) {
+                uint4 v[4];
+#pragma unroll
+                for (int u = 0; u < 4; u++) v[u] = __ldg(reinterpret_cast<const uint4*>(src + i0 + u * 256));
+#pragma unroll
+                for (int u = 0; u < 4; u++) acc4(v[u]);
             }
+            for (; i0 + 8 <= e; i0 += 256) acc4(__ldg(reinterpret_cast<const uint4*>(src + i0)));
         }
         for (; i0 < e; i0 += 256) {   // unaligned chunk or ragged tail
 #pragma unroll
