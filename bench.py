@@ -33,13 +33,16 @@ ROOT = Path(__file__).resolve().parent
 sys.path.insert(0, str(ROOT))
 
 CONFIGS = {
-    "cesm": dict(dims=(1800, 3600), eb=1e-4, mode="valrel", desc="2D CESM-ATM-shaped 1800x3600"),
-    "hurricane": dict(dims=(100, 500, 500), eb=1e-4, mode="valrel",
+    "cesm": dict(dims=(1800, 3600), eb=1e-4, mode="valrel", golden="cesm",
+                 desc="2D CESM-ATM-shaped 1800x3600"),
+    "hurricane": dict(dims=(100, 500, 500), eb=1e-4, mode="valrel", golden="hurricane",
                       desc="3D Hurricane-Isabel-shaped 100x500x500"),
-    "hacc": dict(dims=(280953867,), eb=1e-4, mode="valrel", desc="1D HACC-shaped 280,953,867"),
-    "nyx": dict(dims=(512, 512, 512), eb=1e-4, mode="valrel", desc="3D Nyx-shaped 512^3"),
-    "large": dict(dims=(2048, 2048, 1024), eb=1e-4, mode="valrel",
-                  desc="3D 2048x2048x1024 (17.2 GB fp32)"),
+    "hacc": dict(dims=(280953867,), eb=1e-4, mode="valrel", golden="hacc",
+                 desc="1D HACC-shaped 280,953,867"),
+    "nyx": dict(dims=(512, 512, 512), eb=1e-4, mode="valrel", golden="nyx_smooth_1e-04",
+                desc="3D Nyx-shaped 512^3"),
+    "large": dict(dims=(2048, 2048, 1024), eb=1e-4, mode="valrel", golden="large",
+                  desc="3D 2048x2048x1024 (17.2 GB fp32), BASELINE.json configs[4]"),
 }
 METRIC = "compress & decompress GB/s (fp32 in)"
 L2_FLUSH_BYTES = 512 << 20
@@ -111,88 +114,136 @@ class Clocks:
 # --------------------------------------------------------------------------
 # data
 # --------------------------------------------------------------------------
-def host_field(cfg_name: str, dims, seed: int, rank: int = 0):
-    """Synthetic smooth field (reference synthetic.py profile) as a pinned host array."""
+def host_field(dims, seed: int):
+    """The reference's smooth profile (synthetic.py:25-35), bit-identical to its
+    generate_field, evaluated slab-wise on all host cores straight into pinned
+    memory (the 17.2 GB config never materialises an f64 field)."""
     import torch
+    from concurrent.futures import ThreadPoolExecutor
     from paper_2007_09625_b200 import synthetic
     n = math.prod(dims)
     pinned = torch.empty(n, dtype=torch.float32, pin_memory=True)
     arr = pinned.numpy()
-    if n <= 300_000_000:
-        arr[:] = synthetic.smooth_rows(dims, seed).astype(np.float32).reshape(-1)
-    else:   # slab-wise on the device (host f64 temporaries would not fit)
-        dev = synthetic.smooth_field_device(dims, seed, dtype=torch.float32)
-        pinned.copy_(dev.reshape(-1))
-        del dev
+    inner = math.prod(dims[1:])
+    rows = max(1, min(dims[0], (1 << 24) // max(1, inner))) if len(dims) > 1 else dims[0]
+    if len(dims) == 1:   # 1D: the whole axis at once (ufuncs release the GIL anyway)
+        arr[:] = synthetic.smooth_rows(dims, seed).astype(np.float32)
+        return arr, pinned
+
+    def fill(r0):
+        r1 = min(dims[0], r0 + rows)
+        arr[r0 * inner:r1 * inner] = synthetic.smooth_rows(dims, seed, (r0, r1)).astype(np.float32).reshape(-1)
+
+    with ThreadPoolExecutor(max_workers=min(16, os.cpu_count() or 1)) as ex:
+        list(ex.map(fill, range(0, dims[0], rows)))
     return arr, pinned
 
 
-def device_field(dims, seed: int):
-    import torch
+def golden_for(config: str):
+    """Reference archive hashes of this config (tests/golden/config_golden.json,
+    made by running the reference in the build container)."""
+    try:
+        return json.loads((ROOT / "tests" / "golden" / "config_golden.json").read_text()).get(config)
+    except (OSError, ValueError):
+        return None
+
+
+def cpu_model() -> str:
+    try:
+        for line in Path("/proc/cpuinfo").read_text().splitlines():
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
+# --------------------------------------------------------------------------
+# CPU reference path (oracle port of the reference package, oracle/sdqz_oracle.py)
+# --------------------------------------------------------------------------
+def cpu_sample(cfg, max_points: float):
+    """A bounded sample of the workload: the leading whole blocks of the field
+    (rows along axis 0, then columns along axis 1 for 3D), compressed with the
+    FULL field's resolved bound (abs mode) and chunk size so it quantizes and
+    chunks exactly as the same points do inside the full-field archive."""
     from paper_2007_09625_b200 import synthetic
-    rows = dims[0]
-    step = max(1, int(2**28 // max(1, math.prod(dims[1:]))))   # <= 2 GiB f64 temporaries
-    out = torch.empty(dims, dtype=torch.float32, device="cuda")
-    for r0 in range(0, rows, step):
-        r1 = min(rows, r0 + step)
-        out[r0:r1] = synthetic.smooth_field_device(dims, seed, rows=(r0, r1), dtype=torch.float32)
-    return out.reshape(-1)
+    from paper_2007_09625_b200.huffman import default_chunk_size
+    dims = cfg["dims"]
+    g = golden_for(cfg["golden"]) or {}
+    eb = g.get("eb_resolved")
+    if eb is None:
+        f = synthetic.smooth_rows(dims, 1) if math.prod(dims) < 5e8 else None
+        eb = cfg["eb"] * float(np.float32(f.max()) - np.float32(f.min())) if f is not None else cfg["eb"]
+    b0 = {1: 32, 2: 16, 3: 8}[len(dims)]
+    if len(dims) == 1:
+        m = int(min(dims[0], max(b0, max_points // b0 * b0)))
+        sdims = (m,)
+        data = synthetic.smooth_rows(dims, 1, (0, m))
+    else:
+        inner = math.prod(dims[1:])
+        rows = int(min(dims[0], max(b0, (max_points // inner) // b0 * b0)))
+        cols = dims[1]
+        if rows * inner > 1.5 * max_points and len(dims) == 3:   # one block row, fewer columns
+            cols = int(min(dims[1], max(b0, (max_points // (rows * dims[2])) // b0 * b0)))
+        sdims = (rows, cols) + tuple(dims[2:])
+        data = synthetic.smooth_rows(dims, 1, (0, rows))[:, :cols]
+    data = np.ascontiguousarray(data, dtype=np.float32)
+    chunk = default_chunk_size(math.prod(dims))
+    desc = (f"leading {'x'.join(map(str, sdims))} block-aligned box of the {cfg['desc']} field "
+            f"({data.size} points), abs eb = the full field's resolved bound {eb:.6g}, chunk {chunk}; "
+            f"throughput is per point, so it extrapolates linearly to the full field")
+    return data, sdims, eb, chunk, desc
 
 
-# --------------------------------------------------------------------------
-# reference arm (CPU)
-# --------------------------------------------------------------------------
+def time_cpu(data, sdims, eb, chunk, workers: int, steps: int = 1):
+    from oracle import sdqz_oracle as O
+    t0 = time.perf_counter()
+    for _ in range(steps):
+        blob = O.compress(data, sdims, eb=eb, mode="abs", chunk_size=chunk)
+        O.decompress(blob, workers=workers)
+    return (time.perf_counter() - t0) / steps
+
+
 def reference_arm(args, cfg, world, rank):
+    """The CPU reference path on the host cores (the oracle port: the reference
+    is pure Python + numpy and is not importable on the GPU box)."""
     if rank != 0:
         return 0
-    from oracle import sdqz_oracle as O
-    from paper_2007_09625_b200 import synthetic
-    dims = cfg["dims"]
-    # bounded sample: leading rows of the same field (~6e6 points)
-    rows = max(1, min(dims[0], int(math.ceil(6e6 / max(1, math.prod(dims[1:]))))))
-    sdims = (rows,) + tuple(dims[1:])
-    data = synthetic.smooth_rows(dims, 1, (0, rows)).astype(np.float32)
-    if len(dims) == 1:
-        data = data[:rows]
-    n = data.size
+    data, sdims, eb, chunk, desc = cpu_sample(cfg, 2e6)
     cores = os.cpu_count() or 1
-    for _ in range(args.warmup):
-        O.decompress(O.compress(data, sdims, eb=cfg["eb"], mode=cfg["mode"]), workers=cores)
-    t0 = time.perf_counter()
-    for _ in range(args.steps):
-        blob = O.compress(data, sdims, eb=cfg["eb"], mode=cfg["mode"])
-        O.decompress(blob, workers=cores)
-    dt = time.perf_counter() - t0
-    value = 4 * n * args.steps / dt / 1e9
-    sample = f"rows [0,{rows}) of the {cfg['desc']} field ({n} points) per step"
+    # the reference's `workers` threads only its decode (numpy holds the GIL
+    # elsewhere) and can be slower than one thread: warm up both, time the faster
+    w1 = time_cpu(data, sdims, eb, chunk, 1, steps=max(1, args.warmup // 2))
+    wn = time_cpu(data, sdims, eb, chunk, cores, steps=max(1, args.warmup - args.warmup // 2))
+    workers = cores if wn < w1 else 1
+    dt = time_cpu(data, sdims, eb, chunk, workers, steps=args.steps) * args.steps
+    value = 4 * data.size * args.steps / dt / 1e9
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": "GB/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": dt / args.steps * 1e3,
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-        "data": "synthetic", "config": {"workload": args.config, "dims": list(dims),
-                                        "eb": cfg["eb"], "mode": cfg["mode"], "sample_dims": list(sdims)},
-        "cpu_baseline": {"value": value, "unit": "GB/s", "cores": cores, "kind": "port",
-                         "sample": sample},
+        "higher_is_better": True, "scaling": "strong" if args.config == "large" else "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": args.config, "dims": list(cfg["dims"]), "eb": cfg["eb"],
+                   "mode": cfg["mode"], "sample_dims": list(sdims)},
+        "cpu_baseline": {"value": value, "unit": "GB/s", "cores": workers, "kind": "port",
+                         "cpu": cpu_model(), "host_cores": cores, "workers": workers,
+                         "workers_choice": f"faster of workers=1 ({w1:.2f} s/step) and "
+                                           f"workers={cores} ({wn:.2f} s/step) in warm-up",
+                         "sample": desc + " (per step)"},
         "e2e": {"value": value, "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
     return 0
 
 
-def cpu_baseline(data, dims, cfg):
-    """Oracle port, one thread, on a bounded sample of the same field."""
-    from oracle import sdqz_oracle as O
-    # up to 2.5e7 points: the whole Hurricane workload (~5-10 s of one core)
-    rows = max(1, min(dims[0], int(math.ceil(2.5e7 / max(1, math.prod(dims[1:]))))))
-    sdims = (rows,) + tuple(dims[1:])
-    sample = data.reshape(dims)[:rows].copy()
-    t0 = time.perf_counter()
-    blob = O.compress(sample, sdims, eb=cfg["eb"], mode=cfg["mode"])
-    O.decompress(blob, workers=1)
-    dt = time.perf_counter() - t0
-    return {"value": 4 * sample.size / dt / 1e9, "unit": "GB/s", "cores": 1, "kind": "port",
-            "sample": f"rows [0,{rows}) of the field ({sample.size} points), compress+decompress, "
-                      f"oracle/sdqz_oracle.py (numpy port of the reference), 1 step"}
+def cpu_baseline(cfg):
+    """Oracle port on one core (workers=1), a ~10-20 s bounded sample."""
+    data, sdims, eb, chunk, desc = cpu_sample(cfg, 8e6)
+    dt = time_cpu(data, sdims, eb, chunk, 1)
+    return {"value": 4 * data.size / dt / 1e9, "unit": "GB/s", "cores": 1, "kind": "port",
+            "cpu": cpu_model(), "workers": 1,
+            "sample": desc + "; compress + decompress, oracle/sdqz_oracle.py (numpy port of the "
+                             "reference, same speed as the reference in the build container), 1 step"}
 
 
 # --------------------------------------------------------------------------
@@ -250,6 +301,8 @@ def load_traffic(config: str, kernel: str):
 # our arm
 # --------------------------------------------------------------------------
 def ours_arm(args, cfg, world, rank, local_rank):
+    import hashlib
+
     import torch
     import torch.distributed as dist
 
@@ -261,12 +314,10 @@ def ours_arm(args, cfg, world, rank, local_rank):
     dims = cfg["dims"]
     n = math.prod(dims)
     seed = 1 + rank
-    if args.config == "large":
-        d_in = device_field(dims, seed)
-        h_in, h_pinned = None, None
-    else:
-        h_in, h_pinned = host_field(args.config, dims, seed, rank)
-        d_in = torch.from_numpy(h_in).cuda()
+    t0 = time.perf_counter()
+    h_in, h_pinned = host_field(dims, seed)
+    log(f"field {dims} generated in {time.perf_counter() - t0:.1f} s")
+    d_in = h_pinned.cuda()
     flush = torch.empty(L2_FLUSH_BYTES // 4, dtype=torch.float32, device="cuda")
     ctx = _lib.context()
 
@@ -275,24 +326,29 @@ def ours_arm(args, cfg, world, rank, local_rank):
     dplan = DecompressPlan(dev)
 
     def step():
-        plan.run()
-        dplan.run()
+        dplan.run(plan.run())
 
     for _ in range(max(args.warmup, 1)):
         step()
-    hdr = plan.hdr
+    dev = plan.run()
+    hdr = dev.header
     K, C, P = int(hdr.n_outliers), int(hdr.n_chunks), int(hdr.payload_bytes)
     archive_bytes = hdr.total_bytes
-    # correctness guard on the measured data: the error bound holds
-    out = dplan.run().reshape(-1)
+    # parity guard on the measured data: the archive is the reference's (SHA-256
+    # of the reference-run archive, tests/golden/config_golden.json) and the
+    # error bound holds
+    golden = golden_for(cfg["golden"]) if seed == 1 else None
+    sha = hashlib.sha256(dev.to_bytes()).hexdigest()
+    matches = (sha == golden["archive_sha256"]) if golden else None
+    out = dplan.run(dev).reshape(-1)
     q = S.quality(d_in, out)   # one native fp64 pass (no field-sized temporaries)
     err = q.max_abs_error
     amax = max(abs(float(d_in.min())), abs(float(d_in.max())))
     assert err <= hdr.eb_resolved * (1 + 1e-9) + 2 * np.spacing(np.float32(amax)), err
+    del out
 
     stream = torch.cuda.current_stream()
-    starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
-    ends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    ev = [[torch.cuda.Event(enable_timing=True) for _ in range(3)] for _ in range(args.steps)]
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
@@ -300,15 +356,19 @@ def ours_arm(args, cfg, world, rank, local_rank):
     with Clocks(local_rank) as clk:
         for i in range(args.steps):
             flush.zero_()                       # evict the field/archive from L2
-            starts[i].record(stream)
-            step()
-            ends[i].record(stream)
+            ev[i][0].record(stream)
+            d = plan.run()
+            ev[i][1].record(stream)             # compress / decompress split (no timers)
+            dplan.run(d)
+            ev[i][2].record(stream)
         torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
     launches = ctx.launches - launches0
     replays = ctx.graph_replays - replays0
-    step_ms = [s.elapsed_time(e) for s, e in zip(starts, ends)]
+    step_ms = [a.elapsed_time(c) for a, b, c in ev]
+    c_ms = [a.elapsed_time(b) for a, b, c in ev]
+    d_ms = [b.elapsed_time(c) for a, b, c in ev]
     t_local = sum(step_ms) / 1e3
     t = torch.tensor([t_local], dtype=torch.float64, device="cuda")
     if world > 1:
@@ -316,21 +376,14 @@ def ours_arm(args, cfg, world, rank, local_rank):
     t_max = float(t.item())
     value = world * 4 * n * args.steps / t_max / 1e9
 
-    # split compress / decompress and per-kernel shares (probe pass, same events API)
+    # per-kernel device times (separate probe pass: the context's event timer
+    # marks every launch, which turns graph replay off)
     ctx.set_timing(True)
     probe = max(3, min(args.steps, 10))
-    c_ms, d_ms = [], []
     for _ in range(probe):
         flush.zero_()
-        a, b, c2 = (torch.cuda.Event(enable_timing=True) for _ in range(3))
-        a.record(stream)
-        plan.run()
-        b.record(stream)
-        dplan.run()
-        c2.record(stream)
-        torch.cuda.synchronize()
-        c_ms.append(a.elapsed_time(b))
-        d_ms.append(b.elapsed_time(c2))
+        dplan.run(plan.run())
+    torch.cuda.synchronize()
     ktimes = {k: v / probe for k, v in ctx.kernel_times().items()}
     ctx.set_timing(False)
     kernels = {k: v for k, v in ktimes.items() if not k.startswith("(") and k != "status_readback"}
@@ -341,56 +394,68 @@ def ours_arm(args, cfg, world, rank, local_rank):
     peak, peak_kind = load_peak()
     abytes = algorithmic_bytes(dom, n, K, C, P)
     achieved = abytes / (kernels[dom] / 1e3) / 1e9 if abytes else None
+    tc, td = statistics.median(c_ms) / 1e3, statistics.median(d_ms) / 1e3
+    comp_bytes = (12 if cfg["mode"] == "valrel" else 8) * n + P + 16 * K + 4 * C
+    decomp_bytes = 8 * n + P + 16 * K + 4 * C
 
-    # e2e through the public API with host buffers
-    e2e_steps = max(5, min(args.steps, 10))
-    e2e = None
-    if h_in is not None:
-        # three warm-up round trips: graph capture of both pipelines, the second result buffer of the pinned pool
-        # (the previous result is still alive when the next one is allocated)
-        for _ in range(3):
-            blob = S.compress(h_in.reshape(dims), eb=cfg["eb"], mode=cfg["mode"])
-            rec = S.decompress(blob)
-        if world > 1:
-            dist.barrier()
-        torch.cuda.synchronize()
-        t0 = time.perf_counter()
-        for _ in range(e2e_steps):
-            blob = S.compress(h_in.reshape(dims), eb=cfg["eb"], mode=cfg["mode"])
-            rec = S.decompress(blob)
-        torch.cuda.synchronize()
-        te = time.perf_counter() - t0
-        te_t = torch.tensor([te], dtype=torch.float64, device="cuda")
-        if world > 1:
-            dist.all_reduce(te_t, op=dist.ReduceOp.MAX)
-        te = float(te_t.item())
-        assert rec.shape == tuple(dims)
-        e2e = {"value": world * 4 * n * e2e_steps / te / 1e9, "unit": "GB/s",
-               "h2d_bytes_per_step": 4 * n + len(blob), "d2h_bytes_per_step": len(blob) + 4 * n,
-               "steps": e2e_steps, "timing": "wall clock, cuda synchronize on both sides",
-               "api": "paper_2007_09625_b200.compress(pinned np.ndarray) -> bytes; "
-                      "decompress(bytes) -> np.ndarray"}
+    # e2e through the public API with host buffers: pinned host field ->
+    # compress() -> archive bytes -> decompress() -> host field, every step
+    e2e_steps = max(3, min(args.steps, 5 if n > 1e9 else 10))
+    for _ in range(2):   # graph capture of both pipelines, pinned result pool
+        blob = S.compress(h_in.reshape(dims), eb=cfg["eb"], mode=cfg["mode"])
+        rec = S.decompress(blob)
+        del rec
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    for _ in range(e2e_steps):
+        blob = S.compress(h_in.reshape(dims), eb=cfg["eb"], mode=cfg["mode"])
+        rec = S.decompress(blob)
+    torch.cuda.synchronize()
+    te = time.perf_counter() - t0
+    te_t = torch.tensor([te], dtype=torch.float64, device="cuda")
+    if world > 1:
+        dist.all_reduce(te_t, op=dist.ReduceOp.MAX)
+    te = float(te_t.item())
+    assert rec.shape == tuple(dims) and len(blob) == archive_bytes
+    e2e = {"value": world * 4 * n * e2e_steps / te / 1e9, "unit": "GB/s",
+           "h2d_bytes_per_step": 4 * n + len(blob), "d2h_bytes_per_step": len(blob) + 4 * n,
+           "steps": e2e_steps, "timing": "wall clock, cuda synchronize on both sides",
+           "api": "paper_2007_09625_b200.compress(pinned np.ndarray) -> bytes; "
+                  "decompress(bytes) -> np.ndarray"}
+    del rec, blob
 
     base = None
-    if rank == 0 and world == 1 and not args.no_cpu_baseline and h_in is not None:
-        base = cpu_baseline(h_in, dims, cfg)
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        base = cpu_baseline(cfg)
 
     if rank == 0:
         line = {
             "metric": METRIC, "value": value, "unit": "GB/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup,
-            "ms_per_step": t_max / args.steps * 1e3, "higher_is_better": True, "scaling": "weak",
-            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "ms_per_step": t_max / args.steps * 1e3, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": {"workload": args.config, "desc": cfg["desc"], "dims": list(dims),
                        "eb": cfg["eb"], "mode": cfg["mode"], "cap": 1024,
-                       "profile": "smooth (reference synthetic.py), seed 1+rank, fp32",
+                       "profile": "smooth (reference synthetic.py), seed 1+rank, fp32, bit-identical "
+                                  "to the reference's generate_field",
                        "l2": "flushed between steps (512 MiB write); per-step CUDA events",
-                       "per_rank_points": n, "parallelism": f"replicas x{world}" if world > 1 else "1 GPU"},
-            "compress_gbs": 4 * n / (statistics.median(c_ms) / 1e3) / 1e9,
-            "decompress_gbs": 4 * n / (statistics.median(d_ms) / 1e3) / 1e9,
+                       "per_rank_points": n,
+                       "parallelism": f"replicas x{world}" if world > 1 else "1 GPU"},
+            "compress_gbs": 4 * n / tc / 1e9,
+            "decompress_gbs": 4 * n / td / 1e9,
             "compression_ratio": 4 * n / archive_bytes,
-            "archive": {"bytes": archive_bytes, "n_outliers": K, "n_chunks": C, "payload_bytes": P,
-                        "max_abs_err_over_eb": err / hdr.eb_resolved},
+            "parity": {"archive_sha256": sha, "reference_sha256": golden["archive_sha256"] if golden else None,
+                       "archive_matches_reference": matches,
+                       "max_abs_err_over_eb": err / hdr.eb_resolved},
+            "archive": {"bytes": archive_bytes, "n_outliers": K, "n_chunks": C, "payload_bytes": P},
+            "pipeline_roofline": {
+                "compress": {"algorithmic_bytes": comp_bytes, "ms": tc * 1e3,
+                             "gbs": comp_bytes / tc / 1e9, "frac": comp_bytes / tc / 1e9 / peak},
+                "decompress": {"algorithmic_bytes": decomp_bytes, "ms": td * 1e3,
+                               "gbs": decomp_bytes / td / 1e9, "frac": decomp_bytes / td / 1e9 / peak},
+                "bytes": "compress 12N+P+16K+4C (valrel), decompress 8N+P+16K+4C (SURVEY.md 8d)"},
             "kernel_ms": {k: round(v, 5) for k, v in sorted(kernels.items(), key=lambda x: -x[1])},
             "roofline": {"kernel": dom, "bound": "hbm", "achieved": achieved, "peak": peak,
                          "peak_kind": peak_kind, "unit": "GB/s",
@@ -423,7 +488,7 @@ def main():
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--config", default="hurricane", choices=sorted(CONFIGS))
+    ap.add_argument("--config", default="large", choices=sorted(CONFIGS))
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()
     if args.warmup < 3:

@@ -180,11 +180,16 @@ SDQZ_API int sdqz_compress(sdqz_ctx* ctx, const void* d_in, int dtype, int ndims
                   sdqz_header* hdr);
 /* Total archive bytes of the last compress. */
 SDQZ_API uint64_t sdqz_archive_size(const sdqz_ctx* ctx);
-/* Write the last compress's archive (header + sections) to host memory. */
-SDQZ_API int sdqz_archive_write(sdqz_ctx* ctx, uint8_t* h_dst, uint64_t capacity);
-/* Device pointers to the last compress's sections (bitwidths, outlier records,
+/* Id of the last compress's archive (unique per process; 0 = none, e.g. after
+ * a call that reused the section buffers).  A device-archive handle records it
+ * and passes it to the two calls below, which reject a stale id with
+ * SDQZ_EINVAL instead of returning another archive's sections. */
+SDQZ_API uint64_t sdqz_archive_generation(const sdqz_ctx* ctx);
+/* Write archive `gen` (header + sections) to host memory (gen 0: the last). */
+SDQZ_API int sdqz_archive_write(sdqz_ctx* ctx, uint64_t gen, uint8_t* h_dst, uint64_t capacity);
+/* Device pointers to archive `gen`'s sections (bitwidths, outlier records,
  * chunk bits, payload) -- for device-resident decompress and sharding. */
-SDQZ_API int sdqz_archive_sections(sdqz_ctx* ctx, const uint8_t** d_bw, const void** d_outliers,
+SDQZ_API int sdqz_archive_sections(sdqz_ctx* ctx, uint64_t gen, const uint8_t** d_bw, const void** d_outliers,
                           const uint32_t** d_chunk_bits, const uint8_t** d_payload);
 
 /* parse_header (archive.py:143-181): validate and decode the 93-byte header. */

@@ -34,6 +34,11 @@ class Header(Structure):
         ("n_outliers", c_uint64), ("n_chunks", c_uint64), ("payload_bytes", c_uint64),
     ]
 
+    def copy(self) -> "Header":
+        h = Header()
+        ctypes.pointer(h)[0] = self
+        return h
+
     @property
     def total_bytes(self) -> int:
         return (HEADER_SIZE + self.cap + 16 * self.n_outliers + 4 * self.n_chunks
@@ -79,8 +84,9 @@ _SIGS = {
                               POINTER(c_uint32), c_int, c_double, c_uint32, c_uint32,
                               POINTER(Header)]),
     "sdqz_archive_size": (c_uint64, [c_void_p]),
-    "sdqz_archive_write": (c_int, [c_void_p, c_void_p, c_uint64]),
-    "sdqz_archive_sections": (c_int, [c_void_p, POINTER(c_void_p), POINTER(c_void_p),
+    "sdqz_archive_generation": (c_uint64, [c_void_p]),
+    "sdqz_archive_write": (c_int, [c_void_p, c_uint64, c_void_p, c_uint64]),
+    "sdqz_archive_sections": (c_int, [c_void_p, c_uint64, POINTER(c_void_p), POINTER(c_void_p),
                                       POINTER(c_void_p), POINTER(c_void_p)]),
     "sdqz_parse_header": (c_int, [c_void_p, c_void_p, c_uint64, POINTER(Header)]),
     "sdqz_decompress": (c_int, [c_void_p, c_void_p, c_uint64, c_void_p]),
@@ -166,6 +172,10 @@ class Context:
                 k, v = item.split("=")
                 out[k] = float(v)
         return out
+
+    @property
+    def archive_generation(self) -> int:
+        return int(self.lib.sdqz_archive_generation(self.h))
 
     @property
     def launches(self) -> int:

@@ -10,6 +10,10 @@
 
 #include <vector>
 
+#include <atomic>
+#include <map>
+#include <mutex>
+
 #include <omp.h>
 #include <sys/mman.h>
 
@@ -37,6 +41,8 @@ void* scratch(sdqz_ctx* ctx, int slot, size_t bytes, cudaError_t* e) {
     if (bytes == 0) bytes = 16;
     if (b.bytes >= bytes) return b.p;
     ctx->gen++;   // device pointers change: captured graphs are stale
+    if (slot == S_BW || slot == S_OUTREC || slot == S_CHUNK_BITS || slot == S_PAYLOAD)
+        ctx->have_archive = false;   // the last archive's sections are gone
     if (b.p) {
         cudaStreamSynchronize(ctx->stream);
         cudaFree(b.p);
@@ -57,6 +63,19 @@ void* scratch(sdqz_ctx* ctx, int slot, size_t bytes, cudaError_t* e) {
     }
     b.bytes = want;
     return b.p;
+}
+
+void ensure_smem(const sdqz_ctx* ctx, const void* func, size_t bytes) {
+    if (!bytes) return;
+    static std::mutex mu;
+    static std::map<std::pair<const void*, int>, size_t> applied;
+    std::lock_guard<std::mutex> lock(mu);
+    size_t& have = applied[{func, ctx->device}];
+    if (have >= bytes) return;
+    if (cudaFuncSetAttribute(func, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes) == cudaSuccess)
+        have = bytes;
+    else
+        cudaGetLastError();   // the launch reports the failure
 }
 
 namespace {
@@ -514,6 +533,8 @@ int compress_finish(sdqz_ctx* ctx, CompressState& c, sdqz_header* hdr) {
     h.payload_bytes = s.payload_bytes;
     ctx->last_hdr = h;
     ctx->have_archive = true;
+    static std::atomic<uint64_t> next_gen{1};   // unique across contexts
+    ctx->archive_gen = next_gen++;
     if (hdr) *hdr = h;
     return SDQZ_OK;
 }
@@ -805,6 +826,7 @@ int sdqz_outliers(sdqz_ctx* ctx, const void* d_in, int in_kind, const uint16_t* 
     *k_out = 0;
     if (n == 0) return SDQZ_OK;
     if ((rc = reset_status_eb(ctx, eb, true))) return rc;
+    ctx->have_archive = false;   // reuses the chunk-bits section buffer
     uint32_t* cbits = scratch_as<uint32_t>(ctx, S_CHUNK_BITS, ceil_div(n, 4096), &rc);
     if (!cbits) return rc;
     DeflateJob job;
@@ -1047,9 +1069,21 @@ uint64_t sdqz_archive_size(const sdqz_ctx* ctx) {
     return ctx->have_archive ? archive_total(ctx->last_hdr) : 0;
 }
 
-int sdqz_archive_sections(sdqz_ctx* ctx, const uint8_t** d_bw, const void** d_outliers,
+uint64_t sdqz_archive_generation(const sdqz_ctx* ctx) {
+    return ctx && ctx->have_archive ? ctx->archive_gen : 0;
+}
+
+static int check_archive(sdqz_ctx* ctx, uint64_t gen) {
+    if (!ctx->have_archive || (gen && gen != ctx->archive_gen))
+        return set_error(ctx, SDQZ_EINVAL,
+                         "stale device archive: a later compress on this context replaced its "
+                         "sections (call to_bytes() before compressing again)");
+    return SDQZ_OK;
+}
+
+int sdqz_archive_sections(sdqz_ctx* ctx, uint64_t gen, const uint8_t** d_bw, const void** d_outliers,
                           const uint32_t** d_chunk_bits, const uint8_t** d_payload) {
-    if (!ctx->have_archive) return set_error(ctx, SDQZ_EINVAL, "no archive");
+    if (int rc = check_archive(ctx, gen)) return rc;
     *d_bw = (const uint8_t*)ctx->bufs[S_BW].p;
     *d_outliers = ctx->bufs[S_OUTREC].p;
     *d_chunk_bits = (const uint32_t*)ctx->bufs[S_CHUNK_BITS].p;
@@ -1057,8 +1091,8 @@ int sdqz_archive_sections(sdqz_ctx* ctx, const uint8_t** d_bw, const void** d_ou
     return SDQZ_OK;
 }
 
-int sdqz_archive_write(sdqz_ctx* ctx, uint8_t* h_dst, uint64_t capacity) {
-    if (!ctx->have_archive) return set_error(ctx, SDQZ_EINVAL, "no archive");
+int sdqz_archive_write(sdqz_ctx* ctx, uint64_t gen, uint8_t* h_dst, uint64_t capacity) {
+    if (int rc = check_archive(ctx, gen)) return rc;
     const sdqz_header& h = ctx->last_hdr;
     uint64_t total = archive_total(h);
     if (capacity < total) return set_error(ctx, SDQZ_EINVAL, "destination too small");

@@ -173,6 +173,8 @@ struct sdqz_ctx {
     // state of the last fused compress (sections live in scratch buffers)
     sdqz_header last_hdr{};
     bool have_archive = false;
+    uint64_t archive_gen = 0;   // id of the last compress's archive (0: none);
+                                // handles holding another id are stale
 
     // captured pipelines (CUDA graphs), valid while the scratch arena's
     // generation is unchanged
@@ -213,6 +215,10 @@ int reset_status(sdqz_ctx* ctx);      // memset status on stream
 int enqueue_status_copy(sdqz_ctx* ctx);   // D2H of the status block (no sync)
 int sync_status(sdqz_ctx* ctx);           // stream sync (+ timer flush)
 int reset_status_eb(sdqz_ctx* ctx, double eb, bool has_eb);   // ... and set eb / 2eb
+// cudaFuncSetAttribute(MaxDynamicSharedMemorySize) applies per device: raise a
+// kernel's limit on the context's device to >= bytes (remembered per
+// (kernel, device) under a lock).
+void ensure_smem(const sdqz_ctx* ctx, const void* func, size_t bytes);
 
 #define SDQZ_CUDA(ctx, expr)                                                      \
     do {                                                                          \

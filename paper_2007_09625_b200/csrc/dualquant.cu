@@ -1082,12 +1082,10 @@ int launch_kind(sdqz_ctx* ctx, const void* d_in, int ndims, const uint64_t dims[
                 const uint32_t block[3], uint32_t cap, uint16_t* d_codes,
                 unsigned long long* d_hist) {
     size_t smem = (d_hist && cap <= kSmemHistMax) ? cap * sizeof(uint32_t) : 0;
-    if (smem > 48 * 1024) {
-        cudaFuncSetAttribute(dq3d_kernel<KIND>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        cudaFuncSetAttribute(dq2d_kernel<KIND>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        cudaFuncSetAttribute(dq1d_kernel<KIND>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        cudaFuncSetAttribute(dq_generic_kernel<KIND>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    }
+    ensure_smem(ctx, (const void*)dq3d_kernel<KIND>, smem);
+    ensure_smem(ctx, (const void*)dq2d_kernel<KIND>, smem);
+    ensure_smem(ctx, (const void*)dq1d_kernel<KIND>, smem);
+    ensure_smem(ctx, (const void*)dq_generic_kernel<KIND>, smem);
     uint64_t n = dims[0] * dims[1] * dims[2];
     int max_grid = ctx->num_sms * 8;
     // TMA-fed 3D path: fp32, 16-byte aligned base and row pitch, extents TMA can address
@@ -1101,12 +1099,7 @@ int launch_kind(sdqz_ctx* ctx, const void* d_in, int ndims, const uint64_t dims[
         if (make_tensor_map(&map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, d_in, gd, gs, box)) {
             const size_t tsm = kTmaWarps * kStages * kPair * 4 + kTmaWarps * kStages * 8 +
                                kTmaWarps * kHot * 32 * 4 + smem;
-            static bool attr_done = false;
-            if (!attr_done) {
-                cudaFuncSetAttribute(dq3d_tma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     kTmaWarps * kStages * kPair * 4 + kTmaWarps * kHot * 32 * 4 + 16 * 4096 + 256);
-                attr_done = true;
-            }
+            ensure_smem(ctx, (const void*)dq3d_tma_kernel, tsm);
             const uint64_t ntask =
                 ceil_div(ceil_div(dims[2], 8), 4) * ceil_div(dims[1], 8) * ceil_div(dims[0], 8);
             int per_sm = 1;
@@ -1125,13 +1118,8 @@ int launch_kind(sdqz_ctx* ctx, const void* d_in, int ndims, const uint64_t dims[
         ((uintptr_t)d_in & 15) == 0 && ((uintptr_t)d_codes & 7) == 0 && !env_disabled("SDQZ_NO_VEC1D")) {
         const uint64_t nt = dims[0] / kVecTask;
         const size_t vsm = kWarpsPerCta * kHot * 32 * 4 + smem;
-        static bool vattr = false;
-        if (!vattr) {
-            const int mx = kWarpsPerCta * kHot * 32 * 4 + kSmemHistMax * 4;
-            cudaFuncSetAttribute(dq1d_vec_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
-            cudaFuncSetAttribute(dq1d_vec_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
-            vattr = true;
-        }
+        ensure_smem(ctx, (const void*)dq1d_vec_kernel<true>, vsm);
+        ensure_smem(ctx, (const void*)dq1d_vec_kernel<false>, vsm);
         uint64_t grid = ceil_div(nt, kWarpsPerCta);
         if (grid > (uint64_t)ctx->num_sms * 2) grid = (uint64_t)ctx->num_sms * 2;
         if (smem)
@@ -1154,13 +1142,8 @@ int launch_kind(sdqz_ctx* ctx, const void* d_in, int ndims, const uint64_t dims[
         ((uintptr_t)d_in & 15) == 0 && ((uintptr_t)d_codes & 7) == 0 && !env_disabled("SDQZ_NO_VEC2D")) {
         const uint64_t nt = ceil_div(dims[1], 128) * ceil_div(dims[0], 16);
         const size_t vsm = kWarpsPerCta * kHot * 32 * 4 + smem;
-        static bool vattr = false;
-        if (!vattr) {
-            const int mx = kWarpsPerCta * kHot * 32 * 4 + kSmemHistMax * 4;
-            cudaFuncSetAttribute(dq2d_vec_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
-            cudaFuncSetAttribute(dq2d_vec_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
-            vattr = true;
-        }
+        ensure_smem(ctx, (const void*)dq2d_vec_kernel<true>, vsm);
+        ensure_smem(ctx, (const void*)dq2d_vec_kernel<false>, vsm);
         uint64_t grid = ceil_div(nt, kWarpsPerCta);
         if (grid > (uint64_t)ctx->num_sms * 2) grid = (uint64_t)ctx->num_sms * 2;
         if (smem)
@@ -1217,18 +1200,16 @@ bool env_disabled(const char* name) {
 
 bool make_tensor_map(CUtensorMap* map, CUtensorMapDataType dtype, uint32_t rank, const void* base,
                      const uint64_t* dims, const uint64_t* strides_bytes, const uint32_t* box) {
-    static PFN_cuTensorMapEncodeTiled_v12000 encode = nullptr;
-    static bool tried = false;
-    if (!tried) {
-        tried = true;
+    // resolved once per process (thread-safe static initialisation)
+    static const PFN_cuTensorMapEncodeTiled_v12000 encode = [] {
         void* fn = nullptr;
         cudaDriverEntryPointQueryResult q;
         if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) == cudaSuccess &&
             q == cudaDriverEntryPointSuccess)
-            encode = (PFN_cuTensorMapEncodeTiled_v12000)fn;
-        else
-            cudaGetLastError();
-    }
+            return (PFN_cuTensorMapEncodeTiled_v12000)fn;
+        cudaGetLastError();
+        return (PFN_cuTensorMapEncodeTiled_v12000) nullptr;
+    }();
     if (!encode) return false;
     cuuint64_t gd[5], gs[4];
     cuuint32_t bx[5], es[5];

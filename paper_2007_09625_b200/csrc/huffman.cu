@@ -1412,12 +1412,8 @@ int run_deflate(sdqz_ctx* ctx, DeflateArgs& a, bool payload) {
     chunk_scan_kernel<<<kScanCtas, 1024, 0, ctx->stream>>>(a);
     SDQZ_LAUNCHED_NAMED(ctx, "chunk_scan_kernel");
     if (SRC == SRC_CODES) {
-        static bool attr = false;   // 28.8 KB static + up to 32 KB table > the 48 KB default
-        if (!attr) {
-            cudaFuncSetAttribute(chunk_pack_run_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 4096 * 8);
-            attr = true;
-        }
+        // 28.8 KB static + up to 32 KB table > the 48 KB default
+        ensure_smem(ctx, (const void*)chunk_pack_run_kernel<true>, 4096 * 8);
         if (payload && a.gtable) {   // 32-bit units (device-decided; no-op otherwise)
             if (ts) chunk_pack32_kernel<true><<<(unsigned)grid, 256, 0, ctx->stream>>>(a);
             else chunk_pack32_kernel<false><<<(unsigned)grid, 256, 0, ctx->stream>>>(a);
@@ -1440,8 +1436,7 @@ int run_deflate(sdqz_ctx* ctx, DeflateArgs& a, bool payload) {
 int launch_histogram_u32(sdqz_ctx* ctx, const uint32_t* codes, uint64_t n, uint32_t cap,
                          unsigned long long* hist) {
     size_t smem = cap <= 16384 ? cap * 4 : 0;
-    if (smem > 48 * 1024)
-        cudaFuncSetAttribute(hist_u32_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    ensure_smem(ctx, (const void*)hist_u32_kernel, smem);
     uint64_t grid = ceil_div(n, 256);
     if (grid > (uint64_t)ctx->num_sms * 4) grid = ctx->num_sms * 4;
     if (grid < 1) grid = 1;
@@ -1470,17 +1465,13 @@ int launch_codebook(sdqz_ctx* ctx, const unsigned long long* d_hist, uint8_t* d_
         gs.dep = u + 3 * cap;
         gs.jmp = u + 7 * cap;
     }
-    static size_t attr_smem = 0;   // static shared memory (~17 KB) + dynamic can pass 48 KB
-    if (smem > attr_smem) {
-        cudaFuncSetAttribute(codebook_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        attr_smem = smem;
-    }
-    static uint32_t round_min = 0;
-    if (!round_min) {
+    // static shared memory (~17 KB) + dynamic can pass 48 KB
+    ensure_smem(ctx, (const void*)codebook_kernel<true>, smem);
+    static const uint32_t round_min = [] {
         const char* e = getenv("SDQZ_ROUND_MIN");
-        round_min = e ? (uint32_t)atoi(e) : 4u;
-        if (!round_min) round_min = 1;
-    }
+        const uint32_t r = e ? (uint32_t)atoi(e) : 4u;
+        return r ? r : 1u;
+    }();
     if (cap <= kSmemSortMax)
         codebook_kernel<true><<<1, kBookThreads, smem, ctx->stream>>>(d_hist, d_bw, cap, book, ctx->d_status,
                                                                    build_tree ? 1 : 0, canon ? 1 : 0, gs,

@@ -815,11 +815,7 @@ void launch_inflate_fast_w(sdqz_ctx* ctx, const uint8_t* payload, uint64_t nword
     uint32_t stage_words = (uint32_t)umin(((2 * avg + 64) / 4 + 15) & ~15ull, room);
     if (stage_words < 64) stage_words = 64;
     const size_t smem = fixed + (size_t)kWarps * stage_words * 4;
-    static size_t attr_smem = 0;
-    if (smem > attr_smem) {
-        cudaFuncSetAttribute(inflate_fast_kernel<kWarps>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        attr_smem = smem;
-    }
+    ensure_smem(ctx, (const void*)inflate_fast_kernel<kWarps>, smem);
     int per_sm = 1;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, inflate_fast_kernel<kWarps>, kWarps * 32, smem);
     if (per_sm < 1) per_sm = 1;

@@ -19,6 +19,7 @@ from __future__ import annotations
 
 import ctypes
 import math
+import struct
 from dataclasses import dataclass
 
 import numpy as np
@@ -37,24 +38,39 @@ _PyBytes_AsString.argtypes = [ctypes.py_object]
 
 @dataclass
 class DeviceArchive:
-    """Archive sections resident in a context's device memory (last compress)."""
+    """Archive sections resident in a context's device memory.
+
+    The sections live in the context's scratch arena until the next compress
+    on that context; `gen` identifies this archive, and the C-ABI refuses a
+    stale handle (SdqzError) instead of handing out the newer archive."""
 
     header: _lib.Header
     ctx: _lib.Context
+    gen: int = 0
 
     @property
     def nbytes(self) -> int:
         return self.header.total_bytes
 
+    @property
+    def valid(self) -> bool:
+        return self.gen != 0 and self.ctx.archive_generation == self.gen
+
     def to_bytes(self) -> bytes:
         n = self.header.total_bytes
         out = _PyBytes_FromStringAndSize(None, n)
-        self.ctx.call("sdqz_archive_write", ctypes.c_void_p(_PyBytes_AsString(out)), n)
+        self.ctx.call("sdqz_archive_write", self.gen, ctypes.c_void_p(_PyBytes_AsString(out)), n)
         return out
 
     def write_into(self, host_ptr: int, capacity: int) -> int:
-        self.ctx.call("sdqz_archive_write", ctypes.c_void_p(host_ptr), capacity)
+        self.ctx.call("sdqz_archive_write", self.gen, ctypes.c_void_p(host_ptr), capacity)
         return self.header.total_bytes
+
+    def sections(self):
+        """Device pointers (bitwidths, outlier records, chunk bits, payload)."""
+        ptrs = [ctypes.c_void_p() for _ in range(4)]
+        self.ctx.call("sdqz_archive_sections", self.gen, *(ctypes.byref(p) for p in ptrs))
+        return ptrs
 
 
 def _check_request(arr, dims, eb, mode, cap, block_shape, chunk_size):
@@ -81,6 +97,10 @@ def _check_request(arr, dims, eb, mode, cap, block_shape, chunk_size):
         pending = e
     if pending is None and chunk_size is not None and chunk_size != 0 and chunk_size < 1:
         pending = SdqzError("chunk_size must be >= 1")
+    if pending is None and chunk_size is not None and chunk_size > 0xFFFFFFFF:
+        # the header stores chunk_size as u32 (archive.py:34-35): the reference's
+        # serialize fails in struct.pack; never truncate it into another archive
+        pending = struct.error("'I' format requires 0 <= number <= 4294967295")
     return dims, block, pending
 
 
@@ -110,7 +130,7 @@ def compress_device(data, dims=None, *, eb: float, mode: str = "abs", cap: int =
     ctx.call("sdqz_compress", _lib.ptr(t), 0 if dt == np.float32 else 1, len(dims),
              _lib.dims3(dims), _lib.block3(block), 0 if mode == "abs" else 1, float(eb),
              int(cap), int(chunk_size or 0), ctypes.byref(hdr))
-    return DeviceArchive(hdr, ctx)
+    return DeviceArchive(hdr, ctx, ctx.archive_generation)
 
 
 def compress(data, dims=None, *, eb: float, mode: str = "abs", cap: int = 1024,
@@ -145,9 +165,7 @@ def decompress_device(src, out=None):
         ctx = src.ctx
         ctx.sync_stream()
         h = src.header
-        bw, rec, cb, pay = (ctypes.c_void_p() for _ in range(4))
-        ctx.call("sdqz_archive_sections", ctypes.byref(bw), ctypes.byref(rec), ctypes.byref(cb),
-                 ctypes.byref(pay))
+        bw, rec, cb, pay = src.sections()
         o = _out_tensor(h, out)
         ctx.call("sdqz_decompress_sections", ctypes.byref(h), bw, rec, cb, pay, _lib.ptr(o))
         return o.view(*_dims_of(h))
@@ -251,7 +269,7 @@ class CompressPlan:
 
     def run(self) -> DeviceArchive:
         self.ctx.call("sdqz_compress", *self.args, ctypes.byref(self.hdr))
-        return DeviceArchive(self.hdr, self.ctx)
+        return DeviceArchive(self.hdr.copy(), self.ctx, self.ctx.archive_generation)
 
 
 class DecompressPlan:
@@ -262,10 +280,10 @@ class DecompressPlan:
         self.dev = dev
         self.out = _out_tensor(dev.header)
 
-    def run(self):
-        ctx, h = self.dev.ctx, self.dev.header
-        bw, rec, cb, pay = (ctypes.c_void_p() for _ in range(4))
-        ctx.call("sdqz_archive_sections", ctypes.byref(bw), ctypes.byref(rec), ctypes.byref(cb),
-                 ctypes.byref(pay))
+    def run(self, dev: DeviceArchive | None = None):
+        """Decompress `dev` (default: the plan's archive) into the plan's buffer."""
+        dev = dev or self.dev
+        ctx, h = dev.ctx, dev.header
+        bw, rec, cb, pay = dev.sections()
         ctx.call("sdqz_decompress_sections", ctypes.byref(h), bw, rec, cb, pay, _lib.ptr(self.out))
         return self.out

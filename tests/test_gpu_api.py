@@ -1,0 +1,78 @@
+"""Device-API behaviour: archive handles, argument ranges, per-device contexts."""
+
+from __future__ import annotations
+
+import struct
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+if not torch.cuda.is_available():  # pragma: no cover
+    pytest.skip("needs a CUDA device", allow_module_level=True)
+
+import paper_2007_09625_b200 as S  # noqa: E402
+from oracle import sdqz_oracle as O  # noqa: E402
+from paper_2007_09625_b200.pipeline import CompressPlan, DecompressPlan  # noqa: E402
+
+
+def fields():
+    a = S.generate_field("smooth", (24, 40, 56), seed=1).astype(np.float32)
+    b = S.generate_field("smooth", (30, 20, 44), seed=2).astype(np.float32)
+    return a, b
+
+
+def test_stale_device_archive_is_refused():
+    a, b = fields()
+    da = S.compress_device(torch.from_numpy(a).cuda(), eb=1e-4, mode="valrel")
+    blob_a = da.to_bytes()
+    assert blob_a == O.compress(a, eb=1e-4, mode="valrel")
+    db = S.compress_device(torch.from_numpy(b).cuda(), eb=1e-4, mode="valrel")
+    assert not da.valid and db.valid
+    with pytest.raises(S.SdqzError, match="stale device archive"):
+        da.to_bytes()
+    with pytest.raises(S.SdqzError, match="stale device archive"):
+        S.decompress_device(da)
+    assert db.to_bytes() == O.compress(b, eb=1e-4, mode="valrel")
+    out = S.decompress_device(db).cpu().numpy()
+    assert np.array_equal(out.view(np.uint32), O.decompress(db.to_bytes()).view(np.uint32))
+
+
+def test_plan_headers_are_per_run():
+    a, b = fields()
+    pa = CompressPlan(torch.from_numpy(a).cuda(), a.shape, eb=1e-4, mode="valrel")
+    pb = CompressPlan(torch.from_numpy(b).cuda(), b.shape, eb=1e-4, mode="valrel")
+    da = pa.run()
+    ha = (da.header.n_outliers, da.header.payload_bytes)
+    db = pb.run()
+    assert (da.header.n_outliers, da.header.payload_bytes) == ha
+    assert db.header.dims[0] == 30 and da.header.dims[0] == 24
+    dp = DecompressPlan(db)
+    out = dp.run().cpu().numpy()
+    assert np.array_equal(out.view(np.uint32), O.decompress(db.to_bytes()).reshape(-1).view(np.uint32))
+    with pytest.raises(S.SdqzError, match="stale"):
+        DecompressPlan(da).run()
+
+
+def test_chunk_size_beyond_u32_is_not_truncated():
+    a = np.linspace(-1, 1, 1000, dtype=np.float32)
+    with pytest.raises(struct.error):
+        S.compress(a, eb=1e-3, chunk_size=2**32)
+    with pytest.raises(struct.error):
+        S.compress(a, eb=1e-3, chunk_size=2**32 + 256)
+    # errors the reference raises earlier still win
+    with pytest.raises(S.SdqzError, match="NaN"):
+        S.compress(np.array([1.0, np.nan], np.float32), eb=1e-3, chunk_size=2**32)
+
+
+def test_second_device_context_if_present():
+    if torch.cuda.device_count() < 2:
+        pytest.skip("one GPU")
+    a, _ = fields()
+    blobs = []
+    for d in range(2):
+        with torch.cuda.device(d):
+            blobs.append(S.compress(a, eb=1e-4, mode="valrel"))
+    assert blobs[0] == blobs[1]
