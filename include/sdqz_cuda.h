@@ -87,6 +87,8 @@ SDQZ_API int sdqz_set_timing(sdqz_ctx* ctx, int on);
 /* Diagnostics of the last call (inflate: lane redecodes, unsynchronised
  * chunks, chunks decoded by the sequential path). */
 SDQZ_API int sdqz_debug_counters(sdqz_ctx* ctx, uint64_t* out, int n);
+/* Copy `bytes` of context scratch slot `slot` to host (diagnostics only). */
+SDQZ_API int sdqz_debug_read(sdqz_ctx* ctx, int slot, void* host, uint64_t bytes);
 SDQZ_API int sdqz_kernel_times(sdqz_ctx* ctx, char* buf, uint64_t len);
 
 /* ---- L1: field description (core.py:136-175) ---------------------------- */

@@ -54,6 +54,7 @@ _SIGS = {
     "sdqz_graph_replays": (c_uint64, [c_void_p]),
     "sdqz_set_timing": (c_int, [c_void_p, c_int]),
     "sdqz_debug_counters": (c_int, [c_void_p, POINTER(c_uint64), c_int]),
+    "sdqz_debug_read": (c_int, [c_void_p, c_int, c_void_p, c_uint64]),
     "sdqz_kernel_times": (c_int, [c_void_p, c_char_p, c_uint64]),
     "sdqz_describe": (c_int, [c_void_p, c_void_p, c_int, c_uint64, POINTER(c_double),
                               POINTER(c_double), POINTER(c_int)]),

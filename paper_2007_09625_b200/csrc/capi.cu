@@ -360,7 +360,7 @@ int decompress_core(sdqz_ctx* ctx, const sdqz_header* hdr, const uint8_t* d_bw, 
         // (the sequential decoder's LUT is built with the fast decoder's tables)
         if (chunks_ok) {
             if ((r2 = launch_inflate(ctx, d_payload, payload_alloc, d_cbits, C, hdr->chunk_size,
-                                     book.first, book.offsets, book.symbols, book.lut, -1, n, codes,
+                                     book.first, book.offsets, book.symbols, book.lut, -1, cap, n, codes,
                                      false)))
                 return r2;
         }
@@ -735,6 +735,15 @@ int sdqz_debug_counters(sdqz_ctx* ctx, uint64_t* out, int n) {
     return SDQZ_OK;
 }
 
+int sdqz_debug_read(sdqz_ctx* ctx, int slot, void* host, uint64_t bytes) {
+    if (slot < 0 || slot >= S_NSLOTS || (int)ctx->bufs.size() <= slot) return SDQZ_EINVAL;
+    const auto& b = ctx->bufs[slot];
+    if (!b.p || bytes > b.bytes) return SDQZ_EINVAL;
+    SDQZ_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
+    SDQZ_CUDA(ctx, cudaMemcpy(host, b.p, bytes, cudaMemcpyDeviceToHost));
+    return SDQZ_OK;
+}
+
 int sdqz_set_timing(sdqz_ctx* ctx, int on) {
     cudaStreamSynchronize(ctx->stream);
     ctx->marks.clear();
@@ -1016,7 +1025,7 @@ int sdqz_inflate(sdqz_ctx* ctx, const uint8_t* d_payload, uint64_t payload_bytes
     if ((rc = reset_status(ctx))) return rc;
     if ((rc = launch_build_lut(ctx, d_first, d_offsets, d_symbols, max_bw, lut))) return rc;
     if ((rc = launch_inflate(ctx, d_payload, payload_bytes, d_chunk_bits, n_chunks, chunk, d_first,
-                             d_offsets, d_symbols, lut, max_bw, n, d_codes_u32, true)))
+                             d_offsets, d_symbols, lut, max_bw, 65536, n, d_codes_u32, true)))
         return rc;
     if ((rc = fetch_status(ctx))) return rc;
     return decode_error(ctx);
@@ -1184,7 +1193,7 @@ int sdqz_decompress_slab(sdqz_ctx* ctx, const sdqz_header* hdr, const uint8_t* d
     if ((rc = launch_codebook(ctx, nullptr, const_cast<uint8_t*>(d_bw), cap, book, false, true, true))) return rc;
     if (n_chunks &&
         (rc = launch_inflate(ctx, d_payload, payload_bytes, d_chunk_bits, n_chunks, hdr->chunk_size, book.first,
-                             book.offsets, book.symbols, book.lut, -1, n_range, codes, false)))
+                             book.offsets, book.symbols, book.lut, -1, cap, n_range, codes, false)))
         return rc;
     // zero codes of the slab alone (the decoder counted the whole chunk range)
     SDQZ_CUDA(ctx, cudaMemsetAsync(&ctx->d_status->n_zero, 0, sizeof(unsigned long long), ctx->stream));

@@ -66,7 +66,7 @@ int launch_encode_u32(sdqz_ctx* ctx, const uint32_t* codes, uint64_t n, const ui
 int launch_inflate(sdqz_ctx* ctx, const uint8_t* payload, uint64_t payload_bytes,
                    const uint32_t* chunk_bits, uint64_t n_chunks, uint32_t chunk,
                    const uint64_t* first, const int64_t* offsets, const uint32_t* symbols,
-                   const uint32_t* lut, int max_bw, uint64_t n, void* codes, bool out32);
+                   const uint32_t* lut, int max_bw, uint32_t cap, uint64_t n, void* codes, bool out32);
 
 // inflate.cu: decode tables (primary 12-bit + second level) and the warp-per-chunk
 // self-synchronising decoder; chunks it cannot finish are flagged in `redo`.
