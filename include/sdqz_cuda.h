@@ -189,10 +189,52 @@ SDQZ_API uint64_t sdqz_archive_size(const sdqz_ctx* ctx);
 SDQZ_API uint64_t sdqz_archive_generation(const sdqz_ctx* ctx);
 /* Write archive `gen` (header + sections) to host memory (gen 0: the last). */
 SDQZ_API int sdqz_archive_write(sdqz_ctx* ctx, uint64_t gen, uint8_t* h_dst, uint64_t capacity);
+/* Copy archive `gen`'s sections into caller device buffers (stream-ordered,
+ * no sync; any pointer may be NULL to skip that section). */
+SDQZ_API int sdqz_archive_copy(sdqz_ctx* ctx, uint64_t gen, uint8_t* d_bw, void* d_outliers,
+                               uint32_t* d_chunk_bits, uint8_t* d_payload);
 /* Device pointers to archive `gen`'s sections (bitwidths, outlier records,
  * chunk bits, payload) -- for device-resident decompress and sharding. */
 SDQZ_API int sdqz_archive_sections(sdqz_ctx* ctx, uint64_t gen, const uint8_t** d_bw, const void** d_outliers,
                           const uint32_t** d_chunk_bits, const uint8_t** d_payload);
+
+/* ---- sharded compress (one rank, one slab of whole block rows)
+ * The reference composes the same slab decomposition for workers > 1
+ * (dualquant.py:230-273); these phases wrap the per-slab pipeline around the
+ * caller's collectives:
+ *   describe -> [all-reduce MAX of d_range] -> quantize -> [all-reduce SUM of
+ *   d_hist] -> (head/tail code exchange if chunks straddle slabs) -> encode.
+ * Nothing reaches the host before encode's sizes.  After encode the rank's
+ * sections (bitwidths, its outlier records with GLOBAL indices, its chunk
+ * bits, its payload) are this context's archive (sdqz_archive_sections). */
+typedef struct {
+    uint64_t n_chunks;       /* chunks this rank packed                   */
+    uint64_t payload_bytes;  /* their payload bytes                       */
+    uint64_t n_outliers;     /* this slab's outlier records               */
+    uint32_t unit_width;     /* 32 | 64 (global codebook: same everywhere) */
+    uint32_t max_bw;
+    double eb_resolved;      /* same everywhere (core.py:161-175)         */
+} sdqz_shard_sizes;
+/* describe (core.py:136-158) of this slab into d_range[3] = {-min, max,
+ * nonfinite} (device doubles) for an all-reduce MAX.  No host sync. */
+SDQZ_API int sdqz_shard_describe(sdqz_ctx* ctx, const void* d_in, int dtype, uint64_t n, double* d_range);
+/* resolve the bound from the reduced range (valrel) or eb (abs) on device,
+ * dual-quant the slab (local dims) into the context's code buffer and its
+ * histogram into d_hist (u64[cap], device) for an all-reduce SUM.  No sync. */
+SDQZ_API int sdqz_shard_quantize(sdqz_ctx* ctx, const void* d_in, int dtype, int ndims, const uint64_t dims[3],
+                                 const uint32_t block[3], int eb_mode, double eb, uint32_t cap,
+                                 const double* d_range, uint64_t* d_hist);
+/* copy the slab's first `count` codes (its head, packed by the previous rank
+ * when chunks straddle the slab start) to d_dst. */
+SDQZ_API int sdqz_shard_head(sdqz_ctx* ctx, uint64_t count, uint16_t* d_dst);
+/* codebook from the global histogram (huffman.py:98-190), deflate
+ * (huffman.py:219-269) of codes [head, n) + the next ranks' n_tail head codes
+ * in chunks of `chunk`, outlier records (dualquant.py:190-194) of all n slab
+ * points with global index idx_base + local.  Synchronous; checks in the
+ * reference's order (resolve_error_bound first). */
+SDQZ_API int sdqz_shard_encode(sdqz_ctx* ctx, const uint64_t* d_hist, uint32_t chunk, uint64_t head,
+                               const uint16_t* d_tail, uint64_t n_tail, uint64_t idx_base,
+                               sdqz_shard_sizes* out);
 
 /* parse_header (archive.py:143-181): validate and decode the 93-byte header. */
 SDQZ_API int sdqz_parse_header(sdqz_ctx* ctx, const uint8_t* h_buf, uint64_t len, sdqz_header* hdr);
@@ -210,13 +252,16 @@ SDQZ_API int sdqz_decompress_sections(sdqz_ctx* ctx, const sdqz_header* hdr, con
  * [c0, c0 + n_chunks) covering this rank's slab (device sections: the range's
  * chunk bit lengths and payload bytes, zero padded by >= 64 bytes), then
  * reconstruct the slab whose first code is `lo` codes into the range, with
- * the slab's outlier records (indices slab-local, ascending).  Checks as
- * decompress for the slab: decode errors, record range/order, codes[idx] == 0,
- * zero-code count of the slab.  Replaces the per-rank pipeline.py:42-58. */
+ * the slab's outlier records (ascending; index - idx_base is slab-local, so
+ * the records of a sharded archive are used as they are with idx_base = the
+ * slab's first point).  Checks as decompress for the slab: decode errors,
+ * record range/order, codes[idx] == 0, zero-code count of the slab.
+ * Replaces the per-rank pipeline.py:42-58. */
 SDQZ_API int sdqz_decompress_slab(sdqz_ctx* ctx, const sdqz_header* hdr, const uint8_t* d_bw,
-                                  const void* d_rec, uint64_t k, const uint32_t* d_chunk_bits,
-                                  uint64_t n_chunks, const uint8_t* d_payload, uint64_t payload_bytes,
-                                  uint64_t n_range, uint64_t lo, const uint64_t local_dims[3], void* d_out);
+                                  const void* d_rec, uint64_t k, uint64_t idx_base,
+                                  const uint32_t* d_chunk_bits, uint64_t n_chunks, const uint8_t* d_payload,
+                                  uint64_t payload_bytes, uint64_t n_range, uint64_t lo,
+                                  const uint64_t local_dims[3], void* d_out);
 
 #ifdef __cplusplus
 }

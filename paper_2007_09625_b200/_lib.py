@@ -45,6 +45,13 @@ class Header(Structure):
                 + self.payload_bytes)
 
 
+class ShardSizes(Structure):
+    """sdqz_shard_sizes (include/sdqz_cuda.h)."""
+
+    _fields_ = [("n_chunks", c_uint64), ("payload_bytes", c_uint64), ("n_outliers", c_uint64),
+                ("unit_width", c_uint32), ("max_bw", c_uint32), ("eb_resolved", c_double)]
+
+
 _SIGS = {
     "sdqz_ctx_create": (c_int, [c_int, c_void_p, POINTER(c_void_p)]),
     "sdqz_ctx_destroy": (c_int, [c_void_p]),
@@ -87,15 +94,22 @@ _SIGS = {
     "sdqz_archive_size": (c_uint64, [c_void_p]),
     "sdqz_archive_generation": (c_uint64, [c_void_p]),
     "sdqz_archive_write": (c_int, [c_void_p, c_uint64, c_void_p, c_uint64]),
+    "sdqz_archive_copy": (c_int, [c_void_p, c_uint64, c_void_p, c_void_p, c_void_p, c_void_p]),
     "sdqz_archive_sections": (c_int, [c_void_p, c_uint64, POINTER(c_void_p), POINTER(c_void_p),
                                       POINTER(c_void_p), POINTER(c_void_p)]),
     "sdqz_parse_header": (c_int, [c_void_p, c_void_p, c_uint64, POINTER(Header)]),
     "sdqz_decompress": (c_int, [c_void_p, c_void_p, c_uint64, c_void_p]),
     "sdqz_decompress_sections": (c_int, [c_void_p, POINTER(Header), c_void_p, c_void_p,
                                          c_void_p, c_void_p, c_void_p]),
-    "sdqz_decompress_slab": (c_int, [c_void_p, POINTER(Header), c_void_p, c_void_p, c_uint64, c_void_p,
-                                     c_uint64, c_void_p, c_uint64, c_uint64, c_uint64,
+    "sdqz_decompress_slab": (c_int, [c_void_p, POINTER(Header), c_void_p, c_void_p, c_uint64, c_uint64,
+                                     c_void_p, c_uint64, c_void_p, c_uint64, c_uint64, c_uint64,
                                      POINTER(c_uint64), c_void_p]),
+    "sdqz_shard_describe": (c_int, [c_void_p, c_void_p, c_int, c_uint64, c_void_p]),
+    "sdqz_shard_quantize": (c_int, [c_void_p, c_void_p, c_int, c_int, POINTER(c_uint64), POINTER(c_uint32),
+                                    c_int, c_double, c_uint32, c_void_p, c_void_p]),
+    "sdqz_shard_head": (c_int, [c_void_p, c_uint64, c_void_p]),
+    "sdqz_shard_encode": (c_int, [c_void_p, c_void_p, c_uint32, c_uint64, c_void_p, c_uint64, c_uint64,
+                                  POINTER(ShardSizes)]),
 }
 
 EXPORTS = tuple(_SIGS)
@@ -239,6 +253,6 @@ def env_flag(name: str) -> bool:
     return os.environ.get(name, "") not in ("", "0")
 
 
-__all__ = ["Context", "Header", "EXPORTS", "LIB_PATH", "load_library", "context", "dims3",
+__all__ = ["Context", "Header", "ShardSizes", "EXPORTS", "LIB_PATH", "load_library", "context", "dims3",
            "block3", "ptr", "require_cuda", "c_int", "c_uint32", "c_uint64", "c_double",
            "c_int64", "byref", "c_void_p"]

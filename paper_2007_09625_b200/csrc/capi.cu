@@ -65,6 +65,11 @@ void* scratch(sdqz_ctx* ctx, int slot, size_t bytes, cudaError_t* e) {
     return b.p;
 }
 
+uint64_t next_archive_gen() {
+    static std::atomic<uint64_t> next{1};   // unique across contexts
+    return next++;
+}
+
 void ensure_smem(const sdqz_ctx* ctx, const void* func, size_t bytes) {
     if (!bytes) return;
     static std::mutex mu;
@@ -90,6 +95,46 @@ __global__ void init_status_kernel(DevStatus* st, double eb, int has_eb) {
         st->two_eb = __dmul_rn(2.0, eb);
     }
 }
+
+// sharded compress: this slab's describe result as {-min, max, nonfinite}
+// doubles (an all-reduce MAX over the ranks gives the field's), and back
+__global__ void range_out_kernel(const DevStatus* st, int dtype, double* r) {
+    double vmin, vmax;
+    if (dtype == 0) {
+        vmin = (double)ord2f((uint32_t)st->vmin_bits);
+        vmax = (double)ord2f((uint32_t)st->vmax_bits);
+    } else {
+        vmin = ord2d(st->vmin_bits);
+        vmax = ord2d(st->vmax_bits);
+    }
+    r[0] = -vmin;
+    r[1] = vmax;
+    r[2] = (st->flags & F_NONFINITE) ? 1.0 : 0.0;
+}
+
+__global__ void range_in_kernel(const double* r, int dtype, DevStatus* st) {
+    if (dtype == 0) {   // the values were floats: exact round trip
+        st->vmin_bits = f2ord((float)(-r[0]));
+        st->vmax_bits = f2ord((float)r[1]);
+    } else {
+        st->vmin_bits = d2ord(-r[0]);
+        st->vmax_bits = d2ord(r[1]);
+    }
+    if (r[2] > 0.0) st->flags |= F_NONFINITE;
+}
+
+// records with global indices -> slab-local (an index below the base wraps to a
+// huge value, which the range check then reports)
+__global__ void rebase_records_kernel(const unsigned long long* in, uint64_t k, uint64_t base,
+                                      unsigned long long* out) {
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < k; i += (uint64_t)gridDim.x * blockDim.x) {
+        out[2 * i] = in[2 * i] - base;
+        out[2 * i + 1] = in[2 * i + 1];
+    }
+}
+
+// this slab's outlier count = its own histogram's bin 0 (before the all-reduce)
+__global__ void save_zeros_kernel(const unsigned long long* hist, unsigned long long* dst) { *dst = hist[0]; }
 
 }  // namespace
 
@@ -533,8 +578,7 @@ int compress_finish(sdqz_ctx* ctx, CompressState& c, sdqz_header* hdr) {
     h.payload_bytes = s.payload_bytes;
     ctx->last_hdr = h;
     ctx->have_archive = true;
-    static std::atomic<uint64_t> next_gen{1};   // unique across contexts
-    ctx->archive_gen = next_gen++;
+    ctx->archive_gen = next_archive_gen();
     if (hdr) *hdr = h;
     return SDQZ_OK;
 }
@@ -1074,6 +1118,202 @@ int sdqz_compress(sdqz_ctx* ctx, const void* d_in, int dtype, int ndims, const u
     return SDQZ_OK;
 }
 
+
+// ---------------------------------------------------------------------------
+// sharded compress: one rank's pipeline in three phases around
+// the caller's collectives -- all-reduce MAX of the range, all-reduce SUM of
+// the histogram -- with nothing but the final sizes coming back to the host.
+// ---------------------------------------------------------------------------
+int sdqz_shard_describe(sdqz_ctx* ctx, const void* d_in, int dtype, uint64_t n, double* d_range) {
+    int rc;
+    if ((rc = reset_status(ctx))) return rc;
+    if (n && (rc = launch_describe(ctx, d_in, dtype, n))) return rc;
+    range_out_kernel<<<1, 1, 0, ctx->stream>>>(ctx->d_status, dtype, d_range);
+    SDQZ_LAUNCHED_NAMED(ctx, "range_out_kernel");
+    return SDQZ_OK;
+}
+
+int sdqz_shard_quantize(sdqz_ctx* ctx, const void* d_in, int dtype, int ndims, const uint64_t dims[3],
+                        const uint32_t block[3], int eb_mode, double eb, uint32_t cap, const double* d_range,
+                        uint64_t* d_hist) {
+    int rc = SDQZ_OK;
+    if (ndims < 1 || ndims > 3) return set_error(ctx, SDQZ_EINVAL, "rank must be 1-3");
+    if (!valid_cap(cap)) return set_error(ctx, SDQZ_EINVAL, "bad cap");
+    ctx->have_archive = false;
+    const uint64_t n = prod3(dims);
+    auto& sh = ctx->shard;
+    sh = {};
+    sh.d_in = d_in;
+    sh.dtype = dtype;
+    sh.eb_mode = eb_mode;
+    sh.eb = eb;
+    sh.cap = cap;
+    sh.ndims = ndims;
+    sh.n = n;
+    for (int a = 0; a < 3; a++) { sh.dims[a] = dims[a]; sh.block[a] = block[a]; }
+    uint16_t* codes = scratch_as<uint16_t>(ctx, S_CODES, n + 64, &rc);
+    unsigned long long* zsave = scratch_as<unsigned long long>(ctx, S_MISC, 2, &rc);
+    if (!codes || !zsave) return rc;
+    if ((rc = reset_status(ctx))) return rc;
+    range_in_kernel<<<1, 1, 0, ctx->stream>>>(d_range, dtype, ctx->d_status);
+    SDQZ_LAUNCHED_NAMED(ctx, "range_in_kernel");
+    if ((rc = launch_resolve(ctx, dtype, eb_mode, eb))) return rc;
+    SDQZ_CUDA(ctx, cudaMemsetAsync(d_hist, 0, cap * 8ull, ctx->stream));
+    if (n && (rc = launch_dualquant(ctx, d_in, dtype, ndims, dims, block, cap, codes,
+                                    (unsigned long long*)d_hist)))
+        return rc;
+    save_zeros_kernel<<<1, 1, 0, ctx->stream>>>((const unsigned long long*)d_hist, zsave);
+    SDQZ_LAUNCHED_NAMED(ctx, "save_zeros_kernel");
+    sh.ready = true;
+    return SDQZ_OK;
+}
+
+int sdqz_shard_head(sdqz_ctx* ctx, uint64_t count, uint16_t* d_dst) {
+    const auto& sh = ctx->shard;
+    if (!sh.ready || count > sh.n) return set_error(ctx, SDQZ_EINVAL, "no quantized slab (or head too long)");
+    if (count)
+        SDQZ_CUDA(ctx, cudaMemcpyAsync(d_dst, ctx->bufs[S_CODES].p, count * 2, cudaMemcpyDeviceToDevice,
+                                       ctx->stream));
+    return SDQZ_OK;
+}
+
+int sdqz_shard_encode(sdqz_ctx* ctx, const uint64_t* d_hist, uint32_t chunk, uint64_t head,
+                      const uint16_t* d_tail, uint64_t n_tail, uint64_t idx_base, sdqz_shard_sizes* out) {
+    int rc = SDQZ_OK;
+    auto& sh = ctx->shard;
+    if (!sh.ready) return set_error(ctx, SDQZ_EINVAL, "no quantized slab");
+    if (chunk < 1) return set_error(ctx, SDQZ_EINVAL, "chunk_size must be >= 1");
+    if (head > sh.n) return set_error(ctx, SDQZ_EINVAL, "head longer than the slab");
+    *out = sdqz_shard_sizes{};
+    const uint32_t cap = sh.cap;
+    const uint64_t n_pack = sh.n - head + n_tail;
+    const uint64_t C = ceil_div(n_pack, chunk);
+    BookDev book;
+    if ((rc = book_tables(ctx, cap, &book))) return rc;
+    uint16_t* codes = (uint16_t*)ctx->bufs[S_CODES].p;
+    const uint16_t* src = codes + head;
+    if (n_tail) {   // a chunk straddles the slab end: own codes + the next ranks' head codes
+        uint16_t* cat = scratch_as<uint16_t>(ctx, S_WORK, n_pack + 64, &rc);
+        if (!cat) return rc;
+        SDQZ_CUDA(ctx, cudaMemcpyAsync(cat, src, (sh.n - head) * 2, cudaMemcpyDeviceToDevice, ctx->stream));
+        SDQZ_CUDA(ctx, cudaMemcpyAsync(cat + (sh.n - head), d_tail, n_tail * 2, cudaMemcpyDeviceToDevice,
+                                       ctx->stream));
+        src = cat;
+    }
+    uint32_t* cbits = scratch_as<uint32_t>(ctx, S_CHUNK_BITS, C + 20, &rc);   // (+ the head job's <= 16)
+    if (!cbits) return rc;
+    // the identical codebook on every rank (global histogram; K3 is deterministic)
+    if ((rc = launch_codebook(ctx, (const unsigned long long*)d_hist, book.bw, cap, book, true, true, false)))
+        return rc;
+    const int in_kind = sh.dtype;
+    const char* in_bytes = (const char*)sh.d_in;
+    const size_t esz = sh.dtype == 0 ? 4 : 8;
+    // outlier records: the head's (packed by the previous rank, values are ours)
+    // first, then the packed range's own points (global index = idx_base + local)
+    uint64_t head_k = 0;
+    unsigned long long* rec = nullptr;
+    uint64_t rec_cap = ctx->bufs[S_OUTREC].bytes ? ctx->bufs[S_OUTREC].bytes / 16 : (sh.n / 32 + 1024);
+    for (int attempt = 0; attempt < 2; attempt++) {
+        rec = scratch_as<unsigned long long>(ctx, S_OUTREC, 2 * (rec_cap + 1), &rc);
+        uint64_t pay_cap = ctx->bufs[S_PAYLOAD].bytes ? ctx->bufs[S_PAYLOAD].bytes : (n_pack / 2 + C + 4096);
+        uint8_t* payload = scratch_as<uint8_t>(ctx, S_PAYLOAD, pay_cap, &rc);
+        if (!rec || !payload) return rc;
+        pay_cap = ctx->bufs[S_PAYLOAD].bytes;
+        rec_cap = ctx->bufs[S_OUTREC].bytes / 16;
+        SDQZ_CUDA(ctx, cudaMemsetAsync(&ctx->d_status->flags, 0, 8, ctx->stream));   // keep eb, max_bw
+        head_k = 0;
+        if (head) {
+            DeflateJob hj;
+            hj.codes = codes;
+            hj.n = head;
+            hj.chunk = 4096;
+            hj.cap = cap;
+            hj.chunk_bits = cbits;   // scratch use only; rewritten below
+            hj.payload_cap = ~0ull;
+            hj.in = sh.d_in;
+            hj.in_kind = in_kind;
+            hj.idx_base = idx_base;
+            hj.out_records = rec;
+            hj.out_cap = rec_cap;
+            hj.want_payload = false;
+            hj.trusted = true;
+            if ((rc = launch_deflate(ctx, hj))) return rc;
+            if ((rc = fetch_status(ctx))) return rc;
+            head_k = ctx->h_status->n_outliers;
+            if (head_k > rec_cap) { rec_cap = 2 * head_k + sh.n / 32; continue; }
+        }
+        DeflateJob job;
+        job.codes = src;
+        job.n = n_pack;
+        job.chunk = chunk;
+        job.entries = book.entries;
+        job.cap = cap;
+        job.chunk_bits = cbits;
+        job.payload = payload;
+        job.payload_cap = pay_cap;
+        job.in = in_bytes + head * esz;
+        job.in_kind = in_kind;
+        job.idx_base = idx_base + head;
+        job.rec_limit = sh.n - head;   // the tail's outliers belong to the next ranks
+        job.out_records = rec + 2 * head_k;
+        job.out_cap = rec_cap - head_k;
+        job.trusted = true;
+        if (n_pack && (rc = launch_deflate(ctx, job))) return rc;
+        // this slab's outlier count (its histogram bin 0, saved before the all-reduce)
+        SDQZ_CUDA(ctx, cudaMemcpyAsync(&ctx->d_status->bad_count, ctx->bufs[S_MISC].p, 8,
+                                       cudaMemcpyDeviceToDevice, ctx->stream));
+        if ((rc = fetch_status(ctx))) return rc;
+        const DevStatus& s = *ctx->h_status;
+        if (!(s.flags & F_OVERFLOW)) break;
+        if (attempt == 1) return set_error(ctx, SDQZ_EINVAL, "internal: capacity still exceeded");
+        // grow to the exact sizes the scan reported and redo
+        if (!scratch_as<uint8_t>(ctx, S_PAYLOAD, s.payload_bytes + 64, &rc)) return rc;
+        rec_cap = head_k + s.n_outliers + 1;
+    }
+    const DevStatus& s = *ctx->h_status;
+    // resolve_error_bound / QuantConfig order (core.py:161-175)
+    if (s.flags & F_NONFINITE)
+        return set_error(ctx, SDQZ_EINVAL, "field contains NaN/Inf values and cannot be compressed");
+    if (!(sh.eb > 0 && std::isfinite(sh.eb))) return set_error(ctx, SDQZ_EINVAL, "error bound must be positive");
+    if (s.flags & F_RANGE_ZERO)
+        return set_error(ctx, SDQZ_EINVAL,
+                         "value-range-relative bound is undefined on a constant field; use an "
+                         "absolute error bound instead");
+    if (!(s.eb > 0 && std::isfinite(s.eb)))
+        return set_error(ctx, SDQZ_EINVAL, "error bound must be positive and finite");
+    if ((rc = table_error(ctx, s.flags, false))) return rc;
+    {   // zero padding after the payload (decoders peek past the last chunk)
+        auto& pb = ctx->bufs[S_PAYLOAD];
+        const uint64_t P = n_pack ? s.payload_bytes : 0;
+        SDQZ_CUDA(ctx, cudaMemsetAsync((uint8_t*)pb.p + P, 0, std::min<uint64_t>(64, pb.bytes - P), ctx->stream));
+    }
+    out->n_chunks = C;
+    out->payload_bytes = n_pack ? s.payload_bytes : 0;
+    out->n_outliers = s.bad_count;   // == head_k + the packed range's own records
+    out->max_bw = (uint32_t)s.max_bw;
+    out->unit_width = (uint32_t)unit_for((uint32_t)s.max_bw);
+    out->eb_resolved = s.eb;
+    // the rank's sections are this context's archive (sdqz_archive_sections)
+    sdqz_header h{};
+    h.dtype_code = (uint8_t)sh.dtype;
+    h.ndims = (uint8_t)sh.ndims;
+    h.eb_mode = (uint8_t)sh.eb_mode;
+    h.unit_width = (uint8_t)out->unit_width;
+    for (int a = 0; a < 3; a++) { h.dims[a] = sh.dims[a]; h.block[a] = sh.block[a]; }
+    h.eb_resolved = s.eb;
+    h.eb_specified = sh.eb;
+    h.cap = cap;
+    h.chunk_size = chunk;
+    h.n_outliers = out->n_outliers;
+    h.n_chunks = C;
+    h.payload_bytes = out->payload_bytes;
+    ctx->last_hdr = h;
+    ctx->have_archive = true;
+    ctx->archive_gen = next_archive_gen();
+    sh.ready = false;
+    return SDQZ_OK;
+}
+
 uint64_t sdqz_archive_size(const sdqz_ctx* ctx) {
     return ctx->have_archive ? archive_total(ctx->last_hdr) : 0;
 }
@@ -1097,6 +1337,20 @@ int sdqz_archive_sections(sdqz_ctx* ctx, uint64_t gen, const uint8_t** d_bw, con
     *d_outliers = ctx->bufs[S_OUTREC].p;
     *d_chunk_bits = (const uint32_t*)ctx->bufs[S_CHUNK_BITS].p;
     *d_payload = (const uint8_t*)ctx->bufs[S_PAYLOAD].p;
+    return SDQZ_OK;
+}
+
+int sdqz_archive_copy(sdqz_ctx* ctx, uint64_t gen, uint8_t* d_bw, void* d_outliers, uint32_t* d_chunk_bits,
+                      uint8_t* d_payload) {
+    if (int rc = check_archive(ctx, gen)) return rc;
+    const sdqz_header& h = ctx->last_hdr;
+    const Seg segs[4] = {{d_bw, h.cap}, {d_outliers, 16 * h.n_outliers}, {d_chunk_bits, 4ull * h.n_chunks},
+                         {d_payload, h.payload_bytes}};
+    const int slots[4] = {S_BW, S_OUTREC, S_CHUNK_BITS, S_PAYLOAD};
+    for (int i = 0; i < 4; i++)
+        if (segs[i].len && segs[i].dev)
+            SDQZ_CUDA(ctx, cudaMemcpyAsync(segs[i].dev, ctx->bufs[slots[i]].p, segs[i].len, cudaMemcpyDeviceToDevice,
+                                           ctx->stream));
     return SDQZ_OK;
 }
 
@@ -1166,9 +1420,9 @@ int sdqz_decompress_sections(sdqz_ctx* ctx, const sdqz_header* hdr, const uint8_
 }
 
 int sdqz_decompress_slab(sdqz_ctx* ctx, const sdqz_header* hdr, const uint8_t* d_bw, const void* d_rec,
-                         uint64_t k, const uint32_t* d_chunk_bits, uint64_t n_chunks, const uint8_t* d_payload,
-                         uint64_t payload_bytes, uint64_t n_range, uint64_t lo, const uint64_t local_dims[3],
-                         void* d_out) {
+                         uint64_t k, uint64_t idx_base, const uint32_t* d_chunk_bits, uint64_t n_chunks,
+                         const uint8_t* d_payload, uint64_t payload_bytes, uint64_t n_range, uint64_t lo,
+                         const uint64_t local_dims[3], void* d_out) {
     int rc = SDQZ_OK;
     const uint32_t cap = hdr->cap;
     uint64_t ldims[3] = {1, 1, 1};
@@ -1182,6 +1436,14 @@ int sdqz_decompress_slab(sdqz_ctx* ctx, const sdqz_header* hdr, const uint8_t* d
     }
     if (lo + n_local > n_range) return set_error(ctx, SDQZ_EINVAL, "slab outside the chunk range");
     if (n_local == 0) return SDQZ_OK;
+    if (idx_base && k) {   // global record indices -> slab-local (a rebased copy)
+        unsigned long long* r2 = scratch_as<unsigned long long>(ctx, S_REBASE, 2 * k, &rc);
+        if (!r2) return rc;
+        rebase_records_kernel<<<(unsigned)umin(ceil_div(k, 256), 4096), 256, 0, ctx->stream>>>(
+            (const unsigned long long*)d_rec, k, idx_base, r2);
+        SDQZ_LAUNCHED_NAMED(ctx, "rebase_records_kernel");
+        d_rec = r2;
+    }
     BookDev book;
     if ((rc = book_tables(ctx, cap, &book))) return rc;
     uint16_t* codes = scratch_as<uint16_t>(ctx, S_CODES, n_range + 64, &rc);

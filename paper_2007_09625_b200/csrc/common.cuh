@@ -176,6 +176,18 @@ struct sdqz_ctx {
     uint64_t archive_gen = 0;   // id of the last compress's archive (0: none);
                                 // handles holding another id are stale
 
+    // sharded compress in progress (sdqz_shard_quantize -> sdqz_shard_encode)
+    struct Shard {
+        const void* d_in = nullptr;
+        int dtype = 0, eb_mode = 0, ndims = 0;
+        double eb = 0;
+        uint32_t cap = 0;
+        uint64_t n = 0;
+        uint64_t dims[3] = {1, 1, 1};
+        uint32_t block[3] = {1, 1, 1};
+        bool ready = false;
+    } shard;
+
     // captured pipelines (CUDA graphs), valid while the scratch arena's
     // generation is unchanged
     struct Graph {
@@ -204,7 +216,7 @@ namespace sdqz {
 enum Slot : int {
     S_CODES = 0, S_HIST, S_BW, S_ENTRIES, S_FIRST, S_OFFSETS, S_SYMBOLS, S_LUT,
     S_CHUNK_BITS, S_CHUNK_AUX, S_BYTE_OFF, S_OUT_OFF, S_PAYLOAD, S_OUTREC, S_SORT,
-    S_TREE, S_STAGE, S_DENSE, S_WORK, S_BLOCKFLAG, S_MISC, S_REDO, S_DTAB, S_COUNTER, S_QUAL, S_NSLOTS
+    S_TREE, S_STAGE, S_DENSE, S_WORK, S_BLOCKFLAG, S_MISC, S_REDO, S_DTAB, S_COUNTER, S_QUAL, S_REBASE, S_NSLOTS
 };
 
 int set_error(sdqz_ctx* ctx, int code, const std::string& msg);
@@ -219,6 +231,7 @@ int reset_status_eb(sdqz_ctx* ctx, double eb, bool has_eb);   // ... and set eb 
 // kernel's limit on the context's device to >= bytes (remembered per
 // (kernel, device) under a lock).
 void ensure_smem(const sdqz_ctx* ctx, const void* func, size_t bytes);
+uint64_t next_archive_gen();   // process-unique archive ids
 
 #define SDQZ_CUDA(ctx, expr)                                                      \
     do {                                                                          \

@@ -541,6 +541,7 @@ struct DeflateArgs {
     uint64_t in_split;
     const void* in_tail;
     uint64_t idx_base;
+    uint64_t rec_limit;                  // records only for indices below (sharded: own slab)
     unsigned long long* records;         // {idx, f64 bits} pairs
     unsigned long long out_cap;
     DevStatus* st;
@@ -877,9 +878,11 @@ __global__ void __launch_bounds__(256) chunk_pack_kernel(DeflateArgs a) {
                 for (int k = 0; k < 8; k++) {
                     const uint64_t i = i0 + k;
                     if (i < e && code8[k] == 0) {
-                        double v = outlier_value(a, i, two_eb);
-                        a.records[2 * slot] = i + a.idx_base;
-                        a.records[2 * slot + 1] = (unsigned long long)__double_as_longlong(v);
+                        if (i < a.rec_limit) {
+                            const double v = outlier_value(a, i, two_eb);
+                            a.records[2 * slot] = i + a.idx_base;
+                            a.records[2 * slot + 1] = (unsigned long long)__double_as_longlong(v);
+                        }
                         slot++;
                     }
                 }
@@ -1042,9 +1045,11 @@ __global__ void __launch_bounds__(256, 3) chunk_pack32_kernel(DeflateArgs a) {
                 for (int k = 0; k < kRun; k++) {
                     if ((uint32_t)k < cnt && code[k] == 0) {
                         const uint64_t i = i0 + k;
-                        const double v = outlier_value(a, i, two_eb);
-                        a.records[2 * slot] = i + a.idx_base;
-                        a.records[2 * slot + 1] = (unsigned long long)__double_as_longlong(v);
+                        if (i < a.rec_limit) {
+                            const double v = outlier_value(a, i, two_eb);
+                            a.records[2 * slot] = i + a.idx_base;
+                            a.records[2 * slot + 1] = (unsigned long long)__double_as_longlong(v);
+                        }
                         slot++;
                     }
                 }
@@ -1184,9 +1189,11 @@ __global__ void __launch_bounds__(256) chunk_pack_run_kernel(DeflateArgs a, int 
                 for (int k = 0; k < kRun; k++) {
                     if ((uint32_t)k < cnt && code[k] == 0) {
                         const uint64_t i = i0 + k;
-                        const double v = outlier_value(a, i, two_eb);
-                        a.records[2 * slot] = i + a.idx_base;
-                        a.records[2 * slot + 1] = (unsigned long long)__double_as_longlong(v);
+                        if (i < a.rec_limit) {
+                            const double v = outlier_value(a, i, two_eb);
+                            a.records[2 * slot] = i + a.idx_base;
+                            a.records[2 * slot + 1] = (unsigned long long)__double_as_longlong(v);
+                        }
                         slot++;
                     }
                 }
@@ -1507,6 +1514,7 @@ int launch_deflate(sdqz_ctx* ctx, const DeflateJob& job) {
     a.in_split = job.in_split;
     a.in_tail = job.in_tail;
     a.idx_base = job.idx_base;
+    a.rec_limit = job.rec_limit;
     a.records = (unsigned long long*)job.out_records;
     a.out_cap = job.out_cap;
     a.trusted = job.trusted;

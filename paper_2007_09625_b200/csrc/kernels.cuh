@@ -52,6 +52,7 @@ struct DeflateJob {
     uint64_t in_split = ~0ull;           // indices >= in_split read from `in_tail`
     const void* in_tail = nullptr;
     uint64_t idx_base = 0;               // added to every emitted index
+    uint64_t rec_limit = ~0ull;          // records only for (job-local) indices below this
     void* out_records = nullptr;         // {u64, f64}[max]
     uint64_t out_cap = 0;
     bool want_payload = true;

@@ -22,12 +22,13 @@ import torch.distributed as dist
 import torch.multiprocessing as mp
 
 from oracle import sdqz_oracle as O
+import paper_2007_09625_b200 as S
 from paper_2007_09625_b200 import sharded
-from paper_2007_09625_b200.sharded import Book
 
 
 class OracleShardOps:
-    """Checker backend: the oracle's stages behind the DeviceShardOps interface."""
+    """Checker backend: the oracle's stages behind the DeviceShardOps interface
+    (describe -> quantize -> head -> encode; decompress_slab)."""
 
     device = torch.device("cpu")
 
@@ -38,42 +39,66 @@ class OracleShardOps:
         return torch.from_numpy(a.copy()), np.dtype(dt)
 
     def describe(self, t, dt):
+        if t.numel() == 0:
+            return torch.tensor([-np.inf, -np.inf, 0.0], dtype=torch.float64)
         vmin, vmax, nf, _ = O.describe(t.numpy())
-        return vmin, vmax, nf
+        return torch.tensor([-vmin, vmax, 1.0 if nf else 0.0], dtype=torch.float64)
 
-    def quantize(self, t, dt, local_dims, cfg):
-        codes, oi, ov = O.dualquant(t.numpy(), local_dims, cfg.eb, cfg.cap, cfg.block_shape)
-        self._out = (oi, ov)
-        c16 = torch.from_numpy(codes.astype(np.uint16).view(np.int16).copy())
-        return c16, torch.from_numpy(O.histogram(codes, cfg.cap)), False
+    def quantize(self, t, dt, local_dims, block, mode, eb, cap, rng):
+        r = rng.numpy()
+        self.eb = O.resolve_eb(mode, eb, -r[0], r[1], r[2] > 0)
+        self.cap = cap
+        if t.numel():
+            codes, oi, ov = O.dualquant(t.numpy(), local_dims, self.eb, cap, block)
+        else:
+            codes, oi, ov = np.zeros(0, np.uint32), np.zeros(0, np.uint64), np.zeros(0)
+        self.codes, self.oi, self.ov = codes.reshape(-1), oi, ov
+        return torch.from_numpy(O.histogram(self.codes, cap))
 
-    def codebook(self, hist, cap):
-        bw = O.tree_bitwidths(hist.numpy())
-        book = O.canonical_book(bw)
-        return Book(bw.astype(np.uint8), book.unit, int(book.max_bw), book)
+    def head(self, count):
+        return torch.from_numpy(self.codes[:count].astype(np.uint16).view(np.int16).copy())
 
-    def deflate(self, codes, chunk, book, cap):
-        c = codes.numpy().view(np.uint16).astype(np.uint32)
-        bits, payload = O.deflate(O.encode(c, book.handle), chunk)
-        return (torch.from_numpy(bits.view(np.int32).copy()),
-                torch.from_numpy(np.frombuffer(payload, np.uint8).copy()))
+    def encode(self, hist, chunk, head, tail, idx_base):
+        book = O.canonical_book(O.tree_bitwidths(hist.numpy()))
+        parts = [self.codes[head:]]
+        if tail is not None:
+            parts.append(tail.numpy().view(np.uint16).astype(np.uint32))
+        packed = np.concatenate(parts)
+        if packed.size:
+            bits, payload = O.deflate(O.encode(packed, book), chunk)
+        else:
+            bits, payload = np.zeros(0, np.uint32), b""
+        rec = np.empty((self.oi.size, 2), np.int64)
+        rec[:, 0] = self.oi.astype(np.int64) + idx_base
+        rec[:, 1] = self.ov.astype(np.float64).view(np.int64)
+        pay = np.zeros(len(payload) + 64, np.uint8)
+        pay[: len(payload)] = np.frombuffer(payload, np.uint8)
+        bw = O.tree_bitwidths(hist.numpy()).astype(np.uint8)
+        sec = {"bitwidths": torch.from_numpy(bw), "outliers": torch.from_numpy(rec.reshape(-1)),
+               "chunk_bits": torch.from_numpy(bits.astype(np.uint32).view(np.int32).copy()),
+               "payload": torch.from_numpy(pay), "payload_bytes": len(payload)}
+        sizes = {"n_chunks": int(bits.size), "payload_bytes": len(payload), "n_outliers": int(self.oi.size),
+                 "unit_width": int(book.unit), "eb_resolved": float(self.eb)}
+        return sizes, sec
 
-    def outliers(self, t, dt, codes, eb):
-        oi, ov = self._out
-        rec = np.empty((oi.size, 2), np.int64)
-        rec[:, 0] = oi.astype(np.int64)
-        rec[:, 1] = ov.astype(np.float64).view(np.int64)
-        return torch.from_numpy(rec.reshape(-1))
-
-    def inflate(self, payload, chunk_bits, chunk, n_codes, bitwidths):
-        book = O.canonical_book(bitwidths)
-        return O.inflate(chunk_bits, payload.tobytes(), chunk, book, n_codes)
-
-    def reconstruct(self, codes, idx, vals, local_dims, cfg, dtype):
+    def decompress_slab(self, h, bw, rec, k, idx_base, bits, payload, payload_bytes, n_range, lo, local_dims):
+        book = O.canonical_book(bw.numpy())
+        codes = O.inflate(bits.numpy().view(np.uint32), payload.numpy()[:payload_bytes].tobytes(),
+                          h.chunk_size, book, n_range)
         n = math.prod(local_dims)
-        O.validate_quant(codes, idx, vals, n, cfg.cap)
-        v = O.reconstruct(codes, idx, vals, local_dims, cfg.eb, cfg.cap, cfg.block_shape)
-        return v.reshape(local_dims).astype(dtype)
+        codes = np.asarray(codes)[lo: lo + n]
+        r = rec.numpy().reshape(-1, 2)[:k]
+        idx = r[:, 0].astype(np.uint64) - np.uint64(idx_base)
+        vals = r[:, 1].view(np.float64)
+        O.validate_quant(codes, idx, vals, n, h.cap)
+        v = O.reconstruct(codes, idx, vals, local_dims, h.eb_resolved, h.cap, h.block_shape[: h.ndims])
+        return torch.from_numpy(v.reshape(local_dims).astype(h.np_dtype))
+
+    def upload(self, a):
+        return torch.from_numpy(np.ascontiguousarray(a).copy())
+
+    def to_numpy(self, t):
+        return t.numpy()
 
 
 def _free_port():
@@ -84,7 +109,7 @@ def _free_port():
     return port
 
 
-def _worker(rank, world, port, case, backend, q):
+def _worker(rank, world, port, case, backend, q, tmpdir):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
@@ -92,9 +117,16 @@ def _worker(rank, world, port, case, backend, q):
         data, dims, rows, kw = case
         r0 = sum(rows[:rank])
         local = data.reshape(dims)[r0: r0 + rows[rank]] if len(dims) > 1 else data[r0: r0 + rows[rank]]
-        blob = sharded.compress_sharded(local, dims, ops=ops, **kw)
-        slab = sharded.decompress_sharded(blob, rows=rows, ops=ops)
-        q.put((rank, blob, slab))
+        ar = sharded.compress_sharded_device(local, dims, ops=ops, **kw)
+        blob = ar.to_bytes()
+        path = os.path.join(tmpdir, "sharded.sdqz")
+        ar.write(path)
+        with open(path, "rb") as f:
+            written = f.read()
+        gathered = ar.gather(root=0)
+        slab = sharded.decompress_sharded(blob, rows=rows, ops=ops)             # bytes path
+        slab2 = sharded.decompress_sharded(ar, ops=ops)                          # in place (or fallback)
+        q.put((rank, (blob, written, gathered), (slab, slab2)))
     except Exception as e:  # surfaced by the parent
         q.put((rank, e, None))
     finally:
@@ -102,10 +134,13 @@ def _worker(rank, world, port, case, backend, q):
 
 
 def run_sharded(case, world, backend="oracle"):
+    import tempfile
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, world, port, case, backend, q)) for r in range(world)]
+    tmpdir = tempfile.mkdtemp(prefix="sdqz_sharded_")
+    procs = [ctx.Process(target=_worker, args=(r, world, port, case, backend, q, tmpdir))
+             for r in range(world)]
     for p in procs:
         p.start()
     res = dict()
@@ -133,21 +168,38 @@ CASES = [
     ("2d-default-chunk", (70, 50), [32, 38], dict(eb=1e-4, mode="valrel")),
     ("2d-empty-slab", (40, 33), [32, 0, 8], dict(eb=1e-2, mode="valrel", chunk_size=300)),
     ("3d-cap64-outliers", (16, 12, 20), [8, 8], dict(eb=1e-5, mode="valrel", cap=64, chunk_size=512)),
+    # slabs on chunk boundaries (the 2048x2048x1024 layout in miniature): in-place decompress
+    ("3d-chunk-aligned", (32, 16, 32), [8, 16, 8], dict(eb=1e-4, mode="valrel", chunk_size=512)),
+    ("3d-aligned-4ranks", (64, 24, 40), [16, 16, 16, 16], dict(eb=1e-4, mode="valrel", chunk_size=3840)),
 ]
+
+
+def _field(name, dims):
+    data = _smooth(dims)
+    if name.startswith("3d-cap64"):
+        data = data + np.random.default_rng(3).normal(0, 0.3, data.shape).astype(np.float32)
+    return data
+
+
+def _check(ref, dims, outs, slabs):
+    """Every assembly path gives the single-field archive; both decompress
+    paths give its decompressed field."""
+    dec = O.decompress(ref)
+    for r, (blob, written, gathered) in enumerate(outs):
+        assert blob == ref
+        assert written == ref
+        assert gathered == (ref if r == 0 else None)
+    for k in range(2):
+        got = np.concatenate([np.asarray(s[k]).reshape((-1,) + tuple(dims[1:])) for s in slabs], axis=0)
+        assert np.array_equal(got.reshape(dec.shape).view(np.uint32), dec.view(np.uint32)), k
 
 
 @pytest.mark.parametrize("name,dims,rows,kw", CASES, ids=[c[0] for c in CASES])
 def test_sharded_archive_equals_single_field(name, dims, rows, kw):
-    data = _smooth(dims)
-    if name.startswith("3d-cap64"):
-        data = data + np.random.default_rng(3).normal(0, 0.3, data.shape).astype(np.float32)
+    data = _field(name, dims)
     ref = O.compress(data, dims, **kw)
-    blobs, slabs = run_sharded((data.reshape(-1), dims, rows, kw), len(rows))
-    for b in blobs:
-        assert b == ref
-    dec = O.decompress(ref)
-    got = np.concatenate([s.reshape((-1,) + tuple(dims[1:])) for s in slabs], axis=0)
-    assert np.array_equal(got.reshape(dec.shape).view(np.uint32), dec.view(np.uint32))
+    outs, slabs = run_sharded((data.reshape(-1), dims, rows, kw), len(rows))
+    _check(ref, dims, outs, slabs)
 
 
 def test_slab_rows_split():
@@ -162,30 +214,49 @@ def test_misaligned_slab_rejected():
         run_sharded((_smooth(dims).reshape(-1), dims, [7, 13], dict(eb=1e-3)), 2)
 
 
-@pytest.mark.gpu
-def test_sharded_device_two_ranks_one_gpu():
-    dims = (24, 40, 56)
-    kw = dict(eb=1e-4, mode="valrel", chunk_size=1024)
-    data = _smooth(dims)
-    ref = O.compress(data, dims, **kw)
-    blobs, slabs = run_sharded((data.reshape(-1), dims, [8, 16], kw), 2, backend="device")
-    assert blobs[0] == ref and blobs[1] == ref
-    got = np.concatenate(slabs, axis=0)
-    assert np.array_equal(got.view(np.uint32), O.decompress(ref).view(np.uint32))
+def _decompress_worker(rank, world, port, blob, rows, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        sharded.decompress_sharded(blob, rows=rows, ops=OracleShardOps())
+        q.put((rank, None))
+    except Exception as e:
+        q.put((rank, e))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_decompress_misaligned_rows_rejected():
+    """Caller-supplied slab heights must be whole block rows (as compress
+    requires), or the slab's block grid would not match the encoder's."""
+    dims = (20, 6, 6)
+    blob = O.compress(_smooth(dims), dims, eb=1e-3)
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_decompress_worker, args=(r, 2, port, blob, [7, 13], q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    errs = [q.get(timeout=120)[1] for _ in range(2)]
+    for p in procs:
+        p.join(60)
+    assert all(isinstance(e, Exception) and "multiple of the block extent" in str(e) for e in errs)
+
+
+def test_record_checks():
+    with pytest.raises(S.ArchiveFormatError, match="not strictly ascending"):
+        sharded._validate_records(np.array([3, 3], np.uint64), 10)
+    with pytest.raises(S.ArchiveFormatError, match="out of range"):
+        sharded._validate_records(np.array([3, 10], np.uint64), 10)
 
 
 @pytest.mark.gpu
 @pytest.mark.parametrize("name,dims,rows,kw", CASES, ids=[c[0] for c in CASES])
 def test_sharded_device_cases(name, dims, rows, kw):
-    """Every protocol case through the device backend (sdqz_decompress_slab):
-    straddling chunks, a chunk spanning three slabs, an empty slab, outliers."""
-    data = _smooth(dims)
-    if name.startswith("3d-cap64"):
-        data = data + np.random.default_rng(3).normal(0, 0.3, data.shape).astype(np.float32)
+    """Every protocol case through the fused device pipeline (sdqz_shard_*,
+    sdqz_decompress_slab), ranks sharing cuda:0 over gloo: straddling chunks,
+    a chunk spanning three slabs, an empty slab, outliers, in-place decompress."""
+    data = _field(name, dims)
     ref = O.compress(data, dims, **kw)
-    blobs, slabs = run_sharded((data.reshape(-1), dims, rows, kw), len(rows), backend="device")
-    for b in blobs:
-        assert b == ref
-    dec = O.decompress(ref)
-    got = np.concatenate([s.reshape((-1,) + tuple(dims[1:])) for s in slabs], axis=0)
-    assert np.array_equal(got.reshape(dec.shape).view(np.uint32), dec.view(np.uint32))
+    outs, slabs = run_sharded((data.reshape(-1), dims, rows, kw), len(rows), backend="device")
+    _check(ref, dims, outs, slabs)
