@@ -482,6 +482,150 @@ def ours_arm(args, cfg, world, rank, local_rank):
     return 0
 
 
+def sharded_arm(args, cfg, world, rank, local_rank):
+    """N > 1: the config's field split into slabs of whole block rows over the
+    ranks (strong scaling: the field is fixed, each rank holds 1/N of it),
+    compressed into one ShardedArchive and decompressed in place
+    (paper_2007_09625_b200.sharded)."""
+    import hashlib
+
+    import torch
+    import torch.distributed as dist
+
+    from paper_2007_09625_b200 import _lib, sharded, synthetic
+    from paper_2007_09625_b200.core import QuantConfig
+
+    dims = cfg["dims"]
+    n = math.prod(dims)
+    inner = math.prod(dims[1:])
+    b0 = QuantConfig.for_rank(1.0, len(dims)).block_shape[0]
+    rows = sharded.slab_rows(dims[0], b0, world)
+    r0 = sum(rows[:rank])
+    n_local = rows[rank] * inner
+    # this rank's slab of the reference's smooth field (bit-identical rows)
+    t0 = time.perf_counter()
+    pinned = torch.empty(max(n_local, 1), dtype=torch.float32, pin_memory=True)
+    arr = pinned.numpy()
+    step_rows = max(1, (1 << 24) // max(1, inner))
+    from concurrent.futures import ThreadPoolExecutor
+
+    def fill(a):
+        b = min(rows[rank], a + step_rows)
+        arr[a * inner:b * inner] = synthetic.smooth_rows(dims, 1, (r0 + a, r0 + b)).astype(np.float32).reshape(-1)
+
+    with ThreadPoolExecutor(max_workers=max(1, min(16, (os.cpu_count() or 1) // world))) as ex:
+        list(ex.map(fill, range(0, rows[rank], step_rows)))
+    local_dims = (rows[rank],) + tuple(dims[1:])
+    d_in = pinned[:n_local].cuda().view(local_dims)
+    log(f"rank {rank}: slab rows [{r0}, {r0 + rows[rank]}) generated in {time.perf_counter() - t0:.1f} s")
+    ctx = _lib.context()
+    kw = dict(eb=cfg["eb"], mode=cfg["mode"])
+
+    def step():
+        ar = sharded.compress_sharded_device(d_in, dims, **kw)
+        out = sharded.decompress_sharded(ar, device=True)
+        return ar, out
+
+    for _ in range(max(args.warmup, 1)):
+        ar, out = step()
+    # parity guard: the assembled archive is the reference's (gathered once,
+    # outside the timed region), and the slab's error bound holds
+    golden = golden_for(cfg["golden"])
+    blob = ar.gather(root=0)
+    sha = hashlib.sha256(blob).hexdigest() if blob is not None else None
+    del blob
+    import paper_2007_09625_b200 as S
+    err = S.quality(d_in.reshape(-1), out.reshape(-1)).max_abs_error if n_local else 0.0
+    assert err <= ar.header.eb_resolved * (1 + 1e-9) + 2 * np.spacing(np.float32(8)), err
+    del out
+    stream = torch.cuda.current_stream()
+    ev = [[torch.cuda.Event(enable_timing=True) for _ in range(3)] for _ in range(args.steps)]
+    dist.barrier()
+    torch.cuda.synchronize()
+    launches0 = ctx.launches
+    with Clocks(torch.cuda.current_device()) as clk:
+        for i in range(args.steps):
+            ev[i][0].record(stream)
+            ar = sharded.compress_sharded_device(d_in, dims, **kw)
+            ev[i][1].record(stream)
+            out = sharded.decompress_sharded(ar, device=True)
+            ev[i][2].record(stream)
+            del out
+        torch.cuda.synchronize()
+    dist.barrier()
+    launches = ctx.launches - launches0
+    c_ms = [a.elapsed_time(b) for a, b, c in ev]
+    d_ms = [b.elapsed_time(c) for a, b, c in ev]
+    tt = torch.tensor([sum(c_ms) + sum(d_ms), statistics.median(c_ms), statistics.median(d_ms)],
+                      dtype=torch.float64)
+    tt = tt.cuda() if dist.get_backend() == "nccl" else tt
+    dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+    t_max, c_med, d_med = (float(x) for x in tt.cpu())
+    value = 4 * n * args.steps / (t_max / 1e3) / 1e9
+
+    # e2e through the public API with host buffers: this rank's pinned slab ->
+    # device -> compress_sharded_device -> ShardedArchive.write (every rank
+    # writes its own byte ranges of one archive file) -> decompress_sharded ->
+    # host slab
+    path = os.environ.get("SDQZ_BENCH_ARCHIVE", f"/dev/shm/sdqz_bench_{os.getpid() if world == 1 else 'n' + str(world)}.sdqz")
+    host_out = torch.empty(max(n_local, 1), dtype=torch.float32, pin_memory=True)
+    e2e_steps = max(2, min(args.steps, 3))
+    dist.barrier()
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    for _ in range(e2e_steps):
+        d = pinned[:n_local].cuda().view(local_dims)
+        ar = sharded.compress_sharded_device(d, dims, **kw)
+        nbytes = ar.write(path)
+        o = sharded.decompress_sharded(ar, device=True)
+        host_out[:n_local].copy_(o.reshape(-1))
+        del d, o
+    torch.cuda.synchronize()
+    te = torch.tensor([time.perf_counter() - t0], dtype=torch.float64)
+    te = te.cuda() if dist.get_backend() == "nccl" else te
+    dist.all_reduce(te, op=dist.ReduceOp.MAX)
+    te = float(te.cpu())
+    my_bytes = 16 * int(ar.rank_sizes[rank, 2]) + 4 * int(ar.rank_sizes[rank, 0]) + int(ar.rank_sizes[rank, 1])
+    if rank == 0:
+        try:
+            os.remove(path)
+        except OSError:
+            pass
+        line = {
+            "metric": METRIC, "value": value, "unit": "GB/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": t_max / args.steps,
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic",
+            "config": {"workload": args.config, "desc": cfg["desc"], "dims": list(dims), "eb": cfg["eb"],
+                       "mode": cfg["mode"], "cap": 1024,
+                       "profile": "smooth (reference synthetic.py), seed 1, fp32, bit-identical slab rows",
+                       "parallelism": f"{world} slabs of {rows[0]} rows (axis 0), one GPU each",
+                       "collective_backend": dist.get_backend(),
+                       "l2": "inputs larger than L2 (per-rank slab >= 2 GB)",
+                       "per_rank_points": n_local},
+            "compress_gbs": 4 * n / (c_med / 1e3) / 1e9,
+            "decompress_gbs": 4 * n / (d_med / 1e3) / 1e9,
+            "compression_ratio": 4 * n / ar.nbytes,
+            "parity": {"archive_sha256": sha,
+                       "reference_sha256": golden["archive_sha256"] if golden else None,
+                       "archive_matches_reference": (sha == golden["archive_sha256"]) if golden else None,
+                       "max_abs_err_over_eb (rank 0 slab)": err / ar.header.eb_resolved},
+            "archive": {"bytes": ar.nbytes, "n_outliers": ar.header.n_outliers,
+                        "n_chunks": ar.header.n_chunks, "payload_bytes": ar.header.payload_bytes},
+            "e2e": {"value": 4 * n * e2e_steps / te / 1e9, "unit": "GB/s",
+                    "h2d_bytes_per_step": 4 * n_local, "d2h_bytes_per_step": my_bytes + 4 * n_local,
+                    "steps": e2e_steps, "timing": "wall clock, max over ranks",
+                    "api": "sharded.compress_sharded_device(pinned slab) -> ShardedArchive.write(path) "
+                           "(parallel byte-range writes of one archive file); "
+                           "decompress_sharded(archive) -> pinned host slab"},
+            "gpu_launches": launches,
+            "clocks": clk.summary(),
+            "cpu_baseline": None,
+        }
+        print(json.dumps(line), flush=True)
+    return 0
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -503,9 +647,15 @@ def main():
     if world > 1:
         import torch
         import torch.distributed as dist
-        torch.cuda.set_device(local_rank)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+        ndev = torch.cuda.device_count()
+        torch.cuda.set_device(local_rank % ndev)
+        if ndev >= world and os.environ.get("SDQZ_BENCH_BACKEND", "nccl") == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+        else:   # several ranks per GPU (tests on one GPU): gloo
+            dist.init_process_group("gloo")
     try:
+        if world > 1:
+            return sharded_arm(args, cfg, world, rank, local_rank)
         return ours_arm(args, cfg, world, rank, local_rank)
     finally:
         if world > 1:

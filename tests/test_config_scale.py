@@ -120,3 +120,76 @@ def test_large_matches_reference():
         host.copy_(out[r0 * inner:(r0 + rows) * inner])
         outs.append(sha(host.numpy().tobytes()))
     assert slab_digest(outs) == g["output_slab_digest"]
+
+
+def _large_sharded_worker(rank, world, port, q):
+    import torch.distributed as dist
+
+    from paper_2007_09625_b200 import sharded
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        g = CG["large"]
+        dims = tuple(g["dims"])
+        inner = math.prod(dims[1:])
+        rows = sharded.slab_rows(dims[0], 8, world)
+        r0 = sum(rows[:rank])
+        slab = torch.empty(rows[rank] * inner, dtype=torch.float32, pin_memory=True)
+        arr = slab.numpy()
+        step = 16
+
+        def fill(a):
+            arr[a * inner:(a + step) * inner] = synthetic.smooth_rows(dims, 1, (r0 + a, r0 + a + step)) \
+                .astype(np.float32).reshape(-1)
+
+        with ThreadPoolExecutor(max_workers=max(1, 16 // world)) as ex:
+            list(ex.map(fill, range(0, rows[rank], step)))
+        d = slab.cuda().view((rows[rank],) + dims[1:])
+        del slab, arr
+        ar = sharded.compress_sharded_device(d, dims, eb=g["eb"], mode=g["mode"])
+        blob = ar.gather(root=0)
+        sha_ar = hashlib.sha256(blob).hexdigest() if blob is not None else None
+        del blob
+        # in-place decompress of this rank's slab: per-16-row-slab output digests
+        out = sharded.decompress_sharded(ar, device=True).reshape(-1)
+        host = torch.empty(16 * inner, dtype=torch.float32, pin_memory=True)
+        hs = []
+        for a in range(0, rows[rank], 16):
+            host.copy_(out[a * inner:(a + 16) * inner])
+            hs.append(sha(host.numpy().tobytes()))
+        q.put((rank, sha_ar, hs, None))
+    except Exception as e:  # surfaced by the parent
+        q.put((rank, None, None, repr(e)))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.skipif("large" not in CG, reason="large golden not generated")
+@pytest.mark.parametrize("world", [2, 4])
+def test_large_sharded_matches_reference(world):
+    """The 17.2 GB field split over `world` ranks (gloo, sharing cuda:0): the
+    assembled sharded archive and the in-place slab decompress equal the
+    reference's archive and output (the same hashes as the single-GPU test)."""
+    import socket
+
+    import torch.multiprocessing as mp
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=_large_sharded_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = {}
+    for _ in range(world):
+        r, sha_ar, hs, err = q.get(timeout=1200)
+        res[r] = (sha_ar, hs, err)
+    for p in procs:
+        p.join(120)
+    for r in range(world):
+        assert res[r][2] is None, res[r][2]
+    g = CG["large"]
+    assert res[0][0] == g["archive_sha256"]
+    assert slab_digest([h for r in range(world) for h in res[r][1]]) == g["output_slab_digest"]
