@@ -1173,6 +1173,7 @@ __global__ void __launch_bounds__(256) chunk_pack_run_kernel(DeflateArgs a, int 
                 __syncwarp();
                 const uint32_t used = (total + 31) >> 5;
                 const uint32_t cw_last = (total & 31) ? buf[full] : 0u;
+                __syncwarp();   // every lane has read the carry word before it is cleared
                 for (uint32_t j = lane; j < used; j += 32) buf[j] = 0;
                 __syncwarp();
                 if (lane == 0) buf[0] = cw_last;
@@ -1306,15 +1307,16 @@ __global__ void __launch_bounds__(64) inflate_kernel(
     // `only` != null: decode just the chunks the warp-parallel decoder handed
     // back (tiny chunks, corrupt streams -> exact reference error semantics)
     const uint64_t c = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
-    if (only && st->pad[1] == 0) return;   // the warp-parallel decoder handed nothing back
-    if (only && !__any_sync(kFull, c < nchunks && only[c])) return;
+    if (only && st->pad[1] == 0) return;   // the warp-parallel decoder handed nothing back (CTA-uniform)
+    // a CTA whose chunks were all decoded by the warp-parallel decoder has nothing to do
+    if (!__syncthreads_or(!only || (c < nchunks && only[c]))) return;
     __shared__ uint32_t lut[1 << kLutBits];
     __shared__ unsigned long long first[58];
     __shared__ long long offs[59];
-    for (uint32_t i = lane_id(); i < (1u << kLutBits); i += 32) lut[i] = glut[i];
-    for (uint32_t i = lane_id(); i < 58; i += 32) first[i] = gfirst[i];
-    for (uint32_t i = lane_id(); i < 59; i += 32) offs[i] = goffsets[i];
-    __syncwarp();
+    for (uint32_t i = threadIdx.x; i < (1u << kLutBits); i += blockDim.x) lut[i] = glut[i];
+    for (uint32_t i = threadIdx.x; i < 58; i += blockDim.x) first[i] = gfirst[i];
+    for (uint32_t i = threadIdx.x; i < 59; i += blockDim.x) offs[i] = goffsets[i];
+    __syncthreads();
     const int mx = max_bw_arg > 0 ? max_bw_arg : (int)st->max_bw;
     if (mx < 1 || mx > kMaxBw) return;
     const int lb = mx < kLutBits ? mx : kLutBits;

@@ -10,6 +10,8 @@ import pytest
 ROOT = Path(__file__).resolve().parent.parent
 sys.path.insert(0, str(ROOT))
 GOLDEN = Path(__file__).parent / "golden"
+# the reference's own suite runs in a subprocess (tests/test_ref_suite.py)
+collect_ignore = ["ref_suite"]
 
 try:
     from hypothesis import settings

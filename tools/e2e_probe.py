@@ -14,9 +14,9 @@ from paper_2007_09625_b200 import pipeline as P  # noqa: E402
 
 cfg = bench.CONFIGS[sys.argv[1] if len(sys.argv) > 1 else "hurricane"]
 dims = cfg["dims"]
-h, pinned = bench.host_field("x", dims, 1)
+h, pinned = bench.host_field(dims, 1)
 h = h.reshape(dims)
-pageable = np.array(h)
+pageable = np.array(h) if h.size < 1e9 else h
 
 
 def t(label, fn, reps=5):
@@ -33,7 +33,7 @@ def t(label, fn, reps=5):
 
 
 blob = t("compress(pinned) -> bytes", lambda: S.compress(h, eb=cfg["eb"], mode=cfg["mode"]))
-t("compress(pageable) -> bytes", lambda: S.compress(pageable, eb=cfg["eb"], mode=cfg["mode"]))
+if h.size < 1e9: t("compress(pageable) -> bytes", lambda: S.compress(pageable, eb=cfg["eb"], mode=cfg["mode"]))
 dev = t("compress_device(pinned)", lambda: P.compress_device(h, eb=cfg["eb"], mode=cfg["mode"]))
 t("  to_device only", lambda: P._device.to_device(h))
 t("  archive to_bytes", lambda: dev.to_bytes())
