@@ -1,31 +1,37 @@
 // inflate.cu -- K5: chunk-parallel canonical Huffman decode (huffman.py:272-356).
 //
 // The archive fixes the chunking (default_chunk_size, huffman.py:206-212:
-// ~1e4-6e4 chunks), too few for a thread per chunk.  A warp decodes one chunk:
-// its bit range is cut into L <= 32 equal lane slices (>= kSliceMin bits).
+// ~1e4-6e4 chunks of 256..65536 codes), too few for a thread per chunk.  A
+// warp decodes one chunk in ROUNDS: a round cuts the next stretch of the
+// chunk's bits into L <= 32 lane slices of S bits (S ~ 48 codewords at the
+// chunk's average code length), so any chunk size runs out of a small,
+// bounded shared-memory stage (the round's payload bytes, prefetched with
+// cp.async while the previous round decodes).
 //
-//   phase 1  every lane decodes from its slice start (usually mid-codeword)
-//            to the first codeword start at/after its slice end (its exit),
-//            counting codewords and recording the codeword starts of the first
-//            kWin bits of its slice (head mask).  It then decodes on into the
-//            next slice until one of its codeword starts is also in the next
-//            lane's head mask: from that synchronisation point on both paths
-//            coincide (decoding is a function of the position).
+//   phase 1  every lane decodes from its slice start (usually mid-codeword;
+//            lane 0 starts on the round's true boundary) to the first
+//            codeword start at/after its slice end (its exit), STORING the
+//            symbols in a lane-private shared-memory buffer and recording the
+//            codeword starts of the first kWin bits of its slice (head mask).
+//            It then decodes on into the next slice until one of its codeword
+//            starts is also in the next lane's head mask: from that
+//            synchronisation point on both paths coincide (decoding is a
+//            function of the position), so those tail symbols are the true
+//            symbols of the next lane's unsynchronised prefix.
 //   phase 2  lane 0 starts on a true boundary; lane l is on the true path if
 //            lane l-1 is and l-1 synchronised with it.  The first lane that
-//            did not sync redecodes from its predecessor's exit (a true
-//            boundary) -- rare with a 128-bit window.
-//   phase 3  a warp scan of the per-lane true-span symbol counts gives output
-//            offsets and every lane decodes its span again, storing codes.
+//            did not sync redecodes from its predecessor's exit -- rare.
+//   copy     a warp scan of the per-lane true-span counts gives output
+//            offsets; every lane copies its buffered span out with 16-byte
+//            stores.  The last lane's exit is the next round's true start.
 //
-// Tables (shared memory, built once per call by dtab_kernel from the
-// canonical codebook) are indexed by the next 12 payload bits and resolve
-// SEVERAL codewords per lookup: T1 gives the total length, count and the
-// codeword-start mask of the greedy decode of the 12-bit window (phase 1
-// needs no symbols); T3 gives up to three symbols with their cumulative
-// lengths (phase 3).  Codewords longer than 12 bits go through a second-level
-// table (or, past its budget, a canonical limit search).  With ~2-4 bits per
-// code this decodes ~3 codewords per table step.
+// Each symbol is decoded once.  The table (shared memory, built by
+// decode_prep_kernel from the canonical codebook) is indexed by the next 12
+// payload bits and resolves up to three codewords per lookup: their symbols,
+// total length and codeword-start mask.  Codewords longer than 12 bits go
+// through a second-level table (or, past its budget, a canonical limit
+// search).  The bit cursor is a 64-bit register window refilled one word at a
+// time from the stage, so a table step's dependency chain is one shared load.
 //
 // Chunks whose codes exceed 32 bits, or whose decode fails any check, are
 // handed to the sequential decoder (huffman.cu inflate_kernel), which
@@ -40,22 +46,22 @@ namespace {
 constexpr int kL1 = 12;                    // table index bits
 constexpr uint32_t kL1Size = 1u << kL1;
 constexpr uint32_t kL2Max = 4096;          // second-level entries (long codes)
-constexpr uint32_t kSliceMin = 64;         // bits per lane slice (short chunks keep more lanes busy)
-constexpr uint32_t kWin = 128;             // synchronisation window (bits)
-// layout of the table block (u32 words): T1 | L2 | T3 (u64)
-constexpr uint32_t kOffL2 = kL1Size;
-constexpr uint32_t kOffT3 = kL1Size + kL2Max;
-constexpr uint32_t kTabWords = kOffT3 + 2 * kL1Size;
+// layout of the table block (u32 words): T (u64[4096]) | L2 (u32[4096])
+constexpr uint32_t kOffL2 = 2 * kL1Size;
+constexpr uint32_t kTabWords = kOffL2 + kL2Max;
 
-// T1 entry:  len (0-3) | count (4-7) | codeword-start mask (8-19) | invalid (20)
-//            count 0 = first codeword longer than 12 bits (or invalid)
-// T3 entry:  sym0 (0-15) | sym1 (16-31) | sym2 (32-47) | n (48-49) | len1 (50-53)
-//            | len12 (54-57) | len123 (58-61) | zeros (62-63)
-//            n 0 = long: bits 0-11 second-level base, 12-16 extra bits k,
-//            17 second level present, 18 invalid
+// T entry (u64), len = bits 60-63:
+//   len != 0: the greedy decode of the window, up to three codewords:
+//             sym0 (0-15) | sym1 (16-31) | sym2 (32-47) | some sym == 0 (48)
+//             | codeword starts at offsets 1..11 (49-59; offset 0 implicit)
+//             -> n = 1 + popc(starts)
+//   len == 0: the first codeword is longer than 12 bits: second-level base
+//             (0-15) | extra bits k (16-20) | second level present (21) | no
+//             codeword has this prefix (22); neither flag: canonical search
 // L2 entry:  sym << 16 | len
-constexpr uint32_t kT1Invalid = 1u << 20;
-constexpr uint32_t kLongInvalid = 0x81;    // len 1 + flag (sym|len form)
+constexpr uint32_t kLongL2 = 1u << 21;
+constexpr uint32_t kLongNone = 1u << 22;
+constexpr uint32_t kSymInvalid = 0x81;     // long-path result "no codeword": len 1 + flag bit 7
 
 // ---------------------------------------------------------------------------
 // decode tables: one CTA
@@ -69,7 +75,7 @@ __device__ __forceinline__ uint32_t swz12(uint32_t w) {
     return w ^ ((h ^ (h >> 5)) & 31u);
 }
 
-// parts 0-3: a quarter of the T1/T3 windows each; part 4: second-level table;
+// parts 0-3: a quarter of the T windows each; part 4: second-level table;
 // part 5: the fallback LUT;
 // part -1: everything (both parts compute the shared preliminaries)
 __device__ __forceinline__ void dtab_body(const uint64_t* __restrict__ first,
@@ -77,11 +83,11 @@ __device__ __forceinline__ void dtab_body(const uint64_t* __restrict__ first,
                                           const uint32_t* __restrict__ symbols, int max_bw_arg,
                                           const DevStatus* st, uint32_t* __restrict__ tab,
                                           uint32_t* __restrict__ old_lut, int part) {
-    constexpr int kT13Parts = 4;
-    // p0: T1/T3 windows [w0, w1); pl2: second-level table; plut: fallback LUT
-    const bool p0 = part < kT13Parts, pl2 = part < 0 || part == kT13Parts, plut = part < 0 || part == kT13Parts + 1;
-    const uint32_t w0 = part >= 0 && part < kT13Parts ? (uint32_t)part * (kL1Size / kT13Parts) : 0u;
-    const uint32_t w1 = part >= 0 && part < kT13Parts ? w0 + kL1Size / kT13Parts : kL1Size;
+    constexpr int kTParts = 4;
+    // p0: T windows [w0, w1); pl2: second-level table; plut: fallback LUT
+    const bool p0 = part < kTParts, pl2 = part < 0 || part == kTParts, plut = part < 0 || part == kTParts + 1;
+    const uint32_t w0 = part >= 0 && part < kTParts ? (uint32_t)part * (kL1Size / kTParts) : 0u;
+    const uint32_t w1 = part >= 0 && part < kTParts ? w0 + kL1Size / kTParts : kL1Size;
     __shared__ uint32_t pmax[kL1Size];
     __shared__ uint32_t s_one[kL1Size];   // first codeword of a 12-bit window: sym << 16 | len
     __shared__ uint16_t pbase[kL1Size];   // second-level base, 0xFFFF = none
@@ -122,7 +128,7 @@ __device__ __forceinline__ void dtab_body(const uint64_t* __restrict__ first,
     for (int b = threadIdx.x; b < 35; b += blockDim.x) s_off[b] = b <= mx + 1 ? offsets[b] : offsets[mx + 1];
     for (uint32_t i = threadIdx.x; i < kL1Size; i += blockDim.x) pmax[i] = 0;
     if (pl2)
-        for (uint32_t i = threadIdx.x; i < kL2Max; i += blockDim.x) tab[kOffL2 + i] = kLongInvalid;
+        for (uint32_t i = threadIdx.x; i < kL2Max; i += blockDim.x) tab[kOffL2 + i] = kSymInvalid;
     __syncthreads();
     const long long nsym = s_off[mx + 1];
     // longest code under each 12-bit prefix
@@ -210,44 +216,31 @@ __device__ __forceinline__ void dtab_body(const uint64_t* __restrict__ first,
         }
     }
     __syncthreads();
-    // T1 / T3: greedy decode of each 12-bit window, one table lookup per codeword
+    // T: greedy decode of each 12-bit window (<= 3 codewords), one lookup per codeword
     for (uint32_t i = w0 + threadIdx.x; p0 && i < w1; i += blockDim.x) {
-        uint32_t o = 0, m = 0, mask = 0, zeros = 0, sym[3] = {0, 0, 0}, cum[3] = {0, 0, 0};
-        while (o < (uint32_t)kL1) {
+        uint32_t o = 0, m = 0, starts = 0, zero = 0, sym[3] = {0, 0, 0};
+        while (o < (uint32_t)kL1 && m < 3) {
             const uint32_t one = s_one[swz12((i << o) & (kL1Size - 1))];
             const uint32_t b = one & 63u;
             if (!b || b > kL1 - o) break;
-            const uint32_t sv = one >> 16;
-            mask |= 1u << o;
-            if (m < 3) {
-                sym[m] = sv;
-                cum[m] = o + b;
-                zeros += sv == 0;
-            }
+            sym[m] = one >> 16;
+            zero |= sym[m] == 0;
+            starts |= 1u << o;
             m++;
             o += b;
         }
-        uint32_t t1;
-        unsigned long long t3;
+        unsigned long long e;
         if (m) {
-            t1 = o | (m << 4) | (mask << 8);
-            const uint32_t n3 = m < 3 ? m : 3;
-            t3 = (unsigned long long)sym[0] | ((unsigned long long)sym[1] << 16) |
-                 ((unsigned long long)sym[2] << 32) | ((unsigned long long)n3 << 48) |
-                 ((unsigned long long)cum[0] << 50) | ((unsigned long long)cum[n3 > 1 ? 1 : 0] << 54) |
-                 ((unsigned long long)cum[n3 - 1] << 58) | ((unsigned long long)zeros << 62);
+            e = (unsigned long long)sym[0] | ((unsigned long long)sym[1] << 16) |
+                ((unsigned long long)sym[2] << 32) | ((unsigned long long)zero << 48) |
+                ((unsigned long long)(starts >> 1) << 49) | ((unsigned long long)o << 60);
         } else if (pmax[i]) {   // the codeword is longer than 12 bits
-            t1 = 1u << 8;
-            t3 = pbase[i] != 0xFFFF ? ((unsigned long long)pbase[i] | ((unsigned long long)(pmax[i] - kL1) << 12) |
-                                    (1ull << 17))
-                                 : 0ull;
+            e = pbase[i] != 0xFFFF ? ((unsigned long long)pbase[i] | ((unsigned long long)(pmax[i] - kL1) << 16) | kLongL2)
+                                   : 0ull;
         } else {                // no codeword has this prefix (incomplete code)
-            t1 = (1u << 8) | kT1Invalid;
-            t3 = 1ull << 18;
+            e = kLongNone;
         }
-        tab[i] = t1;
-        tab[kOffT3 + 2 * i] = (uint32_t)t3;
-        tab[kOffT3 + 2 * i + 1] = (uint32_t)(t3 >> 32);
+        reinterpret_cast<unsigned long long*>(tab)[i] = e;
     }
     // second-level entries
     for (long long i = lo + threadIdx.x; pl2 && i < nsym; i += blockDim.x) {
@@ -263,19 +256,9 @@ __device__ __forceinline__ void dtab_body(const uint64_t* __restrict__ first,
         for (uint32_t j = 0; j < (1u << (k - extra)); j++) tab[kOffL2 + start + j] = e;
     }
 }
-
-__global__ void __launch_bounds__(1024) dtab_kernel(const uint64_t* __restrict__ first,
-                                                    const int64_t* __restrict__ offsets,
-                                                    const uint32_t* __restrict__ symbols,
-                                                    int max_bw_arg, const DevStatus* st,
-                                                    uint32_t* __restrict__ tab,
-                                                    uint32_t* __restrict__ old_lut) {
-    dtab_body(first, offsets, symbols, max_bw_arg, st, tab, old_lut, -1);
-}
-
 // decompress prep in one launch of two clusters: cluster 0 scans the chunk
-// byte offsets and clears the hand-back flags and the chunk counter; CTAs 0/1
-// of cluster 1 build the decode tables (T1/T3 | second level + fallback LUT)
+// byte offsets and clears the hand-back flags and the chunk counter; CTAs of
+// cluster 1 build the decode tables (4 x T quarter | L2 | fallback LUT)
 __global__ void __cluster_dims__(kScanCtas, 1, 1) __launch_bounds__(1024) decode_prep_kernel(
     const uint64_t* __restrict__ first, const int64_t* __restrict__ offsets,
     const uint32_t* __restrict__ symbols, int max_bw_arg, DevStatus* st, uint32_t* __restrict__ tab,
@@ -285,19 +268,23 @@ __global__ void __cluster_dims__(kScanCtas, 1, 1) __launch_bounds__(1024) decode
         for (uint64_t i = blockIdx.x * 1024ull + threadIdx.x; i < C; i += kScanCtas * 1024ull) redo[i] = 0;
         if (blockIdx.x == 0 && threadIdx.x == 0) *counter = 0;
         cluster_chunk_scan(blockIdx.x, chunk_bits, nullptr, C, byte_off, nullptr, ~0ull, false, 0, st);
-    } else if (blockIdx.x < kScanCtas + 6) {   // cluster 1: decode tables (4 x T1/T3 quarter | L2 | LUT)
+    } else if (blockIdx.x < kScanCtas + 6) {   // cluster 1: decode tables
         dtab_body(first, offsets, symbols, max_bw_arg, st, tab, old_lut, (int)(blockIdx.x - kScanCtas));
     }
 }
 
 // ---------------------------------------------------------------------------
-// shared decode state
+// decoder
 // ---------------------------------------------------------------------------
-struct Tabs {
-    uint32_t tab_s;           // shared address of the table block
-    const uint32_t* symbols;  // global, slow path only
-    int mx;
-};
+constexpr uint32_t kSliceMin = 64;         // bits per lane slice
+constexpr uint32_t kSliceMax = 192;
+constexpr uint32_t kTargetCodes = 44;      // codewords per lane slice (sets S from the chunk's bits/code)
+constexpr uint32_t kFinalSlices = 48;      // a round whose rest fits 48 slices of S is the chunk's last
+constexpr uint32_t kBufStride = 59;        // u32 words per lane buffer (odd: distinct banks at equal slots)
+constexpr uint32_t kStoreMax = 2 * kBufStride - 3;   // a step stores 3 slots at P <= kStoreMax
+// stage of one round: up to kFinalSlices slices + the last exit's overrun + the reader's look-ahead
+constexpr uint32_t kStageUnits = (kFinalSlices * kSliceMax + 32 + 255) / 128 + 3;   // 16-byte units
+constexpr int kDecWarps = 16;
 
 __shared__ unsigned long long sh_lim[34];   // (first[b] + count[b]), b <= 32
 __shared__ unsigned long long sh_first[34];
@@ -313,387 +300,381 @@ __device__ __forceinline__ unsigned long long lds64(uint32_t addr) {
     asm volatile("ld.shared.u64 %0, [%1];" : "=l"(v) : "r"(addr));
     return v;
 }
+__device__ __forceinline__ uint32_t lds16(uint32_t addr) {
+    unsigned short v;
+    asm volatile("ld.shared.u16 %0, [%1];" : "=h"(v) : "r"(addr));
+    return v;
+}
+__device__ __forceinline__ void sts16(uint32_t addr, uint32_t v) {
+    asm volatile("st.shared.u16 [%0], %1;" ::"r"(addr), "h"((unsigned short)v) : "memory");
+}
+
+struct Dec {
+    uint32_t tab_s;           // shared address of the table block
+    const uint32_t* symbols;  // global, canonical search only
+    int mx;
+};
 
 // codeword longer than 12 bits at the top of `peek`, past the second-level
 // budget: canonical limit search -> sym << 16 | len
-__device__ __noinline__ uint32_t long_search(const Tabs& t, uint32_t peek) {
-    for (int b = kL1 + 1; b <= t.mx; b++) {
+__device__ __noinline__ uint32_t long_search(const uint32_t* symbols, int mx, uint32_t peek) {
+    for (int b = kL1 + 1; b <= mx; b++) {
         const unsigned long long top = peek >> (32 - b);
         if (top < sh_lim[b]) {
-            if (top < sh_first[b]) return kLongInvalid;
-            return (t.symbols[sh_off[b] + (long long)(top - sh_first[b])] << 16) | (uint32_t)b;
+            if (top < sh_first[b]) return kSymInvalid;
+            return (symbols[sh_off[b] + (long long)(top - sh_first[b])] << 16) | (uint32_t)b;
         }
     }
-    return kLongInvalid;
+    return kSymInvalid;
 }
 
-// codeword longer than 12 bits at the top of `peek` -> sym << 16 | len, given
-// the window's T3 entry (second-level pointer)
-__device__ __forceinline__ uint32_t long_entry3(const Tabs& t, uint32_t peek, unsigned long long e3) {
-    if (e3 & (1ull << 17)) {
-        const uint32_t k = (uint32_t)(e3 >> 12) & 31u;
-        const uint32_t idx = (uint32_t)(e3 & 0xFFF) + ((peek << kL1) >> (32 - k));
-        return lds32(t.tab_s + (kOffL2 + idx) * 4);
-    }
-    if (e3 & (1ull << 18)) return kLongInvalid;
-    return long_search(t, peek);
-}
-
-__device__ __forceinline__ uint32_t long_entry(const Tabs& t, uint32_t peek) {
-    return long_entry3(t, peek, lds64(t.tab_s + (kOffT3 + 2 * (peek >> (32 - kL1))) * 4));
-}
-
-// one phase-1 table step at `peek`: total length, codeword count, start mask
-__device__ __forceinline__ void step1(const Tabs& t, uint32_t peek, uint32_t& len, uint32_t& m,
-                                      uint32_t& mask, uint32_t& bad) {
-    const uint32_t e = lds32(t.tab_s + ((peek >> (32 - kL1)) << 2));
-    if (e & 15u) {
-        len = e & 15u;
-        m = (e >> 4) & 15u;
-        mask = (e >> 8) & 0xFFFu;
-    } else {
-        const uint32_t ee = (e & kT1Invalid) ? kLongInvalid : long_entry(t, peek);
+// One table step at `peek`: total length, codeword-start mask, symbols
+// (s01 = sym0 | sym1 << 16, s2 = sym2 | zero flag << 16).
+__device__ __forceinline__ void dstep(const Dec& d, uint32_t peek, uint32_t& len, uint32_t& mask,
+                                      uint32_t& s01, uint32_t& s2, uint32_t& bad) {
+    const unsigned long long e = lds64(d.tab_s + ((peek >> (32 - kL1)) << 3));
+    s01 = (uint32_t)e;
+    s2 = (uint32_t)(e >> 32);
+    len = s2 >> 28;
+    if (len) {
+        mask = ((s2 >> 16) & 0xFFEu) | 1u;
+    } else {   // long codeword (or a prefix no codeword has)
+        uint32_t ee;
+        if (s01 & kLongL2) {
+            const uint32_t k = (s01 >> 16) & 31u;
+            ee = lds32(d.tab_s + (kOffL2 + (s01 & 0xFFFFu) + ((peek << kL1) >> (32 - k))) * 4);
+        } else if (s01 & kLongNone) {
+            ee = kSymInvalid;
+        } else {
+            ee = long_search(d.symbols, d.mx, peek);
+        }
         bad |= ee & 0x80u;
         len = ee & 63u;
-        m = 1;
-        mask = 1;
+        s01 = ee >> 16;
+        s2 = s01 ? 0u : 0x10000u;
+        mask = 1u;
     }
 }
 
-// Chunk bits staged in shared memory (big-endian words): the peek is two LDS
-// of the words under the bit position and a funnel shift.  Positions are
-// absolute bits of the staged window.
-struct SmemReader {
-    uint32_t base_s;   // shared address of word 0
-    uint32_t a;        // bit position
-    __device__ __forceinline__ void seek(uint32_t bit) { a = bit; }
-    __device__ __forceinline__ uint32_t pos() const { return a; }
-    __device__ __forceinline__ uint32_t peek() const {
-        const uint32_t wa = base_s + ((a >> 5) << 2);
-        return __funnelshift_l(lds32(wa + 4), lds32(wa), a);
+// MSB-first bit cursor over a round's stage (raw payload bytes, 16-byte
+// aligned): three big-endian words in registers, a funnel shift for the peek
+// and a branch-free word advance (the next word is always loaded one step
+// ahead of its use).  Positions are bits relative to the chunk's 16-byte base.
+struct Cursor {
+    uint32_t w0, w1, w2;   // w0 holds the bits [pos - o, pos - o + 32)
+    uint32_t o;            // bit offset of pos in w0
+    uint32_t na;           // shared address of the word after w2
+    uint32_t pos;
+    __device__ __forceinline__ void seek(uint32_t stage_s, uint32_t origin, uint32_t bit) {
+        const uint32_t r = bit - origin;
+        const uint32_t a = stage_s + ((r >> 5) << 2);
+        w0 = bswap32(lds32(a));
+        w1 = bswap32(lds32(a + 4));
+        w2 = bswap32(lds32(a + 8));
+        na = a + 12;
+        o = r & 31u;
+        pos = bit;
     }
-    __device__ __forceinline__ void adv(uint32_t n) { a += n; }
-};
-
-// Chunk bits read from global memory: two words in registers + one prefetched.
-struct GlobalReader {
-    const uint32_t* w;    // payload words (chunk-relative)
-    uint32_t last;        // last readable word index
-    uint32_t wi;          // index of w2
-    uint32_t w0, w1, w2;
-    uint32_t s, p;
-    __device__ __forceinline__ uint32_t ld(uint32_t i) const {
-        return bswap32(__ldg(w + (i < last ? i : last)));
-    }
-    __device__ __forceinline__ void seek(uint32_t bit) {
-        const uint32_t i = bit >> 5;
-        p = bit;
-        s = bit & 31u;
-        w0 = ld(i);
-        w1 = ld(i + 1);
-        wi = i + 2;
-        w2 = ld(wi);
-    }
-    __device__ __forceinline__ uint32_t pos() const { return p; }
-    __device__ __forceinline__ uint32_t peek() const { return __funnelshift_l(w1, w0, s); }
+    __device__ __forceinline__ uint32_t peek() const { return __funnelshift_l(w1, w0, o); }
     __device__ __forceinline__ void adv(uint32_t n) {   // n <= 32
-        const uint32_t s2 = s + n;
-        p += n;
-        if (s2 >= 32) {
-            w0 = w1;
-            w1 = w2;
-            wi++;
-            w2 = ld(wi);
-        }
-        s = s2 & 31u;
+        const uint32_t nw = bswap32(lds32(na));
+        o += n;
+        pos += n;
+        const bool c = o >= 32;
+        w0 = c ? w1 : w0;
+        w1 = c ? w2 : w1;
+        w2 = c ? nw : w2;
+        na += c ? 4u : 0u;
+        o -= c ? 32u : 0u;
     }
 };
 
-// 128-bit (lo, hi) view of `mask` (<= 12 bits) shifted left by r < 128
-__device__ __forceinline__ void shl128(uint32_t mask, uint32_t r, unsigned long long& lo,
-                                       unsigned long long& hi) {
-    const unsigned long long mm = mask;
-    lo = r < 64 ? (mm << r) : 0ull;
-    hi = r >= 64 ? (mm << (r - 64)) : (r > 52 ? (mm >> (64 - r)) : 0ull);
+// store a step's three symbol slots at ordinal P (slots past n are
+// overwritten by the next step; ordinals past the buffer pile up in its last
+// slots and the span is then decoded again by lane_direct)
+__device__ __forceinline__ void put3(uint32_t buf_s, uint32_t P, uint32_t s01, uint32_t s2) {
+    const uint32_t a = buf_s + 2 * (P < kStoreMax ? P : kStoreMax);
+    sts16(a, s01);
+    sts16(a + 2, s01 >> 16);
+    sts16(a + 4, s2);
 }
 
-// Phase 1a: decode [A0, H) recording codeword starts relative to A0 in (lo, hi).
-// The position only grows, so the 128-bit record splits into three loops with
-// plain 64-bit shifts: steps wholly inside lo, steps straddling 64, steps in hi.
-template <class Rd>
-__device__ __forceinline__ void lane_head(const Tabs& t, Rd& rd, uint32_t A0, uint32_t H,
-                                          uint32_t& k, uint32_t& bad, unsigned long long& lo,
-                                          unsigned long long& hi) {
-    unsigned long long l = 0, h = 0;
-    const uint32_t h52 = A0 + 52 < H ? A0 + 52 : H, h64 = A0 + 64 < H ? A0 + 64 : H;
-    while (rd.pos() < h52) {   // mask (12 bits) << r stays below bit 64
-        uint32_t len, m, mask;
-        step1(t, rd.peek(), len, m, mask, bad);
-        l |= (unsigned long long)mask << (rd.pos() - A0);
-        k += m;
-        rd.adv(len);
-    }
-    while (rd.pos() < h64) {
-        uint32_t len, m, mask;
-        step1(t, rd.peek(), len, m, mask, bad);
-        const uint32_t r = rd.pos() - A0;
-        l |= (unsigned long long)mask << r;
-        h |= (unsigned long long)mask >> (64 - r);
-        k += m;
-        rd.adv(len);
-    }
-    while (rd.pos() < H) {
-        uint32_t len, m, mask;
-        step1(t, rd.peek(), len, m, mask, bad);
-        h |= (unsigned long long)mask << (rd.pos() - A0 - 64);
-        k += m;
+// Phase 1a of one lane: decode from the cursor to the slice end S storing
+// symbols at ordinals P.. (lane 0 and restarted lanes start on a true
+// boundary), recording the codeword starts of the first 64 bits after A0 in
+// `lo` (head mask).  tl = the starts at/after S of the step crossing S (bit
+// 0 = S).  One loop: lanes diverge only in its trip count.
+__device__ __forceinline__ void lane_decode(const Dec& d, Cursor& rd, uint32_t A0, uint32_t S, uint32_t buf_s,
+                                            uint32_t& P, uint32_t& bad, uint32_t& zf, unsigned long long& lo,
+                                            uint32_t& tl) {
+    uint32_t len = 0, mask = 0, s01, s2, p = rd.pos;
+    unsigned long long l = 0;
+    while (rd.pos < S) {
+        p = rd.pos;
+        dstep(d, rd.peek(), len, mask, s01, s2, bad);
+        put3(buf_s, P, s01, s2);
+        zf |= s2 & 0x10000u;
+        const uint32_t r = p - A0;
+        if (r < 64) l |= (unsigned long long)mask << r;
+        P += __popc(mask);
         rd.adv(len);
     }
     lo = l;
-    hi = h;
+    const uint32_t dS = S - p;   // the last step crossed S when it started < 12 bits before it
+    tl = (p < S && dS < 12) ? mask >> dS : 0u;
 }
 
-// Phase 1b: decode to the slice end S (counting codewords that start before
-// S; exit = first codeword start >= S), then on until a codeword start is in
-// the next lane's head mask (nlo, nhi, relative to S) -- the synchronisation
-// point -- or T is reached.  kt counts the codewords in [exit, sync).
-template <class Rd>
-__device__ __forceinline__ bool lane_rest(const Tabs& t, Rd& rd, uint32_t S, uint32_t T,
-                                          unsigned long long nlo, unsigned long long nhi,
-                                          uint32_t& k, uint32_t& bad, uint32_t& exit_pos,
-                                          uint32_t& sync_pos, uint32_t& kt) {
-    while (rd.pos() < S) {
-        const uint32_t p = rd.pos();
-        uint32_t len, m, mask;
-        step1(t, rd.peek(), len, m, mask, bad);
-        if (p + len <= S) {
-            k += m;
-            rd.adv(len);
-        } else {   // the step crosses S: count starts before S, stop at the first >= S
-            const uint32_t d = S - p;
-            k += __popc(mask & ((1u << d) - 1));
-            const uint32_t mh = mask >> d;
-            rd.adv(mh ? d + (uint32_t)__ffs(mh) - 1 : len);
-            break;
-        }
+// Phase 1b: from the exit, decode on (ordinals P..) until one of the starts
+// at/after S is also in the next lane's head mask `nlo` (relative to S) --
+// the synchronisation point -- or S + 52.  sync_pos = the synchronisation
+// point (or the tail's end: a true codeword start as well, on a true lane);
+// kt = tail codewords before it.
+__device__ __forceinline__ bool lane_tail(const Dec& d, Cursor& rd, uint32_t S, uint32_t tl,
+                                          unsigned long long nlo, uint32_t buf_s, uint32_t& P, uint32_t& bad,
+                                          uint32_t& zf, uint32_t& sync_pos, uint32_t& kt) {
+    const unsigned long long h0 = (unsigned long long)tl & nlo;
+    if (h0) {   // the crossing step already met the next lane's path
+        const uint32_t b = (uint32_t)(__ffsll((long long)h0) - 1);
+        sync_pos = S + b;
+        kt = __popc(tl & ((1u << b) - 1));
+        return true;
     }
-    exit_pos = rd.pos();
-    uint32_t n = 0;
-    bool found = false;
-    // synchronisation usually comes within a few codewords: steps that start
-    // below bit 52 of the window compare against nlo alone
-    const uint32_t t52 = S + 52 < T ? S + 52 : T;
-    while (rd.pos() < t52) {
-        const uint32_t r = rd.pos() - S;
-        uint32_t len, m, mask;
-        step1(t, rd.peek(), len, m, mask, bad);
-        const unsigned long long a = ((unsigned long long)mask << r) & nlo;
-        if (a) {
-            const uint32_t q = (uint32_t)(__ffsll((long long)a) - 1);
-            n += __popc(mask & ((1u << (q - r)) - 1));
-            rd.adv(q - r);
-            found = true;
-            break;
+    uint32_t n = __popc(tl);
+    uint32_t len, mask, s01, s2;
+    while (rd.pos < S + 52) {
+        const uint32_t rt = rd.pos - S;
+        dstep(d, rd.peek(), len, mask, s01, s2, bad);
+        put3(buf_s, P, s01, s2);
+        zf |= s2 & 0x10000u;
+        const unsigned long long hit = ((unsigned long long)mask << rt) & nlo;
+        if (hit) {
+            const uint32_t b = (uint32_t)(__ffsll((long long)hit) - 1) - rt;
+            sync_pos = rd.pos + b;
+            kt = n + __popc(mask & ((1u << b) - 1));
+            return true;
         }
-        n += m;
+        n += __popc(mask);
+        P += __popc(mask);
         rd.adv(len);
     }
-    while (!found && rd.pos() < T) {
-        const uint32_t r = rd.pos() - S;
-        uint32_t len, m, mask;
-        step1(t, rd.peek(), len, m, mask, bad);
-        unsigned long long a, b;
-        shl128(mask, r, a, b);
-        a &= nlo;
-        b &= nhi;
-        if (a | b) {
-            const uint32_t q = a ? (uint32_t)(__ffsll((long long)a) - 1) : 64u + (uint32_t)(__ffsll((long long)b) - 1);
-            n += __popc(mask & ((1u << (q - r)) - 1));
-            rd.adv(q - r);
-            found = true;
-            break;
-        }
-        n += m;
-        rd.adv(len);
-    }
-    sync_pos = rd.pos();
+    sync_pos = rd.pos;
     kt = n;
-    return found;
+    return false;
 }
 
-// codeword starts of (lo, hi) below bit r (r <= 128)
-__device__ __forceinline__ uint32_t below(unsigned long long lo, unsigned long long hi, uint32_t r) {
-    if (r == 0) return 0;
-    if (r <= 64) return __popcll(r == 64 ? lo : (lo & ((1ull << r) - 1)));
-    return __popcll(lo) + __popcll(r >= 128 ? hi : (hi & ((1ull << (r - 64)) - 1)));
+__device__ __forceinline__ uint32_t zero_halves(uint32_t w) {
+    return ((w & 0xFFFFu) == 0) + ((w >> 16) == 0);
 }
 
-// Phase 3 of one lane: `count` codewords from `start` (must end at `end`) into
-// dst.  Symbols go through a 16-slot per-lane ring in shared memory; every
-// completed 16-byte output vector is written with one store.
-template <class Rd>
-__device__ __forceinline__ bool lane_store(const Tabs& t, Rd& rd, uint32_t start, uint32_t end,
-                                           uint32_t count, uint16_t* dst, uint32_t ring_s,
-                                           uint32_t& zeros) {
-    rd.seek(start);
-    const uint32_t aoff = (uint32_t)((uintptr_t)dst >> 1) & 7u;   // slots before dst in its vector
-    uint16_t* const dal = dst - aoff;                               // 16-byte aligned
-    uint32_t P = aoff;              // next ring slot (absolute)
-    uint32_t nextv = 8;             // slot count at which vector (nextv/8 - 1) completes
-    uint32_t j = 0, bad = 0, z = 0;
+// Copy the buffered span (slots [a, a + nl)) to dst: 16-byte stores once dst
+// is aligned, 4-byte stores around them.  Zero codes are counted only when
+// the lane decoded one (cz).
+__device__ __forceinline__ uint32_t copy_out(uint32_t buf_s, uint32_t a, uint32_t nl, uint16_t* dst, bool cz) {
+    uint32_t z = 0, s = a, n = nl;
+    auto pair = [&](uint32_t slot) -> uint32_t {   // slots slot, slot+1 as one word
+        const uint32_t wa = buf_s + ((slot >> 1) << 2);
+        const uint32_t w0 = lds32(wa);
+        return (slot & 1) ? __byte_perm(w0, lds32(wa + 4), 0x5432) : w0;
+    };
+    if (n && ((uint32_t)(uintptr_t)dst & 2u)) {   // odd element: one u16
+        const uint32_t v = lds16(buf_s + 2 * s);
+        *dst = (uint16_t)v;
+        z += v == 0;
+        s++;
+        dst++;
+        n--;
+    }
+    while (n >= 2 && ((uint32_t)(uintptr_t)dst & 15u)) {
+        const uint32_t w = pair(s);
+        *reinterpret_cast<uint32_t*>(dst) = w;
+        if (cz) z += zero_halves(w);
+        s += 2;
+        dst += 2;
+        n -= 2;
+    }
+    for (; n >= 8; n -= 8, s += 8, dst += 8) {
+        const uint32_t wa = buf_s + ((s >> 1) << 2);
+        uint4 v;
+        v.x = lds32(wa);
+        v.y = lds32(wa + 4);
+        v.z = lds32(wa + 8);
+        v.w = lds32(wa + 12);
+        if (s & 1) {
+            const uint32_t w4 = lds32(wa + 16);
+            v.x = __byte_perm(v.x, v.y, 0x5432);
+            v.y = __byte_perm(v.y, v.z, 0x5432);
+            v.z = __byte_perm(v.z, v.w, 0x5432);
+            v.w = __byte_perm(v.w, w4, 0x5432);
+        }
+        *reinterpret_cast<uint4*>(dst) = v;
+        if (cz) z += zero_halves(v.x) + zero_halves(v.y) + zero_halves(v.z) + zero_halves(v.w);
+    }
+    for (; n >= 2; n -= 2, s += 2, dst += 2) {
+        const uint32_t w = pair(s);
+        *reinterpret_cast<uint32_t*>(dst) = w;
+        if (cz) z += zero_halves(w);
+    }
+    if (n) {
+        const uint32_t v = lds16(buf_s + 2 * s);
+        *dst = (uint16_t)v;
+        z += v == 0;
+    }
+    return z;
+}
+
+// A lane whose true span overflowed its buffer decodes it again straight to
+// global memory (rare: a slice of unusually short codewords).
+__device__ __noinline__ uint32_t lane_direct(const Dec& d, uint32_t stage_s, uint32_t origin, uint32_t start,
+                                             uint32_t count, uint16_t* dst) {
+    Cursor rd;
+    rd.seek(stage_s, origin, start);
+    uint32_t j = 0, z = 0, bad = 0;
     while (j < count) {
-        const uint32_t peek = rd.peek();
-        unsigned long long e3 = lds64(t.tab_s + (kOffT3 + 2 * (peek >> (32 - kL1))) * 4);
-        uint32_t n3 = (uint32_t)(e3 >> 48) & 3u, len;
-        if (n3 == 0) {   // long codeword (or invalid pattern)
-            const uint32_t ee = long_entry3(t, peek, e3);
-            bad |= ee & 0x80u;
-            len = ee & 63u;
-            e3 = ee >> 16;
-            n3 = 1;
-            z += (ee >> 16) == 0;
-        } else if (j + n3 > count) {   // the span ends inside this step
-            const uint32_t take = count - j;
-            len = take == 1 ? (uint32_t)(e3 >> 50) & 15u : (uint32_t)(e3 >> 54) & 15u;
-            z += ((e3 & 0xFFFF) == 0) + (take > 1 && ((e3 >> 16) & 0xFFFF) == 0);
-            n3 = take;
-        } else {
-            len = (uint32_t)(e3 >> 58) & 15u;
-            z += (uint32_t)(e3 >> 62);
+        uint32_t len, mask, s01, s2;
+        dstep(d, rd.peek(), len, mask, s01, s2, bad);
+        const uint32_t n = __popc(mask), take = n < count - j ? n : count - j;
+        const uint32_t v[3] = {s01 & 0xFFFFu, s01 >> 16, s2 & 0xFFFFu};
+        for (uint32_t q = 0; q < take; q++) {
+            dst[j + q] = (uint16_t)v[q];
+            z += v[q] == 0;
         }
-#pragma unroll
-        for (uint32_t q = 0; q < 3; q++) {
-            if (q < n3) {
-                asm volatile("st.shared.u16 [%0], %1;" ::"r"(ring_s + ((P + q) & 15u) * 2),
-                             "h"((unsigned short)(e3 >> (16 * q))));
-            }
-        }
-        P += n3;
-        j += n3;
+        j += take;
         rd.adv(len);
-        if (P >= nextv) {   // vector v = nextv/8 - 1 complete (lane-private ring)
-            const uint32_t v = nextv / 8 - 1;
-            const uint32_t rs = ring_s + ((8 * v) & 15u) * 2;
-            uint4 qv;
-            asm volatile("ld.shared.v2.u32 {%0, %1}, [%2];" : "=r"(qv.x), "=r"(qv.y) : "r"(rs));
-            asm volatile("ld.shared.v2.u32 {%0, %1}, [%2];" : "=r"(qv.z), "=r"(qv.w) : "r"(rs + 8));
-            if (v == 0 && aoff) {
-                const uint32_t h[8] = {qv.x & 0xFFFF, qv.x >> 16, qv.y & 0xFFFF, qv.y >> 16,
-                                       qv.z & 0xFFFF, qv.z >> 16, qv.w & 0xFFFF, qv.w >> 16};
-#pragma unroll
-                for (uint32_t s = 1; s < 8; s++)
-                    if (s >= aoff) dal[s] = (uint16_t)h[s];
-            } else {
-                *reinterpret_cast<uint4*>(dal + 8 * v) = qv;
-            }
-            nextv += 8;
-        }
     }
-    // trailing partial vector
-    const uint32_t v = nextv / 8 - 1;
-    for (uint32_t s = (v == 0 ? aoff : 0); 8 * v + s < P; s++) {
-        unsigned short h;
-        asm volatile("ld.shared.u16 %0, [%1];" : "=h"(h) : "r"(ring_s + ((8 * v + s) & 15u) * 2));
-        dal[8 * v + s] = h;
-    }
-    zeros += z;
-    return !bad && rd.pos() == end;
+    return z;
 }
 
-// Phases 1-3 of one chunk by one warp; positions are absolute bits (the chunk
-// occupies [sbit, sbit + B)).  false = hand the chunk back.
-template <class Rd>
-__device__ __forceinline__ bool decode_chunk(const Tabs& t, Rd rd, uint32_t sbit, uint32_t B,
-                                             uint32_t cnt, uint16_t* out, uint32_t ring_s,
-                                             uint32_t& zeros, DevStatus* st) {
+// One lane's phase 1 from `start` (ordinal 0): slice, exit, tail.
+__device__ __forceinline__ void lane_phase1(const Dec& d, Cursor& rd, uint32_t stage_s, uint32_t origin,
+                                            uint32_t start, uint32_t s0, uint32_t s1, bool last,
+                                            unsigned long long nlo, uint32_t buf_s, uint32_t& P, uint32_t& bad,
+                                            uint32_t& zf, unsigned long long& lo, uint32_t& ex, uint32_t& k,
+                                            uint32_t& sp, uint32_t& kt, bool& fwd) {
+    uint32_t tl;
+    rd.seek(stage_s, origin, start);
+    P = 0;
+    lane_decode(d, rd, s0, s1, buf_s, P, bad, zf, lo, tl);
+    ex = tl ? s1 + (uint32_t)(__ffs(tl) - 1) : rd.pos;   // first codeword start >= s1
+    k = P - (uint32_t)__popc(tl);                        // ordinals before the exit
+    fwd = false;
+    sp = ex;
+    kt = 0;
+    if (!last) fwd = lane_tail(d, rd, s1, tl, nlo, buf_s, P, bad, zf, sp, kt);
+}
+
+// One round: lanes [0, L) decode the slices [s0, s1) of one stretch of a
+// chunk (lane 0 from the round's true start); the buffered true spans go to
+// out[ob ...].  Returns false to hand the chunk back; next_q = the last
+// lane's exit (the next round's true start).
+__device__ __forceinline__ bool decode_round(const Dec& d, uint32_t stage_s, uint32_t origin, uint32_t L,
+                                             uint32_t s0, uint32_t s1, uint32_t buf_s, uint16_t* out,
+                                             uint32_t& ob, uint32_t cnt, uint32_t& next_q, uint32_t& zeros,
+                                             DevStatus* st) {
     const uint32_t lane = lane_id();
-    uint32_t L = B / kSliceMin;
-    L = L < 1 ? 1 : (L > 32 ? 32 : L);
     const bool active = lane < L;
     const bool last = lane + 1 == L;
-    const uint32_t s0 = sbit + (active ? (uint32_t)(((uint64_t)lane * B) / L) : B);
-    const uint32_t s1 = sbit + (active ? (uint32_t)(((uint64_t)(lane + 1) * B) / L) : B);
-    const uint32_t T = last || !active ? s1 : (s1 + kWin < sbit + B ? s1 + kWin : sbit + B);
-    uint32_t k = 0, bad = 0, ex = s1, sp = s1, kt = 0, start = s0;
-    unsigned long long lo = 0, hi = 0;
-    bool fwd = false;   // this lane's tail met the next lane's path
+    Cursor rd;
+    uint32_t P = 0, bad = 0, zf = 0, tl = 0;
+    unsigned long long lo = 0;
     if (active) {
-        rd.seek(s0);
-        // the head window ends >= 12 bits (one table step) before the slice end,
-        // so its last step cannot run past S (lane_rest counts exactly to S)
-        const uint32_t hend = s1 > s0 + 12 ? (s0 + kWin < s1 - 12 ? s0 + kWin : s1 - 12) : s0;
-        lane_head(t, rd, s0, hend, k, bad, lo, hi);
+        rd.seek(stage_s, origin, s0);
+        lane_decode(d, rd, s0, s1, buf_s, P, bad, zf, lo, tl);
     }
     const unsigned long long nlo = __shfl_down_sync(kFull, lo, 1);
-    const unsigned long long nhi = __shfl_down_sync(kFull, hi, 1);
-    if (active) fwd = lane_rest(t, rd, s1, T, nlo, nhi, k, bad, ex, sp, kt);
-    bool ok = bad == 0;
-    // phase 2: lane l is on the true path if lane l-1 is and l-1's tail met it;
-    // the first lane that is not redecodes from its predecessor's exit
-    bool restarted = lane == 0;
-    uint32_t q = s0;   // start of the lane's true span
+    uint32_t ex = s1, k = 0, sp = s1, kt = 0;
+    bool fwd = false;   // this lane's tail met the next lane's path
+    if (active) {
+        ex = tl ? s1 + (uint32_t)(__ffs(tl) - 1) : rd.pos;
+        k = P - (uint32_t)__popc(tl);
+        sp = ex;
+        if (!last) fwd = lane_tail(d, rd, s1, tl, nlo, buf_s, P, bad, zf, sp, kt);
+    }
+    // phase 2: lane l continues lane l-1's true path from q = sp(l-1): at the
+    // synchronisation point (l-1's tail met l's path: l's ordinals before q are
+    // dropped), or else at the end of l-1's tail, where l decodes again.  Lanes
+    // whose link is broken all redecode at once (failures are rare and
+    // isolated); a broken lane 0 or a redecode that fails hands the chunk back.
+    bool restarted = false;
+    uint32_t rstart = 0;   // where a restarted lane began
     for (uint32_t round = 0;; round++) {
         const bool pfwd = __shfl_up_sync(kFull, fwd, 1);
-        const uint32_t pe = __shfl_up_sync(kFull, ex, 1);
         const uint32_t psp = __shfl_up_sync(kFull, sp, 1);
-        const bool synced = !active || (ok && (restarted || pfwd));
-        const unsigned badl = __ballot_sync(kFull, !synced);
-        if (badl == 0) {
-            if (active && !restarted) q = psp;
-            break;
-        }
-        const uint32_t f = (uint32_t)(__ffs(badl) - 1);
-        if (f == 0 || round >= L) return false;
-        if (lane == f) {
+        const bool link = !active || (bad == 0 && (lane == 0 || (restarted ? rstart == psp : pfwd)));
+        const unsigned broken = __ballot_sync(kFull, !link);
+        if (broken == 0) break;
+        if ((broken & 1u) || round >= L) return false;
+        if (!link) {
             restarted = true;
-            q = start = pe;
-            k = 0;
+            rstart = psp;
             bad = 0;
-            rd.seek(pe);
-            fwd = lane_rest(t, rd, s1, T, nlo, nhi, k, bad, ex, sp, kt);
-            ok = bad == 0;
-            atomicAdd(&st->pad[0], 1ull);   // diagnostics: lane redecodes
+            zf = 0;
+            lane_phase1(d, rd, stage_s, origin, psp, s0, s1, last, nlo, buf_s, P, bad, zf, lo, ex, k, sp, kt, fwd);
+            atomicAdd(&st->pad[0], 1ull);   // diagnostics: lane redecodes (low word)
         }
-        if (!__shfl_sync(kFull, ok ? 1u : 0u, f)) return false;
     }
-    // true-span length of each lane: its codewords from q to its exit, plus its
-    // tail codewords up to the next lane's start (if that lane synced on it)
-    const bool nrestart = __shfl_down_sync(kFull, restarted, 1);
-    const uint32_t nq = __shfl_down_sync(kFull, q, 1);
-    const uint32_t last_e = __shfl_sync(kFull, ex, L - 1);
-    uint32_t nl = 0;
+    // true span: ordinals [a, k) up to the exit, plus the tail up to sp
+    const uint32_t psp = __shfl_up_sync(kFull, sp, 1);
+    const uint32_t q = lane == 0 ? s0 : psp;
+    uint32_t a = 0, nl = 0;
     if (active) {
-        nl = k - (restarted ? 0u : below(lo, hi, q - s0));
-        if (!last && !nrestart) nl += kt;
+        if (lane != 0 && !restarted) a = (uint32_t)__popcll(lo & ((1ull << (q - s0)) - 1));
+        nl = k - a;
+        if (!last) nl += kt;
     }
     int total;
     const uint32_t o = (uint32_t)warp_excl_scan((int)nl, &total);
-    if (last_e != sbit + B || (uint32_t)total != cnt) return false;
-    // phase 3
-    bool ok3 = true;
-    uint32_t z = 0;
-    const uint32_t end = last ? sbit + B : nq;
-    if (active && nl) ok3 = lane_store(t, rd, q, end, nl, out + o, ring_s, z);
-    if (!__all_sync(kFull, ok3)) return false;
-    zeros += z;
+    next_q = __shfl_sync(kFull, ex, L - 1);
+    if (ob + (uint32_t)total > cnt) return false;
+    if (nl) {
+        uint16_t* dst = out + ob + o;
+        if (a + nl <= kStoreMax) {
+            zeros += copy_out(buf_s, a, nl, dst, zf != 0);
+        } else {
+            zeros += lane_direct(d, stage_s, origin, q, nl, dst);
+            atomicAdd(&st->pad[0], 1ull << 32);   // diagnostics: buffer overflows (high word)
+        }
+    }
+    ob += (uint32_t)total;
     return true;
 }
 
-// one CTA per SM shares one copy of the tables: 32 warps, or 24 for chunks of
-// >= 16384 codes (longer lane spans: the register budget of 1024-thread CTAs
-// is the limit there, and fewer warps leave more staging per warp)
-constexpr uint32_t kRingStride = 40;   // 16 u16 slots per lane + 8 bytes: 2-way bank conflicts
+// issue the cp.async loads of stage units [u0, u0 + units) (chunk-relative
+// 16-byte units from cb16) into stage_s; units past the payload read zeros
+__device__ __forceinline__ void stage_issue(uint32_t stage_s, const uint4* payload4, uint64_t n4, uint64_t cb16,
+                                            uint32_t u0, uint32_t units) {
+    if (units > kStageUnits) units = kStageUnits;
+    for (uint32_t i = lane_id(); i < units; i += 32) {
+        const uint64_t u = cb16 + u0 + i;
+        const bool in = u < n4;
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(stage_s + 16 * i),
+                     "l"(payload4 + (in ? u : 0)), "r"(in ? 16 : 0)
+                     : "memory");
+    }
+    asm volatile("cp.async.commit_group;" ::: "memory");
+}
 
-// dynamic shared memory: tables (kTabWords) | per-lane rings | one staging
-// buffer of `stage_words` words per warp
+// stage units [first, last] covering a round that starts at q and ends by `end` (bits)
+__device__ __forceinline__ void round_units(uint32_t q, uint32_t end, uint32_t& u0, uint32_t& units) {
+    u0 = q >> 7;
+    units = ((end + 32 + 255) >> 7) - u0 + 1;
+}
+
+// slice size: ~kTargetCodes codewords at the chunk's mean code length
+__device__ __forceinline__ uint32_t slice_bits(uint32_t B, uint32_t cnt) {
+    const unsigned long long s = (unsigned long long)kTargetCodes * B / (cnt ? cnt : 1);
+    return (uint32_t)(s < kSliceMin ? kSliceMin : (s > kSliceMax ? kSliceMax : s));
+}
+
+// dynamic shared memory: tables (kTabWords) | per-warp lane buffers | per-warp
+// double stage
 template <int kWarps>
-__global__ void __launch_bounds__(kWarps * 32) inflate_fast_kernel(
+__global__ void __launch_bounds__(kWarps * 32, 1) inflate_fast_kernel(
     const uint8_t* __restrict__ payload, uint64_t nwords, const uint32_t* __restrict__ chunk_bits,
     const unsigned long long* __restrict__ byte_off, uint64_t nchunks, uint32_t chunk, uint64_t n,
     const uint64_t* __restrict__ gfirst, const int64_t* __restrict__ goffsets,
     const uint32_t* __restrict__ symbols, const uint32_t* __restrict__ gtab, int max_bw_arg,
     uint16_t* __restrict__ out, uint8_t* __restrict__ redo, unsigned int* __restrict__ next_chunk,
-    uint32_t stage_words, DevStatus* st) {
+    DevStatus* st) {
     extern __shared__ __align__(16) uint32_t s_tab[];
     const int mx = max_bw_arg > 0 ? max_bw_arg : (int)st->max_bw;
     if (mx < 1 || mx > 32) {   // 64-bit codes: everything goes to the sequential decoder
@@ -706,7 +687,8 @@ __global__ void __launch_bounds__(kWarps * 32) inflate_fast_kernel(
     {
         const uint4* src = reinterpret_cast<const uint4*>(gtab);
         uint4* dst = reinterpret_cast<uint4*>(s_tab);
-        for (uint32_t i = threadIdx.x; i < kTabWords / 4; i += blockDim.x) dst[i] = __ldg(src + i);
+        const uint32_t words = mx > kL1 ? kTabWords : kOffL2;   // the second level only for long codes
+        for (uint32_t i = threadIdx.x; i < words / 4; i += blockDim.x) dst[i] = __ldg(src + i);
         for (int b = threadIdx.x; b < 34; b += blockDim.x) {
             const bool in = b >= 1 && b <= mx;
             sh_first[b] = in ? gfirst[b] : 0;
@@ -715,75 +697,110 @@ __global__ void __launch_bounds__(kWarps * 32) inflate_fast_kernel(
         for (int b = threadIdx.x; b < 35; b += blockDim.x) sh_off[b] = b <= mx + 1 ? goffsets[b] : 0;
     }
     __syncthreads();
-    Tabs t;
+    Dec d;
     const uint32_t smem_base = (uint32_t)__cvta_generic_to_shared(s_tab);
-    asm volatile("mov.u32 %0, %1;" : "=r"(t.tab_s) : "r"(smem_base));
-    t.symbols = symbols;
-    t.mx = mx;
+    // opaque copies: keep the shared addresses in registers instead of
+    // re-deriving them from the CTA's shared window inside the loops
+    asm volatile("mov.u32 %0, %1;" : "=r"(d.tab_s) : "r"(smem_base));
+    d.symbols = symbols;
+    d.mx = mx;
     const uint32_t lane = lane_id(), wid = threadIdx.x >> 5;
-    const uint32_t ring_s = smem_base + kTabWords * 4 + threadIdx.x * kRingStride;
-    uint32_t* stage = s_tab + kTabWords + (kWarps * 32 * kRingStride) / 4 + wid * stage_words;
-    const uint32_t* words = reinterpret_cast<const uint32_t*>(payload);
-    const uint4* words4 = reinterpret_cast<const uint4*>(payload);
-    uint32_t zeros_total = 0;
+    uint32_t buf_s;
+    asm volatile("mov.u32 %0, %1;" : "=r"(buf_s) : "r"(smem_base + kTabWords * 4 + (wid * 32 + lane) * kBufStride * 4));
+    const uint32_t stage0 = smem_base + kTabWords * 4 + kWarps * 32 * kBufStride * 4 + wid * 2 * kStageUnits * 16;
+    const uint4* payload4 = reinterpret_cast<const uint4*>(payload);
+    const uint64_t n4 = nwords / 4;
+    uint32_t zeros = 0, cur = 0;
+    bool have = false;   // stage[cur] holds (in flight) the first round of chunk c
 
     uint32_t c = 0;
     if (lane == 0) c = atomicAdd(next_chunk, 1u);
     c = __shfl_sync(kFull, c, 0);
     while (c < nchunks) {
-        uint32_t cn = 0;   // claim the next chunk early: the atomic's latency hides behind this one
+        uint32_t cn = 0;   // claim the next chunk early: its first stage is prefetched
         if (lane == 0) cn = atomicAdd(next_chunk, 1u);
+        cn = __shfl_sync(kFull, cn, 0);
         const uint32_t B = chunk_bits[c];
         const unsigned long long boff = byte_off[c];
         const uint64_t base = (uint64_t)c * chunk;
         const uint32_t cnt = (uint32_t)umin(chunk, n - base);
-        // 16-byte aligned window of the payload holding the chunk (+ 2 words of peek slack)
-        const uint64_t q0 = boff >> 4;
+        const uint64_t cb16 = boff >> 4;
         const uint32_t sbit = (uint32_t)(boff & 15) * 8;
-        const uint32_t nq4 = (uint32_t)(((uint64_t)sbit + B + 63 + 127) >> 7);
-        bool good;
-        if (nq4 * 4 <= stage_words && (q0 + nq4) * 4 <= nwords) {
-            for (uint32_t i = lane; i < nq4; i += 32) {
-                const uint4 v = __ldg(words4 + q0 + i);
-                reinterpret_cast<uint4*>(stage)[i] =
-                    make_uint4(bswap32(v.x), bswap32(v.y), bswap32(v.z), bswap32(v.w));
+        const uint32_t E = sbit + B;
+        bool good = B != 0 && cnt != 0;
+        if (good) {
+            const uint32_t S = slice_bits(B, cnt);
+            uint32_t q = sbit, ob = 0, u0, units;
+            round_units(q, (E - q <= kFinalSlices * S) ? E : q + 32 * S, u0, units);
+            if (!have) stage_issue(stage0 + cur * kStageUnits * 16, payload4, n4, cb16, u0, units);
+            have = false;
+            for (;;) {
+                const uint32_t R = E - q;
+                const bool fin = R <= kFinalSlices * S;
+                uint32_t L, s0, s1, nu0 = 0;
+                if (fin) {
+                    L = R / kSliceMin;
+                    L = L < 1 ? 1 : (L > 32 ? 32 : L);
+                    s0 = q + (uint32_t)(((uint64_t)(lane < L ? lane : L) * R) / L);
+                    s1 = q + (uint32_t)(((uint64_t)(lane < L ? lane + 1 : L) * R) / L);
+                } else {
+                    L = 32;
+                    s0 = q + lane * S;
+                    s1 = s0 + S;
+                }
+                // prefetch: the next round of this chunk, or the next chunk's first round
+                const uint32_t nstage = stage0 + (cur ^ 1) * kStageUnits * 16;
+                if (!fin) {
+                    const uint32_t nq = q + 32 * S;   // the next round starts in [nq, nq + 32)
+                    uint32_t nunits;
+                    const uint32_t nend = E - nq <= kFinalSlices * S + 32 ? E : nq + 32 + 32 * S;
+                    round_units(nq, nend, nu0, nunits);
+                    stage_issue(nstage, payload4, n4, cb16, nu0, nunits);
+                } else if (cn < nchunks) {
+                    const unsigned long long nboff = byte_off[cn];
+                    const uint32_t nB = chunk_bits[cn];
+                    const uint32_t ncnt = (uint32_t)umin(chunk, n - (uint64_t)cn * chunk);
+                    const uint32_t nS = slice_bits(nB, ncnt);
+                    const uint32_t nsb = (uint32_t)(nboff & 15) * 8;
+                    uint32_t a0, au;
+                    round_units(nsb, (nB <= kFinalSlices * nS) ? nsb + nB : nsb + 32 * nS, a0, au);
+                    stage_issue(nstage, payload4, n4, nboff >> 4, a0, au);
+                    have = true;
+                } else {
+                    asm volatile("cp.async.commit_group;" ::: "memory");
+                }
+                asm volatile("cp.async.wait_group 1;" ::: "memory");
+                __syncwarp();
+                uint32_t next_q = 0;
+                good = decode_round(d, stage0 + cur * kStageUnits * 16, u0 * 128, L, s0, s1, buf_s, out + base, ob,
+                                    cnt, next_q, zeros, st);
+                __syncwarp();   // the stage and the buffers are refilled next
+                cur ^= 1;
+                if (good && fin) good = next_q == E && ob == cnt;
+                if (!good || fin) {
+                    if (!good && !fin) {   // the prefetched next round is not needed
+                        asm volatile("cp.async.wait_all;" ::: "memory");
+                        __syncwarp();
+                    }
+                    break;
+                }
+                if (next_q < q + 32 * S || next_q >= E) { good = false; asm volatile("cp.async.wait_all;" ::: "memory"); __syncwarp(); break; }
+                q = next_q;
+                u0 = nu0;
             }
-            __syncwarp();
-            SmemReader rd;
-            rd.base_s = (uint32_t)__cvta_generic_to_shared(stage);
-            good = decode_chunk(t, rd, sbit, B, cnt, out + base, ring_s, zeros_total, st);
-            __syncwarp();   // the stage is refilled by the next chunk
-        } else {
-            const uint64_t wbase = boff >> 2;
-            GlobalReader rd;
-            rd.w = words + wbase;
-            rd.last = (uint32_t)umin(nwords > wbase ? nwords - 1 - wbase : 0, 0xFFFFFFFFull);
-            good = decode_chunk(t, rd, (uint32_t)(boff & 3) * 8, B, cnt, out + base, ring_s,
-                                zeros_total, st);
         }
         if (!good && lane == 0) {
             redo[c] = 1;
             atomicAdd(&st->pad[1], 1ull);       // diagnostics: chunks handed back
         }
-        c = __shfl_sync(kFull, cn, 0);
+        c = cn;
     }
-    zeros_total = __reduce_add_sync(kFull, zeros_total);
-    if (lane == 0 && zeros_total) atomicAdd(&st->n_zero, (unsigned long long)zeros_total);
+    asm volatile("cp.async.wait_all;" ::: "memory");
+    zeros = __reduce_add_sync(kFull, zeros);
+    if (lane == 0 && zeros) atomicAdd(&st->n_zero, (unsigned long long)zeros);
 }
 
 }  // namespace
-
-int launch_decode_tables(sdqz_ctx* ctx, const uint64_t* first, const int64_t* offsets,
-                         const uint32_t* symbols, int max_bw, uint32_t** tab_out, uint32_t* old_lut) {
-    int rc = SDQZ_OK;
-    uint32_t* tab = scratch_as<uint32_t>(ctx, S_DTAB, kTabWords, &rc);
-    if (!tab) return rc;
-    dtab_kernel<<<1, 1024, 0, ctx->stream>>>(first, offsets, symbols, max_bw, ctx->d_status, tab,
-                                             old_lut);
-    SDQZ_LAUNCHED_NAMED(ctx, "dtab_kernel");
-    *tab_out = tab;
-    return SDQZ_OK;
-}
 
 int launch_decode_prep(sdqz_ctx* ctx, const uint64_t* first, const int64_t* offsets,
                        const uint32_t* symbols, int max_bw, uint32_t** tab_out, uint32_t* old_lut,
@@ -794,38 +811,11 @@ int launch_decode_prep(sdqz_ctx* ctx, const uint64_t* first, const int64_t* offs
     unsigned int* counter = scratch_as<unsigned int>(ctx, S_COUNTER, 4, &rc);
     if (!tab || !counter) return rc;
     decode_prep_kernel<<<2 * kScanCtas, 1024, 0, ctx->stream>>>(first, offsets, symbols, max_bw, ctx->d_status, tab,
-                                                    old_lut, chunk_bits, n_chunks, byte_off, redo,
-                                                    counter);
+                                                                old_lut, chunk_bits, n_chunks, byte_off, redo,
+                                                                counter);
     SDQZ_LAUNCHED_NAMED(ctx, "decode_prep_kernel");
     *tab_out = tab;
     return SDQZ_OK;
-}
-
-template <int kWarps>
-void launch_inflate_fast_w(sdqz_ctx* ctx, const uint8_t* payload, uint64_t nwords, const uint32_t* chunk_bits,
-                           const unsigned long long* byte_off, uint64_t n_chunks, uint32_t chunk, uint64_t n,
-                           const uint64_t* first, const int64_t* offsets, const uint32_t* symbols,
-                           const uint32_t* tab, int max_bw, uint16_t* codes, uint8_t* redo, unsigned int* counter) {
-    // per-warp staging: room for ~2x the average chunk (bigger chunks read global memory)
-    const uint64_t avg = n_chunks ? (nwords * 4) / n_chunks : 0;
-    const size_t fixed = (size_t)kTabWords * 4 + (size_t)kWarps * 32 * kRingStride;
-    int smem_max = 0;
-    cudaDeviceGetAttribute(&smem_max, cudaDevAttrMaxSharedMemoryPerBlockOptin, ctx->device);
-    const uint32_t room = (uint32_t)(((size_t)smem_max - 1024 - fixed) / (kWarps * 4)) & ~15u;
-    uint32_t stage_words = (uint32_t)umin(((2 * avg + 64) / 4 + 15) & ~15ull, room);
-    if (stage_words < 64) stage_words = 64;
-    const size_t smem = fixed + (size_t)kWarps * stage_words * 4;
-    ensure_smem(ctx, (const void*)inflate_fast_kernel<kWarps>, smem);
-    int per_sm = 1;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, inflate_fast_kernel<kWarps>, kWarps * 32, smem);
-    if (per_sm < 1) per_sm = 1;
-    uint64_t grid = ceil_div(n_chunks, kWarps);
-    const uint64_t cap = (uint64_t)ctx->num_sms * per_sm;
-    if (grid > cap) grid = cap;
-    if (grid < 1) grid = 1;
-    inflate_fast_kernel<kWarps><<<(unsigned)grid, kWarps * 32, smem, ctx->stream>>>(
-        payload, nwords, chunk_bits, byte_off, n_chunks, chunk, n, first, offsets, symbols, tab,
-        max_bw, codes, redo, counter, stage_words, ctx->d_status);
 }
 
 int launch_inflate_fast(sdqz_ctx* ctx, const uint8_t* payload, uint64_t nwords,
@@ -836,12 +826,15 @@ int launch_inflate_fast(sdqz_ctx* ctx, const uint8_t* payload, uint64_t nwords,
     int rc = SDQZ_OK;
     unsigned int* counter = scratch_as<unsigned int>(ctx, S_COUNTER, 4, &rc);   // cleared by the prep kernel
     if (!counter) return rc;
-    if (chunk >= 16384)
-        launch_inflate_fast_w<24>(ctx, payload, nwords, chunk_bits, byte_off, n_chunks, chunk, n, first, offsets,
-                                  symbols, tab, max_bw, codes, redo, counter);
-    else
-        launch_inflate_fast_w<32>(ctx, payload, nwords, chunk_bits, byte_off, n_chunks, chunk, n, first, offsets,
-                                  symbols, tab, max_bw, codes, redo, counter);
+    constexpr int kW = kDecWarps;
+    const size_t smem = (size_t)kTabWords * 4 + (size_t)kW * 32 * kBufStride * 4 + (size_t)kW * 2 * kStageUnits * 16 + 16;
+    ensure_smem(ctx, (const void*)inflate_fast_kernel<kW>, smem);
+    uint64_t grid = ceil_div(n_chunks, kW);
+    if (grid > (uint64_t)ctx->num_sms) grid = ctx->num_sms;
+    if (grid < 1) grid = 1;
+    inflate_fast_kernel<kW><<<(unsigned)grid, kW * 32, smem, ctx->stream>>>(
+        payload, nwords, chunk_bits, byte_off, n_chunks, chunk, n, first, offsets, symbols, tab, max_bw, codes,
+        redo, counter, ctx->d_status);
     SDQZ_LAUNCHED_NAMED(ctx, "inflate_fast_kernel");
     return SDQZ_OK;
 }

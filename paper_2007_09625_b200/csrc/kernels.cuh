@@ -72,8 +72,6 @@ int launch_inflate(sdqz_ctx* ctx, const uint8_t* payload, uint64_t payload_bytes
 // inflate.cu: decode tables (primary 12-bit + second level) and the warp-per-chunk
 // self-synchronising decoder; chunks it cannot finish are flagged in `redo`.
 // (old_lut, if non-null, also receives the sequential decoder's 12-bit table)
-int launch_decode_tables(sdqz_ctx* ctx, const uint64_t* first, const int64_t* offsets,
-                         const uint32_t* symbols, int max_bw, uint32_t** tab_out, uint32_t* old_lut);
 int launch_decode_prep(sdqz_ctx* ctx, const uint64_t* first, const int64_t* offsets,
                        const uint32_t* symbols, int max_bw, uint32_t** tab_out, uint32_t* old_lut,
                        const uint32_t* chunk_bits, uint64_t n_chunks, unsigned long long* byte_off,
