@@ -278,13 +278,20 @@ __global__ void __cluster_dims__(kScanCtas, 1, 1) __launch_bounds__(1024) decode
 // ---------------------------------------------------------------------------
 constexpr uint32_t kSliceMin = 64;         // bits per lane slice
 constexpr uint32_t kSliceMax = 192;
-constexpr uint32_t kTargetCodes = 44;      // codewords per lane slice (sets S from the chunk's bits/code)
+constexpr uint32_t kTargetCodes = 56;      // codewords per lane slice (sets S from the chunk's bits/code)
 constexpr uint32_t kFinalSlices = 48;      // a round whose rest fits 48 slices of S is the chunk's last
 constexpr uint32_t kBufStride = 59;        // u32 words per lane buffer (odd: distinct banks at equal slots)
 constexpr uint32_t kStoreMax = 2 * kBufStride - 3;   // a step stores 3 slots at P <= kStoreMax
 // stage of one round: up to kFinalSlices slices + the last exit's overrun + the reader's look-ahead
 constexpr uint32_t kStageUnits = (kFinalSlices * kSliceMax + 32 + 255) / 128 + 3;   // 16-byte units
 constexpr int kDecWarps = 16;
+// synchronisation window: the head mask `lo` covers the first 64 bits of a
+// slice; kHeadHi adds a second mask over [52, 116).  Measured: the second mask
+// cuts lane redecodes ~7x but its per-step cost outweighs them on every
+// config, so the tail gives up after 52 bits and the next lane redecodes.
+constexpr bool kHeadHi = false;
+constexpr uint32_t kHeadBits = 64;
+constexpr uint32_t kTailBits = kHeadHi ? 116 : 52;
 
 __shared__ unsigned long long sh_lim[34];   // (first[b] + count[b]), b <= 32
 __shared__ unsigned long long sh_first[34];
@@ -361,7 +368,7 @@ __device__ __forceinline__ void dstep(const Dec& d, uint32_t peek, uint32_t& len
 // and a branch-free word advance (the next word is always loaded one step
 // ahead of its use).  Positions are bits relative to the chunk's 16-byte base.
 struct Cursor {
-    uint32_t w0, w1, w2;   // w0 holds the bits [pos - o, pos - o + 32)
+    uint32_t w0, w1, w2;   // w0 holds the bits [pos - o, pos - o + 32); w2 raw
     uint32_t o;            // bit offset of pos in w0
     uint32_t na;           // shared address of the word after w2
     uint32_t pos;
@@ -370,22 +377,23 @@ struct Cursor {
         const uint32_t a = stage_s + ((r >> 5) << 2);
         w0 = bswap32(lds32(a));
         w1 = bswap32(lds32(a + 4));
-        w2 = bswap32(lds32(a + 8));
+        w2 = lds32(a + 8);   // kept raw: swapped when it moves into w1
         na = a + 12;
         o = r & 31u;
         pos = bit;
     }
     __device__ __forceinline__ uint32_t peek() const { return __funnelshift_l(w1, w0, o); }
+    // (w2 holds the raw little-endian word: its load latency hides until the window moves again)
     __device__ __forceinline__ void adv(uint32_t n) {   // n <= 32
-        const uint32_t nw = bswap32(lds32(na));
         o += n;
         pos += n;
-        const bool c = o >= 32;
-        w0 = c ? w1 : w0;
-        w1 = c ? w2 : w1;
-        w2 = c ? nw : w2;
-        na += c ? 4u : 0u;
-        o -= c ? 32u : 0u;
+        if (o >= 32) {   // predicated: the next word is loaded only when the window moves
+            w0 = w1;
+            w1 = bswap32(w2);
+            w2 = lds32(na);
+            na += 4;
+            o -= 32;
+        }
     }
 };
 
@@ -401,37 +409,42 @@ __device__ __forceinline__ void put3(uint32_t buf_s, uint32_t P, uint32_t s01, u
 
 // Phase 1a of one lane: decode from the cursor to the slice end S storing
 // symbols at ordinals P.. (lane 0 and restarted lanes start on a true
-// boundary), recording the codeword starts of the first 64 bits after A0 in
-// `lo` (head mask).  tl = the starts at/after S of the step crossing S (bit
+// boundary), recording the codeword starts of the first 116 bits after A0 in
+// two overlapping 64-bit head masks: `lo` = [0, 64), `hi` = [52, 116).  tl = the starts at/after S of the step crossing S (bit
 // 0 = S).  One loop: lanes diverge only in its trip count.
 __device__ __forceinline__ void lane_decode(const Dec& d, Cursor& rd, uint32_t A0, uint32_t S, uint32_t buf_s,
                                             uint32_t& P, uint32_t& bad, uint32_t& zf, unsigned long long& lo,
-                                            uint32_t& tl) {
+                                            unsigned long long& hi, uint32_t& tl) {
     uint32_t len = 0, mask = 0, s01, s2, p = rd.pos;
-    unsigned long long l = 0;
+    unsigned long long l = 0, h = 0;
     while (rd.pos < S) {
         p = rd.pos;
         dstep(d, rd.peek(), len, mask, s01, s2, bad);
         put3(buf_s, P, s01, s2);
         zf |= s2 & 0x10000u;
         const uint32_t r = p - A0;
-        if (r < 64) l |= (unsigned long long)mask << r;
+        if (r < kHeadBits) l |= (unsigned long long)mask << r;
+        if (kHeadHi && r - 52 < 64) h |= (unsigned long long)mask << (r - 52);
         P += __popc(mask);
         rd.adv(len);
     }
-    lo = l;
+    // keep the starts inside the slice (the crossing step may record some past S)
+    const uint32_t x = S - A0;
+    lo = x < 64 ? l & ((1ull << x) - 1) : l;
+    hi = (!kHeadHi || x <= 52) ? 0ull : (x - 52 < 64 ? h & ((1ull << (x - 52)) - 1) : h);
     const uint32_t dS = S - p;   // the last step crossed S when it started < 12 bits before it
     tl = (p < S && dS < 12) ? mask >> dS : 0u;
 }
 
 // Phase 1b: from the exit, decode on (ordinals P..) until one of the starts
-// at/after S is also in the next lane's head mask `nlo` (relative to S) --
-// the synchronisation point -- or S + 52.  sync_pos = the synchronisation
-// point (or the tail's end: a true codeword start as well, on a true lane);
-// kt = tail codewords before it.
-__device__ __forceinline__ bool lane_tail(const Dec& d, Cursor& rd, uint32_t S, uint32_t tl,
-                                          unsigned long long nlo, uint32_t buf_s, uint32_t& P, uint32_t& bad,
-                                          uint32_t& zf, uint32_t& sync_pos, uint32_t& kt) {
+// at/after S is also in the next lane's head masks (nlo, nhi, relative to S)
+// -- the synchronisation point -- or S + 116 / the next lane's slice end S2.  sync_pos = the
+// synchronisation point (or the tail's end: a true codeword start as well, on
+// a true lane); kt = tail codewords before it.
+__device__ __forceinline__ bool lane_tail(const Dec& d, Cursor& rd, uint32_t S, uint32_t S2, uint32_t tl,
+                                          unsigned long long nlo, unsigned long long nhi, uint32_t buf_s,
+                                          uint32_t& P, uint32_t& bad, uint32_t& zf, uint32_t& sync_pos,
+                                          uint32_t& kt) {
     const unsigned long long h0 = (unsigned long long)tl & nlo;
     if (h0) {   // the crossing step already met the next lane's path
         const uint32_t b = (uint32_t)(__ffsll((long long)h0) - 1);
@@ -441,14 +454,17 @@ __device__ __forceinline__ bool lane_tail(const Dec& d, Cursor& rd, uint32_t S, 
     }
     uint32_t n = __popc(tl);
     uint32_t len, mask, s01, s2;
-    while (rd.pos < S + 52) {
+    const uint32_t T = S + kTailBits < S2 ? S + kTailBits : S2;   // the next lane's head masks end at its slice end
+    while (rd.pos < T) {
         const uint32_t rt = rd.pos - S;
         dstep(d, rd.peek(), len, mask, s01, s2, bad);
         put3(buf_s, P, s01, s2);
         zf |= s2 & 0x10000u;
-        const unsigned long long hit = ((unsigned long long)mask << rt) & nlo;
-        if (hit) {
-            const uint32_t b = (uint32_t)(__ffsll((long long)hit) - 1) - rt;
+        const unsigned long long hl = rt < 64 ? ((unsigned long long)mask << rt) & nlo : 0ull;
+            const unsigned long long hh = (kHeadHi && rt >= 52) ? ((unsigned long long)mask << (rt - 52)) & nhi : 0ull;
+        if (hl | hh) {
+            const uint32_t b = hl ? (uint32_t)(__ffsll((long long)hl) - 1) - rt
+                                  : (uint32_t)(__ffsll((long long)hh) - 1) + 52 - rt;
             sync_pos = rd.pos + b;
             kt = n + __popc(mask & ((1u << b) - 1));
             return true;
@@ -460,6 +476,12 @@ __device__ __forceinline__ bool lane_tail(const Dec& d, Cursor& rd, uint32_t S, 
     sync_pos = rd.pos;
     kt = n;
     return false;
+}
+
+// codeword starts of the head masks below bit x (x < 116)
+__device__ __forceinline__ uint32_t head_below(unsigned long long lo, unsigned long long hi, uint32_t x) {
+    if (x <= 64) return (uint32_t)__popcll(x == 64 ? lo : (lo & ((1ull << x) - 1)));
+    return (uint32_t)__popcll(lo) + (uint32_t)__popcll(hi & ((1ull << (x - 52)) - 1) & ~0xFFFull);
 }
 
 __device__ __forceinline__ uint32_t zero_halves(uint32_t w) {
@@ -546,20 +568,21 @@ __device__ __noinline__ uint32_t lane_direct(const Dec& d, uint32_t stage_s, uin
 
 // One lane's phase 1 from `start` (ordinal 0): slice, exit, tail.
 __device__ __forceinline__ void lane_phase1(const Dec& d, Cursor& rd, uint32_t stage_s, uint32_t origin,
-                                            uint32_t start, uint32_t s0, uint32_t s1, bool last,
-                                            unsigned long long nlo, uint32_t buf_s, uint32_t& P, uint32_t& bad,
-                                            uint32_t& zf, unsigned long long& lo, uint32_t& ex, uint32_t& k,
-                                            uint32_t& sp, uint32_t& kt, bool& fwd) {
+                                            uint32_t start, uint32_t s0, uint32_t s1, uint32_t s2, bool last,
+                                            unsigned long long nlo, unsigned long long nhi, uint32_t buf_s,
+                                            uint32_t& P, uint32_t& bad, uint32_t& zf, unsigned long long& lo,
+                                            unsigned long long& hi, uint32_t& ex, uint32_t& k, uint32_t& sp,
+                                            uint32_t& kt, bool& fwd) {
     uint32_t tl;
     rd.seek(stage_s, origin, start);
     P = 0;
-    lane_decode(d, rd, s0, s1, buf_s, P, bad, zf, lo, tl);
+    lane_decode(d, rd, s0, s1, buf_s, P, bad, zf, lo, hi, tl);
     ex = tl ? s1 + (uint32_t)(__ffs(tl) - 1) : rd.pos;   // first codeword start >= s1
     k = P - (uint32_t)__popc(tl);                        // ordinals before the exit
     fwd = false;
     sp = ex;
     kt = 0;
-    if (!last) fwd = lane_tail(d, rd, s1, tl, nlo, buf_s, P, bad, zf, sp, kt);
+    if (!last) fwd = lane_tail(d, rd, s1, s2, tl, nlo, nhi, buf_s, P, bad, zf, sp, kt);
 }
 
 // One round: lanes [0, L) decode the slices [s0, s1) of one stretch of a
@@ -575,19 +598,21 @@ __device__ __forceinline__ bool decode_round(const Dec& d, uint32_t stage_s, uin
     const bool last = lane + 1 == L;
     Cursor rd;
     uint32_t P = 0, bad = 0, zf = 0, tl = 0;
-    unsigned long long lo = 0;
+    unsigned long long lo = 0, hi = 0;
     if (active) {
         rd.seek(stage_s, origin, s0);
-        lane_decode(d, rd, s0, s1, buf_s, P, bad, zf, lo, tl);
+        lane_decode(d, rd, s0, s1, buf_s, P, bad, zf, lo, hi, tl);
     }
     const unsigned long long nlo = __shfl_down_sync(kFull, lo, 1);
+    const unsigned long long nhi = __shfl_down_sync(kFull, hi, 1);
+    const uint32_t s2 = __shfl_down_sync(kFull, s1, 1);
     uint32_t ex = s1, k = 0, sp = s1, kt = 0;
     bool fwd = false;   // this lane's tail met the next lane's path
     if (active) {
         ex = tl ? s1 + (uint32_t)(__ffs(tl) - 1) : rd.pos;
         k = P - (uint32_t)__popc(tl);
         sp = ex;
-        if (!last) fwd = lane_tail(d, rd, s1, tl, nlo, buf_s, P, bad, zf, sp, kt);
+        if (!last) fwd = lane_tail(d, rd, s1, s2, tl, nlo, nhi, buf_s, P, bad, zf, sp, kt);
     }
     // phase 2: lane l continues lane l-1's true path from q = sp(l-1): at the
     // synchronisation point (l-1's tail met l's path: l's ordinals before q are
@@ -608,7 +633,8 @@ __device__ __forceinline__ bool decode_round(const Dec& d, uint32_t stage_s, uin
             rstart = psp;
             bad = 0;
             zf = 0;
-            lane_phase1(d, rd, stage_s, origin, psp, s0, s1, last, nlo, buf_s, P, bad, zf, lo, ex, k, sp, kt, fwd);
+            lane_phase1(d, rd, stage_s, origin, psp, s0, s1, s2, last, nlo, nhi, buf_s, P, bad, zf, lo, hi, ex, k, sp, kt,
+                        fwd);
             atomicAdd(&st->pad[0], 1ull);   // diagnostics: lane redecodes (low word)
         }
     }
@@ -617,7 +643,7 @@ __device__ __forceinline__ bool decode_round(const Dec& d, uint32_t stage_s, uin
     const uint32_t q = lane == 0 ? s0 : psp;
     uint32_t a = 0, nl = 0;
     if (active) {
-        if (lane != 0 && !restarted) a = (uint32_t)__popcll(lo & ((1ull << (q - s0)) - 1));
+        if (lane != 0 && !restarted) a = head_below(lo, hi, q - s0);
         nl = k - a;
         if (!last) nl += kt;
     }
@@ -659,9 +685,9 @@ __device__ __forceinline__ void round_units(uint32_t q, uint32_t end, uint32_t& 
     units = ((end + 32 + 255) >> 7) - u0 + 1;
 }
 
-// slice size: ~kTargetCodes codewords at the chunk's mean code length
-__device__ __forceinline__ uint32_t slice_bits(uint32_t B, uint32_t cnt) {
-    const unsigned long long s = (unsigned long long)kTargetCodes * B / (cnt ? cnt : 1);
+// slice size: ~target codewords at the chunk's mean code length
+__device__ __forceinline__ uint32_t slice_bits(uint32_t B, uint32_t cnt, uint32_t target) {
+    const unsigned long long s = (unsigned long long)target * B / (cnt ? cnt : 1);
     return (uint32_t)(s < kSliceMin ? kSliceMin : (s > kSliceMax ? kSliceMax : s));
 }
 
@@ -674,7 +700,7 @@ __global__ void __launch_bounds__(kWarps * 32, 1) inflate_fast_kernel(
     const uint64_t* __restrict__ gfirst, const int64_t* __restrict__ goffsets,
     const uint32_t* __restrict__ symbols, const uint32_t* __restrict__ gtab, int max_bw_arg,
     uint16_t* __restrict__ out, uint8_t* __restrict__ redo, unsigned int* __restrict__ next_chunk,
-    DevStatus* st) {
+    uint32_t target, DevStatus* st) {
     extern __shared__ __align__(16) uint32_t s_tab[];
     const int mx = max_bw_arg > 0 ? max_bw_arg : (int)st->max_bw;
     if (mx < 1 || mx > 32) {   // 64-bit codes: everything goes to the sequential decoder
@@ -729,8 +755,8 @@ __global__ void __launch_bounds__(kWarps * 32, 1) inflate_fast_kernel(
         const uint32_t E = sbit + B;
         bool good = B != 0 && cnt != 0;
         if (good) {
-            const uint32_t S = slice_bits(B, cnt);
-            uint32_t q = sbit, ob = 0, u0, units;
+            const uint32_t S = slice_bits(B, cnt, target);
+            uint32_t q = sbit, ob = 0, u0, units, cz = 0;   // cz: zero codes of this chunk
             round_units(q, (E - q <= kFinalSlices * S) ? E : q + 32 * S, u0, units);
             if (!have) stage_issue(stage0 + cur * kStageUnits * 16, payload4, n4, cb16, u0, units);
             have = false;
@@ -760,7 +786,7 @@ __global__ void __launch_bounds__(kWarps * 32, 1) inflate_fast_kernel(
                     const unsigned long long nboff = byte_off[cn];
                     const uint32_t nB = chunk_bits[cn];
                     const uint32_t ncnt = (uint32_t)umin(chunk, n - (uint64_t)cn * chunk);
-                    const uint32_t nS = slice_bits(nB, ncnt);
+                    const uint32_t nS = slice_bits(nB, ncnt, target);
                     const uint32_t nsb = (uint32_t)(nboff & 15) * 8;
                     uint32_t a0, au;
                     round_units(nsb, (nB <= kFinalSlices * nS) ? nsb + nB : nsb + 32 * nS, a0, au);
@@ -773,7 +799,7 @@ __global__ void __launch_bounds__(kWarps * 32, 1) inflate_fast_kernel(
                 __syncwarp();
                 uint32_t next_q = 0;
                 good = decode_round(d, stage0 + cur * kStageUnits * 16, u0 * 128, L, s0, s1, buf_s, out + base, ob,
-                                    cnt, next_q, zeros, st);
+                                    cnt, next_q, cz, st);
                 __syncwarp();   // the stage and the buffers are refilled next
                 cur ^= 1;
                 if (good && fin) good = next_q == E && ob == cnt;
@@ -788,6 +814,7 @@ __global__ void __launch_bounds__(kWarps * 32, 1) inflate_fast_kernel(
                 q = next_q;
                 u0 = nu0;
             }
+            if (good) zeros += cz;   // a chunk handed back is counted by the sequential decoder
         }
         if (!good && lane == 0) {
             redo[c] = 1;
@@ -818,6 +845,16 @@ int launch_decode_prep(sdqz_ctx* ctx, const uint64_t* first, const int64_t* offs
     return SDQZ_OK;
 }
 
+// codewords per lane slice (SDQZ_DEC_TARGET overrides, for tuning)
+static uint32_t dec_target() {
+    static const uint32_t t = [] {
+        const char* e = getenv("SDQZ_DEC_TARGET");
+        const int v = e ? atoi(e) : 0;
+        return (uint32_t)(v >= 8 && v <= 200 ? v : kTargetCodes);
+    }();
+    return t;
+}
+
 int launch_inflate_fast(sdqz_ctx* ctx, const uint8_t* payload, uint64_t nwords,
                         const uint32_t* chunk_bits, const unsigned long long* byte_off,
                         uint64_t n_chunks, uint32_t chunk, uint64_t n, const uint64_t* first,
@@ -834,7 +871,7 @@ int launch_inflate_fast(sdqz_ctx* ctx, const uint8_t* payload, uint64_t nwords,
     if (grid < 1) grid = 1;
     inflate_fast_kernel<kW><<<(unsigned)grid, kW * 32, smem, ctx->stream>>>(
         payload, nwords, chunk_bits, byte_off, n_chunks, chunk, n, first, offsets, symbols, tab, max_bw, codes,
-        redo, counter, ctx->d_status);
+        redo, counter, dec_target(), ctx->d_status);
     SDQZ_LAUNCHED_NAMED(ctx, "inflate_fast_kernel");
     return SDQZ_OK;
 }
