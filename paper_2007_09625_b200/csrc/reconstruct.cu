@@ -159,125 +159,6 @@ __device__ __forceinline__ int row_final32(int dlt, bool isout, int vout, int K,
     return S + (mine ? corr : 0) + K;
 }
 
-// 3D block 8x8x8 reconstruction.  The task's 64 codes per lane are loaded up
-// front (64 independent coalesced row loads in flight), then the Lorenzo
-// inverse runs in int32 with an overflow guard (every final and outlier value
-// below 2^28 / 2^27 keeps every intermediate inside int32); a task that trips
-// the guard is recomputed in int64 (rq3d_task64).
-template <int OUTK>
-__device__ __noinline__ void rq3d_task64(const uint16_t* __restrict__ codes,
-                                         const unsigned long long* __restrict__ dense,
-                                         uint64_t base, uint64_t YX, uint64_t X, bool xin, bool skip,
-                                         int ny, int nz, int r, double two_eb, uint32_t lane,
-                                         void* __restrict__ out) {
-    long long F[8];
-#pragma unroll
-    for (int y = 0; y < 8; y++) F[y] = 0;
-    for (int z = 0; z < nz; z++) {
-        long long R = 0, lag = 0;
-#pragma unroll
-        for (int y = 0; y < 8; y++) {
-            const bool valid = xin && y < ny;
-            const uint64_t i = base + z * YX + y * X;
-            const uint32_t code = valid ? codes[i] : (uint32_t)r;
-            const bool isout = valid && code == 0;
-            const int dlt = isout ? 0 : (int)code - r;
-            const long long vout = isout ? outlier_int(dense, i) : 0;
-            const long long K = R + F[y] - (y ? F[y - 1] : 0);
-            const long long fin = row_final<8>(dlt, isout, vout, K, lane);
-            R = fin;
-            if (y) F[y - 1] = lag;
-            lag = fin;
-            if (valid && !skip) store_out<OUTK>(out, i, fin, two_eb);
-        }
-        F[7] = lag;
-    }
-}
-
-template <int OUTK>
-__global__ void __launch_bounds__(kThreads) rq3d_kernel(const uint16_t* __restrict__ codes,
-                                                        const unsigned long long* __restrict__ dense,
-                                                        const uint8_t* __restrict__ blockflag,
-                                                        int any_slow, uint64_t Z, uint64_t Y,
-                                                        uint64_t X, uint32_t cap, double two_eb,
-                                                        void* __restrict__ out) {
-    __shared__ __align__(16) uint16_t s_codes[kWarpsPerCta][64 * 32];
-    const int r = (int)(cap >> 1);
-    const uint32_t lane = lane_id();
-    const uint64_t nbx = ceil_div(X, 8), nbx4 = ceil_div(nbx, 4), nby = ceil_div(Y, 8), nbz = ceil_div(Z, 8);
-    const uint64_t ntask = nbx4 * nby * nbz;
-    const uint64_t YX = Y * X;
-    for (uint64_t task = blockIdx.x * (uint64_t)kWarpsPerCta + (threadIdx.x >> 5); task < ntask;
-         task += (uint64_t)gridDim.x * kWarpsPerCta) {
-        const uint64_t bx4 = task % nbx4, t2 = task / nbx4;
-        const uint64_t by = t2 % nby, bz = t2 / nby;
-        const uint64_t x = bx4 * 32 + lane, y0 = by * 8, z0 = bz * 8;
-        const bool xin = x < X;
-        bool skip = false;
-        if (any_slow && xin) skip = blockflag[(bz * nby + by) * nbx + (x >> 3)] != 0;
-        const int ny = (int)umin(8, Y - y0), nz = (int)umin(8, Z - z0);
-        const uint64_t base = z0 * YX + y0 * X + x;
-        // stage the task's 8x8 rows of 32 codes in shared memory with
-        // cp.async (4-byte pieces, 16 lanes per row, two rows per instruction)
-        uint16_t* tile = s_codes[threadIdx.x >> 5];
-        {
-            const uint64_t row0 = z0 * YX + y0 * X + bx4 * 32;
-            const uint32_t half = lane >> 4, piece = lane & 15;
-#pragma unroll 8
-            for (int k = 0; k < 32; k++) {
-                const int row = 2 * k + half, z = row >> 3, y = row & 7;
-                if (z < nz && y < ny) {
-                    const uint16_t* src = codes + row0 + z * YX + y * X + 2 * piece;
-                    asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(
-                                     (uint32_t)__cvta_generic_to_shared(tile + row * 32 + 2 * piece)),
-                                 "l"(src)
-                                 : "memory");
-                }
-            }
-            asm volatile("cp.async.wait_all;" ::: "memory");
-            __syncwarp();
-        }
-        int F[8];
-#pragma unroll
-        for (int y = 0; y < 8; y++) F[y] = 0;
-        bool ovf = false;
-        float* outf = (float*)out;
-        double* outd = (double*)out;
-#pragma unroll 1
-        for (int z = 0; z < nz; z++) {
-            int R = 0, lag = 0;
-            const uint64_t zoff = base + z * YX;
-#pragma unroll
-            for (int y = 0; y < 8; y++) {
-                const bool valid = xin && y < ny;
-                const uint32_t code = valid ? tile[(z * 8 + y) * 32 + lane] : (uint32_t)r;
-                const bool isout = valid && code == 0;
-                const int dlt = isout ? 0 : (int)code - r;
-                int vout = 0;
-                if (isout) {
-                    const long long v = outlier_int(dense, zoff + y * X);
-                    ovf |= v >= (1ll << 27) || v <= -(1ll << 27);
-                    vout = (int)v;
-                }
-                const int K = R + F[y] - (y ? F[y - 1] : 0);
-                const int fin = row_final32<8>(dlt, isout, vout, K, lane);
-                ovf |= fin >= (1 << 28) || fin <= -(1 << 28);
-                R = fin;
-                if (y) F[y - 1] = lag;
-                lag = fin;
-                if (valid && !skip) {
-                    const double v = __dmul_rn((double)fin, two_eb);
-                    if (OUTK == 0) outf[zoff + y * X] = __double2float_rn(v);
-                    else outd[zoff + y * X] = v;
-                }
-            }
-            F[7] = lag;
-        }
-        if (__any_sync(kFull, ovf))
-            rq3d_task64<OUTK>(codes, dense, base, YX, X, xin, skip, ny, nz, r, two_eb, lane, out);
-        __syncwarp();   // tile reused by the next task
-    }
-}
 
 // ----------------------------------------------------------------------------
 // 3D block 8x8x8, one thread per block.  With H = prefix_x(delta),
@@ -293,29 +174,6 @@ __global__ void __launch_bounds__(kThreads) rq3d_kernel(const uint16_t* __restri
 // ----------------------------------------------------------------------------
 // one row of 8 points: x-prefix, then the y and z recurrences; outliers
 // (code 0) take their stored value.  Returns false on the magnitude guard.
-template <bool OUT>
-__device__ __forceinline__ void rq_row8(const uint32_t (&cw)[8], int r, int (&Gp)[8], int (&Fr)[8],
-                                        const unsigned long long* __restrict__ dense, uint64_t rb,
-                                        int& mn, int& mx) {
-    int H = 0;
-#pragma unroll
-    for (int x = 0; x < 8; x++) {
-        H += (int)cw[x] - r;
-        int G = H + Gp[x];
-        int f = G + Fr[x];
-        if (OUT && cw[x] == 0) {   // outlier: its final value is stored verbatim
-            const long long v = outlier_int(dense, rb + x);
-            const bool fits = v < (1ll << 28) && v > -(1ll << 28);
-            f = fits ? (int)v : (1 << 29);   // out of int32 range: trip the guard
-            G = f - Fr[x];
-            H = G - Gp[x];
-        }
-        mx = max(mx, f);
-        mn = min(mn, f);
-        Gp[x] = G;
-        Fr[x] = f;
-    }
-}
 
 template <int OUTK>
 __device__ __forceinline__ void rq_store8(void* __restrict__ out, uint64_t rb, const int (&F)[8],
@@ -341,131 +199,6 @@ __device__ __forceinline__ void rq_store8(void* __restrict__ out, uint64_t rb, c
     }
 }
 
-__device__ __forceinline__ __attribute__((unused)) bool has_zero16(uint32_t w) {   // either 16-bit half == 0
-    return ((w - 0x00010001u) & ~w & 0x80008000u) != 0;
-}
-
-// One half-row (4 points) of a block row whose other half lives in the
-// neighbouring lane.  Computed with a zero x-carry, then corrected: the true
-// x-prefix adds the left half's final H (`carry`) to every point before this
-// half's first outlier (an outlier resets the prefix).
-template <int OUTK, bool VEC>
-__device__ __forceinline__ void rq_half_row(uint2 w, int r, uint32_t h, int (&Gp)[4], int (&Fr)[4],
-                                            const unsigned long long* __restrict__ dense, uint64_t rb,
-                                            double two_eb, void* __restrict__ out, bool store, int nv,
-                                            int& mn, int& mx) {
-    const uint32_t cw[4] = {w.x & 0xFFFF, w.x >> 16, w.y & 0xFFFF, w.y >> 16};
-    int H = 0, G[4], F[4];
-    int fo = 4;   // first outlier position in this half
-    if (has_zero16(w.x) | has_zero16(w.y)) {
-#pragma unroll
-        for (int x = 3; x >= 0; x--)
-            if (cw[x] == 0) fo = x;
-#pragma unroll
-        for (int x = 0; x < 4; x++) {
-            H += (int)cw[x] - r;
-            G[x] = H + Gp[x];
-            F[x] = G[x] + Fr[x];
-            if (cw[x] == 0) {   // outlier: its final value is stored verbatim
-                const long long v = outlier_int(dense, rb + x);
-                F[x] = (v < (1ll << 28) && v > -(1ll << 28)) ? (int)v : (1 << 29);   // guard trips
-                G[x] = F[x] - Fr[x];
-                H = G[x] - Gp[x];
-            }
-        }
-    } else {
-#pragma unroll
-        for (int x = 0; x < 4; x++) {
-            H += (int)cw[x] - r;
-            G[x] = H + Gp[x];
-            F[x] = G[x] + Fr[x];
-        }
-    }
-    // x-carry from the left half (after its own outliers)
-    const int hl = __shfl_xor_sync(kFull, H, 1);
-    const int carry = h ? hl : 0;
-#pragma unroll
-    for (int x = 0; x < 4; x++) {
-        const int cx = x < fo ? carry : 0;
-        G[x] += cx;
-        F[x] += cx;
-        Gp[x] = G[x];
-        Fr[x] = F[x];
-        mx = max(mx, F[x]);
-        mn = min(mn, F[x]);
-    }
-    if (store) {
-        if (OUTK == 0) {
-            float o[4];
-#pragma unroll
-            for (int x = 0; x < 4; x++) o[x] = __double2float_rn(__dmul_rn((double)F[x], two_eb));
-            if (VEC) {
-                *reinterpret_cast<float4*>((float*)out + rb) = make_float4(o[0], o[1], o[2], o[3]);
-            } else {
-#pragma unroll
-                for (int x = 0; x < 4; x++)
-                    if (x < nv) ((float*)out)[rb + x] = o[x];
-            }
-        } else {
-            double* op = (double*)out + rb;
-#pragma unroll
-            for (int x = 0; x < 4; x++)
-                if (VEC || x < nv) op[x] = __dmul_rn((double)F[x], two_eb);
-        }
-    }
-}
-
-// 4 codes of a half row; missing points (x >= nv) read as residual 0 (code r)
-template <bool VEC>
-__device__ __forceinline__ uint2 load_half(const uint16_t* __restrict__ codes, uint64_t i, int nv, int r) {
-    if (VEC) return __ldg(reinterpret_cast<const uint2*>(codes + i));
-    uint32_t c[4];
-#pragma unroll
-    for (int x = 0; x < 4; x++) c[x] = x < nv ? codes[i + x] : (uint32_t)r;
-    return make_uint2(c[0] | (c[1] << 16), c[2] | (c[3] << 16));
-}
-
-// Block of full x-extent (8), two lanes per block (x 0-3 / 4-7); the next
-// plane's 8 row loads are in flight while the current plane is processed.
-// Rows past the field (ny < 8) load a clamped row and are never stored;
-// their values only feed later rows, so stored values are unaffected.
-template <int OUTK, bool VEC>
-__device__ __forceinline__ bool rq3d_half_block(const uint16_t* __restrict__ codes,
-                                                const unsigned long long* __restrict__ dense,
-                                                uint64_t base, uint64_t YX, uint64_t X, int nx, int ny,
-                                                int nz, int r, double two_eb, void* __restrict__ out,
-                                                uint32_t h, bool active) {
-    const int nv = VEC ? 4 : (active ? nx - 4 * (int)h : 0);   // valid points of this half
-    int Fp[8][4];
-#pragma unroll
-    for (int y = 0; y < 8; y++)
-#pragma unroll
-        for (int x = 0; x < 4; x++) Fp[y][x] = 0;
-    int mx = 0, mn = 0;
-    const uint64_t hb = base + 4 * h;
-    uint2 cur[8];
-#pragma unroll
-    for (int y = 0; y < 8; y++)
-        cur[y] = active ? load_half<VEC>(codes, hb + (uint64_t)min(y, ny - 1) * X, nv, r) : make_uint2(0, 0);
-#pragma unroll 1
-    for (int z = 0; z < nz; z++) {
-        uint2 nxt[8];
-        const uint64_t zb = hb + (uint64_t)z * YX;
-        if (z + 1 < nz && active) {
-#pragma unroll
-            for (int y = 0; y < 8; y++)
-                nxt[y] = load_half<VEC>(codes, zb + YX + (uint64_t)min(y, ny - 1) * X, nv, r);
-        }
-        int Gp[4] = {0, 0, 0, 0};
-#pragma unroll
-        for (int y = 0; y < 8; y++)
-            rq_half_row<OUTK, VEC>(cur[y], r, h, Gp, Fp[y], dense, zb + (uint64_t)y * X, two_eb, out,
-                                   active && y < ny && nv > 0, nv, mn, mx);
-#pragma unroll
-        for (int y = 0; y < 8; y++) cur[y] = nxt[y];
-    }
-    return mx < (1 << 28) && mn > -(1 << 28);
-}
 
 // One thread per block (full x-extent, 8-byte aligned rows): F of the previous
 // plane lives in shared memory, transposed ([y][x/4][thread] int4) so the
@@ -557,7 +290,8 @@ __device__ __forceinline__ bool rq3d_block_smem(const uint16_t* __restrict__ cod
                     G[x] = H + Gp[x];
                     F[x] = G[x] + F0[x];
                     if (cw[x] == 0) {   // outlier: its final value is stored verbatim
-                        const long long v = outlier_int(dense, rb + x);
+                        // rows past the field hold a clamped copy of the last row (never stored)
+                        const long long v = outlier_int(dense, (y < ny ? rb : zb + (uint64_t)(ny - 1) * X) + x);
                         F[x] = (v < (1ll << 28) && v > -(1ll << 28)) ? (int)v : (1 << 29);
                         G[x] = F[x] - F0[x];
                         H = G[x] - Gp[x];
@@ -613,51 +347,6 @@ __global__ void __launch_bounds__(kRqThreads) rq3d_block_kernel(const uint16_t* 
     }
 }
 
-template <int OUTK>
-__global__ void __launch_bounds__(kThreads) rq3d_kernel_old(const uint16_t* __restrict__ codes,
-                                                        const unsigned long long* __restrict__ dense,
-                                                        const uint8_t* __restrict__ blockflag,
-                                                        int any_slow, uint64_t Z, uint64_t Y,
-                                                        uint64_t X, uint32_t cap, double two_eb,
-                                                        void* __restrict__ out) {
-    const int r = (int)(cap >> 1);
-    const uint32_t lane = lane_id();
-    const uint64_t nbx = ceil_div(X, 8), nbx4 = ceil_div(nbx, 4), nby = ceil_div(Y, 8), nbz = ceil_div(Z, 8);
-    const uint64_t ntask = nbx4 * nby * nbz;
-    const uint64_t YX = Y * X;
-    for (uint64_t task = blockIdx.x * (uint64_t)kWarpsPerCta + (threadIdx.x >> 5); task < ntask;
-         task += (uint64_t)gridDim.x * kWarpsPerCta) {
-        const uint64_t bx4 = task % nbx4, t2 = task / nbx4;
-        const uint64_t by = t2 % nby, bz = t2 / nby;
-        const uint64_t x = bx4 * 32 + lane, y0 = by * 8, z0 = bz * 8;
-        const bool xin = x < X;
-        bool skip = false;
-        if (any_slow && xin) skip = blockflag[(bz * nby + by) * nbx + (x >> 3)] != 0;
-        const int ny = (int)umin(8, Y - y0), nz = (int)umin(8, Z - z0);
-        long long F[8];
-#pragma unroll
-        for (int y = 0; y < 8; y++) F[y] = 0;
-        for (int z = 0; z < nz; z++) {
-            long long R = 0, lag = 0;
-#pragma unroll
-            for (int y = 0; y < 8; y++) {
-                const bool valid = xin && y < ny;
-                const uint64_t i = (z0 + z) * YX + (y0 + y) * X + x;
-                uint32_t code = valid ? codes[i] : (uint32_t)r;
-                const bool isout = valid && code == 0;
-                const int dlt = isout ? 0 : (int)code - r;
-                const long long vout = isout ? outlier_int(dense, i) : 0;
-                const long long K = R + F[y] - (y ? F[y - 1] : 0);
-                const long long fin = row_final<8>(dlt, isout, vout, K, lane);
-                R = fin;
-                if (y) F[y - 1] = lag;
-                lag = fin;
-                if (valid && !skip) store_out<OUTK>(out, i, fin, two_eb);
-            }
-            F[7] = lag;
-        }
-    }
-}
 
 template <int OUTK>
 __global__ void __launch_bounds__(kThreads) rq2d_kernel(const uint16_t* __restrict__ codes,
@@ -1316,7 +1005,6 @@ int launch_reconstruct(sdqz_ctx* ctx, const uint16_t* codes, const uint64_t* den
         if (grid < 1) grid = 1;
         int slow = any_slow ? 1 : 0;
         // cp.async staging needs 4-byte aligned code rows
-        const bool staged = dims[2] % 2 == 0 && ((uintptr_t)codes & 3) == 0;
         const uint64_t nblk3 = ndims == 3 ? ceil_div(dims[0], 8) * ceil_div(dims[1], 8) * ceil_div(dims[2], 8) : 1;
         uint64_t bgrid = ceil_div(nblk3, 64);
         if (bgrid > (uint64_t)ctx->num_sms * 16) bgrid = (uint64_t)ctx->num_sms * 16;
@@ -1334,15 +1022,9 @@ int launch_reconstruct(sdqz_ctx* ctx, const uint16_t* codes, const uint64_t* den
         if (vgrid > (uint64_t)ctx->num_sms * 8) vgrid = (uint64_t)ctx->num_sms * 8;
         if (vgrid < 1) vgrid = 1;
 #define RQ_LAUNCH(K)                                                                                 \
-        if (ndims == 3 && !env_disabled("SDQZ_RQ_WARP"))                                             \
+        if (ndims == 3)                                                                              \
             rq3d_block_kernel<K><<<(unsigned)bgrid, 64, 0, ctx->stream>>>(codes, dn, const_cast<uint8_t*>(blockflag), slow, \
                                                                         dims[0], dims[1], dims[2], cap, two_eb, out, ctx->d_status); \
-        else if (ndims == 3 && staged)                                                               \
-            rq3d_kernel<K><<<(unsigned)grid, kThreads, 0, ctx->stream>>>(codes, dn, blockflag, slow,   \
-                                                                        dims[0], dims[1], dims[2], cap, two_eb, out); \
-        else if (ndims == 3)                                                                         \
-            rq3d_kernel_old<K><<<(unsigned)grid, kThreads, 0, ctx->stream>>>(codes, dn, blockflag, slow, \
-                                                                        dims[0], dims[1], dims[2], cap, two_eb, out); \
         else if (vec2d)                                                                              \
             rq2d_vec_kernel<K><<<(unsigned)grid2, kThreads, 0, ctx->stream>>>(codes, dn, blockflag, slow, \
                                                                              dims[0], dims[1], cap, two_eb, out); \

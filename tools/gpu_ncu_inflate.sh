@@ -3,6 +3,6 @@
 set -u
 OUT=gpurun_out
 for c in ${CFGS:-large hacc}; do
-timeout 900 ncu --set full --clock-control none --import-source on -k regex:"${K:-inflate_fast}" -c 1 -o $OUT/prof_inflate_$c python tools/profile_step.py $c 1 > $OUT/ncu_$c.log 2>&1
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:"${K:-inflate_fast}" -c ${NC:-1} -o $OUT/prof_inflate_$c python tools/profile_step.py $c 1 > $OUT/ncu_$c.log 2>&1
 echo "ncu_$c=$?"
 done

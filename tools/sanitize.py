@@ -45,6 +45,9 @@ def main():
     walk = np.cumsum(res).astype(np.float32)
     rt(walk, eb=0.5, cap=64, block_shape=(walk.size,))                                           # 64-bit units
     rt(rng.normal(0, 1, (300,)).astype(np.float32), eb=0.05, chunk_size=7)                       # odd chunks
+    # chunks of 65536 codes: the warp decoder's multi-round path (staged rounds, prefetch)
+    rt(S.generate_field("smooth", (150000,), seed=4).astype(np.float32), eb=1e-4, mode="valrel", chunk_size=65536)
+    rt(S.generate_field("sparse-near-zero", (64, 48, 40), seed=5).astype(np.float32), eb=1e-5, mode="valrel", chunk_size=16384)
     # corrupted payload: the warp decoder hands chunks back to the exact decoder
     blob = bytearray(S.compress(f3, eb=1e-4, mode="valrel"))
     h = S.parse_header(bytes(blob))
