@@ -244,6 +244,23 @@ SDQZ_API int sdqz_parse_header(sdqz_ctx* ctx, const uint8_t* h_buf, uint64_t len
 SDQZ_API int sdqz_decompress(sdqz_ctx* ctx, const uint8_t* h_archive, uint64_t len, void* d_out);
 
 /* decompress from device-resident sections (same checks as deserialize). */
+/* ---- host-buffer pipeline (no caller-side device memory) ----------------
+ * The same compress / decompress / quality with HOST input and output
+ * buffers: inputs go through the context's pinned staging into context-owned
+ * device memory, outputs come back the same way.  For callers without a
+ * device allocator (the CLI: python -m paper_2007_09625_b200, cli.py:68-109). */
+SDQZ_API int sdqz_device_count(int* n);
+/* compress (pipeline.py:15-39) of a host field; archive via sdqz_archive_write. */
+SDQZ_API int sdqz_compress_host(sdqz_ctx* ctx, const void* h_in, int dtype, int ndims, const uint64_t dims[3],
+                                const uint32_t block[3], int eb_mode, double eb, uint32_t cap, uint32_t chunk,
+                                sdqz_header* hdr);
+/* decompress (pipeline.py:56-58) of a host archive into host memory
+ * (float32/float64 per header dtype, dims[0]*dims[1]*dims[2] values). */
+SDQZ_API int sdqz_decompress_host(sdqz_ctx* ctx, const uint8_t* h_archive, uint64_t len, void* h_out);
+/* quality (metrics.py:52-76) of two host arrays (out as sdqz_quality). */
+SDQZ_API int sdqz_quality_host(sdqz_ctx* ctx, const void* h_orig, int orig_dtype, const void* h_recon,
+                               int recon_dtype, uint64_t n, double* out);
+
 SDQZ_API int sdqz_decompress_sections(sdqz_ctx* ctx, const sdqz_header* hdr, const uint8_t* d_bw,
                              const void* d_outliers, const uint32_t* d_chunk_bits,
                              const uint8_t* d_payload, void* d_out);

@@ -104,6 +104,13 @@ _SIGS = {
     "sdqz_decompress_slab": (c_int, [c_void_p, POINTER(Header), c_void_p, c_void_p, c_uint64, c_uint64,
                                      c_void_p, c_uint64, c_void_p, c_uint64, c_uint64, c_uint64,
                                      POINTER(c_uint64), c_void_p]),
+    "sdqz_device_count": (c_int, [POINTER(c_int)]),
+    "sdqz_compress_host": (c_int, [c_void_p, c_void_p, c_int, c_int, POINTER(c_uint64),
+                                   POINTER(c_uint32), c_int, c_double, c_uint32, c_uint32,
+                                   POINTER(Header)]),
+    "sdqz_decompress_host": (c_int, [c_void_p, c_void_p, c_uint64, c_void_p]),
+    "sdqz_quality_host": (c_int, [c_void_p, c_void_p, c_int, c_void_p, c_int, c_uint64,
+                                  POINTER(c_double)]),
     "sdqz_shard_describe": (c_int, [c_void_p, c_void_p, c_int, c_uint64, c_void_p]),
     "sdqz_shard_quantize": (c_int, [c_void_p, c_void_p, c_int, c_int, POINTER(c_uint64), POINTER(c_uint32),
                                     c_int, c_double, c_uint32, c_void_p, c_void_p]),
@@ -208,7 +215,48 @@ class Context:
             pass
 
 
+class HostContext(Context):
+    """A context with its own CUDA stream and no torch: for the host-buffer
+    entry points (sdqz_*_host), e.g. the CLI, which then never imports torch."""
+
+    def __init__(self, device: int):  # noqa: D401 - no torch here
+        self.lib = load_library()
+        self.device = device
+        self.torch = None
+        h = c_void_p()
+        rc = self.lib.sdqz_ctx_create(device, None, byref(h))
+        if rc:
+            raise RuntimeError(f"sdqz_ctx_create failed ({rc}) on cuda:{device}")
+        self.h = h
+
+    def sync_stream(self):
+        pass
+
+
 _tls = threading.local()
+
+
+def host_context() -> HostContext:
+    """The calling thread's torch-free context (device: torch's current one if
+    torch is loaded, else $SDQZ_DEVICE or 0).  Raises without a CUDA device."""
+    import sys
+    lib = load_library()
+    n = c_int(0)
+    lib.sdqz_device_count(byref(n))
+    if n.value < 1:
+        raise RuntimeError("sdqz (B200 build) needs a CUDA device; no CPU fallback exists")
+    torch = sys.modules.get("torch")
+    if torch is not None and torch.cuda.is_initialized():
+        device = torch.cuda.current_device()
+    else:
+        device = int(os.environ.get("SDQZ_DEVICE", "0"))
+    hc = getattr(_tls, "hctx", None)
+    if hc is None:
+        hc = _tls.hctx = {}
+    ctx = hc.get(device)
+    if ctx is None:
+        ctx = hc[device] = HostContext(device)
+    return ctx
 
 
 def require_cuda():

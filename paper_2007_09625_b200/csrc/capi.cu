@@ -1506,4 +1506,56 @@ int sdqz_decompress(sdqz_ctx* ctx, const uint8_t* h, uint64_t len, void* d_out) 
     return sdqz_decompress_sections(ctx, &hdr, bw, rec, cb, pay, d_out);
 }
 
+
+// ---- host-buffer entry points (no caller-side device memory) --------------
+int sdqz_device_count(int* n) {
+    if (!n) return SDQZ_EINVAL;
+    *n = 0;
+    if (cudaGetDeviceCount(n) != cudaSuccess) *n = 0;
+    return SDQZ_OK;
+}
+
+int sdqz_compress_host(sdqz_ctx* ctx, const void* h_in, int dtype, int ndims, const uint64_t dims[3],
+                       const uint32_t block[3], int eb_mode, double eb, uint32_t cap, uint32_t chunk,
+                       sdqz_header* hdr) {
+    int rc = SDQZ_OK;
+    if (!h_in || !dims || ndims < 1 || ndims > 3) return set_error(ctx, SDQZ_EINVAL, "invalid arguments");
+    uint64_t n = 1;
+    for (int a = 0; a < ndims; a++) n *= dims[a];
+    const uint64_t bytes = n * (dtype ? 8 : 4);
+    uint8_t* d_in = scratch_as<uint8_t>(ctx, S_HOST_A, bytes + 16, &rc);
+    if (!d_in) return rc;
+    const Seg seg{d_in, bytes};
+    if ((rc = staged_copy(ctx, (uint8_t*)const_cast<void*>(h_in), &seg, 1, false))) return rc;
+    return sdqz_compress(ctx, d_in, dtype, ndims, dims, block, eb_mode, eb, cap, chunk, hdr);
+}
+
+int sdqz_decompress_host(sdqz_ctx* ctx, const uint8_t* h_archive, uint64_t len, void* h_out) {
+    int rc = SDQZ_OK;
+    sdqz_header hdr;
+    if ((rc = sdqz_parse_header(ctx, h_archive, len, &hdr))) return rc;
+    uint64_t n = 1;
+    for (uint32_t a = 0; a < hdr.ndims && a < 3; a++) n *= hdr.dims[a];
+    const uint64_t bytes = n * (hdr.dtype_code ? 8 : 4);
+    uint8_t* d_out = scratch_as<uint8_t>(ctx, S_HOST_B, bytes + 16, &rc);
+    if (!d_out) return rc;
+    if ((rc = sdqz_decompress(ctx, h_archive, len, d_out))) return rc;
+    const Seg seg{d_out, bytes};
+    return staged_copy(ctx, (uint8_t*)h_out, &seg, 1, true);
+}
+
+int sdqz_quality_host(sdqz_ctx* ctx, const void* h_orig, int orig_dtype, const void* h_recon, int recon_dtype,
+                      uint64_t n, double* out) {
+    int rc = SDQZ_OK;
+    if (n == 0) return set_error(ctx, SDQZ_EINVAL, "cannot score empty arrays");
+    const uint64_t ba = n * (orig_dtype ? 8 : 4), bb = n * (recon_dtype ? 8 : 4);
+    uint8_t* da = scratch_as<uint8_t>(ctx, S_HOST_A, ba + 16, &rc);
+    uint8_t* db = scratch_as<uint8_t>(ctx, S_HOST_B, bb + 16, &rc);
+    if (!da || !db) return rc;
+    const Seg sa{da, ba}, sb{db, bb};
+    if ((rc = staged_copy(ctx, (uint8_t*)const_cast<void*>(h_orig), &sa, 1, false))) return rc;
+    if ((rc = staged_copy(ctx, (uint8_t*)const_cast<void*>(h_recon), &sb, 1, false))) return rc;
+    return sdqz_quality(ctx, da, orig_dtype, db, recon_dtype, n, out);
+}
+
 }  // extern "C"

@@ -216,7 +216,9 @@ namespace sdqz {
 enum Slot : int {
     S_CODES = 0, S_HIST, S_BW, S_ENTRIES, S_FIRST, S_OFFSETS, S_SYMBOLS, S_LUT,
     S_CHUNK_BITS, S_CHUNK_AUX, S_BYTE_OFF, S_OUT_OFF, S_PAYLOAD, S_OUTREC, S_SORT,
-    S_TREE, S_STAGE, S_DENSE, S_WORK, S_BLOCKFLAG, S_MISC, S_REDO, S_DTAB, S_COUNTER, S_QUAL, S_REBASE, S_NSLOTS
+    S_TREE, S_STAGE, S_DENSE, S_WORK, S_BLOCKFLAG, S_MISC, S_REDO, S_DTAB, S_COUNTER, S_QUAL, S_REBASE,
+    S_HOST_A, S_HOST_B,   // device copies of host-buffer inputs / outputs (sdqz_*_host)
+    S_NSLOTS
 };
 
 int set_error(sdqz_ctx* ctx, int code, const std::string& msg);

@@ -143,6 +143,57 @@ def compress(data, dims=None, *, eb: float, mode: str = "abs", cap: int = 1024,
                            chunk_size=chunk_size).to_bytes()
 
 
+def compress_host(data, dims=None, *, eb: float, mode: str = "abs", cap: int = 1024,
+                  block_shape=None, chunk_size: int | None = None) -> bytes:
+    """compress() of a host array through the host-buffer C-ABI
+    (sdqz_compress_host): the field is staged to the device by the library,
+    the archive comes back the same way; torch is never imported."""
+    arr = np.asarray(data)
+    dims, block, pending = _check_request(arr, dims, eb, mode, cap, block_shape, chunk_size)
+    dt = _device.field_dtype(arr)
+    a = np.ascontiguousarray(arr, dtype=dt).reshape(-1)
+    if pending is not None:
+        # what resolve_error_bound raises first (core.py:161-175), then the pending error
+        from .core import describe_field, resolve_error_bound
+        ebr = resolve_error_bound(ErrorBoundSpec(mode, eb), describe_field(a, (a.size,)))
+        if not (ebr > 0 and math.isfinite(ebr)):
+            raise SdqzError("error bound must be positive and finite")
+        raise pending
+    ctx = _lib.host_context()
+    hdr = _lib.Header()
+    ctx.call("sdqz_compress_host", ctypes.c_void_p(a.ctypes.data), 0 if dt == np.float32 else 1,
+             len(dims), _lib.dims3(dims), _lib.block3(block), 0 if mode == "abs" else 1, float(eb),
+             int(cap), int(chunk_size or 0), ctypes.byref(hdr))
+    n = hdr.total_bytes
+    out = _PyBytes_FromStringAndSize(None, n)
+    ctx.call("sdqz_archive_write", ctx.archive_generation, ctypes.c_void_p(_PyBytes_AsString(out)), n)
+    return out
+
+
+def decompress_host(blob: bytes) -> np.ndarray:
+    """decompress() into a host array through the host-buffer C-ABI
+    (sdqz_decompress_host); torch is never imported."""
+    blob = bytes(blob)
+    ctx = _lib.host_context()
+    h = _lib.Header()
+    base = ctypes.c_void_p(_PyBytes_AsString(blob))
+    try:
+        ctx.call("sdqz_parse_header", base, len(blob), ctypes.byref(h))
+    except ArchiveFormatError as e:
+        if str(e) == "bad magic":
+            raise ArchiveFormatError(f"bad magic {blob[:4]!r}") from None
+        raise
+    dims = _dims_of(h)
+    out = np.empty(math.prod(dims), np.float32 if h.dtype_code == 0 else np.float64)
+    try:
+        ctx.call("sdqz_decompress_host", base, len(blob), ctypes.c_void_p(out.ctypes.data))
+        _check_geometry(h)
+    except SdqzError as e:
+        _rewrite_geometry_error(e, blob)
+        raise
+    return out.reshape(dims)
+
+
 def _dims_of(h) -> tuple[int, ...]:
     return tuple(int(h.dims[a]) for a in range(h.ndims))
 
@@ -248,7 +299,8 @@ def decompress_archive(ar: Archive, workers: int | None = None) -> np.ndarray:
 
 
 __all__ = ["compress", "decompress", "decompress_archive", "compress_device",
-           "decompress_device", "DeviceArchive", "DEFAULT_BLOCK_SHAPES"]
+           "decompress_device", "compress_host", "decompress_host", "DeviceArchive",
+           "DEFAULT_BLOCK_SHAPES"]
 
 
 class CompressPlan:

@@ -10,5 +10,5 @@ from paper_2007_09625_b200 import *  # noqa: F401,F403
 from paper_2007_09625_b200 import __all__  # noqa: F401
 
 __version__ = getattr(_pkg, "__version__", "0.1.0")
-for _m in ("archive", "core", "dualquant", "huffman", "metrics", "pipeline", "synthetic"):
+for _m in ("archive", "core", "dualquant", "huffman", "metrics", "pipeline", "synthetic", "cli"):
     sys.modules[f"{__name__}.{_m}"] = importlib.import_module(f"paper_2007_09625_b200.{_m}")

@@ -76,3 +76,34 @@ def test_second_device_context_if_present():
         with torch.cuda.device(d):
             blobs.append(S.compress(a, eb=1e-4, mode="valrel"))
     assert blobs[0] == blobs[1]
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("shape,mode,eb", [((40, 56, 24), "valrel", 1e-4), ((1800, 36), "abs", 0.05),
+                                           ((100003,), "valrel", 1e-3)])
+def test_host_buffer_path_matches(shape, mode, eb):
+    """sdqz_compress_host / sdqz_decompress_host / sdqz_quality_host (the CLI's
+    torch-free path) produce the same archive, field and scores."""
+    import paper_2007_09625_b200 as S
+    from paper_2007_09625_b200 import metrics, pipeline
+    f = S.generate_field("smooth", shape, seed=3).astype(np.float32)
+    blob = S.compress(f, eb=eb, mode=mode)
+    assert pipeline.compress_host(f, eb=eb, mode=mode) == blob
+    out = pipeline.decompress_host(blob)
+    assert out.shape == shape and np.array_equal(out.view(np.uint32), S.decompress(blob).view(np.uint32))
+    assert metrics.quality_host(f, out) == metrics.quality(f, out)
+
+
+@pytest.mark.gpu
+def test_host_buffer_path_errors():
+    import paper_2007_09625_b200 as S
+    from paper_2007_09625_b200 import pipeline
+    bad = np.ones(64, np.float32)
+    bad[3] = np.nan
+    with pytest.raises(S.SdqzError, match="NaN"):
+        pipeline.compress_host(bad, eb=0.1)
+    with pytest.raises(S.ArchiveFormatError, match="bad magic"):
+        pipeline.decompress_host(b"XXXX" + bytes(100))
+    blob = bytearray(S.compress(S.generate_field("smooth", (32, 32), seed=1).astype(np.float32), eb=1e-3))
+    with pytest.raises(S.ArchiveFormatError):
+        pipeline.decompress_host(bytes(blob[:60]))

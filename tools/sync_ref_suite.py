@@ -1,5 +1,5 @@
-"""Copy the reference's own test suite (/root/reference/pkg/tests, the CLI
-tests excluded -- the CLI is out of scope) into tests/ref_suite/_ref, a
+"""Copy the reference's own test suite (/root/reference/pkg/tests, CLI tests
+included: paper_2007_09625_b200/cli.py routes the CLI through the GPU) into tests/ref_suite/_ref, a
 git-ignored directory that travels to the GPU box with the repo snapshot.
 tests/test_ref_suite.py runs it there against the drop-in through the `sdqz`
 shim (tests/ref_suite/shim).  The golden archive the reference's acceptance
@@ -13,7 +13,7 @@ SRC = Path("/root/reference/pkg/tests")
 ROOT = Path(__file__).resolve().parents[1]
 DST = ROOT / "tests" / "ref_suite" / "_ref"
 FILES = ("conftest.py", "reference.py", "test_acceptance.py", "test_archive.py", "test_core.py",
-         "test_dualquant.py", "test_huffman.py", "test_metrics.py")
+         "test_dualquant.py", "test_huffman.py", "test_metrics.py", "test_cli.py")
 
 
 def main() -> int:
