@@ -244,6 +244,17 @@ SDQZ_API int sdqz_parse_header(sdqz_ctx* ctx, const uint8_t* h_buf, uint64_t len
 SDQZ_API int sdqz_decompress(sdqz_ctx* ctx, const uint8_t* h_archive, uint64_t len, void* d_out);
 
 /* decompress from device-resident sections (same checks as deserialize). */
+/* decompress_sections + quality (metrics.py:52-76) against the original
+ * device field d_orig, the reduction fused into the reconstruct kernels'
+ * epilogue (one pass: codes + original in, field out).  q5 as sdqz_quality.
+ * *fused = 0 when the path had no fused kernel (generic block shapes, blocks
+ * replayed in fp64); the scores then come from a separate pass.  Used by
+ * rd_sweep / the CLI sweep (metrics.py:89-118). */
+SDQZ_API int sdqz_decompress_quality(sdqz_ctx* ctx, const sdqz_header* hdr, const uint8_t* d_bw,
+                                     const void* d_outliers, const uint32_t* d_chunk_bits,
+                                     const uint8_t* d_payload, void* d_out, const void* d_orig, int orig_dtype,
+                                     double* q5, int* fused);
+
 /* ---- host-buffer pipeline (no caller-side device memory) ----------------
  * The same compress / decompress / quality with HOST input and output
  * buffers: inputs go through the context's pinned staging into context-owned

@@ -104,6 +104,8 @@ _SIGS = {
     "sdqz_decompress_slab": (c_int, [c_void_p, POINTER(Header), c_void_p, c_void_p, c_uint64, c_uint64,
                                      c_void_p, c_uint64, c_void_p, c_uint64, c_uint64, c_uint64,
                                      POINTER(c_uint64), c_void_p]),
+    "sdqz_decompress_quality": (c_int, [c_void_p, POINTER(Header), c_void_p, c_void_p, c_void_p, c_void_p,
+                                        c_void_p, c_void_p, c_int, POINTER(c_double), POINTER(c_int)]),
     "sdqz_device_count": (c_int, [POINTER(c_int)]),
     "sdqz_compress_host": (c_int, [c_void_p, c_void_p, c_int, c_int, POINTER(c_uint64),
                                    POINTER(c_uint32), c_int, c_double, c_uint32, c_uint32,

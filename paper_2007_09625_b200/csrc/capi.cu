@@ -369,7 +369,7 @@ void capture_graph(sdqz_ctx* ctx, sdqz_ctx::Graph& g, const std::string& key, En
     cudaGraphDestroy(graph);
 }
 
-bool graphs_on(const sdqz_ctx* ctx) { return !ctx->timing && !env_disabled("SDQZ_NO_GRAPH"); }
+bool graphs_on(const sdqz_ctx* ctx) { return !ctx->timing && !ctx->qual.orig && !env_disabled("SDQZ_NO_GRAPH"); }
 
 // Shared decompress core over device-resident sections.  The enqueue part (all
 // launches + the status copy) replays as a CUDA graph when a call repeats the
@@ -1506,6 +1506,35 @@ int sdqz_decompress(sdqz_ctx* ctx, const uint8_t* h, uint64_t len, void* d_out) 
     return sdqz_decompress_sections(ctx, &hdr, bw, rec, cb, pay, d_out);
 }
 
+
+// ---- decompress with the quality reduction fused into reconstruct ---------
+int sdqz_decompress_quality(sdqz_ctx* ctx, const sdqz_header* hdr, const uint8_t* d_bw, const void* d_outliers,
+                            const uint32_t* d_chunk_bits, const uint8_t* d_payload, void* d_out,
+                            const void* d_orig, int orig_dtype, double* q5, int* fused) {
+    int rc = SDQZ_OK;
+    if (!hdr || !d_orig || !q5) return set_error(ctx, SDQZ_EINVAL, "invalid arguments");
+    uint64_t n = 1;
+    for (uint32_t a = 0; a < hdr->ndims && a < 3; a++) n *= hdr->dims[a];
+    if (n == 0) return set_error(ctx, SDQZ_EINVAL, "cannot score empty arrays");
+    double* part = scratch_as<double>(ctx, S_QUAL, 5 * 4096 + 8, &rc);
+    if (!part) return rc;
+    ctx->qual.orig = d_orig;
+    ctx->qual.okind = orig_dtype;
+    ctx->qual.part = part;
+    ctx->qual.nparts = 0;
+    rc = sdqz_decompress_sections(ctx, hdr, d_bw, d_outliers, d_chunk_bits, d_payload, d_out);
+    const uint64_t nparts = ctx->qual.nparts;
+    ctx->qual = QualArgs{};
+    if (rc) return rc;
+    // fused only when a fast kernel scored every point (no fp64 replay of blocks)
+    const bool ok = nparts > 0 && nparts <= 4096 && !(ctx->h_status->flags & F_OUT_SLOW);
+    if (fused) *fused = ok ? 1 : 0;
+    if (!ok) return sdqz_quality(ctx, d_orig, orig_dtype, d_out, hdr->dtype_code, n, q5);
+    if ((rc = launch_quality_fold(ctx, part, nparts, part + 5 * 4096))) return rc;
+    SDQZ_CUDA(ctx, cudaMemcpyAsync(q5, part + 5 * 4096, 5 * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
+    SDQZ_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
+    return SDQZ_OK;
+}
 
 // ---- host-buffer entry points (no caller-side device memory) --------------
 int sdqz_device_count(int* n) {

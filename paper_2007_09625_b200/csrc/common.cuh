@@ -151,6 +151,16 @@ __device__ __forceinline__ int warp_excl_scan(int v, int* total) {
 // Context (opaque to callers).  Owns a stream, a grow-only scratch arena and
 // the pinned status block.
 // ---------------------------------------------------------------------------
+// Reconstruction quality fused into the reconstruct kernels' epilogue
+// (metrics.py:52-76; sdqz_decompress_quality): the original field, and one
+// 5-double partial {sum d^2, max |d|, min orig, max orig, nonfinite} per CTA.
+struct QualArgs {
+    const void* orig = nullptr;   // nullptr: off
+    int okind = 0;                // 0 f32, 1 f64
+    double* part = nullptr;
+    uint64_t nparts = 0;          // set by the launcher that fused it (0: not fused)
+};
+
 struct sdqz_ctx {
     int device = 0;
     cudaStream_t stream = nullptr;
@@ -208,6 +218,7 @@ struct sdqz_ctx {
     size_t ev_used = 0;
     std::vector<std::pair<const char*, size_t>> marks;   // (name, event index)
     std::vector<std::pair<std::string, double>> ktotals; // accumulated ms per kernel
+    QualArgs qual;                                     // fused-quality request (sdqz_decompress_quality)
 };
 
 namespace sdqz {

@@ -182,6 +182,12 @@ __global__ void quality_final_kernel(const double* __restrict__ part, int nparts
 
 }  // namespace
 
+int launch_quality_fold(sdqz_ctx* ctx, const double* d_part, uint64_t nparts, double* d_out) {
+    quality_final_kernel<<<1, 1, 0, ctx->stream>>>(d_part, (int)nparts, d_out);
+    SDQZ_LAUNCHED_NAMED(ctx, "quality_final_kernel");
+    return SDQZ_OK;
+}
+
 int launch_quality(sdqz_ctx* ctx, const void* a, int a_dtype, const void* b, int b_dtype, uint64_t n,
                    double* d_part, double* d_out) {
     uint64_t g = ceil_div(n, 256 * 4);

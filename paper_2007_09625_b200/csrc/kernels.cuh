@@ -94,6 +94,8 @@ bool rq1d_records_ok(int ndims, const uint64_t dims[3], const uint32_t block[3],
 int launch_reconstruct_1d_records(sdqz_ctx* ctx, const uint16_t* codes, const void* records, uint64_t k,
                                   uint64_t n, uint32_t cap, double two_eb, void* out, int out_kind,
                                   uint64_t* dense, uint8_t* blockflag);
+// fixed-order fold of per-CTA quality partials (5 doubles each) into d_out[5]
+int launch_quality_fold(sdqz_ctx* ctx, const double* d_part, uint64_t nparts, double* d_out);
 int launch_quality(sdqz_ctx* ctx, const void* a, int a_dtype, const void* b, int b_dtype, uint64_t n,
                    double* d_part, double* d_out);
 int launch_reconstruct(sdqz_ctx* ctx, const uint16_t* codes, const uint64_t* dense,

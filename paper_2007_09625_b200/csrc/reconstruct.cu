@@ -115,6 +115,51 @@ __device__ __forceinline__ void store_out(void* out, uint64_t i, long long fin, 
     else ((double*)out)[i] = v;
 }
 
+// fused quality (metrics.py:52-76): per-thread partials of the stored values
+// against the original field, folded per CTA into part[blockIdx.x]
+struct QAcc {
+    double ss = 0.0, mx = 0.0, mn = INFINITY, mo = -INFINITY;
+    bool bad = false;
+    __device__ __forceinline__ void add(const QualArgs& q, uint64_t i, double y) {
+        const double x = q.okind ? __ldcs((const double*)q.orig + i) : (double)__ldcs((const float*)q.orig + i);
+        const double d = __dsub_rn(x, y);
+        ss = __fma_rn(d, d, ss);
+        mx = isnan(d) ? d : fmax(mx, fabs(d));
+        mn = fmin(mn, x);
+        mo = fmax(mo, x);
+        bad |= !isfinite(x);
+    }
+};
+
+// block reduction of the partials (every thread of the CTA calls it once)
+__device__ void qacc_flush(QAcc& a, const QualArgs& q) {
+    __shared__ double s[5][32];
+    const uint32_t lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = (blockDim.x + 31) >> 5;
+#pragma unroll
+    for (int o = 16; o; o >>= 1) {
+        a.ss += __shfl_down_sync(kFull, a.ss, o);
+        const double m2 = __shfl_down_sync(kFull, a.mx, o);
+        a.mx = isnan(m2) ? m2 : fmax(a.mx, m2);
+        a.mn = fmin(a.mn, __shfl_down_sync(kFull, a.mn, o));
+        a.mo = fmax(a.mo, __shfl_down_sync(kFull, a.mo, o));
+    }
+    const bool wbad = __any_sync(kFull, a.bad);
+    if (lane == 0) { s[0][w] = a.ss; s[1][w] = a.mx; s[2][w] = a.mn; s[3][w] = a.mo; s[4][w] = wbad ? 1.0 : 0.0; }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double r0 = 0.0, r1 = 0.0, r2 = INFINITY, r3 = -INFINITY, r4 = 0.0;
+        for (uint32_t k = 0; k < nw; k++) {
+            r0 += s[0][k];
+            r1 = isnan(s[1][k]) ? s[1][k] : fmax(r1, s[1][k]);
+            r2 = fmin(r2, s[2][k]);
+            r3 = fmax(r3, s[3][k]);
+            r4 = fmax(r4, s[4][k]);
+        }
+        double* p = q.part + 5 * blockIdx.x;
+        p[0] = r0; p[1] = r1; p[2] = r2; p[3] = r3; p[4] = r4;
+    }
+}
+
 __device__ __forceinline__ long long outlier_int(const unsigned long long* dense, uint64_t i) {
     return (long long)__longlong_as_double((long long)dense[i]);
 }
@@ -177,11 +222,16 @@ __device__ __forceinline__ int row_final32(int dlt, bool isout, int vout, int K,
 
 template <int OUTK>
 __device__ __forceinline__ void rq_store8(void* __restrict__ out, uint64_t rb, const int (&F)[8],
-                                          double two_eb, int nx, bool vec) {
+                                          double two_eb, int nx, bool vec, const QualArgs& q, QAcc& acc) {
     if (OUTK == 0) {
         float o[8];
 #pragma unroll
         for (int x = 0; x < 8; x++) o[x] = __double2float_rn(__dmul_rn((double)F[x], two_eb));
+        if (q.orig) {
+#pragma unroll
+            for (int x = 0; x < 8; x++)
+                if (x < nx) acc.add(q, rb + x, (double)o[x]);
+        }
         float* op = (float*)out + rb;
         if (vec) {
             *reinterpret_cast<float4*>(op) = make_float4(o[0], o[1], o[2], o[3]);
@@ -196,6 +246,11 @@ __device__ __forceinline__ void rq_store8(void* __restrict__ out, uint64_t rb, c
 #pragma unroll
         for (int x = 0; x < 8; x++)
             if (vec || x < nx) op[x] = __dmul_rn((double)F[x], two_eb);
+        if (q.orig) {
+#pragma unroll
+            for (int x = 0; x < 8; x++)
+                if (x < nx) acc.add(q, rb + x, __dmul_rn((double)F[x], two_eb));
+        }
     }
 }
 
@@ -221,7 +276,7 @@ __device__ __forceinline__ bool rq3d_block_smem(const uint16_t* __restrict__ cod
                                                 uint64_t base, uint64_t YX, uint64_t X, int nx, int ny,
                                                 int nz, int r, double two_eb, void* __restrict__ out,
                                                 int4* __restrict__ fp, uint2* __restrict__ cs, bool vec,
-                                                bool vec_out) {
+                                                bool vec_out, const QualArgs& q, QAcc& acc) {
     // vec: 8-byte aligned rows whose 16-byte reads stay inside the array
     // (cp.async); otherwise rows are gathered with guarded scalar loads.
     // x >= nx (partial edge block): the row read runs into the next row; those
@@ -306,7 +361,7 @@ __device__ __forceinline__ bool rq3d_block_smem(const uint16_t* __restrict__ cod
             }
             fp[(y * 2) * kRqThreads] = make_int4(F[0], F[1], F[2], F[3]);
             fp[(y * 2 + 1) * kRqThreads] = make_int4(F[4], F[5], F[6], F[7]);
-            if (y < ny) rq_store8<OUTK>(out, rb, F, two_eb, nx, OUTK == 0 && !edge && vec_out);
+            if (y < ny) rq_store8<OUTK>(out, rb, F, two_eb, nx, OUTK == 0 && !edge && vec_out, q, acc);
         }
     }
     cp_async_wait1();
@@ -319,8 +374,9 @@ __global__ void __launch_bounds__(kRqThreads) rq3d_block_kernel(const uint16_t* 
                                                          uint8_t* __restrict__ blockflag,
                                                          int any_slow, uint64_t Z, uint64_t Y,
                                                          uint64_t X, uint32_t cap, double two_eb,
-                                                         void* __restrict__ out, DevStatus* st) {
+                                                         void* __restrict__ out, DevStatus* st, QualArgs q) {
     __shared__ int4 s_fp[16 * kRqThreads];
+    QAcc acc;
     __shared__ uint2 s_cs[2 * 16 * kRqThreads];
     const int r = (int)(cap >> 1);
     const uint64_t nbx = ceil_div(X, 8), nby = ceil_div(Y, 8), nbz = ceil_div(Z, 8);
@@ -339,12 +395,13 @@ __global__ void __launch_bounds__(kRqThreads) rq3d_block_kernel(const uint16_t* 
         const bool inside = base + (uint64_t)(nz - 1) * YX + (uint64_t)(ny - 1) * X + 8 <= Z * YX;
         const bool ok = rq3d_block_smem<OUTK>(codes, dense, base, YX, X, nx, ny, nz, r, two_eb, out,
                                               s_fp + threadIdx.x, s_cs + threadIdx.x, vec_ok && inside,
-                                              vec_out);
+                                              vec_out, q, acc);
         if (!ok) {   // magnitude guard: the fp64 replay kernel redoes the block
             blockflag[b] = 1;
             atomicOr(&st->flags, (unsigned long long)F_OUT_SLOW);
         }
     }
+    if (q.orig) qacc_flush(acc, q);
 }
 
 
@@ -393,7 +450,8 @@ __global__ void __launch_bounds__(kThreads) rq2d_kernel(const uint16_t* __restri
 template <typename V, int OUTK>
 __device__ __forceinline__ void rq2d_vec_rows(const uint2 (&cw)[16], const unsigned long long* __restrict__ dense,
                                               uint64_t X, uint64_t y0, int ny, uint64_t x0, bool xin, bool store,
-                                              int r, uint32_t lane, double two_eb, void* __restrict__ out) {
+                                              int r, uint32_t lane, double two_eb, void* __restrict__ out,
+                                              const QualArgs& q, QAcc& acc) {
     V K[4] = {0, 0, 0, 0};
     const uint32_t sl = lane & 3;
     const uint32_t below = ((1u << sl) - 1u) << (lane & ~3u);
@@ -438,9 +496,19 @@ __device__ __forceinline__ void rq2d_vec_rows(const uint2 (&cw)[16], const unsig
                 o4.z = __double2float_rn(__dmul_rn((double)K[2], two_eb));
                 o4.w = __double2float_rn(__dmul_rn((double)K[3], two_eb));
                 __stcs(reinterpret_cast<float4*>((float*)out + i0), o4);
+                if (q.orig) {
+                    acc.add(q, i0, (double)o4.x);
+                    acc.add(q, i0 + 1, (double)o4.y);
+                    acc.add(q, i0 + 2, (double)o4.z);
+                    acc.add(q, i0 + 3, (double)o4.w);
+                }
             } else {
 #pragma unroll
                 for (int k = 0; k < 4; k++) ((double*)out)[i0 + k] = __dmul_rn((double)K[k], two_eb);
+                if (q.orig) {
+#pragma unroll
+                    for (int k = 0; k < 4; k++) acc.add(q, i0 + k, __dmul_rn((double)K[k], two_eb));
+                }
             }
         }
     }
@@ -452,9 +520,10 @@ __global__ void __launch_bounds__(kThreads) rq2d_vec_kernel(const uint16_t* __re
                                                             const uint8_t* __restrict__ blockflag,
                                                             int any_slow, uint64_t Y, uint64_t X,
                                                             uint32_t cap, double two_eb,
-                                                            void* __restrict__ out) {
+                                                            void* __restrict__ out, QualArgs q) {
     const int r = (int)(cap >> 1);
     const uint32_t lane = lane_id();
+    QAcc acc;
     const uint64_t nbx = ceil_div(X, 16), ntx = ceil_div(X, 128), nty = ceil_div(Y, 16);
     const uint64_t ntask = ntx * nty;
     for (uint64_t task = blockIdx.x * (uint64_t)kWarpsPerCta + (threadIdx.x >> 5); task < ntask;
@@ -486,10 +555,11 @@ __global__ void __launch_bounds__(kThreads) rq2d_vec_kernel(const uint16_t* __re
             }
         }
         if (__any_sync(kFull, big))
-            rq2d_vec_rows<long long, OUTK>(cw, dense, X, y0, ny, x0, xin, store, r, lane, two_eb, out);
+            rq2d_vec_rows<long long, OUTK>(cw, dense, X, y0, ny, x0, xin, store, r, lane, two_eb, out, q, acc);
         else
-            rq2d_vec_rows<int, OUTK>(cw, dense, X, y0, ny, x0, xin, store, r, lane, two_eb, out);
+            rq2d_vec_rows<int, OUTK>(cw, dense, X, y0, ny, x0, xin, store, r, lane, two_eb, out, q, acc);
     }
+    if (q.orig) qacc_flush(acc, q);
 }
 
 template <int OUTK>
@@ -530,7 +600,7 @@ __global__ void __launch_bounds__(kThreads) rq1d_kernel(const uint16_t* __restri
 template <typename V, int OUTK>
 __device__ __forceinline__ void rq1d_rec_row(const uint32_t (&c)[4], const V (&vout)[4], uint64_t i0,
                                              uint32_t nvalid, int r, uint32_t lane, double two_eb,
-                                             void* __restrict__ out, bool store) {
+                                             void* __restrict__ out, bool store, const QualArgs& q, QAcc& acc) {
     V fin[4];
     V t = 0;
     bool f = false;
@@ -565,10 +635,23 @@ __device__ __forceinline__ void rq1d_rec_row(const uint32_t (&c)[4], const V (&v
         o4.z = __double2float_rn(__dmul_rn((double)fin[2], two_eb));
         o4.w = __double2float_rn(__dmul_rn((double)fin[3], two_eb));
         __stcs(reinterpret_cast<float4*>((float*)out + i0), o4);
+        if (q.orig) {
+            acc.add(q, i0, (double)o4.x);
+            acc.add(q, i0 + 1, (double)o4.y);
+            acc.add(q, i0 + 2, (double)o4.z);
+            acc.add(q, i0 + 3, (double)o4.w);
+        }
     } else {
 #pragma unroll
-        for (int k = 0; k < 4; k++)
-            if ((uint32_t)k < nvalid) store_out<OUTK>(out, i0 + k, (long long)fin[k], two_eb);
+        for (int k = 0; k < 4; k++) {
+            if ((uint32_t)k < nvalid) {
+                store_out<OUTK>(out, i0 + k, (long long)fin[k], two_eb);
+                if (q.orig) {
+                    const double v = __dmul_rn((double)fin[k], two_eb);
+                    acc.add(q, i0 + k, OUTK == 0 ? (double)__double2float_rn(v) : v);
+                }
+            }
+        }
     }
 }
 
@@ -595,7 +678,7 @@ __device__ __forceinline__ void rq1d_rec_rows(const uint2 (&cw)[8], const double
                                               const unsigned long long* __restrict__ trec, uint32_t m,
                                               uint64_t t0, uint64_t n, const uint8_t* __restrict__ blockflag,
                                               bool any_slow, int r, uint32_t lane, double two_eb,
-                                              void* __restrict__ out) {
+                                              void* __restrict__ out, const QualArgs& qa, QAcc& acc) {
     const uint32_t lt = (1u << lane) - 1u;
     uint32_t base = 0;
 #pragma unroll
@@ -623,7 +706,7 @@ __device__ __forceinline__ void rq1d_rec_rows(const uint2 (&cw)[8], const double
             }
             base += __popc(b0) + __popc(b1) + __popc(b2) + __popc(b3);
         }
-        rq1d_rec_row<V, OUTK>(c, v4, i0, FULL ? 4u : nvalid, r, lane, two_eb, out, store);
+        rq1d_rec_row<V, OUTK>(c, v4, i0, FULL ? 4u : nvalid, r, lane, two_eb, out, store, qa, acc);
     }
 }
 
@@ -639,8 +722,9 @@ __global__ void __launch_bounds__(kThreads) rq1d_rec_kernel(const uint16_t* __re
                                                             const unsigned long long* __restrict__ start,
                                                             uint64_t k, const uint8_t* __restrict__ blockflag,
                                                             uint64_t n, uint32_t cap, double two_eb,
-                                                            void* __restrict__ out, DevStatus* st) {
+                                                            void* __restrict__ out, DevStatus* st, QualArgs qa) {
     __shared__ double s_vals[kWarpsPerCta][kVals];
+    QAcc acc;
     const int r = (int)(cap >> 1);
     const uint32_t lane = lane_id();
     double* const vals = s_vals[threadIdx.x >> 5];
@@ -694,15 +778,16 @@ __global__ void __launch_bounds__(kThreads) rq1d_rec_kernel(const uint16_t* __re
         const bool wide = __any_sync(kFull, big);
         const uint32_t m = (uint32_t)(s1 - s0);   // records of the task (< 2^31: <= 1024 if consistent)
         if (full) {
-            if (wide) rq1d_rec_rows<true, long long, OUTK>(cw, vals, rec + 2 * s0, m, t0, n, blockflag, any_slow, r, lane, two_eb, out);
-            else rq1d_rec_rows<true, int, OUTK>(cw, vals, rec + 2 * s0, m, t0, n, blockflag, any_slow, r, lane, two_eb, out);
+            if (wide) rq1d_rec_rows<true, long long, OUTK>(cw, vals, rec + 2 * s0, m, t0, n, blockflag, any_slow, r, lane, two_eb, out, qa, acc);
+            else rq1d_rec_rows<true, int, OUTK>(cw, vals, rec + 2 * s0, m, t0, n, blockflag, any_slow, r, lane, two_eb, out, qa, acc);
         } else {
-            if (wide) rq1d_rec_rows<false, long long, OUTK>(cw, vals, rec + 2 * s0, m, t0, n, blockflag, any_slow, r, lane, two_eb, out);
-            else rq1d_rec_rows<false, int, OUTK>(cw, vals, rec + 2 * s0, m, t0, n, blockflag, any_slow, r, lane, two_eb, out);
+            if (wide) rq1d_rec_rows<false, long long, OUTK>(cw, vals, rec + 2 * s0, m, t0, n, blockflag, any_slow, r, lane, two_eb, out, qa, acc);
+            else rq1d_rec_rows<false, int, OUTK>(cw, vals, rec + 2 * s0, m, t0, n, blockflag, any_slow, r, lane, two_eb, out, qa, acc);
         }
         __syncwarp();
     }
     if (__any_sync(kFull, nz) && lane == 0) atomicOr(&st->flags, (unsigned long long)F_OUT_NONZERO);
+    if (qa.orig) qacc_flush(acc, qa);
 }
 
 template <typename V, int OUTK>
@@ -945,12 +1030,17 @@ int launch_reconstruct_1d_records(sdqz_ctx* ctx, const uint16_t* codes, const vo
     uint64_t grid = ceil_div(ntask, kWarpsPerCta);
     if (grid > (uint64_t)ctx->num_sms * 8) grid = ctx->num_sms * 8;
     if (grid < 1) grid = 1;
+    QualArgs qa;   // fused quality (sdqz_decompress_quality)
+    if (ctx->qual.orig) {
+        qa = ctx->qual;
+        ctx->qual.nparts = grid;
+    }
     if (out_kind == 0)
         rq1d_rec_kernel<0><<<(unsigned)grid, kThreads, 0, ctx->stream>>>(codes, rec, start, k, blockflag, n, cap,
-                                                                       two_eb, out, ctx->d_status);
+                                                                       two_eb, out, ctx->d_status, qa);
     else
         rq1d_rec_kernel<1><<<(unsigned)grid, kThreads, 0, ctx->stream>>>(codes, rec, start, k, blockflag, n, cap,
-                                                                       two_eb, out, ctx->d_status);
+                                                                       two_eb, out, ctx->d_status, qa);
     SDQZ_LAUNCHED_NAMED(ctx, "rq1d_rec_kernel");
     uint64_t gg = ceil_div(g.nblk[0], 128);
     if (gg > (uint64_t)ctx->num_sms) gg = ctx->num_sms;
@@ -1021,13 +1111,20 @@ int launch_reconstruct(sdqz_ctx* ctx, const uint16_t* codes, const uint64_t* den
         uint64_t vgrid = ceil_div(nt1, kWarpsPerCta);
         if (vgrid > (uint64_t)ctx->num_sms * 8) vgrid = (uint64_t)ctx->num_sms * 8;
         if (vgrid < 1) vgrid = 1;
+        // fused quality: the 3D block and vectorised 2D kernels (any other path
+        // leaves nparts = 0 and the caller scores in a separate pass)
+        QualArgs qa;
+        if (ctx->qual.orig && (ndims == 3 || vec2d)) {
+            qa = ctx->qual;
+            ctx->qual.nparts = ndims == 3 ? bgrid : grid2;
+        }
 #define RQ_LAUNCH(K)                                                                                 \
         if (ndims == 3)                                                                              \
             rq3d_block_kernel<K><<<(unsigned)bgrid, 64, 0, ctx->stream>>>(codes, dn, const_cast<uint8_t*>(blockflag), slow, \
-                                                                        dims[0], dims[1], dims[2], cap, two_eb, out, ctx->d_status); \
+                                                                        dims[0], dims[1], dims[2], cap, two_eb, out, ctx->d_status, qa); \
         else if (vec2d)                                                                              \
             rq2d_vec_kernel<K><<<(unsigned)grid2, kThreads, 0, ctx->stream>>>(codes, dn, blockflag, slow, \
-                                                                             dims[0], dims[1], cap, two_eb, out); \
+                                                                             dims[0], dims[1], cap, two_eb, out, qa); \
         else if (ndims == 2)                                                                         \
             rq2d_kernel<K><<<(unsigned)grid, kThreads, 0, ctx->stream>>>(codes, dn, blockflag, slow,   \
                                                                         dims[0], dims[1], cap, two_eb, out); \

@@ -239,6 +239,27 @@ def decompress_device(src, out=None):
     return o.view(*_dims_of(h))
 
 
+def decompress_quality(src: DeviceArchive, orig, out=None):
+    """decompress_device(src) and the quality sums of the result against
+    `orig` in one pass: the reduction runs in the reconstruct kernels'
+    epilogue (sdqz_decompress_quality).  Returns (field, q5, fused) with q5 =
+    (sum d^2, max |d|, min orig, max orig, nonfinite(orig)) -- metrics.quality's
+    inputs -- and fused False when this path scored in a separate pass."""
+    ctx = src.ctx
+    ctx.sync_stream()
+    h = src.header
+    bw, rec, cb, pay = src.sections()
+    o = _out_tensor(h, out)
+    t, dt = _device.to_device(_device.as_field(orig))
+    if t.numel() != o.numel():
+        raise SdqzError(f"length mismatch: {t.numel()} vs {o.numel()} values")
+    q5 = (ctypes.c_double * 5)()
+    fused = ctypes.c_int(0)
+    ctx.call("sdqz_decompress_quality", ctypes.byref(h), bw, rec, cb, pay, _lib.ptr(o), _lib.ptr(t),
+             0 if dt == np.float32 else 1, q5, ctypes.byref(fused))
+    return o.view(*_dims_of(h)), tuple(q5), bool(fused.value)
+
+
 def _check_geometry(h):
     block = tuple(int(h.block[a]) for a in range(h.ndims))
     QuantConfig(eb=h.eb_resolved, cap=h.cap, block_shape=block)
@@ -299,7 +320,7 @@ def decompress_archive(ar: Archive, workers: int | None = None) -> np.ndarray:
 
 
 __all__ = ["compress", "decompress", "decompress_archive", "compress_device",
-           "decompress_device", "compress_host", "decompress_host", "DeviceArchive",
+           "decompress_device", "compress_host", "decompress_host", "decompress_quality", "DeviceArchive",
            "DEFAULT_BLOCK_SHAPES"]
 
 

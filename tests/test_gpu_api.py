@@ -107,3 +107,30 @@ def test_host_buffer_path_errors():
     blob = bytearray(S.compress(S.generate_field("smooth", (32, 32), seed=1).astype(np.float32), eb=1e-3))
     with pytest.raises(S.ArchiveFormatError):
         pipeline.decompress_host(bytes(blob[:60]))
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("shape,kw,want_fused", [
+    ((40, 56, 24), dict(eb=1e-4, mode="valrel"), True),                 # 3D block kernel
+    ((300, 256), dict(eb=1e-3, mode="valrel"), True),                   # vectorised 2D
+    ((100003,), dict(eb=1e-4, mode="valrel"), True),                    # 1D records kernel
+    ((30, 33, 20), dict(eb=0.02, block_shape=(4, 3, 2)), False),        # generic shape: separate pass
+])
+def test_fused_quality_matches_separate(shape, kw, want_fused):
+    """sdqz_decompress_quality: the same field as decompress_device and the
+    same scores as quality() (sum of squares up to summation order)."""
+    from paper_2007_09625_b200 import metrics, pipeline
+    f = S.generate_field("smooth", shape, seed=5).astype(np.float32)
+    t = torch.from_numpy(f).cuda()
+    dev = S.compress_device(t, **kw)
+    ref = S.decompress_device(dev).clone()
+    out, q5, fused = pipeline.decompress_quality(dev, t)
+    assert fused == want_fused
+    assert torch.equal(out.view(torch.int32), ref.view(torch.int32))
+    q = metrics.quality(t, ref)
+    qf = metrics._report(q5, f.size)
+    assert qf.max_abs_error == q.max_abs_error and qf.value_range == q.value_range
+    assert qf.rmse == pytest.approx(q.rmse, rel=1e-12)
+    rows = S.rd_sweep(f, S.describe_field(f, shape), [S.ErrorBoundSpec(kw.get("mode", "abs"), kw["eb"])],
+                      **({"chunk_size": None} if "block_shape" not in kw else {}))
+    assert rows[0].error is None or "block" in rows[0].error
