@@ -180,6 +180,13 @@ SDQZ_API int sdqz_inflate(sdqz_ctx* ctx, const uint8_t* d_payload, uint64_t payl
 SDQZ_API int sdqz_compress(sdqz_ctx* ctx, const void* d_in, int dtype, int ndims, const uint64_t dims[3],
                   const uint32_t block[3], int eb_mode, double eb, uint32_t cap, uint32_t chunk,
                   sdqz_header* hdr);
+/* sdqz_compress with the field's K1 result supplied: stats = {vmin, vmax,
+ * nonfinite} as returned by sdqz_describe of the same (unchanged) field; the
+ * describe pass is skipped.  rd_sweep reuses one describe across its bounds
+ * (metrics.py:89-118). */
+SDQZ_API int sdqz_compress_described(sdqz_ctx* ctx, const void* d_in, int dtype, int ndims,
+                                     const uint64_t dims[3], const uint32_t block[3], int eb_mode, double eb,
+                                     uint32_t cap, uint32_t chunk, const double stats[3], sdqz_header* hdr);
 /* Total archive bytes of the last compress. */
 SDQZ_API uint64_t sdqz_archive_size(const sdqz_ctx* ctx);
 /* Id of the last compress's archive (unique per process; 0 = none, e.g. after

@@ -91,6 +91,9 @@ _SIGS = {
     "sdqz_compress": (c_int, [c_void_p, c_void_p, c_int, c_int, POINTER(c_uint64),
                               POINTER(c_uint32), c_int, c_double, c_uint32, c_uint32,
                               POINTER(Header)]),
+    "sdqz_compress_described": (c_int, [c_void_p, c_void_p, c_int, c_int, POINTER(c_uint64),
+                                        POINTER(c_uint32), c_int, c_double, c_uint32, c_uint32,
+                                        POINTER(c_double), POINTER(Header)]),
     "sdqz_archive_size": (c_uint64, [c_void_p]),
     "sdqz_archive_generation": (c_uint64, [c_void_p]),
     "sdqz_archive_write": (c_int, [c_void_p, c_uint64, c_void_p, c_uint64]),

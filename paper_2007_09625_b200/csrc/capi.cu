@@ -85,6 +85,26 @@ void ensure_smem(const sdqz_ctx* ctx, const void* func, size_t bytes) {
 
 namespace {
 
+// host copies of the ordered-int encodings describe_kernel uses (common.cuh)
+unsigned long long host_f2ord(float f) {
+    uint32_t u;
+    memcpy(&u, &f, 4);
+    return (u & 0x80000000u) ? ~u : (u | 0x80000000u);
+}
+unsigned long long host_d2ord(double d) {
+    unsigned long long u;
+    memcpy(&u, &d, 8);
+    return (u & 0x8000000000000000ull) ? ~u : (u | 0x8000000000000000ull);
+}
+
+// the K1 result of an earlier describe of the same field (sweeps reuse it)
+__global__ void set_described_kernel(DevStatus* st, unsigned long long vmin_bits, unsigned long long vmax_bits,
+                                     int nonfinite) {
+    st->vmin_bits = vmin_bits;
+    st->vmax_bits = vmax_bits;
+    if (nonfinite) st->flags |= F_NONFINITE;
+}
+
 __global__ void init_status_kernel(DevStatus* st, double eb, int has_eb) {
     memset(st, 0, sizeof(DevStatus));
     st->decode_key = ~0ull;
@@ -469,6 +489,11 @@ struct CompressState {
     uint8_t* payload;
     unsigned long long* rec;
     DeflateJob job;
+    // K1 result supplied by the caller (sdqz_compress_described): ordered
+    // encodings as describe_kernel leaves them in the status block
+    bool pre = false;
+    unsigned long long pre_min = 0, pre_max = 0;
+    int pre_nonfinite = 0;
 };
 
 // ---------------------------------------------------------------------------
@@ -508,7 +533,10 @@ int compress_prepare(sdqz_ctx* ctx, CompressState& c) {
 int compress_enqueue(sdqz_ctx* ctx, const CompressState& c) {
     int rc;
     if ((rc = reset_status(ctx))) return rc;
-    if (c.eb_mode == 1 || !(c.eb > 0 && std::isfinite(c.eb))) {
+    if (c.pre) {
+        set_described_kernel<<<1, 1, 0, ctx->stream>>>(ctx->d_status, c.pre_min, c.pre_max, c.pre_nonfinite);
+        SDQZ_LAUNCHED_NAMED(ctx, "set_described_kernel");
+    } else if (c.eb_mode == 1 || !(c.eb > 0 && std::isfinite(c.eb))) {
         if ((rc = launch_describe(ctx, c.d_in, c.dtype, c.n))) return rc;
     }
     if ((rc = launch_resolve(ctx, c.dtype, c.eb_mode, c.eb))) return rc;
@@ -594,6 +622,10 @@ std::string compress_key(const CompressState& c) {
     key_put(k, c.cap);
     key_put(k, c.cs);
     key_put(k, c.pay_cap);
+    key_put(k, c.pre);
+    key_put(k, c.pre_min);
+    key_put(k, c.pre_max);
+    key_put(k, c.pre_nonfinite);
     key_put(k, c.rec_cap);
     return k;
 }
@@ -1078,9 +1110,9 @@ int sdqz_inflate(sdqz_ctx* ctx, const uint8_t* d_payload, uint64_t payload_bytes
 // ---------------------------------------------------------------------------
 // fused pipeline
 // ---------------------------------------------------------------------------
-int sdqz_compress(sdqz_ctx* ctx, const void* d_in, int dtype, int ndims, const uint64_t dims[3],
-                  const uint32_t block[3], int eb_mode, double eb, uint32_t cap, uint32_t chunk,
-                  sdqz_header* hdr) {
+static int compress_impl(sdqz_ctx* ctx, const void* d_in, int dtype, int ndims, const uint64_t dims[3],
+                         const uint32_t block[3], int eb_mode, double eb, uint32_t cap, uint32_t chunk,
+                         const double* pre_stats, sdqz_header* hdr) {
     int rc = SDQZ_OK;
     ctx->have_archive = false;
     if (ndims < 1 || ndims > 3) return set_error(ctx, SDQZ_EINVAL, "rank must be 1-3");
@@ -1098,6 +1130,17 @@ int sdqz_compress(sdqz_ctx* ctx, const void* d_in, int dtype, int ndims, const u
     cst.n = n;
     cst.cs = chunk ? chunk : default_chunk_size(n);
     cst.C = ceil_div(n, cst.cs);
+    if (pre_stats) {   // {vmin, vmax, nonfinite} from an earlier sdqz_describe of this field
+        cst.pre = true;
+        if (dtype == 0) {
+            cst.pre_min = host_f2ord((float)pre_stats[0]);
+            cst.pre_max = host_f2ord((float)pre_stats[1]);
+        } else {
+            cst.pre_min = host_d2ord(pre_stats[0]);
+            cst.pre_max = host_d2ord(pre_stats[1]);
+        }
+        cst.pre_nonfinite = pre_stats[2] != 0.0;
+    }
     if ((rc = compress_prepare(ctx, cst))) return rc;
     // Graph replay: a call identical to the previous one (same pointers and
     // parameters, unchanged scratch arena) re-launches the captured pipeline
@@ -1116,6 +1159,19 @@ int sdqz_compress(sdqz_ctx* ctx, const void* d_in, int dtype, int ndims, const u
     if (graphs && ctx->last_comp_key == key && ctx->gen == gen0) capture_compress(ctx, cst, key);
     ctx->last_comp_key = key;
     return SDQZ_OK;
+}
+
+int sdqz_compress(sdqz_ctx* ctx, const void* d_in, int dtype, int ndims, const uint64_t dims[3],
+                  const uint32_t block[3], int eb_mode, double eb, uint32_t cap, uint32_t chunk,
+                  sdqz_header* hdr) {
+    return compress_impl(ctx, d_in, dtype, ndims, dims, block, eb_mode, eb, cap, chunk, nullptr, hdr);
+}
+
+int sdqz_compress_described(sdqz_ctx* ctx, const void* d_in, int dtype, int ndims, const uint64_t dims[3],
+                            const uint32_t block[3], int eb_mode, double eb, uint32_t cap, uint32_t chunk,
+                            const double stats[3], sdqz_header* hdr) {
+    if (!stats) return set_error(ctx, SDQZ_EINVAL, "invalid arguments");
+    return compress_impl(ctx, d_in, dtype, ndims, dims, block, eb_mode, eb, cap, chunk, stats, hdr);
 }
 
 

@@ -116,9 +116,11 @@ def _raise_resolve_errors(t, dt, mode, eb):
 
 
 def compress_device(data, dims=None, *, eb: float, mode: str = "abs", cap: int = 1024,
-                    block_shape=None, chunk_size: int | None = None) -> DeviceArchive:
+                    block_shape=None, chunk_size: int | None = None, stats=None) -> DeviceArchive:
     """compress() whose input may be a CUDA tensor and whose output stays on
-    the device (sections in the calling thread's context)."""
+    the device (sections in the calling thread's context).  `stats` =
+    (vmin, vmax, nonfinite) of an earlier describe of the same unchanged
+    field skips the describe pass (sdqz_compress_described; rd_sweep)."""
     arr = _device.as_field(data)
     dims, block, pending = _check_request(arr, dims, eb, mode, cap, block_shape, chunk_size)
     t, dt = _device.to_device(arr)
@@ -127,9 +129,14 @@ def compress_device(data, dims=None, *, eb: float, mode: str = "abs", cap: int =
         raise pending
     ctx = _lib.context()
     hdr = _lib.Header()
-    ctx.call("sdqz_compress", _lib.ptr(t), 0 if dt == np.float32 else 1, len(dims),
-             _lib.dims3(dims), _lib.block3(block), 0 if mode == "abs" else 1, float(eb),
-             int(cap), int(chunk_size or 0), ctypes.byref(hdr))
+    args = (_lib.ptr(t), 0 if dt == np.float32 else 1, len(dims), _lib.dims3(dims), _lib.block3(block),
+            0 if mode == "abs" else 1, float(eb), int(cap), int(chunk_size or 0))
+    if stats is None:
+        ctx.call("sdqz_compress", *args, ctypes.byref(hdr))
+    else:
+        ctx.call("sdqz_compress_described", *args,
+                 (ctypes.c_double * 3)(float(stats[0]), float(stats[1]), 1.0 if stats[2] else 0.0),
+                 ctypes.byref(hdr))
     return DeviceArchive(hdr, ctx, ctx.archive_generation)
 
 

@@ -134,3 +134,24 @@ def test_fused_quality_matches_separate(shape, kw, want_fused):
     rows = S.rd_sweep(f, S.describe_field(f, shape), [S.ErrorBoundSpec(kw.get("mode", "abs"), kw["eb"])],
                       **({"chunk_size": None} if "block_shape" not in kw else {}))
     assert rows[0].error is None or "block" in rows[0].error
+
+
+@pytest.mark.gpu
+def test_compress_described_matches():
+    """sdqz_compress_described (rd_sweep's K1 reuse) gives the same archives,
+    and the same errors, as sdqz_compress."""
+    from paper_2007_09625_b200 import _device
+    f = S.generate_field("smooth", (33, 40, 48), seed=6).astype(np.float32)
+    t = torch.from_numpy(f).cuda().reshape(-1)
+    stats = _device.describe(t, np.dtype(np.float32))
+    for eb in (1e-2, 1e-3, 1e-4, 1e-5):
+        want = S.compress(f, eb=eb, mode="valrel")
+        assert S.compress_device(t, f.shape, eb=eb, mode="valrel", stats=stats).to_bytes() == want
+    bad = f.copy()
+    bad[3, 4, 5] = np.inf
+    tb = torch.from_numpy(bad).cuda().reshape(-1)
+    with pytest.raises(S.SdqzError, match="NaN/Inf"):
+        S.compress_device(tb, bad.shape, eb=1e-3, mode="valrel", stats=_device.describe(tb, np.dtype(np.float32)))
+    rows = S.rd_sweep(f, S.describe_field(f, f.shape), [S.ErrorBoundSpec("valrel", e) for e in (1e-2, 1e-4)])
+    assert [r.n_outliers for r in rows] == [S.parse_header(S.compress(f, eb=e, mode="valrel")).n_outliers
+                                           for e in (1e-2, 1e-4)]
