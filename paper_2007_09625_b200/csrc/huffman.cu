@@ -1061,6 +1061,241 @@ __global__ void __launch_bounds__(256, 3) chunk_pack32_kernel(DeflateArgs a) {
     }
 }
 
+// --------------------------------------------------------------------------
+// pack for long chunks (>= 32768 codes; 32-bit units): warp per chunk, rounds of
+// 32 x Q x R codes.  Lane l owns Q consecutive sub-runs of R codes and shifts
+// each sub-run's codewords into a 64-bit register (entry {width, codeword}:
+// two funnel shifts, an OR and an add per code; no per-code shared traffic).
+// One warp scan of the lane widths places every sub-run in the round's bit
+// stream; a sub-run's left-aligned bits go to the <= 3 words of a per-warp
+// shared buffer it touches: words whose first bit it holds by plain stores,
+// then (after a warp sync) the word it starts inside of by one shared OR --
+// every word has exactly one first-bit owner, so no zero fill is needed.
+// Completed words go to global memory coalesced; the trailing partial word
+// carries into the next round.  R is picked per chunk from its mean code
+// length so a sub-run rarely exceeds 64 bits; one that does zeroes the words
+// it owns and ORs its codewords in one by one.
+// --------------------------------------------------------------------------
+constexpr int kLaneCodes = 32;                             // Q x R codes per lane and round
+constexpr int kPackBufWords = 32 * kLaneCodes * 24 / 32 + 4;   // 32-bit units: <= 24 bits per code
+
+__device__ __forceinline__ uint32_t min_u16x2(uint32_t a, uint32_t b) {
+    uint32_t d;
+    asm("min.u16x2 %0, %1, %2;" : "=r"(d) : "r"(a), "r"(b));
+    return d;
+}
+
+__device__ __forceinline__ void red_or(uint32_t addr, uint32_t v) {
+    asm volatile("red.shared.or.b32 [%0], %1;" ::"r"(addr), "r"(v) : "memory");
+}
+__device__ __forceinline__ void sts32(uint32_t addr, uint32_t v) {
+    asm volatile("st.shared.u32 [%0], %1;" ::"r"(addr), "r"(v) : "memory");
+}
+
+__device__ __forceinline__ uint32_t code_at(const uint32_t* wv, int k) {
+    return (k & 1) ? (wv[k >> 1] >> 16) : (wv[k >> 1] & 0xFFFFu);
+}
+
+template <int R, int Q, bool TS>
+__device__ __forceinline__ void pack32_chunk(const DeflateArgs& a, const uint2* s_tab, uint32_t* buf, uint64_t s,
+                                             uint64_t e, uint64_t B, uint64_t Bend, uint64_t orec,
+                                             double two_eb, uint32_t lane) {
+    constexpr uint32_t LC = Q * R;       // codes per lane and round
+    constexpr uint32_t RC = 32 * LC;     // codes per round
+    static_assert(LC % 8 == 0 && LC <= kLaneCodes, "lane codes: whole 16-byte loads");
+    const uint16_t* src = (const uint16_t*)a.src;
+    auto lookup = [&](uint32_t code) -> uint2 {
+        if (TS) return s_tab[code];
+        const unsigned long long u = __ldg(a.gtable + code);
+        return make_uint2((uint32_t)(u >> 24), (uint32_t)(u & 0xFFFFFFull));
+    };
+    const uint32_t bufs = smem_u32(buf);
+    uint64_t wbyte = B & ~3ull;
+    uint32_t carry = (uint32_t)(B & 3) * 8, carry_word = 0;
+    bool first_round = true;
+    // a lane's codes of the next round are in flight while this round packs
+    // (16-byte loads when its run is whole and aligned)
+    auto fetch = [&](uint64_t g, uint32_t (&wv)[LC / 2]) -> bool {
+        const uint64_t i0 = g + (uint64_t)LC * lane;
+        if (i0 + LC > e || (i0 & 7)) return false;
+        const uint4* p = reinterpret_cast<const uint4*>(src + i0);
+#pragma unroll
+        for (int u = 0; u < (int)LC / 8; u++) {
+            const uint4 v = __ldg(p + u);
+            wv[4 * u] = v.x; wv[4 * u + 1] = v.y; wv[4 * u + 2] = v.z; wv[4 * u + 3] = v.w;
+        }
+        return true;
+    };
+    uint32_t nw[LC / 2];
+#pragma unroll
+    for (int k = 0; k < (int)LC / 2; k++) nw[k] = 0x00010001u;
+    bool nvalid = fetch(s, nw);
+    for (uint64_t g = s; g < e; g += RC) {
+        const uint64_t i0 = g + (uint64_t)LC * lane;
+        const uint32_t cnt = i0 < e ? (uint32_t)umin(LC, e - i0) : 0u;
+        uint32_t wv[LC / 2];
+#pragma unroll
+        for (int k = 0; k < (int)LC / 2; k++) wv[k] = nw[k];
+        const bool valid = nvalid;
+        nvalid = g + RC < e && fetch(g + RC, nw);
+        if (!valid) {   // ragged / unaligned run: scalar loads, past-the-end codes read as 1
+#pragma unroll
+            for (int k = 0; k < (int)LC; k += 2) {
+                const uint32_t c0 = (uint32_t)k < cnt ? src[i0 + k] : 1u;
+                const uint32_t c1 = (uint32_t)k + 1 < cnt ? src[i0 + k + 1] : 1u;
+                wv[k >> 1] = c0 | (c1 << 16);
+            }
+        }
+        // sub-runs in 64-bit registers, right-aligned, nb[q] bits (exact even past 64)
+        uint32_t hi[Q] = {}, lo[Q] = {}, nb[Q] = {}, nbt = 0;
+        auto append = [&](int q, uint2 t) {
+            hi[q] = __funnelshift_l(lo[q], hi[q], t.x);
+            lo[q] = __funnelshift_l(0u, lo[q], t.x) | t.y;
+            nb[q] += t.x;
+        };
+        if (cnt == LC) {
+#pragma unroll
+            for (int k = 0; k < (int)LC; k++) append(k / R, lookup(code_at(wv, k)));
+        } else {
+#pragma unroll
+            for (int k = 0; k < (int)LC; k++)
+                append(k / R, ((uint32_t)k < cnt) ? lookup(code_at(wv, k)) : make_uint2(0u, 0u));
+        }
+#pragma unroll
+        for (int q = 0; q < Q; q++) nbt += nb[q];
+        int total_l;
+        const uint32_t off = (uint32_t)warp_excl_scan((int)nbt, &total_l) + carry;
+        const uint32_t total = carry + (uint32_t)total_l;
+        // phase A: the words whose first bit a sub-run holds (the carry owns word 0's)
+        if (lane == 0 && carry) sts32(bufs, carry_word);
+        uint32_t Lh[Q], Ll[Q];
+        {
+            uint32_t o = off;
+#pragma unroll
+            for (int q = 0; q < Q; q++) {
+                const uint32_t sh = o & 31u, a0 = bufs + ((o >> 5) << 2), end = o + nb[q];
+                const uint32_t nxt = (o | 31u) + 1;   // first bit of the next word
+                if (nb[q] <= 64) {
+                    const uint32_t sl = 64 - nb[q];   // left-align
+                    Lh[q] = sl >= 32 ? lo[q] << (sl - 32) : __funnelshift_l(lo[q], hi[q], sl);
+                    Ll[q] = sl >= 32 ? 0u : lo[q] << sl;
+                    if (sh == 0 && nb[q]) sts32(a0, Lh[q]);
+                    if (nxt < end) sts32(a0 + 4, __funnelshift_r(Ll[q], Lh[q], sh));
+                    if (nxt + 32 < end) sts32(a0 + 8, __funnelshift_r(0u, Ll[q], sh));
+                } else {   // longer than 64 bits: zero the owned words, OR codewords in below
+                    for (uint32_t j = (o + 31) >> 5; 32 * j < end; j++) sts32(bufs + 4 * j, 0u);
+                }
+                o = end;
+            }
+        }
+        __syncwarp();
+        // phase B: the word each sub-run starts inside of
+        {
+            uint32_t o = off;
+#pragma unroll
+            for (int q = 0; q < Q; q++) {
+                const uint32_t sh = o & 31u, a0 = bufs + ((o >> 5) << 2);
+                if (nb[q] <= 64) {
+                    if (sh && nb[q]) red_or(a0, Lh[q] >> sh);
+                } else {
+                    uint32_t p = o;
+#pragma unroll
+                    for (int k = q * R; k < (q + 1) * R; k++) {
+                        const uint2 t = ((uint32_t)k < cnt) ? lookup(code_at(wv, k)) : make_uint2(0u, 0u);
+                        if (t.x) {
+                            const uint32_t al = t.y << (32 - t.x);
+                            const uint32_t ps = p & 31u, pa = bufs + ((p >> 5) << 2);
+                            red_or(pa, al >> ps);
+                            if (ps + t.x > 32) red_or(pa + 4, __funnelshift_r(0u, al, ps));
+                            p += t.x;
+                        }
+                    }
+                }
+                o += nb[q];
+            }
+        }
+        __syncwarp();
+        const uint32_t full = total >> 5;
+        for (uint32_t j = lane; j < full; j += 32) {
+            const uint32_t w = buf[j];
+            if (j == 0 && first_round) store_word(a.payload, wbyte, w, B, Bend);   // may start before B
+            else *reinterpret_cast<uint32_t*>(a.payload + wbyte + 4ull * j) = bswap32(w);
+        }
+        carry_word = (total & 31) ? buf[full] : 0u;
+        __syncwarp();
+        wbyte += 4ull * full;
+        carry = total & 31;
+        first_round = first_round && full == 0;
+        // outliers (code 0) in row-major order
+        if (a.records) {
+            uint32_t m = wv[0];
+#pragma unroll
+            for (int k = 1; k < (int)LC / 2; k++) m = min_u16x2(m, wv[k]);
+            const bool anyz = cnt != 0 && zero_half(m);
+            if (__any_sync(kFull, anyz)) {
+                uint32_t zc = 0;
+#pragma unroll
+                for (int k = 0; k < (int)LC; k++) zc += ((uint32_t)k < cnt) & (code_at(wv, k) == 0);
+                int ztot;
+                const uint32_t zoff = (uint32_t)warp_excl_scan((int)zc, &ztot);
+                uint64_t slot = orec + zoff;
+#pragma unroll
+                for (int k = 0; k < (int)LC; k++) {
+                    if ((uint32_t)k < cnt && code_at(wv, k) == 0) {
+                        const uint64_t i = i0 + k;
+                        if (i < a.rec_limit) {
+                            const double v = outlier_value(a, i, two_eb);
+                            a.records[2 * slot] = i + a.idx_base;
+                            a.records[2 * slot + 1] = (unsigned long long)__double_as_longlong(v);
+                        }
+                        slot++;
+                    }
+                }
+                orec += (uint64_t)ztot;
+            }
+        }
+    }
+    if (carry && lane == 0) store_word(a.payload, wbyte, carry_word, B, Bend);
+    __syncwarp();
+}
+
+constexpr size_t kPack32Smem = 4096 * sizeof(uint2) + 8 * kPackBufWords * 4;
+
+template <bool TS>
+__global__ void __launch_bounds__(256, 2) chunk_pack32_runs_kernel(DeflateArgs a) {
+    extern __shared__ __align__(16) unsigned char pack_smem[];
+    uint2* s_tab = reinterpret_cast<uint2*>(pack_smem);
+    uint32_t* s_buf = reinterpret_cast<uint32_t*>(pack_smem + (TS ? 4096 * sizeof(uint2) : 0));
+    if (a.st->flags & (F_CODE_RANGE | F_ABSENT_SYM | F_ZERO_WIDTH | F_OVERFLOW | F_BW_TOO_BIG |
+                       F_KRAFT | F_NO_PRESENT | F_ALL_ZERO_HIST))
+        return;
+    if (unit_of(a) != 32) return;   // 64-bit units: chunk_pack_run_kernel
+    if (TS)
+        for (uint32_t i = threadIdx.x; i < a.cap; i += blockDim.x) {
+            const unsigned long long u = a.gtable[i];
+            s_tab[i] = make_uint2((uint32_t)(u >> 24), (uint32_t)(u & 0xFFFFFFull));
+        }
+    __syncthreads();
+    const double two_eb = a.st->two_eb;
+    const uint32_t lane = lane_id(), wid = threadIdx.x >> 5;
+    uint32_t* buf = s_buf + wid * kPackBufWords;
+    for (uint64_t c = blockIdx.x * 8ull + wid; c < a.nchunks; c += gridDim.x * 8ull) {
+        const uint64_t s = c * a.chunk, e = umin(s + a.chunk, a.n);
+        const uint32_t bits = a.chunk_bits[c];
+        const uint64_t B = a.byte_off[c];
+        const uint64_t Bend = B + ((bits + 7) >> 3);
+        const uint64_t orec = a.out_off ? a.out_off[c] : 0;
+        // sub-runs of ~44 bits at the chunk's mean code length
+        const uint64_t len = e - s;
+        if (16ull * bits <= 44ull * len)
+            pack32_chunk<16, 2, TS>(a, s_tab, buf, s, e, B, Bend, orec, two_eb, lane);
+        else if (8ull * bits <= 44ull * len)
+            pack32_chunk<8, 4, TS>(a, s_tab, buf, s, e, B, Bend, orec, two_eb, lane);
+        else
+            pack32_chunk<4, 4, TS>(a, s_tab, buf, s, e, B, Bend, orec, two_eb, lane);
+    }
+}
+
 template <bool TS>
 __global__ void __launch_bounds__(256) chunk_pack_run_kernel(DeflateArgs a, int want_payload) {
     extern __shared__ unsigned long long stable[];
@@ -1424,8 +1659,16 @@ int run_deflate(sdqz_ctx* ctx, DeflateArgs& a, bool payload) {
         // 28.8 KB static + up to 32 KB table > the 48 KB default
         ensure_smem(ctx, (const void*)chunk_pack_run_kernel<true>, 4096 * 8);
         if (payload && a.gtable) {   // 32-bit units (device-decided; no-op otherwise)
-            if (ts) chunk_pack32_kernel<true><<<(unsigned)grid, 256, 0, ctx->stream>>>(a);
-            else chunk_pack32_kernel<false><<<(unsigned)grid, 256, 0, ctx->stream>>>(a);
+            if (a.chunk >= 32768) {   // long chunks: register runs (amortise the per-round warp work)
+                ensure_smem(ctx, (const void*)chunk_pack32_runs_kernel<true>, kPack32Smem);
+                ensure_smem(ctx, (const void*)chunk_pack32_runs_kernel<false>, 8 * kPackBufWords * 4);
+                if (ts) chunk_pack32_runs_kernel<true><<<(unsigned)grid, 256, kPack32Smem, ctx->stream>>>(a);
+                else chunk_pack32_runs_kernel<false><<<(unsigned)grid, 256, 8 * kPackBufWords * 4, ctx->stream>>>(a);
+            } else if (ts) {
+                chunk_pack32_kernel<true><<<(unsigned)grid, 256, 0, ctx->stream>>>(a);
+            } else {
+                chunk_pack32_kernel<false><<<(unsigned)grid, 256, 0, ctx->stream>>>(a);
+            }
             SDQZ_LAUNCHED_NAMED(ctx, "chunk_pack32_kernel");
         }
         // 64-bit units (or no payload): device-decided, usually an idle launch;
@@ -1587,11 +1830,12 @@ int launch_inflate(sdqz_ctx* ctx, const uint8_t* payload, uint64_t payload_bytes
     // one launch: decode tables (+ the fallback LUT) | chunk byte offsets + clears
     (void)cap;
     uint32_t* tab = nullptr;
+    const int ns = decode_ns(payload_bytes, n);
     if ((rc = launch_decode_prep(ctx, first, offsets, symbols, max_bw, &tab, const_cast<uint32_t*>(lut),
-                                 chunk_bits, n_chunks, a.byte_off, redo)))
+                                 chunk_bits, n_chunks, a.byte_off, redo, ns)))
         return rc;
     if ((rc = launch_inflate_fast(ctx, payload, nwords, chunk_bits, a.byte_off, n_chunks, chunk, n,
-                                  first, offsets, symbols, tab, max_bw, (uint16_t*)codes, redo)))
+                                  first, offsets, symbols, tab, max_bw, (uint16_t*)codes, redo, ns)))
         return rc;
     inflate_kernel<false><<<(unsigned)grid, 64, 0, ctx->stream>>>(
         payload, nwords, chunk_bits, a.byte_off, n_chunks, chunk, n, first, offsets, symbols, lut,

@@ -46,11 +46,18 @@ namespace {
 constexpr int kL1 = 12;                    // table index bits
 constexpr uint32_t kL1Size = 1u << kL1;
 constexpr uint32_t kL2Max = 4096;          // second-level entries (long codes)
-// layout of the table block (u32 words): T (u64[4096]) | L2 (u32[4096])
-constexpr uint32_t kOffL2 = 2 * kL1Size;
-constexpr uint32_t kTabWords = kOffL2 + kL2Max;
+// layout of the table block (u32 words): T | L2 (u32[4096]); T holds u64
+// entries of up to three codewords (NS = 3) or u128 entries of up to six
+// (NS = 6, for streams of short codes: fewer table steps per codeword)
+template <int NS>
+struct Fmt {
+    static constexpr uint32_t kEntryWords = NS == 6 ? 4 : 2;
+    static constexpr uint32_t kOffL2 = kEntryWords * kL1Size;
+    static constexpr uint32_t kTabWords = kOffL2 + kL2Max;
+};
+constexpr uint32_t kTabWordsMax = Fmt<6>::kTabWords;
 
-// T entry (u64), len = bits 60-63:
+// T entry (NS = 3, u64), len = bits 60-63:
 //   len != 0: the greedy decode of the window, up to three codewords:
 //             sym0 (0-15) | sym1 (16-31) | sym2 (32-47) | some sym == 0 (48)
 //             | codeword starts at offsets 1..11 (49-59; offset 0 implicit)
@@ -58,6 +65,10 @@ constexpr uint32_t kTabWords = kOffL2 + kL2Max;
 //   len == 0: the first codeword is longer than 12 bits: second-level base
 //             (0-15) | extra bits k (16-20) | second level present (21) | no
 //             codeword has this prefix (22); neither flag: canonical search
+// T entry (NS = 6, u128): words 0-2 = sym0|sym1<<16, sym2|sym3<<16,
+//   sym4|sym5<<16; word 3 = meta: len (28-31); len != 0: some sym == 0 (0)
+//   | codeword starts at offsets 1..11 (1-11); len == 0: the long-codeword
+//   fields of the u64 entry's low word
 // L2 entry:  sym << 16 | len
 constexpr uint32_t kLongL2 = 1u << 21;
 constexpr uint32_t kLongNone = 1u << 22;
@@ -82,7 +93,7 @@ __device__ __forceinline__ void dtab_body(const uint64_t* __restrict__ first,
                                           const int64_t* __restrict__ offsets,
                                           const uint32_t* __restrict__ symbols, int max_bw_arg,
                                           const DevStatus* st, uint32_t* __restrict__ tab,
-                                          uint32_t* __restrict__ old_lut, int part) {
+                                          uint32_t* __restrict__ old_lut, int part, int ns) {
     constexpr int kTParts = 4;
     // p0: T windows [w0, w1); pl2: second-level table; plut: fallback LUT
     const bool p0 = part < kTParts, pl2 = part < 0 || part == kTParts, plut = part < 0 || part == kTParts + 1;
@@ -94,6 +105,7 @@ __device__ __forceinline__ void dtab_body(const uint64_t* __restrict__ first,
     __shared__ unsigned long long s_first[34];
     __shared__ long long s_off[35];
     const int mx = max_bw_arg > 0 ? max_bw_arg : (int)st->max_bw;
+    const uint32_t offl2 = ns == 6 ? Fmt<6>::kOffL2 : Fmt<3>::kOffL2;
     if (mx < 1 || mx > kMaxBw) return;
     if (mx > 32) {   // 64-bit codes: only the sequential decoder's table (lut_kernel's rule)
         if (!old_lut || !plut) return;
@@ -128,7 +140,7 @@ __device__ __forceinline__ void dtab_body(const uint64_t* __restrict__ first,
     for (int b = threadIdx.x; b < 35; b += blockDim.x) s_off[b] = b <= mx + 1 ? offsets[b] : offsets[mx + 1];
     for (uint32_t i = threadIdx.x; i < kL1Size; i += blockDim.x) pmax[i] = 0;
     if (pl2)
-        for (uint32_t i = threadIdx.x; i < kL2Max; i += blockDim.x) tab[kOffL2 + i] = kSymInvalid;
+        for (uint32_t i = threadIdx.x; i < kL2Max; i += blockDim.x) tab[offl2 + i] = kSymInvalid;
     __syncthreads();
     const long long nsym = s_off[mx + 1];
     // longest code under each 12-bit prefix
@@ -216,10 +228,10 @@ __device__ __forceinline__ void dtab_body(const uint64_t* __restrict__ first,
         }
     }
     __syncthreads();
-    // T: greedy decode of each 12-bit window (<= 3 codewords), one lookup per codeword
+    // T: greedy decode of each 12-bit window (<= ns codewords), one lookup per codeword
     for (uint32_t i = w0 + threadIdx.x; p0 && i < w1; i += blockDim.x) {
-        uint32_t o = 0, m = 0, starts = 0, zero = 0, sym[3] = {0, 0, 0};
-        while (o < (uint32_t)kL1 && m < 3) {
+        uint32_t o = 0, m = 0, starts = 0, zero = 0, sym[6] = {0, 0, 0, 0, 0, 0};
+        while (o < (uint32_t)kL1 && m < (uint32_t)ns) {
             const uint32_t one = s_one[swz12((i << o) & (kL1Size - 1))];
             const uint32_t b = one & 63u;
             if (!b || b > kL1 - o) break;
@@ -229,18 +241,24 @@ __device__ __forceinline__ void dtab_body(const uint64_t* __restrict__ first,
             m++;
             o += b;
         }
-        unsigned long long e;
-        if (m) {
-            e = (unsigned long long)sym[0] | ((unsigned long long)sym[1] << 16) |
-                ((unsigned long long)sym[2] << 32) | ((unsigned long long)zero << 48) |
-                ((unsigned long long)(starts >> 1) << 49) | ((unsigned long long)o << 60);
-        } else if (pmax[i]) {   // the codeword is longer than 12 bits
-            e = pbase[i] != 0xFFFF ? ((unsigned long long)pbase[i] | ((unsigned long long)(pmax[i] - kL1) << 16) | kLongL2)
-                                   : 0ull;
-        } else {                // no codeword has this prefix (incomplete code)
-            e = kLongNone;
+        // long entries: second-level base | extra bits | flags (no flag: canonical search)
+        const uint32_t longe = pmax[i] ? (pbase[i] != 0xFFFF ? (pbase[i] | ((pmax[i] - kL1) << 16) | kLongL2) : 0u)
+                                       : kLongNone;
+        if (ns == 6) {
+            uint4 e;
+            e.x = sym[0] | (sym[1] << 16);
+            e.y = sym[2] | (sym[3] << 16);
+            e.z = sym[4] | (sym[5] << 16);
+            e.w = m ? (zero | (starts & 0xFFEu) | (o << 28)) : longe;
+            reinterpret_cast<uint4*>(tab)[i] = e;
+        } else {
+            const unsigned long long e =
+                m ? ((unsigned long long)sym[0] | ((unsigned long long)sym[1] << 16) |
+                     ((unsigned long long)sym[2] << 32) | ((unsigned long long)zero << 48) |
+                     ((unsigned long long)(starts >> 1) << 49) | ((unsigned long long)o << 60))
+                  : (unsigned long long)longe;
+            reinterpret_cast<unsigned long long*>(tab)[i] = e;
         }
-        reinterpret_cast<unsigned long long*>(tab)[i] = e;
     }
     // second-level entries
     for (long long i = lo + threadIdx.x; pl2 && i < nsym; i += blockDim.x) {
@@ -253,7 +271,7 @@ __device__ __forceinline__ void dtab_body(const uint64_t* __restrict__ first,
         const uint32_t low = (uint32_t)(code & ((1ull << extra) - 1));
         const uint32_t start = pbase[p] + (low << (k - extra));
         const uint32_t e = (symbols[i] << 16) | (uint32_t)b;
-        for (uint32_t j = 0; j < (1u << (k - extra)); j++) tab[kOffL2 + start + j] = e;
+        for (uint32_t j = 0; j < (1u << (k - extra)); j++) tab[offl2 + start + j] = e;
     }
 }
 // decompress prep in one launch of two clusters: cluster 0 scans the chunk
@@ -263,13 +281,13 @@ __global__ void __cluster_dims__(kScanCtas, 1, 1) __launch_bounds__(1024) decode
     const uint64_t* __restrict__ first, const int64_t* __restrict__ offsets,
     const uint32_t* __restrict__ symbols, int max_bw_arg, DevStatus* st, uint32_t* __restrict__ tab,
     uint32_t* __restrict__ old_lut, const uint32_t* __restrict__ chunk_bits, uint64_t C,
-    unsigned long long* __restrict__ byte_off, uint8_t* __restrict__ redo, unsigned int* counter) {
+    unsigned long long* __restrict__ byte_off, uint8_t* __restrict__ redo, unsigned int* counter, int ns) {
     if (blockIdx.x < kScanCtas) {   // cluster 0: chunk byte offsets, flag clears
         for (uint64_t i = blockIdx.x * 1024ull + threadIdx.x; i < C; i += kScanCtas * 1024ull) redo[i] = 0;
         if (blockIdx.x == 0 && threadIdx.x == 0) *counter = 0;
         cluster_chunk_scan(blockIdx.x, chunk_bits, nullptr, C, byte_off, nullptr, ~0ull, false, 0, st);
     } else if (blockIdx.x < kScanCtas + 6) {   // cluster 1: decode tables
-        dtab_body(first, offsets, symbols, max_bw_arg, st, tab, old_lut, (int)(blockIdx.x - kScanCtas));
+        dtab_body(first, offsets, symbols, max_bw_arg, st, tab, old_lut, (int)(blockIdx.x - kScanCtas), ns);
     }
 }
 
@@ -277,13 +295,18 @@ __global__ void __cluster_dims__(kScanCtas, 1, 1) __launch_bounds__(1024) decode
 // decoder
 // ---------------------------------------------------------------------------
 constexpr uint32_t kSliceMin = 64;         // bits per lane slice
-constexpr uint32_t kSliceMax = 192;
+template <int NS>
+constexpr uint32_t kSliceMax = NS == 6 ? 160 : 192;   // (NS = 6: short codes, smaller stages)
 constexpr uint32_t kTargetCodes = 56;      // codewords per lane slice (sets S from the chunk's bits/code)
 constexpr uint32_t kFinalSlices = 48;      // a round whose rest fits 48 slices of S is the chunk's last
-constexpr uint32_t kBufStride = 59;        // u32 words per lane buffer (odd: distinct banks at equal slots)
-constexpr uint32_t kStoreMax = 2 * kBufStride - 3;   // a step stores 3 slots at P <= kStoreMax
+// u32 words per lane buffer (odd: distinct banks at equal slots)
+template <int NS>
+constexpr uint32_t kBufStride = NS == 6 ? 53 : 59;
+template <int NS>
+constexpr uint32_t kStoreMax = 2 * kBufStride<NS> - NS;   // a step stores NS slots at P <= kStoreMax
 // stage of one round: up to kFinalSlices slices + the last exit's overrun + the reader's look-ahead
-constexpr uint32_t kStageUnits = (kFinalSlices * kSliceMax + 32 + 255) / 128 + 3;   // 16-byte units
+template <int NS>
+constexpr uint32_t kStageUnits = (kFinalSlices * kSliceMax<NS> + 32 + 255) / 128 + 3;   // 16-byte units
 constexpr int kDecWarps = 16;
 // synchronisation window: the head mask `lo` covers the first 64 bits of a
 // slice; kHeadHi adds a second mask over [52, 116).  Measured: the second mask
@@ -305,6 +328,11 @@ __device__ __forceinline__ uint32_t lds32(uint32_t addr) {
 __device__ __forceinline__ unsigned long long lds64(uint32_t addr) {
     unsigned long long v;
     asm volatile("ld.shared.u64 %0, [%1];" : "=l"(v) : "r"(addr));
+    return v;
+}
+__device__ __forceinline__ uint4 lds128(uint32_t addr) {
+    uint4 v;
+    asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "r"(addr));
     return v;
 }
 __device__ __forceinline__ uint32_t lds16(uint32_t addr) {
@@ -335,30 +363,59 @@ __device__ __noinline__ uint32_t long_search(const uint32_t* symbols, int mx, ui
     return kSymInvalid;
 }
 
-// One table step at `peek`: total length, codeword-start mask, symbols
-// (s01 = sym0 | sym1 << 16, s2 = sym2 | zero flag << 16).
+// symbol words of one table step: NS = 3: sym0 | sym1 << 16, sym2 | zero
+// flag << 16; NS = 6: three words of two symbols, then the zero flag (bit 0)
+template <int NS>
+struct Syms {
+    uint32_t w[NS == 6 ? 4 : 2];
+    __device__ __forceinline__ uint32_t zero() const { return NS == 6 ? (w[3] & 1u) : (w[1] & 0x10000u); }
+    __device__ __forceinline__ uint32_t sym(int q) const {
+        return (w[q >> 1] >> (16 * (q & 1))) & 0xFFFFu;
+    }
+};
+
+// the long-codeword path: second level, no codeword, or canonical search
+__device__ __forceinline__ uint32_t long_step(const Dec& d, uint32_t info, uint32_t peek, uint32_t offl2) {
+    if (info & kLongL2) {
+        const uint32_t k = (info >> 16) & 31u;
+        return lds32(d.tab_s + (offl2 + (info & 0xFFFFu) + ((peek << kL1) >> (32 - k))) * 4);
+    }
+    if (info & kLongNone) return kSymInvalid;
+    return long_search(d.symbols, d.mx, peek);
+}
+
+// One table step at `peek`: total length, codeword-start mask, symbols.
+template <int NS>
 __device__ __forceinline__ void dstep(const Dec& d, uint32_t peek, uint32_t& len, uint32_t& mask,
-                                      uint32_t& s01, uint32_t& s2, uint32_t& bad) {
-    const unsigned long long e = lds64(d.tab_s + ((peek >> (32 - kL1)) << 3));
-    s01 = (uint32_t)e;
-    s2 = (uint32_t)(e >> 32);
-    len = s2 >> 28;
-    if (len) {
-        mask = ((s2 >> 16) & 0xFFEu) | 1u;
-    } else {   // long codeword (or a prefix no codeword has)
-        uint32_t ee;
-        if (s01 & kLongL2) {
-            const uint32_t k = (s01 >> 16) & 31u;
-            ee = lds32(d.tab_s + (kOffL2 + (s01 & 0xFFFFu) + ((peek << kL1) >> (32 - k))) * 4);
-        } else if (s01 & kLongNone) {
-            ee = kSymInvalid;
-        } else {
-            ee = long_search(d.symbols, d.mx, peek);
-        }
+                                      Syms<NS>& sv, uint32_t& bad) {
+    uint32_t info;
+    if (NS == 6) {
+        const uint4 e = lds128(d.tab_s + ((peek >> (32 - kL1)) << 4));
+        sv.w[0] = e.x;
+        sv.w[1] = e.y;
+        sv.w[2] = e.z;
+        sv.w[NS == 6 ? 3 : 1] = e.w;
+        len = e.w >> 28;
+        mask = (e.w & 0xFFEu) | 1u;
+        info = e.w;
+    } else {
+        const unsigned long long e = lds64(d.tab_s + ((peek >> (32 - kL1)) << 3));
+        sv.w[0] = (uint32_t)e;
+        sv.w[1] = (uint32_t)(e >> 32);
+        len = sv.w[1] >> 28;
+        mask = ((sv.w[1] >> 16) & 0xFFEu) | 1u;
+        info = sv.w[0];
+    }
+    if (!len) {   // long codeword (or a prefix no codeword has)
+        const uint32_t ee = long_step(d, info, peek, Fmt<NS>::kOffL2);
         bad |= ee & 0x80u;
         len = ee & 63u;
-        s01 = ee >> 16;
-        s2 = s01 ? 0u : 0x10000u;
+        sv.w[0] = ee >> 16;
+        if (NS == 6) {
+            sv.w[NS == 6 ? 3 : 1] = sv.w[0] ? 0u : 1u;
+        } else {
+            sv.w[1] = sv.w[0] ? 0u : 0x10000u;
+        }
         mask = 1u;
     }
 }
@@ -397,14 +454,43 @@ struct Cursor {
     }
 };
 
-// store a step's three symbol slots at ordinal P (slots past n are
+// Lane buffers are interleaved across the warp: slots 2j, 2j+1 of lane l are
+// the two halves of word j * 32 + l, so a lane only ever touches its own bank
+// (no conflicts whatever the lanes' ordinals).  buf_s = the lane's word 0.
+__device__ __forceinline__ uint32_t slot_addr(uint32_t buf_s, uint32_t s) {
+    return buf_s + ((s >> 1) << 7) + ((s & 1) << 1);
+}
+__device__ __forceinline__ void sts32(uint32_t addr, uint32_t v) {
+    asm volatile("st.shared.u32 [%0], %1;" ::"r"(addr), "r"(v) : "memory");
+}
+
+// store a step's NS symbol slots at ordinal P (slots past n are
 // overwritten by the next step; ordinals past the buffer pile up in its last
-// slots and the span is then decoded again by lane_direct)
-__device__ __forceinline__ void put3(uint32_t buf_s, uint32_t P, uint32_t s01, uint32_t s2) {
-    const uint32_t a = buf_s + 2 * (P < kStoreMax ? P : kStoreMax);
-    sts16(a, s01);
-    sts16(a + 2, s01 >> 16);
-    sts16(a + 4, s2);
+// slots and the span is then decoded again by lane_direct): whole slot pairs
+// as 32-bit stores, plus a 16-bit store at each odd end
+template <int NS>
+__device__ __forceinline__ void put(uint32_t buf_s, uint32_t P, const Syms<NS>& sv) {
+    const uint32_t Pc = P < kStoreMax<NS> ? P : kStoreMax<NS>;
+    const uint32_t w = buf_s + ((Pc >> 1) << 7);   // word of slot Pc
+    if (NS == 3) {
+        // even: [s0 s1] [s2 .]   odd: [. s0] [s1 s2]
+        const bool odd = Pc & 1;
+        const uint32_t pair = odd ? __byte_perm(sv.w[0], sv.w[1], 0x5432) : sv.w[0];
+        sts32(odd ? w + 128 : w, pair);
+        sts16(odd ? w + 2 : w + 128, odd ? sv.w[0] : sv.w[1]);
+    } else {
+        // even: [s0 s1] [s2 s3] [s4 s5]   odd: [. s0] [s1 s2] [s3 s4] [s5 .]
+        if (Pc & 1) {
+            sts16(w + 2, sv.w[0]);
+            sts32(w + 128, __byte_perm(sv.w[0], sv.w[1], 0x5432));
+            sts32(w + 256, __byte_perm(sv.w[1], sv.w[2], 0x5432));
+            sts16(w + 384, sv.w[2] >> 16);
+        } else {
+            sts32(w, sv.w[0]);
+            sts32(w + 128, sv.w[1]);
+            sts32(w + 256, sv.w[2]);
+        }
+    }
 }
 
 // Phase 1a of one lane: decode from the cursor to the slice end S storing
@@ -412,16 +498,18 @@ __device__ __forceinline__ void put3(uint32_t buf_s, uint32_t P, uint32_t s01, u
 // boundary), recording the codeword starts of the first 116 bits after A0 in
 // two overlapping 64-bit head masks: `lo` = [0, 64), `hi` = [52, 116).  tl = the starts at/after S of the step crossing S (bit
 // 0 = S).  One loop: lanes diverge only in its trip count.
+template <int NS>
 __device__ __forceinline__ void lane_decode(const Dec& d, Cursor& rd, uint32_t A0, uint32_t S, uint32_t buf_s,
                                             uint32_t& P, uint32_t& bad, uint32_t& zf, unsigned long long& lo,
                                             unsigned long long& hi, uint32_t& tl) {
-    uint32_t len = 0, mask = 0, s01, s2, p = rd.pos;
+    uint32_t len = 0, mask = 0, p = rd.pos;
+    Syms<NS> sv;
     unsigned long long l = 0, h = 0;
     while (rd.pos < S) {
         p = rd.pos;
-        dstep(d, rd.peek(), len, mask, s01, s2, bad);
-        put3(buf_s, P, s01, s2);
-        zf |= s2 & 0x10000u;
+        dstep<NS>(d, rd.peek(), len, mask, sv, bad);
+        put<NS>(buf_s, P, sv);
+        zf |= sv.zero();
         const uint32_t r = p - A0;
         if (r < kHeadBits) l |= (unsigned long long)mask << r;
         if (kHeadHi && r - 52 < 64) h |= (unsigned long long)mask << (r - 52);
@@ -441,6 +529,7 @@ __device__ __forceinline__ void lane_decode(const Dec& d, Cursor& rd, uint32_t A
 // -- the synchronisation point -- or S + 116 / the next lane's slice end S2.  sync_pos = the
 // synchronisation point (or the tail's end: a true codeword start as well, on
 // a true lane); kt = tail codewords before it.
+template <int NS>
 __device__ __forceinline__ bool lane_tail(const Dec& d, Cursor& rd, uint32_t S, uint32_t S2, uint32_t tl,
                                           unsigned long long nlo, unsigned long long nhi, uint32_t buf_s,
                                           uint32_t& P, uint32_t& bad, uint32_t& zf, uint32_t& sync_pos,
@@ -453,13 +542,14 @@ __device__ __forceinline__ bool lane_tail(const Dec& d, Cursor& rd, uint32_t S, 
         return true;
     }
     uint32_t n = __popc(tl);
-    uint32_t len, mask, s01, s2;
+    uint32_t len, mask;
+    Syms<NS> sv;
     const uint32_t T = S + kTailBits < S2 ? S + kTailBits : S2;   // the next lane's head masks end at its slice end
     while (rd.pos < T) {
         const uint32_t rt = rd.pos - S;
-        dstep(d, rd.peek(), len, mask, s01, s2, bad);
-        put3(buf_s, P, s01, s2);
-        zf |= s2 & 0x10000u;
+        dstep<NS>(d, rd.peek(), len, mask, sv, bad);
+        put<NS>(buf_s, P, sv);
+        zf |= sv.zero();
         const unsigned long long hl = rt < 64 ? ((unsigned long long)mask << rt) & nlo : 0ull;
             const unsigned long long hh = (kHeadHi && rt >= 52) ? ((unsigned long long)mask << (rt - 52)) & nhi : 0ull;
         if (hl | hh) {
@@ -493,13 +583,14 @@ __device__ __forceinline__ uint32_t zero_halves(uint32_t w) {
 // the lane decoded one (cz).
 __device__ __forceinline__ uint32_t copy_out(uint32_t buf_s, uint32_t a, uint32_t nl, uint16_t* dst, bool cz) {
     uint32_t z = 0, s = a, n = nl;
-    auto pair = [&](uint32_t slot) -> uint32_t {   // slots slot, slot+1 as one word
-        const uint32_t wa = buf_s + ((slot >> 1) << 2);
+    // slots slot, slot+1 as one word (an odd slot straddles two of the lane's words)
+    auto pair = [&](uint32_t slot) -> uint32_t {
+        const uint32_t wa = buf_s + ((slot >> 1) << 7);
         const uint32_t w0 = lds32(wa);
-        return (slot & 1) ? __byte_perm(w0, lds32(wa + 4), 0x5432) : w0;
+        return (slot & 1) ? __byte_perm(w0, lds32(wa + 128), 0x5432) : w0;
     };
     if (n && ((uint32_t)(uintptr_t)dst & 2u)) {   // odd element: one u16
-        const uint32_t v = lds16(buf_s + 2 * s);
+        const uint32_t v = lds16(slot_addr(buf_s, s));
         *dst = (uint16_t)v;
         z += v == 0;
         s++;
@@ -515,14 +606,14 @@ __device__ __forceinline__ uint32_t copy_out(uint32_t buf_s, uint32_t a, uint32_
         n -= 2;
     }
     for (; n >= 8; n -= 8, s += 8, dst += 8) {
-        const uint32_t wa = buf_s + ((s >> 1) << 2);
+        const uint32_t wa = buf_s + ((s >> 1) << 7);
         uint4 v;
         v.x = lds32(wa);
-        v.y = lds32(wa + 4);
-        v.z = lds32(wa + 8);
-        v.w = lds32(wa + 12);
+        v.y = lds32(wa + 128);
+        v.z = lds32(wa + 256);
+        v.w = lds32(wa + 384);
         if (s & 1) {
-            const uint32_t w4 = lds32(wa + 16);
+            const uint32_t w4 = lds32(wa + 512);
             v.x = __byte_perm(v.x, v.y, 0x5432);
             v.y = __byte_perm(v.y, v.z, 0x5432);
             v.z = __byte_perm(v.z, v.w, 0x5432);
@@ -537,7 +628,7 @@ __device__ __forceinline__ uint32_t copy_out(uint32_t buf_s, uint32_t a, uint32_
         if (cz) z += zero_halves(w);
     }
     if (n) {
-        const uint32_t v = lds16(buf_s + 2 * s);
+        const uint32_t v = lds16(slot_addr(buf_s, s));
         *dst = (uint16_t)v;
         z += v == 0;
     }
@@ -546,19 +637,21 @@ __device__ __forceinline__ uint32_t copy_out(uint32_t buf_s, uint32_t a, uint32_
 
 // A lane whose true span overflowed its buffer decodes it again straight to
 // global memory (rare: a slice of unusually short codewords).
+template <int NS>
 __device__ __noinline__ uint32_t lane_direct(const Dec& d, uint32_t stage_s, uint32_t origin, uint32_t start,
                                              uint32_t count, uint16_t* dst) {
     Cursor rd;
     rd.seek(stage_s, origin, start);
     uint32_t j = 0, z = 0, bad = 0;
     while (j < count) {
-        uint32_t len, mask, s01, s2;
-        dstep(d, rd.peek(), len, mask, s01, s2, bad);
+        uint32_t len, mask;
+        Syms<NS> sv;
+        dstep<NS>(d, rd.peek(), len, mask, sv, bad);
         const uint32_t n = __popc(mask), take = n < count - j ? n : count - j;
-        const uint32_t v[3] = {s01 & 0xFFFFu, s01 >> 16, s2 & 0xFFFFu};
         for (uint32_t q = 0; q < take; q++) {
-            dst[j + q] = (uint16_t)v[q];
-            z += v[q] == 0;
+            const uint32_t v = sv.sym((int)q);
+            dst[j + q] = (uint16_t)v;
+            z += v == 0;
         }
         j += take;
         rd.adv(len);
@@ -567,6 +660,7 @@ __device__ __noinline__ uint32_t lane_direct(const Dec& d, uint32_t stage_s, uin
 }
 
 // One lane's phase 1 from `start` (ordinal 0): slice, exit, tail.
+template <int NS>
 __device__ __forceinline__ void lane_phase1(const Dec& d, Cursor& rd, uint32_t stage_s, uint32_t origin,
                                             uint32_t start, uint32_t s0, uint32_t s1, uint32_t s2, bool last,
                                             unsigned long long nlo, unsigned long long nhi, uint32_t buf_s,
@@ -576,19 +670,20 @@ __device__ __forceinline__ void lane_phase1(const Dec& d, Cursor& rd, uint32_t s
     uint32_t tl;
     rd.seek(stage_s, origin, start);
     P = 0;
-    lane_decode(d, rd, s0, s1, buf_s, P, bad, zf, lo, hi, tl);
+    lane_decode<NS>(d, rd, s0, s1, buf_s, P, bad, zf, lo, hi, tl);
     ex = tl ? s1 + (uint32_t)(__ffs(tl) - 1) : rd.pos;   // first codeword start >= s1
     k = P - (uint32_t)__popc(tl);                        // ordinals before the exit
     fwd = false;
     sp = ex;
     kt = 0;
-    if (!last) fwd = lane_tail(d, rd, s1, s2, tl, nlo, nhi, buf_s, P, bad, zf, sp, kt);
+    if (!last) fwd = lane_tail<NS>(d, rd, s1, s2, tl, nlo, nhi, buf_s, P, bad, zf, sp, kt);
 }
 
 // One round: lanes [0, L) decode the slices [s0, s1) of one stretch of a
 // chunk (lane 0 from the round's true start); the buffered true spans go to
 // out[ob ...].  Returns false to hand the chunk back; next_q = the last
 // lane's exit (the next round's true start).
+template <int NS>
 __device__ __forceinline__ bool decode_round(const Dec& d, uint32_t stage_s, uint32_t origin, uint32_t L,
                                              uint32_t s0, uint32_t s1, uint32_t buf_s, uint16_t* out,
                                              uint32_t& ob, uint32_t cnt, uint32_t& next_q, uint32_t& zeros,
@@ -601,7 +696,7 @@ __device__ __forceinline__ bool decode_round(const Dec& d, uint32_t stage_s, uin
     unsigned long long lo = 0, hi = 0;
     if (active) {
         rd.seek(stage_s, origin, s0);
-        lane_decode(d, rd, s0, s1, buf_s, P, bad, zf, lo, hi, tl);
+        lane_decode<NS>(d, rd, s0, s1, buf_s, P, bad, zf, lo, hi, tl);
     }
     const unsigned long long nlo = __shfl_down_sync(kFull, lo, 1);
     const unsigned long long nhi = __shfl_down_sync(kFull, hi, 1);
@@ -612,7 +707,7 @@ __device__ __forceinline__ bool decode_round(const Dec& d, uint32_t stage_s, uin
         ex = tl ? s1 + (uint32_t)(__ffs(tl) - 1) : rd.pos;
         k = P - (uint32_t)__popc(tl);
         sp = ex;
-        if (!last) fwd = lane_tail(d, rd, s1, s2, tl, nlo, nhi, buf_s, P, bad, zf, sp, kt);
+        if (!last) fwd = lane_tail<NS>(d, rd, s1, s2, tl, nlo, nhi, buf_s, P, bad, zf, sp, kt);
     }
     // phase 2: lane l continues lane l-1's true path from q = sp(l-1): at the
     // synchronisation point (l-1's tail met l's path: l's ordinals before q are
@@ -633,8 +728,8 @@ __device__ __forceinline__ bool decode_round(const Dec& d, uint32_t stage_s, uin
             rstart = psp;
             bad = 0;
             zf = 0;
-            lane_phase1(d, rd, stage_s, origin, psp, s0, s1, s2, last, nlo, nhi, buf_s, P, bad, zf, lo, hi, ex, k, sp, kt,
-                        fwd);
+            lane_phase1<NS>(d, rd, stage_s, origin, psp, s0, s1, s2, last, nlo, nhi, buf_s, P, bad, zf, lo, hi, ex, k, sp,
+                            kt, fwd);
             atomicAdd(&st->pad[0], 1ull);   // diagnostics: lane redecodes (low word)
         }
     }
@@ -653,10 +748,10 @@ __device__ __forceinline__ bool decode_round(const Dec& d, uint32_t stage_s, uin
     if (ob + (uint32_t)total > cnt) return false;
     if (nl) {
         uint16_t* dst = out + ob + o;
-        if (a + nl <= kStoreMax) {
+        if (a + nl <= kStoreMax<NS>) {
             zeros += copy_out(buf_s, a, nl, dst, zf != 0);
         } else {
-            zeros += lane_direct(d, stage_s, origin, q, nl, dst);
+            zeros += lane_direct<NS>(d, stage_s, origin, q, nl, dst);
             atomicAdd(&st->pad[0], 1ull << 32);   // diagnostics: buffer overflows (high word)
         }
     }
@@ -666,9 +761,10 @@ __device__ __forceinline__ bool decode_round(const Dec& d, uint32_t stage_s, uin
 
 // issue the cp.async loads of stage units [u0, u0 + units) (chunk-relative
 // 16-byte units from cb16) into stage_s; units past the payload read zeros
+template <int NS>
 __device__ __forceinline__ void stage_issue(uint32_t stage_s, const uint4* payload4, uint64_t n4, uint64_t cb16,
                                             uint32_t u0, uint32_t units) {
-    if (units > kStageUnits) units = kStageUnits;
+    if (units > kStageUnits<NS>) units = kStageUnits<NS>;
     for (uint32_t i = lane_id(); i < units; i += 32) {
         const uint64_t u = cb16 + u0 + i;
         const bool in = u < n4;
@@ -686,14 +782,15 @@ __device__ __forceinline__ void round_units(uint32_t q, uint32_t end, uint32_t& 
 }
 
 // slice size: ~target codewords at the chunk's mean code length
+template <int NS>
 __device__ __forceinline__ uint32_t slice_bits(uint32_t B, uint32_t cnt, uint32_t target) {
     const unsigned long long s = (unsigned long long)target * B / (cnt ? cnt : 1);
-    return (uint32_t)(s < kSliceMin ? kSliceMin : (s > kSliceMax ? kSliceMax : s));
+    return (uint32_t)(s < kSliceMin ? kSliceMin : (s > kSliceMax<NS> ? kSliceMax<NS> : s));
 }
 
 // dynamic shared memory: tables (kTabWords) | per-warp lane buffers | per-warp
 // double stage
-template <int kWarps>
+template <int kWarps, int NS>
 __global__ void __launch_bounds__(kWarps * 32, 1) inflate_fast_kernel(
     const uint8_t* __restrict__ payload, uint64_t nwords, const uint32_t* __restrict__ chunk_bits,
     const unsigned long long* __restrict__ byte_off, uint64_t nchunks, uint32_t chunk, uint64_t n,
@@ -713,7 +810,7 @@ __global__ void __launch_bounds__(kWarps * 32, 1) inflate_fast_kernel(
     {
         const uint4* src = reinterpret_cast<const uint4*>(gtab);
         uint4* dst = reinterpret_cast<uint4*>(s_tab);
-        const uint32_t words = mx > kL1 ? kTabWords : kOffL2;   // the second level only for long codes
+        const uint32_t words = mx > kL1 ? Fmt<NS>::kTabWords : Fmt<NS>::kOffL2;   // the second level only for long codes
         for (uint32_t i = threadIdx.x; i < words / 4; i += blockDim.x) dst[i] = __ldg(src + i);
         for (int b = threadIdx.x; b < 34; b += blockDim.x) {
             const bool in = b >= 1 && b <= mx;
@@ -732,8 +829,10 @@ __global__ void __launch_bounds__(kWarps * 32, 1) inflate_fast_kernel(
     d.mx = mx;
     const uint32_t lane = lane_id(), wid = threadIdx.x >> 5;
     uint32_t buf_s;
-    asm volatile("mov.u32 %0, %1;" : "=r"(buf_s) : "r"(smem_base + kTabWords * 4 + (wid * 32 + lane) * kBufStride * 4));
-    const uint32_t stage0 = smem_base + kTabWords * 4 + kWarps * 32 * kBufStride * 4 + wid * 2 * kStageUnits * 16;
+    constexpr uint32_t kTW = Fmt<NS>::kTabWords;
+    constexpr uint32_t kBS = kBufStride<NS>, kSU = kStageUnits<NS>;
+    asm volatile("mov.u32 %0, %1;" : "=r"(buf_s) : "r"(smem_base + kTW * 4 + (wid * 32 * kBS + lane) * 4));
+    const uint32_t stage0 = smem_base + kTW * 4 + kWarps * 32 * kBS * 4 + wid * 2 * kSU * 16;
     const uint4* payload4 = reinterpret_cast<const uint4*>(payload);
     const uint64_t n4 = nwords / 4;
     uint32_t zeros = 0, cur = 0;
@@ -755,10 +854,10 @@ __global__ void __launch_bounds__(kWarps * 32, 1) inflate_fast_kernel(
         const uint32_t E = sbit + B;
         bool good = B != 0 && cnt != 0;
         if (good) {
-            const uint32_t S = slice_bits(B, cnt, target);
+            const uint32_t S = slice_bits<NS>(B, cnt, target);
             uint32_t q = sbit, ob = 0, u0, units, cz = 0;   // cz: zero codes of this chunk
             round_units(q, (E - q <= kFinalSlices * S) ? E : q + 32 * S, u0, units);
-            if (!have) stage_issue(stage0 + cur * kStageUnits * 16, payload4, n4, cb16, u0, units);
+            if (!have) stage_issue<NS>(stage0 + cur * kSU * 16, payload4, n4, cb16, u0, units);
             have = false;
             for (;;) {
                 const uint32_t R = E - q;
@@ -775,22 +874,22 @@ __global__ void __launch_bounds__(kWarps * 32, 1) inflate_fast_kernel(
                     s1 = s0 + S;
                 }
                 // prefetch: the next round of this chunk, or the next chunk's first round
-                const uint32_t nstage = stage0 + (cur ^ 1) * kStageUnits * 16;
+                const uint32_t nstage = stage0 + (cur ^ 1) * kSU * 16;
                 if (!fin) {
                     const uint32_t nq = q + 32 * S;   // the next round starts in [nq, nq + 32)
                     uint32_t nunits;
                     const uint32_t nend = E - nq <= kFinalSlices * S + 32 ? E : nq + 32 + 32 * S;
                     round_units(nq, nend, nu0, nunits);
-                    stage_issue(nstage, payload4, n4, cb16, nu0, nunits);
+                    stage_issue<NS>(nstage, payload4, n4, cb16, nu0, nunits);
                 } else if (cn < nchunks) {
                     const unsigned long long nboff = byte_off[cn];
                     const uint32_t nB = chunk_bits[cn];
                     const uint32_t ncnt = (uint32_t)umin(chunk, n - (uint64_t)cn * chunk);
-                    const uint32_t nS = slice_bits(nB, ncnt, target);
+                    const uint32_t nS = slice_bits<NS>(nB, ncnt, target);
                     const uint32_t nsb = (uint32_t)(nboff & 15) * 8;
                     uint32_t a0, au;
                     round_units(nsb, (nB <= kFinalSlices * nS) ? nsb + nB : nsb + 32 * nS, a0, au);
-                    stage_issue(nstage, payload4, n4, nboff >> 4, a0, au);
+                    stage_issue<NS>(nstage, payload4, n4, nboff >> 4, a0, au);
                     have = true;
                 } else {
                     asm volatile("cp.async.commit_group;" ::: "memory");
@@ -798,7 +897,7 @@ __global__ void __launch_bounds__(kWarps * 32, 1) inflate_fast_kernel(
                 asm volatile("cp.async.wait_group 1;" ::: "memory");
                 __syncwarp();
                 uint32_t next_q = 0;
-                good = decode_round(d, stage0 + cur * kStageUnits * 16, u0 * 128, L, s0, s1, buf_s, out + base, ob,
+                good = decode_round<NS>(d, stage0 + cur * kSU * 16, u0 * 128, L, s0, s1, buf_s, out + base, ob,
                                     cnt, next_q, cz, st);
                 __syncwarp();   // the stage and the buffers are refilled next
                 cur ^= 1;
@@ -832,14 +931,14 @@ __global__ void __launch_bounds__(kWarps * 32, 1) inflate_fast_kernel(
 int launch_decode_prep(sdqz_ctx* ctx, const uint64_t* first, const int64_t* offsets,
                        const uint32_t* symbols, int max_bw, uint32_t** tab_out, uint32_t* old_lut,
                        const uint32_t* chunk_bits, uint64_t n_chunks, unsigned long long* byte_off,
-                       uint8_t* redo) {
+                       uint8_t* redo, int ns) {
     int rc = SDQZ_OK;
-    uint32_t* tab = scratch_as<uint32_t>(ctx, S_DTAB, kTabWords, &rc);
+    uint32_t* tab = scratch_as<uint32_t>(ctx, S_DTAB, kTabWordsMax, &rc);
     unsigned int* counter = scratch_as<unsigned int>(ctx, S_COUNTER, 4, &rc);
     if (!tab || !counter) return rc;
     decode_prep_kernel<<<2 * kScanCtas, 1024, 0, ctx->stream>>>(first, offsets, symbols, max_bw, ctx->d_status, tab,
                                                                 old_lut, chunk_bits, n_chunks, byte_off, redo,
-                                                                counter);
+                                                                counter, ns);
     SDQZ_LAUNCHED_NAMED(ctx, "decode_prep_kernel");
     *tab_out = tab;
     return SDQZ_OK;
@@ -855,23 +954,51 @@ static uint32_t dec_target() {
     return t;
 }
 
+template <int kW, int NS>
+static void launch_inflate_ns(sdqz_ctx* ctx, const uint8_t* payload, uint64_t nwords,
+                              const uint32_t* chunk_bits, const unsigned long long* byte_off,
+                              uint64_t n_chunks, uint32_t chunk, uint64_t n, const uint64_t* first,
+                              const int64_t* offsets, const uint32_t* symbols, const uint32_t* tab,
+                              int max_bw, uint16_t* codes, uint8_t* redo, unsigned int* counter) {
+    constexpr size_t smem = (size_t)Fmt<NS>::kTabWords * 4 + (size_t)kW * 32 * kBufStride<NS> * 4 +
+                            (size_t)kW * 2 * kStageUnits<NS> * 16 + 16;
+    static_assert(smem <= 227 * 1024, "decoder shared memory");
+    ensure_smem(ctx, (const void*)inflate_fast_kernel<kW, NS>, smem);
+    uint64_t grid = ceil_div(n_chunks, kW);
+    if (grid > (uint64_t)ctx->num_sms) grid = ctx->num_sms;
+    if (grid < 1) grid = 1;
+    inflate_fast_kernel<kW, NS><<<(unsigned)grid, kW * 32, smem, ctx->stream>>>(
+        payload, nwords, chunk_bits, byte_off, n_chunks, chunk, n, first, offsets, symbols, tab, max_bw, codes,
+        redo, counter, dec_target(), ctx->d_status);
+}
+
+// symbols per table step: 6 (u128 entries; measured as fast or faster than
+// u64 entries of three on every config, 2 to 7 bits per code); SDQZ_DEC_NS=3
+// selects the u64 table (tests keep both paths exact)
+int decode_ns(uint64_t payload_bytes, uint64_t n) {
+    (void)payload_bytes;
+    (void)n;
+    static const int forced = [] {
+        const char* e = getenv("SDQZ_DEC_NS");
+        return e ? atoi(e) : 0;
+    }();
+    return forced == 3 ? 3 : 6;
+}
+
 int launch_inflate_fast(sdqz_ctx* ctx, const uint8_t* payload, uint64_t nwords,
                         const uint32_t* chunk_bits, const unsigned long long* byte_off,
                         uint64_t n_chunks, uint32_t chunk, uint64_t n, const uint64_t* first,
                         const int64_t* offsets, const uint32_t* symbols, const uint32_t* tab,
-                        int max_bw, uint16_t* codes, uint8_t* redo) {
+                        int max_bw, uint16_t* codes, uint8_t* redo, int ns) {
     int rc = SDQZ_OK;
     unsigned int* counter = scratch_as<unsigned int>(ctx, S_COUNTER, 4, &rc);   // cleared by the prep kernel
     if (!counter) return rc;
-    constexpr int kW = kDecWarps;
-    const size_t smem = (size_t)kTabWords * 4 + (size_t)kW * 32 * kBufStride * 4 + (size_t)kW * 2 * kStageUnits * 16 + 16;
-    ensure_smem(ctx, (const void*)inflate_fast_kernel<kW>, smem);
-    uint64_t grid = ceil_div(n_chunks, kW);
-    if (grid > (uint64_t)ctx->num_sms) grid = ctx->num_sms;
-    if (grid < 1) grid = 1;
-    inflate_fast_kernel<kW><<<(unsigned)grid, kW * 32, smem, ctx->stream>>>(
-        payload, nwords, chunk_bits, byte_off, n_chunks, chunk, n, first, offsets, symbols, tab, max_bw, codes,
-        redo, counter, dec_target(), ctx->d_status);
+    if (ns == 6)
+        launch_inflate_ns<kDecWarps, 6>(ctx, payload, nwords, chunk_bits, byte_off, n_chunks, chunk, n, first,
+                                         offsets, symbols, tab, max_bw, codes, redo, counter);
+    else
+        launch_inflate_ns<kDecWarps, 3>(ctx, payload, nwords, chunk_bits, byte_off, n_chunks, chunk, n, first,
+                                        offsets, symbols, tab, max_bw, codes, redo, counter);
     SDQZ_LAUNCHED_NAMED(ctx, "inflate_fast_kernel");
     return SDQZ_OK;
 }

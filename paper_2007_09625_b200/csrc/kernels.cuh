@@ -75,12 +75,14 @@ int launch_inflate(sdqz_ctx* ctx, const uint8_t* payload, uint64_t payload_bytes
 int launch_decode_prep(sdqz_ctx* ctx, const uint64_t* first, const int64_t* offsets,
                        const uint32_t* symbols, int max_bw, uint32_t** tab_out, uint32_t* old_lut,
                        const uint32_t* chunk_bits, uint64_t n_chunks, unsigned long long* byte_off,
-                       uint8_t* redo);
+                       uint8_t* redo, int ns);
+// symbols per decode-table step (3 or 6) for a stream of n codes in payload_bytes
+int decode_ns(uint64_t payload_bytes, uint64_t n);
 int launch_inflate_fast(sdqz_ctx* ctx, const uint8_t* payload, uint64_t nwords,
                         const uint32_t* chunk_bits, const unsigned long long* byte_off,
                         uint64_t n_chunks, uint32_t chunk, uint64_t n, const uint64_t* first,
                         const int64_t* offsets, const uint32_t* symbols, const uint32_t* tab,
-                        int max_bw, uint16_t* codes, uint8_t* redo);
+                        int max_bw, uint16_t* codes, uint8_t* redo, int ns);
 
 // reconstruct.cu ------------------------------------------------------------
 // Validate outlier records (range, order, code==0) and scatter their fp64

@@ -607,6 +607,18 @@ class TestLargeChunks:
         assert h.payload_bytes / h.n_chunks > 8192
         assert np.array_equal(bits(S.decompress(blob)), bits(O.decompress(blob)))
 
+    @pytest.mark.parametrize("eb,chunk", [(3e-2, 32768), (1e-3, 40001), (2e-5, 65536), (1e-6, 32768)])
+    def test_register_run_packer(self, eb, chunk):
+        """Chunks >= 32768 codes take the register-run packer (chunk_pack32_runs_kernel):
+        low to high code entropy (16-, 8- and 4-code sub-runs, runs over 64 bits),
+        an odd chunk size (unaligned chunk starts), outliers."""
+        f = S.generate_field("smooth", (40, 96, 128), seed=7).astype(np.float32)
+        f[::7, ::5, ::3] += np.float32(3.0)
+        kw = dict(eb=eb, mode="valrel", chunk_size=chunk)
+        blob = S.compress(f, **kw)
+        assert blob == O.compress(f, **kw)
+        assert np.array_equal(bits(S.decompress(blob)), bits(O.decompress(blob)))
+
     def test_big_chunk_bitflips(self):
         rng = np.random.default_rng(99)
         f = np.cumsum(rng.normal(0, 1, 200_000)).astype(np.float32)

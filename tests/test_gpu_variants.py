@@ -1,0 +1,58 @@
+"""Kernel variants behind environment switches stay bit-exact: each switch is
+read once per process, so every case runs in a fresh interpreter that
+compresses / decompresses a few fields through the package and compares
+archive bytes and decompressed bits with the oracle (oracle/sdqz_oracle.py).
+
+  SDQZ_DEC_NS=3     the u64 three-symbol decode table (default: u128, six)
+  SDQZ_NO_TMA=1     3D dual-quant without the TMA tile pipeline
+  SDQZ_NO_VEC1D=1   scalar 1D dual-quant / reconstruct
+  SDQZ_NO_VEC2D=1   scalar 2D dual-quant / reconstruct
+  SDQZ_NO_GRAPH=1   no CUDA-graph replay of the pipelines
+"""
+import os
+import subprocess
+import sys
+from pathlib import Path
+
+import pytest
+
+ROOT = Path(__file__).resolve().parent.parent
+
+SCRIPT = r"""
+import sys
+import numpy as np
+sys.path.insert(0, sys.argv[1])
+import paper_2007_09625_b200 as S
+from oracle import sdqz_oracle as O
+
+def bits(a):
+    a = np.ascontiguousarray(a)
+    return a.view(np.uint32 if a.dtype == np.float32 else np.uint64)
+
+rng = np.random.default_rng(5)
+fields = [
+    (S.generate_field("smooth", (24, 40, 56), seed=3).astype(np.float32), dict(eb=1e-4, mode="valrel")),
+    (S.generate_field("smooth", (24, 40, 56), seed=4).astype(np.float32), dict(eb=2e-6, mode="valrel")),
+    (S.generate_field("smooth", (300, 451), seed=5).astype(np.float32), dict(eb=1e-3, mode="valrel")),
+    (np.cumsum(rng.normal(0, 1, 200_003)).astype(np.float32), dict(eb=0.01, mode="abs")),
+    (rng.normal(0, 3, (17, 33, 65)).astype(np.float32), dict(eb=0.05, mode="abs", chunk_size=333)),
+]
+for f, kw in fields:
+    blob = S.compress(f, **kw)
+    ref = O.compress(f, **kw)
+    assert blob == ref, ("archive differs", f.shape, kw)
+    assert np.array_equal(bits(S.decompress(blob)), bits(O.decompress(ref))), ("output differs", f.shape, kw)
+print("ok", len(fields))
+"""
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("env", ["SDQZ_DEC_NS=3", "SDQZ_NO_TMA=1", "SDQZ_NO_VEC1D=1", "SDQZ_NO_VEC2D=1",
+                                 "SDQZ_NO_GRAPH=1"])
+def test_variant_bit_exact(env):
+    k, v = env.split("=")
+    e = dict(os.environ, **{k: v})
+    r = subprocess.run([sys.executable, "-c", SCRIPT, str(ROOT)], env=e, capture_output=True, text=True,
+                       timeout=600)
+    assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-4000:]
+    assert r.stdout.strip().startswith("ok"), r.stdout
