@@ -1001,6 +1001,7 @@ struct Geo {
     uint64_t dims[3];
     uint32_t block[3];
     uint64_t stride[3];
+    uint64_t nblk[3];
 };
 
 template <int KIND>
@@ -1064,6 +1065,111 @@ __global__ void __launch_bounds__(kThreads) dq_generic_kernel(const void* __rest
     }
     hist_flush(h);
     if (__any_sync(kFull, bad) && lane_id() == 0) atomicOr(&st->flags, (unsigned long long)F_NONFINITE);
+    hist_finish(h);
+}
+
+// ----------------------------------------------------------------------------
+// Generic block shapes, one thread per block (blocks of <= kBlkMaxSlots plane +
+// row slots): the block is walked in raster order; the prequantized values
+// of the previous row (R[x]) and of the previous plane (P[y][x]) sit in the
+// thread's shared-memory slots ([slot][thread], conflict-free), the x - 1
+// neighbours in registers, so every point is prequantized once and its
+// Lorenzo prediction is the reference's fp64 expression in the reference's
+// term order (dualquant.py:81-129; exactly dq_generic_kernel's arithmetic).
+// P[y-1][x] is overwritten with the current plane's row y-1 as soon as row y
+// has read it, and the last row moves in at the end of the plane.
+// ----------------------------------------------------------------------------
+constexpr uint32_t kBlkMaxSlots = 512;   // per-thread fp64 slots (4 KB)
+
+__host__ __device__ __forceinline__ uint32_t blk_slots(int nd, const uint32_t* block) {
+    const uint32_t bx = block[nd - 1], by = nd >= 2 ? block[nd - 2] : 1;
+    return (nd == 3 ? bx * by : 0) + (nd >= 2 ? bx : 0);
+}
+
+// per-thread flush of the packed window counters (no warp synchronisation:
+// threads of a warp walk blocks of different sizes)
+__device__ __forceinline__ void hist_flush_thread(HistCtx& h) {
+#pragma unroll
+    for (int k = 0; k < 16; k++) {
+        const uint32_t c = (uint32_t)(((k < 8) ? (h.lo >> (8 * k)) : (h.hi >> (8 * (k - 8)))) & 0xFF);
+        if (c) {
+            if (h.shist) atomicAdd(&h.shist[h.wbase + k], c);
+            else if (h.ghist) atomicAdd(&h.ghist[h.wbase + k], (unsigned long long)c);
+        }
+    }
+    h.lo = h.hi = 0;
+}
+
+template <int KIND>
+__global__ void __launch_bounds__(64) dq_blocks_kernel(const void* __restrict__ in, Geo g, uint32_t cap,
+                                                       uint32_t hist_bytes, DevStatus* st,
+                                                       uint16_t* __restrict__ codes, unsigned long long* ghist) {
+    extern __shared__ __align__(128) unsigned char dsm[];
+    HistCtx h;
+    hist_init(h, reinterpret_cast<uint32_t*>(dsm), ghist, cap);
+    const uint32_t T = blockDim.x, tid = threadIdx.x;
+    double* buf = reinterpret_cast<double*>(dsm + hist_bytes) + tid;   // slot s at buf[s * T]
+    const int nd = g.nd;
+    const uint32_t bx = g.block[nd - 1], by = nd >= 2 ? g.block[nd - 2] : 1;
+    double* P = buf;                                          // [by][bx] (3D)
+    double* R = buf + (size_t)(nd == 3 ? bx * by : 0) * T;    // [bx] (2D, 3D)
+    const uint64_t nbx = g.nblk[nd - 1], nby = nd >= 2 ? g.nblk[nd - 2] : 1;
+    const uint64_t nblocks = g.nblk[0] * g.nblk[1] * g.nblk[2];
+    const uint64_t sy = nd >= 2 ? g.stride[nd - 2] : 0, sz = nd == 3 ? g.stride[0] : 0;
+    const uint64_t X = g.dims[nd - 1], Y = nd >= 2 ? g.dims[nd - 2] : 1, Z = nd == 3 ? g.dims[0] : 1;
+    const uint32_t bz = nd == 3 ? g.block[0] : 1;
+    const double two_eb = st->two_eb;
+    const int r = (int)(cap >> 1);
+    bool bad = false;
+    uint32_t cnt = 0;
+    for (uint64_t b = blockIdx.x * (uint64_t)T + tid; b < nblocks; b += (uint64_t)gridDim.x * T) {
+        const uint64_t cx = b % nbx, t2 = b / nbx, cy = t2 % nby, cz = t2 / nby;
+        const uint32_t nx = (uint32_t)umin(bx, X - cx * bx), ny = (uint32_t)umin(by, Y - cy * by),
+                       nz = (uint32_t)umin(bz, Z - cz * bz);
+        const uint64_t base = cz * bz * sz + cy * by * sy + cx * bx;
+        for (uint32_t z = 0; z < nz; z++) {
+            for (uint32_t y = 0; y < ny; y++) {
+                double a = 0.0, e = 0.0, f = 0.0, gq = 0.0;   // (x-1) neighbours: own row, row y-1, plane z-1, both
+                const uint64_t rb = base + z * sz + y * sy;
+                for (uint32_t x = 0; x < nx; x++) {
+                    const double q = load_q<KIND>(in, rb + x, two_eb, bad);
+                    const double bb = (nd >= 2 && y > 0) ? R[(size_t)x * T] : 0.0;
+                    const double cc = (nd == 3 && z > 0) ? P[(size_t)(y * bx + x) * T] : 0.0;
+                    const double dd = (nd == 3 && z > 0 && y > 0) ? P[(size_t)((y - 1) * bx + x) * T] : 0.0;
+                    double pred;
+                    if (nd == 1) {
+                        pred = a;
+                    } else if (nd == 2) {
+                        pred = __dsub_rn(__dadd_rn(bb, a), e);
+                    } else {
+                        pred = __dadd_rn(cc, bb);
+                        pred = __dadd_rn(pred, a);
+                        pred = __dsub_rn(pred, dd);
+                        pred = __dsub_rn(pred, f);
+                        pred = __dsub_rn(pred, e);
+                        pred = __dadd_rn(pred, gq);
+                    }
+                    const uint32_t code = code_of_f64(__dsub_rn(q, pred), r);
+                    codes[rb + x] = (uint16_t)code;
+                    hist_add(h, code);
+                    if (++cnt == 200) {   // 8-bit packed counters
+                        hist_flush_thread(h);
+                        cnt = 0;
+                    }
+                    if (nd == 3 && y > 0) P[(size_t)((y - 1) * bx + x) * T] = bb;   // plane z, row y-1
+                    if (nd >= 2) R[(size_t)x * T] = q;
+                    a = q;
+                    e = bb;
+                    f = cc;
+                    gq = dd;
+                }
+            }
+            if (nd == 3)
+                for (uint32_t x = 0; x < nx; x++) P[(size_t)((ny - 1) * bx + x) * T] = R[(size_t)x * T];
+        }
+    }
+    hist_flush_thread(h);
+    if (bad) atomicOr(&st->flags, (unsigned long long)F_NONFINITE);
     hist_finish(h);
 }
 
@@ -1177,9 +1283,29 @@ int launch_kind(sdqz_ctx* ctx, const void* d_in, int ndims, const uint64_t dims[
     } else {
         Geo g;
         g.nd = ndims;
-        for (int a = 0; a < 3; a++) { g.dims[a] = dims[a]; g.block[a] = block[a]; }
+        for (int a = 0; a < 3; a++) {
+            g.dims[a] = a < ndims ? dims[a] : 1;
+            g.block[a] = a < ndims ? block[a] : 1;
+            g.nblk[a] = a < ndims ? ceil_div(dims[a], block[a]) : 1;
+        }
         g.stride[ndims - 1] = 1;
         for (int a = ndims - 2; a >= 0; a--) g.stride[a] = g.stride[a + 1] * dims[a + 1];
+        const uint32_t slots = blk_slots(ndims, block);
+        if (slots <= kBlkMaxSlots && !env_disabled("SDQZ_NO_BLK")) {
+            // thread per block; 64 threads per CTA while the slots stay <= 1 KB per thread
+            const uint32_t T = slots * 8 <= 1024 ? 64 : 32;
+            const uint32_t hist_bytes = (uint32_t)((smem + 15) & ~(size_t)15);
+            const size_t dsm = hist_bytes + (size_t)T * slots * 8;
+            ensure_smem(ctx, (const void*)dq_blocks_kernel<KIND>, dsm);
+            const uint64_t nblocks = g.nblk[0] * g.nblk[1] * g.nblk[2];
+            uint64_t grid = ceil_div(nblocks, T);
+            if (grid > (uint64_t)ctx->num_sms * 64) grid = (uint64_t)ctx->num_sms * 64;
+            if (grid < 1) grid = 1;
+            dq_blocks_kernel<KIND><<<(unsigned)grid, T, dsm, ctx->stream>>>(d_in, g, cap, hist_bytes, ctx->d_status,
+                                                                           d_codes, d_hist);
+            SDQZ_LAUNCHED_NAMED(ctx, "dq_blocks_kernel");
+            return SDQZ_OK;
+        }
         uint64_t grid = ceil_div(n, kThreads);
         if (grid > (uint64_t)max_grid) grid = max_grid;
         if (grid < 1) grid = 1;

@@ -891,7 +891,7 @@ __global__ void rq_generic_kernel(const uint16_t* __restrict__ codes,
                                   const unsigned long long* __restrict__ dense,
                                   const uint8_t* __restrict__ blockflag, int only_flagged, Geo g,
                                   uint32_t cap, double two_eb, double* __restrict__ work,
-                                  void* __restrict__ out, const DevStatus* st) {
+                                  void* __restrict__ out, const DevStatus* st, uint64_t slot_pts) {
     if (only_flagged && !(st->flags & F_OUT_SLOW)) return;
     const double r = (double)(cap >> 1);
     const uint64_t nblocks = g.nblk[0] * g.nblk[1] * g.nblk[2];
@@ -910,8 +910,8 @@ __global__ void rq_generic_kernel(const uint16_t* __restrict__ codes,
         uint64_t base = o[0] * st0 + (g.nd > 1 ? o[1] * st1 : 0) + (g.nd > 2 ? o[2] * st2 : 0);
         auto gat = [&](uint64_t a, uint64_t bb, uint64_t c) { return base + a * st0 + bb * st1 + c * st2; };
         // work: the whole-field array (all blocks), or this thread's block-sized
-        // slot when only flagged blocks of a <= 512-point shape are replayed
-        const uint64_t wbase = only_flagged ? (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) * kSlotPts : 0;
+        // slot (slot_pts >= the block's points) when only flagged blocks are replayed
+        const uint64_t wbase = only_flagged ? (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) * slot_pts : 0;
         auto at = [&](uint64_t a, uint64_t bb, uint64_t c) {
             return only_flagged ? wbase + (a * e[1] + bb) * e[2] + c : gat(a, bb, c);
         };
@@ -960,6 +960,81 @@ __global__ void rq_generic_kernel(const uint16_t* __restrict__ codes,
                     if (OUTK == 0) ((float*)out)[gi] = __double2float_rn(v);
                     else ((double*)out)[gi] = v;
                 }
+    }
+}
+
+// Generic block shapes, one thread per block (row f4; the fast shapes have
+// their own kernels): the block is walked in raster order with the same
+// integer recurrence as rq3d_block_kernel -- H = prefix_x(delta), G = H + G of
+// row y-1, F = G + F of plane z-1, an outlier fixing F = v and re-deriving G,
+// H (the reference's box corrections in raster order, dualquant.py:218-226).
+// G of the previous row and F of the previous plane sit in the thread's
+// shared-memory slots ([slot][thread]); each is read and overwritten in
+// place.  int32 with the fast kernels' magnitude guard: a block that trips it
+// (or holds a non-integer outlier value, flagged by the scatter) is replayed
+// in the reference's fp64 order by rq_generic_kernel.
+constexpr uint32_t kBlkMaxSlots = 1024;   // per-thread int32 slots (4 KB)
+
+__host__ __device__ __forceinline__ uint32_t blk_slots(int nd, const uint32_t* block) {
+    const uint32_t bx = block[nd - 1], by = nd >= 2 ? block[nd - 2] : 1;
+    return (nd == 3 ? bx * by : 0) + (nd >= 2 ? bx : 0);
+}
+
+template <int OUTK>
+__global__ void __launch_bounds__(64) rq_blocks_kernel(const uint16_t* __restrict__ codes,
+                                                       const unsigned long long* __restrict__ dense,
+                                                       uint8_t* __restrict__ blockflag, Geo g, uint32_t cap,
+                                                       double two_eb, void* __restrict__ out, DevStatus* st) {
+    extern __shared__ __align__(16) int blk_smem[];
+    const uint32_t T = blockDim.x, tid = threadIdx.x;
+    const int nd = g.nd;
+    const uint32_t bx = g.block[nd - 1], by = nd >= 2 ? g.block[nd - 2] : 1, bz = nd == 3 ? g.block[0] : 1;
+    int* P = blk_smem + tid;                                      // [by][bx]: F of plane z-1 (3D)
+    int* Gs = P + (size_t)(nd == 3 ? bx * by : 0) * T;            // [bx]: G of row y-1 (2D, 3D)
+    const uint64_t nbx = g.nblk[nd - 1], nby = nd >= 2 ? g.nblk[nd - 2] : 1;
+    const uint64_t nblocks = g.nblk[0] * g.nblk[1] * g.nblk[2];
+    const uint64_t sy = nd >= 2 ? g.stride[nd - 2] : 0, sz = nd == 3 ? g.stride[0] : 0;
+    const uint64_t X = g.dims[nd - 1], Y = nd >= 2 ? g.dims[nd - 2] : 1, Z = nd == 3 ? g.dims[0] : 1;
+    const int r = (int)(cap >> 1);
+    for (uint64_t b = blockIdx.x * (uint64_t)T + tid; b < nblocks; b += (uint64_t)gridDim.x * T) {
+        if (blockflag[b]) continue;   // non-integer outlier value: the fp64 replay owns it
+        const uint64_t cx = b % nbx, t2 = b / nbx, cy = t2 % nby, cz = t2 / nby;
+        const uint32_t nx = (uint32_t)umin(bx, X - cx * bx), ny = (uint32_t)umin(by, Y - cy * by),
+                       nz = (uint32_t)umin(bz, Z - cz * bz);
+        const uint64_t base = cz * bz * sz + cy * by * sy + cx * bx;
+        int mx = 0, mn = 0;
+        for (uint32_t z = 0; z < nz; z++) {
+            for (uint32_t y = 0; y < ny; y++) {
+                const uint64_t rb = base + z * sz + y * sy;
+                int H = 0;
+                for (uint32_t x = 0; x < nx; x++) {
+                    const uint32_t code = codes[rb + x];
+                    const int Gp = (nd >= 2 && y > 0) ? Gs[(size_t)x * T] : 0;
+                    int* pf = P + (size_t)(y * bx + x) * T;
+                    const int F0 = (nd == 3 && z > 0) ? *pf : 0;
+                    int G, F;
+                    if (code != 0) {
+                        H += (int)code - r;
+                        G = H + Gp;
+                        F = G + F0;
+                    } else {   // outlier: its final value is stored verbatim
+                        const long long v = outlier_int(dense, rb + x);
+                        F = (v < (1ll << 28) && v > -(1ll << 28)) ? (int)v : (1 << 29);
+                        G = F - F0;
+                        H = G - Gp;
+                    }
+                    mx = max(mx, F);
+                    mn = min(mn, F);
+                    if (nd == 3) *pf = F;
+                    if (nd >= 2) Gs[(size_t)x * T] = G;
+                    store_out<OUTK>(out, rb + x, F, two_eb);
+                }
+            }
+        }
+        if (!(mx < (1 << 28) && mn > -(1 << 28))) {   // magnitude guard: the fp64 replay redoes the block
+            blockflag[b] = 1;
+            atomicOr(&st->flags, (unsigned long long)F_OUT_SLOW);
+        }
     }
 }
 
@@ -1049,10 +1124,10 @@ int launch_reconstruct_1d_records(sdqz_ctx* ctx, const uint16_t* codes, const vo
     if (!work) return rc;
     if (out_kind == 0)
         rq_generic_kernel<0><<<(unsigned)gg, 128, 0, ctx->stream>>>(codes, (const unsigned long long*)dense, blockflag, 1,
-                                                                  g, cap, two_eb, work, out, ctx->d_status);
+                                                                  g, cap, two_eb, work, out, ctx->d_status, kSlotPts);
     else
         rq_generic_kernel<1><<<(unsigned)gg, 128, 0, ctx->stream>>>(codes, (const unsigned long long*)dense, blockflag, 1,
-                                                                  g, cap, two_eb, work, out, ctx->d_status);
+                                                                  g, cap, two_eb, work, out, ctx->d_status, kSlotPts);
     SDQZ_LAUNCHED_NAMED(ctx, "rq_generic_kernel");
     return SDQZ_OK;
 }
@@ -1145,23 +1220,48 @@ int launch_reconstruct(sdqz_ctx* ctx, const uint16_t* codes, const uint64_t* den
         else SDQZ_LAUNCHED_NAMED(ctx, vec1d ? "rq1d_vec_kernel" : "rq1d_kernel");
         if (!any_slow) return SDQZ_OK;
     }
+    // generic shapes: thread per block (int32 recurrence) unless the per-thread
+    // slots or the replay slots get too large
+    uint64_t bpts = 1;
+    for (int a = 0; a < ndims; a++) bpts *= block[a];
+    const uint32_t slots = blk_slots(ndims, g.block);
+    const bool blk = !fast && slots <= kBlkMaxSlots && bpts <= 65536 && !env_disabled("SDQZ_NO_BLK");
     uint64_t nblocks = g.nblk[0] * g.nblk[1] * g.nblk[2];
+    if (blk) {
+        const uint32_t T = slots * 4 <= 1024 ? 64 : 32;
+        const size_t dsm = (size_t)T * slots * 4;
+        uint64_t bg = ceil_div(nblocks, T);
+        if (bg > (uint64_t)ctx->num_sms * 64) bg = (uint64_t)ctx->num_sms * 64;
+        if (bg < 1) bg = 1;
+        if (out_kind == 0) {
+            ensure_smem(ctx, (const void*)rq_blocks_kernel<0>, dsm);
+            rq_blocks_kernel<0><<<(unsigned)bg, T, dsm, ctx->stream>>>(codes, dn, const_cast<uint8_t*>(blockflag), g,
+                                                                     cap, two_eb, out, ctx->d_status);
+        } else {
+            ensure_smem(ctx, (const void*)rq_blocks_kernel<1>, dsm);
+            rq_blocks_kernel<1><<<(unsigned)bg, T, dsm, ctx->stream>>>(codes, dn, const_cast<uint8_t*>(blockflag), g,
+                                                                     cap, two_eb, out, ctx->d_status);
+        }
+        SDQZ_LAUNCHED_NAMED(ctx, "rq_blocks_kernel");
+    }
+    const bool only_flagged = fast || blk;
     uint64_t grid = ceil_div(nblocks, 128);
     // flagged-blocks-only replay: usually nothing to do (the kernel exits on
     // the status word), so one CTA per SM bounds the idle launch cost
-    if (fast && grid > (uint64_t)ctx->num_sms) grid = ctx->num_sms;
+    if (only_flagged && grid > (uint64_t)ctx->num_sms) grid = ctx->num_sms;
     if (grid > (uint64_t)max_grid) grid = max_grid;
     if (grid < 1) grid = 1;
-    // whole-field fp64 scratch for generic shapes; per-thread block slots otherwise
-    double* work = scratch_as<double>(ctx, S_WORK, fast ? grid * 128 * kSlotPts : n, &rc);
+    // whole-field fp64 scratch for the all-blocks replay; per-thread block slots otherwise
+    const uint64_t slot_pts = bpts > kSlotPts ? bpts : kSlotPts;
+    double* work = scratch_as<double>(ctx, S_WORK, only_flagged ? grid * 128 * slot_pts : n, &rc);
     if (!work) return rc;
-    int only = fast ? 1 : 0;
+    int only = only_flagged ? 1 : 0;
     if (out_kind == 0)
         rq_generic_kernel<0><<<(unsigned)grid, 128, 0, ctx->stream>>>(codes, dn, blockflag, only, g, cap,
-                                                                    two_eb, work, out, ctx->d_status);
+                                                                    two_eb, work, out, ctx->d_status, slot_pts);
     else
         rq_generic_kernel<1><<<(unsigned)grid, 128, 0, ctx->stream>>>(codes, dn, blockflag, only, g, cap,
-                                                                    two_eb, work, out, ctx->d_status);
+                                                                    two_eb, work, out, ctx->d_status, slot_pts);
     SDQZ_LAUNCHED_NAMED(ctx, "rq_generic_kernel");
     return SDQZ_OK;
 }

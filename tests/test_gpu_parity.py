@@ -656,3 +656,33 @@ class TestHostStaging:
         out = S.decompress(blob)
         err = np.abs(out.astype(np.float64) - f.astype(np.float64)).max()
         assert err <= 1e-3 * (1 + 1e-9) + 2 * np.spacing(np.float32(1.25))
+
+
+class TestGenericShapes:
+    """Non-default block shapes run the thread-per-block kernels
+    (dq_blocks_kernel / rq_blocks_kernel, row f4): archive bytes and
+    decompressed bits equal the oracle's, including partial edge blocks,
+    outliers, the int32 magnitude guard (fp64 replay of the block) and
+    blocks too large for the per-thread slots (generic kernels)."""
+
+    @pytest.mark.parametrize("dims,block", [
+        ((37, 45, 70), (16, 16, 16)), ((37, 45, 70), (4, 4, 4)), ((30, 41, 66), (2, 8, 32)),
+        ((19, 23, 130), (1, 1, 64)), ((33, 40, 50), (5, 3, 7)), ((20, 20, 40), (3, 40, 40)),
+        ((300, 257), (32, 32)), ((300, 257), (4, 64)), ((129, 130), (1, 7)), ((64, 700), (2, 1000)),
+        ((100_003,), (256,)), ((100_003,), (16,)), ((100_003,), (1,)), ((70_001,), (70_000,)),
+    ])
+    def test_shapes(self, dims, block):
+        f = S.generate_field("smooth", dims, seed=len(dims) + block[0]).astype(np.float32)
+        f.reshape(-1)[::97] += np.float32(5.0)          # outliers
+        for kw in (dict(eb=1e-4, mode="valrel"), dict(eb=0.02, mode="abs", cap=64)):
+            blob = S.compress(f, block_shape=block, **kw)
+            assert blob == O.compress(f, block_shape=block, **kw)
+            assert np.array_equal(bits(S.decompress(blob)), bits(O.decompress(blob)))
+
+    def test_guard_and_f64(self):
+        rng = np.random.default_rng(3)
+        f = (rng.normal(0, 1, (24, 24, 24)) * 1e6).astype(np.float64)   # |F| far past 2^28 at eb 1e-3
+        for block in ((6, 6, 6), (12, 2, 3)):
+            blob = S.compress(f, eb=1e-3, mode="abs", block_shape=block)
+            assert blob == O.compress(f, eb=1e-3, mode="abs", block_shape=block)
+            assert np.array_equal(bits(S.decompress(blob)), bits(O.decompress(blob)))
