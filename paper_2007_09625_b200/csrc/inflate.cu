@@ -297,7 +297,7 @@ __global__ void __cluster_dims__(kScanCtas, 1, 1) __launch_bounds__(1024) decode
 constexpr uint32_t kSliceMin = 64;         // bits per lane slice
 template <int NS>
 constexpr uint32_t kSliceMax = NS == 6 ? 160 : 192;   // (NS = 6: short codes, smaller stages)
-constexpr uint32_t kTargetCodes = 56;      // codewords per lane slice (sets S from the chunk's bits/code)
+constexpr uint32_t kTargetCodes = 64;      // codewords per lane slice (sets S from the chunk's bits/code)
 constexpr uint32_t kFinalSlices = 48;      // a round whose rest fits 48 slices of S is the chunk's last
 // u32 words per lane buffer (odd: distinct banks at equal slots)
 template <int NS>
@@ -502,17 +502,26 @@ template <int NS>
 __device__ __forceinline__ void lane_decode(const Dec& d, Cursor& rd, uint32_t A0, uint32_t S, uint32_t buf_s,
                                             uint32_t& P, uint32_t& bad, uint32_t& zf, unsigned long long& lo,
                                             unsigned long long& hi, uint32_t& tl) {
+    static_assert(!kHeadHi, "the split loop below records the low head mask only");
     uint32_t len = 0, mask = 0, p = rd.pos;
     Syms<NS> sv;
     unsigned long long l = 0, h = 0;
+    // the first kHeadBits of the slice record codeword starts; the rest only decodes
+    const uint32_t HB = S - A0 < kHeadBits ? S : A0 + kHeadBits;
+    while (rd.pos < HB) {
+        p = rd.pos;
+        dstep<NS>(d, rd.peek(), len, mask, sv, bad);
+        put<NS>(buf_s, P, sv);
+        zf |= sv.zero();
+        l |= (unsigned long long)mask << (p - A0);
+        P += __popc(mask);
+        rd.adv(len);
+    }
     while (rd.pos < S) {
         p = rd.pos;
         dstep<NS>(d, rd.peek(), len, mask, sv, bad);
         put<NS>(buf_s, P, sv);
         zf |= sv.zero();
-        const uint32_t r = p - A0;
-        if (r < kHeadBits) l |= (unsigned long long)mask << r;
-        if (kHeadHi && r - 52 < 64) h |= (unsigned long long)mask << (r - 52);
         P += __popc(mask);
         rd.adv(len);
     }
