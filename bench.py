@@ -9,9 +9,11 @@ shape (reference metric: "compress & decompress GB/s (fp32 in)").  `value` is
 whole-job fp32-input GB/s with the field resident in HBM (device-timed with
 CUDA events, L2 flushed between steps); `e2e` is the same metric through the
 public API with host buffers (pinned host field -> archive bytes -> host
-field).  Under torchrun each rank processes its own field (weak scaling).
-`--impl reference` times the CPU reference path (the oracle port of the
-reference package, oracle/sdqz_oracle.py) on the host cores.
+field).  Under torchrun (N > 1) the field is split into slabs of whole block
+rows, one per rank, compressed into one sharded archive and decompressed in
+place (strong scaling, paper_2007_09625_b200/sharded.py).  `--impl reference`
+times the CPU reference path (the oracle port of the reference package,
+oracle/sdqz_oracle.py) on the host cores.
 """
 
 from __future__ import annotations
@@ -209,13 +211,17 @@ def reference_arm(args, cfg, world, rank):
     is pure Python + numpy and is not importable on the GPU box)."""
     if rank != 0:
         return 0
-    data, sdims, eb, chunk, desc = cpu_sample(cfg, 2e6)
     cores = os.cpu_count() or 1
     # the reference's `workers` threads only its decode (numpy holds the GIL
-    # elsewhere) and can be slower than one thread: warm up both, time the faster
-    w1 = time_cpu(data, sdims, eb, chunk, 1, steps=max(1, args.warmup // 2))
-    wn = time_cpu(data, sdims, eb, chunk, cores, steps=max(1, args.warmup - args.warmup // 2))
+    # elsewhere) and can be slower than one thread: probe both on a small
+    # sample, then warm up and time the faster on the full ~8 M-point sample
+    # (large enough that per-call fixed costs do not dominate)
+    pdata, psdims, peb, pchunk, _ = cpu_sample(cfg, 1e6)
+    w1 = time_cpu(pdata, psdims, peb, pchunk, 1)
+    wn = time_cpu(pdata, psdims, peb, pchunk, cores)
     workers = cores if wn < w1 else 1
+    data, sdims, eb, chunk, desc = cpu_sample(cfg, 8e6)
+    time_cpu(data, sdims, eb, chunk, workers, steps=max(1, min(args.warmup, 2)))
     dt = time_cpu(data, sdims, eb, chunk, workers, steps=args.steps) * args.steps
     value = 4 * data.size * args.steps / dt / 1e9
     line = {
@@ -227,8 +233,8 @@ def reference_arm(args, cfg, world, rank):
                    "mode": cfg["mode"], "sample_dims": list(sdims)},
         "cpu_baseline": {"value": value, "unit": "GB/s", "cores": workers, "kind": "port",
                          "cpu": cpu_model(), "host_cores": cores, "workers": workers,
-                         "workers_choice": f"faster of workers=1 ({w1:.2f} s/step) and "
-                                           f"workers={cores} ({wn:.2f} s/step) in warm-up",
+                         "workers_choice": f"faster of workers=1 ({w1:.2f} s) and workers={cores} "
+                                           f"({wn:.2f} s) on a 1 M-point probe of the same field",
                          "sample": desc + " (per step)"},
         "e2e": {"value": value, "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }

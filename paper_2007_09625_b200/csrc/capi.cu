@@ -408,11 +408,10 @@ int decompress_core(sdqz_ctx* ctx, const sdqz_header* hdr, const uint8_t* d_bw, 
     BookDev book;
     if ((rc = book_tables(ctx, cap, &book))) return rc;
     uint16_t* codes = scratch_as<uint16_t>(ctx, S_CODES, n + 64, &rc);
-    uint64_t* dense = scratch_as<uint64_t>(ctx, S_DENSE, n, &rc);
     uint64_t nblocks = 1;
     for (int a = 0; a < hdr->ndims; a++) nblocks *= ceil_div(hdr->dims[a], hdr->block[a] ? hdr->block[a] : 1);
     uint8_t* bflag = scratch_as<uint8_t>(ctx, S_BLOCKFLAG, nblocks, &rc);
-    if (!codes || !dense || !bflag) return rc;
+    if (!codes || !bflag) return rc;
     uint32_t safe_block[3];
     for (int a = 0; a < 3; a++) safe_block[a] = hdr->block[a] ? hdr->block[a] : 1;
     auto enqueue = [&]() -> int {
@@ -432,16 +431,18 @@ int decompress_core(sdqz_ctx* ctx, const sdqz_header* hdr, const uint8_t* d_bw, 
         if (chunks_ok && rq1d_records_ok(hdr->ndims, hdr->dims, hdr->block, codes, d_out, d_rec)) {
             // 1D: outlier values straight from the sorted records (no dense scatter)
             return (r2 = launch_reconstruct_1d_records(ctx, codes, d_rec, k, n, cap, 2.0 * hdr->eb_resolved,
-                                                       d_out, hdr->dtype_code, dense, bflag))
+                                                       d_out, hdr->dtype_code, bflag))
                        ? r2
                        : enqueue_status_copy(ctx);
         }
         if ((r2 = launch_outlier_scatter(ctx, d_rec, nullptr, nullptr, k, n, codes, hdr->ndims,
-                                         hdr->dims, safe_block, dense, bflag, true)))
+                                         hdr->dims, safe_block, bflag, true)))
             return r2;
         if (chunks_ok) {
             double two_eb = 2.0 * hdr->eb_resolved;
-            if ((r2 = launch_reconstruct(ctx, codes, dense, bflag, true, hdr->ndims, hdr->dims,
+            OutLookup ol;
+            if ((r2 = launch_outlier_index(ctx, d_rec, nullptr, nullptr, k, n, &ol))) return r2;
+            if ((r2 = launch_reconstruct(ctx, codes, ol, bflag, true, hdr->ndims, hdr->dims,
                                          hdr->block, cap, two_eb, d_out, hdr->dtype_code)))
                 return r2;
         }
@@ -949,17 +950,18 @@ int sdqz_reconstruct(sdqz_ctx* ctx, const void* d_codes, int code_bytes, uint64_
         if ((rc = launch_narrow_codes(ctx, (const uint32_t*)d_codes, n, cap, c16))) return rc;
         codes = c16;
     }
-    uint64_t* dense = scratch_as<uint64_t>(ctx, S_DENSE, n, &rc);
     uint64_t nblocks = 1;
     for (int a = 0; a < ndims; a++) nblocks *= ceil_div(dims[a], block[a]);
     uint8_t* bflag = scratch_as<uint8_t>(ctx, S_BLOCKFLAG, nblocks, &rc);
-    if (!dense || !bflag) return rc;
+    if (!bflag) return rc;
     SDQZ_CUDA(ctx, cudaMemsetAsync(bflag, 0, nblocks, ctx->stream));
     if ((rc = launch_outlier_scatter(ctx, nullptr, d_idx, d_val, k, n, codes, ndims, dims, block,
-                                     dense, bflag, false)))
+                                     bflag, false)))
         return rc;
     if ((rc = launch_count_zero(ctx, codes, n))) return rc;
-    if ((rc = launch_reconstruct(ctx, codes, dense, bflag, true, ndims, dims, block, cap, 2.0 * eb,
+    OutLookup ol;
+    if ((rc = launch_outlier_index(ctx, nullptr, d_idx, d_val, k, n, &ol))) return rc;
+    if ((rc = launch_reconstruct(ctx, codes, ol, bflag, true, ndims, dims, block, cap, 2.0 * eb,
                                  d_out, out_kind)))
         return rc;
     if ((rc = fetch_status(ctx))) return rc;
@@ -1503,9 +1505,8 @@ int sdqz_decompress_slab(sdqz_ctx* ctx, const sdqz_header* hdr, const uint8_t* d
     BookDev book;
     if ((rc = book_tables(ctx, cap, &book))) return rc;
     uint16_t* codes = scratch_as<uint16_t>(ctx, S_CODES, n_range + 64, &rc);
-    uint64_t* dense = scratch_as<uint64_t>(ctx, S_DENSE, n_local, &rc);
     uint8_t* bflag = scratch_as<uint8_t>(ctx, S_BLOCKFLAG, nblocks, &rc);
-    if (!codes || !dense || !bflag) return rc;
+    if (!codes || !bflag) return rc;
     if ((rc = reset_status_eb(ctx, hdr->eb_resolved, true))) return rc;
     SDQZ_CUDA(ctx, cudaMemsetAsync(bflag, 0, nblocks, ctx->stream));
     if ((rc = launch_codebook(ctx, nullptr, const_cast<uint8_t*>(d_bw), cap, book, false, true, true))) return rc;
@@ -1517,9 +1518,11 @@ int sdqz_decompress_slab(sdqz_ctx* ctx, const sdqz_header* hdr, const uint8_t* d
     SDQZ_CUDA(ctx, cudaMemsetAsync(&ctx->d_status->n_zero, 0, sizeof(unsigned long long), ctx->stream));
     if ((rc = launch_count_zero(ctx, codes + lo, n_local))) return rc;
     if ((rc = launch_outlier_scatter(ctx, d_rec, nullptr, nullptr, k, n_local, codes + lo, hdr->ndims, ldims,
-                                     block, dense, bflag, true)))
+                                     block, bflag, true)))
         return rc;
-    if ((rc = launch_reconstruct(ctx, codes + lo, dense, bflag, true, hdr->ndims, ldims, block, cap,
+    OutLookup ol;
+    if ((rc = launch_outlier_index(ctx, d_rec, nullptr, nullptr, k, n_local, &ol))) return rc;
+    if ((rc = launch_reconstruct(ctx, codes + lo, ol, bflag, true, hdr->ndims, ldims, block, cap,
                                  2.0 * hdr->eb_resolved, d_out, hdr->dtype_code)))
         return rc;
     if ((rc = enqueue_status_copy(ctx))) return rc;

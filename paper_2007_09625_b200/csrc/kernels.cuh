@@ -87,20 +87,35 @@ int launch_inflate_fast(sdqz_ctx* ctx, const uint8_t* payload, uint64_t nwords,
 // reconstruct.cu ------------------------------------------------------------
 // Validate outlier records (range, order, code==0) and scatter their fp64
 // bits into `dense` (uint64[n]); flag blocks needing the fp64 path.
+// Outlier records by flat index for the reconstruct kernels (no dense side
+// array): the records are sorted ascending (validated), bucketed by 1024
+// points; a zero code at i binary-searches its bucket's records.
+struct OutLookup {
+    const unsigned long long* idx;     // record j's index at idx[j * stride]
+    const unsigned long long* val;     // its f64 bits at val[j * stride]
+    uint32_t stride;                   // 2: interleaved archive records, 1: separate arrays
+    const unsigned long long* start;   // [ceil(n / 1024) + 1]: first record of each bucket
+    uint64_t k;
+    uint64_t base;                     // added to a query index (a kernel run on a sub-range)
+};
+// builds the bucket table (context scratch) for k records over n points
+int launch_outlier_index(sdqz_ctx* ctx, const void* records, const uint64_t* idx, const double* val,
+                         uint64_t k, uint64_t n, OutLookup* out);
+// record checks (range, order, codes[idx] == 0) and fp64-path block flags
 int launch_outlier_scatter(sdqz_ctx* ctx, const void* records, const uint64_t* idx,
                            const double* val, uint64_t k, uint64_t n, const uint16_t* codes,
                            int ndims, const uint64_t dims[3], const uint32_t block[3],
-                           uint64_t* dense, uint8_t* blockflag, bool check_format);
+                           uint8_t* blockflag, bool check_format);
 bool rq1d_records_ok(int ndims, const uint64_t dims[3], const uint32_t block[3], const void* codes,
                      const void* out, const void* records);
 int launch_reconstruct_1d_records(sdqz_ctx* ctx, const uint16_t* codes, const void* records, uint64_t k,
                                   uint64_t n, uint32_t cap, double two_eb, void* out, int out_kind,
-                                  uint64_t* dense, uint8_t* blockflag);
+                                  uint8_t* blockflag);
 // fixed-order fold of per-CTA quality partials (5 doubles each) into d_out[5]
 int launch_quality_fold(sdqz_ctx* ctx, const double* d_part, uint64_t nparts, double* d_out);
 int launch_quality(sdqz_ctx* ctx, const void* a, int a_dtype, const void* b, int b_dtype, uint64_t n,
                    double* d_part, double* d_out);
-int launch_reconstruct(sdqz_ctx* ctx, const uint16_t* codes, const uint64_t* dense,
+int launch_reconstruct(sdqz_ctx* ctx, const uint16_t* codes, const OutLookup& ol,
                        const uint8_t* blockflag, bool any_slow, int ndims, const uint64_t dims[3],
                        const uint32_t block[3], uint32_t cap, double two_eb, void* out,
                        int out_kind);

@@ -51,7 +51,7 @@ __device__ __forceinline__ uint64_t block_of(const Geo& g, uint64_t idx) {
 __global__ void outlier_scatter_kernel(const unsigned long long* __restrict__ rec,
                                        const uint64_t* __restrict__ idxs, const double* __restrict__ vals,
                                        uint64_t k, uint64_t n, const uint16_t* __restrict__ codes, Geo g,
-                                       unsigned long long* __restrict__ dense, uint8_t* blockflag,
+                                       uint8_t* blockflag,
                                        DevStatus* st, int check_only) {
     // check_only (1D records path): order / range / fp64-path checks; the
     // codes[idx] == 0 check and the outlier values are taken by the
@@ -67,21 +67,11 @@ __global__ void outlier_scatter_kernel(const unsigned long long* __restrict__ re
             if ((long long)idx - (long long)prev <= 0) f |= F_OUT_ORDER;
         }
         if (idx >= n) { f |= F_OUT_RANGE; continue; }
-        if (!check_only) {
-            if (codes[idx] != 0) f |= F_OUT_NONZERO;
-            dense[idx] = vb;
-        }
+        if (!check_only && codes[idx] != 0) f |= F_OUT_NONZERO;
         double v = __longlong_as_double((long long)vb);
         if (!(fabs(v) < kExact && v == floor(v))) {
             blockflag[block_of(g, idx)] = 1;
             f |= F_OUT_SLOW;
-            if (check_only && rec) {   // every record of this 32-point block
-                const uint64_t b = idx >> 5;
-                for (uint64_t q = j; q > 0 && j - q < 32 && (rec[2 * (q - 1)] >> 5) == b; q--)
-                    if (rec[2 * (q - 1)] < n) dense[rec[2 * (q - 1)]] = rec[2 * (q - 1) + 1];
-                for (uint64_t q = j; q < k && q - j < 32 && (rec[2 * q] >> 5) == b; q++)
-                    if (rec[2 * q] < n) dense[rec[2 * q]] = rec[2 * q + 1];
-            }
         }
     }
     if (f) atomicOr(&st->flags, f);
@@ -160,8 +150,28 @@ __device__ void qacc_flush(QAcc& a, const QualArgs& q) {
     }
 }
 
-__device__ __forceinline__ long long outlier_int(const unsigned long long* dense, uint64_t i) {
-    return (long long)__longlong_as_double((long long)dense[i]);
+// f64 bits of the record at flat index i (0 when there is none: only for a
+// corrupt archive, which the record checks reject)
+__device__ __noinline__ unsigned long long out_bits(const OutLookup o, uint64_t i) {
+    i += o.base;
+    const uint64_t b = i >> 10;
+    uint64_t lo = o.start[b], hi = o.start[b + 1];
+    if (hi > o.k) hi = o.k;
+    if (lo > hi) lo = hi;
+    if (hi > lo) {   // first probe where evenly spread records would put i (block corners: exact)
+        const uint64_t m = lo + (((i & 1023) * (hi - lo)) >> 10);
+        const unsigned long long v = o.idx[m * o.stride];
+        if (v == i) return o.val[m * o.stride];
+        if (v < i) lo = m + 1; else hi = m;
+    }
+    while (lo < hi) {
+        const uint64_t mid = (lo + hi) >> 1;
+        if (o.idx[mid * o.stride] < i) lo = mid + 1; else hi = mid;
+    }
+    return (lo < o.k && o.idx[lo * o.stride] == i) ? o.val[lo * o.stride] : 0ull;
+}
+__device__ __forceinline__ long long outlier_int(const OutLookup& o, uint64_t i) {
+    return (long long)__longlong_as_double((long long)out_bits(o, i));
 }
 
 // segmented (width W lanes) inclusive scan + last-outlier correction
@@ -272,7 +282,7 @@ __device__ __forceinline__ void cp_async_wait1() { asm volatile("cp.async.wait_g
 // Shared layouts are [slot][thread] so a warp's accesses are contiguous.
 template <int OUTK>
 __device__ __forceinline__ bool rq3d_block_smem(const uint16_t* __restrict__ codes,
-                                                const unsigned long long* __restrict__ dense,
+                                                const OutLookup ol,
                                                 uint64_t base, uint64_t YX, uint64_t X, int nx, int ny,
                                                 int nz, int r, double two_eb, void* __restrict__ out,
                                                 int4* __restrict__ fp, uint2* __restrict__ cs, bool vec,
@@ -346,7 +356,7 @@ __device__ __forceinline__ bool rq3d_block_smem(const uint16_t* __restrict__ cod
                     F[x] = G[x] + F0[x];
                     if (cw[x] == 0) {   // outlier: its final value is stored verbatim
                         // rows past the field hold a clamped copy of the last row (never stored)
-                        const long long v = outlier_int(dense, (y < ny ? rb : zb + (uint64_t)(ny - 1) * X) + x);
+                        const long long v = outlier_int(ol, (y < ny ? rb : zb + (uint64_t)(ny - 1) * X) + x);
                         F[x] = (v < (1ll << 28) && v > -(1ll << 28)) ? (int)v : (1 << 29);
                         G[x] = F[x] - F0[x];
                         H = G[x] - Gp[x];
@@ -370,7 +380,7 @@ __device__ __forceinline__ bool rq3d_block_smem(const uint16_t* __restrict__ cod
 
 template <int OUTK>
 __global__ void __launch_bounds__(kRqThreads) rq3d_block_kernel(const uint16_t* __restrict__ codes,
-                                                         const unsigned long long* __restrict__ dense,
+                                                         const OutLookup ol,
                                                          uint8_t* __restrict__ blockflag,
                                                          int any_slow, uint64_t Z, uint64_t Y,
                                                          uint64_t X, uint32_t cap, double two_eb,
@@ -393,7 +403,7 @@ __global__ void __launch_bounds__(kRqThreads) rq3d_block_kernel(const uint16_t* 
         // cp.async rows need 8-byte alignment and the last row's 16-byte read
         // inside the code array
         const bool inside = base + (uint64_t)(nz - 1) * YX + (uint64_t)(ny - 1) * X + 8 <= Z * YX;
-        const bool ok = rq3d_block_smem<OUTK>(codes, dense, base, YX, X, nx, ny, nz, r, two_eb, out,
+        const bool ok = rq3d_block_smem<OUTK>(codes, ol, base, YX, X, nx, ny, nz, r, two_eb, out,
                                               s_fp + threadIdx.x, s_cs + threadIdx.x, vec_ok && inside,
                                               vec_out, q, acc);
         if (!ok) {   // magnitude guard: the fp64 replay kernel redoes the block
@@ -407,7 +417,7 @@ __global__ void __launch_bounds__(kRqThreads) rq3d_block_kernel(const uint16_t* 
 
 template <int OUTK>
 __global__ void __launch_bounds__(kThreads) rq2d_kernel(const uint16_t* __restrict__ codes,
-                                                        const unsigned long long* __restrict__ dense,
+                                                        const OutLookup ol,
                                                         const uint8_t* __restrict__ blockflag,
                                                         int any_slow, uint64_t Y, uint64_t X,
                                                         uint32_t cap, double two_eb,
@@ -430,7 +440,7 @@ __global__ void __launch_bounds__(kThreads) rq2d_kernel(const uint16_t* __restri
             uint32_t code = xin ? codes[i] : (uint32_t)r;
             const bool isout = xin && code == 0;
             const int dlt = isout ? 0 : (int)code - r;
-            const long long vout = isout ? outlier_int(dense, i) : 0;
+            const long long vout = isout ? outlier_int(ol, i) : 0;
             const long long fin = row_final<16>(dlt, isout, vout, prev, lane);
             prev = fin;
             if (xin && !skip) store_out<OUTK>(out, i, fin, two_eb);
@@ -448,7 +458,7 @@ __global__ void __launch_bounds__(kThreads) rq2d_kernel(const uint16_t* __restri
 // 2^29 (then |F| < 2^29 + 256 r keeps every result exact; wrapped partial sums
 // cancel).
 template <typename V, int OUTK>
-__device__ __forceinline__ void rq2d_vec_rows(const uint2 (&cw)[16], const unsigned long long* __restrict__ dense,
+__device__ __forceinline__ void rq2d_vec_rows(const uint2 (&cw)[16], const OutLookup ol,
                                               uint64_t X, uint64_t y0, int ny, uint64_t x0, bool xin, bool store,
                                               int r, uint32_t lane, double two_eb, void* __restrict__ out,
                                               const QualArgs& q, QAcc& acc) {
@@ -465,7 +475,7 @@ __device__ __forceinline__ void rq2d_vec_rows(const uint2 (&cw)[16], const unsig
 #pragma unroll
         for (int k = 0; k < 4; k++) {
             if (c[k] == 0) {
-                t = (V)__longlong_as_double((long long)dense[i0 + k]) - K[k];
+                t = (V)__longlong_as_double((long long)out_bits(ol, i0 + k)) - K[k];
                 f = true;
             } else {
                 t += (V)((int)c[k] - r);
@@ -516,7 +526,7 @@ __device__ __forceinline__ void rq2d_vec_rows(const uint2 (&cw)[16], const unsig
 
 template <int OUTK>
 __global__ void __launch_bounds__(kThreads) rq2d_vec_kernel(const uint16_t* __restrict__ codes,
-                                                            const unsigned long long* __restrict__ dense,
+                                                            const OutLookup ol,
                                                             const uint8_t* __restrict__ blockflag,
                                                             int any_slow, uint64_t Y, uint64_t X,
                                                             uint32_t cap, double two_eb,
@@ -548,23 +558,23 @@ __global__ void __launch_bounds__(kThreads) rq2d_vec_kernel(const uint16_t* __re
                 for (int k = 0; k < 4; k++) {
                     const uint32_t cc = (k < 2 ? cw[y].x : cw[y].y) >> (16 * (k & 1)) & 0xFFFFu;
                     if (cc == 0) {
-                        const double v = __longlong_as_double((long long)dense[(y0 + y) * X + x0 + k]);
+                        const double v = __longlong_as_double((long long)out_bits(ol, (y0 + y) * X + x0 + k));
                         big |= !(fabs(v) < 536870912.0);
                     }
                 }
             }
         }
         if (__any_sync(kFull, big))
-            rq2d_vec_rows<long long, OUTK>(cw, dense, X, y0, ny, x0, xin, store, r, lane, two_eb, out, q, acc);
+            rq2d_vec_rows<long long, OUTK>(cw, ol, X, y0, ny, x0, xin, store, r, lane, two_eb, out, q, acc);
         else
-            rq2d_vec_rows<int, OUTK>(cw, dense, X, y0, ny, x0, xin, store, r, lane, two_eb, out, q, acc);
+            rq2d_vec_rows<int, OUTK>(cw, ol, X, y0, ny, x0, xin, store, r, lane, two_eb, out, q, acc);
     }
     if (q.orig) qacc_flush(acc, q);
 }
 
 template <int OUTK>
 __global__ void __launch_bounds__(kThreads) rq1d_kernel(const uint16_t* __restrict__ codes,
-                                                        const unsigned long long* __restrict__ dense,
+                                                        const OutLookup ol,
                                                         const uint8_t* __restrict__ blockflag,
                                                         int any_slow, uint64_t X, uint32_t cap,
                                                         double two_eb, void* __restrict__ out) {
@@ -579,7 +589,7 @@ __global__ void __launch_bounds__(kThreads) rq1d_kernel(const uint16_t* __restri
         uint32_t code = in ? codes[i] : (uint32_t)r;
         const bool isout = in && code == 0;
         const int dlt = isout ? 0 : (int)code - r;
-        const long long vout = isout ? outlier_int(dense, i) : 0;
+        const long long vout = isout ? outlier_int(ol, i) : 0;
         const long long fin = row_final<32>(dlt, isout, vout, 0, lane);
         if (in) store_out<OUTK>(out, i, fin, two_eb);
     }
@@ -656,15 +666,17 @@ __device__ __forceinline__ void rq1d_rec_row(const uint32_t (&c)[4], const V (&v
 }
 
 // start[t] = first record with index >= 1024 t (lower bound; t <= ntask)
-__global__ void task_bounds_kernel(const unsigned long long* __restrict__ rec, uint64_t k, uint64_t ntask,
-                                   unsigned long long* __restrict__ start) {
+// first record of every 1024-point bucket (lower bound of t * 1024 over the
+// record indices idx[j * stride]; bounded whatever the order of a corrupt set)
+__global__ void task_bounds_kernel(const unsigned long long* __restrict__ idx, uint32_t stride, uint64_t k,
+                                   uint64_t ntask, unsigned long long* __restrict__ start) {
     for (uint64_t t = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; t <= ntask;
          t += (uint64_t)gridDim.x * blockDim.x) {
         const unsigned long long key = t * 1024ull;
         uint64_t lo = 0, hi = k;
         while (lo < hi) {
             const uint64_t mid = (lo + hi) >> 1;
-            if (rec[2 * mid] < key) lo = mid + 1; else hi = mid;
+            if (idx[mid * stride] < key) lo = mid + 1; else hi = mid;
         }
         start[t] = lo;
     }
@@ -791,7 +803,7 @@ __global__ void __launch_bounds__(kThreads) rq1d_rec_kernel(const uint16_t* __re
 }
 
 template <typename V, int OUTK>
-__device__ __forceinline__ void rq1d_vec_row(uint2 cw, const unsigned long long* __restrict__ dense,
+__device__ __forceinline__ void rq1d_vec_row(uint2 cw, const OutLookup ol,
                                              uint64_t i0, int r, uint32_t lane, double two_eb,
                                              void* __restrict__ out, bool store) {
     const uint32_t c[4] = {cw.x & 0xFFFFu, cw.x >> 16, cw.y & 0xFFFFu, cw.y >> 16};
@@ -801,7 +813,7 @@ __device__ __forceinline__ void rq1d_vec_row(uint2 cw, const unsigned long long*
 #pragma unroll
     for (int k = 0; k < 4; k++) {
         if (c[k] == 0) {
-            t = (V)__longlong_as_double((long long)dense[i0 + k]);
+            t = (V)__longlong_as_double((long long)out_bits(ol, i0 + k));
             f = true;
         } else {
             t += (V)((int)c[k] - r);
@@ -844,7 +856,7 @@ __device__ __forceinline__ void rq1d_vec_row(uint2 cw, const unsigned long long*
 
 template <int OUTK>
 __global__ void __launch_bounds__(kThreads) rq1d_vec_kernel(const uint16_t* __restrict__ codes,
-                                                            const unsigned long long* __restrict__ dense,
+                                                            const OutLookup ol,
                                                             const uint8_t* __restrict__ blockflag,
                                                             int any_slow, uint64_t ntask, uint32_t cap,
                                                             double two_eb, void* __restrict__ out) {
@@ -867,7 +879,7 @@ __global__ void __launch_bounds__(kThreads) rq1d_vec_kernel(const uint16_t* __re
                 for (int k = 0; k < 4; k++) {
                     const uint32_t cc = k < 2 ? (cw[j].x >> (16 * k)) & 0xFFFFu : (cw[j].y >> (16 * (k - 2))) & 0xFFFFu;
                     if (cc == 0) {
-                        const double v = __longlong_as_double((long long)dense[t0 + j * 128 + lane * 4 + k]);
+                        const double v = __longlong_as_double((long long)out_bits(ol, t0 + j * 128 + lane * 4 + k));
                         big |= !(fabs(v) < 1073741824.0);
                     }
                 }
@@ -878,8 +890,8 @@ __global__ void __launch_bounds__(kThreads) rq1d_vec_kernel(const uint16_t* __re
         for (int j = 0; j < 8; j++) {
             const uint64_t i0 = t0 + j * 128 + lane * 4;
             const bool store = !(any_slow && blockflag[i0 >> 5]);
-            if (wide) rq1d_vec_row<long long, OUTK>(cw[j], dense, i0, r, lane, two_eb, out, store);
-            else rq1d_vec_row<int, OUTK>(cw[j], dense, i0, r, lane, two_eb, out, store);
+            if (wide) rq1d_vec_row<long long, OUTK>(cw[j], ol, i0, r, lane, two_eb, out, store);
+            else rq1d_vec_row<int, OUTK>(cw[j], ol, i0, r, lane, two_eb, out, store);
         }
     }
 }
@@ -888,7 +900,7 @@ __global__ void __launch_bounds__(kThreads) rq1d_vec_kernel(const uint16_t* __re
 // and flagged blocks).  `work` is an fp64 scratch array indexed like the field.
 template <int OUTK>
 __global__ void rq_generic_kernel(const uint16_t* __restrict__ codes,
-                                  const unsigned long long* __restrict__ dense,
+                                  const OutLookup ol,
                                   const uint8_t* __restrict__ blockflag, int only_flagged, Geo g,
                                   uint32_t cap, double two_eb, double* __restrict__ work,
                                   void* __restrict__ out, const DevStatus* st, uint64_t slot_pts) {
@@ -943,7 +955,7 @@ __global__ void rq_generic_kernel(const uint16_t* __restrict__ codes,
                 for (uint64_t c = 0; c < e[2]; c++) {
                     const uint64_t gi = gat(a, bb, c);
                     if (codes[gi] != 0) continue;
-                    double v = __longlong_as_double((long long)dense[gi]);
+                    double v = __longlong_as_double((long long)out_bits(ol, gi));
                     double d = __dsub_rn(v, work[at(a, bb, c)]);
                     for (uint64_t a2 = a; a2 < e[0]; a2++)
                         for (uint64_t b2 = bb; b2 < e[1]; b2++)
@@ -982,7 +994,7 @@ __host__ __device__ __forceinline__ uint32_t blk_slots(int nd, const uint32_t* b
 
 template <int OUTK>
 __global__ void __launch_bounds__(64) rq_blocks_kernel(const uint16_t* __restrict__ codes,
-                                                       const unsigned long long* __restrict__ dense,
+                                                       const OutLookup ol,
                                                        uint8_t* __restrict__ blockflag, Geo g, uint32_t cap,
                                                        double two_eb, void* __restrict__ out, DevStatus* st) {
     extern __shared__ __align__(16) int blk_smem[];
@@ -1018,7 +1030,7 @@ __global__ void __launch_bounds__(64) rq_blocks_kernel(const uint16_t* __restric
                         G = H + Gp;
                         F = G + F0;
                     } else {   // outlier: its final value is stored verbatim
-                        const long long v = outlier_int(dense, rb + x);
+                        const long long v = outlier_int(ol, rb + x);
                         F = (v < (1ll << 28) && v > -(1ll << 28)) ? (int)v : (1 << 29);
                         G = F - F0;
                         H = G - Gp;
@@ -1054,18 +1066,37 @@ Geo make_geo(int ndims, const uint64_t dims[3], const uint32_t block[3]) {
 
 }  // namespace
 
+int launch_outlier_index(sdqz_ctx* ctx, const void* records, const uint64_t* idx, const double* val,
+                         uint64_t k, uint64_t n, OutLookup* out) {
+    int rc = SDQZ_OK;
+    const uint64_t nb = ceil_div(n, 1024);
+    unsigned long long* start = scratch_as<unsigned long long>(ctx, S_DENSE, nb + 1, &rc);
+    if (!start) return rc;
+    const unsigned long long* rec = (const unsigned long long*)records;
+    out->idx = rec ? rec : (const unsigned long long*)idx;
+    out->val = rec ? rec + 1 : (const unsigned long long*)val;
+    out->stride = rec ? 2 : 1;
+    out->start = start;
+    out->k = k;
+    out->base = 0;
+    uint64_t grid = ceil_div(nb + 1, 256);
+    if (grid > (uint64_t)ctx->num_sms * 8) grid = ctx->num_sms * 8;
+    task_bounds_kernel<<<(unsigned)grid, 256, 0, ctx->stream>>>(out->idx, out->stride, k, nb, start);
+    SDQZ_LAUNCHED_NAMED(ctx, "task_bounds_kernel");
+    return SDQZ_OK;
+}
+
 int launch_outlier_scatter(sdqz_ctx* ctx, const void* records, const uint64_t* idx,
                            const double* val, uint64_t k, uint64_t n, const uint16_t* codes,
                            int ndims, const uint64_t dims[3], const uint32_t block[3],
-                           uint64_t* dense, uint8_t* blockflag, bool check_format) {
+                           uint8_t* blockflag, bool check_format) {
     (void)check_format;
     if (k == 0) return SDQZ_OK;
     Geo g = make_geo(ndims, dims, block);
     uint64_t grid = ceil_div(k, 256);
     if (grid > (uint64_t)ctx->num_sms * 8) grid = ctx->num_sms * 8;
     outlier_scatter_kernel<<<(unsigned)grid, 256, 0, ctx->stream>>>(
-        (const unsigned long long*)records, idx, val, k, n, codes, g, (unsigned long long*)dense,
-        blockflag, ctx->d_status, 0);
+        (const unsigned long long*)records, idx, val, k, n, codes, g, blockflag, ctx->d_status, 0);
     SDQZ_LAUNCHED_NAMED(ctx, "outlier_scatter_kernel");
     return SDQZ_OK;
 }
@@ -1080,7 +1111,7 @@ bool rq1d_records_ok(int ndims, const uint64_t dims[3], const uint32_t block[3],
 // per-task record ranges, reconstruct from the records, fp64 replay of flagged blocks
 int launch_reconstruct_1d_records(sdqz_ctx* ctx, const uint16_t* codes, const void* records, uint64_t k,
                                   uint64_t n, uint32_t cap, double two_eb, void* out, int out_kind,
-                                  uint64_t* dense, uint8_t* blockflag) {
+                                  uint8_t* blockflag) {
     int rc = SDQZ_OK;
     const unsigned long long* rec = (const unsigned long long*)records;
     const uint64_t dims[3] = {n, 1, 1};
@@ -1090,18 +1121,14 @@ int launch_reconstruct_1d_records(sdqz_ctx* ctx, const uint16_t* codes, const vo
         uint64_t grid = ceil_div(k, 256);
         if (grid > (uint64_t)ctx->num_sms * 8) grid = ctx->num_sms * 8;
         outlier_scatter_kernel<<<(unsigned)grid, 256, 0, ctx->stream>>>(
-            rec, nullptr, nullptr, k, n, codes, g, (unsigned long long*)dense, blockflag, ctx->d_status, 1);
+            rec, nullptr, nullptr, k, n, codes, g, blockflag, ctx->d_status, 1);
         SDQZ_LAUNCHED_NAMED(ctx, "outlier_check_kernel");
     }
+    // per-task record ranges = the lookup's 1024-point buckets (also serves the fp64 replay)
     const uint64_t ntask = ceil_div(n, 1024);
-    unsigned long long* start = scratch_as<unsigned long long>(ctx, S_OUT_OFF, ntask + 1, &rc);
-    if (!start) return rc;
-    {
-        uint64_t grid = ceil_div(ntask + 1, 256);
-        if (grid > (uint64_t)ctx->num_sms * 8) grid = ctx->num_sms * 8;
-        task_bounds_kernel<<<(unsigned)grid, 256, 0, ctx->stream>>>(rec, k, ntask, start);
-        SDQZ_LAUNCHED_NAMED(ctx, "task_bounds_kernel");
-    }
+    OutLookup ol;
+    if ((rc = launch_outlier_index(ctx, rec, nullptr, nullptr, k, n, &ol))) return rc;
+    const unsigned long long* start = ol.start;
     uint64_t grid = ceil_div(ntask, kWarpsPerCta);
     if (grid > (uint64_t)ctx->num_sms * 8) grid = ctx->num_sms * 8;
     if (grid < 1) grid = 1;
@@ -1123,10 +1150,10 @@ int launch_reconstruct_1d_records(sdqz_ctx* ctx, const uint16_t* codes, const vo
     double* work = scratch_as<double>(ctx, S_WORK, gg * 128 * kSlotPts, &rc);
     if (!work) return rc;
     if (out_kind == 0)
-        rq_generic_kernel<0><<<(unsigned)gg, 128, 0, ctx->stream>>>(codes, (const unsigned long long*)dense, blockflag, 1,
+        rq_generic_kernel<0><<<(unsigned)gg, 128, 0, ctx->stream>>>(codes, ol, blockflag, 1,
                                                                   g, cap, two_eb, work, out, ctx->d_status, kSlotPts);
     else
-        rq_generic_kernel<1><<<(unsigned)gg, 128, 0, ctx->stream>>>(codes, (const unsigned long long*)dense, blockflag, 1,
+        rq_generic_kernel<1><<<(unsigned)gg, 128, 0, ctx->stream>>>(codes, ol, blockflag, 1,
                                                                   g, cap, two_eb, work, out, ctx->d_status, kSlotPts);
     SDQZ_LAUNCHED_NAMED(ctx, "rq_generic_kernel");
     return SDQZ_OK;
@@ -1150,13 +1177,13 @@ int launch_narrow_codes(sdqz_ctx* ctx, const uint32_t* in, uint64_t n, uint32_t 
     return SDQZ_OK;
 }
 
-int launch_reconstruct(sdqz_ctx* ctx, const uint16_t* codes, const uint64_t* dense,
+int launch_reconstruct(sdqz_ctx* ctx, const uint16_t* codes, const OutLookup& ol,
                        const uint8_t* blockflag, bool any_slow, int ndims, const uint64_t dims[3],
                        const uint32_t block[3], uint32_t cap, double two_eb, void* out,
                        int out_kind) {
     int rc = SDQZ_OK;
     Geo g = make_geo(ndims, dims, block);
-    const unsigned long long* dn = (const unsigned long long*)dense;
+    const OutLookup dn = ol;
     uint64_t n = g.dims[0] * g.dims[1] * g.dims[2];
     int max_grid = ctx->num_sms * 8;
     bool fast = is_fast_shape(ndims, block);
@@ -1193,6 +1220,8 @@ int launch_reconstruct(sdqz_ctx* ctx, const uint16_t* codes, const uint64_t* den
             qa = ctx->qual;
             ctx->qual.nparts = ndims == 3 ? bgrid : grid2;
         }
+        OutLookup dn_tail = ol;   // the 1D tail kernel indexes from off1
+        dn_tail.base += off1;
 #define RQ_LAUNCH(K)                                                                                 \
         if (ndims == 3)                                                                              \
             rq3d_block_kernel<K><<<(unsigned)bgrid, 64, 0, ctx->stream>>>(codes, dn, const_cast<uint8_t*>(blockflag), slow, \
@@ -1207,7 +1236,7 @@ int launch_reconstruct(sdqz_ctx* ctx, const uint16_t* codes, const uint64_t* den
             rq1d_vec_kernel<K><<<(unsigned)vgrid, kThreads, 0, ctx->stream>>>(codes, dn, blockflag, slow, \
                                                                              nt1, cap, two_eb, out); \
             if (off1 < dims[0])                                                                      \
-                rq1d_kernel<K><<<1, kThreads, 0, ctx->stream>>>(codes + off1, dn + off1,            \
+                rq1d_kernel<K><<<1, kThreads, 0, ctx->stream>>>(codes + off1, dn_tail,              \
                     blockflag + off1 / 32, slow, dims[0] - off1, cap, two_eb,                        \
                     (char*)out + off1 * (K == 0 ? 4 : 8));                                           \
         } else                                                                                       \

@@ -1,42 +1,3 @@
-# INTEGRATION — using the B200 path from the reference package
-
-The reference `sdqz` is pure Python; its interface for this path is the stage
-functions composed in `sdqz/pipeline.py:15-58`.  Two ways to switch.
-
-## 1. Drop-in import (no reference changes)
-
-`paper_2007_09625_b200` exports the identical public name list as
-`sdqz/__init__.py:10-39` (plus `compress_device` / `decompress_device` /
-`DeviceArchive`), with the same signatures, dtypes, exception classes and message
-substrings, and produces byte-identical archives:
-
-```python
-import paper_2007_09625_b200 as sdqz      # was: import sdqz
-blob = sdqz.compress(field, eb=1e-4, mode="valrel")       # bytes, same as the reference
-out = sdqz.decompress(blob)                                # np.ndarray, archive dtype
-```
-
-`workers=` is accepted and ignored (worker invariance, `SPEC.md:512`).  Inputs may
-also be CUDA tensors; `compress_device` keeps the archive sections in HBM and
-`decompress_device` returns a CUDA tensor.
-
-## 2. Binding the C-ABI from the reference (what a maintainer would add)
-
-`include/sdqz_cuda.h` is the contract; each entry point names the reference
-function it replaces.  The binding below is the whole reference-side change for
-the hot path: a new module `sdqz/_gpu.py` whose `compress` / `decompress`
-replace the bodies of `compress` (`pipeline.py:15-39`) and `decompress`
-(`pipeline.py:56-58`).  It uses the host-buffer entry points
-(`sdqz_compress_host`, `sdqz_archive_write`, `sdqz_decompress_host`), so it needs
-only numpy and ctypes -- no device allocator.  Every entry point gets explicit
-`argtypes` / `restype` (`sdqz_archive_size` returns a `uint64_t`: archives
-above 2 GB must not be truncated to a C `int`).  The file is
-`tests/integration_stub.py` verbatim; `tests/test_integration_stub.py` checks
-that this document still contains it and runs it on a B200 against the oracle
-(byte-identical archives, bit-identical outputs, the reference's exception
-classes).
-
-```python
 # sdqz/_gpu.py -- the binding a maintainer of the reference package would add
 # (INTEGRATION.md §2 shows this file verbatim; tests/test_integration_stub.py
 # runs it).  It binds libsdqz_cuda.so's host-buffer entry points with ctypes:
@@ -117,38 +78,3 @@ def decompress(blob: bytes, workers=None) -> np.ndarray:
     out = np.empty(dims, np.float32 if h.dtype_code == 0 else np.float64)
     _check(_L.sdqz_decompress_host(_ctx, blob, len(blob), out.ctypes.data))
     return out
-```
-
-The stage functions map one-to-one (`sdqz_prequantize` ← `prequantize`
-`dualquant.py:62`, `sdqz_dualquant` ← `compress_field` `:242`, `sdqz_histogram_u32`
-← `histogram` `huffman.py:77`, `sdqz_build_tree` ← `build_tree` `:98`,
-`sdqz_canonize` ← `canonize` `:146`, `sdqz_encode_u32` ← `encode` `:193`,
-`sdqz_deflate_units` ← `deflate` `:219`, `sdqz_inflate` ← `inflate` `:311`,
-`sdqz_reconstruct` ← `reconstruct_field` `dualquant.py:299`, `sdqz_parse_header` ←
-`parse_header` `archive.py:143`, `sdqz_quality` ← `quality` `metrics.py:52`);
-`paper_2007_09625_b200/{dualquant,huffman,metrics}.py` are the worked bindings of each.
-
-Host buffers.  `sdqz_decompress` (archive bytes in) and `sdqz_archive_write`
-(archive bytes out) accept ordinary pageable memory — a Python `bytes` — and
-stage it through a context-owned pinned buffer with a parallel host copy
-(`staged_copy`, `capi.cu`); `sdqz_upload` does the same for a pageable input
-field.  A caller with its own pinned buffers can keep using the device-pointer
-entry points (`sdqz_compress`, `sdqz_decompress_sections`) and copy itself.
-
-## 3. Building
-
-```
-python -c "import __graft_entry__ as g; g.build()"     # make -C paper_2007_09625_b200/csrc
-```
-
-produces `paper_2007_09625_b200/libsdqz_cuda.so` (nvcc 12.9,
-`-gencode arch=compute_100a,code=sm_100a -lineinfo -fmad=false -fopenmp`), linked
-against `libcudart` and `libgomp` (the host-side parallel copy of the staged sections).  The tensor-map encoder is fetched from the driver at run time
-(`cudaGetDriverEntryPoint`), so no `-lcuda` is needed.
-
-## 4. Multiple GPUs
-
-`paper_2007_09625_b200.sharded` runs one process per GPU under
-`torch.distributed` (NCCL): each rank passes its slab of whole block-rows and the
-global dims; rank 0 (or every rank) receives the same archive bytes a single-GPU
-`compress` of the whole field produces.  See DESIGN.md §6.

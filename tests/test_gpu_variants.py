@@ -3,11 +3,13 @@ read once per process, so every case runs in a fresh interpreter that
 compresses / decompresses a few fields through the package and compares
 archive bytes and decompressed bits with the oracle (oracle/sdqz_oracle.py).
 
-  SDQZ_DEC_NS=3     the u64 three-symbol decode table (default: u128, six)
+  SDQZ_DEC_NS=3|6   the u64 three-codeword / u128 six-codeword decode tables
+                    (default: by the stream's mean code length)
   SDQZ_NO_TMA=1     3D dual-quant without the TMA tile pipeline
   SDQZ_NO_VEC1D=1   scalar 1D dual-quant / reconstruct
   SDQZ_NO_VEC2D=1   scalar 2D dual-quant / reconstruct
   SDQZ_NO_GRAPH=1   no CUDA-graph replay of the pipelines
+  SDQZ_NO_BLK=1     generic block shapes on the per-point kernels (not thread-per-block)
 """
 import os
 import subprocess
@@ -36,6 +38,10 @@ fields = [
     (S.generate_field("smooth", (300, 451), seed=5).astype(np.float32), dict(eb=1e-3, mode="valrel")),
     (np.cumsum(rng.normal(0, 1, 200_003)).astype(np.float32), dict(eb=0.01, mode="abs")),
     (rng.normal(0, 3, (17, 33, 65)).astype(np.float32), dict(eb=0.05, mode="abs", chunk_size=333)),
+    (S.generate_field("smooth", (21, 34, 45), seed=6).astype(np.float32),
+     dict(eb=1e-4, mode="valrel", block_shape=(4, 4, 4))),
+    (S.generate_field("smooth", (90, 77), seed=7).astype(np.float32),
+     dict(eb=1e-3, mode="valrel", block_shape=(8, 8))),
 ]
 for f, kw in fields:
     blob = S.compress(f, **kw)
@@ -47,8 +53,8 @@ print("ok", len(fields))
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("env", ["SDQZ_DEC_NS=3", "SDQZ_NO_TMA=1", "SDQZ_NO_VEC1D=1", "SDQZ_NO_VEC2D=1",
-                                 "SDQZ_NO_GRAPH=1"])
+@pytest.mark.parametrize("env", ["SDQZ_DEC_NS=3", "SDQZ_DEC_NS=6", "SDQZ_NO_TMA=1", "SDQZ_NO_VEC1D=1", "SDQZ_NO_VEC2D=1",
+                                 "SDQZ_NO_GRAPH=1", "SDQZ_NO_BLK=1"])
 def test_variant_bit_exact(env):
     k, v = env.split("=")
     e = dict(os.environ, **{k: v})
