@@ -566,6 +566,8 @@ def sharded_arm(args, cfg, world, rank, local_rank):
     launches = ctx.launches - launches0
     c_ms = [a.elapsed_time(b) for a, b, c in ev]
     d_ms = [b.elapsed_time(c) for a, b, c in ev]
+    log(f"rank {rank}: compress ms per step {[round(x, 2) for x in c_ms]}, "
+        f"decompress ms per step {[round(x, 2) for x in d_ms]}")
     tt = torch.tensor([sum(c_ms) + sum(d_ms), statistics.median(c_ms), statistics.median(d_ms)],
                       dtype=torch.float64)
     tt = tt.cuda() if dist.get_backend() == "nccl" else tt
@@ -577,7 +579,12 @@ def sharded_arm(args, cfg, world, rank, local_rank):
     # device -> compress_sharded_device -> ShardedArchive.write (every rank
     # writes its own byte ranges of one archive file) -> decompress_sharded ->
     # host slab
-    path = os.environ.get("SDQZ_BENCH_ARCHIVE", f"/dev/shm/sdqz_bench_{os.getpid() if world == 1 else 'n' + str(world)}.sdqz")
+    import shutil
+    import tempfile
+    # one archive file in RAM-backed /dev/shm when it has room, else the temp dir
+    shm = "/dev/shm" if os.path.isdir("/dev/shm") and shutil.disk_usage("/dev/shm").free > 4 * 4 * n // 10 \
+        else tempfile.gettempdir()
+    path = os.environ.get("SDQZ_BENCH_ARCHIVE", os.path.join(shm, f"sdqz_bench_n{world}.sdqz"))
     host_out = torch.empty(max(n_local, 1), dtype=torch.float32, pin_memory=True)
     e2e_steps = max(2, min(args.steps, 3))
     dist.barrier()

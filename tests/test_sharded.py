@@ -109,9 +109,14 @@ def _free_port():
     return port
 
 
-def _worker(rank, world, port, case, backend, q, tmpdir):
+def _worker(rank, world, port, case, backend, q, tmpdir, pg="gloo"):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
-    dist.init_process_group("gloo", rank=rank, world_size=world)
+    if pg == "nccl":   # the box's backend: collectives on CUDA tensors (one rank per GPU)
+        import torch
+        torch.cuda.set_device(rank)
+        dist.init_process_group("nccl", rank=rank, world_size=world, device_id=torch.device("cuda", rank))
+    else:
+        dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
         ops = OracleShardOps() if backend == "oracle" else None
         data, dims, rows, kw = case
@@ -133,13 +138,13 @@ def _worker(rank, world, port, case, backend, q, tmpdir):
         dist.destroy_process_group()
 
 
-def run_sharded(case, world, backend="oracle"):
+def run_sharded(case, world, backend="oracle", pg="gloo"):
     import tempfile
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
     tmpdir = tempfile.mkdtemp(prefix="sdqz_sharded_")
-    procs = [ctx.Process(target=_worker, args=(r, world, port, case, backend, q, tmpdir))
+    procs = [ctx.Process(target=_worker, args=(r, world, port, case, backend, q, tmpdir, pg))
              for r in range(world)]
     for p in procs:
         p.start()
@@ -259,4 +264,21 @@ def test_sharded_device_cases(name, dims, rows, kw):
     data = _field(name, dims)
     ref = O.compress(data, dims, **kw)
     outs, slabs = run_sharded((data.reshape(-1), dims, rows, kw), len(rows), backend="device")
+    _check(ref, dims, outs, slabs)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("name", ["3d-straddle", "2d-default-chunk", "1d-span3"])
+def test_sharded_nccl_backend(name):
+    """The NCCL code path (collectives on CUDA tensors, as on the multi-GPU box)
+    with one rank per GPU available here: the whole field as one slab."""
+    import torch
+    if not torch.cuda.is_available() or not torch.distributed.is_nccl_available():
+        pytest.skip("needs CUDA + NCCL")
+    world = min(torch.cuda.device_count(), 2)
+    _, dims, rows, kw = next(c for c in CASES if c[0] == name)
+    data = _field(name, dims)
+    ref = O.compress(data, dims, **kw)
+    rows = sharded.slab_rows(dims[0], {1: 32, 2: 16, 3: 8}[len(dims)], world)
+    outs, slabs = run_sharded((data.reshape(-1), dims, rows, kw), world, backend="device", pg="nccl")
     _check(ref, dims, outs, slabs)
