@@ -1288,7 +1288,12 @@ int launch_reconstruct(sdqz_ctx* ctx, const uint16_t* codes, const OutLookup& ol
     if (grid > (uint64_t)max_grid) grid = max_grid;
     if (grid < 1) grid = 1;
     // whole-field fp64 scratch for the all-blocks replay; per-thread block slots otherwise
+    // (at most ~512 MB of slots: fewer replay threads for big blocks)
     const uint64_t slot_pts = bpts > kSlotPts ? bpts : kSlotPts;
+    if (only_flagged) {
+        const uint64_t max_threads = std::max<uint64_t>(128, (512ull << 20) / 8 / slot_pts);
+        if (grid * 128 > max_threads) grid = std::max<uint64_t>(1, max_threads / 128);
+    }
     double* work = scratch_as<double>(ctx, S_WORK, only_flagged ? grid * 128 * slot_pts : n, &rc);
     if (!work) return rc;
     int only = only_flagged ? 1 : 0;
