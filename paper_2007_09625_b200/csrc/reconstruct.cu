@@ -12,13 +12,15 @@
 // the last outlier at or left of it in its segment (ballot + shuffle): O(1)
 // per point, no per-outlier loop, exact in int64.
 //
-// Outlier values are scattered beforehand into a dense fp64 side array at
-// their flat index (only those slots are ever read: code 0 <=> outlier,
-// validated).  A block whose outlier values are not integers below 2^40 (the
-// int64 path would no longer match fp64 rounding) is flagged and redone by a
-// generic kernel that replays the reference's fp64 operation order exactly
-// (cumsum per axis, then per-outlier box corrections in raster order); the
-// generic kernel also serves non-default block shapes.
+// Outlier values come straight from the archive's sorted records: a zero code
+// at flat index i (code 0 <=> outlier, validated) finds its record in the
+// 1024-point bucket i/1024 of a bucket table (OutLookup, one probe where the
+// records are evenly spread, else a short binary search) -- no dense side
+// array.  A block whose outlier values are not integers below 2^40 (the int64
+// path would no longer match fp64 rounding) is flagged and redone by a generic
+// kernel that replays the reference's fp64 operation order exactly (cumsum per
+// axis, then per-outlier box corrections in raster order); non-default block
+// shapes run the thread-per-block rq_blocks_kernel.
 #include "kernels.cuh"
 
 namespace sdqz {
