@@ -35,6 +35,10 @@ def main():
     rt(S.generate_field("smooth", (40, 256), seed=2).astype(np.float32), eb=1e-4, mode="valrel")  # 2D vec
     rt(S.generate_field("smooth", (5000,), seed=3).astype(np.float32), eb=1e-4, mode="valrel")    # 1D vec
     rt(rng.normal(0, 1, (9, 7, 5)).astype(np.float32), eb=0.02, cap=64, block_shape=(4, 3, 2))     # generic
+    rt(S.generate_field("smooth", (20, 33, 40), seed=8).astype(np.float32), eb=1e-4, mode="valrel",
+       block_shape=(16, 16, 16))                                     # dq/rq_blocks, partial blocks
+    rt(S.generate_field("smooth", (50, 70), seed=9).astype(np.float32), eb=1e-3, mode="valrel", block_shape=(8, 8))
+    rt(rng.normal(0, 1, (12, 12, 12)) * 1e6, eb=1e-3, block_shape=(6, 6, 6))                     # int32 guard: fp64 replay
     rt(rng.normal(0, 1, (10, 11, 12)), eb=1e-3, mode="valrel")                                     # f64
     rt(rng.normal(0, 1000, (33, 47)).astype(np.float32), eb=0.01, cap=16)                         # outliers
     fib = [1, 1]
