@@ -619,6 +619,25 @@ class TestLargeChunks:
         assert blob == O.compress(f, **kw)
         assert np.array_equal(bits(S.decompress(blob)), bits(O.decompress(blob)))
 
+    def test_fused_pack_64bit_units(self):
+        """Chunks >= 32768 codes with codewords over 24 bits: the fused 32-bit
+        stats + pack kernel stands down and the 64-bit path (stats, scan, run
+        packer) packs, decided on the device."""
+        rng = np.random.default_rng(11)
+        fib = [1, 1]
+        while len(fib) < 27:
+            fib.append(fib[-1] + fib[-2])
+        res = np.repeat(np.arange(-13, 14), fib)
+        rng.shuffle(res)
+        walk = np.cumsum(np.concatenate([res, res[: 70_000 - res.size]]) if res.size < 70_000 else res)
+        walk = walk.astype(np.float32)
+        for chunk in (32768, 65536):
+            kw = dict(eb=0.5, cap=64, block_shape=(walk.size,), chunk_size=chunk)
+            blob = S.compress(walk, **kw)
+            assert S.parse_header(blob).unit_width == 64
+            assert blob == O.compress(walk, **kw)
+            assert np.array_equal(bits(S.decompress(blob)), bits(O.decompress(blob)))
+
     def test_big_chunk_bitflips(self):
         rng = np.random.default_rng(99)
         f = np.cumsum(rng.normal(0, 1, 200_000)).astype(np.float32)
