@@ -74,6 +74,25 @@ __device__ __forceinline__ double load_q(const void* in, uint64_t i, double two_
     return KIND == 2 ? v : prequant(v, two_eb);
 }
 
+// load_q for one thread (no warp vote): fp32 input by the reciprocal multiply
+// of prequant_int_fast with the same tie window; a value inside it, at or
+// above 2^27 units, or non-finite takes the exact division
+template <int KIND>
+__device__ __forceinline__ double load_q_fast(const void* in, uint64_t i, double two_eb, double rcp, bool& bad) {
+    if (KIND != 0) return load_q<KIND>(in, i, two_eb, bad);
+    const float v = __ldg((const float*)in + i);
+    bad |= !isfinite(v);
+    const double y = __dmul_rn((double)v, rcp);
+    const double ay = fabs(y);
+    if (ay < 134217728.0) {
+        const double t = __dadd_rn(ay, 0.5);
+        const double fl = floor(t);
+        const double fr = __dsub_rn(t, fl);
+        if (fr >= 2.384185791015625e-07 && fr <= 1.0 - 2.384185791015625e-07) return copysign(fl, y);
+    }
+    return prequant((double)v, two_eb);
+}
+
 __device__ __forceinline__ uint32_t code_of_int(int delta, int r) {
     return (delta > -r && delta < r) ? (uint32_t)(delta + r) : 0u;
 }
@@ -1119,6 +1138,7 @@ __global__ void __launch_bounds__(64) dq_blocks_kernel(const void* __restrict__ 
     const uint64_t X = g.dims[nd - 1], Y = nd >= 2 ? g.dims[nd - 2] : 1, Z = nd == 3 ? g.dims[0] : 1;
     const uint32_t bz = nd == 3 ? g.block[0] : 1;
     const double two_eb = st->two_eb;
+    const double rcp = __drcp_rn(two_eb);
     const int r = (int)(cap >> 1);
     bool bad = false;
     uint32_t cnt = 0;
@@ -1132,7 +1152,7 @@ __global__ void __launch_bounds__(64) dq_blocks_kernel(const void* __restrict__ 
                 double a = 0.0, e = 0.0, f = 0.0, gq = 0.0;   // (x-1) neighbours: own row, row y-1, plane z-1, both
                 const uint64_t rb = base + z * sz + y * sy;
                 for (uint32_t x = 0; x < nx; x++) {
-                    const double q = load_q<KIND>(in, rb + x, two_eb, bad);
+                    const double q = load_q_fast<KIND>(in, rb + x, two_eb, rcp, bad);
                     const double bb = (nd >= 2 && y > 0) ? R[(size_t)x * T] : 0.0;
                     const double cc = (nd == 3 && z > 0) ? P[(size_t)(y * bx + x) * T] : 0.0;
                     const double dd = (nd == 3 && z > 0 && y > 0) ? P[(size_t)((y - 1) * bx + x) * T] : 0.0;
@@ -1166,6 +1186,88 @@ __global__ void __launch_bounds__(64) dq_blocks_kernel(const void* __restrict__ 
             }
             if (nd == 3)
                 for (uint32_t x = 0; x < nx; x++) P[(size_t)((ny - 1) * bx + x) * T] = R[(size_t)x * T];
+        }
+    }
+    hist_flush_thread(h);
+    if (bad) atomicOr(&st->flags, (unsigned long long)F_NONFINITE);
+    hist_finish(h);
+}
+
+// Generic block shapes, one thread per block-row segment (3D/2D: the x-extent
+// of one block in one row; 1D: one point): every neighbour the reference's
+// prediction reads is prequantized again by this thread (x-1 values carried
+// along the row), so each segment is independent -- millions of threads and
+// coalesced row reads where dq_blocks_kernel has one sequential thread per
+// block.  Same fp64 expression and term order (dualquant.py:81-129).
+template <int KIND>
+__global__ void __launch_bounds__(256) dq_rows_kernel(const void* __restrict__ in, Geo g, uint64_t nitems,
+                                                      uint32_t cap, DevStatus* st, uint16_t* __restrict__ codes,
+                                                      unsigned long long* ghist) {
+    extern __shared__ __align__(128) unsigned char rsm[];
+    HistCtx h;
+    hist_init(h, reinterpret_cast<uint32_t*>(rsm), ghist, cap);
+    const int nd = g.nd;
+    const uint32_t bx = g.block[nd - 1], by = nd >= 2 ? g.block[nd - 2] : 1, bz = nd == 3 ? g.block[0] : 1;
+    const uint64_t X = g.dims[nd - 1], Y = nd >= 2 ? g.dims[nd - 2] : 1;
+    const uint64_t nbx = g.nblk[nd - 1];
+    const uint64_t sy = nd >= 2 ? g.stride[nd - 2] : 0, sz = nd == 3 ? g.stride[0] : 0;
+    const double two_eb = st->two_eb;
+    const double rcp = __drcp_rn(two_eb);
+    const int r = (int)(cap >> 1);
+    bool bad = false;
+    uint32_t cnt = 0;
+    auto emit = [&](uint64_t i, double delta) {
+        const uint32_t code = code_of_f64(delta, r);
+        codes[i] = (uint16_t)code;
+        hist_add(h, code);
+        if (++cnt == 200) {   // 8-bit packed counters
+            hist_flush_thread(h);
+            cnt = 0;
+        }
+    };
+    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+    if (nd == 1) {   // point it; its left neighbour unless it starts a block (position kept incrementally)
+        uint64_t it = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+        uint64_t pos = it % bx;
+        const uint64_t step = stride % bx;
+        for (; it < nitems; it += stride) {
+            const double q = load_q_fast<KIND>(in, it, two_eb, rcp, bad);
+            const double a = pos ? load_q_fast<KIND>(in, it - 1, two_eb, rcp, bad) : 0.0;
+            emit(it, __dsub_rn(q, a));
+            pos += step;
+            if (pos >= bx) pos -= bx;
+        }
+    }
+    for (uint64_t it = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; nd > 1 && it < nitems; it += stride) {
+        const uint64_t cx = it % nbx, row = it / nbx;
+        const uint64_t y = row % Y, z = row / Y;
+        const bool hy = (y % by) != 0, hz = nd == 3 && (z % bz) != 0;   // neighbours inside the block
+        const uint64_t x0 = cx * bx;
+        const uint32_t nx = (uint32_t)umin(bx, X - x0);
+        const uint64_t rb = z * sz + y * sy + x0;
+        double a = 0.0, e = 0.0, f = 0.0, gq = 0.0;   // (x-1): own row, row y-1, plane z-1, both
+        for (uint32_t x = 0; x < nx; x++) {
+            const uint64_t i = rb + x;
+            const double q = load_q_fast<KIND>(in, i, two_eb, rcp, bad);
+            const double bb = hy ? load_q_fast<KIND>(in, i - sy, two_eb, rcp, bad) : 0.0;
+            double pred;
+            if (nd == 2) {
+                pred = __dsub_rn(__dadd_rn(bb, a), e);
+            } else {
+                const double cc = hz ? load_q_fast<KIND>(in, i - sz, two_eb, rcp, bad) : 0.0;
+                const double dd = (hy && hz) ? load_q_fast<KIND>(in, i - sz - sy, two_eb, rcp, bad) : 0.0;
+                pred = __dadd_rn(cc, bb);
+                pred = __dadd_rn(pred, a);
+                pred = __dsub_rn(pred, dd);
+                pred = __dsub_rn(pred, f);
+                pred = __dsub_rn(pred, e);
+                pred = __dadd_rn(pred, gq);
+                f = cc;
+                gq = dd;
+            }
+            emit(i, __dsub_rn(q, pred));
+            a = q;
+            e = bb;
         }
     }
     hist_flush_thread(h);
@@ -1291,6 +1393,23 @@ int launch_kind(sdqz_ctx* ctx, const void* d_in, int ndims, const uint64_t dims[
         g.stride[ndims - 1] = 1;
         for (int a = ndims - 2; a >= 0; a--) g.stride[a] = g.stride[a + 1] * dims[a + 1];
         const uint32_t slots = blk_slots(ndims, block);
+        const uint64_t nblocks_all = g.nblk[0] * g.nblk[1] * g.nblk[2];
+        // few large blocks: thread per block-row segment (parallel, coalesced);
+        // many small ones: thread per block (each point prequantized once)
+        const char* rows_env = getenv("SDQZ_DQ_ROWS");
+        const bool rows = rows_env ? rows_env[0] == '1'
+                                   : (ndims == 1 ? block[0] >= 32 : nblocks_all < (uint64_t)ctx->num_sms * 2048);
+        if (rows && !env_disabled("SDQZ_NO_BLK")) {
+            ensure_smem(ctx, (const void*)dq_rows_kernel<KIND>, smem);
+            const uint64_t nitems = ndims == 1 ? dims[0] : (n / dims[ndims - 1]) * g.nblk[ndims - 1];
+            uint64_t grid = ceil_div(nitems, 256);
+            if (grid > (uint64_t)ctx->num_sms * 16) grid = (uint64_t)ctx->num_sms * 16;
+            if (grid < 1) grid = 1;
+            dq_rows_kernel<KIND><<<(unsigned)grid, 256, smem, ctx->stream>>>(d_in, g, nitems, cap, ctx->d_status,
+                                                                            d_codes, d_hist);
+            SDQZ_LAUNCHED_NAMED(ctx, "dq_rows_kernel");
+            return SDQZ_OK;
+        }
         if (slots <= kBlkMaxSlots && !env_disabled("SDQZ_NO_BLK")) {
             // thread per block; 64 threads per CTA while the slots stay <= 1 KB per thread
             const uint32_t T = slots * 8 <= 1024 ? 64 : 32;

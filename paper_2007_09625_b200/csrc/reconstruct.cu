@@ -1059,6 +1059,54 @@ __global__ void __launch_bounds__(64) rq_blocks_kernel(const uint16_t* __restric
     }
 }
 
+// 1D generic block length bx >= 32: a warp per task of whole blocks (>= 1024
+// points), lane = point, 32 points per step.  The reconstruct is the linear
+// recurrence F_i = a_i F_{i-1} + b_i with (a, b) = (1, delta) for an in-cap
+// code, (0, delta) at a block start, (0, v) at an outlier -- an inclusive warp
+// scan of (a, b) pairs plus the previous step's F as carry, exact in int64.
+// Blocks whose outlier values are not integers below 2^40 are flagged by the
+// scatter and rewritten afterwards by the fp64 replay.
+template <int OUTK>
+__global__ void __launch_bounds__(256) rq1d_seg_kernel(const uint16_t* __restrict__ codes, const OutLookup ol,
+                                                       uint64_t n, uint32_t bx, uint64_t task, uint32_t cap,
+                                                       double two_eb, void* __restrict__ out) {
+    const uint32_t lane = lane_id();
+    const int r = (int)(cap >> 1);
+    const uint64_t ntask = ceil_div(n, task);
+    const uint32_t step = 32 % bx;
+    for (uint64_t t = blockIdx.x * (uint64_t)(blockDim.x >> 5) + (threadIdx.x >> 5); t < ntask;
+         t += (uint64_t)gridDim.x * (blockDim.x >> 5)) {
+        const uint64_t t0 = t * task, t1 = umin(t0 + task, n);
+        long long carry = 0;
+        uint32_t pos = lane % bx;
+        for (uint64_t i0 = t0; i0 < t1; i0 += 32) {
+            const uint64_t i = i0 + lane;
+            const bool in = i < t1;
+            const uint32_t code = in ? codes[i] : (uint32_t)r;
+            bool a = pos != 0;
+            long long b = (long long)code - r;
+            if (code == 0) {
+                a = false;
+                b = (long long)__longlong_as_double((long long)out_bits(ol, i));
+            }
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const bool ap = __shfl_up_sync(kFull, a, o);
+                const long long bp = __shfl_up_sync(kFull, b, o);
+                if (lane >= (uint32_t)o) {
+                    if (a) b += bp;
+                    a = a && ap;
+                }
+            }
+            const long long F = a ? carry + b : b;
+            if (in) store_out<OUTK>(out, i, F, two_eb);
+            carry = __shfl_sync(kFull, F, 31);
+            pos += step;
+            if (pos >= bx) pos -= bx;
+        }
+    }
+}
+
 Geo make_geo(int ndims, const uint64_t dims[3], const uint32_t block[3]) {
     Geo g{};
     g.nd = ndims;
@@ -1265,7 +1313,17 @@ int launch_reconstruct(sdqz_ctx* ctx, const uint16_t* codes, const OutLookup& ol
     const uint32_t slots = blk_slots(ndims, g.block);
     const bool blk = !fast && slots <= kBlkMaxSlots && bpts <= 65536 && !env_disabled("SDQZ_NO_BLK");
     uint64_t nblocks = g.nblk[0] * g.nblk[1] * g.nblk[2];
-    if (blk) {
+    if (blk && ndims == 1 && block[0] >= 32) {   // long 1D blocks: warp-wide scans over tasks of whole blocks
+        const uint64_t task = (uint64_t)block[0] * ceil_div(1024, block[0]);
+        uint64_t bg = ceil_div(ceil_div(n, task), 8);
+        if (bg > (uint64_t)ctx->num_sms * 16) bg = (uint64_t)ctx->num_sms * 16;
+        if (bg < 1) bg = 1;
+        if (out_kind == 0)
+            rq1d_seg_kernel<0><<<(unsigned)bg, 256, 0, ctx->stream>>>(codes, dn, n, block[0], task, cap, two_eb, out);
+        else
+            rq1d_seg_kernel<1><<<(unsigned)bg, 256, 0, ctx->stream>>>(codes, dn, n, block[0], task, cap, two_eb, out);
+        SDQZ_LAUNCHED_NAMED(ctx, "rq1d_seg_kernel");
+    } else if (blk) {
         const uint32_t T = slots * 4 <= 1024 ? 64 : 32;
         const size_t dsm = (size_t)T * slots * 4;
         uint64_t bg = ceil_div(nblocks, T);

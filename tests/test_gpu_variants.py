@@ -10,6 +10,7 @@ archive bytes and decompressed bits with the oracle (oracle/sdqz_oracle.py).
   SDQZ_NO_VEC2D=1   scalar 2D dual-quant / reconstruct
   SDQZ_NO_GRAPH=1   no CUDA-graph replay of the pipelines
   SDQZ_NO_BLK=1     generic block shapes on the per-point kernels (not thread-per-block)
+  SDQZ_DQ_ROWS=0|1  generic-shape dual-quant thread per block / per block-row segment
 """
 import os
 import subprocess
@@ -54,7 +55,7 @@ print("ok", len(fields))
 
 @pytest.mark.gpu
 @pytest.mark.parametrize("env", ["SDQZ_DEC_NS=3", "SDQZ_DEC_NS=6", "SDQZ_NO_TMA=1", "SDQZ_NO_VEC1D=1", "SDQZ_NO_VEC2D=1",
-                                 "SDQZ_NO_GRAPH=1", "SDQZ_NO_BLK=1"])
+                                 "SDQZ_NO_GRAPH=1", "SDQZ_NO_BLK=1", "SDQZ_DQ_ROWS=0", "SDQZ_DQ_ROWS=1"])
 def test_variant_bit_exact(env):
     k, v = env.split("=")
     e = dict(os.environ, **{k: v})
