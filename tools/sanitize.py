@@ -39,6 +39,10 @@ def main():
        block_shape=(16, 16, 16))                                     # dq/rq_blocks, partial blocks
     rt(S.generate_field("smooth", (50, 70), seed=9).astype(np.float32), eb=1e-3, mode="valrel", block_shape=(8, 8))
     rt(rng.normal(0, 1, (12, 12, 12)) * 1e6, eb=1e-3, block_shape=(6, 6, 6))                     # int32 guard: fp64 replay
+    rt(S.generate_field("smooth", (20_001,), seed=10).astype(np.float32), eb=1e-4, mode="valrel",
+       block_shape=(64,))                                            # dq_rows (1D), rq1d_seg
+    rt(S.generate_field("smooth", (200, 300), seed=11).astype(np.float32), eb=1e-4, mode="valrel",
+       block_shape=(2, 2))                                           # dq_blocks (many small blocks)
     rt(rng.normal(0, 1, (10, 11, 12)), eb=1e-3, mode="valrel")                                     # f64
     rt(rng.normal(0, 1000, (33, 47)).astype(np.float32), eb=0.01, cap=16)                         # outliers
     fib = [1, 1]
