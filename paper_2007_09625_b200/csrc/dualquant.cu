@@ -21,6 +21,7 @@
 // counters (two u64 per thread, flushed per task with __reduce_add_sync);
 // codes outside that window use shared-memory atomics; each CTA merges its
 // shared histogram into the global uint64 histogram once.
+#include <type_traits>
 #include "kernels.cuh"
 #include "tma.cuh"
 
@@ -1275,6 +1276,204 @@ __global__ void __launch_bounds__(256) dq_rows_kernel(const void* __restrict__ i
     hist_finish(h);
 }
 
+// prequantized value of an already loaded input element (load_q_fast without the load)
+template <int KIND>
+__device__ __forceinline__ double q_of(typename std::conditional<KIND == 0, float, double>::type v, double two_eb,
+                                       double rcp, bool& bad) {
+    bad |= !isfinite(v);
+    if (KIND == 2) return v;
+    if (KIND == 0) {
+        const double y = __dmul_rn((double)v, rcp);
+        const double ay = fabs(y);
+        if (ay < 134217728.0) {
+            const double t = __dadd_rn(ay, 0.5);
+            const double fl = floor(t);
+            const double fr = __dsub_rn(t, fl);
+            if (fr >= 2.384185791015625e-07 && fr <= 1.0 - 2.384185791015625e-07) return copysign(fl, y);
+        }
+    }
+    return prequant((double)v, two_eb);
+}
+
+// dq_strip_kernel's Lorenzo prediction of the point with prequantized value q
+// (T = int when every value is below 2^27, else double): row y-1 / plane z-1
+// from the lane-private slots (which it then updates), x-1 from the lane to the
+// left or the carried lane 31 of the previous segment.  Term order of
+// dualquant.py:81-129.
+template <typename T, bool ONE>
+__device__ __forceinline__ T strip_pred(int nd, T q, double* R, double* D, double* P, uint32_t s, uint32_t y,
+                                        uint32_t z, uint32_t steps, bool seg0, uint32_t lane, T& cq, T& cb, T& ccq,
+                                        T& cdq) {
+    T* Rs = reinterpret_cast<T*>(R + s * 32);
+    const T bb = y > 0 ? *Rs : T(0);
+    T cc = T(0), dd = T(0);
+    if (nd == 3) {
+        T* pp = reinterpret_cast<T*>(P + (size_t)(y * steps + s) * 32);
+        T* Ds = reinterpret_cast<T*>(D + s * 32);
+        if (z > 0) {
+            cc = *pp;
+            dd = y > 0 ? *Ds : T(0);
+        }
+        *Ds = cc;   // row y of plane z-1, for row y+1
+        *pp = q;
+    }
+    *Rs = q;
+    T a = __shfl_up_sync(kFull, q, 1), e = __shfl_up_sync(kFull, bb, 1), f = T(0), gq = T(0);
+    if (nd == 3) {
+        f = __shfl_up_sync(kFull, cc, 1);
+        gq = __shfl_up_sync(kFull, dd, 1);
+    }
+    if (!ONE) {
+        if (lane == 0) { a = cq; e = cb; f = ccq; gq = cdq; }
+        cq = __shfl_sync(kFull, q, 31);
+        cb = __shfl_sync(kFull, bb, 31);
+        if (nd == 3) {
+            ccq = __shfl_sync(kFull, cc, 31);
+            cdq = __shfl_sync(kFull, dd, 31);
+        }
+    }
+    if (ONE ? seg0 : (seg0 && s == 0)) a = e = f = gq = T(0);
+    if constexpr (sizeof(T) == 4) {
+        return nd == 2 ? bb + a - e : cc + bb + a - dd - f - e + gq;
+    } else {
+        if (nd == 2) return __dsub_rn(__dadd_rn(bb, a), e);
+        T p = __dadd_rn(cc, bb);
+        p = __dadd_rn(p, a);
+        p = __dsub_rn(p, dd);
+        p = __dsub_rn(p, f);
+        p = __dsub_rn(p, e);
+        return __dadd_rn(p, gq);
+    }
+}
+
+constexpr int kStripPf = 16;  // strip-kernel rows in flight (cp.async ring slots) per warp
+
+// 2D / 3D generic block shapes, warp per strip of block columns (the layout
+// of rq_rows_kernel): 32 / bx whole blocks side by side when bx <= 32 (ONE),
+// one block in `steps` 32-lane segments otherwise, over nyb block rows;
+// lane = column, rows in sequence.  Each point is loaded and prequantized
+// once: the x-1 neighbours come from the lane to the left (shuffle; the
+// previous segment's lane 31 across segments), row y-1 and plane z-1 from
+// lane-private shared-memory slots.  Same fp64 expression and term order as
+// dq_blocks_kernel (dualquant.py:81-129).
+template <int KIND, bool ONE>
+__global__ void __launch_bounds__(256) dq_strip_kernel(const void* __restrict__ in, Geo g, uint32_t W,
+                                                       uint32_t steps, uint32_t nyb, uint32_t cap,
+                                                       uint32_t hist_bytes, DevStatus* st,
+                                                       uint16_t* __restrict__ codes,
+                                                       unsigned long long* ghist) {
+    using raw_t = typename std::conditional<KIND == 0, float, double>::type;
+    extern __shared__ __align__(128) unsigned char ssm[];
+    HistCtx h;
+    hist_init(h, reinterpret_cast<uint32_t*>(ssm), ghist, cap);
+    const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int nd = g.nd;
+    const uint32_t bx = g.block[nd - 1], by = g.block[nd - 2], bz = nd == 3 ? g.block[0] : 1;
+    const uint32_t per_warp = steps * (nd == 3 ? 2 + by : 1) * 32;
+    double* R = reinterpret_cast<double*>(ssm + hist_bytes) + warp * per_warp + lane;   // [steps]: q of row y-1
+    double* D = R + steps * 32;                 // [steps]: q of row y-1 in plane z-1 (3D)
+    double* P = D + steps * 32;                 // [by][steps]: q of plane z-1 (3D)
+    const raw_t* ring = reinterpret_cast<const raw_t*>(ssm + hist_bytes + (size_t)(blockDim.x >> 5) * per_warp * sizeof(double)) +
+                        warp * kStripPf * 32 + lane;   // [kStripPf][32] loads in flight
+    const uint32_t ring_s = (uint32_t)__cvta_generic_to_shared(ring);
+    const uint64_t X = g.dims[nd - 1], Y = g.dims[nd - 2], Z = nd == 3 ? g.dims[0] : 1;
+    const uint64_t sy = g.stride[nd - 2], sz = nd == 3 ? g.stride[0] : 0;
+    const uint64_t nby = g.nblk[nd - 2], nbz = nd == 3 ? g.nblk[0] : 1;
+    const uint64_t ntx = ceil_div(X, W), nyg = ceil_div(nby, nyb), ntask = ntx * nyg * nbz;
+    const double two_eb = st->two_eb;
+    const double rcp = __drcp_rn(two_eb);
+    const int r = (int)(cap >> 1);
+    const bool seg0 = ONE ? lane % bx == 0 : lane == 0;
+    // int32 path: the field's described range bounds every |q| below 2^27
+    // (abs-mode calls skip the describe: fp64 path)
+    bool ip = false;
+    if (KIND != 2 && st->vmin_bits <= st->vmax_bits && !(st->flags & F_NONFINITE)) {
+        const double lo = KIND == 0 ? (double)ord2f((uint32_t)st->vmin_bits) : ord2d(st->vmin_bits);
+        const double hi = KIND == 0 ? (double)ord2f((uint32_t)st->vmax_bits) : ord2d(st->vmax_bits);
+        ip = fmax(fabs(lo), fabs(hi)) * rcp < 134217724.0;
+    }
+    bool bad = false;
+    uint32_t cnt = 0;
+    for (uint64_t t = blockIdx.x * (uint64_t)(blockDim.x >> 5) + warp; t < ntask;
+         t += (uint64_t)gridDim.x * (blockDim.x >> 5)) {
+        const uint64_t tx = t % ntx, t2 = t / ntx, cyg = t2 % nyg, cz = t2 / nyg;
+        const uint64_t x0 = tx * W;
+        const uint32_t lim = (uint32_t)umin(W, X - x0);
+        const uint32_t nz = (uint32_t)umin(bz, Z - cz * bz);
+        const uint64_t cy1 = umin(cyg * nyb + nyb, nby);
+        for (uint64_t cy = cyg * nyb; cy < cy1; cy++) {
+            const uint32_t ny = (uint32_t)umin(by, Y - cy * by);
+            const uint32_t nit = nz * ny * steps;
+            const uint64_t base = cz * bz * sz + cy * by * sy + x0;
+            const uint64_t zjump = sz - (uint64_t)(ny - 1) * sy;
+            uint64_t lrow = base, prow = base;
+            uint32_t ls = 0, ly = 0, lit = 0, ps = 0, py = 0, pz = 0;
+            double cd4[4] = {0.0, 0.0, 0.0, 0.0};   // previous segment's lane 31 (q, bb, cc, dd)
+            int ci[4] = {0, 0, 0, 0};
+            // cp.async ring: iteration lit's element lands in slot lit % kStripPf
+            auto issue = [&]() {
+                if (lit < nit) {
+                    const uint32_t c = ONE ? lane : ls * 32 + lane;
+                    const raw_t* src = (const raw_t*)in + lrow + (c < lim ? c : 0);
+                    const uint32_t dst = ring_s + ((lit % kStripPf) * 32) * (uint32_t)sizeof(raw_t);
+                    if (sizeof(raw_t) == 4)
+                        asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;" ::"r"(dst), "l"(src),
+                                     "r"(c < lim ? 4 : 0) : "memory");
+                    else
+                        asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;" ::"r"(dst), "l"(src),
+                                     "r"(c < lim ? 8 : 0) : "memory");
+                    if (ONE || ++ls == steps) {
+                        ls = 0;
+                        if (++ly == ny) { ly = 0; lrow += zjump; } else lrow += sy;
+                    }
+                }
+                asm volatile("cp.async.commit_group;" ::: "memory");
+                lit++;
+            };
+#pragma unroll 1
+            for (int j = 0; j < kStripPf; j++) issue();
+#pragma unroll 1
+            for (uint32_t it = 0; it < nit; it++) {
+                asm volatile("cp.async.wait_group %0;" ::"n"(kStripPf - 1) : "memory");
+                const raw_t raw = ring[(it % kStripPf) * 32];
+                {
+                    const uint32_t s = ONE ? 0 : ps, y = py, z = pz;
+                    const uint64_t rb = prow;
+                    if (ONE || ++ps == steps) {
+                        ps = 0;
+                        if (++py == ny) { py = 0; pz++; prow += zjump; } else prow += sy;
+                    }
+                    const uint32_t c = s * 32 + lane;
+                    const bool valid = c < lim;
+                    const double q = valid ? q_of<KIND>(raw, two_eb, rcp, bad) : 0.0;
+                    issue();   // iteration it + kStripPf into the slot just consumed
+                    uint32_t code;
+                    if (ip) {   // every |q| < 2^27: the fp64 sums below are exact, so int32 gives the same
+                        const int qi = (int)q;
+                        code = code_of_int(qi - strip_pred<int, ONE>(nd, qi, R, D, P, s, y, z, steps, seg0, lane,
+                                                                     ci[0], ci[1], ci[2], ci[3]), r);
+                    } else {
+                        code = code_of_f64(__dsub_rn(q, strip_pred<double, ONE>(nd, q, R, D, P, s, y, z, steps, seg0,
+                                                                                 lane, cd4[0], cd4[1], cd4[2], cd4[3])), r);
+                    }
+                    if (valid) {
+                        codes[rb + c] = (uint16_t)code;
+                        hist_add(h, code);
+                    }
+                    if (++cnt == 200) {   // 8-bit packed counters (warp-uniform count)
+                        hist_flush(h);
+                        cnt = 0;
+                    }
+                }
+            }
+            asm volatile("cp.async.wait_all;" ::: "memory");
+        }
+    }
+    hist_flush(h);
+    if (bad) atomicOr(&st->flags, (unsigned long long)F_NONFINITE);
+    hist_finish(h);
+}
+
 __global__ void prequantize_kernel(const void* __restrict__ in, int dtype, uint64_t n,
                                    const DevStatus* st, double* __restrict__ out) {
     const double two_eb = st->two_eb;
@@ -1399,6 +1598,35 @@ int launch_kind(sdqz_ctx* ctx, const void* d_in, int ndims, const uint64_t dims[
         const char* rows_env = getenv("SDQZ_DQ_ROWS");
         const bool rows = rows_env ? rows_env[0] == '1'
                                    : (ndims == 1 ? block[0] >= 32 : nblocks_all < (uint64_t)ctx->num_sms * 2048);
+        // 2D / 3D blocks of >= 128 points: warp per strip of block columns
+        // (lane-private slots <= 12 KB a warp)
+        uint64_t bpts = 1;
+        for (int a = 0; a < ndims; a++) bpts *= block[a];
+        const uint32_t bxx = block[ndims - 1];
+        const uint32_t rw = bxx <= 32 ? (32 / bxx) * bxx : bxx, rsteps = (rw + 31) / 32;
+        const uint64_t per_warp = (uint64_t)rsteps * (ndims == 3 ? 2 + block[ndims - 2] : 1);
+        const char* strip_env = getenv("SDQZ_STRIP");
+        const bool strip = ndims >= 2 && per_warp <= 48 && !env_disabled("SDQZ_NO_BLK") &&
+                           (strip_env ? strip_env[0] == '1' : bpts >= 128);
+        if (strip) {
+            const uint64_t iters = (uint64_t)rsteps * block[ndims - 2] * (ndims == 3 ? block[0] : 1);
+            const uint32_t nyb = iters >= 32 ? 1 : (uint32_t)ceil_div(32, iters);
+            const uint64_t ntask = ceil_div(dims[ndims - 1], rw) * ceil_div(g.nblk[ndims - 2], nyb) *
+                                   (ndims == 3 ? g.nblk[0] : 1);
+            uint64_t grid = ceil_div(ntask, 8);
+            if (grid > (uint64_t)ctx->num_sms * 8) grid = (uint64_t)ctx->num_sms * 8;
+            if (grid < 1) grid = 1;
+            const uint32_t hist_bytes = (uint32_t)((smem + 15) & ~(size_t)15);
+            const size_t dsm = hist_bytes + (size_t)8 * per_warp * 32 * 8 + (size_t)8 * kStripPf * 32 * (KIND == 0 ? 4 : 8);
+#define DQ_STRIP(ONE)                                                                                   \
+            ensure_smem(ctx, (const void*)dq_strip_kernel<KIND, ONE>, dsm);                             \
+            dq_strip_kernel<KIND, ONE><<<(unsigned)grid, 256, dsm, ctx->stream>>>(                      \
+                d_in, g, rw, rsteps, nyb, cap, hist_bytes, ctx->d_status, d_codes, d_hist);
+            if (rsteps == 1) { DQ_STRIP(true) } else { DQ_STRIP(false) }
+#undef DQ_STRIP
+            SDQZ_LAUNCHED_NAMED(ctx, "dq_strip_kernel");
+            return SDQZ_OK;
+        }
         if (rows && !env_disabled("SDQZ_NO_BLK")) {
             ensure_smem(ctx, (const void*)dq_rows_kernel<KIND>, smem);
             const uint64_t nitems = ndims == 1 ? dims[0] : (n / dims[ndims - 1]) * g.nblk[ndims - 1];

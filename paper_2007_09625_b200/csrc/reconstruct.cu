@@ -1059,6 +1059,8 @@ __global__ void __launch_bounds__(64) rq_blocks_kernel(const uint16_t* __restric
     }
 }
 
+constexpr int kRowPf = 8;   // row-kernel iterations whose code loads are issued together
+
 // 1D generic block length bx >= 32: a warp per task of whole blocks (>= 1024
 // points), lane = point, 32 points per step.  The reconstruct is the linear
 // recurrence F_i = a_i F_{i-1} + b_i with (a, b) = (1, delta) for an in-cap
@@ -1079,10 +1081,20 @@ __global__ void __launch_bounds__(256) rq1d_seg_kernel(const uint16_t* __restric
         const uint64_t t0 = t * task, t1 = umin(t0 + task, n);
         long long carry = 0;
         uint32_t pos = lane % bx;
-        for (uint64_t i0 = t0; i0 < t1; i0 += 32) {
+        for (uint64_t g0 = t0; g0 < t1; g0 += 32 * kRowPf) {
+          uint32_t cc[kRowPf];   // the group's codes, loaded together
+#pragma unroll
+          for (int k = 0; k < kRowPf; k++) {
+            const uint64_t i = g0 + 32 * k + lane;
+            cc[k] = i < t1 ? (uint32_t)codes[i] : (uint32_t)r;
+          }
+#pragma unroll
+          for (int k = 0; k < kRowPf; k++) {
+            const uint64_t i0 = g0 + 32 * k;
+            if (i0 >= t1) break;
             const uint64_t i = i0 + lane;
             const bool in = i < t1;
-            const uint32_t code = in ? codes[i] : (uint32_t)r;
+            const uint32_t code = cc[k];
             bool a = pos != 0;
             long long b = (long long)code - r;
             if (code == 0) {
@@ -1103,6 +1115,121 @@ __global__ void __launch_bounds__(256) rq1d_seg_kernel(const uint16_t* __restric
             carry = __shfl_sync(kFull, F, 31);
             pos += step;
             if (pos >= bx) pos -= bx;
+          }
+        }
+    }
+}
+
+// 2D / 3D generic block shapes: a warp per strip of block columns -- 32 / bx
+// whole blocks side by side when bx <= 32 (ONE), one block of `steps` 32-lane
+// segments otherwise -- over nyb consecutive block rows; lane = column.  Rows
+// go sequentially; inside a row H (the x prefix of the Lorenzo deltas) is a
+// warp prefix sum restarted at the last reset lane at or left of each lane
+// (block start, or an outlier whose H is v - F0 - Gp), so G = H + Gp (G of
+// row y-1 in this plane) and F = G + F0 (F of the row in plane z-1).  Gp and
+// F0 are lane-private shared-memory slots.  int32 modular arithmetic with the
+// rq_blocks_kernel magnitude guard: the sequentially first |F| >= 2^28 is
+// computed exactly, so a block that trips it is flagged and rewritten by the
+// fp64 replay.
+template <int OUTK, bool ONE>
+__global__ void __launch_bounds__(256, 3) rq_rows_kernel(const uint16_t* __restrict__ codes, const OutLookup ol,
+                                                      uint8_t* __restrict__ blockflag, Geo g, uint32_t W,
+                                                      uint32_t steps, uint32_t nyb, uint32_t cap, double two_eb,
+                                                      void* __restrict__ out, DevStatus* st) {
+    extern __shared__ __align__(16) int blk_smem[];
+    const uint32_t lane = lane_id(), warp = threadIdx.x >> 5;
+    const int nd = g.nd;
+    const uint32_t bx = g.block[nd - 1], by = g.block[nd - 2], bz = nd == 3 ? g.block[0] : 1;
+    const uint32_t per_warp = steps * (1 + (nd == 3 ? by : 0)) * 32;
+    int* Gs = blk_smem + warp * per_warp + lane;   // [steps][32]: G of row y-1
+    int* F0s = Gs + steps * 32;                    // [by][steps][32]: F of plane z-1 (3D)
+    const uint64_t X = g.dims[nd - 1], Y = g.dims[nd - 2], Z = nd == 3 ? g.dims[0] : 1;
+    const uint64_t sy = g.stride[nd - 2], sz = nd == 3 ? g.stride[0] : 0;
+    const uint64_t nbx = g.nblk[nd - 1], nby = g.nblk[nd - 2], nbz = nd == 3 ? g.nblk[0] : 1;
+    const uint64_t ntx = ceil_div(X, W), nyg = ceil_div(nby, nyb), ntask = ntx * nyg * nbz;
+    const int r = (int)(cap >> 1);
+    const bool seg0 = ONE ? lane % bx == 0 : lane == 0;   // block start (ONE) / first lane of a block row
+    const unsigned upto = (2u << lane) - 1u;              // lanes 0..lane (lane 31: all)
+    for (uint64_t t = blockIdx.x * (uint64_t)(blockDim.x >> 5) + warp; t < ntask;
+         t += (uint64_t)gridDim.x * (blockDim.x >> 5)) {
+        const uint64_t tx = t % ntx, t2 = t / ntx, cyg = t2 % nyg, cz = t2 / nyg;
+        const uint64_t x0 = tx * W;
+        const uint32_t lim = (uint32_t)umin(W, X - x0);   // valid columns of the strip
+        const uint32_t nz = (uint32_t)umin(bz, Z - cz * bz);
+        const uint64_t bcol = ONE ? (x0 + umin(lane, lim - 1)) / bx : x0 / bx;
+        const uint64_t cy1 = umin(cyg * nyb + nyb, nby);
+        for (uint64_t cy = cyg * nyb; cy < cy1; cy++) {
+            const uint32_t ny = (uint32_t)umin(by, Y - cy * by);
+            const uint64_t blk = (cz * nby + cy) * nbx + bcol;
+            const bool skip = blockflag[blk] != 0;   // non-integer outlier: the fp64 replay owns it
+            bool bad = false;
+            // (z, y, s) iterations in groups of kRowPf: the group's codes are
+            // loaded together (independent loads in flight) before the scans
+            const uint32_t nit = nz * ny * steps;
+            const uint64_t base = cz * bz * sz + cy * by * sy + x0;
+            const uint64_t zjump = sz - (uint64_t)(ny - 1) * sy;   // row ny-1 of plane z -> row 0 of plane z+1
+            uint64_t lrow = base, prow = base;
+            uint32_t ls = 0, ly = 0, ps = 0, py = 0, pz = 0;
+            int carry = 0;
+            for (uint32_t it0 = 0; it0 < nit; it0 += kRowPf) {
+                uint32_t cc[kRowPf];
+#pragma unroll
+                for (int k = 0; k < kRowPf; k++) {
+                    const uint32_t c = ONE ? lane : ls * 32 + lane;
+                    cc[k] = it0 + k < nit && c < lim ? (uint32_t)codes[lrow + c] : (uint32_t)r;
+                    if (ONE || ++ls == steps) {
+                        ls = 0;
+                        if (++ly == ny) { ly = 0; lrow += zjump; } else lrow += sy;
+                    }
+                }
+#pragma unroll
+                for (int k = 0; k < kRowPf; k++) {
+                    if (it0 + k >= nit) break;
+                    const uint32_t s = ONE ? 0 : ps, y = py, z = pz;
+                    const uint64_t rb = prow;
+                    if (ONE || ++ps == steps) {
+                        ps = 0;
+                        if (++py == ny) { py = 0; pz++; prow += zjump; } else prow += sy;
+                    }
+                    const uint32_t c = s * 32 + lane;   // column within the strip
+                    const bool valid = c < lim;
+                    const uint32_t code = skip ? (uint32_t)r : cc[k];
+                    const int Gp = y > 0 ? Gs[s * 32] : 0;
+                    int* pf = F0s + (y * steps + s) * 32;
+                    const int F0 = nd == 3 && z > 0 ? *pf : 0;
+                    bool reset = ONE ? seg0 : (s == 0 && seg0);
+                    int b = (int)code - r;
+                    if (code == 0) {   // outlier: its final value is stored verbatim
+                        const long long v = outlier_int(ol, rb + c);
+                        const int Fv = (v < (1ll << 28) && v > -(1ll << 28)) ? (int)v : (1 << 29);
+                        reset = true;
+                        b = (int)((unsigned)Fv - (unsigned)F0 - (unsigned)Gp);
+                    }
+                    unsigned S = (unsigned)b;   // inclusive prefix sum of b
+#pragma unroll
+                    for (int o = 1; o < 32; o <<= 1) {
+                        const unsigned u = __shfl_up_sync(kFull, S, o);
+                        if (lane >= (uint32_t)o) S += u;
+                    }
+                    const unsigned m = __ballot_sync(kFull, reset) & upto;
+                    const int L = 31 - __clz((int)m);   // last reset lane at or left of this one
+                    const unsigned Sx = __shfl_sync(kFull, S - (unsigned)b, L < 0 ? 0 : L);
+                    const unsigned H = m ? S - Sx : (unsigned)carry + S;
+                    if (!ONE) carry = (int)__shfl_sync(kFull, H, 31);
+                    const int G = (int)(H + (unsigned)Gp);
+                    const int F = (int)((unsigned)G + (unsigned)F0);
+                    if (valid && !skip) {
+                        bad |= !(F < (1 << 28) && F > -(1 << 28));
+                        store_out<OUTK>(out, rb + c, F, two_eb);
+                    }
+                    Gs[s * 32] = G;
+                    if (nd == 3) *pf = F;
+                }
+            }
+            if (bad) {   // magnitude guard: the fp64 replay redoes the block
+                blockflag[blk] = 1;
+                atomicOr(&st->flags, (unsigned long long)F_OUT_SLOW);
+            }
         }
     }
 }
@@ -1313,6 +1440,13 @@ int launch_reconstruct(sdqz_ctx* ctx, const uint16_t* codes, const OutLookup& ol
     const uint32_t slots = blk_slots(ndims, g.block);
     const bool blk = !fast && slots <= kBlkMaxSlots && bpts <= 65536 && !env_disabled("SDQZ_NO_BLK");
     uint64_t nblocks = g.nblk[0] * g.nblk[1] * g.nblk[2];
+    // 2D / 3D row kernel: strips of 32 / bx whole blocks (bx <= 32) or one
+    // block in ceil(bx / 32) lane segments; lane-private slots <= 12 KB a warp
+    const uint32_t bxx = block[ndims - 1];
+    const uint32_t rw = bxx <= 32 ? (32 / bxx) * bxx : bxx, rsteps = (rw + 31) / 32;
+    const char* rows_env = getenv("SDQZ_RQ_ROWS");   // 0 | 1: force off / on (tests)
+    const bool rows_ok = ndims >= 2 && (uint64_t)rsteps * (1 + (ndims == 3 ? block[ndims - 2] : 0)) <= 96 &&
+                         (rows_env ? rows_env[0] == '1' : bpts >= 128);
     if (blk && ndims == 1 && block[0] >= 32) {   // long 1D blocks: warp-wide scans over tasks of whole blocks
         const uint64_t task = (uint64_t)block[0] * ceil_div(1024, block[0]);
         uint64_t bg = ceil_div(ceil_div(n, task), 8);
@@ -1323,6 +1457,27 @@ int launch_reconstruct(sdqz_ctx* ctx, const uint16_t* codes, const OutLookup& ol
         else
             rq1d_seg_kernel<1><<<(unsigned)bg, 256, 0, ctx->stream>>>(codes, dn, n, block[0], task, cap, two_eb, out);
         SDQZ_LAUNCHED_NAMED(ctx, "rq1d_seg_kernel");
+    } else if (blk && ndims >= 2 && rows_ok) {   // warp per strip of block columns, lane = column
+        // block rows per task: >= 32 row iterations a warp task
+        const uint64_t iters = (uint64_t)rsteps * block[ndims - 2] * (ndims == 3 ? block[0] : 1);
+        const uint32_t nyb = iters >= 32 ? 1 : (uint32_t)ceil_div(32, iters);
+        const uint64_t ntask = ceil_div(g.dims[ndims - 1], rw) * ceil_div(g.nblk[ndims - 2], nyb) *
+                               (ndims == 3 ? g.nblk[0] : 1);
+        uint64_t bg = ceil_div(ntask, 8);
+        if (bg > (uint64_t)ctx->num_sms * 16) bg = (uint64_t)ctx->num_sms * 16;
+        if (bg < 1) bg = 1;
+        const size_t dsm = (size_t)8 * rsteps * (1 + (ndims == 3 ? block[ndims - 2] : 0)) * 32 * 4;
+#define RQ_ROWS(K, ONE)                                                                                       \
+        ensure_smem(ctx, (const void*)rq_rows_kernel<K, ONE>, dsm);                                           \
+        rq_rows_kernel<K, ONE><<<(unsigned)bg, 256, dsm, ctx->stream>>>(codes, dn, const_cast<uint8_t*>(blockflag), \
+                                                                      g, rw, rsteps, nyb, cap, two_eb, out, ctx->d_status);
+        if (out_kind == 0) {
+            if (rsteps == 1) { RQ_ROWS(0, true) } else { RQ_ROWS(0, false) }
+        } else {
+            if (rsteps == 1) { RQ_ROWS(1, true) } else { RQ_ROWS(1, false) }
+        }
+#undef RQ_ROWS
+        SDQZ_LAUNCHED_NAMED(ctx, "rq_rows_kernel");
     } else if (blk) {
         const uint32_t T = slots * 4 <= 1024 ? 64 : 32;
         const size_t dsm = (size_t)T * slots * 4;

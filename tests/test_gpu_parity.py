@@ -698,6 +698,17 @@ class TestGenericShapes:
             assert blob == O.compress(f, block_shape=block, **kw)
             assert np.array_equal(bits(S.decompress(blob)), bits(O.decompress(blob)))
 
+    @pytest.mark.parametrize("block", [(16, 16, 16), (2, 8, 40), (8, 40)])
+    def test_wide_prequant_range(self, block):
+        """valrel on a field far from zero: max|x| / 2eb >= 2^27, so the strip
+        dual-quant takes its fp64 path (the int32 one needs every |q| < 2^27)."""
+        dims = (40, 41, 90) if len(block) == 3 else (300, 257)
+        f = S.generate_field("smooth", dims, seed=9).astype(np.float32) + np.float32(3e4)
+        for eb in (1e-7, 1e-5):
+            blob = S.compress(f, eb=eb, mode="valrel", block_shape=block)
+            assert blob == O.compress(f, eb=eb, mode="valrel", block_shape=block)
+            assert np.array_equal(bits(S.decompress(blob)), bits(O.decompress(blob)))
+
     def test_guard_and_f64(self):
         rng = np.random.default_rng(3)
         f = (rng.normal(0, 1, (24, 24, 24)) * 1e6).astype(np.float64)   # |F| far past 2^28 at eb 1e-3

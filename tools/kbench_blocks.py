@@ -1,6 +1,7 @@
 """Compress / decompress device time for non-default block shapes (row f4).
 
     python tools/kbench_blocks.py            (Nyx-shaped 512^3, 2D 8192^2, 1D 2^28)
+    python tools/kbench_blocks.py 8192,8192:8,8 512,512,512:4,4,4     (selected cases)
 """
 import json
 import math
@@ -62,5 +63,6 @@ def run(dims, block, reps=5):
 
 
 if __name__ == "__main__":
-    for dims, block in CASES:
+    sel = [tuple(tuple(int(v) for v in p.split(",")) for p in a.split(":")) for a in sys.argv[1:]]
+    for dims, block in sel or CASES:
         run(dims, block)
