@@ -1194,6 +1194,25 @@ __global__ void __launch_bounds__(64) dq_blocks_kernel(const void* __restrict__ 
     hist_finish(h);
 }
 
+// prequantized value of an already loaded input element (load_q_fast without the load)
+template <int KIND>
+__device__ __forceinline__ double q_of(typename std::conditional<KIND == 0, float, double>::type v, double two_eb,
+                                       double rcp, bool& bad) {
+    bad |= !isfinite(v);
+    if (KIND == 2) return v;
+    if (KIND == 0) {
+        const double y = __dmul_rn((double)v, rcp);
+        const double ay = fabs(y);
+        if (ay < 134217728.0) {
+            const double t = __dadd_rn(ay, 0.5);
+            const double fl = floor(t);
+            const double fr = __dsub_rn(t, fl);
+            if (fr >= 2.384185791015625e-07 && fr <= 1.0 - 2.384185791015625e-07) return copysign(fl, y);
+        }
+    }
+    return prequant((double)v, two_eb);
+}
+
 // Generic block shapes, one thread per block-row segment (3D/2D: the x-extent
 // of one block in one row; 1D: one point): every neighbour the reference's
 // prediction reads is prequantized again by this thread (x-1 values carried
@@ -1227,16 +1246,36 @@ __global__ void __launch_bounds__(256) dq_rows_kernel(const void* __restrict__ i
         }
     };
     const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
-    if (nd == 1) {   // point it; its left neighbour unless it starts a block (position kept incrementally)
-        uint64_t it = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
-        uint64_t pos = it % bx;
-        const uint64_t step = stride % bx;
-        for (; it < nitems; it += stride) {
-            const double q = load_q_fast<KIND>(in, it, two_eb, rcp, bad);
-            const double a = pos ? load_q_fast<KIND>(in, it - 1, two_eb, rcp, bad) : 0.0;
-            emit(it, __dsub_rn(q, a));
-            pos += step;
-            if (pos >= bx) pos -= bx;
+    if (nd == 1) {   // warp per 512-point task, lane = point: the left neighbour is the lane to the left's q
+        using raw_t = typename std::conditional<KIND == 0, float, double>::type;
+        constexpr int kG = 16;   // 32-point steps per task, loaded together
+        const uint32_t lane = threadIdx.x & 31;
+        const uint64_t nw = stride >> 5, ntask = ceil_div(nitems, 32 * kG);
+        const uint32_t step = 32 % bx;
+        for (uint64_t t = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5; t < ntask; t += nw) {
+            const uint64_t i0 = t * 32 * kG;
+            raw_t v[kG];
+#pragma unroll
+            for (int k = 0; k < kG; k++) {
+                const uint64_t i = i0 + 32 * k + lane;
+                v[k] = i < nitems ? __ldg((const raw_t*)in + i) : (raw_t)0;
+            }
+            // the point before the task (lane 0's left neighbour at step 0)
+            double carry = (lane == 0 && i0 > 0 && (i0 % bx) != 0) ? load_q_fast<KIND>(in, i0 - 1, two_eb, rcp, bad) : 0.0;
+            uint32_t pos = (uint32_t)((i0 + lane) % bx);
+#pragma unroll
+            for (int k = 0; k < kG; k++) {
+                const uint64_t i = i0 + 32 * k + lane;
+                const bool in_range = i < nitems;
+                const double q = in_range ? q_of<KIND>(v[k], two_eb, rcp, bad) : 0.0;
+                double a = __shfl_up_sync(kFull, q, 1);
+                if (lane == 0) a = carry;
+                carry = __shfl_sync(kFull, q, 31);
+                if (pos == 0) a = 0.0;
+                if (in_range) emit(i, __dsub_rn(q, a));
+                pos += step;
+                if (pos >= bx) pos -= bx;
+            }
         }
     }
     for (uint64_t it = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; nd > 1 && it < nitems; it += stride) {
@@ -1274,25 +1313,6 @@ __global__ void __launch_bounds__(256) dq_rows_kernel(const void* __restrict__ i
     hist_flush_thread(h);
     if (bad) atomicOr(&st->flags, (unsigned long long)F_NONFINITE);
     hist_finish(h);
-}
-
-// prequantized value of an already loaded input element (load_q_fast without the load)
-template <int KIND>
-__device__ __forceinline__ double q_of(typename std::conditional<KIND == 0, float, double>::type v, double two_eb,
-                                       double rcp, bool& bad) {
-    bad |= !isfinite(v);
-    if (KIND == 2) return v;
-    if (KIND == 0) {
-        const double y = __dmul_rn((double)v, rcp);
-        const double ay = fabs(y);
-        if (ay < 134217728.0) {
-            const double t = __dadd_rn(ay, 0.5);
-            const double fl = floor(t);
-            const double fr = __dsub_rn(t, fl);
-            if (fr >= 2.384185791015625e-07 && fr <= 1.0 - 2.384185791015625e-07) return copysign(fl, y);
-        }
-    }
-    return prequant((double)v, two_eb);
 }
 
 // dq_strip_kernel's Lorenzo prediction of the point with prequantized value q

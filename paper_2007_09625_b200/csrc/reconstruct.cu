@@ -1063,9 +1063,10 @@ constexpr int kRowPf = 8;   // row-kernel iterations whose code loads are issued
 
 // 1D generic block length bx >= 32: a warp per task of whole blocks (>= 1024
 // points), lane = point, 32 points per step.  The reconstruct is the linear
-// recurrence F_i = a_i F_{i-1} + b_i with (a, b) = (1, delta) for an in-cap
-// code, (0, delta) at a block start, (0, v) at an outlier -- an inclusive warp
-// scan of (a, b) pairs plus the previous step's F as carry, exact in int64.
+// recurrence F_i = F_{i-1} + delta_i restarted at a block start (F = delta)
+// and at an outlier (F = v): a warp prefix sum minus its value just before
+// the last restart lane at or left of each lane (the previous step's F as
+// carry when there is none), exact in int64.
 // Blocks whose outlier values are not integers below 2^40 are flagged by the
 // scatter and rewritten afterwards by the fp64 replay.
 template <int OUTK>
@@ -1076,6 +1077,7 @@ __global__ void __launch_bounds__(256) rq1d_seg_kernel(const uint16_t* __restric
     const int r = (int)(cap >> 1);
     const uint64_t ntask = ceil_div(n, task);
     const uint32_t step = 32 % bx;
+    const unsigned upto = (2u << lane) - 1u;   // lanes 0..lane (lane 31: all)
     for (uint64_t t = blockIdx.x * (uint64_t)(blockDim.x >> 5) + (threadIdx.x >> 5); t < ntask;
          t += (uint64_t)gridDim.x * (blockDim.x >> 5)) {
         const uint64_t t0 = t * task, t1 = umin(t0 + task, n);
@@ -1095,22 +1097,22 @@ __global__ void __launch_bounds__(256) rq1d_seg_kernel(const uint16_t* __restric
             const uint64_t i = i0 + lane;
             const bool in = i < t1;
             const uint32_t code = cc[k];
-            bool a = pos != 0;
+            bool reset = pos == 0;
             long long b = (long long)code - r;
             if (code == 0) {
-                a = false;
+                reset = true;
                 b = (long long)__longlong_as_double((long long)out_bits(ol, i));
             }
+            long long S = b;   // inclusive prefix sum, restarted at the last reset lane at or left of this one
 #pragma unroll
             for (int o = 1; o < 32; o <<= 1) {
-                const bool ap = __shfl_up_sync(kFull, a, o);
-                const long long bp = __shfl_up_sync(kFull, b, o);
-                if (lane >= (uint32_t)o) {
-                    if (a) b += bp;
-                    a = a && ap;
-                }
+                const long long u = __shfl_up_sync(kFull, S, o);
+                if (lane >= (uint32_t)o) S += u;
             }
-            const long long F = a ? carry + b : b;
+            const unsigned m = __ballot_sync(kFull, reset) & upto;
+            const int L = 31 - __clz((int)m);
+            const long long Sx = __shfl_sync(kFull, S - b, L < 0 ? 0 : L);
+            const long long F = m ? S - Sx : carry + S;
             if (in) store_out<OUTK>(out, i, F, two_eb);
             carry = __shfl_sync(kFull, F, 31);
             pos += step;
