@@ -709,6 +709,26 @@ class TestGenericShapes:
             assert blob == O.compress(f, eb=eb, mode="valrel", block_shape=block)
             assert np.array_equal(bits(S.decompress(blob)), bits(O.decompress(blob)))
 
+    def test_random_strip_shapes(self):
+        """Seeded sweep over the strip / row kernels' geometry: block widths
+        below, at and above 32 (one and several lane segments, strips of
+        32 // bx blocks with idle lanes), 1-row / 1-plane blocks, fields not a
+        multiple of the block, fp32 / fp64, valrel / abs, sprinkled outliers."""
+        rng = np.random.default_rng(2024)
+        for case in range(24):
+            nd = 2 + case % 2
+            block = tuple(int(v) for v in rng.choice([1, 2, 3, 5, 8, 16], size=nd - 1)) + \
+                (int(rng.choice([3, 7, 12, 31, 32, 33, 40, 64, 100])),)
+            dims = tuple(int(b * rng.integers(1, 4) + rng.integers(0, b + 1)) for b in block)
+            dims = tuple(max(2, d) for d in dims[:-1]) + (max(3, dims[-1]),)
+            dtype = np.float64 if case % 3 == 0 else np.float32
+            f = S.generate_field("smooth", dims, seed=case).astype(dtype)
+            f.reshape(-1)[rng.integers(0, f.size, size=max(1, f.size // 50))] += dtype(7.0)
+            kw = dict(eb=1e-4, mode="valrel") if case % 2 == 0 else dict(eb=0.01, mode="abs", cap=256)
+            blob = S.compress(f, block_shape=block, **kw)
+            assert blob == O.compress(f, block_shape=block, **kw), (dims, block, dtype, kw)
+            assert np.array_equal(bits(S.decompress(blob)), bits(O.decompress(blob))), (dims, block, dtype, kw)
+
     def test_guard_and_f64(self):
         rng = np.random.default_rng(3)
         f = (rng.normal(0, 1, (24, 24, 24)) * 1e6).astype(np.float64)   # |F| far past 2^28 at eb 1e-3

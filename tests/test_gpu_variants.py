@@ -45,6 +45,12 @@ fields = [
      dict(eb=1e-4, mode="valrel", block_shape=(4, 4, 4))),
     (S.generate_field("smooth", (90, 77), seed=7).astype(np.float32),
      dict(eb=1e-3, mode="valrel", block_shape=(8, 8))),
+    (S.generate_field("smooth", (7, 11, 70), seed=8).astype(np.float32),
+     dict(eb=1e-4, mode="valrel", block_shape=(2, 3, 33))),
+    (S.generate_field("smooth", (40, 100), seed=9).astype(np.float32),
+     dict(eb=0.01, mode="abs", block_shape=(3, 7))),
+    (S.generate_field("smooth", (5, 9, 83), seed=10),
+     dict(eb=1e-5, mode="valrel", block_shape=(2, 2, 40))),
 ]
 for f, kw in fields:
     blob = S.compress(f, **kw)
