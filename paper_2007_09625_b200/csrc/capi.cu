@@ -389,6 +389,25 @@ void capture_graph(sdqz_ctx* ctx, sdqz_ctx::Graph& g, const std::string& key, En
     cudaGraphDestroy(graph);
 }
 
+// the context's forked-branch stream and its fork / join events (created on
+// first use; false leaves the caller on one stream)
+bool side_stream(sdqz_ctx* ctx) {
+    if (env_disabled("SDQZ_NO_FORK")) return false;
+    if (!ctx->side) {
+        if (cudaStreamCreateWithFlags(&ctx->side, cudaStreamNonBlocking) != cudaSuccess ||
+            cudaEventCreateWithFlags(&ctx->ev_fork, cudaEventDisableTiming) != cudaSuccess ||
+            cudaEventCreateWithFlags(&ctx->ev_join, cudaEventDisableTiming) != cudaSuccess) {
+            cudaGetLastError();
+            if (ctx->side) cudaStreamDestroy(ctx->side);
+            if (ctx->ev_fork) cudaEventDestroy(ctx->ev_fork);
+            ctx->side = nullptr;
+            ctx->ev_fork = ctx->ev_join = nullptr;
+            return false;
+        }
+    }
+    return true;
+}
+
 bool graphs_on(const sdqz_ctx* ctx) { return !ctx->timing && !ctx->qual.orig && !env_disabled("SDQZ_NO_GRAPH"); }
 
 // Shared decompress core over device-resident sections.  The enqueue part (all
@@ -414,10 +433,26 @@ int decompress_core(sdqz_ctx* ctx, const sdqz_header* hdr, const uint8_t* d_bw, 
     if (!codes || !bflag) return rc;
     uint32_t safe_block[3];
     for (int a = 0; a < 3; a++) safe_block[a] = hdr->block[a] ? hdr->block[a] : 1;
+    const bool rec1d = chunks_ok && rq1d_records_ok(hdr->ndims, hdr->dims, hdr->block, codes, d_out, d_rec);
+    // the outlier lookup index depends only on the records: it runs on a
+    // forked branch beside the codebook / decode (a parallel graph branch when
+    // captured) and joins before the reconstruct; per-kernel timing keeps one stream
+    const bool fork = chunks_ok && !rec1d && !ctx->timing && side_stream(ctx);
     auto enqueue = [&]() -> int {
         int r2;
         if ((r2 = reset_status_eb(ctx, hdr->eb_resolved, true))) return r2;
         SDQZ_CUDA(ctx, cudaMemsetAsync(bflag, 0, nblocks, ctx->stream));
+        OutLookup ol;
+        if (fork) {
+            const cudaStream_t main = ctx->stream;
+            SDQZ_CUDA(ctx, cudaEventRecord(ctx->ev_fork, main));
+            SDQZ_CUDA(ctx, cudaStreamWaitEvent(ctx->side, ctx->ev_fork, 0));
+            ctx->stream = ctx->side;
+            r2 = launch_outlier_index(ctx, d_rec, nullptr, nullptr, k, n, &ol);
+            ctx->stream = main;
+            if (r2) return r2;
+            SDQZ_CUDA(ctx, cudaEventRecord(ctx->ev_join, ctx->side));
+        }
         // canonical tables from the stored bitwidths (deserialize checks + canonize)
         if ((r2 = launch_codebook(ctx, nullptr, const_cast<uint8_t*>(d_bw), cap, book, false, true, true)))
             return r2;
@@ -428,7 +463,7 @@ int decompress_core(sdqz_ctx* ctx, const sdqz_header* hdr, const uint8_t* d_bw, 
                                      false)))
                 return r2;
         }
-        if (chunks_ok && rq1d_records_ok(hdr->ndims, hdr->dims, hdr->block, codes, d_out, d_rec)) {
+        if (rec1d) {
             // 1D: outlier values straight from the sorted records (no dense scatter)
             return (r2 = launch_reconstruct_1d_records(ctx, codes, d_rec, k, n, cap, 2.0 * hdr->eb_resolved,
                                                        d_out, hdr->dtype_code, bflag))
@@ -440,8 +475,8 @@ int decompress_core(sdqz_ctx* ctx, const sdqz_header* hdr, const uint8_t* d_bw, 
             return r2;
         if (chunks_ok) {
             double two_eb = 2.0 * hdr->eb_resolved;
-            OutLookup ol;
-            if ((r2 = launch_outlier_index(ctx, d_rec, nullptr, nullptr, k, n, &ol))) return r2;
+            if (fork) SDQZ_CUDA(ctx, cudaStreamWaitEvent(ctx->stream, ctx->ev_join, 0));
+            else if ((r2 = launch_outlier_index(ctx, d_rec, nullptr, nullptr, k, n, &ol))) return r2;
             if ((r2 = launch_reconstruct(ctx, codes, ol, bflag, true, hdr->ndims, hdr->dims,
                                          hdr->block, cap, two_eb, d_out, hdr->dtype_code)))
                 return r2;
@@ -781,6 +816,9 @@ int sdqz_ctx_destroy(sdqz_ctx* ctx) {
         if (b.p) cudaFree(b.p);
     if (ctx->g_comp.exec) cudaGraphExecDestroy(ctx->g_comp.exec);
     if (ctx->cap_stream) cudaStreamDestroy(ctx->cap_stream);
+    if (ctx->side) cudaStreamDestroy(ctx->side);
+    if (ctx->ev_fork) cudaEventDestroy(ctx->ev_fork);
+    if (ctx->ev_join) cudaEventDestroy(ctx->ev_join);
     if (ctx->g_decomp.exec) cudaGraphExecDestroy(ctx->g_decomp.exec);
     if (ctx->d_status) cudaFree(ctx->d_status);
     if (ctx->h_status) cudaFreeHost(ctx->h_status);

@@ -211,6 +211,8 @@ struct sdqz_ctx {
     std::string last_comp_key, last_decomp_key;
     uint64_t graph_replays = 0;
     cudaStream_t cap_stream = nullptr;   // capture stream
+    cudaStream_t side = nullptr;         // forked branch (outlier lookup index beside the decode)
+    cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
 
     // optional per-kernel device timer (bench / profiling)
     bool timing = false;

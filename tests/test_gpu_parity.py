@@ -1,6 +1,8 @@
 """GPU parity: every stage of the CUDA path against the reference's golden
 vectors (tests/golden) and the CPU oracle, bit-exact."""
 
+import os
+
 import numpy as np
 import pytest
 
@@ -736,3 +738,27 @@ class TestGenericShapes:
             blob = S.compress(f, eb=1e-3, mode="abs", block_shape=block)
             assert blob == O.compress(f, eb=1e-3, mode="abs", block_shape=block)
             assert np.array_equal(bits(S.decompress(blob)), bits(O.decompress(blob)))
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("dims,block", [((33, 70, 90), None), ((300, 700), None), ((250_001,), None),
+                                        ((40, 48, 64), (16, 16, 16)), ((120, 200), (4, 64))])
+def test_graph_replay_bit_exact(dims, block):
+    """Repeated calls with the same geometry replay the captured CUDA graphs
+    (the decompress graph carries the forked outlier-index branch): every
+    replay's archive and output equal the oracle's."""
+    from paper_2007_09625_b200 import _lib
+    f = S.generate_field("smooth", dims, seed=11).astype(np.float32)
+    f.reshape(-1)[::61] += np.float32(9.0)
+    kw = dict(eb=1e-4, mode="valrel", block_shape=block)
+    ref = O.compress(f, **kw)
+    want = bits(O.decompress(ref))
+    ctx = _lib.context()
+    r0 = ctx.graph_replays
+    for _ in range(4):
+        blob = S.compress(f, **kw)
+        assert blob == ref
+        assert np.array_equal(bits(S.decompress(blob)), want)
+    if not os.environ.get("SDQZ_NO_GRAPH"):
+        assert ctx.graph_replays > r0
+
