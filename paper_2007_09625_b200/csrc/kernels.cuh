@@ -97,6 +97,7 @@ struct OutLookup {
     const unsigned long long* start;   // [ceil(n / 1024) + 1]: first record of each bucket
     uint64_t k;
     uint64_t base;                     // added to a query index (a kernel run on a sub-range)
+    const unsigned long long* big;     // [1]: nonzero when some record's |value| >= 2^29 (or NaN)
 };
 // builds the bucket table (context scratch) for k records over n points
 int launch_outlier_index(sdqz_ctx* ctx, const void* records, const uint64_t* idx, const double* val,

@@ -532,7 +532,7 @@ __device__ __forceinline__ void rq2d_vec_rows(const uint2 (&cw)[16], const OutLo
 }
 
 template <int OUTK>
-__global__ void __launch_bounds__(kThreads) rq2d_vec_kernel(const uint16_t* __restrict__ codes,
+__global__ void __launch_bounds__(kThreads, 3) rq2d_vec_kernel(const uint16_t* __restrict__ codes,
                                                             const OutLookup ol,
                                                             const uint8_t* __restrict__ blockflag,
                                                             int any_slow, uint64_t Y, uint64_t X,
@@ -543,6 +543,7 @@ __global__ void __launch_bounds__(kThreads) rq2d_vec_kernel(const uint16_t* __re
     QAcc acc;
     const uint64_t nbx = ceil_div(X, 16), ntx = ceil_div(X, 128), nty = ceil_div(Y, 16);
     const uint64_t ntask = ntx * nty;
+    const bool big = *ol.big != 0;
     for (uint64_t task = blockIdx.x * (uint64_t)kWarpsPerCta + (threadIdx.x >> 5); task < ntask;
          task += (uint64_t)gridDim.x * kWarpsPerCta) {
         const uint64_t tx = task % ntx, ty = task / ntx;
@@ -557,21 +558,7 @@ __global__ void __launch_bounds__(kThreads) rq2d_vec_kernel(const uint16_t* __re
             if (xin && y < ny) cw[y] = __ldcs(reinterpret_cast<const uint2*>(codes + (y0 + y) * X + x0));
         }
         const bool store = !(any_slow && xin && blockflag[ty * nbx + (x0 >> 4)]);
-        bool big = false;
-#pragma unroll
-        for (int y = 0; y < 16; y++) {
-            if (__vcmpeq2(cw[y].x, 0u) | __vcmpeq2(cw[y].y, 0u)) {
-#pragma unroll
-                for (int k = 0; k < 4; k++) {
-                    const uint32_t cc = (k < 2 ? cw[y].x : cw[y].y) >> (16 * (k & 1)) & 0xFFFFu;
-                    if (cc == 0) {
-                        const double v = __longlong_as_double((long long)out_bits(ol, (y0 + y) * X + x0 + k));
-                        big |= !(fabs(v) < 536870912.0);
-                    }
-                }
-            }
-        }
-        if (__any_sync(kFull, big))
+        if (big)   // some outlier value >= 2^29 (task_bounds_kernel): int64 rows
             rq2d_vec_rows<long long, OUTK>(cw, ol, X, y0, ny, x0, xin, store, r, lane, two_eb, out, q, acc);
         else
             rq2d_vec_rows<int, OUTK>(cw, ol, X, y0, ny, x0, xin, store, r, lane, two_eb, out, q, acc);
@@ -677,7 +664,8 @@ __device__ __forceinline__ void rq1d_rec_row(const uint32_t (&c)[4], const V (&v
 // record indices idx[j * stride]; bounded whatever the order of a corrupt set).
 // (A galloping search from the evenly-spread guess measured slower: the 3D
 // block-corner outliers cluster in every 64th row of buckets.)
-__global__ void task_bounds_kernel(const unsigned long long* __restrict__ idx, uint32_t stride, uint64_t k,
+__global__ void task_bounds_kernel(const unsigned long long* __restrict__ idx,
+                                   const unsigned long long* __restrict__ val, uint32_t stride, uint64_t k,
                                    uint64_t ntask, unsigned long long* __restrict__ start) {
     for (uint64_t t = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; t <= ntask;
          t += (uint64_t)gridDim.x * blockDim.x) {
@@ -689,6 +677,12 @@ __global__ void task_bounds_kernel(const unsigned long long* __restrict__ idx, u
         }
         start[t] = lo;
     }
+    // start[ntask + 1]: some record's value is at least 2^29 in magnitude (or NaN):
+    // the int32 2D reconstruct is not exact for it (zeroed by the launcher)
+    bool big = false;
+    for (uint64_t j = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; j < k; j += (uint64_t)gridDim.x * blockDim.x)
+        big |= !(fabs(__longlong_as_double((long long)val[j * stride])) < 536870912.0);
+    if (__any_sync(kFull, big) && lane_id() == 0) atomicOr(&start[ntask + 1], 1ull);
 }
 
 // the 8 rows of a task; zero codes take the value of the task record of the
@@ -1256,8 +1250,9 @@ int launch_outlier_index(sdqz_ctx* ctx, const void* records, const uint64_t* idx
                          uint64_t k, uint64_t n, OutLookup* out) {
     int rc = SDQZ_OK;
     const uint64_t nb = ceil_div(n, 1024);
-    unsigned long long* start = scratch_as<unsigned long long>(ctx, S_DENSE, nb + 1, &rc);
+    unsigned long long* start = scratch_as<unsigned long long>(ctx, S_DENSE, nb + 2, &rc);
     if (!start) return rc;
+    SDQZ_CUDA(ctx, cudaMemsetAsync(start + nb + 1, 0, 8, ctx->stream));
     const unsigned long long* rec = (const unsigned long long*)records;
     out->idx = rec ? rec : (const unsigned long long*)idx;
     out->val = rec ? rec + 1 : (const unsigned long long*)val;
@@ -1265,9 +1260,11 @@ int launch_outlier_index(sdqz_ctx* ctx, const void* records, const uint64_t* idx
     out->start = start;
     out->k = k;
     out->base = 0;
-    uint64_t grid = ceil_div(nb + 1, 256);
+    out->big = start + nb + 1;
+    uint64_t grid = ceil_div((nb + 1 > k ? nb + 1 : k), 256);
     if (grid > (uint64_t)ctx->num_sms * 8) grid = ctx->num_sms * 8;
-    task_bounds_kernel<<<(unsigned)grid, 256, 0, ctx->stream>>>(out->idx, out->stride, k, nb, start);
+    if (grid < 1) grid = 1;
+    task_bounds_kernel<<<(unsigned)grid, 256, 0, ctx->stream>>>(out->idx, out->val, out->stride, k, nb, start);
     SDQZ_LAUNCHED_NAMED(ctx, "task_bounds_kernel");
     return SDQZ_OK;
 }
