@@ -4,7 +4,7 @@
     compute-sanitizer --tool racecheck --error-exitcode 9 python tools/sanitize.py
 
 fast 1D/2D/3D dual-quant and reconstruct (TMA 3D, vectorised 1D/2D), generic
-block shapes, f64 input, 64-bit codewords, the warp-parallel decoder and its
+block shapes (strip / row / thread-per-block kernels), f64 input, 64-bit codewords, the warp-parallel decoder and its
 sequential hand-back (a corrupted payload), the stage API, the sharded phases
 on one rank, quality.  Every result is checked against the oracle."""
 import sys
@@ -36,7 +36,13 @@ def main():
     rt(S.generate_field("smooth", (5000,), seed=3).astype(np.float32), eb=1e-4, mode="valrel")    # 1D vec
     rt(rng.normal(0, 1, (9, 7, 5)).astype(np.float32), eb=0.02, cap=64, block_shape=(4, 3, 2))     # generic
     rt(S.generate_field("smooth", (20, 33, 40), seed=8).astype(np.float32), eb=1e-4, mode="valrel",
-       block_shape=(16, 16, 16))                                     # dq/rq_blocks, partial blocks
+       block_shape=(16, 16, 16))                                     # dq_strip / rq_rows, partial blocks
+    rt(S.generate_field("smooth", (7, 11, 90), seed=12).astype(np.float32), eb=1e-4, mode="valrel",
+       block_shape=(2, 3, 40))                                       # strip in two lane segments
+    rt(S.generate_field("smooth", (60, 100), seed=13).astype(np.float32) + np.float32(3e4), eb=1e-6,
+       mode="valrel", block_shape=(16, 30))                          # strip fp64 prediction, idle lanes
+    rt(S.generate_field("smooth", (9, 10, 11), seed=14).astype(np.float32), eb=1e-4, mode="valrel",
+       block_shape=(4, 4, 4))                                        # dq/rq_blocks (small blocks)
     rt(S.generate_field("smooth", (50, 70), seed=9).astype(np.float32), eb=1e-3, mode="valrel", block_shape=(8, 8))
     rt(rng.normal(0, 1, (12, 12, 12)) * 1e6, eb=1e-3, block_shape=(6, 6, 6))                     # int32 guard: fp64 replay
     rt(S.generate_field("smooth", (20_001,), seed=10).astype(np.float32), eb=1e-4, mode="valrel",
