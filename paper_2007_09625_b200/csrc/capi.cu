@@ -460,7 +460,7 @@ int decompress_core(sdqz_ctx* ctx, const sdqz_header* hdr, const uint8_t* d_bw, 
         if (chunks_ok) {
             if ((r2 = launch_inflate(ctx, d_payload, payload_alloc, d_cbits, C, hdr->chunk_size,
                                      book.first, book.offsets, book.symbols, book.lut, -1, cap, n, codes,
-                                     false)))
+                                     false, hdr->payload_bytes)))
                 return r2;
         }
         if (rec1d) {

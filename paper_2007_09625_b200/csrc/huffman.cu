@@ -1798,7 +1798,8 @@ int launch_encode_u32(sdqz_ctx* ctx, const uint32_t* codes, uint64_t n, const ui
 int launch_inflate(sdqz_ctx* ctx, const uint8_t* payload, uint64_t payload_bytes,
                    const uint32_t* chunk_bits, uint64_t n_chunks, uint32_t chunk,
                    const uint64_t* first, const int64_t* offsets, const uint32_t* symbols,
-                   const uint32_t* lut, int max_bw, uint32_t cap, uint64_t n, void* codes, bool out32) {
+                   const uint32_t* lut, int max_bw, uint32_t cap, uint64_t n, void* codes, bool out32,
+                   uint64_t stream_bytes) {
     // readable words: the payload plus its zero padding (callers pad >= 16 bytes)
     const uint64_t nwords = (payload_bytes + 16) / 4;
     int rc = SDQZ_OK;
@@ -1830,7 +1831,8 @@ int launch_inflate(sdqz_ctx* ctx, const uint8_t* payload, uint64_t payload_bytes
     // one launch: decode tables (+ the fallback LUT) | chunk byte offsets + clears
     (void)cap;
     uint32_t* tab = nullptr;
-    const int ns = decode_ns(payload_bytes, n);
+    // table width from the stream's mean code length (its own size, not the buffer's)
+    const int ns = decode_ns(stream_bytes ? stream_bytes : payload_bytes, n);
     if ((rc = launch_decode_prep(ctx, first, offsets, symbols, max_bw, &tab, const_cast<uint32_t*>(lut),
                                  chunk_bits, n_chunks, a.byte_off, redo, ns)))
         return rc;

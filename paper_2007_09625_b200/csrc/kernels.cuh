@@ -67,7 +67,8 @@ int launch_encode_u32(sdqz_ctx* ctx, const uint32_t* codes, uint64_t n, const ui
 int launch_inflate(sdqz_ctx* ctx, const uint8_t* payload, uint64_t payload_bytes,
                    const uint32_t* chunk_bits, uint64_t n_chunks, uint32_t chunk,
                    const uint64_t* first, const int64_t* offsets, const uint32_t* symbols,
-                   const uint32_t* lut, int max_bw, uint32_t cap, uint64_t n, void* codes, bool out32);
+                   const uint32_t* lut, int max_bw, uint32_t cap, uint64_t n, void* codes, bool out32,
+                   uint64_t stream_bytes = 0);   // the payload's own size when payload_bytes is a buffer capacity
 
 // inflate.cu: decode tables (primary 12-bit + second level) and the warp-per-chunk
 // self-synchronising decoder; chunks it cannot finish are flagged in `redo`.
