@@ -563,6 +563,14 @@ int compress_prepare(sdqz_ctx* ctx, CompressState& c) {
     c.job.out_records = c.rec;
     c.job.out_cap = c.rec_cap;
     c.job.trusted = true;   // K2's codes: < cap and all present in the book
+    // 1D fp32: the dual-quant hands the packer its outlier block heads' values
+    const uint64_t span = dq1d_vec_span(c.dtype, c.ndims, c.dims, c.block, c.d_in, c.codes);
+    if (span && !env_disabled("SDQZ_NO_HEADS")) {
+        double* heads = scratch_as<double>(ctx, S_HEADS, span / 32, &rc);
+        if (!heads) return rc;
+        c.job.heads = heads;
+        c.job.heads_limit = span;
+    }
     return SDQZ_OK;
 }
 
@@ -577,7 +585,8 @@ int compress_enqueue(sdqz_ctx* ctx, const CompressState& c) {
     }
     if ((rc = launch_resolve(ctx, c.dtype, c.eb_mode, c.eb))) return rc;
     SDQZ_CUDA(ctx, cudaMemsetAsync(c.hist, 0, c.cap * 8ull, ctx->stream));
-    if ((rc = launch_dualquant(ctx, c.d_in, c.dtype, c.ndims, c.dims, c.block, c.cap, c.codes, c.hist)))
+    if ((rc = launch_dualquant(ctx, c.d_in, c.dtype, c.ndims, c.dims, c.block, c.cap, c.codes, c.hist,
+                               const_cast<double*>(c.job.heads))))
         return rc;
     if ((rc = launch_codebook(ctx, c.hist, c.book.bw, c.cap, c.book, true, true, false))) return rc;
     if ((rc = launch_deflate(ctx, c.job))) return rc;

@@ -230,6 +230,7 @@ enum Slot : int {
     S_CODES = 0, S_HIST, S_BW, S_ENTRIES, S_FIRST, S_OFFSETS, S_SYMBOLS, S_LUT,
     S_CHUNK_BITS, S_CHUNK_AUX, S_BYTE_OFF, S_OUT_OFF, S_PAYLOAD, S_OUTREC, S_SORT,
     S_TREE, S_STAGE, S_DENSE, S_WORK, S_BLOCKFLAG, S_MISC, S_REDO, S_DTAB, S_COUNTER, S_QUAL, S_REBASE,
+    S_HEADS,              // 1D block-head outlier values (dq1d_vec -> packer)
     S_HOST_A, S_HOST_B,   // device copies of host-buffer inputs / outputs (sdqz_*_host)
     S_NSLOTS
 };

@@ -740,7 +740,8 @@ __device__ __forceinline__ void dq1d_count(uint32_t c, uint32_t wbase, uint32_t 
 template <bool SH>
 __device__ __noinline__ void dq1d_task_f64(const float4* __restrict__ src, uint2* __restrict__ dst,
                                            uint32_t lane, double two_eb, int r, uint32_t wbase,
-                                           uint32_t hb, uint32_t shist_s, HistCtx h, bool& bad) {
+                                           uint32_t hb, uint32_t shist_s, HistCtx h, bool& bad,
+                                           double* __restrict__ hd) {
     const bool lead = (lane & 7) == 0;
     for (int j = 0; j < 8; j++) {
         const float4 w = __ldg(src + 32 * j);
@@ -759,6 +760,7 @@ __device__ __noinline__ void dq1d_task_f64(const float4* __restrict__ src, uint2
             cc[c] = code_of_f64(__dsub_rn(d[c], c ? d[c - 1] : left), r);
             dq1d_count<SH>(cc[c], wbase, hb, shist_s, h);
         }
+        if (hd && lead && cc[0] == 0) hd[(32 * j + lane) >> 3] = d[0];
         dst[32 * j] = make_uint2(cc[0] | (cc[1] << 16), cc[2] | (cc[3] << 16));
     }
 }
@@ -767,7 +769,8 @@ template <bool SH>
 __global__ void __launch_bounds__(kThreads, 2) dq1d_vec_kernel(const float* __restrict__ in, uint64_t ntask,
                                                                uint32_t cap, DevStatus* st,
                                                                uint16_t* __restrict__ codes,
-                                                               unsigned long long* ghist) {
+                                                               unsigned long long* ghist,
+                                                               double* __restrict__ heads) {
     extern __shared__ __align__(16) uint32_t dsm1[];
     uint32_t* hot = dsm1;   // [warp][kHot][32]
     for (uint32_t i = threadIdx.x; i < kWarpsPerCta * kHot * 32; i += blockDim.x) hot[i] = 0;
@@ -805,8 +808,9 @@ __global__ void __launch_bounds__(kThreads, 2) dq1d_vec_kernel(const float* __re
                 q[j][c] = (int)__funnelshift_r(lo, hi, 22);
             }
         }
+        double* hd = heads ? heads + task * (kVecTask / 32) : nullptr;   // this task's 32 block heads
         if (__any_sync(kFull, mark)) {   // rare: huge magnitudes or non-finite values
-            dq1d_task_f64<SH>(src, dst, lane, two_eb, r, wbase, hb, shist_s, h, bad);
+            dq1d_task_f64<SH>(src, dst, lane, two_eb, r, wbase, hb, shist_s, h, bad, hd);
             continue;
         }
         if (__any_sync(kFull, amb)) {   // rare: exact division near a rounding tie
@@ -838,6 +842,8 @@ __global__ void __launch_bounds__(kThreads, 2) dq1d_vec_kernel(const float* __re
                 cc[c] = (uu - 1u) < (uint32_t)(2 * r - 1) ? uu : 0u;   // -r < delta < r
                 dq1d_count<SH>(cc[c], wbase, hb, shist_s, h);
             }
+            // an outlier block head (|q| >= r >= 2, so never -0.0): its exact prequantized value
+            if (hd && lead && cc[0] == 0) hd[(32 * j + lane) >> 3] = (double)(q[j][0] - kFixK);
             dst[32 * j] = make_uint2(cc[0] | (cc[1] << 16), cc[2] | (cc[3] << 16));
         }
     }
@@ -1507,7 +1513,7 @@ __global__ void prequantize_kernel(const void* __restrict__ in, int dtype, uint6
 template <int KIND>
 int launch_kind(sdqz_ctx* ctx, const void* d_in, int ndims, const uint64_t dims[3],
                 const uint32_t block[3], uint32_t cap, uint16_t* d_codes,
-                unsigned long long* d_hist) {
+                unsigned long long* d_hist, double* d_heads) {
     size_t smem = (d_hist && cap <= kSmemHistMax) ? cap * sizeof(uint32_t) : 0;
     ensure_smem(ctx, (const void*)dq3d_kernel<KIND>, smem);
     ensure_smem(ctx, (const void*)dq2d_kernel<KIND>, smem);
@@ -1541,8 +1547,7 @@ int launch_kind(sdqz_ctx* ctx, const void* d_in, int ndims, const uint64_t dims[
         }
     }
     // vectorised 1D path: whole 1024-point tasks, then the tail by dq1d_kernel
-    if (KIND == 0 && ndims == 1 && is_fast_shape(ndims, block) && dims[0] >= kVecTask &&
-        ((uintptr_t)d_in & 15) == 0 && ((uintptr_t)d_codes & 7) == 0 && !env_disabled("SDQZ_NO_VEC1D")) {
+    if (dq1d_vec_span(KIND, ndims, dims, block, d_in, d_codes)) {
         const uint64_t nt = dims[0] / kVecTask;
         const size_t vsm = kWarpsPerCta * kHot * 32 * 4 + smem;
         ensure_smem(ctx, (const void*)dq1d_vec_kernel<true>, vsm);
@@ -1551,10 +1556,10 @@ int launch_kind(sdqz_ctx* ctx, const void* d_in, int ndims, const uint64_t dims[
         if (grid > (uint64_t)ctx->num_sms * 2) grid = (uint64_t)ctx->num_sms * 2;
         if (smem)
             dq1d_vec_kernel<true><<<(unsigned)grid, kThreads, vsm, ctx->stream>>>(
-                (const float*)d_in, nt, cap, ctx->d_status, d_codes, d_hist);
+                (const float*)d_in, nt, cap, ctx->d_status, d_codes, d_hist, d_heads);
         else
             dq1d_vec_kernel<false><<<(unsigned)grid, kThreads, vsm, ctx->stream>>>(
-                (const float*)d_in, nt, cap, ctx->d_status, d_codes, d_hist);
+                (const float*)d_in, nt, cap, ctx->d_status, d_codes, d_hist, d_heads);
         SDQZ_LAUNCHED_NAMED(ctx, "dq1d_vec_kernel");
         const uint64_t off = nt * kVecTask;
         if (off < dims[0]) {
@@ -1724,13 +1729,21 @@ bool is_fast_shape(int ndims, const uint32_t block[3]) {
     return ndims == 1 && block[0] == 32;
 }
 
+uint64_t dq1d_vec_span(int in_kind, int ndims, const uint64_t dims[3], const uint32_t block[3],
+                       const void* d_in, const uint16_t* d_codes) {
+    if (in_kind == 0 && ndims == 1 && is_fast_shape(ndims, block) && dims[0] >= kVecTask &&
+        ((uintptr_t)d_in & 15) == 0 && ((uintptr_t)d_codes & 7) == 0 && !env_disabled("SDQZ_NO_VEC1D"))
+        return dims[0] / kVecTask * kVecTask;
+    return 0;
+}
+
 int launch_dualquant(sdqz_ctx* ctx, const void* d_in, int in_kind, int ndims,
                      const uint64_t dims[3], const uint32_t block[3], uint32_t cap,
-                     uint16_t* d_codes, unsigned long long* d_hist) {
+                     uint16_t* d_codes, unsigned long long* d_hist, double* d_heads) {
     switch (in_kind) {
-        case 0: return launch_kind<0>(ctx, d_in, ndims, dims, block, cap, d_codes, d_hist);
-        case 1: return launch_kind<1>(ctx, d_in, ndims, dims, block, cap, d_codes, d_hist);
-        default: return launch_kind<2>(ctx, d_in, ndims, dims, block, cap, d_codes, d_hist);
+        case 0: return launch_kind<0>(ctx, d_in, ndims, dims, block, cap, d_codes, d_hist, d_heads);
+        case 1: return launch_kind<1>(ctx, d_in, ndims, dims, block, cap, d_codes, d_hist, nullptr);
+        default: return launch_kind<2>(ctx, d_in, ndims, dims, block, cap, d_codes, d_hist, nullptr);
     }
 }
 

@@ -544,6 +544,8 @@ struct DeflateArgs {
     uint64_t rec_limit;                  // records only for indices below (sharded: own slab)
     unsigned long long* records;         // {idx, f64 bits} pairs
     unsigned long long out_cap;
+    const double* heads;                 // block-head outlier values (i % 32 == 0, i < heads_limit)
+    uint64_t heads_limit;
     DevStatus* st;
     bool trusted;
 };
@@ -731,6 +733,9 @@ __device__ __forceinline__ void store_word(uint8_t* payload, uint64_t wbyte, uin
 }
 
 __device__ __forceinline__ double outlier_value(const DeflateArgs& a, uint64_t i, double two_eb) {
+    // a 1D block head: the dual-quant kept its prequantized value (no
+    // scattered re-read of the input, one 128 B line per head)
+    if (i < a.heads_limit && (i & 31) == 0) return a.heads[i >> 5];
     const void* p = a.in;
     uint64_t j = i;
     if (i >= a.in_split) { p = a.in_tail; j = i - a.in_split; }
@@ -1762,6 +1767,8 @@ int launch_deflate(sdqz_ctx* ctx, const DeflateJob& job) {
     a.rec_limit = job.rec_limit;
     a.records = (unsigned long long*)job.out_records;
     a.out_cap = job.out_cap;
+    a.heads = job.heads;
+    a.heads_limit = job.heads ? job.heads_limit : 0;
     a.trusted = job.trusted;
     a.st = ctx->d_status;
     if (a.nchunks == 0) return SDQZ_OK;

@@ -16,7 +16,13 @@ int launch_resolve(sdqz_ctx* ctx, int dtype, int eb_mode, double magnitude);
 // the status block.  d_hist (uint64[cap]) must be zeroed by the caller.
 int launch_dualquant(sdqz_ctx* ctx, const void* d_in, int in_kind, int ndims,
                      const uint64_t dims[3], const uint32_t block[3], uint32_t cap,
-                     uint16_t* d_codes, unsigned long long* d_hist);
+                     uint16_t* d_codes, unsigned long long* d_hist, double* d_heads = nullptr);
+// points [0, span) take the vectorised 1D dual-quant (block 32, 1024-point
+// tasks) for this input: with d_heads it also stores the prequantized value of
+// every block head whose code is an outlier at d_heads[i / 32], so the packer
+// need not re-read the input there.  0 when that path does not apply.
+uint64_t dq1d_vec_span(int in_kind, int ndims, const uint64_t dims[3], const uint32_t block[3],
+                       const void* d_in, const uint16_t* d_codes);
 int launch_prequantize(sdqz_ctx* ctx, const void* d_in, int dtype, uint64_t n, double* d_out);
 
 // huffman.cu ----------------------------------------------------------------
@@ -54,6 +60,8 @@ struct DeflateJob {
     uint64_t idx_base = 0;               // added to every emitted index
     uint64_t rec_limit = ~0ull;          // records only for (job-local) indices below this
     void* out_records = nullptr;         // {u64, f64}[max]
+    const double* heads = nullptr;       // outlier values of 1D block heads below heads_limit (dq1d_vec)
+    uint64_t heads_limit = 0;
     uint64_t out_cap = 0;
     bool want_payload = true;
     bool trusted = false;                // codes came from K2 (< cap, all present in the book)
