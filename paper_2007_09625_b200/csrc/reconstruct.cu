@@ -732,7 +732,7 @@ __device__ __forceinline__ void rq1d_rec_rows(const uint2 (&cw)[8], const double
 // of the same rank among the task's zero codes (equal sets once the count
 // check of dualquant.py:292-294 passes, which the host makes after this).
 template <int OUTK>
-__global__ void __launch_bounds__(kThreads) rq1d_rec_kernel(const uint16_t* __restrict__ codes,
+__global__ void __launch_bounds__(kThreads, 4) rq1d_rec_kernel(const uint16_t* __restrict__ codes,
                                                             const unsigned long long* __restrict__ rec,
                                                             const unsigned long long* __restrict__ start,
                                                             uint64_t k, const uint8_t* __restrict__ blockflag,
