@@ -1664,7 +1664,11 @@ int run_deflate(sdqz_ctx* ctx, DeflateArgs& a, bool payload) {
         // 28.8 KB static + up to 32 KB table > the 48 KB default
         ensure_smem(ctx, (const void*)chunk_pack_run_kernel<true>, 4096 * 8);
         if (payload && a.gtable) {   // 32-bit units (device-decided; no-op otherwise)
-            if (a.chunk >= 32768) {   // long chunks: register runs (amortise the per-round warp work)
+            static const uint32_t runs_min = [] {   // SDQZ_PACK_RUNS_MIN: tuning override
+                const char* e = getenv("SDQZ_PACK_RUNS_MIN");
+                return e ? (uint32_t)atoi(e) : 32768u;
+            }();
+            if (a.chunk >= runs_min) {   // long chunks: register runs (amortise the per-round warp work)
                 ensure_smem(ctx, (const void*)chunk_pack32_runs_kernel<true>, kPack32Smem);
                 ensure_smem(ctx, (const void*)chunk_pack32_runs_kernel<false>, 8 * kPackBufWords * 4);
                 if (ts) chunk_pack32_runs_kernel<true><<<(unsigned)grid, 256, kPack32Smem, ctx->stream>>>(a);
