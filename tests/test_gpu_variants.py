@@ -11,6 +11,8 @@ archive bytes and decompressed bits with the oracle (oracle/sdqz_oracle.py).
   SDQZ_NO_GRAPH=1   no CUDA-graph replay of the pipelines
   SDQZ_NO_FORK=1    decompress on one stream (no forked outlier-index branch)
   SDQZ_NO_HEADS=1   1D packer re-reads the input for outlier block heads (no dual-quant side channel)
+  SDQZ_PACK_RUNS_MIN=256  register-run packer for every chunk size (default: chunks >= 32768)
+  SDQZ_DEC_TARGET=24      short decoder slices (many rounds per chunk)
   SDQZ_NO_BLK=1     generic block shapes on the per-point kernels (not thread-per-block)
   SDQZ_DQ_ROWS=0|1  generic-shape dual-quant thread per block / per block-row segment
   SDQZ_STRIP=0|1    2D/3D generic-shape dual-quant warp per strip of block columns off / for every size
@@ -65,7 +67,8 @@ print("ok", len(fields))
 
 @pytest.mark.gpu
 @pytest.mark.parametrize("env", ["SDQZ_DEC_NS=3", "SDQZ_DEC_NS=6", "SDQZ_NO_TMA=1", "SDQZ_NO_VEC1D=1", "SDQZ_NO_VEC2D=1",
-                                 "SDQZ_NO_GRAPH=1", "SDQZ_NO_FORK=1", "SDQZ_NO_HEADS=1", "SDQZ_NO_BLK=1", "SDQZ_DQ_ROWS=0", "SDQZ_DQ_ROWS=1",
+                                 "SDQZ_NO_GRAPH=1", "SDQZ_NO_FORK=1", "SDQZ_NO_HEADS=1", "SDQZ_PACK_RUNS_MIN=256",
+                                 "SDQZ_DEC_TARGET=24", "SDQZ_NO_BLK=1", "SDQZ_DQ_ROWS=0", "SDQZ_DQ_ROWS=1",
                                  "SDQZ_RQ_ROWS=0", "SDQZ_RQ_ROWS=1", "SDQZ_STRIP=0", "SDQZ_STRIP=1"])
 def test_variant_bit_exact(env):
     k, v = env.split("=")
