@@ -1382,7 +1382,7 @@ constexpr int kStripPf = 16;  // strip-kernel rows in flight (cp.async ring slot
 // previous segment's lane 31 across segments), row y-1 and plane z-1 from
 // lane-private shared-memory slots.  Same fp64 expression and term order as
 // dq_blocks_kernel (dualquant.py:81-129).
-template <int KIND, bool ONE>
+template <int KIND, bool ONE, int ND>
 __global__ void __launch_bounds__(256) dq_strip_kernel(const void* __restrict__ in, Geo g, uint32_t W,
                                                        uint32_t steps, uint32_t nyb, uint32_t cap,
                                                        uint32_t hist_bytes, DevStatus* st,
@@ -1393,7 +1393,7 @@ __global__ void __launch_bounds__(256) dq_strip_kernel(const void* __restrict__ 
     HistCtx h;
     hist_init(h, reinterpret_cast<uint32_t*>(ssm), ghist, cap);
     const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const int nd = g.nd;
+    constexpr int nd = ND;   // 2 or 3 (template: no per-point dimension branches)
     const uint32_t bx = g.block[nd - 1], by = g.block[nd - 2], bz = nd == 3 ? g.block[0] : 1;
     const uint32_t per_warp = steps * (nd == 3 ? 2 + by : 1) * 32;
     double* R = reinterpret_cast<double*>(ssm + hist_bytes) + warp * per_warp + lane;   // [steps]: q of row y-1
@@ -1643,11 +1643,15 @@ int launch_kind(sdqz_ctx* ctx, const void* d_in, int ndims, const uint64_t dims[
             if (grid < 1) grid = 1;
             const uint32_t hist_bytes = (uint32_t)((smem + 15) & ~(size_t)15);
             const size_t dsm = hist_bytes + (size_t)8 * per_warp * 32 * 8 + (size_t)8 * kStripPf * 32 * (KIND == 0 ? 4 : 8);
-#define DQ_STRIP(ONE)                                                                                   \
-            ensure_smem(ctx, (const void*)dq_strip_kernel<KIND, ONE>, dsm);                             \
-            dq_strip_kernel<KIND, ONE><<<(unsigned)grid, 256, dsm, ctx->stream>>>(                      \
+#define DQ_STRIP(ONE, ND)                                                                               \
+            ensure_smem(ctx, (const void*)dq_strip_kernel<KIND, ONE, ND>, dsm);                         \
+            dq_strip_kernel<KIND, ONE, ND><<<(unsigned)grid, 256, dsm, ctx->stream>>>(                  \
                 d_in, g, rw, rsteps, nyb, cap, hist_bytes, ctx->d_status, d_codes, d_hist);
-            if (rsteps == 1) { DQ_STRIP(true) } else { DQ_STRIP(false) }
+            if (ndims == 3) {
+                if (rsteps == 1) { DQ_STRIP(true, 3) } else { DQ_STRIP(false, 3) }
+            } else {
+                if (rsteps == 1) { DQ_STRIP(true, 2) } else { DQ_STRIP(false, 2) }
+            }
 #undef DQ_STRIP
             SDQZ_LAUNCHED_NAMED(ctx, "dq_strip_kernel");
             return SDQZ_OK;

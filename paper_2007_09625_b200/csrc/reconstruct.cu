@@ -1127,14 +1127,14 @@ __global__ void __launch_bounds__(256) rq1d_seg_kernel(const uint16_t* __restric
 // rq_blocks_kernel magnitude guard: the sequentially first |F| >= 2^28 is
 // computed exactly, so a block that trips it is flagged and rewritten by the
 // fp64 replay.
-template <int OUTK, bool ONE>
+template <int OUTK, bool ONE, int ND>
 __global__ void __launch_bounds__(256, 3) rq_rows_kernel(const uint16_t* __restrict__ codes, const OutLookup ol,
                                                       uint8_t* __restrict__ blockflag, Geo g, uint32_t W,
                                                       uint32_t steps, uint32_t nyb, uint32_t cap, double two_eb,
                                                       void* __restrict__ out, DevStatus* st) {
     extern __shared__ __align__(16) int blk_smem[];
     const uint32_t lane = lane_id(), warp = threadIdx.x >> 5;
-    const int nd = g.nd;
+    constexpr int nd = ND;   // 2 or 3 (template: no per-point dimension branches)
     const uint32_t bx = g.block[nd - 1], by = g.block[nd - 2], bz = nd == 3 ? g.block[0] : 1;
     const uint32_t per_warp = steps * (1 + (nd == 3 ? by : 0)) * 32;
     int* Gs = blk_smem + warp * per_warp + lane;   // [steps][32]: G of row y-1
@@ -1466,15 +1466,17 @@ int launch_reconstruct(sdqz_ctx* ctx, const uint16_t* codes, const OutLookup& ol
         if (bg > (uint64_t)ctx->num_sms * 16) bg = (uint64_t)ctx->num_sms * 16;
         if (bg < 1) bg = 1;
         const size_t dsm = (size_t)8 * rsteps * (1 + (ndims == 3 ? block[ndims - 2] : 0)) * 32 * 4;
-#define RQ_ROWS(K, ONE)                                                                                       \
-        ensure_smem(ctx, (const void*)rq_rows_kernel<K, ONE>, dsm);                                           \
-        rq_rows_kernel<K, ONE><<<(unsigned)bg, 256, dsm, ctx->stream>>>(codes, dn, const_cast<uint8_t*>(blockflag), \
-                                                                      g, rw, rsteps, nyb, cap, two_eb, out, ctx->d_status);
+#define RQ_ROWS(K, ONE, ND)                                                                                   \
+        ensure_smem(ctx, (const void*)rq_rows_kernel<K, ONE, ND>, dsm);                                       \
+        rq_rows_kernel<K, ONE, ND><<<(unsigned)bg, 256, dsm, ctx->stream>>>(codes, dn, const_cast<uint8_t*>(blockflag), \
+                                                                          g, rw, rsteps, nyb, cap, two_eb, out, ctx->d_status);
+#define RQ_ROWS_ND(K, ONE) if (ndims == 3) { RQ_ROWS(K, ONE, 3) } else { RQ_ROWS(K, ONE, 2) }
         if (out_kind == 0) {
-            if (rsteps == 1) { RQ_ROWS(0, true) } else { RQ_ROWS(0, false) }
+            if (rsteps == 1) { RQ_ROWS_ND(0, true) } else { RQ_ROWS_ND(0, false) }
         } else {
-            if (rsteps == 1) { RQ_ROWS(1, true) } else { RQ_ROWS(1, false) }
+            if (rsteps == 1) { RQ_ROWS_ND(1, true) } else { RQ_ROWS_ND(1, false) }
         }
+#undef RQ_ROWS_ND
 #undef RQ_ROWS
         SDQZ_LAUNCHED_NAMED(ctx, "rq_rows_kernel");
     } else if (blk) {
