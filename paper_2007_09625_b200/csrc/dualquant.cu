@@ -1126,7 +1126,7 @@ __device__ __forceinline__ void hist_flush_thread(HistCtx& h) {
     h.lo = h.hi = 0;
 }
 
-template <int KIND>
+template <int KIND, int ND>
 __global__ void __launch_bounds__(64) dq_blocks_kernel(const void* __restrict__ in, Geo g, uint32_t cap,
                                                        uint32_t hist_bytes, DevStatus* st,
                                                        uint16_t* __restrict__ codes, unsigned long long* ghist) {
@@ -1135,7 +1135,7 @@ __global__ void __launch_bounds__(64) dq_blocks_kernel(const void* __restrict__ 
     hist_init(h, reinterpret_cast<uint32_t*>(dsm), ghist, cap);
     const uint32_t T = blockDim.x, tid = threadIdx.x;
     double* buf = reinterpret_cast<double*>(dsm + hist_bytes) + tid;   // slot s at buf[s * T]
-    const int nd = g.nd;
+    constexpr int nd = ND;
     const uint32_t bx = g.block[nd - 1], by = nd >= 2 ? g.block[nd - 2] : 1;
     double* P = buf;                                          // [by][bx] (3D)
     double* R = buf + (size_t)(nd == 3 ? bx * by : 0) * T;    // [bx] (2D, 3D)
@@ -1672,13 +1672,16 @@ int launch_kind(sdqz_ctx* ctx, const void* d_in, int ndims, const uint64_t dims[
             const uint32_t T = slots * 8 <= 1024 ? 64 : 32;
             const uint32_t hist_bytes = (uint32_t)((smem + 15) & ~(size_t)15);
             const size_t dsm = hist_bytes + (size_t)T * slots * 8;
-            ensure_smem(ctx, (const void*)dq_blocks_kernel<KIND>, dsm);
             const uint64_t nblocks = g.nblk[0] * g.nblk[1] * g.nblk[2];
             uint64_t grid = ceil_div(nblocks, T);
             if (grid > (uint64_t)ctx->num_sms * 64) grid = (uint64_t)ctx->num_sms * 64;
             if (grid < 1) grid = 1;
-            dq_blocks_kernel<KIND><<<(unsigned)grid, T, dsm, ctx->stream>>>(d_in, g, cap, hist_bytes, ctx->d_status,
-                                                                           d_codes, d_hist);
+#define DQ_BLOCKS(ND)                                                                                   \
+            ensure_smem(ctx, (const void*)dq_blocks_kernel<KIND, ND>, dsm);                             \
+            dq_blocks_kernel<KIND, ND><<<(unsigned)grid, T, dsm, ctx->stream>>>(d_in, g, cap, hist_bytes, \
+                                                                              ctx->d_status, d_codes, d_hist);
+            if (ndims == 3) { DQ_BLOCKS(3) } else if (ndims == 2) { DQ_BLOCKS(2) } else { DQ_BLOCKS(1) }
+#undef DQ_BLOCKS
             SDQZ_LAUNCHED_NAMED(ctx, "dq_blocks_kernel");
             return SDQZ_OK;
         }

@@ -995,14 +995,14 @@ __host__ __device__ __forceinline__ uint32_t blk_slots(int nd, const uint32_t* b
     return (nd == 3 ? bx * by : 0) + (nd >= 2 ? bx : 0);
 }
 
-template <int OUTK>
+template <int OUTK, int ND>
 __global__ void __launch_bounds__(64) rq_blocks_kernel(const uint16_t* __restrict__ codes,
                                                        const OutLookup ol,
                                                        uint8_t* __restrict__ blockflag, Geo g, uint32_t cap,
                                                        double two_eb, void* __restrict__ out, DevStatus* st) {
     extern __shared__ __align__(16) int blk_smem[];
     const uint32_t T = blockDim.x, tid = threadIdx.x;
-    const int nd = g.nd;
+    const int nd = ND ? ND : g.nd;   // ND 0: runtime (1D measured faster that way)
     const uint32_t bx = g.block[nd - 1], by = nd >= 2 ? g.block[nd - 2] : 1, bz = nd == 3 ? g.block[0] : 1;
     int* P = blk_smem + tid;                                      // [by][bx]: F of plane z-1 (3D)
     int* Gs = P + (size_t)(nd == 3 ? bx * by : 0) * T;            // [bx]: G of row y-1 (2D, 3D)
@@ -1485,15 +1485,14 @@ int launch_reconstruct(sdqz_ctx* ctx, const uint16_t* codes, const OutLookup& ol
         uint64_t bg = ceil_div(nblocks, T);
         if (bg > (uint64_t)ctx->num_sms * 64) bg = (uint64_t)ctx->num_sms * 64;
         if (bg < 1) bg = 1;
-        if (out_kind == 0) {
-            ensure_smem(ctx, (const void*)rq_blocks_kernel<0>, dsm);
-            rq_blocks_kernel<0><<<(unsigned)bg, T, dsm, ctx->stream>>>(codes, dn, const_cast<uint8_t*>(blockflag), g,
+#define RQ_BLOCKS(K, ND)                                                                                  \
+        ensure_smem(ctx, (const void*)rq_blocks_kernel<K, ND>, dsm);                                      \
+        rq_blocks_kernel<K, ND><<<(unsigned)bg, T, dsm, ctx->stream>>>(codes, dn, const_cast<uint8_t*>(blockflag), g, \
                                                                      cap, two_eb, out, ctx->d_status);
-        } else {
-            ensure_smem(ctx, (const void*)rq_blocks_kernel<1>, dsm);
-            rq_blocks_kernel<1><<<(unsigned)bg, T, dsm, ctx->stream>>>(codes, dn, const_cast<uint8_t*>(blockflag), g,
-                                                                     cap, two_eb, out, ctx->d_status);
-        }
+#define RQ_BLOCKS_ND(K) if (ndims == 3) { RQ_BLOCKS(K, 3) } else if (ndims == 2) { RQ_BLOCKS(K, 2) } else { RQ_BLOCKS(K, 0) }
+        if (out_kind == 0) { RQ_BLOCKS_ND(0) } else { RQ_BLOCKS_ND(1) }
+#undef RQ_BLOCKS_ND
+#undef RQ_BLOCKS
         SDQZ_LAUNCHED_NAMED(ctx, "rq_blocks_kernel");
     }
     const bool only_flagged = fast || blk;
