@@ -1225,14 +1225,14 @@ __device__ __forceinline__ double q_of(typename std::conditional<KIND == 0, floa
 // along the row), so each segment is independent -- millions of threads and
 // coalesced row reads where dq_blocks_kernel has one sequential thread per
 // block.  Same fp64 expression and term order (dualquant.py:81-129).
-template <int KIND>
+template <int KIND, int ND>
 __global__ void __launch_bounds__(256) dq_rows_kernel(const void* __restrict__ in, Geo g, uint64_t nitems,
                                                       uint32_t cap, DevStatus* st, uint16_t* __restrict__ codes,
                                                       unsigned long long* ghist) {
     extern __shared__ __align__(128) unsigned char rsm[];
     HistCtx h;
     hist_init(h, reinterpret_cast<uint32_t*>(rsm), ghist, cap);
-    const int nd = g.nd;
+    constexpr int nd = ND;
     const uint32_t bx = g.block[nd - 1], by = nd >= 2 ? g.block[nd - 2] : 1, bz = nd == 3 ? g.block[0] : 1;
     const uint64_t X = g.dims[nd - 1], Y = nd >= 2 ? g.dims[nd - 2] : 1;
     const uint64_t nbx = g.nblk[nd - 1];
@@ -1657,13 +1657,16 @@ int launch_kind(sdqz_ctx* ctx, const void* d_in, int ndims, const uint64_t dims[
             return SDQZ_OK;
         }
         if (rows && !env_disabled("SDQZ_NO_BLK")) {
-            ensure_smem(ctx, (const void*)dq_rows_kernel<KIND>, smem);
             const uint64_t nitems = ndims == 1 ? dims[0] : (n / dims[ndims - 1]) * g.nblk[ndims - 1];
             uint64_t grid = ceil_div(nitems, 256);
             if (grid > (uint64_t)ctx->num_sms * 16) grid = (uint64_t)ctx->num_sms * 16;
             if (grid < 1) grid = 1;
-            dq_rows_kernel<KIND><<<(unsigned)grid, 256, smem, ctx->stream>>>(d_in, g, nitems, cap, ctx->d_status,
-                                                                            d_codes, d_hist);
+#define DQ_ROWS(ND)                                                                                     \
+            ensure_smem(ctx, (const void*)dq_rows_kernel<KIND, ND>, smem);                              \
+            dq_rows_kernel<KIND, ND><<<(unsigned)grid, 256, smem, ctx->stream>>>(d_in, g, nitems, cap,  \
+                                                                                ctx->d_status, d_codes, d_hist);
+            if (ndims == 3) { DQ_ROWS(3) } else if (ndims == 2) { DQ_ROWS(2) } else { DQ_ROWS(1) }
+#undef DQ_ROWS
             SDQZ_LAUNCHED_NAMED(ctx, "dq_rows_kernel");
             return SDQZ_OK;
         }
