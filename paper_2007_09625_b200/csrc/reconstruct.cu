@@ -1128,7 +1128,7 @@ __global__ void __launch_bounds__(256) rq1d_seg_kernel(const uint16_t* __restric
 // computed exactly, so a block that trips it is flagged and rewritten by the
 // fp64 replay.
 template <int OUTK, bool ONE, int ND>
-__global__ void __launch_bounds__(256, 3) rq_rows_kernel(const uint16_t* __restrict__ codes, const OutLookup ol,
+__global__ void __launch_bounds__(256, 4) rq_rows_kernel(const uint16_t* __restrict__ codes, const OutLookup ol,
                                                       uint8_t* __restrict__ blockflag, Geo g, uint32_t W,
                                                       uint32_t steps, uint32_t nyb, uint32_t cap, double two_eb,
                                                       void* __restrict__ out, DevStatus* st) {
