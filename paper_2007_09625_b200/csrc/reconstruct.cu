@@ -1055,64 +1055,75 @@ __global__ void __launch_bounds__(64) rq_blocks_kernel(const uint16_t* __restric
 
 constexpr int kRowPf = 8;   // row-kernel iterations whose code loads are issued together
 
-// 1D generic block length bx >= 32: a warp per task of whole blocks (>= 1024
-// points), lane = point, 32 points per step.  The reconstruct is the linear
-// recurrence F_i = F_{i-1} + delta_i restarted at a block start (F = delta)
-// and at an outlier (F = v): a warp prefix sum minus its value just before
-// the last restart lane at or left of each lane (the previous step's F as
-// carry when there is none), exact in int64.
-// Blocks whose outlier values are not integers below 2^40 are flagged by the
-// scatter and rewritten afterwards by the fp64 replay.
-template <int OUTK>
-__global__ void __launch_bounds__(256) rq1d_seg_kernel(const uint16_t* __restrict__ codes, const OutLookup ol,
-                                                       uint64_t n, uint32_t bx, uint64_t task, uint32_t cap,
-                                                       double two_eb, void* __restrict__ out) {
-    const uint32_t lane = lane_id();
-    const int r = (int)(cap >> 1);
-    const uint64_t ntask = ceil_div(n, task);
+// one task of rq1d_seg_kernel with F in V (int32 when every value fits, else int64)
+template <typename V, int OUTK>
+__device__ __forceinline__ void rq1d_seg_task(const uint16_t* __restrict__ codes, const OutLookup& ol,
+                                              uint64_t t0, uint64_t t1, uint32_t bx, int r, uint32_t lane,
+                                              unsigned upto, double two_eb, void* __restrict__ out) {
     const uint32_t step = 32 % bx;
-    const unsigned upto = (2u << lane) - 1u;   // lanes 0..lane (lane 31: all)
-    for (uint64_t t = blockIdx.x * (uint64_t)(blockDim.x >> 5) + (threadIdx.x >> 5); t < ntask;
-         t += (uint64_t)gridDim.x * (blockDim.x >> 5)) {
-        const uint64_t t0 = t * task, t1 = umin(t0 + task, n);
-        long long carry = 0;
-        uint32_t pos = lane % bx;
-        for (uint64_t g0 = t0; g0 < t1; g0 += 32 * kRowPf) {
-          uint32_t cc[kRowPf];   // the group's codes, loaded together
+    V carry = 0;
+    uint32_t pos = lane % bx;
+    for (uint64_t g0 = t0; g0 < t1; g0 += 32 * kRowPf) {
+        uint32_t cc[kRowPf];   // the group's codes, loaded together
 #pragma unroll
-          for (int k = 0; k < kRowPf; k++) {
+        for (int k = 0; k < kRowPf; k++) {
             const uint64_t i = g0 + 32 * k + lane;
             cc[k] = i < t1 ? (uint32_t)codes[i] : (uint32_t)r;
-          }
+        }
 #pragma unroll
-          for (int k = 0; k < kRowPf; k++) {
+        for (int k = 0; k < kRowPf; k++) {
             const uint64_t i0 = g0 + 32 * k;
             if (i0 >= t1) break;
             const uint64_t i = i0 + lane;
             const bool in = i < t1;
             const uint32_t code = cc[k];
             bool reset = pos == 0;
-            long long b = (long long)code - r;
+            V b = (V)((int)code - r);
             if (code == 0) {
                 reset = true;
-                b = (long long)__longlong_as_double((long long)out_bits(ol, i));
+                b = (V)(long long)__longlong_as_double((long long)out_bits(ol, i));
             }
-            long long S = b;   // inclusive prefix sum, restarted at the last reset lane at or left of this one
+            V S = b;   // inclusive prefix sum, restarted at the last reset lane at or left of this one
 #pragma unroll
             for (int o = 1; o < 32; o <<= 1) {
-                const long long u = __shfl_up_sync(kFull, S, o);
+                const V u = __shfl_up_sync(kFull, S, o);
                 if (lane >= (uint32_t)o) S += u;
             }
             const unsigned m = __ballot_sync(kFull, reset) & upto;
             const int L = 31 - __clz((int)m);
-            const long long Sx = __shfl_sync(kFull, S - b, L < 0 ? 0 : L);
-            const long long F = m ? S - Sx : carry + S;
-            if (in) store_out<OUTK>(out, i, F, two_eb);
+            const V Sx = __shfl_sync(kFull, S - b, L < 0 ? 0 : L);
+            const V F = m ? S - Sx : carry + S;
+            if (in) store_out<OUTK>(out, i, (long long)F, two_eb);
             carry = __shfl_sync(kFull, F, 31);
             pos += step;
             if (pos >= bx) pos -= bx;
-          }
         }
+    }
+}
+
+// 1D generic block length bx >= 32: a warp per task of whole blocks (>= 1024
+// points), lane = point, 32 points per step.  The reconstruct is the linear
+// recurrence F_i = F_{i-1} + delta_i restarted at a block start (F = delta)
+// and at an outlier (F = v): a warp prefix sum minus its value just before
+// the last restart lane at or left of each lane (the previous step's F as
+// carry when there is none).  int32 when every outlier value is below 2^29
+// (task_bounds_kernel's flag) and bx * r < 2^29 (then |F| < 2^30 throughout),
+// else int64.  Blocks whose outlier values are not integers below 2^40 are
+// flagged by the scatter and rewritten afterwards by the fp64 replay.
+template <int OUTK>
+__global__ void __launch_bounds__(256) rq1d_seg_kernel(const uint16_t* __restrict__ codes, const OutLookup ol,
+                                                       uint64_t n, uint32_t bx, uint64_t task, uint32_t cap,
+                                                       double two_eb, void* __restrict__ out, int narrow_ok) {
+    const uint32_t lane = lane_id();
+    const int r = (int)(cap >> 1);
+    const uint64_t ntask = ceil_div(n, task);
+    const unsigned upto = (2u << lane) - 1u;   // lanes 0..lane (lane 31: all)
+    const bool narrow = narrow_ok && *ol.big == 0;
+    for (uint64_t t = blockIdx.x * (uint64_t)(blockDim.x >> 5) + (threadIdx.x >> 5); t < ntask;
+         t += (uint64_t)gridDim.x * (blockDim.x >> 5)) {
+        const uint64_t t0 = t * task, t1 = umin(t0 + task, n);
+        if (narrow) rq1d_seg_task<int, OUTK>(codes, ol, t0, t1, bx, r, lane, upto, two_eb, out);
+        else rq1d_seg_task<long long, OUTK>(codes, ol, t0, t1, bx, r, lane, upto, two_eb, out);
     }
 }
 
@@ -1448,13 +1459,16 @@ int launch_reconstruct(sdqz_ctx* ctx, const uint16_t* codes, const OutLookup& ol
                          (rows_env ? rows_env[0] == '1' : bpts >= 128);
     if (blk && ndims == 1 && block[0] >= 32) {   // long 1D blocks: warp-wide scans over tasks of whole blocks
         const uint64_t task = (uint64_t)block[0] * ceil_div(1024, block[0]);
+        const int narrow_ok = (uint64_t)block[0] * (cap >> 1) < (1ull << 29) ? 1 : 0;   // int32 F bound
         uint64_t bg = ceil_div(ceil_div(n, task), 8);
         if (bg > (uint64_t)ctx->num_sms * 16) bg = (uint64_t)ctx->num_sms * 16;
         if (bg < 1) bg = 1;
         if (out_kind == 0)
-            rq1d_seg_kernel<0><<<(unsigned)bg, 256, 0, ctx->stream>>>(codes, dn, n, block[0], task, cap, two_eb, out);
+            rq1d_seg_kernel<0><<<(unsigned)bg, 256, 0, ctx->stream>>>(codes, dn, n, block[0], task, cap, two_eb, out,
+                                                                     narrow_ok);
         else
-            rq1d_seg_kernel<1><<<(unsigned)bg, 256, 0, ctx->stream>>>(codes, dn, n, block[0], task, cap, two_eb, out);
+            rq1d_seg_kernel<1><<<(unsigned)bg, 256, 0, ctx->stream>>>(codes, dn, n, block[0], task, cap, two_eb, out,
+                                                                     narrow_ok);
         SDQZ_LAUNCHED_NAMED(ctx, "rq1d_seg_kernel");
     } else if (blk && ndims >= 2 && rows_ok) {   // warp per strip of block columns, lane = column
         // block rows per task: >= 32 row iterations a warp task

@@ -738,6 +738,12 @@ class TestGenericShapes:
             blob = S.compress(f, eb=1e-3, mode="abs", block_shape=block)
             assert blob == O.compress(f, eb=1e-3, mode="abs", block_shape=block)
             assert np.array_equal(bits(S.decompress(blob)), bits(O.decompress(blob)))
+        # 1D blocks >= 32: outlier values past 2^29 switch the warp-scan reconstruct to int64
+        g = np.cumsum(rng.normal(0, 1, 20_000)) * 1e7
+        for block in ((64,), (200,)):
+            blob = S.compress(g, eb=1e-3, mode="abs", block_shape=block)
+            assert blob == O.compress(g, eb=1e-3, mode="abs", block_shape=block)
+            assert np.array_equal(bits(S.decompress(blob)), bits(O.decompress(blob)))
 
 
 @pytest.mark.gpu
