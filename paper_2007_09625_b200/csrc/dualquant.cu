@@ -1622,7 +1622,7 @@ int launch_kind(sdqz_ctx* ctx, const void* d_in, int ndims, const uint64_t dims[
         // many small ones: thread per block (each point prequantized once)
         const char* rows_env = getenv("SDQZ_DQ_ROWS");
         const bool rows = rows_env ? rows_env[0] == '1'
-                                   : (ndims == 1 ? block[0] >= 32 : nblocks_all < (uint64_t)ctx->num_sms * 2048);
+                                   : (ndims == 1 ? block[0] >= 16 : nblocks_all < (uint64_t)ctx->num_sms * 2048);
         // 2D / 3D blocks of >= 128 points: warp per strip of block columns
         // (lane-private slots <= 12 KB a warp)
         uint64_t bpts = 1;
